@@ -1,0 +1,364 @@
+"""ctypes mirror of include/mlt.h (the C ABI of the B200 decode hot path).
+
+The Python side is plumbing only: tests and bench.py call the C ABI through
+these bindings exactly as a reference maintainer's ctypes stub would
+(INTEGRATION.md).  `bind(lib, prefix)` binds either the product library
+(prefix "mlt_") or the reference shim built under oracle/_ref (prefix "ref_",
+tests only) with the same struct layouts.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmlt.so")
+
+MLT_OK = 0
+ERRORS = {-1: "invalid argument", -2: "infeasible policy", -3: "unsupported combination",
+          -4: "cycle detected", -5: "empty timeline", -6: "cuda error", -7: "budget exceeded",
+          -8: "internal error"}
+
+
+class MltError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class InfeasiblePolicyError(MltError):
+    pass
+
+
+class UnsupportedCombinationError(MltError):
+    pass
+
+
+class CycleDetectedError(MltError):
+    pass
+
+
+class EmptyTimelineError(MltError):
+    pass
+
+
+_EXC = {-2: InfeasiblePolicyError, -3: UnsupportedCombinationError, -4: CycleDetectedError,
+        -5: EmptyTimelineError}
+
+
+class HardwareSpec(C.Structure):
+    _fields_ = [(n, C.c_double) for n in
+                ("gpu_mem_bytes", "cpu_mem_bytes", "gpu_bw", "cpu_bw", "link_bw", "gpu_flops",
+                 "cpu_flops")]
+
+
+class ModelSpec(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in
+                ("layers", "hidden_dim", "ffn_dim", "q_heads", "kv_heads", "experts", "top_k")] + \
+               [("weight_dtype_bytes", C.c_double), ("kv_dtype_bytes", C.c_double)]
+
+    def head_dim(self) -> int:
+        return self.hidden_dim // self.q_heads if self.q_heads > 0 else 0
+
+
+class WorkloadSpec(C.Structure):
+    _fields_ = [("prompt_len", C.c_int64), ("gen_len", C.c_int64)]
+
+
+class Policy(C.Structure):
+    _fields_ = [("batch", C.c_int64), ("micro_batch", C.c_int64), ("attn_on_gpu", C.c_int32),
+                ("ffn_on_gpu", C.c_int32), ("weights_on_gpu", C.c_double),
+                ("kv_on_gpu", C.c_double)]
+
+    def micro_batch_count(self) -> int:
+        return self.batch // self.micro_batch if self.micro_batch > 0 else 0
+
+
+class OpProfile(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("flops", "gpu_bytes", "cpu_bytes", "link_bytes")]
+
+
+class LayerWeightBytes(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("experts", "qkv", "output", "router")]
+
+    def total(self) -> float:
+        return self.experts + self.qkv + self.output + self.router
+
+
+class TransferSizes(C.Structure):
+    _fields_ = [(n, C.c_double) for n in
+                ("qkv_offload", "hidden_upload", "weight_stream", "kv_upload")]
+
+
+class LatencyBreakdown(C.Structure):
+    _fields_ = [(n, C.c_double) for n in
+                ("link_upload", "gpu_attention", "gpu_ffn", "cpu_attention", "cpu_ffn",
+                 "layer_total")]
+
+    def gpu_total(self):
+        return self.gpu_attention + self.gpu_ffn
+
+    def cpu_total(self):
+        return self.cpu_attention + self.cpu_ffn
+
+
+class MemoryFootprint(C.Structure):
+    _fields_ = [("gpu_bytes", C.c_double), ("cpu_bytes", C.c_double), ("feasible", C.c_int32)]
+
+
+class PlanResult(C.Structure):
+    _fields_ = [("policy", Policy), ("breakdown", LatencyBreakdown), ("memory", MemoryFootprint),
+                ("decode_throughput", C.c_double), ("generation_throughput", C.c_double),
+                ("objective", C.c_double)]
+
+
+class StepDurations(C.Structure):
+    _fields_ = [(n, C.c_double) for n in
+                ("pre_attn", "offload_qkv", "cpu_attn", "load_hidden", "post_attn",
+                 "weight_stage", "weight_upload", "kv_load", "gpu_attn")]
+
+
+class Task(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in
+                ("kind", "step", "layer", "microbatch", "page", "resource")] + \
+               [("duration", C.c_double), ("n_deps", C.c_int32)]
+
+
+class TimelineEntry(C.Structure):
+    _fields_ = [("task", C.c_int32), ("start", C.c_double), ("end", C.c_double)]
+
+
+class SimMetrics(C.Structure):
+    _fields_ = [("makespan", C.c_double), ("utilization", C.c_double * 5),
+                ("steady_layer_time", C.c_double)]
+
+
+SCHED = {"cgopipe": 0, "s2": 1, "s3": 2, "s4": 3}
+TASK_KINDS = ["pre_attn", "offload_qkv", "cpu_attn", "load_hidden", "post_attn",
+              "weight_to_pinned", "weight_to_gpu", "kv_load", "gpu_attn"]
+RESOURCES = ["gpu", "cpu", "h2d", "d2h", "ctopin"]
+
+P = C.POINTER
+_SIGS = {
+    "last_error": (C.c_char_p, []),
+    "last_status": (C.c_int, []),
+    "op_profiles": (C.c_int, [P(ModelSpec), C.c_double, C.c_double, C.c_double, P(OpProfile)]),
+    "layer_weight_bytes": (C.c_int, [P(ModelSpec), P(LayerWeightBytes)]),
+    "transfer_sizes": (C.c_int, [P(ModelSpec), P(Policy), C.c_double, P(TransferSizes)]),
+    "memory_totals": (C.c_int, [P(ModelSpec), P(WorkloadSpec), C.c_int64, P(C.c_double)]),
+    "layer_latency": (C.c_int, [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(Policy),
+                                C.c_double, P(LatencyBreakdown)]),
+    "memory_footprint": (C.c_int, [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(Policy),
+                                   P(MemoryFootprint)]),
+    "apply_tensor_parallelism": (C.c_int, [P(HardwareSpec), C.c_int, C.c_int, C.c_double,
+                                           P(HardwareSpec)]),
+    "estimate_throughput": (C.c_int, [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(Policy),
+                                      P(PlanResult)]),
+    "schedule_build": (C.c_void_p, [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(Policy),
+                                    C.c_int, C.c_int, C.c_int]),
+    "schedule_build_durations": (C.c_void_p, [P(StepDurations), C.c_int, C.c_int, C.c_int,
+                                              C.c_int]),
+    "dag_from_tasks": (C.c_void_p, [P(Task), C.c_int, P(C.c_int32), C.c_int, C.c_int, C.c_int,
+                                    C.c_int]),
+    "dag_free": (None, [C.c_void_p]),
+    "dag_size": (C.c_int, [C.c_void_p]),
+    "dag_task": (C.c_int, [C.c_void_p, C.c_int, P(Task), P(C.c_int32), C.c_int]),
+    "dag_dump": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
+    "simulate": (C.c_int, [C.c_void_p, P(TimelineEntry), P(C.c_double), P(C.c_double)]),
+    "metrics": (C.c_int, [C.c_void_p, P(TimelineEntry), C.c_int, C.c_double, P(C.c_double),
+                          P(SimMetrics)]),
+    "verify_timeline": (C.c_int, [C.c_void_p, P(TimelineEntry), C.c_int, C.c_double,
+                                  P(C.c_double), C.c_double, C.c_char_p, C.c_size_t]),
+    "timeline_json": (C.c_int, [C.c_void_p, P(TimelineEntry), C.c_int, C.c_double,
+                                P(C.c_double), C.c_char_p, C.c_char_p, C.c_size_t]),
+}
+
+
+@dataclass
+class Timeline:
+    entries: object  # ctypes array of TimelineEntry
+    makespan: float
+    busy: object     # c_double * 5
+
+    def starts(self):
+        return [e.start for e in self.entries]
+
+
+class Dag:
+    """Owning handle on an mlt_dag (ScheduleDag)."""
+
+    def __init__(self, api: "Api", handle):
+        self.api, self.h = api, handle
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.api.fn["dag_free"](self.h)
+            self.h = None
+
+    def __len__(self):
+        return self.api.fn["dag_size"](self.h)
+
+    def task(self, i):
+        t = Task()
+        deps = (C.c_int32 * 64)()
+        n = self.api.check(self.api.fn["dag_task"](self.h, i, C.byref(t), deps, 64))
+        return t, [deps[k] for k in range(min(n, 64))]
+
+    def tasks(self):
+        return [self.task(i) for i in range(len(self))]
+
+    def dump(self) -> str:
+        n = self.api.check(self.api.fn["dag_dump"](self.h, None, 0))
+        buf = C.create_string_buffer(n + 1)
+        self.api.fn["dag_dump"](self.h, buf, n + 1)
+        return buf.value.decode()
+
+    def simulate(self, fn_name="simulate") -> Timeline:
+        n = len(self)
+        entries = (TimelineEntry * max(n, 1))()
+        mk = C.c_double()
+        busy = (C.c_double * 5)()
+        self.api.check(self.api.fn[fn_name](self.h, entries, C.byref(mk), busy))
+        return Timeline(entries, mk.value, busy)
+
+    def metrics(self, tl: Timeline) -> SimMetrics:
+        out = SimMetrics()
+        self.api.check(self.api.fn["metrics"](self.h, tl.entries, len(self), tl.makespan,
+                                              tl.busy, C.byref(out)))
+        return out
+
+    def verify(self, tl: Timeline, tol=1e-9) -> str:
+        buf = C.create_string_buffer(4096)
+        rc = self.api.fn["verify_timeline"](self.h, tl.entries, len(tl.entries), tl.makespan,
+                                            tl.busy, tol, buf, 4096)
+        if rc < 0:
+            self.api.check(rc)
+        return buf.value.decode()
+
+    def timeline_json(self, tl: Timeline, manifest="{}") -> str:
+        f = self.api.fn["timeline_json"]
+        n = self.api.check(f(self.h, tl.entries, len(self), tl.makespan, tl.busy,
+                             manifest.encode(), None, 0))
+        buf = C.create_string_buffer(n + 1)
+        f(self.h, tl.entries, len(self), tl.makespan, tl.busy, manifest.encode(), buf, n + 1)
+        return buf.value.decode()
+
+
+class Api:
+    """Typed wrapper over one library's planner/scheduler entry points."""
+
+    def __init__(self, lib: C.CDLL, prefix: str, extra_sigs=None):
+        self.lib, self.prefix, self.fn = lib, prefix, {}
+        sigs = dict(_SIGS)
+        sigs.update(extra_sigs or {})
+        for name, (res, args) in sigs.items():
+            f = getattr(lib, prefix + name, None)
+            if f is None:
+                continue
+            f.restype, f.argtypes = res, args
+            self.fn[name] = f
+
+    def error(self) -> str:
+        return (self.fn["last_error"]() or b"").decode()
+
+    def check(self, rc: int) -> int:
+        if rc < 0:
+            raise _EXC.get(rc, MltError)(rc, self.error())
+        return rc
+
+    # --- cost model ------------------------------------------------------
+    def op_profiles(self, model, tokens, ctx, r_w=0.0):
+        out = (OpProfile * 4)()
+        self.check(self.fn["op_profiles"](C.byref(model), tokens, ctx, r_w, out))
+        return {"attention": out[0], "ffn": out[1], "qkv": out[2], "output": out[3]}
+
+    def layer_weight_bytes(self, model):
+        out = LayerWeightBytes()
+        self.check(self.fn["layer_weight_bytes"](C.byref(model), C.byref(out)))
+        return out
+
+    def transfer_sizes(self, model, policy, ctx):
+        out = TransferSizes()
+        self.check(self.fn["transfer_sizes"](C.byref(model), C.byref(policy), ctx, C.byref(out)))
+        return out
+
+    def memory_totals(self, model, workload, batch):
+        out = (C.c_double * 2)()
+        self.check(self.fn["memory_totals"](C.byref(model), C.byref(workload), batch, out))
+        return out[0], out[1]
+
+    # --- planner ---------------------------------------------------------
+    def layer_latency(self, hw, model, workload, policy, ctx):
+        out = LatencyBreakdown()
+        self.check(self.fn["layer_latency"](C.byref(hw), C.byref(model), C.byref(workload),
+                                            C.byref(policy), ctx, C.byref(out)))
+        return out
+
+    def memory_footprint(self, hw, model, workload, policy):
+        out = MemoryFootprint()
+        self.check(self.fn["memory_footprint"](C.byref(hw), C.byref(model), C.byref(workload),
+                                               C.byref(policy), C.byref(out)))
+        return out
+
+    def apply_tensor_parallelism(self, hw, tp, b200_rule=False, host_read_cap=0.0):
+        out = HardwareSpec()
+        self.check(self.fn["apply_tensor_parallelism"](C.byref(hw), tp, int(b200_rule),
+                                                       host_read_cap, C.byref(out)))
+        return out
+
+    def estimate_throughput(self, hw, model, workload, policy):
+        out = PlanResult()
+        self.check(self.fn["estimate_throughput"](C.byref(hw), C.byref(model),
+                                                  C.byref(workload), C.byref(policy),
+                                                  C.byref(out)))
+        return out
+
+    # --- scheduler -------------------------------------------------------
+    def _dag(self, h):
+        if not h:
+            raise _EXC.get(self._last_code(), MltError)(self._last_code(), self.error())
+        return Dag(self, h)
+
+    def _last_code(self):
+        return self.fn["last_status"]()
+
+    def build_schedule(self, hw, model, workload, policy, kind="cgopipe", layers=None, steps=1):
+        layers = model.layers if layers is None else layers
+        h = self.fn["schedule_build"](C.byref(hw), C.byref(model), C.byref(workload),
+                                      C.byref(policy), SCHED[kind], layers, steps)
+        return self._dag(h)
+
+    def build_schedule_durations(self, durations, kind, layers, steps, micro_batches):
+        if isinstance(durations, StepDurations):
+            durations = [durations] * steps
+        arr = (StepDurations * max(len(durations), 1))(*durations)
+        h = self.fn["schedule_build_durations"](arr, SCHED[kind], layers, steps, micro_batches)
+        return self._dag(h)
+
+    def dag_from_tasks(self, tasks, layers=1, steps=1, micro_batches=1, kind="cgopipe"):
+        """tasks: list of (Task, deps)."""
+        arr = (Task * max(len(tasks), 1))()
+        flat = []
+        for i, (t, deps) in enumerate(tasks):
+            t.n_deps = len(deps)
+            arr[i] = t
+            flat.extend(deps)
+        dep_arr = (C.c_int32 * max(len(flat), 1))(*flat)
+        h = self.fn["dag_from_tasks"](arr, len(tasks), dep_arr, layers, steps, micro_batches,
+                                      SCHED[kind])
+        return self._dag(h)
+
+
+_product = None
+
+
+def load_product() -> Api:
+    """The product library.  Fails loudly when it has not been built."""
+    global _product
+    if _product is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g;"
+                              f" g.build()'` (make -C paper_2411_11217_b200/csrc)")
+        _product = Api(C.CDLL(LIB_PATH), "mlt_")
+    return _product
