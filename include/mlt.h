@@ -198,6 +198,94 @@ int mlt_timeline_json(const mlt_dag* dag, const mlt_timeline_entry_t* entries, i
                       double makespan, const double busy[5], const char* manifest_json,
                       char* buf, size_t cap);
 
+
+/* ==== Kernel-level entry points (device pointers, caller-owned) ==========
+ * Every pointer below is a device pointer unless named host_*; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  These are the hot-path
+ * kernels of SURVEY.md §2c; the runtime (below) strings them together.  The
+ * packed operand layout is defined in DESIGN.md §3 (kernels/common.cuh).
+ */
+
+/* Host: row-major bf16 [M, K] -> packed weight blocks (M % 128 == 0,
+ * K % 64 == 0); dst holds M*K bf16. */
+int mlt_pack_weight(const uint16_t* host_src, int64_t M, int64_t K, uint16_t* host_dst);
+/* Host: packed activation rows (capacity R) -> row-major bf16 [rows, K]. */
+int mlt_unpack_rows(const uint8_t* host_packed, int64_t R, int64_t rows, int64_t K,
+                    uint16_t* host_dst);
+/* Host: row-major bf16 [rows, K] -> packed activation layout (capacity R). */
+int mlt_pack_rows_host(const uint16_t* host_src, int64_t rows, int64_t K, int64_t R,
+                       uint8_t* host_dst);
+
+typedef struct mlt_gemm_args_t {
+    const void* a_table; /* device array of const void*, [n_mats][G][RB] weight row blocks */
+    int32_t n_mats, G, RB, K;
+    const void* b;       /* packed activations, capacity R rows */
+    int32_t R;
+    const int32_t* b_off; /* [G+1] padded group row offsets or NULL (dense) */
+    const int32_t* b_cnt; /* [G] rows per group or NULL (dense) */
+    int32_t rows_dense, n_cap;
+    int32_t epi;          /* 0: fp32 rows (+ residual); 1: silu(A0)*A1 -> packed bf16 */
+    float alpha;
+    float* out_f32;
+    int32_t ldo;
+    const float* residual;
+    int32_t ldr;
+    void* out_packed;
+    int32_t out_R;
+} mlt_gemm_args_t;
+
+/* Grouped swap-AB tcgen05 GEMM (SURVEY.md §2c expert_gateup_silu /
+ * expert_down / dense projections). */
+int mlt_gemm(const mlt_gemm_args_t* args, void* stream);
+
+int mlt_embed(const int32_t* tokens, const uint16_t* table, int T, int H, float* x_out,
+              void* stream);
+int mlt_rmsnorm_pack(const float* x, const uint16_t* gamma, int T, int H, float eps,
+                     void* out_packed, int R, void* stream);
+int mlt_pack_rows(const uint16_t* src, int ld, int T, int K, void* dst, int R, void* stream);
+int mlt_rope_qkv(const float* qkv, const int32_t* pos, const void* rope_cos_sin, int T, int nq,
+                 int nkv, int d, uint16_t* out, void* stream);
+
+/* Router: top-k over the fixed-tree fp32 logits (bit-exact vs the oracle on
+ * identical bf16 inputs).  Either x+gamma (fused RMSNorm) or hn_in. */
+int mlt_router_topk(const float* x, const uint16_t* gamma, float eps, const uint16_t* hn_in,
+                    const uint16_t* w_router, int T, int H, int E, int K, uint16_t* hn_out,
+                    float* logits, int32_t* topk_idx, float* topk_w, void* stream);
+/* Stable permutation + gather into the packed expert operand. */
+int mlt_moe_permute(const int32_t* topk_idx, const uint16_t* hn, int T, int H, int E, int K,
+                    int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv,
+                    void* x_packed, int R, void* stream);
+int mlt_moe_combine(const float* h, const float* y, int ldy, const int32_t* inv,
+                    const float* topk_w, int T, int H, int K, float* x_out, void* stream);
+
+/* Expert FFN of one MoE layer on the permuted operand: fused gate/up GEMM
+ * (SiLU gating in the TMEM epilogue) -> down GEMM -> top-k weighted combine
+ * with the residual h.  w13_table: [2][E][F/128] row blocks (W1 then W3);
+ * w2_table: [E][H/128]; inter_packed capacity R rows of F; y fp32 [R, H]. */
+int mlt_expert_ffn(const void* x_packed, int R, const int32_t* counts, const int32_t* offsets,
+                   const void* w13_table, const void* w2_table, int E, int H, int F, int n_cap,
+                   void* inter_packed, float* y, const int32_t* inv, const float* topk_w,
+                   const float* h, int T, int K, float* x_out, void* stream);
+
+int mlt_argmax(const float* logits, int T, int V, int32_t* ids, float* margin, void* stream);
+
+int mlt_gqa_decode_paged(const uint16_t* q, int ldq, const uint16_t* k_pool,
+                         const uint16_t* v_pool, const int32_t* block_table, int max_pages,
+                         const int32_t* seq, const int32_t* ctx, int T, int nq, int nkv, int d,
+                         int page, void* out_packed, int R, float* out_rowmajor, void* stream);
+int mlt_kv_append(const uint16_t* qkv_bf16, int nq, int nkv, int d, const int32_t* seq,
+                  const int32_t* pos, int T, const int32_t* block_table, int max_pages, int page,
+                  uint16_t* k_pool, uint16_t* v_pool, void* stream);
+
+/* Host: rotary cos/sin table [max_pos][d/2] as (cos, sin) float pairs, angle
+ * computed in double (theta^(-2i/d) * pos). */
+int mlt_rope_table(int max_pos, int d, double theta, float* host_out);
+
+/* Host: synthetic weights, element i of tensor tid: splitmix64 counter PRNG
+ * (DESIGN.md §3), bf16 RNE.  Multi-threaded. */
+int mlt_synth_bf16(uint64_t seed, uint64_t tid, int64_t n, float scale, int is_norm,
+                   uint16_t* host_out);
+
 #ifdef __cplusplus
 }
 #endif

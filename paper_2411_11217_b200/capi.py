@@ -362,3 +362,73 @@ def load_product() -> Api:
                               f" g.build()'` (make -C paper_2411_11217_b200/csrc)")
         _product = Api(C.CDLL(LIB_PATH), "mlt_")
     return _product
+
+
+# ---------------------------------------------------------------------------
+# Kernel-level entry points (device pointers are passed as integers).
+# ---------------------------------------------------------------------------
+class GemmArgs(C.Structure):
+    _fields_ = [("a_table", C.c_void_p), ("n_mats", C.c_int32), ("G", C.c_int32),
+                ("RB", C.c_int32), ("K", C.c_int32), ("b", C.c_void_p), ("R", C.c_int32),
+                ("b_off", C.c_void_p), ("b_cnt", C.c_void_p), ("rows_dense", C.c_int32),
+                ("n_cap", C.c_int32), ("epi", C.c_int32), ("alpha", C.c_float),
+                ("out_f32", C.c_void_p), ("ldo", C.c_int32), ("residual", C.c_void_p),
+                ("ldr", C.c_int32), ("out_packed", C.c_void_p), ("out_R", C.c_int32)]
+
+
+V, I, F = C.c_void_p, C.c_int, C.c_float
+_KSIGS = {
+    "pack_weight": [V, C.c_int64, C.c_int64, V],
+    "unpack_rows": [V, C.c_int64, C.c_int64, C.c_int64, V],
+    "pack_rows_host": [V, C.c_int64, C.c_int64, C.c_int64, V],
+    "gemm": [C.POINTER(GemmArgs), V],
+    "embed": [V, V, I, I, V, V],
+    "rmsnorm_pack": [V, V, I, I, F, V, I, V],
+    "pack_rows": [V, I, I, I, V, I, V],
+    "rope_qkv": [V, V, V, I, I, I, I, V, V],
+    "router_topk": [V, V, F, V, V, I, I, I, I, V, V, V, V, V],
+    "moe_permute": [V, V, I, I, I, I, V, V, V, V, V, I, V],
+    "moe_combine": [V, V, I, V, V, I, I, I, V, V],
+    "expert_ffn": [V, I, V, V, V, V, I, I, I, I, V, V, V, V, V, I, I, V, V],
+    "argmax": [V, I, I, V, V, V],
+    "gqa_decode_paged": [V, I, V, V, V, I, V, V, I, I, I, I, I, V, I, V, V],
+    "kv_append": [V, I, I, I, V, V, I, V, I, I, V, V, V],
+    "rope_table": [I, I, C.c_double, V],
+    "synth_bf16": [C.c_uint64, C.c_uint64, C.c_int64, F, I, V],
+}
+
+
+class Kernels:
+    """Raw kernel entry points; every call raises MltError on failure."""
+
+    def __init__(self, lib: C.CDLL):
+        self.lib = lib
+        self._err = lib.mlt_last_error
+        self._err.restype = C.c_char_p
+        for name, args in _KSIGS.items():
+            f = getattr(lib, "mlt_" + name)
+            f.restype, f.argtypes = C.c_int, args
+            setattr(self, "_" + name, f)
+
+    def __getattr__(self, name):
+        raw = self.__dict__.get("_" + name)
+        if raw is None:
+            raise AttributeError(name)
+
+        def call(*args):
+            rc = raw(*args)
+            if rc < 0:
+                raise _EXC.get(rc, MltError)(rc, (self._err() or b"").decode())
+            return rc
+        return call
+
+
+_kernels = None
+
+
+def load_kernels() -> Kernels:
+    global _kernels
+    if _kernels is None:
+        load_product()
+        _kernels = Kernels(_product.lib)
+    return _kernels

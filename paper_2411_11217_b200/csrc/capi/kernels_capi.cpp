@@ -1,0 +1,252 @@
+// C ABI over the sm_100a kernels (include/mlt.h, "Kernel-level entry
+// points").  Thin: argument checks, cudaError -> MLT_ERR_CUDA, no hidden
+// allocation except mlt_expert_ffn's (none: all buffers caller-owned).
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../kernels/kernels.hpp"
+#include "../runtime/host_layout.hpp"
+#include "lightplan/pipesim.hpp"
+#include "lightplan/planner.hpp"
+#include "status.hpp"
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+    MLT_GUARD_BODY(lightplan)
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw mlt::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        ck(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
+    }
+    return n;
+}
+
+cudaStream_t st(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
+    mltk::GemmArgs g;
+    g.a_table = reinterpret_cast<const uint8_t* const*>(a->a_table);
+    g.n_mats = a->n_mats;
+    g.G = a->G;
+    g.RB = a->RB;
+    g.K = a->K;
+    g.b = reinterpret_cast<const uint8_t*>(a->b);
+    g.R = a->R;
+    g.b_off = a->b_off;
+    g.b_cnt = a->b_cnt;
+    g.rows_dense = a->rows_dense;
+    g.n_cap = a->n_cap;
+    g.epi = a->epi;
+    g.alpha = a->alpha;
+    g.out_f32 = a->out_f32;
+    g.ldo = a->ldo;
+    g.residual = a->residual;
+    g.ldr = a->ldr;
+    g.out_packed = reinterpret_cast<uint8_t*>(a->out_packed);
+    g.out_R = a->out_R;
+    return g;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mlt_pack_weight(const uint16_t* src, int64_t M, int64_t K, uint16_t* dst) {
+    return guard([&] {
+        if (M % 128 || K % 64 || M <= 0 || K <= 0) throw std::invalid_argument("pack_weight: M%128, K%64");
+        mlt::pack_weight(src, M, K, dst);
+        return MLT_OK;
+    });
+}
+
+int mlt_unpack_rows(const uint8_t* packed, int64_t R, int64_t rows, int64_t K, uint16_t* dst) {
+    return guard([&] {
+        if (K % 64 || R % 8 || rows > R) throw std::invalid_argument("unpack_rows: K%64, R%8, rows<=R");
+        mlt::unpack_rows(packed, R, rows, K, dst);
+        return MLT_OK;
+    });
+}
+
+int mlt_pack_rows_host(const uint16_t* src, int64_t rows, int64_t K, int64_t R, uint8_t* dst) {
+    return guard([&] {
+        if (K % 64 || R % 8 || rows > R) throw std::invalid_argument("pack_rows: K%64, R%8, rows<=R");
+        mlt::pack_rows(src, rows, K, R, dst);
+        return MLT_OK;
+    });
+}
+
+int mlt_gemm(const mlt_gemm_args_t* a, void* stream) {
+    return guard([&] {
+        ck(mltk::launch_gemm(to_args(a), sm_count(), st(stream)), "gemm");
+        return MLT_OK;
+    });
+}
+
+int mlt_embed(const int32_t* tokens, const uint16_t* table, int T, int H, float* x, void* s) {
+    return guard([&] {
+        ck(mltk::launch_embed(tokens, table, T, H, x, st(s)), "embed");
+        return MLT_OK;
+    });
+}
+
+int mlt_rmsnorm_pack(const float* x, const uint16_t* gamma, int T, int H, float eps, void* out,
+                     int R, void* s) {
+    return guard([&] {
+        ck(mltk::launch_rmsnorm_pack(x, gamma, T, H, eps, reinterpret_cast<uint8_t*>(out), R, st(s)),
+           "rmsnorm_pack");
+        return MLT_OK;
+    });
+}
+
+int mlt_pack_rows(const uint16_t* src, int ld, int T, int K, void* dst, int R, void* s) {
+    return guard([&] {
+        ck(mltk::launch_pack_rows(src, ld, T, K, reinterpret_cast<uint8_t*>(dst), R, st(s)), "pack_rows");
+        return MLT_OK;
+    });
+}
+
+int mlt_rope_qkv(const float* qkv, const int32_t* pos, const void* rope, int T, int nq, int nkv,
+                 int d, uint16_t* out, void* s) {
+    return guard([&] {
+        ck(mltk::launch_rope_qkv(qkv, pos, reinterpret_cast<const float2*>(rope), T, nq, nkv, d, out,
+                                 st(s)),
+           "rope_qkv");
+        return MLT_OK;
+    });
+}
+
+int mlt_router_topk(const float* x, const uint16_t* gamma, float eps, const uint16_t* hn_in,
+                    const uint16_t* w, int T, int H, int E, int K, uint16_t* hn_out, float* logits,
+                    int32_t* idx, float* wts, void* s) {
+    return guard([&] {
+        ck(mltk::launch_router(x, gamma, eps, hn_in, w, T, H, E, K, hn_out, logits, idx, wts, st(s)),
+           "router");
+        return MLT_OK;
+    });
+}
+
+int mlt_moe_permute(const int32_t* idx, const uint16_t* hn, int T, int H, int E, int K,
+                    int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv, void* xp, int R,
+                    void* s) {
+    return guard([&] {
+        ck(mltk::launch_moe_permute(idx, hn, T, H, E, K, counts, offsets, perm, inv,
+                                    reinterpret_cast<uint8_t*>(xp), R, st(s)),
+           "moe_permute");
+        return MLT_OK;
+    });
+}
+
+int mlt_moe_combine(const float* h, const float* y, int ldy, const int32_t* inv, const float* w,
+                    int T, int H, int K, float* x, void* s) {
+    return guard([&] {
+        ck(mltk::launch_moe_combine(h, y, ldy, inv, w, T, H, K, x, st(s)), "moe_combine");
+        return MLT_OK;
+    });
+}
+
+int mlt_expert_ffn(const void* xp, int R, const int32_t* counts, const int32_t* offsets,
+                   const void* w13, const void* w2, int E, int H, int F, int n_cap, void* inter,
+                   float* y, const int32_t* inv, const float* wts, const float* h, int T, int K,
+                   float* x_out, void* s) {
+    return guard([&] {
+        if (H % 128 || F % 128) throw std::invalid_argument("expert_ffn: H, F must be multiples of 128");
+        mltk::GemmArgs g;
+        g.a_table = reinterpret_cast<const uint8_t* const*>(w13);
+        g.n_mats = 2;
+        g.G = E;
+        g.RB = F / 128;
+        g.K = H;
+        g.b = reinterpret_cast<const uint8_t*>(xp);
+        g.R = R;
+        g.b_off = offsets;
+        g.b_cnt = counts;
+        g.n_cap = n_cap;
+        g.epi = mltk::kEpiSiluPacked;
+        g.out_packed = reinterpret_cast<uint8_t*>(inter);
+        g.out_R = R;
+        ck(mltk::launch_gemm(g, sm_count(), st(s)), "expert gate/up");
+        mltk::GemmArgs d;
+        d.a_table = reinterpret_cast<const uint8_t* const*>(w2);
+        d.n_mats = 1;
+        d.G = E;
+        d.RB = H / 128;
+        d.K = F;
+        d.b = reinterpret_cast<const uint8_t*>(inter);
+        d.R = R;
+        d.b_off = offsets;
+        d.b_cnt = counts;
+        d.n_cap = n_cap;
+        d.epi = mltk::kEpiF32;
+        d.out_f32 = y;
+        d.ldo = H;
+        ck(mltk::launch_gemm(d, sm_count(), st(s)), "expert down");
+        if (x_out) ck(mltk::launch_moe_combine(h, y, H, inv, wts, T, H, K, x_out, st(s)), "combine");
+        return MLT_OK;
+    });
+}
+
+int mlt_argmax(const float* logits, int T, int V, int32_t* ids, float* margin, void* s) {
+    return guard([&] {
+        ck(mltk::launch_argmax(logits, T, V, ids, margin, st(s)), "argmax");
+        return MLT_OK;
+    });
+}
+
+int mlt_gqa_decode_paged(const uint16_t* q, int ldq, const uint16_t* kp, const uint16_t* vp,
+                         const int32_t* bt, int max_pages, const int32_t* seq, const int32_t* ctx,
+                         int T, int nq, int nkv, int d, int page, void* out_packed, int R,
+                         float* out_f, void* s) {
+    return guard([&] {
+        ck(mltk::launch_gqa_decode_paged(q, ldq, kp, vp, bt, max_pages, seq, ctx, T, nq, nkv, d, page,
+                                         reinterpret_cast<uint8_t*>(out_packed), R, out_f, st(s)),
+           "gqa_decode_paged");
+        return MLT_OK;
+    });
+}
+
+int mlt_kv_append(const uint16_t* qkv, int nq, int nkv, int d, const int32_t* seq,
+                  const int32_t* pos, int T, const int32_t* bt, int max_pages, int page,
+                  uint16_t* kp, uint16_t* vp, void* s) {
+    return guard([&] {
+        ck(mltk::launch_kv_append(qkv, nq, nkv, d, seq, pos, T, bt, max_pages, page, kp, vp, st(s)),
+           "kv_append");
+        return MLT_OK;
+    });
+}
+
+int mlt_rope_table(int max_pos, int d, double theta, float* out) {
+    return guard([&] {
+        const int half = d / 2;
+        for (int p = 0; p < max_pos; ++p)
+            for (int i = 0; i < half; ++i) {
+                const double inv = std::pow(theta, -2.0 * static_cast<double>(i) / static_cast<double>(d));
+                const double ang = static_cast<double>(p) * inv;
+                out[(static_cast<int64_t>(p) * half + i) * 2] = static_cast<float>(std::cos(ang));
+                out[(static_cast<int64_t>(p) * half + i) * 2 + 1] = static_cast<float>(std::sin(ang));
+            }
+        return MLT_OK;
+    });
+}
+
+int mlt_synth_bf16(uint64_t seed, uint64_t tid, int64_t n, float scale, int is_norm, uint16_t* out) {
+    return guard([&] {
+        mlt::synth_bf16(seed, tid, 0, n, scale, is_norm != 0, out);
+        return MLT_OK;
+    });
+}
+
+}  // extern "C"

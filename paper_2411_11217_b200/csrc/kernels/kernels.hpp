@@ -1,0 +1,105 @@
+// Host-side launch interface of the sm_100a kernels (namespace mltk).  The
+// C ABI (capi/kernels_capi.cpp) and the runtime call only these.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mltk {
+
+enum { kEpiF32 = 0, kEpiSiluPacked = 1 };
+
+struct GemmArgs {
+    // A operand: page table of 128-row weight blocks, [n_mats][G][RB].
+    const uint8_t* const* a_table = nullptr;
+    int n_mats = 1;  // 2 = fused gate/up
+    int G = 1;       // groups (experts)
+    int RB = 0;      // 128-row blocks per matrix
+    int K = 0;       // reduction length (multiple of 64)
+    // B operand: packed activations with row capacity R.
+    const uint8_t* b = nullptr;
+    int R = 0;
+    const int32_t* b_off = nullptr;  // [G+1] padded row offset per group (nullptr: dense)
+    const int32_t* b_cnt = nullptr;  // [G] valid rows per group (nullptr: dense)
+    int rows_dense = 0;              // rows when b_cnt == nullptr
+    int n_cap = 16;                  // max tokens per tile (16..256, multiple of 16)
+    // epilogue
+    int epi = kEpiF32;
+    float alpha = 1.0f;
+    float* out_f32 = nullptr;  // [row][ldo], row = b_off[g] + n
+    int ldo = 0;
+    const float* residual = nullptr;  // added in kEpiF32 (same row indexing)
+    int ldr = 0;
+    uint8_t* out_packed = nullptr;  // kEpiSiluPacked: packed B layout, capacity out_R
+    int out_R = 0;
+    // filled by launch_gemm
+    int stages = 0, acc_stages = 0, tmem_cols = 0;
+};
+
+cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream);
+int gemm_smem_bytes(int n_mats, int n_cap, int stages);
+
+// x_out[t][:] = float(table[tokens[t]][:])
+cudaError_t launch_embed(const int32_t* tokens, const uint16_t* table, int T, int H, float* x_out,
+                         cudaStream_t s);
+
+// RMSNorm(x) * gamma -> bf16, written in packed B layout (capacity R rows).
+cudaError_t launch_rmsnorm_pack(const float* x, const uint16_t* gamma, int T, int H, float eps,
+                                uint8_t* out_packed, int R, cudaStream_t s);
+
+// Row-major bf16 [T, K] -> packed B layout (capacity R).
+cudaError_t launch_pack_rows(const uint16_t* src, int ld, int T, int K, uint8_t* dst, int R,
+                             cudaStream_t s);
+
+// RoPE (rotate-half) on the q and k parts of qkv fp32 [T, (nq+2nkv)d] using
+// cos/sin table [max_pos][d/2] (float2), output bf16 [T, (nq+2nkv)d] rows
+// (q | k | v): the D1 offload layout.
+cudaError_t launch_rope_qkv(const float* qkv, const int32_t* pos, const float2* rope, int T,
+                            int nq, int nkv, int d, uint16_t* out, cudaStream_t s);
+
+// Router (SURVEY.md §2c router_topk_permute, first half): optional fused
+// RMSNorm (x fp32 + gamma) or direct bf16 input; logits with the fixed lane
+// tree of oracle orc_router; top-k + softmax over the selected logits.
+cudaError_t launch_router(const float* x, const uint16_t* gamma, float eps,
+                          const uint16_t* hn_in, const uint16_t* w_router, int T, int H, int E,
+                          int K, uint16_t* hn_out, float* logits, int32_t* topk_idx,
+                          float* topk_w, cudaStream_t s);
+
+// Stable (expert, token, slot) permutation with per-expert 16-row padding
+// and gather of hn rows into the packed expert operand X (capacity R rows).
+// counts[E], offsets[E+1] (padded), perm[R] (padded row -> t*K+s, -1 pad),
+// inv[T*K] (slot -> padded row).
+cudaError_t launch_moe_permute(const int32_t* topk_idx, const uint16_t* hn, int T, int H, int E,
+                               int K, int32_t* counts, int32_t* offsets, int32_t* perm,
+                               int32_t* inv, uint8_t* x_packed, int R, cudaStream_t s);
+
+// x_out[t] = h[t] + sum_s w[t,s] * y[inv[t*K+s]]  (fp32, slot order).
+cudaError_t launch_moe_combine(const float* h, const float* y, int ldy, const int32_t* inv,
+                               const float* topk_w, int T, int H, int K, float* x_out,
+                               cudaStream_t s);
+
+// Greedy ids: argmax (ties -> lower index) of fp32 logits [T, V]; margin =
+// top1 - top2 (optional).
+cudaError_t launch_argmax(const float* logits, int T, int V, int32_t* ids, float* margin,
+                          cudaStream_t s);
+
+// GQA decode attention over a paged KV cache (SURVEY.md §2c
+// gqa_decode_paged).  KV pages hold `page` tokens x n_kv heads x d (bf16),
+// K and V in separate pools; block_table[seq][max_pages]; ctx[t] tokens
+// of sequence seq[t].  q bf16 rows with leading dimension ldq (the rope
+// output [T, (nq+2nkv)d] works directly); output written in packed B layout
+// (capacity R) for the O projection and/or fp32 row-major.
+cudaError_t launch_gqa_decode_paged(const uint16_t* q, int ldq, const uint16_t* k_pool,
+                                    const uint16_t* v_pool, const int32_t* block_table,
+                                    int max_pages, const int32_t* seq, const int32_t* ctx, int T,
+                                    int nq, int nkv, int d, int page, uint8_t* out_packed, int R,
+                                    float* out_rowmajor, cudaStream_t s);
+
+// Append this step's k/v (bf16 rows from the rope output [T, (nq+2nkv)d])
+// into the paged cache at position ctx[t]-1 of sequence seq[t].
+cudaError_t launch_kv_append(const uint16_t* qkv_bf16, int nq, int nkv, int d,
+                             const int32_t* seq, const int32_t* pos, int T,
+                             const int32_t* block_table, int max_pages, int page,
+                             uint16_t* k_pool, uint16_t* v_pool, cudaStream_t s);
+
+}  // namespace mltk

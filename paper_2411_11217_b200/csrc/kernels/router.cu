@@ -1,0 +1,216 @@
+// Top-k router + token permutation (north_star item 2; SURVEY.md §2c
+// router_topk_permute), warp-level.
+//
+// router_kernel: one CTA per token.  Optional fused RMSNorm of the fp32
+// residual (the PostAttn norm), then one warp per expert computes the logit
+// with the FIXED reduction tree of oracle/oracle_numerics.c:orc_router —
+// lane l accumulates 8-element chunks c = l, l+32, ... with fmaf in element
+// order, then a xor butterfly 16,8,4,2,1 — so on identical bf16 inputs the
+// logits, the top-k indices and the permutation are bit-identical to the CPU
+// oracle.  Top-k on logits (softmax is monotone), ties to the lower index;
+// weights = softmax over the k selected logits.
+//
+// permute_kernel: every CTA recomputes the stable (expert, token, slot)
+// order from topk_idx with warp ballots (no atomics -> deterministic), pads
+// each expert segment to 16 rows (UMMA N granularity), and gathers its share
+// of hn rows into the packed expert operand.  CTA 0 publishes counts,
+// offsets, perm and inv.
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace mltk {
+namespace {
+
+constexpr int kMaxE = 64;
+constexpr int kMaxSlots = 4096;
+
+__global__ void router_kernel(const float* x, const uint16_t* gamma, float eps,
+                              const uint16_t* hn_in, const uint16_t* w, int H, int E, int K,
+                              uint16_t* hn_out, float* logits, int32_t* topk_idx, float* topk_w) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint16_t* hn = reinterpret_cast<uint16_t*>(sm);                 // H bf16
+    float* lg = reinterpret_cast<float*>(sm + ((H * 2 + 15) & ~15)); // E fp32
+    __shared__ float red[32];
+    const int t = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+
+    if (hn_in) {
+        for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8)
+            *reinterpret_cast<uint4*>(hn + i) =
+                *reinterpret_cast<const uint4*>(hn_in + static_cast<int64_t>(t) * H + i);
+    } else {
+        const float* xr = x + static_cast<int64_t>(t) * H;
+        float ss = 0.0f;
+        for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
+            const float4 v = *reinterpret_cast<const float4*>(xr + i);
+            ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        }
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
+        if (lane == 0) red[warp] = ss;
+        __syncthreads();
+        float tot = 0.0f;
+        for (int i = 0; i < nw; ++i) tot += red[i];
+        const float r = 1.0f / sqrtf(tot / static_cast<float>(H) + eps);
+        for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
+            const float4 a = *reinterpret_cast<const float4*>(xr + i);
+            const float4 b = *reinterpret_cast<const float4*>(xr + i + 4);
+            const uint4 gv = *reinterpret_cast<const uint4*>(gamma + i);
+            const uint16_t* g = reinterpret_cast<const uint16_t*>(&gv);
+            const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            uint4 o;
+            uint16_t* ob = reinterpret_cast<uint16_t*>(&o);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ob[j] = f32_to_bf16_bits(v[j] * r * bf16_bits_to_f32(g[j]));
+            *reinterpret_cast<uint4*>(hn + i) = o;
+        }
+    }
+    __syncthreads();
+    if (hn_out)
+        for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8)
+            *reinterpret_cast<uint4*>(hn_out + static_cast<int64_t>(t) * H + i) =
+                *reinterpret_cast<const uint4*>(hn + i);
+
+    const int chunks = H / 8;
+    for (int e = warp; e < E; e += nw) {
+        const uint16_t* we = w + static_cast<int64_t>(e) * H;
+        float acc = 0.0f;
+        for (int c = lane; c < chunks; c += 32) {
+            const uint4 xv = *reinterpret_cast<const uint4*>(hn + c * 8);
+            const uint4 wv = *reinterpret_cast<const uint4*>(we + c * 8);
+            const uint16_t* xb = reinterpret_cast<const uint16_t*>(&xv);
+            const uint16_t* wb = reinterpret_cast<const uint16_t*>(&wv);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc = __fmaf_rn(bf16_bits_to_f32(xb[j]), bf16_bits_to_f32(wb[j]), acc);
+        }
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, m));
+        if (lane == 0) lg[e] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (logits)
+            for (int e = 0; e < E; ++e) logits[static_cast<int64_t>(t) * E + e] = lg[e];
+        uint64_t used = 0;
+        int sel[8];
+        for (int s = 0; s < K; ++s) {
+            int best = -1;
+            for (int e = 0; e < E; ++e)
+                if (!((used >> e) & 1) && (best < 0 || lg[e] > lg[best])) best = e;
+            used |= 1ull << best;
+            sel[s] = best;
+            topk_idx[t * K + s] = best;
+        }
+        const float top = lg[sel[0]];
+        float ws[8], sum = 0.0f;
+        for (int s = 0; s < K; ++s) {
+            ws[s] = expf(lg[sel[s]] - top);
+            sum += ws[s];
+        }
+        for (int s = 0; s < K; ++s) topk_w[t * K + s] = ws[s] / sum;
+    }
+}
+
+// Exclusive prefix over the block of a per-thread 0/1 flag, in thread order.
+__device__ __forceinline__ int block_excl_scan(int flag, int* warp_tot, int* total) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    const int in_warp = __popc(bal & ((1u << lane) - 1u));
+    __syncthreads();
+    if (lane == 0) warp_tot[warp] = __popc(bal);
+    __syncthreads();
+    int base = 0, tot = 0;
+    for (int i = 0; i < nw; ++i) {
+        const int c = warp_tot[i];
+        if (i < warp) base += c;
+        tot += c;
+    }
+    *total = tot;
+    return base + in_warp;
+}
+
+__global__ void permute_kernel(const int32_t* topk_idx, const uint16_t* hn, int T, int H, int E,
+                               int K, int32_t* counts, int32_t* offsets, int32_t* perm,
+                               int32_t* inv, uint8_t* xp, int R) {
+    __shared__ int s_cnt[kMaxE];
+    __shared__ int s_off[kMaxE + 1];
+    __shared__ int warp_tot[32];
+    extern __shared__ int s_slot_row[];  // [T*K] padded row of each slot
+    const int TK = T * K;
+    // Ranks: slot i = t*K + s; for expert e, rank = #slots j < i choosing e.
+    // Slots are processed in chunks of blockDim (thread order == slot order).
+    for (int e = 0; e < E; ++e) {
+        int running = 0;
+        for (int base = 0; base < TK; base += blockDim.x) {
+            const int i = base + threadIdx.x;
+            const int flag = (i < TK && topk_idx[i] == e) ? 1 : 0;
+            int tot;
+            const int r = block_excl_scan(flag, warp_tot, &tot);
+            if (flag) s_slot_row[i] = running + r;  // rank within expert for now
+            running += tot;
+        }
+        if (threadIdx.x == 0) s_cnt[e] = running;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        s_off[0] = 0;
+        for (int e = 0; e < E; ++e) s_off[e + 1] = s_off[e] + ((s_cnt[e] + 15) & ~15);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < TK; i += blockDim.x) s_slot_row[i] += s_off[topk_idx[i]];
+    __syncthreads();
+    const int rows = s_off[E];
+    if (blockIdx.x == 0) {
+        for (int e = threadIdx.x; e < E; e += blockDim.x) counts[e] = s_cnt[e];
+        for (int e = threadIdx.x; e <= E; e += blockDim.x) offsets[e] = s_off[e];
+        for (int r = threadIdx.x; r < R; r += blockDim.x) perm[r] = -1;
+        __syncthreads();
+        for (int i = threadIdx.x; i < TK; i += blockDim.x) {
+            inv[i] = s_slot_row[i];
+            perm[s_slot_row[i]] = i;
+        }
+    }
+    // Gather: 16-byte chunks of (slot, k) distributed over the grid.
+    const int cpr = H / 8;
+    const int64_t work = static_cast<int64_t>(TK) * cpr;
+    for (int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < work;
+         w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(w / cpr), c = static_cast<int>(w % cpr);
+        const int t = i / K;
+        *reinterpret_cast<uint4*>(xp + b_packed_off(s_slot_row[i], c * 8, R)) =
+            *reinterpret_cast<const uint4*>(hn + static_cast<int64_t>(t) * H + c * 8);
+    }
+    (void)rows;
+}
+
+}  // namespace
+
+cudaError_t launch_router(const float* x, const uint16_t* gamma, float eps, const uint16_t* hn_in,
+                          const uint16_t* w, int T, int H, int E, int K, uint16_t* hn_out,
+                          float* logits, int32_t* topk_idx, float* topk_w, cudaStream_t s) {
+    if (T <= 0) return cudaSuccess;
+    if (H % 256 || E > kMaxE || K > 8 || K > E || (!hn_in && (!x || !gamma)))
+        return cudaErrorInvalidValue;
+    const int smem = ((H * 2 + 15) & ~15) + E * 4;
+    router_kernel<<<T, 256, smem, s>>>(x, gamma, eps, hn_in, w, H, E, K, hn_out, logits, topk_idx,
+                                       topk_w);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_moe_permute(const int32_t* topk_idx, const uint16_t* hn, int T, int H, int E,
+                               int K, int32_t* counts, int32_t* offsets, int32_t* perm,
+                               int32_t* inv, uint8_t* xp, int R, cudaStream_t s) {
+    if (T <= 0) return cudaSuccess;
+    if (E > kMaxE || T * K > kMaxSlots || H % 64 || R < T * K + 16 * E) return cudaErrorInvalidValue;
+    const int64_t work = static_cast<int64_t>(T) * K * (H / 8);
+    int grid = static_cast<int>((work + 255) / 256);
+    if (grid > 296) grid = 296;
+    if (grid < 1) grid = 1;
+    permute_kernel<<<grid, 256, T * K * sizeof(int), s>>>(topk_idx, hn, T, H, E, K, counts, offsets,
+                                                          perm, inv, xp, R);
+    return cudaGetLastError();
+}
+
+}  // namespace mltk

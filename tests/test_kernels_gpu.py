@@ -1,0 +1,264 @@
+"""Kernel parity on the B200 through the C ABI (mlt_*).
+
+* GEMM / expert FFN / RMSNorm / attention: against a plain PyTorch fp32
+  reference of the same op on the same bf16 inputs (tolerances stated per
+  test; only summation order differs).
+* Router: BIT-EXACT against the CPU oracle (oracle/oracle_numerics.c
+  orc_router) on identical bf16 inputs — logits, top-k indices and the
+  stable permutation (BASELINE.json correctness item 1).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2411_11217_b200 import capi  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+@pytest.fixture(scope="module")
+def K():
+    return capi.load_kernels()
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def rand_bf16(*shape, scale=1.0, gen=None):
+    return (torch.randn(*shape, generator=gen) * scale).to(torch.bfloat16)
+
+
+def bf16_bits(t):  # torch bf16 -> numpy uint16 view
+    return t.contiguous().view(torch.int16).numpy().view(np.uint16)
+
+
+def pack_weight_dev(K, w_bf16):
+    """Host-pack a [M, K] bf16 weight and upload; returns (device buffer, block pointers)."""
+    M, Kd = w_bf16.shape
+    src = bf16_bits(w_bf16.cpu())
+    dst = np.empty_like(src)
+    K.pack_weight(src.ctypes.data_as(C.c_void_p), M, Kd, dst.ctypes.data_as(C.c_void_p))
+    dev = torch.from_numpy(dst.view(np.int16).copy()).cuda()
+    blocks = [dev.data_ptr() + rb * 128 * Kd * 2 for rb in range(M // 128)]
+    return dev, blocks
+
+
+def table(ptr_lists):
+    flat = [p for lst in ptr_lists for p in lst]
+    return torch.tensor(flat, dtype=torch.int64, device="cuda")
+
+
+def pack_rows_dev(K, x_bf16, R):
+    T, Kd = x_bf16.shape
+    out = torch.zeros(R * Kd, dtype=torch.int16, device="cuda")
+    xd = x_bf16.cuda().contiguous()
+    K.pack_rows(ptr(xd), Kd, T, Kd, ptr(out), R, stream())
+    return out
+
+
+@pytest.mark.parametrize("T,M,Kd,n_cap", [(1, 128, 64, 16), (16, 256, 512, 16), (37, 384, 1024, 64),
+                                          (64, 256, 4096, 64), (200, 128, 256, 208),
+                                          (256, 512, 1024, 256), (300, 256, 512, 128)])
+def test_dense_gemm_matches_torch(K, T, M, Kd, n_cap):
+    g = torch.Generator().manual_seed(T * 7 + M)
+    w = rand_bf16(M, Kd, scale=Kd ** -0.5, gen=g)
+    x = rand_bf16(T, Kd, gen=g)
+    R = (T + 15) // 16 * 16
+    wdev, blocks = pack_weight_dev(K, w)
+    tab = table([blocks])
+    xp = pack_rows_dev(K, x, R)
+    res = torch.randn(T, M, device="cuda")
+    out = torch.zeros(R, M, device="cuda")
+    a = capi.GemmArgs(a_table=tab.data_ptr(), n_mats=1, G=1, RB=M // 128, K=Kd, b=xp.data_ptr(),
+                      R=R, b_off=None, b_cnt=None, rows_dense=T, n_cap=n_cap, epi=0, alpha=1.0,
+                      out_f32=out.data_ptr(), ldo=M, residual=res.data_ptr(), ldr=M)
+    K.gemm(C.byref(a), stream())
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().T + res.cpu()
+    err = (out[:T].cpu() - ref).abs().max().item()
+    assert err <= 2e-3 * max(1.0, ref.abs().max().item()), err
+
+
+def _expert_setup(T, H, Fd, E, Kk, seed):
+    g = torch.Generator().manual_seed(seed)
+    hn = rand_bf16(T, H, gen=g)
+    w1 = [rand_bf16(Fd, H, scale=H ** -0.5, gen=g) for _ in range(E)]
+    w3 = [rand_bf16(Fd, H, scale=H ** -0.5, gen=g) for _ in range(E)]
+    w2 = [rand_bf16(H, Fd, scale=Fd ** -0.5, gen=g) for _ in range(E)]
+    wr = rand_bf16(E, H, scale=H ** -0.5, gen=g)
+    return hn, w1, w3, w2, wr
+
+
+@pytest.mark.parametrize("T,H,Fd,E,Kk,n_cap", [(4, 256, 384, 8, 2, 16), (64, 512, 768, 8, 2, 64),
+                                               (256, 512, 256, 8, 2, 256), (33, 256, 256, 16, 4, 32)])
+def test_router_permute_expert_ffn(K, T, H, Fd, E, Kk, n_cap):
+    from oracle import bind as orc
+    hn, w1, w3, w2, wr = _expert_setup(T, H, Fd, E, Kk, seed=T + H)
+    hn_d, wr_d = hn.cuda(), wr.cuda()
+    logits = torch.zeros(T, E, device="cuda")
+    idx = torch.zeros(T, Kk, dtype=torch.int32, device="cuda")
+    wts = torch.zeros(T, Kk, device="cuda")
+    K.router_topk(None, None, 0.0, ptr(hn_d), ptr(wr_d), T, H, E, Kk, None, ptr(logits), ptr(idx),
+                  ptr(wts), stream())
+    R = T * Kk + 16 * E
+    R = (R + 15) // 16 * 16
+    cnt = torch.zeros(E, dtype=torch.int32, device="cuda")
+    off = torch.zeros(E + 1, dtype=torch.int32, device="cuda")
+    perm = torch.zeros(R, dtype=torch.int32, device="cuda")
+    inv = torch.zeros(T * Kk, dtype=torch.int32, device="cuda")
+    xp = torch.zeros(R * H, dtype=torch.int16, device="cuda")
+    K.moe_permute(ptr(idx), ptr(hn_d), T, H, E, Kk, ptr(cnt), ptr(off), ptr(perm), ptr(inv),
+                  ptr(xp), R, stream())
+    torch.cuda.synchronize()
+
+    # --- bit-exact router vs the CPU oracle on identical bf16 inputs ---
+    o_log, o_idx, o_w, o_perm, o_off = orc.router(bf16_bits(hn), bf16_bits(wr), Kk)
+    assert np.array_equal(logits.cpu().numpy().view(np.uint32), o_log.view(np.uint32))
+    assert np.array_equal(idx.cpu().numpy(), o_idx)
+    assert np.allclose(wts.cpu().numpy(), o_w, rtol=1e-6, atol=1e-7)
+    c = cnt.cpu().numpy()
+    assert np.array_equal(np.concatenate([[0], np.cumsum(c)]), o_off)
+    offs, pm = off.cpu().numpy(), perm.cpu().numpy()
+    unpadded = np.concatenate([pm[offs[e]:offs[e] + c[e]] for e in range(E)])
+    assert np.array_equal(unpadded, o_perm)
+    iv = inv.cpu().numpy()
+    assert all(pm[iv[i]] == i for i in range(T * Kk))
+
+    # --- expert FFN (gate/up + SiLU fused, down) + combine vs torch fp32 ---
+    wd = []
+    b13 = [[], []]
+    b2 = []
+    for e in range(E):
+        d1, p1 = pack_weight_dev(K, w1[e])
+        d3, p3 = pack_weight_dev(K, w3[e])
+        d2, p2 = pack_weight_dev(K, w2[e])
+        wd += [d1, d3, d2]
+        b13[0] += p1
+        b13[1] += p3
+        b2 += p2
+    t13, t2 = table(b13), table([b2])
+    inter = torch.zeros(R * Fd, dtype=torch.int16, device="cuda")
+    y = torch.zeros(R, H, device="cuda")
+    h = torch.randn(T, H, device="cuda")
+    xo = torch.zeros(T, H, device="cuda")
+    K.expert_ffn(ptr(xp), R, ptr(cnt), ptr(off), ptr(t13), ptr(t2), E, H, Fd, n_cap, ptr(inter),
+                 ptr(y), ptr(inv), ptr(wts), ptr(h), T, Kk, ptr(xo), stream())
+    torch.cuda.synchronize()
+    ref = h.cpu().clone()
+    hnf = hn.float()
+    for t in range(T):
+        for s in range(Kk):
+            e = int(o_idx[t, s])
+            a = torch.nn.functional.silu(hnf[t] @ w1[e].float().T) * (hnf[t] @ w3[e].float().T)
+            a = a.to(torch.bfloat16).float()  # the kernel stores the gated product in bf16
+            ref[t] += float(o_w[t, s]) * (a @ w2[e].float().T)
+    err = (xo.cpu() - ref).abs().max().item()
+    assert err <= 1e-2 * max(1.0, ref.abs().max().item()), err
+
+
+def test_rmsnorm_pack_and_embed(K):
+    from oracle import bind as orc
+    T, H, V = 5, 1024, 64
+    g = torch.Generator().manual_seed(3)
+    table_ = rand_bf16(V, H, gen=g).cuda()
+    toks = torch.tensor([3, 0, 63, 7, 7], dtype=torch.int32, device="cuda")
+    x = torch.zeros(T, H, device="cuda")
+    K.embed(ptr(toks), ptr(table_), T, H, ptr(x), stream())
+    gamma = rand_bf16(H, gen=g).cuda()
+    R = 16
+    out = torch.zeros(R * H, dtype=torch.int16, device="cuda")
+    K.rmsnorm_pack(ptr(x), ptr(gamma), T, H, 1e-5, ptr(out), R, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(x.cpu(), table_.cpu()[toks.cpu().long()].float())
+    packed = out.cpu().numpy().view(np.uint16)
+    rows = np.empty((T, H), np.uint16)
+    K.unpack_rows(packed.ctypes.data_as(C.c_void_p), R, T, H, rows.ctypes.data_as(C.c_void_p))
+    ref = orc.rmsnorm(x.cpu().numpy(), bf16_bits(gamma.cpu()), 1e-5, round_bf16=True)
+    got = orc.bf16_to_f32(rows)
+    assert np.abs(got - ref).max() <= 1e-2 * np.abs(ref).max()
+
+
+def test_rope_and_paged_attention(K):
+    from oracle import bind as orc
+    T, nq, nkv, d, page = 6, 8, 2, 128, 16
+    W = (nq + 2 * nkv) * d
+    g = torch.Generator().manual_seed(5)
+    ctx = np.array([1, 15, 16, 17, 100, 300], np.int32)
+    pos = ctx - 1
+    qkv = torch.randn(T, W, generator=g)
+    rope = np.zeros((512, d // 2, 2), np.float32)
+    K.rope_table(512, d, 1e6, rope.ctypes.data_as(C.c_void_p))
+    rope_d = torch.from_numpy(rope).cuda()
+    qkv_d, pos_d = qkv.cuda(), torch.from_numpy(pos).cuda()
+    rb = torch.zeros(T, W, dtype=torch.int16, device="cuda")
+    K.rope_qkv(ptr(qkv_d), ptr(pos_d), ptr(rope_d), T, nq, nkv, d, ptr(rb), stream())
+    torch.cuda.synchronize()
+    roped = orc.rope(qkv.numpy()[:, :(nq + nkv) * d], pos, nq + nkv, d, 1e6)
+    got = orc.bf16_to_f32(rb.cpu().numpy().view(np.uint16))
+    assert np.abs(got[:, :(nq + nkv) * d] - roped).max() < 2e-2
+    assert np.abs(got[:, (nq + nkv) * d:] - qkv.numpy()[:, (nq + nkv) * d:]).max() < 2e-2
+
+    # paged cache: random history for positions < pos, this step's k/v appended by the kernel
+    cap = 320
+    max_pages = cap // page
+    n_pages = T * max_pages
+    perm_pages = np.random.default_rng(0).permutation(n_pages).astype(np.int32)
+    bt = perm_pages.reshape(T, max_pages)
+    kpool = torch.zeros(n_pages * nkv * page * d, dtype=torch.int16, device="cuda")
+    vpool = torch.zeros_like(kpool)
+    hist_k = orc.f32_to_bf16(np.random.default_rng(1).uniform(-1, 1, (T, cap, nkv, d)))
+    hist_v = orc.f32_to_bf16(np.random.default_rng(2).uniform(-1, 1, (T, cap, nkv, d)))
+    kp = np.zeros((n_pages, nkv, page, d), np.uint16)
+    vp = np.zeros_like(kp)
+    for t in range(T):
+        for j in range(pos[t]):
+            pid = bt[t, j // page]
+            kp[pid, :, j % page] = hist_k[t, j]
+            vp[pid, :, j % page] = hist_v[t, j]
+    kpool.copy_(torch.from_numpy(kp.reshape(-1).view(np.int16)))
+    vpool.copy_(torch.from_numpy(vp.reshape(-1).view(np.int16)))
+    bt_d = torch.from_numpy(bt).cuda()
+    seq = torch.arange(T, dtype=torch.int32, device="cuda")
+    ctx_d = torch.from_numpy(ctx).cuda()
+    K.kv_append(ptr(rb), nq, nkv, d, ptr(seq), ptr(pos_d), T, ptr(bt_d), max_pages, page,
+                ptr(kpool), ptr(vpool), stream())
+    out = torch.zeros(T, nq * d, device="cuda")
+    R = 16
+    outp = torch.zeros(R * nq * d, dtype=torch.int16, device="cuda")
+    K.gqa_decode_paged(ptr(rb), W, ptr(kpool), ptr(vpool), ptr(bt_d), max_pages, ptr(seq),
+                       ptr(ctx_d), T, nq, nkv, d, page, ptr(outp), R, ptr(out), stream())
+    torch.cuda.synchronize()
+    rbn = rb.cpu().numpy().view(np.uint16)
+    for t in range(T):  # the appended step
+        hist_k[t, pos[t]] = rbn[t, nq * d:(nq + nkv) * d].reshape(nkv, d)
+        hist_v[t, pos[t]] = rbn[t, (nq + nkv) * d:].reshape(nkv, d)
+    q = orc.bf16_to_f32(rbn[:, :nq * d])
+    ref = orc.attention(q, hist_k, hist_v, ctx, nq, nkv, d)
+    assert np.abs(out.cpu().numpy() - ref).max() < 2e-3
+
+
+def test_argmax(K):
+    T, V = 3, 32000
+    lg = torch.randn(T, V, device="cuda")
+    lg[1, 17] = 100.0
+    lg[1, 5] = 100.0  # tie -> lower index
+    ids = torch.zeros(T, dtype=torch.int32, device="cuda")
+    mg = torch.zeros(T, device="cuda")
+    K.argmax(ptr(lg), T, V, ptr(ids), ptr(mg), stream())
+    torch.cuda.synchronize()
+    ref = lg.cpu().argmax(dim=1)
+    assert ids[0].item() == ref[0].item() and ids[2].item() == ref[2].item()
+    assert ids[1].item() == 5 and mg[1].item() == 0.0
+    top2 = lg[0].topk(2).values
+    assert abs(mg[0].item() - (top2[0] - top2[1]).item()) < 1e-6
