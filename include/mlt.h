@@ -286,6 +286,64 @@ int mlt_rope_table(int max_pos, int d, double theta, float* host_out);
 int mlt_synth_bf16(uint64_t seed, uint64_t tid, int64_t n, float scale, int is_norm,
                    uint16_t* host_out);
 
+/* ==== Decode runtime (one per GPU) =======================================
+ * The engine behind the reference's per-layer decode step: owns the
+ * budget-capped device arena (every device allocation, SURVEY.md §7 hard
+ * part 5), the pinned host weight store and HBM page pool, the host KV cache
+ * and host-core attention, and the CGOPipe executor.  mlt_runtime_decode
+ * builds the reference ScheduleDag for the policy (build_schedule,
+ * pipesim.hpp:85-96), executes it on streams/threads, and returns the
+ * measured per-layer breakdown (LatencyBreakdown fields, planner.hpp:25-35).
+ * Thread-compatible: one caller per runtime.
+ */
+typedef struct mlt_runtime_options_t {
+    int32_t device;
+    double budget_bytes;   /* device memory cap for all runtime allocations */
+    int32_t max_ctx;       /* KV capacity per sequence (>= s + n) */
+    int32_t host_threads;  /* CPU attention threads, 0 = all */
+    int32_t pin_weights;   /* 1: streamed weights page-locked; 0: pageable + pinned staging ring */
+    int32_t vocab;
+    float rms_eps, rope_theta, lm_head_scale;
+    uint64_t seed;         /* synthetic-weight seed */
+} mlt_runtime_options_t;
+
+typedef struct mlt_decode_report_t {
+    double seconds, tokens_per_second;
+    mlt_latency_breakdown_t measured; /* per-layer means of the measured timeline */
+    double h2d_weight_bytes, h2d_bytes, d2h_bytes, steady_layer_time;
+    double utilization[5];
+    int32_t gpu_launches;
+    int32_t timeline_ok; /* 1 when verify_timeline passes on the measured timeline */
+} mlt_decode_report_t;
+
+typedef struct mlt_runtime_info_t {
+    double achieved_weight_ratio;   /* realised r_w */
+    double streamed_bytes_per_layer;
+    double arena_used, arena_capacity;
+    double pin_seconds, gen_seconds;
+} mlt_runtime_info_t;
+
+typedef struct mlt_runtime mlt_runtime;
+
+mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* model, const mlt_policy_t* policy,
+                                const mlt_runtime_options_t* options);
+void mlt_runtime_destroy(mlt_runtime* rt);
+int mlt_runtime_info(const mlt_runtime* rt, mlt_runtime_info_t* out);
+/* Synthetic prompt-stage KV for positions [0, prompt_len); positions := prompt_len. */
+int mlt_runtime_prefill_synthetic(mlt_runtime* rt, int prompt_len, uint64_t seed);
+int mlt_runtime_set_positions(mlt_runtime* rt, const int32_t* host_pos);
+/* `steps` decode steps: host_tokens [N] (step-0 ids), host_forced [steps][N]
+ * or NULL (teacher forcing), host_out [steps][N] greedy ids. */
+int mlt_runtime_decode(mlt_runtime* rt, const int32_t* host_tokens, const int32_t* host_forced,
+                       int steps, int32_t* host_out, mlt_decode_report_t* report);
+/* timeline_json of the last decode's measured timeline; returns length. */
+int mlt_runtime_timeline_json(mlt_runtime* rt, char* buf, size_t cap);
+int mlt_runtime_read_residual(mlt_runtime* rt, float* host_out);
+/* Test tap: copy a named device buffer of the last micro-batch ("h", "hn",
+ * "topk", "topw", "qkv_bf16", "attn_in", "y", "inv", "counts", "offsets",
+ * "logits") to host; returns the byte count (host_out may be NULL). */
+int mlt_runtime_debug_read(mlt_runtime* rt, const char* name, void* host_out, size_t cap);
+
 #ifdef __cplusplus
 }
 #endif

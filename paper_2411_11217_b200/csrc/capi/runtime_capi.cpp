@@ -1,0 +1,135 @@
+// C ABI over mlt::Runtime (include/mlt.h, "Decode runtime").
+#include <memory>
+#include <string>
+
+#include "../runtime/runtime.hpp"
+#include "lightplan/pipesim.hpp"
+#include "lightplan/planner.hpp"
+#include "status.hpp"
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+    MLT_GUARD_BODY(lightplan)
+}
+
+struct Handle {
+    std::unique_ptr<mlt::Runtime> rt;
+    lightplan::sim::ScheduleDag dag;
+    lightplan::sim::Timeline tl;
+    bool has_tl = false;
+};
+
+Handle* H(mlt_runtime* r) { return reinterpret_cast<Handle*>(r); }
+
+}  // namespace
+
+extern "C" {
+
+mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p,
+                                const mlt_runtime_options_t* o) {
+    Handle* h = nullptr;
+    guard([&] {
+        lightplan::ModelSpec ms;
+        ms.layers = m->layers; ms.hidden_dim = m->hidden_dim; ms.ffn_dim = m->ffn_dim;
+        ms.q_heads = m->q_heads; ms.kv_heads = m->kv_heads; ms.experts = m->experts;
+        ms.top_k = m->top_k; ms.weight_dtype_bytes = m->weight_dtype_bytes;
+        ms.kv_dtype_bytes = m->kv_dtype_bytes;
+        lightplan::Policy pol;
+        pol.batch = p->batch; pol.micro_batch = p->micro_batch;
+        pol.attn_on_gpu = p->attn_on_gpu != 0; pol.ffn_on_gpu = p->ffn_on_gpu != 0;
+        pol.weights_on_gpu = p->weights_on_gpu; pol.kv_on_gpu = p->kv_on_gpu;
+        mlt::ModelExt ext;
+        ext.vocab = o->vocab; ext.rms_eps = o->rms_eps; ext.rope_theta = o->rope_theta;
+        ext.lm_head_scale = o->lm_head_scale; ext.seed = o->seed;
+        mlt::RuntimeOptions opt;
+        opt.device = o->device; opt.budget_bytes = o->budget_bytes; opt.max_ctx = o->max_ctx;
+        opt.host_threads = o->host_threads; opt.pin_weights = o->pin_weights;
+        auto hh = std::make_unique<Handle>();
+        hh->rt = std::make_unique<mlt::Runtime>(ms, ext, pol, opt);
+        h = hh.release();
+        return MLT_OK;
+    });
+    return reinterpret_cast<mlt_runtime*>(h);
+}
+
+void mlt_runtime_destroy(mlt_runtime* r) { delete H(r); }
+
+int mlt_runtime_info(const mlt_runtime* r, mlt_runtime_info_t* out) {
+    return guard([&] {
+        const auto& rt = *reinterpret_cast<const Handle*>(r)->rt;
+        out->achieved_weight_ratio = rt.achieved_weight_ratio();
+        out->streamed_bytes_per_layer = static_cast<double>(rt.streamed_bytes_per_layer());
+        out->arena_used = static_cast<double>(rt.arena_used());
+        out->arena_capacity = 0;
+        out->pin_seconds = rt.pin_seconds();
+        out->gen_seconds = rt.gen_seconds();
+        return MLT_OK;
+    });
+}
+
+int mlt_runtime_prefill_synthetic(mlt_runtime* r, int prompt_len, uint64_t seed) {
+    return guard([&] {
+        H(r)->rt->prefill_synthetic(prompt_len, seed);
+        return MLT_OK;
+    });
+}
+
+int mlt_runtime_set_positions(mlt_runtime* r, const int32_t* pos) {
+    return guard([&] {
+        H(r)->rt->set_positions(pos);
+        return MLT_OK;
+    });
+}
+
+int mlt_runtime_decode(mlt_runtime* r, const int32_t* tokens, const int32_t* forced, int steps,
+                       int32_t* out, mlt_decode_report_t* rep) {
+    return guard([&] {
+        Handle* h = H(r);
+        const mlt::DecodeReport d = h->rt->decode(tokens, forced, steps, out, &h->dag, &h->tl);
+        h->has_tl = true;
+        if (rep) {
+            rep->seconds = d.seconds;
+            rep->tokens_per_second = d.tokens_per_second;
+            rep->measured = {d.measured.link_upload, d.measured.gpu_attention, d.measured.gpu_ffn,
+                             d.measured.cpu_attention, d.measured.cpu_ffn, d.measured.layer_total};
+            rep->h2d_weight_bytes = d.h2d_weight_bytes;
+            rep->h2d_bytes = d.h2d_bytes;
+            rep->d2h_bytes = d.d2h_bytes;
+            rep->steady_layer_time = d.steady_layer_time;
+            for (int i = 0; i < 5; ++i) rep->utilization[i] = d.utilization[i];
+            rep->gpu_launches = d.gpu_launches;
+            rep->timeline_ok = d.verify.empty() ? 1 : 0;
+        }
+        if (!d.verify.empty()) mlt::set_error(("timeline: " + d.verify).c_str(), MLT_OK);
+        return MLT_OK;
+    });
+}
+
+int mlt_runtime_timeline_json(mlt_runtime* r, char* buf, size_t cap) {
+    return guard([&] {
+        Handle* h = H(r);
+        if (!h->has_tl) throw std::invalid_argument("no decode has run yet");
+        const std::string s = lightplan::sim::timeline_json(h->dag, h->tl, "{\"source\":\"measured\"}");
+        if (buf && cap) {
+            const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+            std::memcpy(buf, s.data(), n);
+            buf[n] = 0;
+        }
+        return static_cast<int>(s.size());
+    });
+}
+
+int mlt_runtime_read_residual(mlt_runtime* r, float* out) {
+    return guard([&] {
+        H(r)->rt->read_residual(out);
+        return MLT_OK;
+    });
+}
+
+int mlt_runtime_debug_read(mlt_runtime* r, const char* name, void* out, size_t cap) {
+    return guard([&] { return static_cast<int>(H(r)->rt->debug_read(name, out, cap)); });
+}
+
+}  // extern "C"

@@ -1,0 +1,349 @@
+// CGOPipe executor: runs a lightplan ScheduleDag on real resources and
+// returns the measured Timeline (it replaces sim::simulate,
+// proj/src/pipesim.cpp:350-406, with the same FIFO-per-resource semantics,
+// proj/include/lightplan/pipesim.hpp:110-113).
+//
+// One launcher thread per resource walks that resource's tasks in issue
+// order (SURVEY.md §7 hard part 1: enqueue in dependency-ready order, the
+// event_oracle.cpp:22-53 loop with "enqueued" in place of "done"):
+//   gpu  -> kernels on the compute stream      h2d -> cudaMemcpyAsync, copy engine
+//   d2h  -> cudaMemcpyAsync, the other engine  cpu -> host attention (OpenMP)
+//   ctopin -> DRAM -> pinned staging memcpy (only when weights are not pinned)
+// A dependency on a device task is a cudaStreamWaitEvent on its end event
+// (after the producer thread has recorded it); a host task waiting on a
+// device task synchronises that event; anything waiting on a host task
+// waits for its completion flag.  Device tasks are bracketed by CUDA events
+// and host tasks by steady_clock, aligned on one reference event, so the
+// measured timeline can be fed to metrics()/verify_timeline().
+//
+// The reference DAG does not encode buffer reuse (its model assumes the
+// double buffer of planner.cpp:91-92 just works).  The executor adds the
+// write-after-read edges that make reuse safe by construction: pages of
+// global layer g+2 are uploaded into the pool slot of layer g only after
+// every GPU task of layer g; staging pages likewise wait for the upload that
+// read them.  simulate() on the augmented graph proves it acyclic first.
+#include <omp.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../capi/status.hpp"
+#include "runtime.hpp"
+
+namespace mlt {
+
+using lightplan::sim::Resource;
+using lightplan::sim::ScheduleDag;
+using lightplan::sim::Task;
+using lightplan::sim::TaskKind;
+using lightplan::sim::Timeline;
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool on_device(Resource r) {
+    return r == Resource::Gpu || r == Resource::HostToDevice || r == Resource::DeviceToHost;
+}
+
+// Extra write-after-read edges for buffer reuse (see file comment).
+std::vector<std::vector<int>> reuse_edges(const ScheduleDag& dag) {
+    const int n = static_cast<int>(dag.tasks.size());
+    const int L = dag.layers;
+    std::vector<std::vector<int>> extra(n);
+    std::vector<std::vector<int>> gpu_of_layer(L * dag.steps + 2), up_of(L * dag.steps + 2);
+    for (int i = 0; i < n; ++i) {
+        const Task& t = dag.tasks[i];
+        const int g = (t.step - 1) * L + t.layer;
+        if (t.resource == Resource::Gpu) gpu_of_layer[g].push_back(i);
+        if (t.kind == TaskKind::WeightToGpu) up_of[g].push_back(i);
+    }
+    for (int i = 0; i < n; ++i) {
+        const Task& t = dag.tasks[i];
+        const int g = (t.step - 1) * L + t.layer;
+        if (g <= 2) continue;
+        if (t.kind == TaskKind::WeightToGpu)
+            extra[i] = gpu_of_layer[g - 2];
+        else if (t.kind == TaskKind::WeightToPinned)
+            extra[i] = up_of[g - 2];
+    }
+    return extra;
+}
+
+struct Flags {
+    std::mutex m;
+    std::condition_variable cv;
+    std::vector<char> ready;  // device: end event recorded; host: finished
+    bool failed = false;
+    std::string error;
+
+    void set(int i) {
+        {
+            std::lock_guard<std::mutex> g(m);
+            ready[i] = 1;
+        }
+        cv.notify_all();
+    }
+    void fail(const std::string& e) {
+        {
+            std::lock_guard<std::mutex> g(m);
+            if (!failed) error = e;
+            failed = true;
+        }
+        cv.notify_all();
+    }
+    bool wait(int i) {
+        std::unique_lock<std::mutex> g(m);
+        cv.wait(g, [&] { return ready[i] || failed; });
+        return !failed;
+    }
+};
+
+}  // namespace
+
+DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, int steps, int32_t* out,
+                             ScheduleDag* dag_out, Timeline* tl_out) {
+    if (steps < 1 || steps > max_steps_) throw std::invalid_argument("steps must be in [1, 64]");
+    for (int i = 0; i < N_; ++i)
+        if (pos_[i] + steps > max_ctx_) throw std::invalid_argument("KV capacity exceeded (max_ctx)");
+    // ---- schedule: the reference DAG for this policy (durations modeled) ----
+    lightplan::HardwareSpec hw;  // nominal B200 spec for the modeled durations only
+    hw.gpu_mem_bytes = opt_.budget_bytes;
+    hw.cpu_mem_bytes = 1e15;
+    hw.gpu_bw = 6548.5e9;
+    hw.cpu_bw = 111e9;
+    hw.link_bw = 55.6e9;
+    hw.gpu_flops = 1393e12;
+    hw.cpu_flops = 2e12;
+    lightplan::WorkloadSpec wl;
+    wl.prompt_len = pos_[0];
+    wl.gen_len = steps;
+    const auto kind = policy_.attn_on_gpu ? lightplan::sim::ScheduleKind::S4 : lightplan::sim::ScheduleKind::CgoPipe;
+    lightplan::Policy pol = policy_;
+    ScheduleDag dag = lightplan::sim::build_schedule(
+        [&](int step) {
+            lightplan::sim::StepDurations d;
+            (void)step;
+            d.pre_attn = d.post_attn = d.cpu_attn = d.gpu_attn = 1e-4;
+            d.offload_qkv = d.load_hidden = d.kv_load = 1e-5;
+            d.weight_upload = static_cast<double>(layer_blob_bytes_) / hw.link_bw;
+            d.weight_stage = opt_.pin_weights ? 0.0 : static_cast<double>(layer_blob_bytes_) / 87e9;
+            return d;
+        },
+        kind, L_, steps, M_);
+    (void)pol;
+    const int n = static_cast<int>(dag.tasks.size());
+    const auto extra = reuse_edges(dag);
+    {
+        ScheduleDag check = dag;  // prove the augmented graph acyclic
+        for (int i = 0; i < n; ++i)
+            check.tasks[i].deps.insert(check.tasks[i].deps.end(), extra[i].begin(), extra[i].end());
+        lightplan::sim::simulate(check);
+    }
+
+    // ---- inputs (inside the measured region) ----
+    step_pos_.assign(static_cast<size_t>(steps) * N_, 0);
+    std::vector<int32_t> ctx(static_cast<size_t>(steps) * N_);
+    for (int s = 0; s < steps; ++s)
+        for (int i = 0; i < N_; ++i) {
+            step_pos_[static_cast<size_t>(s) * N_ + i] = pos_[i] + s;
+            ctx[static_cast<size_t>(s) * N_ + i] = pos_[i] + s + 1;
+        }
+    cudaEvent_t e0, e_end;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e_end), "event");
+    ck(cudaEventRecord(e0, s_gpu_), "event");
+    ck(cudaEventSynchronize(e0), "event sync");
+    const auto host_t0 = std::chrono::steady_clock::now();
+    std::memcpy(h_tok_, tokens_in, N_ * 4);
+    if (forced) std::memcpy(h_tok_, forced, static_cast<size_t>(steps) * N_ * 4);
+    std::memcpy(h_tok_ + static_cast<size_t>(max_steps_) * N_, step_pos_.data(), step_pos_.size() * 4);
+    std::memcpy(h_tok_ + static_cast<size_t>(max_steps_) * N_ * 2, ctx.data(), ctx.size() * 4);
+    ck(cudaMemcpyAsync(d_tok_in_, h_tok_, static_cast<size_t>(forced ? steps : 1) * N_ * 4, cudaMemcpyHostToDevice,
+                       s_gpu_),
+       "tokens h2d");
+    ck(cudaMemcpyAsync(d_pos_, h_tok_ + static_cast<size_t>(max_steps_) * N_, step_pos_.size() * 4,
+                       cudaMemcpyHostToDevice, s_gpu_),
+       "pos h2d");
+    ck(cudaMemcpyAsync(d_pos_ + static_cast<size_t>(max_steps_) * N_, h_tok_ + static_cast<size_t>(max_steps_) * N_ * 2,
+                       ctx.size() * 4, cudaMemcpyHostToDevice, s_gpu_),
+       "ctx h2d");
+    cudaEvent_t e_inputs;
+    ck(cudaEventCreateWithFlags(&e_inputs, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(e_inputs, s_gpu_), "event");
+    ck(cudaStreamWaitEvent(s_h2d_, e_inputs, 0), "wait");
+    ck(cudaStreamWaitEvent(s_d2h_, e_inputs, 0), "wait");
+
+    // ---- execute ----
+    std::vector<cudaEvent_t> ev_start(n, nullptr), ev_end(n, nullptr);
+    for (int i = 0; i < n; ++i)
+        if (on_device(dag.tasks[i].resource)) {
+            ck(cudaEventCreate(&ev_start[i]), "event");
+            ck(cudaEventCreate(&ev_end[i]), "event");
+        }
+    std::vector<double> h_start(n, 0), h_end(n, 0);
+    Flags flags;
+    flags.ready.assign(n, 0);
+    const Ctx cctx{steps, forced != nullptr};
+    cur_steps_ = steps;
+    launches_ = 0;
+
+    std::array<std::vector<int>, lightplan::sim::kResourceCount> fifo;
+    for (int i = 0; i < n; ++i) fifo[static_cast<int>(dag.tasks[i].resource)].push_back(i);
+
+    auto worker = [&](Resource r) {
+        try {
+            const cudaStream_t st = stream(r);
+            ck(cudaSetDevice(opt_.device), "set device");
+            for (int i : fifo[static_cast<int>(r)]) {
+                const Task& t = dag.tasks[i];
+                auto wait_dep = [&](int d) {
+                    if (!flags.wait(d)) throw std::runtime_error("aborted");
+                    const Resource rd = dag.tasks[d].resource;
+                    if (on_device(rd)) {
+                        if (on_device(r)) {
+                            if (rd != r) ck(cudaStreamWaitEvent(st, ev_end[d], 0), "stream wait");
+                        } else {
+                            ck(cudaEventSynchronize(ev_end[d]), "event sync");
+                        }
+                    }
+                };
+                for (int d : t.deps) wait_dep(d);
+                for (int d : extra[i]) wait_dep(d);
+                if (on_device(r)) {
+                    ck(cudaEventRecord(ev_start[i], st), "record");
+                    switch (t.kind) {
+                        case TaskKind::PreAttn: act_pre_attn(cctx, t.step, t.layer, t.microbatch); break;
+                        case TaskKind::PostAttn: act_post_attn(cctx, t.step, t.layer, t.microbatch); break;
+                        case TaskKind::GpuAttn: act_gpu_attn(t.step, t.layer, t.microbatch); break;
+                        case TaskKind::OffloadQkv: act_offload_qkv(t.layer, t.microbatch); break;
+                        case TaskKind::LoadHidden: act_load_hidden(t.layer, t.microbatch); break;
+                        case TaskKind::WeightToGpu: act_weight_to_gpu((t.step - 1) * L_ + t.layer, t.page); break;
+                        case TaskKind::KvLoad: break;  // r_c = 1: KV resident, nothing to move
+                        default: throw std::logic_error("host task on a device resource");
+                    }
+                    ck(cudaEventRecord(ev_end[i], st), "record");
+                } else {
+                    h_start[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count();
+                    if (t.kind == TaskKind::CpuAttn) act_cpu_attn(t.step, t.layer, t.microbatch);
+                    else if (t.kind == TaskKind::WeightToPinned)
+                        act_weight_to_pinned((t.step - 1) * L_ + t.layer, t.page);
+                    h_end[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count();
+                }
+                flags.set(i);
+            }
+        } catch (const std::exception& e) {
+            flags.fail(e.what());
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int r = 0; r < lightplan::sim::kResourceCount; ++r)
+            if (!fifo[r].empty()) th.emplace_back(worker, static_cast<Resource>(r));
+        for (auto& t : th) t.join();
+    }
+    if (flags.failed) {
+        cudaDeviceSynchronize();
+        for (int i = 0; i < n; ++i) {
+            if (ev_start[i]) cudaEventDestroy(ev_start[i]);
+            if (ev_end[i]) cudaEventDestroy(ev_end[i]);
+        }
+        throw std::runtime_error("executor: " + flags.error);
+    }
+    // join all streams into the compute stream, fetch the greedy ids
+    for (cudaStream_t s : {s_h2d_, s_d2h_}) {
+        cudaEvent_t j;
+        ck(cudaEventCreateWithFlags(&j, cudaEventDisableTiming), "event");
+        ck(cudaEventRecord(j, s), "record");
+        ck(cudaStreamWaitEvent(s_gpu_, j, 0), "wait");
+        cudaEventDestroy(j);
+    }
+    ck(cudaMemcpyAsync(h_tok_ + static_cast<size_t>(max_steps_) * N_ * 3, d_tok_out_, static_cast<size_t>(steps) * N_ * 4,
+                       cudaMemcpyDeviceToHost, s_gpu_),
+       "ids d2h");
+    ck(cudaEventRecord(e_end, s_gpu_), "record");
+    ck(cudaEventSynchronize(e_end), "sync");
+    std::memcpy(out, h_tok_ + static_cast<size_t>(max_steps_) * N_ * 3, static_cast<size_t>(steps) * N_ * 4);
+    for (int i = 0; i < N_; ++i) pos_[i] += steps;
+
+    // ---- measured timeline ----
+    Timeline tl;
+    tl.entries.resize(n);
+    ScheduleDag measured = dag;
+    for (int i = 0; i < n; ++i) {
+        double s, e;
+        if (ev_start[i]) {
+            float a = 0, b = 0;
+            ck(cudaEventElapsedTime(&a, e0, ev_start[i]), "elapsed");
+            ck(cudaEventElapsedTime(&b, e0, ev_end[i]), "elapsed");
+            s = a * 1e-3;
+            e = b * 1e-3;
+        } else {
+            s = h_start[i];
+            e = h_end[i];
+        }
+        tl.entries[i] = {i, s, e};
+        measured.tasks[i].duration = e - s;
+        tl.busy[static_cast<int>(measured.tasks[i].resource)] += e - s;
+        tl.makespan = std::max(tl.makespan, e);
+        if (ev_start[i]) {
+            cudaEventDestroy(ev_start[i]);
+            cudaEventDestroy(ev_end[i]);
+        }
+    }
+    float total_ms = 0;
+    ck(cudaEventElapsedTime(&total_ms, e0, e_end), "elapsed");
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e_end);
+    cudaEventDestroy(e_inputs);
+
+    DecodeReport rep;
+    rep.seconds = total_ms * 1e-3;
+    rep.tokens_per_second = static_cast<double>(N_) * steps / rep.seconds;
+    rep.gpu_launches = launches_;
+    const double layers = static_cast<double>(L_) * steps;
+    for (int i = 0; i < n; ++i) {
+        const Task& t = measured.tasks[i];
+        switch (t.kind) {
+            case TaskKind::PreAttn:
+            case TaskKind::GpuAttn: rep.measured.gpu_attention += t.duration / layers; break;
+            case TaskKind::PostAttn: rep.measured.gpu_ffn += t.duration / layers; break;
+            case TaskKind::CpuAttn: rep.measured.cpu_attention += t.duration / layers; break;
+            case TaskKind::WeightToGpu: {
+                rep.measured.link_upload += t.duration / layers;
+                const auto [b, e] = page_range(t.page);
+                rep.h2d_weight_bytes += static_cast<double>(e - b);
+                rep.h2d_bytes += static_cast<double>(e - b);
+                break;
+            }
+            case TaskKind::LoadHidden:
+                rep.measured.link_upload += t.duration / layers;
+                rep.h2d_bytes += static_cast<double>(Rmu_) * H_ * 2;
+                break;
+            case TaskKind::OffloadQkv: rep.d2h_bytes += static_cast<double>(mu_) * W_ * 2; break;
+            default: break;
+        }
+    }
+    // Host/device clock alignment error is bounded by the e0 synchronisation
+    // latency; verify with 50 us slack.
+    rep.verify = lightplan::sim::verify_timeline_tol(measured, tl, 5e-5);
+    const auto m = lightplan::sim::metrics(measured, tl);
+    rep.steady_layer_time = m.steady_layer_time;
+    rep.measured.layer_total = m.steady_layer_time;
+    for (int r = 0; r < 5; ++r) rep.utilization[r] = m.utilization[r];
+    if (dag_out) *dag_out = std::move(measured);
+    if (tl_out) *tl_out = std::move(tl);
+    return rep;
+}
+
+}  // namespace mlt

@@ -1,0 +1,609 @@
+// Runtime construction (arena, weight catalog + residency, paged weight
+// store, activation buffers) and the per-task actions the CGOPipe executor
+// runs.  See runtime.hpp and DESIGN.md §3-§5.
+#include "runtime.hpp"
+
+#include <sys/mman.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "../capi/status.hpp"
+#include "../kernels/common.cuh"
+#include "../kernels/kernels.hpp"
+#include "host_layout.hpp"
+
+namespace mlt {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// Large host buffers: 2 MiB-aligned, transparent huge pages, first-touched
+// in parallel, then page-locked with cudaHostRegister (measured on the GPU
+// box: ~0.1 s/GB vs ~0.4 s/GB for cudaHostAlloc; tools/pin_probe.cu).
+uint8_t* host_alloc(size_t bytes, bool pin, double* pin_seconds) {
+    const size_t align = 2u << 20;
+    bytes = (bytes + align - 1) / align * align;
+    void* p = std::aligned_alloc(align, bytes);
+    if (!p) throw std::bad_alloc();
+    madvise(p, bytes, MADV_HUGEPAGE);
+    uint8_t* b = static_cast<uint8_t*>(p);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < static_cast<int64_t>(bytes); i += 4096) b[i] = 0;
+    if (pin) {
+        const double t = now_s();
+        ck(cudaHostRegister(p, bytes, cudaHostRegisterDefault), "cudaHostRegister");
+        if (pin_seconds) *pin_seconds += now_s() - t;
+    }
+    return b;
+}
+
+void host_free(void* p, bool pinned) {
+    if (!p) return;
+    if (pinned) cudaHostUnregister(p);
+    std::free(p);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+Arena::Arena(size_t bytes) : cap_(bytes) {
+    ck(cudaMalloc(&base_, bytes), "arena cudaMalloc (budget)");
+}
+Arena::~Arena() {
+    if (base_) cudaFree(base_);
+}
+void* Arena::alloc(size_t bytes, const char* what) {
+    const size_t off = (used_ + 1023) & ~static_cast<size_t>(1023);
+    if (off + bytes > cap_)
+        throw BudgetError(std::string("device budget exceeded allocating ") + what + " (" +
+                          std::to_string(bytes) + " B; used " + std::to_string(off) + " of " +
+                          std::to_string(cap_) + ")");
+    used_ = off + bytes;
+    log_ += std::string(what) + "=" + std::to_string(bytes) + ";";
+    return base_ + off;
+}
+
+// ---------------------------------------------------------------------------
+Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
+                 const lightplan::Policy& policy, const RuntimeOptions& opt)
+    : model_(model), ext_(ext), policy_(policy), opt_(opt) {
+    auto issues = lightplan::validate(model);
+    auto pi = lightplan::validate(policy);
+    issues.insert(issues.end(), pi.begin(), pi.end());
+    if (!issues.empty()) throw std::invalid_argument(lightplan::format_issues(issues));
+    N_ = static_cast<int>(policy.batch);
+    mu_ = static_cast<int>(policy.micro_batch);
+    M_ = static_cast<int>(policy.micro_batch_count());
+    H_ = static_cast<int>(model.hidden_dim);
+    F_ = static_cast<int>(model.ffn_dim);
+    E_ = static_cast<int>(model.experts);
+    K_ = static_cast<int>(model.top_k);
+    nq_ = static_cast<int>(model.q_heads);
+    nkv_ = static_cast<int>(model.kv_heads);
+    d_ = static_cast<int>(model.head_dim());
+    W_ = (nq_ + 2 * nkv_) * d_;
+    V_ = ext.vocab;
+    L_ = static_cast<int>(model.layers);
+    if (model.weight_dtype_bytes != 2 || model.kv_dtype_bytes != 2)
+        throw std::invalid_argument("runtime supports bf16 weights and KV (dt_w = dt_kv = 2)");
+    if (H_ % 256 || F_ % 128 || W_ % 128 || V_ % 128 || d_ != 128 || E_ > 64 || K_ > 8)
+        throw std::invalid_argument("shape: need h1 % 256, h2 % 128, vocab % 128, head_dim 128, n_e <= 64, k <= 8");
+    if (!policy.ffn_on_gpu) throw lightplan::sim::UnsupportedCombinationError("F_g = 0 is not a B200 path");
+    if (policy.attn_on_gpu && policy.kv_on_gpu < 1.0)
+        throw lightplan::sim::UnsupportedCombinationError("A_g = 1 requires r_c = 1 (resident paged KV) in this build");
+    if (opt.max_ctx <= 0) throw std::invalid_argument("max_ctx must be > 0");
+    max_ctx_ = opt.max_ctx;
+    Rmu_ = round_up(mu_, 16);
+    Re_ = round_up(mu_ * K_ + 16 * E_, 16);
+    ncap_ = std::min(256, Rmu_);
+    ncap_e_ = std::min(256, Rmu_);
+    pos_.assign(N_, 0);
+
+    ck(cudaSetDevice(opt.device), "cudaSetDevice");
+    ck(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, opt.device), "sm count");
+    ck(cudaStreamCreateWithFlags(&s_gpu_, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
+    arena_ = std::make_unique<Arena>(static_cast<size_t>(opt.budget_bytes));
+    build_catalog();
+    allocate();
+    generate_weights();
+}
+
+Runtime::~Runtime() {
+    cudaDeviceSynchronize();
+    host_free(host_blob_, host_blob_pinned_);
+    host_free(staging_, true);
+    if (h_qkv_) cudaFreeHost(h_qkv_);
+    if (h_attn_) cudaFreeHost(h_attn_);
+    if (h_tok_) cudaFreeHost(h_tok_);
+    std::free(h_kcache_);
+    std::free(h_vcache_);
+    arena_.reset();
+    if (s_gpu_) cudaStreamDestroy(s_gpu_);
+    if (s_h2d_) cudaStreamDestroy(s_h2d_);
+    if (s_d2h_) cudaStreamDestroy(s_d2h_);
+}
+
+cudaStream_t Runtime::stream(lightplan::sim::Resource r) const {
+    switch (r) {
+        case lightplan::sim::Resource::Gpu: return s_gpu_;
+        case lightplan::sim::Resource::HostToDevice: return s_h2d_;
+        case lightplan::sim::Resource::DeviceToHost: return s_d2h_;
+        default: return nullptr;
+    }
+}
+
+// Per-layer block catalog and residency split.  Resident first: attention
+// projections, then expert row blocks in (expert, W1, W3, W2) order, as long
+// as the layer's resident bytes (router included) stay <= r_w * W_layer —
+// the reference's uniform share (opcost.cpp:71) realised at 128-row-block
+// granularity (SURVEY.md Appendix B "r_w realization").
+void Runtime::build_catalog() {
+    blocks_.clear();
+    auto add = [&](int kind, int expert, int rows, int64_t K) {
+        for (int rb = 0; rb < rows / 128; ++rb)
+            blocks_.push_back({kind, expert, rb, K, 128 * K * 2, false, 0});
+    };
+    add(kWqkv, 0, W_, H_);
+    add(kWo, 0, H_, H_);
+    for (int e = 0; e < E_; ++e) {
+        add(kW1, e, F_, H_);
+        add(kW3, e, F_, H_);
+        add(kW2, e, H_, F_);
+    }
+    const double layer_total = lightplan::layer_weight_bytes(model_).total();
+    const double router = static_cast<double>(E_) * H_ * 2;
+    double budget = policy_.weights_on_gpu * layer_total - router;
+    int64_t res = 0, blob = 0;
+    bool open = true;
+    for (auto& b : blocks_) {
+        if (open && static_cast<double>(res + b.bytes) <= budget) {
+            b.resident = true;
+            b.offset = res;
+            res += b.bytes;
+        } else {
+            open = false;
+            b.resident = false;
+            b.offset = blob;
+            blob += b.bytes;
+        }
+    }
+    layer_res_bytes_ = res;
+    layer_blob_bytes_ = blob;
+    achieved_rw_ = (static_cast<double>(res) + router) / layer_total;
+}
+
+std::pair<int64_t, int64_t> Runtime::page_range(int page) const {
+    if (page <= 0) return {0, layer_blob_bytes_};
+    // n_ub pages per layer (pipesim.cpp:150-162), 4 KiB-aligned boundaries.
+    auto edge = [&](int p) {
+        const int64_t raw = layer_blob_bytes_ * p / M_;
+        return p == M_ ? layer_blob_bytes_ : (raw & ~static_cast<int64_t>(4095));
+    };
+    return {edge(page - 1), edge(page)};
+}
+
+void Runtime::allocate() {
+    Arena& A = *arena_;
+    const int64_t T = static_cast<int64_t>(N_);
+    // weights
+    if (layer_res_bytes_) dev_res_ = static_cast<uint8_t*>(A.alloc(L_ * layer_res_bytes_, "resident_weights"));
+    if (layer_blob_bytes_) dev_pool_ = static_cast<uint8_t*>(A.alloc(2 * layer_blob_bytes_, "page_pool"));
+    d_embed_ = static_cast<uint16_t*>(A.alloc(static_cast<size_t>(V_) * H_ * 2, "embed"));
+    d_lm_ = static_cast<uint16_t*>(A.alloc(static_cast<size_t>(V_) * H_ * 2, "lm_head"));
+    d_final_norm_ = static_cast<uint16_t*>(A.alloc(H_ * 2, "final_norm"));
+    for (int l = 0; l < L_; ++l) {
+        d_attn_norm_.push_back(static_cast<uint16_t*>(A.alloc(H_ * 2, "attn_norm")));
+        d_ffn_norm_.push_back(static_cast<uint16_t*>(A.alloc(H_ * 2, "ffn_norm")));
+        d_router_.push_back(static_cast<uint16_t*>(A.alloc(static_cast<size_t>(E_) * H_ * 2, "router")));
+    }
+    tab_qkv_ = 0;
+    tab_o_ = tab_qkv_ + W_ / 128;
+    tab_w13_ = tab_o_ + H_ / 128;
+    tab_w2_ = tab_w13_ + 2 * E_ * (F_ / 128);
+    table_entries_ = tab_w2_ + E_ * (H_ / 128);
+    dev_tables_ = static_cast<const uint8_t**>(A.alloc(sizeof(void*) * L_ * 2 * table_entries_, "page_tables"));
+    d_lm_table_ = static_cast<const uint8_t**>(A.alloc(sizeof(void*) * (V_ / 128), "lm_table"));
+    d_rope_ = static_cast<float2*>(A.alloc(sizeof(float2) * max_ctx_ * (d_ / 2), "rope"));
+    // activations
+    d_x_ = static_cast<float*>(A.alloc(T * H_ * 4, "x"));
+    d_qkv_bf16_ = static_cast<uint16_t*>(A.alloc(static_cast<size_t>(M_) * mu_ * W_ * 2, "qkv_bf16"));
+    d_attn_in_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(M_) * Rmu_ * H_ * 2, "attn_in"));
+    d_xn_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Rmu_) * H_ * 2, "xn"));
+    d_qkv_f32_ = static_cast<float*>(A.alloc(static_cast<size_t>(Rmu_) * W_ * 4, "qkv_f32"));
+    d_h_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * H_ * 4, "h"));
+    d_hn_ = static_cast<uint16_t*>(A.alloc(static_cast<size_t>(mu_) * H_ * 2, "hn"));
+    d_topk_ = static_cast<int32_t*>(A.alloc(mu_ * K_ * 4, "topk"));
+    d_topw_ = static_cast<float*>(A.alloc(mu_ * K_ * 4, "topw"));
+    d_cnt_ = static_cast<int32_t*>(A.alloc(E_ * 4, "counts"));
+    d_off_ = static_cast<int32_t*>(A.alloc((E_ + 1) * 4, "offsets"));
+    d_perm_ = static_cast<int32_t*>(A.alloc(Re_ * 4, "perm"));
+    d_inv_ = static_cast<int32_t*>(A.alloc(mu_ * K_ * 4, "inv"));
+    d_xe_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Re_) * H_ * 2, "expert_in"));
+    d_inter_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Re_) * F_ * 2, "expert_inter"));
+    d_y_ = static_cast<float*>(A.alloc(static_cast<size_t>(Re_) * H_ * 4, "expert_out"));
+    d_logits_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * V_ * 4, "logits"));
+    d_tok_in_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4, "tok_in"));
+    d_tok_out_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4, "tok_out"));
+    d_pos_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4 * 2, "pos_ctx"));
+    d_seq_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(N_) * 4, "seq"));
+    if (policy_.attn_on_gpu) {
+        max_pages_ = (max_ctx_ + page_ - 1) / page_;
+        const size_t pages = static_cast<size_t>(L_) * N_ * max_pages_;
+        const size_t bytes = pages * nkv_ * page_ * d_ * 2;
+        d_kpool_ = static_cast<uint16_t*>(A.alloc(bytes, "kv_pool_k"));
+        d_vpool_ = static_cast<uint16_t*>(A.alloc(bytes, "kv_pool_v"));
+        d_block_table_ = static_cast<int32_t*>(A.alloc(pages * 4, "block_table"));
+        d_attn_gpu_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Rmu_) * H_ * 2, "attn_gpu"));
+        std::vector<int32_t> bt(pages);
+        for (size_t i = 0; i < pages; ++i) bt[i] = static_cast<int32_t>(i);  // per (layer, seq) page runs
+        ck(cudaMemcpy(d_block_table_, bt.data(), pages * 4, cudaMemcpyHostToDevice), "block table");
+    }
+    std::vector<int32_t> seq(N_);
+    for (int i = 0; i < N_; ++i) seq[i] = i;
+    ck(cudaMemcpy(d_seq_, seq.data(), N_ * 4, cudaMemcpyHostToDevice), "seq");
+    std::vector<float> rope(static_cast<size_t>(max_ctx_) * d_);
+    for (int p = 0; p < max_ctx_; ++p)
+        for (int i = 0; i < d_ / 2; ++i) {
+            const double inv = std::pow(static_cast<double>(ext_.rope_theta), -2.0 * i / static_cast<double>(d_));
+            const double ang = static_cast<double>(p) * inv;
+            rope[(static_cast<size_t>(p) * (d_ / 2) + i) * 2] = static_cast<float>(std::cos(ang));
+            rope[(static_cast<size_t>(p) * (d_ / 2) + i) * 2 + 1] = static_cast<float>(std::sin(ang));
+        }
+    ck(cudaMemcpy(d_rope_, rope.data(), rope.size() * 4, cudaMemcpyHostToDevice), "rope");
+
+    // host side
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_qkv_), static_cast<size_t>(M_) * mu_ * W_ * 2, 0), "h_qkv");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_attn_), static_cast<size_t>(M_) * Rmu_ * H_ * 2, 0), "h_attn");
+    std::memset(h_attn_, 0, static_cast<size_t>(M_) * Rmu_ * H_ * 2);
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_tok_), static_cast<size_t>(max_steps_) * N_ * 4 * 4, 0), "h_tok");
+    if (!policy_.attn_on_gpu) {
+        const size_t kv = static_cast<size_t>(L_) * N_ * nkv_ * max_ctx_ * d_;
+        h_kcache_ = reinterpret_cast<uint16_t*>(host_alloc(kv * 2, false, nullptr));
+        h_vcache_ = reinterpret_cast<uint16_t*>(host_alloc(kv * 2, false, nullptr));
+    }
+}
+
+void Runtime::generate_weights() {
+    const double t0 = now_s();
+    const uint64_t seed = ext_.seed;
+    const double sH = 1.0 / std::sqrt(static_cast<double>(H_));
+    const double sF = 1.0 / std::sqrt(static_cast<double>(F_));
+    host_blob_pinned_ = opt_.pin_weights != 0;
+    if (layer_blob_bytes_) {
+        host_blob_ = host_alloc(static_cast<size_t>(L_) * layer_blob_bytes_, host_blob_pinned_, &pin_seconds_);
+        if (!opt_.pin_weights) staging_ = host_alloc(2 * static_cast<size_t>(layer_blob_bytes_), true, &pin_seconds_);
+    }
+    std::vector<uint8_t> res(static_cast<size_t>(layer_res_bytes_));
+    std::vector<const uint8_t*> tab(static_cast<size_t>(L_) * 2 * table_entries_);
+    for (int l = 0; l < L_; ++l) {
+        int idx_qkv = 0, idx_o = 0;
+        for (const auto& b : blocks_) {
+            const bool down = b.kind == kW2;
+            const int rows = b.kind == kWqkv ? W_ : (b.kind == kWo || down) ? H_ : F_;
+            const float scale = static_cast<float>(down ? sF : sH);
+            uint8_t* dst = b.resident ? res.data() + b.offset
+                                      : host_blob_ + static_cast<int64_t>(l) * layer_blob_bytes_ + b.offset;
+            synth_bf16_packed(seed, tensor_id(l, b.kind, b.expert), rows, b.K, b.rb * 128,
+                              (b.rb + 1) * 128, scale, reinterpret_cast<uint16_t*>(dst));
+            int entry;
+            switch (b.kind) {
+                case kWqkv: entry = tab_qkv_ + idx_qkv++; break;
+                case kWo: entry = tab_o_ + idx_o++; break;
+                case kW1: entry = tab_w13_ + b.expert * (F_ / 128) + b.rb; break;
+                case kW3: entry = tab_w13_ + E_ * (F_ / 128) + b.expert * (F_ / 128) + b.rb; break;
+                default: entry = tab_w2_ + b.expert * (H_ / 128) + b.rb; break;
+            }
+            for (int slot = 0; slot < 2; ++slot) {
+                const uint8_t* p = b.resident ? dev_res_ + static_cast<int64_t>(l) * layer_res_bytes_ + b.offset
+                                              : dev_pool_ + static_cast<int64_t>(slot) * layer_blob_bytes_ + b.offset;
+                tab[(static_cast<size_t>(l) * 2 + slot) * table_entries_ + entry] = p;
+            }
+        }
+        if (layer_res_bytes_)
+            ck(cudaMemcpy(dev_res_ + static_cast<int64_t>(l) * layer_res_bytes_, res.data(), layer_res_bytes_,
+                          cudaMemcpyHostToDevice),
+               "resident upload");
+        std::vector<uint16_t> v(static_cast<size_t>(E_) * H_);
+        synth_bf16(seed, tensor_id(l, kRouter, 0), 0, static_cast<int64_t>(E_) * H_, static_cast<float>(sH), false, v.data());
+        ck(cudaMemcpy(d_router_[l], v.data(), v.size() * 2, cudaMemcpyHostToDevice), "router");
+        synth_bf16(seed, tensor_id(l, kAttnNorm, 0), 0, H_, 0.f, true, v.data());
+        ck(cudaMemcpy(d_attn_norm_[l], v.data(), H_ * 2, cudaMemcpyHostToDevice), "attn_norm");
+        synth_bf16(seed, tensor_id(l, kFfnNorm, 0), 0, H_, 0.f, true, v.data());
+        ck(cudaMemcpy(d_ffn_norm_[l], v.data(), H_ * 2, cudaMemcpyHostToDevice), "ffn_norm");
+    }
+    ck(cudaMemcpy(dev_tables_, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice), "tables");
+    {
+        std::vector<uint16_t> big(static_cast<size_t>(V_) * H_);
+        synth_bf16(seed, tensor_id(-1, kEmbed, 0), 0, static_cast<int64_t>(V_) * H_, 1.0f, false, big.data());
+        ck(cudaMemcpy(d_embed_, big.data(), big.size() * 2, cudaMemcpyHostToDevice), "embed");
+        const float s_lm = static_cast<float>(static_cast<double>(ext_.lm_head_scale) * sH);
+        synth_bf16_packed(seed, tensor_id(-1, kLmHead, 0), V_, H_, 0, V_, s_lm, big.data());
+        ck(cudaMemcpy(d_lm_, big.data(), big.size() * 2, cudaMemcpyHostToDevice), "lm_head");
+        std::vector<const uint8_t*> lt(V_ / 128);
+        for (int rb = 0; rb < V_ / 128; ++rb)
+            lt[rb] = reinterpret_cast<const uint8_t*>(d_lm_) + static_cast<int64_t>(rb) * 128 * H_ * 2;
+        ck(cudaMemcpy(d_lm_table_, lt.data(), lt.size() * sizeof(void*), cudaMemcpyHostToDevice), "lm table");
+        std::vector<uint16_t> g(H_);
+        synth_bf16(seed, tensor_id(-1, kFinalNorm, 0), 0, H_, 0.f, true, g.data());
+        ck(cudaMemcpy(d_final_norm_, g.data(), H_ * 2, cudaMemcpyHostToDevice), "final_norm");
+    }
+    gen_seconds_ = now_s() - t0;
+}
+
+void Runtime::prefill_synthetic(int prompt_len, uint64_t seed) {
+    if (prompt_len < 0 || prompt_len >= max_ctx_) throw std::invalid_argument("prompt_len out of range");
+    const int nkd = nkv_ * d_;
+    std::vector<uint16_t> tmp;
+    for (int l = 0; l < L_; ++l)
+        for (int which = 0; which < 2; ++which) {
+            const uint64_t key = mix64(seed ^ mix64(tensor_id(l, kKCache + which, 0)));
+            if (!policy_.attn_on_gpu) {
+                uint16_t* dst = which ? h_vcache_ : h_kcache_;
+#pragma omp parallel for collapse(2) schedule(static)
+                for (int s = 0; s < N_; ++s)
+                    for (int h = 0; h < nkv_; ++h)
+                        for (int p = 0; p < prompt_len; ++p)
+                            for (int i = 0; i < d_; ++i) {
+                                const uint64_t idx = ((static_cast<uint64_t>(s) << 20) | static_cast<uint64_t>(p)) * nkd + h * d_ + i;
+                                const uint64_t hv = mix64(key + idx);
+                                const float r = 2.0f * (static_cast<float>(hv >> 40) * 0x1p-24f) - 1.0f;
+                                dst[(((static_cast<size_t>(l) * N_ + s) * nkv_ + h) * max_ctx_ + p) * d_ + i] = f32_to_bf16(r);
+                            }
+            } else {
+                // paged device cache: page id = (l*N + s)*max_pages + p/page, [nkv][page][d]
+                const size_t per_seq = static_cast<size_t>(max_pages_) * nkv_ * page_ * d_;
+                tmp.assign(per_seq * N_, 0);
+#pragma omp parallel for collapse(2) schedule(static)
+                for (int s = 0; s < N_; ++s)
+                    for (int h = 0; h < nkv_; ++h)
+                        for (int p = 0; p < prompt_len; ++p)
+                            for (int i = 0; i < d_; ++i) {
+                                const uint64_t idx = ((static_cast<uint64_t>(s) << 20) | static_cast<uint64_t>(p)) * nkd + h * d_ + i;
+                                const uint64_t hv = mix64(key + idx);
+                                const float r = 2.0f * (static_cast<float>(hv >> 40) * 0x1p-24f) - 1.0f;
+                                const size_t page = p / page_;
+                                tmp[static_cast<size_t>(s) * per_seq + ((page * nkv_ + h) * page_ + p % page_) * d_ + i] = f32_to_bf16(r);
+                            }
+                uint16_t* pool = which ? d_vpool_ : d_kpool_;
+                ck(cudaMemcpy(pool + static_cast<size_t>(l) * N_ * per_seq, tmp.data(), tmp.size() * 2,
+                              cudaMemcpyHostToDevice),
+                   "kv prefill");
+            }
+        }
+    std::fill(pos_.begin(), pos_.end(), prompt_len);
+}
+
+void Runtime::set_positions(const int32_t* pos) {
+    for (int i = 0; i < N_; ++i) {
+        if (pos[i] < 0 || pos[i] >= max_ctx_) throw std::invalid_argument("position out of range");
+        pos_[i] = pos[i];
+    }
+}
+
+void Runtime::read_residual(float* out) {
+    ck(cudaStreamSynchronize(s_gpu_), "sync");
+    ck(cudaMemcpy(out, d_x_, static_cast<size_t>(N_) * H_ * 4, cudaMemcpyDeviceToHost), "read x");
+}
+
+void Runtime::read_last_topk(int32_t* out) {
+    ck(cudaStreamSynchronize(s_gpu_), "sync");
+    ck(cudaMemcpy(out, d_topk_, static_cast<size_t>(mu_) * K_ * 4, cudaMemcpyDeviceToHost), "read topk");
+}
+
+size_t Runtime::debug_read(const std::string& name, void* out, size_t cap) {
+    const void* src = nullptr;
+    size_t bytes = 0;
+    if (name == "h") { src = d_h_; bytes = static_cast<size_t>(mu_) * H_ * 4; }
+    else if (name == "hn") { src = d_hn_; bytes = static_cast<size_t>(mu_) * H_ * 2; }
+    else if (name == "topk") { src = d_topk_; bytes = static_cast<size_t>(mu_) * K_ * 4; }
+    else if (name == "topw") { src = d_topw_; bytes = static_cast<size_t>(mu_) * K_ * 4; }
+    else if (name == "qkv_bf16") { src = d_qkv_bf16_ + static_cast<size_t>(M_ - 1) * mu_ * W_; bytes = static_cast<size_t>(mu_) * W_ * 2; }
+    else if (name == "attn_in") { src = d_attn_in_ + static_cast<size_t>(M_ - 1) * Rmu_ * H_ * 2; bytes = static_cast<size_t>(Rmu_) * H_ * 2; }
+    else if (name == "y") { src = d_y_; bytes = static_cast<size_t>(Re_) * H_ * 4; }
+    else if (name == "inv") { src = d_inv_; bytes = static_cast<size_t>(mu_) * K_ * 4; }
+    else if (name == "counts") { src = d_cnt_; bytes = static_cast<size_t>(E_) * 4; }
+    else if (name == "offsets") { src = d_off_; bytes = static_cast<size_t>(E_ + 1) * 4; }
+    else if (name == "logits") { src = d_logits_; bytes = static_cast<size_t>(mu_) * V_ * 4; }
+    else if (name == "xe") { src = d_xe_; bytes = static_cast<size_t>(Re_) * H_ * 2; }
+    else if (name == "inter") { src = d_inter_; bytes = static_cast<size_t>(Re_) * F_ * 2; }
+    else throw std::invalid_argument("unknown debug buffer " + name);
+    if (out) {
+        if (cap < bytes) throw std::invalid_argument("debug_read: buffer too small");
+        ck(cudaStreamSynchronize(s_gpu_), "sync");
+        ck(cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost), "debug read");
+    }
+    return bytes;
+}
+
+// ---------------------------------------------------------------------------
+// Task actions.  step/layer/mb are the 1-based fields of sim::Task.
+// ---------------------------------------------------------------------------
+namespace {
+void kk(cudaError_t e, const char* what) { ck(e, what); }
+}  // namespace
+
+void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
+    const int t0 = (mb - 1) * mu_;
+    const int g = (step - 1) * L_ + layer;
+    const int l = layer - 1;
+    if (layer == 1) {
+        const int32_t* src = (step == 1 || c.forced) ? d_tok_in_ + static_cast<size_t>(step - 1) * N_ + t0
+                                                     : d_tok_out_ + static_cast<size_t>(step - 2) * N_ + t0;
+        kk(mltk::launch_embed(src, d_embed_, mu_, H_, d_x_ + static_cast<size_t>(t0) * H_, s_gpu_), "embed");
+        ++launches_;
+    }
+    kk(mltk::launch_rmsnorm_pack(d_x_ + static_cast<size_t>(t0) * H_, d_attn_norm_[l], mu_, H_, ext_.rms_eps, d_xn_,
+                                 Rmu_, s_gpu_),
+       "rmsnorm");
+    mltk::GemmArgs a;
+    a.a_table = dev_tables_ + (static_cast<size_t>(l) * 2 + slot_of(g)) * table_entries_ + tab_qkv_;
+    a.n_mats = 1;
+    a.G = 1;
+    a.RB = W_ / 128;
+    a.K = H_;
+    a.b = d_xn_;
+    a.R = Rmu_;
+    a.rows_dense = mu_;
+    a.n_cap = ncap_;
+    a.epi = mltk::kEpiF32;
+    a.out_f32 = d_qkv_f32_;
+    a.ldo = W_;
+    kk(mltk::launch_gemm(a, num_sms_, s_gpu_), "qkv gemm");
+    const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
+    uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
+    kk(mltk::launch_rope_qkv(d_qkv_f32_, pos, d_rope_, mu_, nq_, nkv_, d_, qkv, s_gpu_), "rope");
+    launches_ += 3;
+}
+
+void Runtime::act_offload_qkv(int layer, int mb) {
+    (void)layer;
+    const size_t off = static_cast<size_t>(mb - 1) * mu_ * W_;
+    kk(cudaMemcpyAsync(h_qkv_ + off, d_qkv_bf16_ + off, static_cast<size_t>(mu_) * W_ * 2, cudaMemcpyDeviceToHost,
+                       s_d2h_),
+       "offload qkv");
+}
+
+void Runtime::act_cpu_attn(int step, int layer, int mb) { host_attention(layer - 1, mb - 1, step); }
+
+void Runtime::act_load_hidden(int layer, int mb) {
+    (void)layer;
+    const size_t off = static_cast<size_t>(mb - 1) * Rmu_ * H_ * 2;
+    kk(cudaMemcpyAsync(d_attn_in_ + off, h_attn_ + off, static_cast<size_t>(Rmu_) * H_ * 2, cudaMemcpyHostToDevice,
+                       s_h2d_),
+       "load hidden");
+}
+
+void Runtime::act_gpu_attn(int step, int layer, int mb) {
+    const int t0 = (mb - 1) * mu_;
+    const int l = layer - 1;
+    const uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
+    const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
+    const int32_t* ctx = d_pos_ + static_cast<size_t>(max_steps_) * N_ + static_cast<size_t>(step - 1) * N_ + t0;
+    const int32_t* bt = d_block_table_ + static_cast<size_t>(l) * N_ * max_pages_;
+    kk(mltk::launch_kv_append(qkv, nq_, nkv_, d_, d_seq_ + t0, pos, mu_, bt, max_pages_, page_, d_kpool_, d_vpool_,
+                              s_gpu_),
+       "kv append");
+    kk(mltk::launch_gqa_decode_paged(qkv, W_, d_kpool_, d_vpool_, bt, max_pages_, d_seq_ + t0, ctx, mu_, nq_, nkv_,
+                                     d_, page_, d_attn_gpu_, Rmu_, nullptr, s_gpu_),
+       "gqa attention");
+    launches_ += 2;
+}
+
+void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
+    (void)c;
+    const int t0 = (mb - 1) * mu_;
+    const int g = (step - 1) * L_ + layer;
+    const int l = layer - 1;
+    const uint8_t** tab = dev_tables_ + (static_cast<size_t>(l) * 2 + slot_of(g)) * table_entries_;
+    float* x = d_x_ + static_cast<size_t>(t0) * H_;
+    // O projection + residual
+    mltk::GemmArgs o;
+    o.a_table = tab + tab_o_;
+    o.RB = H_ / 128;
+    o.K = H_;
+    o.b = policy_.attn_on_gpu ? d_attn_gpu_ : d_attn_in_ + static_cast<size_t>(mb - 1) * Rmu_ * H_ * 2;
+    o.R = Rmu_;
+    o.rows_dense = mu_;
+    o.n_cap = ncap_;
+    o.out_f32 = d_h_;
+    o.ldo = H_;
+    o.residual = x;
+    o.ldr = H_;
+    kk(mltk::launch_gemm(o, num_sms_, s_gpu_), "o gemm");
+    // RMSNorm + router + permute
+    kk(mltk::launch_router(d_h_, d_ffn_norm_[l], ext_.rms_eps, nullptr, d_router_[l], mu_, H_, E_, K_, d_hn_, nullptr,
+                           d_topk_, d_topw_, s_gpu_),
+       "router");
+    kk(mltk::launch_moe_permute(d_topk_, d_hn_, mu_, H_, E_, K_, d_cnt_, d_off_, d_perm_, d_inv_, d_xe_, Re_, s_gpu_),
+       "permute");
+    // experts: gate/up (SiLU fused) -> down -> combine
+    mltk::GemmArgs gu;
+    gu.a_table = tab + tab_w13_;
+    gu.n_mats = 2;
+    gu.G = E_;
+    gu.RB = F_ / 128;
+    gu.K = H_;
+    gu.b = d_xe_;
+    gu.R = Re_;
+    gu.b_off = d_off_;
+    gu.b_cnt = d_cnt_;
+    gu.n_cap = ncap_e_;
+    gu.epi = mltk::kEpiSiluPacked;
+    gu.out_packed = d_inter_;
+    gu.out_R = Re_;
+    kk(mltk::launch_gemm(gu, num_sms_, s_gpu_), "gate/up gemm");
+    mltk::GemmArgs dn;
+    dn.a_table = tab + tab_w2_;
+    dn.G = E_;
+    dn.RB = H_ / 128;
+    dn.K = F_;
+    dn.b = d_inter_;
+    dn.R = Re_;
+    dn.b_off = d_off_;
+    dn.b_cnt = d_cnt_;
+    dn.n_cap = ncap_e_;
+    dn.out_f32 = d_y_;
+    dn.ldo = H_;
+    kk(mltk::launch_gemm(dn, num_sms_, s_gpu_), "down gemm");
+    kk(mltk::launch_moe_combine(d_h_, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, x, s_gpu_), "combine");
+    launches_ += 6;
+    if (layer == L_) {  // step epilogue: final norm -> lm_head -> greedy ids
+        kk(mltk::launch_rmsnorm_pack(x, d_final_norm_, mu_, H_, ext_.rms_eps, d_xn_, Rmu_, s_gpu_), "final norm");
+        mltk::GemmArgs lm;
+        lm.a_table = d_lm_table_;
+        lm.RB = V_ / 128;
+        lm.K = H_;
+        lm.b = d_xn_;
+        lm.R = Rmu_;
+        lm.rows_dense = mu_;
+        lm.n_cap = ncap_;
+        lm.out_f32 = d_logits_;
+        lm.ldo = V_;
+        kk(mltk::launch_gemm(lm, num_sms_, s_gpu_), "lm_head gemm");
+        kk(mltk::launch_argmax(d_logits_, mu_, V_, d_tok_out_ + static_cast<size_t>(step - 1) * N_ + t0, nullptr,
+                               s_gpu_),
+           "argmax");
+        launches_ += 3;
+    }
+}
+
+void Runtime::act_weight_to_gpu(int g, int page) {
+    if (!layer_blob_bytes_) return;
+    const int l = (g - 1) % L_;
+    const auto [b, e] = page_range(page);
+    if (e <= b) return;
+    const uint8_t* src = opt_.pin_weights ? host_blob_ + static_cast<int64_t>(l) * layer_blob_bytes_
+                                          : staging_ + static_cast<int64_t>(slot_of(g)) * layer_blob_bytes_;
+    kk(cudaMemcpyAsync(dev_pool_ + static_cast<int64_t>(slot_of(g)) * layer_blob_bytes_ + b, src + b, e - b,
+                       cudaMemcpyHostToDevice, s_h2d_),
+       "weight page");
+}
+
+void Runtime::act_weight_to_pinned(int g, int page) {
+    if (opt_.pin_weights || !layer_blob_bytes_) return;  // blob already page-locked
+    const int l = (g - 1) % L_;
+    const auto [b, e] = page_range(page);
+    uint8_t* dst = staging_ + static_cast<int64_t>(slot_of(g)) * layer_blob_bytes_;
+    const uint8_t* src = host_blob_ + static_cast<int64_t>(l) * layer_blob_bytes_;
+    const int64_t chunk = 1 << 20;
+#pragma omp parallel for schedule(static) num_threads(4)
+    for (int64_t off = b; off < e; off += chunk) std::memcpy(dst + off, src + off, std::min(chunk, e - off));
+}
+
+}  // namespace mlt

@@ -1,0 +1,216 @@
+// The B200 decode runtime: budget-capped device arena, paged weight store,
+// host KV + host-core attention, and the CGOPipe executor.
+//
+// One Runtime per GPU.  It is the engine behind the reference's per-layer
+// decode step: `decode()` builds the reference ScheduleDag for the policy
+// (lightplan::sim::build_schedule, identical issue order) and EXECUTES it —
+// GPU tasks on a compute stream, weight pages and hidden uploads on an H2D
+// copy stream, QKV offloads on a D2H stream, CPU attention on host cores —
+// returning the measured sim::Timeline (replacing sim::simulate,
+// proj/src/pipesim.cpp:350-406) and a measured LatencyBreakdown.
+#pragma once
+
+#include <condition_variable>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "lightplan/pipesim.hpp"
+#include "lightplan/planner.hpp"
+
+namespace mlt {
+
+struct ModelExt {
+    int vocab = 32000;
+    float rms_eps = 1e-5f;
+    float rope_theta = 1e6f;
+    float lm_head_scale = 4.0f;
+    uint64_t seed = 1234;
+};
+
+struct RuntimeOptions {
+    int device = 0;
+    double budget_bytes = 16e9;  // every runtime device allocation comes from this arena
+    int max_ctx = 0;             // KV capacity per sequence
+    int host_threads = 0;        // CPU attention threads (0: all)
+    int pin_weights = 1;         // 1: streamed blob pinned; 0: pageable + pinned staging ring
+    int schedule = 0;            // 0 cgopipe, 3 s4
+    int synth_kv_seed = 0;       // unused placeholder
+};
+
+// Bump allocator over one cudaMalloc of the budget (SURVEY.md §7 hard part 5).
+class Arena {
+  public:
+    Arena(size_t bytes);
+    ~Arena();
+    void* alloc(size_t bytes, const char* what);
+    size_t used() const { return used_; }
+    size_t capacity() const { return cap_; }
+    const std::string& log() const { return log_; }
+
+  private:
+    uint8_t* base_ = nullptr;
+    size_t cap_ = 0, used_ = 0;
+    std::string log_;
+};
+
+// One 128-row block of one weight matrix (packed layout, all of K).
+struct WeightBlock {
+    int kind;       // TensorKind (kWqkv, kWo, kW1, kW3, kW2)
+    int expert;
+    int rb;         // row block
+    int64_t K;      // reduction length
+    int64_t bytes;  // 128 * K * 2
+    bool resident;
+    int64_t offset;  // resident: offset in the layer's resident region; streamed: offset in the layer blob
+};
+
+struct DecodeReport {
+    double seconds = 0;              // wall time of the executed DAG (device clock)
+    double tokens_per_second = 0;
+    lightplan::LatencyBreakdown measured;  // per-layer means of the measured timeline
+    double h2d_weight_bytes = 0;     // bytes of weight pages moved
+    double h2d_bytes = 0, d2h_bytes = 0;
+    double steady_layer_time = 0;
+    double utilization[5] = {0, 0, 0, 0, 0};
+    int gpu_launches = 0;
+    std::string verify;              // verify_timeline_tol result on the measured timeline
+};
+
+class Runtime {
+  public:
+    Runtime(const lightplan::ModelSpec& model, const ModelExt& ext, const lightplan::Policy& policy,
+            const RuntimeOptions& opt);
+    ~Runtime();
+    Runtime(const Runtime&) = delete;
+    Runtime& operator=(const Runtime&) = delete;
+
+    // Synthetic prompt-stage KV for positions [0, prompt_len) of every
+    // sequence (uniform(-1,1) bf16, oracle orc_fill_kv semantics); sets every
+    // sequence's position to prompt_len.
+    void prefill_synthetic(int prompt_len, uint64_t seed);
+    void set_positions(const int32_t* pos);
+    const std::vector<int32_t>& positions() const { return pos_; }
+
+    // `steps` decode steps for all N sequences.  tokens_in: [N] host ids of
+    // step 0; forced: optional [steps][N] host ids (teacher forcing); out:
+    // [steps][N] host greedy ids.  Host->device copy of the inputs and
+    // device->host copy of the ids are inside the measured region.
+    DecodeReport decode(const int32_t* tokens_in, const int32_t* forced, int steps, int32_t* out,
+                        lightplan::sim::ScheduleDag* dag_out = nullptr,
+                        lightplan::sim::Timeline* timeline_out = nullptr);
+
+    // Debug/test taps (device -> host copies, synchronous).
+    void read_residual(float* host_out);          // x [N, H] fp32
+    void read_last_topk(int32_t* host_idx);       // last micro-batch's topk [mu, K]
+    size_t debug_read(const std::string& name, void* host_out, size_t cap);
+
+    double achieved_weight_ratio() const { return achieved_rw_; }
+    int64_t streamed_bytes_per_layer() const { return layer_blob_bytes_; }
+    size_t arena_used() const { return arena_->used(); }
+    std::string arena_log() const { return arena_->log(); }
+    const lightplan::Policy& policy() const { return policy_; }
+    const lightplan::ModelSpec& model() const { return model_; }
+    double pin_seconds() const { return pin_seconds_; }
+    double gen_seconds() const { return gen_seconds_; }
+
+    // --- task actions (called by the executor) ---
+    struct Ctx;
+    void act_pre_attn(const Ctx& c, int step, int layer, int mb);
+    void act_offload_qkv(int layer, int mb);
+    void act_cpu_attn(int step, int layer, int mb);
+    void act_load_hidden(int layer, int mb);
+    void act_post_attn(const Ctx& c, int step, int layer, int mb);
+    void act_weight_to_gpu(int global_layer, int page);
+    void act_weight_to_pinned(int global_layer, int page);
+    void act_gpu_attn(int step, int layer, int mb);
+
+    cudaStream_t stream(lightplan::sim::Resource r) const;
+    int launches() const { return launches_; }
+
+  private:
+    void build_catalog();
+    void allocate();
+    void generate_weights();
+    void host_attention(int layer, int mb, int step);
+    int slot_of(int global_layer) const { return global_layer & 1; }
+    std::pair<int64_t, int64_t> page_range(int page) const;  // [begin, end) within layer blob
+
+    lightplan::ModelSpec model_;
+    ModelExt ext_;
+    lightplan::Policy policy_;
+    RuntimeOptions opt_;
+    int N_, mu_, M_, H_, F_, E_, K_, nq_, nkv_, d_, W_, V_, L_;
+    int Rmu_, Re_, ncap_, ncap_e_;
+    int num_sms_ = 148;
+
+    std::unique_ptr<Arena> arena_;
+    // weights
+    std::vector<WeightBlock> blocks_;  // per-layer catalog (same for every layer)
+    int64_t layer_blob_bytes_ = 0, layer_res_bytes_ = 0;
+    double achieved_rw_ = 0;
+    uint8_t* host_blob_ = nullptr;     // [L][layer_blob_bytes_] (pinned or pageable)
+    bool host_blob_pinned_ = false;
+    uint8_t* staging_ = nullptr;       // pinned ring [2][layer_blob_bytes_] when !pin_weights
+    uint8_t* dev_res_ = nullptr;       // [L][layer_res_bytes_]
+    uint8_t* dev_pool_ = nullptr;      // [2][layer_blob_bytes_]
+    const uint8_t** dev_tables_ = nullptr;  // [L][2 slots][table_entries]
+    int table_entries_ = 0;
+    int tab_qkv_ = 0, tab_o_ = 0, tab_w13_ = 0, tab_w2_ = 0;  // offsets within a table
+    uint16_t *d_embed_ = nullptr, *d_lm_ = nullptr, *d_final_norm_ = nullptr;
+    std::vector<uint16_t*> d_attn_norm_, d_ffn_norm_, d_router_;
+    float2* d_rope_ = nullptr;
+    const uint8_t** d_lm_table_ = nullptr;
+
+    // activations
+    float* d_x_ = nullptr;              // [N, H] residual
+    uint16_t* d_qkv_bf16_ = nullptr;    // [M][mu][W]
+    uint8_t* d_attn_in_ = nullptr;      // [M][Rmu*H] packed
+    uint8_t* d_xn_ = nullptr;           // [Rmu*H] packed
+    float* d_qkv_f32_ = nullptr;        // [Rmu, W]
+    float* d_h_ = nullptr;              // [mu, H]
+    uint16_t* d_hn_ = nullptr;          // [mu, H]
+    int32_t *d_topk_ = nullptr, *d_cnt_ = nullptr, *d_off_ = nullptr, *d_perm_ = nullptr, *d_inv_ = nullptr;
+    float* d_topw_ = nullptr;
+    uint8_t* d_xe_ = nullptr;           // [Re*H] packed
+    uint8_t* d_inter_ = nullptr;        // [Re*F] packed
+    float* d_y_ = nullptr;              // [Re, H]
+    float* d_logits_ = nullptr;         // [Rmu, V]
+    int32_t* d_tok_in_ = nullptr;       // [max_steps][N]
+    int32_t* d_tok_out_ = nullptr;      // [max_steps][N]
+    int32_t* d_pos_ = nullptr;          // [max_steps][N]
+    int32_t* d_seq_ = nullptr;          // [N]
+    int max_steps_ = 64;
+    // GPU attention (A_g = 1): paged KV pool
+    uint16_t *d_kpool_ = nullptr, *d_vpool_ = nullptr;
+    int32_t* d_block_table_ = nullptr;  // [L][N][max_pages]
+    int max_pages_ = 0, page_ = 16;
+    uint8_t* d_attn_gpu_ = nullptr;
+
+    // host side
+    uint16_t* h_qkv_ = nullptr;   // pinned [M][mu][W]
+    uint8_t* h_attn_ = nullptr;   // pinned [M][Rmu*H]
+    uint16_t* h_kcache_ = nullptr;  // [L][N][nkv][max_ctx][d]
+    uint16_t* h_vcache_ = nullptr;
+    int32_t* h_tok_ = nullptr;    // pinned [max_steps][N] in / out staging
+    std::vector<int32_t> pos_;
+    int max_ctx_ = 0;
+    int cur_forced_ = 0, cur_steps_ = 0;
+    std::vector<int32_t> step_pos_;  // [steps][N] positions used by the running decode
+
+    cudaStream_t s_gpu_ = nullptr, s_h2d_ = nullptr, s_d2h_ = nullptr;
+    int launches_ = 0;
+    double pin_seconds_ = 0, gen_seconds_ = 0;
+
+  public:
+    struct Ctx {
+        int steps;
+        bool forced;
+    };
+};
+
+}  // namespace mlt

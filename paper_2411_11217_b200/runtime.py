@@ -1,0 +1,136 @@
+"""Python handle on the native decode runtime (mlt_runtime_* in include/mlt.h).
+
+Plumbing only: every byte of compute happens in libmlt.so.  Mirrors the
+reference's vocabulary: a `Runtime` is built from a ModelSpec and a Policy
+(proj/include/lightplan/config.hpp:24-56) and `decode()` returns the greedy
+ids plus the measured per-layer LatencyBreakdown (planner.hpp:25-35).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import capi
+
+
+class RuntimeOptions(C.Structure):
+    _fields_ = [("device", C.c_int32), ("budget_bytes", C.c_double), ("max_ctx", C.c_int32),
+                ("host_threads", C.c_int32), ("pin_weights", C.c_int32), ("vocab", C.c_int32),
+                ("rms_eps", C.c_float), ("rope_theta", C.c_float), ("lm_head_scale", C.c_float),
+                ("seed", C.c_uint64)]
+
+
+class DecodeReport(C.Structure):
+    _fields_ = [("seconds", C.c_double), ("tokens_per_second", C.c_double),
+                ("measured", capi.LatencyBreakdown), ("h2d_weight_bytes", C.c_double),
+                ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double),
+                ("steady_layer_time", C.c_double), ("utilization", C.c_double * 5),
+                ("gpu_launches", C.c_int32), ("timeline_ok", C.c_int32)]
+
+
+class RuntimeInfo(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("achieved_weight_ratio", "streamed_bytes_per_layer",
+                                          "arena_used", "arena_capacity", "pin_seconds",
+                                          "gen_seconds")]
+
+
+_SIGS = {
+    "runtime_create": (C.c_void_p, [C.POINTER(capi.ModelSpec), C.POINTER(capi.Policy),
+                                    C.POINTER(RuntimeOptions)]),
+    "runtime_destroy": (None, [C.c_void_p]),
+    "runtime_info": (C.c_int, [C.c_void_p, C.POINTER(RuntimeInfo)]),
+    "runtime_prefill_synthetic": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64]),
+    "runtime_set_positions": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "runtime_decode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                 C.POINTER(DecodeReport)]),
+    "runtime_timeline_json": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
+    "runtime_read_residual": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "runtime_debug_read": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
+}
+
+
+def _fns():
+    api = capi.load_product()
+    out = {}
+    for n, (r, a) in _SIGS.items():
+        f = getattr(api.lib, "mlt_" + n)
+        f.restype, f.argtypes = r, a
+        out[n] = f
+    return api, out
+
+
+@dataclass
+class Decoded:
+    ids: np.ndarray          # [steps, N]
+    report: DecodeReport
+
+
+class Runtime:
+    def __init__(self, model: capi.ModelSpec, policy: capi.Policy, *, budget_bytes: float,
+                 max_ctx: int, vocab: int = 32000, seed: int = 1234, device: int = 0,
+                 host_threads: int = 0, pin_weights: bool = True, rms_eps: float = 1e-5,
+                 rope_theta: float = 1e6, lm_head_scale: float = 4.0):
+        self.api, self.f = _fns()
+        self.model, self.policy = model, policy
+        self.opts = RuntimeOptions(device, budget_bytes, max_ctx, host_threads, int(pin_weights),
+                                   vocab, rms_eps, rope_theta, lm_head_scale, seed)
+        self.h = self.f["runtime_create"](C.byref(model), C.byref(policy), C.byref(self.opts))
+        if not self.h:
+            code = self.api.fn["last_status"]()
+            raise capi._EXC.get(code, capi.MltError)(code, self.api.error())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.f["runtime_destroy"](self.h)
+            self.h = None
+
+    __del__ = close
+
+    def _ck(self, rc):
+        return self.api.check(rc)
+
+    @property
+    def info(self) -> RuntimeInfo:
+        out = RuntimeInfo()
+        self._ck(self.f["runtime_info"](self.h, C.byref(out)))
+        return out
+
+    def prefill_synthetic(self, prompt_len: int, seed: int = 9012):
+        self._ck(self.f["runtime_prefill_synthetic"](self.h, prompt_len, seed))
+
+    def set_positions(self, pos):
+        pos = np.ascontiguousarray(pos, np.int32)
+        self._ck(self.f["runtime_set_positions"](self.h, pos.ctypes.data_as(C.c_void_p)))
+
+    def decode(self, tokens, steps: int, forced=None) -> Decoded:
+        N = self.policy.batch
+        tokens = np.ascontiguousarray(tokens, np.int32).reshape(N)
+        out = np.zeros((steps, N), np.int32)
+        rep = DecodeReport()
+        fp = None
+        if forced is not None:
+            forced = np.ascontiguousarray(forced, np.int32).reshape(steps, N)
+            fp = forced.ctypes.data_as(C.c_void_p)
+        self._ck(self.f["runtime_decode"](self.h, tokens.ctypes.data_as(C.c_void_p), fp, steps,
+                                          out.ctypes.data_as(C.c_void_p), C.byref(rep)))
+        return Decoded(out, rep)
+
+    def timeline(self) -> dict:
+        n = self._ck(self.f["runtime_timeline_json"](self.h, None, 0))
+        buf = C.create_string_buffer(n + 1)
+        self.f["runtime_timeline_json"](self.h, buf, n + 1)
+        return json.loads(buf.value.decode())
+
+    def residual(self) -> np.ndarray:
+        x = np.zeros((self.policy.batch, self.model.hidden_dim), np.float32)
+        self._ck(self.f["runtime_read_residual"](self.h, x.ctypes.data_as(C.c_void_p)))
+        return x
+
+    def debug_read(self, name: str, dtype) -> np.ndarray:
+        n = self._ck(self.f["runtime_debug_read"](self.h, name.encode(), None, 0))
+        out = np.zeros(n // np.dtype(dtype).itemsize, dtype)
+        self._ck(self.f["runtime_debug_read"](self.h, name.encode(), out.ctypes.data_as(C.c_void_p), n))
+        return out
