@@ -281,6 +281,12 @@ int mlt_kv_append(const uint16_t* qkv_bf16, int nq, int nkv, int d, const int32_
  * computed in double (theta^(-2i/d) * pos). */
 int mlt_rope_table(int max_pos, int d, double theta, float* host_out);
 
+/* Host link measurement (the b_cg of the B200 HardwareSpec): page-locked
+ * host buffer (THP + cudaHostRegister, as the weight store) <-> device,
+ * `bytes` per copy, best of `reps`, CUDA events.  out[0] = H2D GB/s,
+ * out[1] = D2H GB/s, out[2] = H2D GB/s with a concurrent D2H stream. */
+int mlt_measure_link(int device, size_t bytes, int reps, double out[3]);
+
 /* Host: synthetic weights, element i of tensor tid: splitmix64 counter PRNG
  * (DESIGN.md §3), bf16 RNE.  Multi-threaded. */
 int mlt_synth_bf16(uint64_t seed, uint64_t tid, int64_t n, float scale, int is_norm,
@@ -314,6 +320,11 @@ typedef struct mlt_decode_report_t {
     double utilization[5];
     int32_t gpu_launches;
     int32_t timeline_ok; /* 1 when verify_timeline passes on the measured timeline */
+    /* live CUDA-event timing of the dominant kernels inside the decode */
+    double expert_ms_total;  /* expert gate/up + down GEMM pairs */
+    int32_t expert_launches;
+    double dense_ms_total;   /* QKV and O projection GEMMs */
+    int32_t dense_launches;
 } mlt_decode_report_t;
 
 typedef struct mlt_runtime_info_t {

@@ -1,7 +1,9 @@
 // C ABI over the sm_100a kernels (include/mlt.h, "Kernel-level entry
 // points").  Thin: argument checks, cudaError -> MLT_ERR_CUDA, no hidden
 // allocation except mlt_expert_ffn's (none: all buffers caller-owned).
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -238,6 +240,69 @@ int mlt_rope_table(int max_pos, int d, double theta, float* out) {
                 out[(static_cast<int64_t>(p) * half + i) * 2] = static_cast<float>(std::cos(ang));
                 out[(static_cast<int64_t>(p) * half + i) * 2 + 1] = static_cast<float>(std::sin(ang));
             }
+        return MLT_OK;
+    });
+}
+
+int mlt_measure_link(int device, size_t bytes, int reps, double out[3]) {
+    return guard([&] {
+        ck(cudaSetDevice(device), "set device");
+        const size_t align = 2u << 20;
+        bytes = (bytes + align - 1) / align * align;
+        void* h = std::aligned_alloc(align, bytes);
+        if (!h) throw std::bad_alloc();
+        std::memset(h, 1, bytes);
+        void* h2 = nullptr;
+        void* d = nullptr;
+        void* d2 = nullptr;
+        cudaStream_t s1 = nullptr, s2 = nullptr;
+        cudaEvent_t a, b;
+        auto cleanup = [&] {
+            if (d) cudaFree(d);
+            if (d2) cudaFree(d2);
+            if (h2) cudaFreeHost(h2);
+            cudaHostUnregister(h);
+            std::free(h);
+            if (s1) cudaStreamDestroy(s1);
+            if (s2) cudaStreamDestroy(s2);
+        };
+        try {
+            ck(cudaHostRegister(h, bytes, cudaHostRegisterDefault), "register");
+            ck(cudaMalloc(&d, bytes), "malloc");
+            ck(cudaMalloc(&d2, 64u << 20), "malloc");
+            ck(cudaHostAlloc(&h2, 64u << 20, 0), "hostalloc");
+            ck(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking), "stream");
+            ck(cudaEventCreate(&a), "event");
+            ck(cudaEventCreate(&b), "event");
+            auto best = [&](cudaMemcpyKind kind, bool concurrent) {
+                double bw = 0;
+                for (int r = 0; r < reps; ++r) {
+                    ck(cudaEventRecord(a, s1), "record");
+                    if (kind == cudaMemcpyHostToDevice) ck(cudaMemcpyAsync(d, h, bytes, kind, s1), "copy");
+                    else ck(cudaMemcpyAsync(h, d, bytes, kind, s1), "copy");
+                    if (concurrent)
+                        for (int i = 0; i < 8; ++i) ck(cudaMemcpyAsync(h2, d2, 1u << 20, cudaMemcpyDeviceToHost, s2), "copy");
+                    ck(cudaEventRecord(b, s1), "record");
+                    ck(cudaEventSynchronize(b), "sync");
+                    ck(cudaStreamSynchronize(s2), "sync");
+                    float ms = 0;
+                    ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+                    bw = std::max(bw, static_cast<double>(bytes) / (ms * 1e-3) / 1e9);
+                }
+                return bw;
+            };
+            best(cudaMemcpyHostToDevice, false);  // warm
+            out[0] = best(cudaMemcpyHostToDevice, false);
+            out[1] = best(cudaMemcpyDeviceToHost, false);
+            out[2] = best(cudaMemcpyHostToDevice, true);
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
         return MLT_OK;
     });
 }

@@ -101,6 +101,10 @@ int mlt_runtime_decode(mlt_runtime* r, const int32_t* tokens, const int32_t* for
             for (int i = 0; i < 5; ++i) rep->utilization[i] = d.utilization[i];
             rep->gpu_launches = d.gpu_launches;
             rep->timeline_ok = d.verify.empty() ? 1 : 0;
+            rep->expert_ms_total = d.expert_ms_total;
+            rep->expert_launches = d.expert_launches;
+            rep->dense_ms_total = d.qkv_o_ms_total;
+            rep->dense_launches = d.dense_launches;
         }
         if (!d.verify.empty()) mlt::set_error(("timeline: " + d.verify).c_str(), MLT_OK);
         return MLT_OK;

@@ -197,6 +197,9 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
     const Ctx cctx{steps, forced != nullptr};
     cur_steps_ = steps;
     launches_ = 0;
+    ev_expert_.clear();
+    ev_dense_.clear();
+    event_next_ = 0;
 
     std::array<std::vector<int>, lightplan::sim::kResourceCount> fifo;
     for (int i = 0; i < n; ++i) fifo[static_cast<int>(dag.tasks[i].resource)].push_back(i);
@@ -308,6 +311,18 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
     cudaEventDestroy(e_inputs);
 
     DecodeReport rep;
+    for (const auto& [a, b] : ev_expert_) {
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+        rep.expert_ms_total += ms;
+    }
+    rep.expert_launches = static_cast<int>(ev_expert_.size());
+    for (const auto& [a, b] : ev_dense_) {
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+        rep.qkv_o_ms_total += ms;
+    }
+    rep.dense_launches = static_cast<int>(ev_dense_.size());
     rep.seconds = total_ms * 1e-3;
     rep.tokens_per_second = static_cast<double>(N_) * steps / rep.seconds;
     rep.gpu_launches = launches_;

@@ -126,6 +126,7 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
 
 Runtime::~Runtime() {
     cudaDeviceSynchronize();
+    for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
     host_free(host_blob_, host_blob_pinned_);
     host_free(staging_, true);
     if (h_qkv_) cudaFreeHost(h_qkv_);
@@ -431,6 +432,15 @@ size_t Runtime::debug_read(const std::string& name, void* out, size_t cap) {
     return bytes;
 }
 
+cudaEvent_t Runtime::take_event() {
+    if (event_next_ == event_pool_.size()) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "event");
+        event_pool_.push_back(e);
+    }
+    return event_pool_[event_next_++];
+}
+
 // ---------------------------------------------------------------------------
 // Task actions.  step/layer/mb are the 1-based fields of sim::Task.
 // ---------------------------------------------------------------------------
@@ -464,7 +474,11 @@ void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
     a.epi = mltk::kEpiF32;
     a.out_f32 = d_qkv_f32_;
     a.ldo = W_;
+    cudaEvent_t q0 = take_event(), q1 = take_event();
+    kk(cudaEventRecord(q0, s_gpu_), "event");
     kk(mltk::launch_gemm(a, num_sms_, s_gpu_), "qkv gemm");
+    kk(cudaEventRecord(q1, s_gpu_), "event");
+    ev_dense_.push_back({q0, q1});
     const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
     uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
     kk(mltk::launch_rope_qkv(d_qkv_f32_, pos, d_rope_, mu_, nq_, nkv_, d_, qkv, s_gpu_), "rope");
@@ -525,13 +539,19 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     o.ldo = H_;
     o.residual = x;
     o.ldr = H_;
+    cudaEvent_t o0 = take_event(), o1 = take_event();
+    kk(cudaEventRecord(o0, s_gpu_), "event");
     kk(mltk::launch_gemm(o, num_sms_, s_gpu_), "o gemm");
+    kk(cudaEventRecord(o1, s_gpu_), "event");
+    ev_dense_.push_back({o0, o1});
     // RMSNorm + router + permute
     kk(mltk::launch_router(d_h_, d_ffn_norm_[l], ext_.rms_eps, nullptr, d_router_[l], mu_, H_, E_, K_, d_hn_, nullptr,
                            d_topk_, d_topw_, s_gpu_),
        "router");
     kk(mltk::launch_moe_permute(d_topk_, d_hn_, mu_, H_, E_, K_, d_cnt_, d_off_, d_perm_, d_inv_, d_xe_, Re_, s_gpu_),
        "permute");
+    cudaEvent_t ex0 = take_event(), ex1 = take_event();
+    kk(cudaEventRecord(ex0, s_gpu_), "event");
     // experts: gate/up (SiLU fused) -> down -> combine
     mltk::GemmArgs gu;
     gu.a_table = tab + tab_w13_;
@@ -561,6 +581,8 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     dn.out_f32 = d_y_;
     dn.ldo = H_;
     kk(mltk::launch_gemm(dn, num_sms_, s_gpu_), "down gemm");
+    kk(cudaEventRecord(ex1, s_gpu_), "event");
+    ev_expert_.push_back({ex0, ex1});
     kk(mltk::launch_moe_combine(d_h_, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, x, s_gpu_), "combine");
     launches_ += 6;
     if (layer == L_) {  // step epilogue: final norm -> lm_head -> greedy ids

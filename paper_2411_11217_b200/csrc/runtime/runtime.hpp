@@ -79,6 +79,12 @@ struct DecodeReport {
     double utilization[5] = {0, 0, 0, 0, 0};
     int gpu_launches = 0;
     std::string verify;              // verify_timeline_tol result on the measured timeline
+    // Live per-launch timing of the dominant kernel pair (expert gate/up +
+    // down GEMM of one micro-batch), CUDA events on the compute stream.
+    double expert_ms_total = 0;
+    int expert_launches = 0;
+    double qkv_o_ms_total = 0;       // dense QKV + O projections (pairs per micro-batch-layer)
+    int dense_launches = 0;
 };
 
 class Runtime {
@@ -204,6 +210,11 @@ class Runtime {
 
     cudaStream_t s_gpu_ = nullptr, s_h2d_ = nullptr, s_d2h_ = nullptr;
     int launches_ = 0;
+    // kernel event pairs recorded by the GPU worker during decode()
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_expert_, ev_dense_;
+    cudaEvent_t take_event();
+    std::vector<cudaEvent_t> event_pool_;
+    size_t event_next_ = 0;
     double pin_seconds_ = 0, gen_seconds_ = 0;
 
   public:

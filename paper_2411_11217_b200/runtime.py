@@ -28,7 +28,9 @@ class DecodeReport(C.Structure):
                 ("measured", capi.LatencyBreakdown), ("h2d_weight_bytes", C.c_double),
                 ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double),
                 ("steady_layer_time", C.c_double), ("utilization", C.c_double * 5),
-                ("gpu_launches", C.c_int32), ("timeline_ok", C.c_int32)]
+                ("gpu_launches", C.c_int32), ("timeline_ok", C.c_int32),
+                ("expert_ms_total", C.c_double), ("expert_launches", C.c_int32),
+                ("dense_ms_total", C.c_double), ("dense_launches", C.c_int32)]
 
 
 class RuntimeInfo(C.Structure):
