@@ -225,7 +225,7 @@ def run_mlt(args, cfg):
     t = time.perf_counter()
     rt = Runtime(model_spec(cfg), policy(cfg), budget_bytes=cfg["budget"],
                  max_ctx=cfg["prompt"] + args.warmup + args.steps + 8, vocab=cfg["vocab"],
-                 device=local)
+                 device=local, exact_gates=args.gates == "exact")
     info = rt.info
     log(f"[bench] runtime ready in {time.perf_counter() - t:.1f}s (weights gen {info.gen_seconds:.1f}s,"
         f" pin {info.pin_seconds:.1f}s), r_w achieved {info.achieved_weight_ratio:.4f}, "
@@ -242,6 +242,11 @@ def run_mlt(args, cfg):
         t1 = time.perf_counter()
     clocks = clk.summary()
     rep = d.report
+    if not rep.timeline_ok:
+        log(f"[bench] measured timeline check: {api.error()}")
+    if args.timeline:
+        with open(args.timeline, "w") as fh:
+            json.dump(rt.timeline(), fh)
     value = rep.tokens_per_second                # device-timed (CUDA events)
     e2e = cfg["N"] * args.steps / (t1 - t0)      # wall clock around the C-ABI call
     bound = hrm_bound(cfg, link_gbs, pk)
@@ -259,6 +264,7 @@ def run_mlt(args, cfg):
                    "gpu_budget_gb": cfg["budget"] / 1e9, "r_w": cfg["r_w"],
                    "r_w_achieved": info.achieved_weight_ratio, "A_g": cfg["a_g"],
                    "parallelism": "single GPU, CGOPipe paging",
+                   "weight_gates": args.gates,
                    "l2": "weights streamed per step (>> 126 MB L2): no flush needed"},
         "hrm": {"bound_tok_s": bound.decode_throughput, "frac": value / bound.decode_throughput,
                 "binding": "host link (H2D)", "link_gbs_measured": link_gbs,
@@ -293,6 +299,9 @@ def main():
     ap.add_argument("--impl", default="mlt", choices=["mlt", "reference"])
     ap.add_argument("--config", default="mixtral8x7b-16g", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gates", default="exact", choices=["exact", "reference"],
+                    help="weight gates: data-exact (default) or the reference's all-pages gate")
+    ap.add_argument("--timeline", default=None, help="write the measured timeline JSON here")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -311,6 +311,9 @@ typedef struct mlt_runtime_options_t {
     int32_t vocab;
     float rms_eps, rope_theta, lm_head_scale;
     uint64_t seed;         /* synthetic-weight seed */
+    int32_t exact_gates;   /* 1: data-exact weight gates (default); 0: reference gates,
+                              every GPU task of layer g waits for all pages of g
+                              (pipesim.cpp:131-148) */
 } mlt_runtime_options_t;
 
 typedef struct mlt_decode_report_t {

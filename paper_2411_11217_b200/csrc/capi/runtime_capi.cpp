@@ -46,6 +46,7 @@ mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p
         mlt::RuntimeOptions opt;
         opt.device = o->device; opt.budget_bytes = o->budget_bytes; opt.max_ctx = o->max_ctx;
         opt.host_threads = o->host_threads; opt.pin_weights = o->pin_weights;
+        opt.exact_gates = o->exact_gates;
         auto hh = std::make_unique<Handle>();
         hh->rt = std::make_unique<mlt::Runtime>(ms, ext, pol, opt);
         h = hh.release();

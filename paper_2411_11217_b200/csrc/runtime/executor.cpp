@@ -36,6 +36,7 @@
 #include <vector>
 
 #include "../capi/status.hpp"
+#include "host_layout.hpp"
 #include "runtime.hpp"
 
 namespace mlt {
@@ -111,6 +112,49 @@ struct Flags {
 
 }  // namespace
 
+// Data-exact weight gates.  The reference gates every GPU task of layer g on
+// ALL of layer g's pages (pipesim.cpp:131-148: "routing may touch any
+// expert"), which is exact for PostAttn (the expert FFN reads every expert)
+// but over-conservative for PreAttn, which reads only the QKV blocks — often
+// resident.  With the reference gate, PreAttn(g,1) -> OffloadQkv -> CpuAttn ->
+// LoadHidden(g,1) cannot start until the last page of g lands, and because
+// LoadHidden(g,1) precedes the first page of g+1 in the h2d FIFO the link
+// idles for that whole chain every layer (the reference simulator shows the
+// same ~2.6% bubble).  Here each GPU task keeps exactly the page edges whose
+// byte range overlaps a weight block it reads; the issue order is unchanged.
+void Runtime::apply_exact_gates(ScheduleDag& dag) const {
+    const int n = static_cast<int>(dag.tasks.size());
+    const int G = dag.layers * dag.steps;
+    // pages[g][p] -> WeightToGpu task index (p = 0: whole layer)
+    std::vector<std::vector<std::pair<int, int>>> pages(G + 1);
+    for (int i = 0; i < n; ++i) {
+        const Task& t = dag.tasks[i];
+        if (t.kind == TaskKind::WeightToGpu) pages[(t.step - 1) * dag.layers + t.layer].push_back({t.page, i});
+    }
+    auto needs = [&](bool pre, int page) {
+        const auto [b, e] = page_range(page);
+        for (const auto& blk : blocks_) {
+            if (blk.resident) continue;
+            const bool read_by_pre = blk.kind == kWqkv;
+            if (read_by_pre != pre) continue;
+            if (blk.offset < e && blk.offset + blk.bytes > b) return true;
+        }
+        return false;
+    };
+    for (int i = 0; i < n; ++i) {
+        Task& t = dag.tasks[i];
+        if (t.kind != TaskKind::PreAttn && t.kind != TaskKind::PostAttn && t.kind != TaskKind::GpuAttn) continue;
+        const int g = (t.step - 1) * dag.layers + t.layer;
+        std::vector<int> keep;
+        for (int d : t.deps)
+            if (dag.tasks[d].kind != TaskKind::WeightToGpu) keep.push_back(d);
+        if (t.kind != TaskKind::GpuAttn)  // GPU attention reads only the (resident) KV pool
+            for (const auto& [p, idx] : pages[g])
+                if (needs(t.kind == TaskKind::PreAttn, p)) keep.push_back(idx);
+        t.deps = std::move(keep);
+    }
+}
+
 DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, int steps, int32_t* out,
                              ScheduleDag* dag_out, Timeline* tl_out) {
     if (steps < 1 || steps > max_steps_) throw std::invalid_argument("steps must be in [1, 64]");
@@ -143,6 +187,7 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
         kind, L_, steps, M_);
     (void)pol;
     const int n = static_cast<int>(dag.tasks.size());
+    if (opt_.exact_gates) apply_exact_gates(dag);
     const auto extra = reuse_edges(dag);
     {
         ScheduleDag check = dag;  // prove the augmented graph acyclic
@@ -276,10 +321,17 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
        "ids d2h");
     ck(cudaEventRecord(e_end, s_gpu_), "record");
     ck(cudaEventSynchronize(e_end), "sync");
+    const double host_end = std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count();
     std::memcpy(out, h_tok_ + static_cast<size_t>(max_steps_) * N_ * 3, static_cast<size_t>(steps) * N_ * 4);
     for (int i = 0; i < N_; ++i) pos_[i] += steps;
 
     // ---- measured timeline ----
+    // Host (steady_clock) and GPU timers drift by tens of ppm; map host times
+    // onto the device timebase with the two synchronisation points (e0 at
+    // host 0, e_end at host_end).
+    float total_ms = 0;
+    ck(cudaEventElapsedTime(&total_ms, e0, e_end), "elapsed");
+    const double clock_scale = host_end > 0 ? (total_ms * 1e-3) / host_end : 1.0;
     Timeline tl;
     tl.entries.resize(n);
     ScheduleDag measured = dag;
@@ -292,8 +344,8 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
             s = a * 1e-3;
             e = b * 1e-3;
         } else {
-            s = h_start[i];
-            e = h_end[i];
+            s = h_start[i] * clock_scale;
+            e = h_end[i] * clock_scale;
         }
         tl.entries[i] = {i, s, e};
         measured.tasks[i].duration = e - s;
@@ -304,8 +356,6 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
             cudaEventDestroy(ev_end[i]);
         }
     }
-    float total_ms = 0;
-    ck(cudaEventElapsedTime(&total_ms, e0, e_end), "elapsed");
     cudaEventDestroy(e0);
     cudaEventDestroy(e_end);
     cudaEventDestroy(e_inputs);

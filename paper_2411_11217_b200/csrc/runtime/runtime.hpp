@@ -38,8 +38,7 @@ struct RuntimeOptions {
     int max_ctx = 0;             // KV capacity per sequence
     int host_threads = 0;        // CPU attention threads (0: all)
     int pin_weights = 1;         // 1: streamed blob pinned; 0: pageable + pinned staging ring
-    int schedule = 0;            // 0 cgopipe, 3 s4
-    int synth_kv_seed = 0;       // unused placeholder
+    int exact_gates = 1;         // 1: data-exact weight gates; 0: reference gates (all pages of g)
 };
 
 // Bump allocator over one cudaMalloc of the budget (SURVEY.md §7 hard part 5).
@@ -140,6 +139,7 @@ class Runtime {
 
   private:
     void build_catalog();
+    void apply_exact_gates(lightplan::sim::ScheduleDag& dag) const;
     void allocate();
     void generate_weights();
     void host_attention(int layer, int mb, int step);

@@ -20,7 +20,7 @@ class RuntimeOptions(C.Structure):
     _fields_ = [("device", C.c_int32), ("budget_bytes", C.c_double), ("max_ctx", C.c_int32),
                 ("host_threads", C.c_int32), ("pin_weights", C.c_int32), ("vocab", C.c_int32),
                 ("rms_eps", C.c_float), ("rope_theta", C.c_float), ("lm_head_scale", C.c_float),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("exact_gates", C.c_int32)]
 
 
 class DecodeReport(C.Structure):
@@ -74,11 +74,12 @@ class Runtime:
     def __init__(self, model: capi.ModelSpec, policy: capi.Policy, *, budget_bytes: float,
                  max_ctx: int, vocab: int = 32000, seed: int = 1234, device: int = 0,
                  host_threads: int = 0, pin_weights: bool = True, rms_eps: float = 1e-5,
-                 rope_theta: float = 1e6, lm_head_scale: float = 4.0):
+                 rope_theta: float = 1e6, lm_head_scale: float = 4.0, exact_gates: bool = True):
         self.api, self.f = _fns()
         self.model, self.policy = model, policy
         self.opts = RuntimeOptions(device, budget_bytes, max_ctx, host_threads, int(pin_weights),
-                                   vocab, rms_eps, rope_theta, lm_head_scale, seed)
+                                   vocab, rms_eps, rope_theta, lm_head_scale, seed,
+                                   int(exact_gates))
         self.h = self.f["runtime_create"](C.byref(model), C.byref(policy), C.byref(self.opts))
         if not self.h:
             code = self.api.fn["last_status"]()
