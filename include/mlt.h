@@ -350,6 +350,15 @@ int mlt_runtime_set_positions(mlt_runtime* rt, const int32_t* host_pos);
  * or NULL (teacher forcing), host_out [steps][N] greedy ids. */
 int mlt_runtime_decode(mlt_runtime* rt, const int32_t* host_tokens, const int32_t* host_forced,
                        int steps, int32_t* host_out, mlt_decode_report_t* report);
+/* The graph the executor runs for `reference` (a build_schedule DAG of this
+ * model/policy): same tasks and issue order; with exact_gates the
+ * all-pages weight gates (pipesim.cpp:131-148) are replaced by the pages a
+ * task actually reads; buffer-reuse (write-after-read) edges of the two-slot
+ * page pool / staging ring are added to deps.  GPU-free; NULL on error.
+ * info (optional) receives the realised residency split. */
+mlt_dag* mlt_execution_dag(const mlt_dag* reference, const mlt_model_spec_t* model,
+                           const mlt_policy_t* policy, int exact_gates,
+                           mlt_runtime_info_t* info);
 /* timeline_json of the last decode's measured timeline; returns length. */
 int mlt_runtime_timeline_json(mlt_runtime* rt, char* buf, size_t cap);
 int mlt_runtime_read_residual(mlt_runtime* rt, float* host_out);

@@ -336,6 +336,13 @@ class Api:
         h = self.fn["schedule_build_durations"](arr, SCHED[kind], layers, steps, micro_batches)
         return self._dag(h)
 
+    def execution_dag(self, dag: "Dag", model, policy, exact_gates=True):
+        """The DAG the executor runs for `dag` (mlt_execution_dag)."""
+        f = self.lib.mlt_execution_dag
+        f.restype = C.c_void_p
+        f.argtypes = [C.c_void_p, P(ModelSpec), P(Policy), C.c_int, C.c_void_p]
+        return self._dag(f(dag.h, C.byref(model), C.byref(policy), int(exact_gates), None))
+
     def dag_from_tasks(self, tasks, layers=1, steps=1, micro_batches=1, kind="cgopipe"):
         """tasks: list of (Task, deps)."""
         arr = (Task * max(len(tasks), 1))()

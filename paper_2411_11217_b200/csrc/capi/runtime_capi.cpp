@@ -57,6 +57,34 @@ mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p
 
 void mlt_runtime_destroy(mlt_runtime* r) { delete H(r); }
 
+mlt_dag* mlt_execution_dag(const mlt_dag* ref, const mlt_model_spec_t* m, const mlt_policy_t* p,
+                           int exact_gates, mlt_runtime_info_t* info) {
+    mlt_dag* out = nullptr;
+    guard([&] {
+        lightplan::ModelSpec ms;
+        ms.layers = m->layers; ms.hidden_dim = m->hidden_dim; ms.ffn_dim = m->ffn_dim;
+        ms.q_heads = m->q_heads; ms.kv_heads = m->kv_heads; ms.experts = m->experts;
+        ms.top_k = m->top_k; ms.weight_dtype_bytes = m->weight_dtype_bytes;
+        ms.kv_dtype_bytes = m->kv_dtype_bytes;
+        lightplan::Policy pol;
+        pol.batch = p->batch; pol.micro_batch = p->micro_batch;
+        pol.attn_on_gpu = p->attn_on_gpu != 0; pol.ffn_on_gpu = p->ffn_on_gpu != 0;
+        pol.weights_on_gpu = p->weights_on_gpu; pol.kv_on_gpu = p->kv_on_gpu;
+        const auto& dag = *reinterpret_cast<const lightplan::sim::ScheduleDag*>(ref);
+        const mlt::Catalog cat = mlt::build_catalog(ms, pol);
+        auto* d = new lightplan::sim::ScheduleDag(
+            mlt::execution_dag(dag, cat, static_cast<int>(pol.micro_batch_count()), exact_gates != 0));
+        if (info) {
+            info->achieved_weight_ratio = cat.achieved_rw;
+            info->streamed_bytes_per_layer = static_cast<double>(cat.blob_bytes);
+            info->arena_used = info->arena_capacity = info->pin_seconds = info->gen_seconds = 0;
+        }
+        out = reinterpret_cast<mlt_dag*>(d);
+        return MLT_OK;
+    });
+    return out;
+}
+
 int mlt_runtime_info(const mlt_runtime* r, mlt_runtime_info_t* out) {
     return guard([&] {
         const auto& rt = *reinterpret_cast<const Handle*>(r)->rt;

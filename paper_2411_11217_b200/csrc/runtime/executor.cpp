@@ -57,30 +57,6 @@ bool on_device(Resource r) {
     return r == Resource::Gpu || r == Resource::HostToDevice || r == Resource::DeviceToHost;
 }
 
-// Extra write-after-read edges for buffer reuse (see file comment).
-std::vector<std::vector<int>> reuse_edges(const ScheduleDag& dag) {
-    const int n = static_cast<int>(dag.tasks.size());
-    const int L = dag.layers;
-    std::vector<std::vector<int>> extra(n);
-    std::vector<std::vector<int>> gpu_of_layer(L * dag.steps + 2), up_of(L * dag.steps + 2);
-    for (int i = 0; i < n; ++i) {
-        const Task& t = dag.tasks[i];
-        const int g = (t.step - 1) * L + t.layer;
-        if (t.resource == Resource::Gpu) gpu_of_layer[g].push_back(i);
-        if (t.kind == TaskKind::WeightToGpu) up_of[g].push_back(i);
-    }
-    for (int i = 0; i < n; ++i) {
-        const Task& t = dag.tasks[i];
-        const int g = (t.step - 1) * L + t.layer;
-        if (g <= 2) continue;
-        if (t.kind == TaskKind::WeightToGpu)
-            extra[i] = gpu_of_layer[g - 2];
-        else if (t.kind == TaskKind::WeightToPinned)
-            extra[i] = up_of[g - 2];
-    }
-    return extra;
-}
-
 struct Flags {
     std::mutex m;
     std::condition_variable cv;
@@ -111,49 +87,6 @@ struct Flags {
 };
 
 }  // namespace
-
-// Data-exact weight gates.  The reference gates every GPU task of layer g on
-// ALL of layer g's pages (pipesim.cpp:131-148: "routing may touch any
-// expert"), which is exact for PostAttn (the expert FFN reads every expert)
-// but over-conservative for PreAttn, which reads only the QKV blocks — often
-// resident.  With the reference gate, PreAttn(g,1) -> OffloadQkv -> CpuAttn ->
-// LoadHidden(g,1) cannot start until the last page of g lands, and because
-// LoadHidden(g,1) precedes the first page of g+1 in the h2d FIFO the link
-// idles for that whole chain every layer (the reference simulator shows the
-// same ~2.6% bubble).  Here each GPU task keeps exactly the page edges whose
-// byte range overlaps a weight block it reads; the issue order is unchanged.
-void Runtime::apply_exact_gates(ScheduleDag& dag) const {
-    const int n = static_cast<int>(dag.tasks.size());
-    const int G = dag.layers * dag.steps;
-    // pages[g][p] -> WeightToGpu task index (p = 0: whole layer)
-    std::vector<std::vector<std::pair<int, int>>> pages(G + 1);
-    for (int i = 0; i < n; ++i) {
-        const Task& t = dag.tasks[i];
-        if (t.kind == TaskKind::WeightToGpu) pages[(t.step - 1) * dag.layers + t.layer].push_back({t.page, i});
-    }
-    auto needs = [&](bool pre, int page) {
-        const auto [b, e] = page_range(page);
-        for (const auto& blk : blocks_) {
-            if (blk.resident) continue;
-            const bool read_by_pre = blk.kind == kWqkv;
-            if (read_by_pre != pre) continue;
-            if (blk.offset < e && blk.offset + blk.bytes > b) return true;
-        }
-        return false;
-    };
-    for (int i = 0; i < n; ++i) {
-        Task& t = dag.tasks[i];
-        if (t.kind != TaskKind::PreAttn && t.kind != TaskKind::PostAttn && t.kind != TaskKind::GpuAttn) continue;
-        const int g = (t.step - 1) * dag.layers + t.layer;
-        std::vector<int> keep;
-        for (int d : t.deps)
-            if (dag.tasks[d].kind != TaskKind::WeightToGpu) keep.push_back(d);
-        if (t.kind != TaskKind::GpuAttn)  // GPU attention reads only the (resident) KV pool
-            for (const auto& [p, idx] : pages[g])
-                if (needs(t.kind == TaskKind::PreAttn, p)) keep.push_back(idx);
-        t.deps = std::move(keep);
-    }
-}
 
 DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, int steps, int32_t* out,
                              ScheduleDag* dag_out, Timeline* tl_out) {
@@ -187,7 +120,7 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
         kind, L_, steps, M_);
     (void)pol;
     const int n = static_cast<int>(dag.tasks.size());
-    if (opt_.exact_gates) apply_exact_gates(dag);
+    if (opt_.exact_gates) apply_exact_gates(dag, cat_, M_);
     const auto extra = reuse_edges(dag);
     {
         ScheduleDag check = dag;  // prove the augmented graph acyclic

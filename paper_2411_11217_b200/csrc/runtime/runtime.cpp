@@ -149,54 +149,12 @@ cudaStream_t Runtime::stream(lightplan::sim::Resource r) const {
     }
 }
 
-// Per-layer block catalog and residency split.  Resident first: attention
-// projections, then expert row blocks in (expert, W1, W3, W2) order, as long
-// as the layer's resident bytes (router included) stay <= r_w * W_layer —
-// the reference's uniform share (opcost.cpp:71) realised at 128-row-block
-// granularity (SURVEY.md Appendix B "r_w realization").
+// Residency split and blob layout: exec_plan.cpp build_catalog.
 void Runtime::build_catalog() {
-    blocks_.clear();
-    auto add = [&](int kind, int expert, int rows, int64_t K) {
-        for (int rb = 0; rb < rows / 128; ++rb)
-            blocks_.push_back({kind, expert, rb, K, 128 * K * 2, false, 0});
-    };
-    add(kWqkv, 0, W_, H_);
-    add(kWo, 0, H_, H_);
-    for (int e = 0; e < E_; ++e) {
-        add(kW1, e, F_, H_);
-        add(kW3, e, F_, H_);
-        add(kW2, e, H_, F_);
-    }
-    const double layer_total = lightplan::layer_weight_bytes(model_).total();
-    const double router = static_cast<double>(E_) * H_ * 2;
-    double budget = policy_.weights_on_gpu * layer_total - router;
-    int64_t res = 0, blob = 0;
-    bool open = true;
-    for (auto& b : blocks_) {
-        if (open && static_cast<double>(res + b.bytes) <= budget) {
-            b.resident = true;
-            b.offset = res;
-            res += b.bytes;
-        } else {
-            open = false;
-            b.resident = false;
-            b.offset = blob;
-            blob += b.bytes;
-        }
-    }
-    layer_res_bytes_ = res;
-    layer_blob_bytes_ = blob;
-    achieved_rw_ = (static_cast<double>(res) + router) / layer_total;
-}
-
-std::pair<int64_t, int64_t> Runtime::page_range(int page) const {
-    if (page <= 0) return {0, layer_blob_bytes_};
-    // n_ub pages per layer (pipesim.cpp:150-162), 4 KiB-aligned boundaries.
-    auto edge = [&](int p) {
-        const int64_t raw = layer_blob_bytes_ * p / M_;
-        return p == M_ ? layer_blob_bytes_ : (raw & ~static_cast<int64_t>(4095));
-    };
-    return {edge(page - 1), edge(page)};
+    cat_ = mlt::build_catalog(model_, policy_);
+    layer_res_bytes_ = cat_.resident_bytes;
+    layer_blob_bytes_ = cat_.blob_bytes;
+    achieved_rw_ = cat_.achieved_rw;
 }
 
 void Runtime::allocate() {
@@ -294,7 +252,7 @@ void Runtime::generate_weights() {
     std::vector<const uint8_t*> tab(static_cast<size_t>(L_) * 2 * table_entries_);
     for (int l = 0; l < L_; ++l) {
         int idx_qkv = 0, idx_o = 0;
-        for (const auto& b : blocks_) {
+        for (const auto& b : cat_.blocks) {
             const bool down = b.kind == kW2;
             const int rows = b.kind == kWqkv ? W_ : (b.kind == kWo || down) ? H_ : F_;
             const float scale = static_cast<float>(down ? sF : sH);

@@ -19,6 +19,7 @@
 
 #include <cuda_runtime.h>
 
+#include "exec_plan.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
 
@@ -55,17 +56,6 @@ class Arena {
     uint8_t* base_ = nullptr;
     size_t cap_ = 0, used_ = 0;
     std::string log_;
-};
-
-// One 128-row block of one weight matrix (packed layout, all of K).
-struct WeightBlock {
-    int kind;       // TensorKind (kWqkv, kWo, kW1, kW3, kW2)
-    int expert;
-    int rb;         // row block
-    int64_t K;      // reduction length
-    int64_t bytes;  // 128 * K * 2
-    bool resident;
-    int64_t offset;  // resident: offset in the layer's resident region; streamed: offset in the layer blob
 };
 
 struct DecodeReport {
@@ -139,12 +129,14 @@ class Runtime {
 
   private:
     void build_catalog();
-    void apply_exact_gates(lightplan::sim::ScheduleDag& dag) const;
     void allocate();
     void generate_weights();
     void host_attention(int layer, int mb, int step);
     int slot_of(int global_layer) const { return global_layer & 1; }
-    std::pair<int64_t, int64_t> page_range(int page) const;  // [begin, end) within layer blob
+    std::pair<int64_t, int64_t> page_range(int page) const {  // [begin, end) within layer blob
+        return mlt::page_range(layer_blob_bytes_, M_, page);
+    }
+    Catalog cat_;
 
     lightplan::ModelSpec model_;
     ModelExt ext_;
@@ -156,7 +148,6 @@ class Runtime {
 
     std::unique_ptr<Arena> arena_;
     // weights
-    std::vector<WeightBlock> blocks_;  // per-layer catalog (same for every layer)
     int64_t layer_blob_bytes_ = 0, layer_res_bytes_ = 0;
     double achieved_rw_ = 0;
     uint8_t* host_blob_ = nullptr;     // [L][layer_blob_bytes_] (pinned or pageable)

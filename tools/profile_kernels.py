@@ -1,0 +1,136 @@
+"""Kernel microbenchmark at Mixtral-8x7B decode shapes (mu tokens per launch).
+
+Times each hot kernel with CUDA events (warm, back-to-back, weights > L2 so
+every launch streams from HBM) and prints achieved GB/s against the
+measured HBM peak.  Used standalone and under ncu (`--once` runs each kernel
+a fixed small number of times for a capture).
+
+  python tools/profile_kernels.py [--mu 64] [--once]
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2411_11217_b200 import capi  # noqa: E402
+
+H, F, E, K, NQ, NKV, D, V = 4096, 14336, 8, 2, 32, 8, 128, 32000
+W = (NQ + 2 * NKV) * D
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mu", type=int, default=64)
+    ap.add_argument("--once", action="store_true")
+    ap.add_argument("--reps", type=int, default=20)
+    a = ap.parse_args()
+    mu = a.mu
+    KD = capi.load_kernels()
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    torch.manual_seed(0)
+
+    def blocks(rows, k, n_mats=1):
+        """n_mats x E packed weight matrices [rows, k] (random bytes are fine:
+        bandwidth does not depend on values; use small normals to avoid inf)."""
+        w = (torch.randn(n_mats * E * rows * k, device="cuda") * 0.02).to(torch.bfloat16)
+        per = rows * k * 2
+        tab = [w.data_ptr() + (m * E + e) * per + rb * 128 * k * 2
+               for m in range(n_mats) for e in range(E) for rb in range(rows // 128)]
+        return w, torch.tensor(tab, dtype=torch.int64, device="cuda")
+
+    w13, t13 = blocks(F, H, 2)
+    w2, t2 = blocks(H, F, 1)
+    wqkv = (torch.randn(W * H, device="cuda") * 0.02).to(torch.bfloat16)
+    tqkv = torch.tensor([wqkv.data_ptr() + rb * 128 * H * 2 for rb in range(W // 128)],
+                        dtype=torch.int64, device="cuda")
+    wo = (torch.randn(H * H, device="cuda") * 0.02).to(torch.bfloat16)
+    to = torch.tensor([wo.data_ptr() + rb * 128 * H * 2 for rb in range(H // 128)],
+                      dtype=torch.int64, device="cuda")
+    wr = (torch.randn(E, H, device="cuda") * H ** -0.5).to(torch.bfloat16)
+    x = torch.randn(mu, H, device="cuda")
+    gamma = torch.ones(H, device="cuda").to(torch.bfloat16)
+    hn = torch.zeros(mu, H, dtype=torch.bfloat16, device="cuda")
+    idx = torch.zeros(mu, K, dtype=torch.int32, device="cuda")
+    wts = torch.zeros(mu, K, device="cuda")
+    R = (mu * K + 16 * E + 15) // 16 * 16
+    cnt = torch.zeros(E, dtype=torch.int32, device="cuda")
+    off = torch.zeros(E + 1, dtype=torch.int32, device="cuda")
+    perm = torch.zeros(R, dtype=torch.int32, device="cuda")
+    inv = torch.zeros(mu * K, dtype=torch.int32, device="cuda")
+    xp = torch.zeros(R * H, dtype=torch.int16, device="cuda")
+    inter = torch.zeros(R * F, dtype=torch.int16, device="cuda")
+    y = torch.zeros(R, H, device="cuda")
+    xo = torch.zeros(mu, H, device="cuda")
+    Rmu = (mu + 15) // 16 * 16
+    xn = torch.zeros(Rmu * H, dtype=torch.int16, device="cuda")
+    qkv = torch.zeros(Rmu, W, device="cuda")
+    hbuf = torch.zeros(mu, H, device="cuda")
+    ncap = min(256, Rmu)
+
+    def router():
+        KD.router_topk(ptr(x), ptr(gamma), 1e-5, None, ptr(wr), mu, H, E, K, ptr(hn), None,
+                       ptr(idx), ptr(wts), s)
+        KD.moe_permute(ptr(idx), ptr(hn), mu, H, E, K, ptr(cnt), ptr(off), ptr(perm), ptr(inv),
+                       ptr(xp), R, s)
+
+    def expert():
+        KD.expert_ffn(ptr(xp), R, ptr(cnt), ptr(off), ptr(t13), ptr(t2), E, H, F, ncap,
+                      ptr(inter), ptr(y), ptr(inv), ptr(wts), ptr(hbuf), mu, K, ptr(xo), s)
+
+    def dense_qkv():
+        KD.rmsnorm_pack(ptr(x), ptr(gamma), mu, H, 1e-5, ptr(xn), Rmu, s)
+        g = capi.GemmArgs(a_table=tqkv.data_ptr(), n_mats=1, G=1, RB=W // 128, K=H,
+                          b=xn.data_ptr(), R=Rmu, rows_dense=mu, n_cap=ncap, epi=0, alpha=1.0,
+                          out_f32=qkv.data_ptr(), ldo=W)
+        KD.gemm(C.byref(g), s)
+
+    def dense_o():
+        g = capi.GemmArgs(a_table=to.data_ptr(), n_mats=1, G=1, RB=H // 128, K=H,
+                          b=xn.data_ptr(), R=Rmu, rows_dense=mu, n_cap=ncap, epi=0, alpha=1.0,
+                          out_f32=hbuf.data_ptr(), ldo=H, residual=x.data_ptr(), ldr=H)
+        KD.gemm(C.byref(g), s)
+
+    router()
+    torch.cuda.synchronize()
+    touched = int((cnt > 0).sum().item())
+    cases = [
+        ("router+permute", router, mu * H * 4 + E * H * 2 + mu * K * 2 * H * 2),
+        ("expert_ffn (gate/up+down+combine)", expert,
+         touched * 3 * H * F * 2 + mu * K * 2 * H * 2 + mu * H * 2),
+        ("qkv (norm+gemm)", dense_qkv, W * H * 2 + mu * H * 4),
+        ("o_proj (+residual)", dense_o, H * H * 2 + mu * H * 4 * 2),
+    ]
+    reps = 2 if a.once else a.reps
+    out = {}
+    for name, fn, nbytes in cases:
+        for _ in range(2 if not a.once else 0):
+            fn()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        st.record()
+        for _ in range(reps):
+            fn()
+        en.record()
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / reps
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "alg_bytes": nbytes, "GBps": gbs, "frac_hbm": gbs / peak}
+        print(f"{name:36s} mu={mu:4d} {ms * 1e3:9.1f} us  {nbytes / 1e6:9.1f} MB  "
+              f"{gbs:8.1f} GB/s  {100 * gbs / peak:5.1f}% of {peak} GB/s", flush=True)
+    print(json.dumps({"mu": mu, "touched_experts": touched, "kernels": out}))
+
+
+if __name__ == "__main__":
+    main()
