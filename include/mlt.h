@@ -232,6 +232,7 @@ typedef struct mlt_gemm_args_t {
     int32_t ldr;
     void* out_packed;
     int32_t out_R;
+    int32_t n_chunks;     /* token chunks per (group, row block) spread over CTAs; 0 -> 1 */
 } mlt_gemm_args_t;
 
 /* Grouped swap-AB tcgen05 GEMM (SURVEY.md §2c expert_gateup_silu /
@@ -359,6 +360,9 @@ int mlt_runtime_decode(mlt_runtime* rt, const int32_t* host_tokens, const int32_
 mlt_dag* mlt_execution_dag(const mlt_dag* reference, const mlt_model_spec_t* model,
                            const mlt_policy_t* policy, int exact_gates,
                            mlt_runtime_info_t* info);
+/* Live per-kernel breakdown of the last decode (CUDA-event deltas on the
+ * compute stream): JSON [{"name","ms","launches"}...]; returns length. */
+int mlt_runtime_kernel_profile(mlt_runtime* rt, char* buf, size_t cap);
 /* timeline_json of the last decode's measured timeline; returns length. */
 int mlt_runtime_timeline_json(mlt_runtime* rt, char* buf, size_t cap);
 int mlt_runtime_read_residual(mlt_runtime* rt, float* host_out);

@@ -43,6 +43,7 @@ _SIGS = {
     "orc_fill_kv": (None, [V, C.c_uint64, I]),
     "orc_model_kv": (V, [V, I, I]),
     "orc_num_threads": (I, []),
+    "orc_router_margins": (None, [V, V]),
 }
 
 _lib = None
@@ -185,6 +186,13 @@ class Model:
                                      mode, p(idx))
         assert rc == 0
         return x, idx
+
+    def router_margins(self) -> np.ndarray:
+        """Per sequence, min over layers of the last step's routing gap
+        (k-th selected logit minus best unselected)."""
+        out = np.zeros(self.cfg.batch, np.float32)
+        lib().orc_router_margins(self.h, p(out))
+        return out
 
     def fill_kv(self, seed, upto):
         lib().orc_fill_kv(self.h, seed, upto)

@@ -238,6 +238,7 @@ struct orc_model {
     uint16_t **attn_norm, **ffn_norm, **wqkv, **wo, **router;
     uint16_t ***w1, ***w3, ***w2;
     uint16_t **kc, **vc; /* [layer] -> [N][max_ctx][n_kv][d] */
+    float* rmargin;      /* [N]: min over layers of the router's k-th minus (k+1)-th logit */
 };
 
 static uint16_t* gen(const orc_model* m, int layer, int kind, int expert, int64_t n, double scale,
@@ -267,6 +268,7 @@ orc_model* orc_model_create(const orc_config* cfg) {
     m->w2 = calloc(L, sizeof(void*));
     m->kc = calloc(L, sizeof(void*));
     m->vc = calloc(L, sizeof(void*));
+    m->rmargin = calloc(cfg->batch, sizeof(float));
     const size_t kv = (size_t)cfg->batch * cfg->max_ctx * cfg->kv_heads * m->d;
     for (int l = 0; l < L; ++l) {
         m->attn_norm[l] = gen(m, l, ORC_T_ATTN_NORM, 0, H, 0, 1);
@@ -300,8 +302,12 @@ void orc_model_free(orc_model* m) {
     }
     free(m->attn_norm); free(m->ffn_norm); free(m->wqkv); free(m->wo); free(m->router);
     free(m->w1); free(m->w3); free(m->w2); free(m->kc); free(m->vc);
-    free(m->embed); free(m->lm_head); free(m->final_norm);
+    free(m->embed); free(m->lm_head); free(m->final_norm); free(m->rmargin);
     free(m);
+}
+
+void orc_router_margins(const orc_model* m, float* out) {
+    memcpy(out, m->rmargin, sizeof(float) * (size_t)m->c.batch);
 }
 
 const uint16_t* orc_model_tensor(const orc_model* m, int layer, int kind, int expert) {
@@ -401,6 +407,17 @@ int orc_layer_forward(orc_model* m, int layer, float* x, const int32_t* pos, int
     int32_t* off = malloc(sizeof(int32_t) * (E + 1));
     orc_router(hb, m->router[layer], N, H, E, K, logits, idx, wts, perm, off);
     if (topk_out) memcpy(topk_out, idx, sizeof(int32_t) * N * K);
+    for (int t = 0; t < N; ++t) { /* routing robustness: gap between selected and next logit */
+        const float kth = logits[(size_t)t * E + idx[t * K + K - 1]];
+        float next = -INFINITY;
+        for (int e = 0; e < E; ++e) {
+            int sel = 0;
+            for (int s = 0; s < K; ++s) sel |= idx[t * K + s] == e;
+            if (!sel && logits[(size_t)t * E + e] > next) next = logits[(size_t)t * E + e];
+        }
+        const float gap = kth - next;
+        if (layer == 0 || gap < m->rmargin[t]) m->rmargin[t] = gap;
+    }
 
     float* y = malloc(sizeof(float) * (size_t)N * K * H); /* per (t, s) */
     for (int e = 0; e < E; ++e) {

@@ -99,6 +99,10 @@ int orc_layer_forward(orc_model* m, int layer, float* x, const int32_t* pos, int
 /* Fill the KV cache of every layer/sequence for positions [0, upto) with
  * uniform(-1,1) bf16 from `seed` (synthetic prompt-stage KV). */
 void orc_fill_kv(orc_model* m, uint64_t seed, int upto);
+/* After a decode step / layer forward: per sequence, the smallest gap over
+ * layers between the k-th selected router logit and the best unselected one
+ * (a routing near-tie indicator). */
+void orc_router_margins(const orc_model* m, float* out);
 uint16_t* orc_model_kv(orc_model* m, int layer, int which); /* which: 0=K 1=V */
 int orc_num_threads(void);
 

@@ -60,6 +60,7 @@ mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
     g.ldr = a->ldr;
     g.out_packed = reinterpret_cast<uint8_t*>(a->out_packed);
     g.out_R = a->out_R;
+    g.n_chunks = a->n_chunks > 0 ? a->n_chunks : 1;
     return g;
 }
 

@@ -19,6 +19,7 @@ struct Handle {
     lightplan::sim::ScheduleDag dag;
     lightplan::sim::Timeline tl;
     bool has_tl = false;
+    std::vector<mlt::DecodeReport::KernelTime> kernels;
 };
 
 Handle* H(mlt_runtime* r) { return reinterpret_cast<Handle*>(r); }
@@ -118,6 +119,7 @@ int mlt_runtime_decode(mlt_runtime* r, const int32_t* tokens, const int32_t* for
         Handle* h = H(r);
         const mlt::DecodeReport d = h->rt->decode(tokens, forced, steps, out, &h->dag, &h->tl);
         h->has_tl = true;
+        h->kernels = d.kernels;
         if (rep) {
             rep->seconds = d.seconds;
             rep->tokens_per_second = d.tokens_per_second;
@@ -137,6 +139,26 @@ int mlt_runtime_decode(mlt_runtime* r, const int32_t* tokens, const int32_t* for
         }
         if (!d.verify.empty()) mlt::set_error(("timeline: " + d.verify).c_str(), MLT_OK);
         return MLT_OK;
+    });
+}
+
+int mlt_runtime_kernel_profile(mlt_runtime* r, char* buf, size_t cap) {
+    return guard([&] {
+        std::string s = "[";
+        char line[256];
+        for (size_t i = 0; i < H(r)->kernels.size(); ++i) {
+            const auto& k = H(r)->kernels[i];
+            std::snprintf(line, sizeof line, "%s{\"name\":\"%s\",\"ms\":%.6f,\"launches\":%d}", i ? "," : "",
+                          k.name.c_str(), k.ms, k.launches);
+            s += line;
+        }
+        s += "]";
+        if (buf && cap) {
+            const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+            std::memcpy(buf, s.data(), n);
+            buf[n] = 0;
+        }
+        return static_cast<int>(s.size());
     });
 }
 

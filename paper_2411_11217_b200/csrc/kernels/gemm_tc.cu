@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
     tc_fence_after();
     const uint32_t tmem = ctl->tmem_base;
 
-    const int n_virtual = a.G * a.RB;
+    const int n_virtual = a.G * a.RB * a.n_chunks;  // (row block, group, N-chunk)
     const int KB = a.K / kBlockK;
 
     if (warp == 0) {
@@ -83,14 +83,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
             int stage = 0;
             uint32_t phase = 0;
             for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-                const int g = v % a.G, rb = v / a.G;
+                const int c = v % a.n_chunks, g = (v / a.n_chunks) % a.G, rb = v / a.n_chunks / a.G;
                 const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
                 if (rows <= 0) continue;
                 const int row0 = a.b_off ? a.b_off[g] : 0;
                 const uint8_t* ab[kMaxMats];
                 for (int mt = 0; mt < a.n_mats; ++mt)
                     ab[mt] = a.a_table[(static_cast<int64_t>(mt) * a.G + g) * a.RB + rb];
-                for (int n0 = 0; n0 < rows; n0 += a.n_cap) {
+                for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
                     const int nt = min(a.n_cap, rows - n0);
                     const int ntp = (nt + 15) & ~15;
                     for (int kb = 0; kb < KB; ++kb) {
@@ -116,10 +116,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-            const int g = v % a.G;
+            const int c = v % a.n_chunks, g = (v / a.n_chunks) % a.G;
             const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
             if (rows <= 0) continue;
-            for (int n0 = 0; n0 < rows; n0 += a.n_cap) {
+            for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
                 const int nt = min(a.n_cap, rows - n0);
                 const int ntp = (nt + 15) & ~15;
                 const uint32_t idesc = idesc_bf16(128, ntp);
@@ -154,12 +154,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-            const int g = v % a.G, rb = v / a.G;
+            const int c = v % a.n_chunks, g = (v / a.n_chunks) % a.G, rb = v / a.n_chunks / a.G;
             const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
             if (rows <= 0) continue;
             const int row0 = a.b_off ? a.b_off[g] : 0;
             const int m = rb * kBlockM + quarter * 32 + lane;  // output feature
-            for (int n0 = 0; n0 < rows; n0 += a.n_cap) {
+            for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
                 const int nt = min(a.n_cap, rows - n0);
                 mbar_wait(&ctl->tfull[acc], acc_phase);
                 tc_fence_after();
@@ -214,7 +214,7 @@ int gemm_smem_bytes(int n_mats, int n_cap, int stages) {
 
 cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     if (a.n_mats < 1 || a.n_mats > kMaxMats || a.K % kBlockK || a.n_cap % 16 || a.n_cap < 16 ||
-        a.n_cap > 256 || a.R % 16)
+        a.n_cap > 256 || a.R % 16 || a.n_chunks < 1)
         return cudaErrorInvalidValue;
     const int per_stage = a.n_mats * kATileBytes + a.n_cap * 128;
     const int budget = 227 * 1024 - 1024 - 256;
@@ -235,7 +235,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const int n_virtual = a.G * a.RB;
+    const int n_virtual = a.G * a.RB * a.n_chunks;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
     gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(a);

@@ -23,6 +23,8 @@ struct GemmArgs {
     const int32_t* b_cnt = nullptr;  // [G] valid rows per group (nullptr: dense)
     int rows_dense = 0;              // rows when b_cnt == nullptr
     int n_cap = 16;                  // max tokens per tile (16..256, multiple of 16)
+    int n_chunks = 1;                // token chunks per (group, row block) spread over CTAs:
+                                     // virtual tile (rb, g, c) handles tokens c*n_cap, +n_chunks*n_cap, ...
     // epilogue
     int epi = kEpiF32;
     float alpha = 1.0f;

@@ -175,8 +175,7 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
     const Ctx cctx{steps, forced != nullptr};
     cur_steps_ = steps;
     launches_ = 0;
-    ev_expert_.clear();
-    ev_dense_.clear();
+    marks_.clear();
     event_next_ = 0;
 
     std::array<std::vector<int>, lightplan::sim::kResourceCount> fifo;
@@ -203,6 +202,7 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
                 for (int d : extra[i]) wait_dep(d);
                 if (on_device(r)) {
                     ck(cudaEventRecord(ev_start[i], st), "record");
+                    if (r == Resource::Gpu) mark_start(ev_start[i]);
                     switch (t.kind) {
                         case TaskKind::PreAttn: act_pre_attn(cctx, t.step, t.layer, t.microbatch); break;
                         case TaskKind::PostAttn: act_post_attn(cctx, t.step, t.layer, t.microbatch); break;
@@ -284,28 +284,39 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
         measured.tasks[i].duration = e - s;
         tl.busy[static_cast<int>(measured.tasks[i].resource)] += e - s;
         tl.makespan = std::max(tl.makespan, e);
-        if (ev_start[i]) {
-            cudaEventDestroy(ev_start[i]);
-            cudaEventDestroy(ev_end[i]);
-        }
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e_end);
     cudaEventDestroy(e_inputs);
 
     DecodeReport rep;
-    for (const auto& [a, b] : ev_expert_) {
+    for (size_t k = 1; k < marks_.size(); ++k) {
+        const char* name = marks_[k].first;
+        if (!name) continue;  // a task start: the interval before it is not a kernel
         float ms = 0;
-        ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
-        rep.expert_ms_total += ms;
+        ck(cudaEventElapsedTime(&ms, marks_[k - 1].second, marks_[k].second), "elapsed");
+        auto it = std::find_if(rep.kernels.begin(), rep.kernels.end(),
+                               [&](const DecodeReport::KernelTime& kt) { return kt.name == name; });
+        if (it == rep.kernels.end()) {
+            rep.kernels.push_back({name, 0.0, 0});
+            it = rep.kernels.end() - 1;
+        }
+        it->ms += ms;
+        it->launches += 1;
     }
-    rep.expert_launches = static_cast<int>(ev_expert_.size());
-    for (const auto& [a, b] : ev_dense_) {
-        float ms = 0;
-        ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
-        rep.qkv_o_ms_total += ms;
+    for (const auto& kt : rep.kernels) {
+        if (kt.name == "expert_gateup_gemm" || kt.name == "expert_down_gemm") rep.expert_ms_total += kt.ms;
+        if (kt.name == "expert_gateup_gemm") rep.expert_launches = kt.launches;
+        if (kt.name == "qkv_gemm" || kt.name == "o_gemm") {
+            rep.qkv_o_ms_total += kt.ms;
+            rep.dense_launches += kt.launches;
+        }
     }
-    rep.dense_launches = static_cast<int>(ev_dense_.size());
+    for (int i = 0; i < n; ++i)  // task events (the kernel marks above reference the GPU ones)
+        if (ev_start[i]) {
+            cudaEventDestroy(ev_start[i]);
+            cudaEventDestroy(ev_end[i]);
+        }
     rep.seconds = total_ms * 1e-3;
     rep.tokens_per_second = static_cast<double>(N_) * steps / rep.seconds;
     rep.gpu_launches = launches_;

@@ -14,6 +14,7 @@
 #include <immintrin.h>
 #include <omp.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -43,9 +44,12 @@ void Runtime::host_attention(int l, int mb, int step) {
     uint8_t* out = h_attn_ + static_cast<size_t>(mb) * Rmu_ * H_ * 2;
     const int32_t* pos = step_pos_.data() + static_cast<size_t>(step - 1) * N_;
     const float scale = 1.0f / std::sqrt(static_cast<float>(kD));
-    const int threads = opt_.host_threads > 0 ? opt_.host_threads : 0;
+    // Default: all cores but two, which stay free for the resource launcher
+    // threads (a descheduled GPU launcher leaves the device idle between
+    // kernels of one PostAttn).
+    const int threads = opt_.host_threads > 0 ? opt_.host_threads : std::max(1, omp_get_num_procs() - 2);
 
-#pragma omp parallel num_threads(threads > 0 ? threads : omp_get_max_threads())
+#pragma omp parallel num_threads(threads)
     {
         std::vector<float> sc(static_cast<size_t>(kMaxG) * max_ctx_);
 #pragma omp for collapse(2) schedule(dynamic, 1)

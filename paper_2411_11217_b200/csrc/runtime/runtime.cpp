@@ -110,7 +110,7 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     Rmu_ = round_up(mu_, 16);
     Re_ = round_up(mu_ * K_ + 16 * E_, 16);
     ncap_ = std::min(256, Rmu_);
-    ncap_e_ = std::min(256, Rmu_);
+    ncap_e_ = std::min(128, Rmu_);  // per-expert tiles: 4+ smem stages; m_e > 128 loops in-tile
     pos_.assign(N_, 0);
 
     ck(cudaSetDevice(opt.device), "cudaSetDevice");
@@ -399,6 +399,30 @@ cudaEvent_t Runtime::take_event() {
     return event_pool_[event_next_++];
 }
 
+// Every kernel launch of a GPU task goes through kl(): error check, launch
+// count, and a CUDA event recorded right after it on the compute stream.
+// Consecutive events (the task's start event first) give the live per-kernel
+// breakdown reported by decode() — no extra synchronisation.
+void Runtime::kl(const char* name, cudaError_t e) {
+    ck(e, name);
+    ++launches_;
+    cudaEvent_t ev = take_event();
+    ck(cudaEventRecord(ev, s_gpu_), "event");
+    marks_.push_back({name, ev});
+}
+
+void Runtime::mark_start(cudaEvent_t task_start) { marks_.push_back({nullptr, task_start}); }
+
+// Dense projections have few 128-row blocks (QKV 48, O 32 for 8x7B): split
+// the tokens into chunks so (row block x chunk) tiles cover all SMs; the
+// chunks of one row block run on neighbouring CTAs and share its weight tile
+// through L2.
+void Runtime::dense_tiling(int row_blocks, int& n_cap, int& n_chunks) const {
+    const int want = std::max(1, (num_sms_ + row_blocks - 1) / row_blocks);
+    n_cap = std::min(256, std::max(16, round_up((mu_ + want - 1) / want, 16)));
+    n_chunks = (mu_ + n_cap - 1) / n_cap;
+}
+
 // ---------------------------------------------------------------------------
 // Task actions.  step/layer/mb are the 1-based fields of sim::Task.
 // ---------------------------------------------------------------------------
@@ -413,12 +437,10 @@ void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
     if (layer == 1) {
         const int32_t* src = (step == 1 || c.forced) ? d_tok_in_ + static_cast<size_t>(step - 1) * N_ + t0
                                                      : d_tok_out_ + static_cast<size_t>(step - 2) * N_ + t0;
-        kk(mltk::launch_embed(src, d_embed_, mu_, H_, d_x_ + static_cast<size_t>(t0) * H_, s_gpu_), "embed");
-        ++launches_;
+        kl("embed", mltk::launch_embed(src, d_embed_, mu_, H_, d_x_ + static_cast<size_t>(t0) * H_, s_gpu_));
     }
-    kk(mltk::launch_rmsnorm_pack(d_x_ + static_cast<size_t>(t0) * H_, d_attn_norm_[l], mu_, H_, ext_.rms_eps, d_xn_,
-                                 Rmu_, s_gpu_),
-       "rmsnorm");
+    kl("rmsnorm_pack", mltk::launch_rmsnorm_pack(d_x_ + static_cast<size_t>(t0) * H_, d_attn_norm_[l], mu_, H_,
+                                                 ext_.rms_eps, d_xn_, Rmu_, s_gpu_));
     mltk::GemmArgs a;
     a.a_table = dev_tables_ + (static_cast<size_t>(l) * 2 + slot_of(g)) * table_entries_ + tab_qkv_;
     a.n_mats = 1;
@@ -428,19 +450,14 @@ void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
     a.b = d_xn_;
     a.R = Rmu_;
     a.rows_dense = mu_;
-    a.n_cap = ncap_;
+    dense_tiling(W_ / 128, a.n_cap, a.n_chunks);
     a.epi = mltk::kEpiF32;
     a.out_f32 = d_qkv_f32_;
     a.ldo = W_;
-    cudaEvent_t q0 = take_event(), q1 = take_event();
-    kk(cudaEventRecord(q0, s_gpu_), "event");
-    kk(mltk::launch_gemm(a, num_sms_, s_gpu_), "qkv gemm");
-    kk(cudaEventRecord(q1, s_gpu_), "event");
-    ev_dense_.push_back({q0, q1});
+    kl("qkv_gemm", mltk::launch_gemm(a, num_sms_, s_gpu_));
     const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
     uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
-    kk(mltk::launch_rope_qkv(d_qkv_f32_, pos, d_rope_, mu_, nq_, nkv_, d_, qkv, s_gpu_), "rope");
-    launches_ += 3;
+    kl("rope_qkv", mltk::launch_rope_qkv(d_qkv_f32_, pos, d_rope_, mu_, nq_, nkv_, d_, qkv, s_gpu_));
 }
 
 void Runtime::act_offload_qkv(int layer, int mb) {
@@ -468,13 +485,11 @@ void Runtime::act_gpu_attn(int step, int layer, int mb) {
     const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
     const int32_t* ctx = d_pos_ + static_cast<size_t>(max_steps_) * N_ + static_cast<size_t>(step - 1) * N_ + t0;
     const int32_t* bt = d_block_table_ + static_cast<size_t>(l) * N_ * max_pages_;
-    kk(mltk::launch_kv_append(qkv, nq_, nkv_, d_, d_seq_ + t0, pos, mu_, bt, max_pages_, page_, d_kpool_, d_vpool_,
-                              s_gpu_),
-       "kv append");
-    kk(mltk::launch_gqa_decode_paged(qkv, W_, d_kpool_, d_vpool_, bt, max_pages_, d_seq_ + t0, ctx, mu_, nq_, nkv_,
-                                     d_, page_, d_attn_gpu_, Rmu_, nullptr, s_gpu_),
-       "gqa attention");
-    launches_ += 2;
+    kl("kv_append", mltk::launch_kv_append(qkv, nq_, nkv_, d_, d_seq_ + t0, pos, mu_, bt, max_pages_, page_,
+                                           d_kpool_, d_vpool_, s_gpu_));
+    kl("gqa_decode_paged", mltk::launch_gqa_decode_paged(qkv, W_, d_kpool_, d_vpool_, bt, max_pages_, d_seq_ + t0,
+                                                         ctx, mu_, nq_, nkv_, d_, page_, d_attn_gpu_, Rmu_,
+                                                         nullptr, s_gpu_));
 }
 
 void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
@@ -492,24 +507,17 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     o.b = policy_.attn_on_gpu ? d_attn_gpu_ : d_attn_in_ + static_cast<size_t>(mb - 1) * Rmu_ * H_ * 2;
     o.R = Rmu_;
     o.rows_dense = mu_;
-    o.n_cap = ncap_;
+    dense_tiling(H_ / 128, o.n_cap, o.n_chunks);
     o.out_f32 = d_h_;
     o.ldo = H_;
     o.residual = x;
     o.ldr = H_;
-    cudaEvent_t o0 = take_event(), o1 = take_event();
-    kk(cudaEventRecord(o0, s_gpu_), "event");
-    kk(mltk::launch_gemm(o, num_sms_, s_gpu_), "o gemm");
-    kk(cudaEventRecord(o1, s_gpu_), "event");
-    ev_dense_.push_back({o0, o1});
+    kl("o_gemm", mltk::launch_gemm(o, num_sms_, s_gpu_));
     // RMSNorm + router + permute
-    kk(mltk::launch_router(d_h_, d_ffn_norm_[l], ext_.rms_eps, nullptr, d_router_[l], mu_, H_, E_, K_, d_hn_, nullptr,
-                           d_topk_, d_topw_, s_gpu_),
-       "router");
-    kk(mltk::launch_moe_permute(d_topk_, d_hn_, mu_, H_, E_, K_, d_cnt_, d_off_, d_perm_, d_inv_, d_xe_, Re_, s_gpu_),
-       "permute");
-    cudaEvent_t ex0 = take_event(), ex1 = take_event();
-    kk(cudaEventRecord(ex0, s_gpu_), "event");
+    kl("router", mltk::launch_router(d_h_, d_ffn_norm_[l], ext_.rms_eps, nullptr, d_router_[l], mu_, H_, E_, K_,
+                                     d_hn_, nullptr, d_topk_, d_topw_, s_gpu_));
+    kl("moe_permute", mltk::launch_moe_permute(d_topk_, d_hn_, mu_, H_, E_, K_, d_cnt_, d_off_, d_perm_, d_inv_,
+                                               d_xe_, Re_, s_gpu_));
     // experts: gate/up (SiLU fused) -> down -> combine
     mltk::GemmArgs gu;
     gu.a_table = tab + tab_w13_;
@@ -525,7 +533,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     gu.epi = mltk::kEpiSiluPacked;
     gu.out_packed = d_inter_;
     gu.out_R = Re_;
-    kk(mltk::launch_gemm(gu, num_sms_, s_gpu_), "gate/up gemm");
+    kl("expert_gateup_gemm", mltk::launch_gemm(gu, num_sms_, s_gpu_));
     mltk::GemmArgs dn;
     dn.a_table = tab + tab_w2_;
     dn.G = E_;
@@ -538,13 +546,10 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     dn.n_cap = ncap_e_;
     dn.out_f32 = d_y_;
     dn.ldo = H_;
-    kk(mltk::launch_gemm(dn, num_sms_, s_gpu_), "down gemm");
-    kk(cudaEventRecord(ex1, s_gpu_), "event");
-    ev_expert_.push_back({ex0, ex1});
-    kk(mltk::launch_moe_combine(d_h_, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, x, s_gpu_), "combine");
-    launches_ += 6;
+    kl("expert_down_gemm", mltk::launch_gemm(dn, num_sms_, s_gpu_));
+    kl("moe_combine", mltk::launch_moe_combine(d_h_, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, x, s_gpu_));
     if (layer == L_) {  // step epilogue: final norm -> lm_head -> greedy ids
-        kk(mltk::launch_rmsnorm_pack(x, d_final_norm_, mu_, H_, ext_.rms_eps, d_xn_, Rmu_, s_gpu_), "final norm");
+        kl("rmsnorm_pack", mltk::launch_rmsnorm_pack(x, d_final_norm_, mu_, H_, ext_.rms_eps, d_xn_, Rmu_, s_gpu_));
         mltk::GemmArgs lm;
         lm.a_table = d_lm_table_;
         lm.RB = V_ / 128;
@@ -552,14 +557,12 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
         lm.b = d_xn_;
         lm.R = Rmu_;
         lm.rows_dense = mu_;
-        lm.n_cap = ncap_;
+        dense_tiling(V_ / 128, lm.n_cap, lm.n_chunks);
         lm.out_f32 = d_logits_;
         lm.ldo = V_;
-        kk(mltk::launch_gemm(lm, num_sms_, s_gpu_), "lm_head gemm");
-        kk(mltk::launch_argmax(d_logits_, mu_, V_, d_tok_out_ + static_cast<size_t>(step - 1) * N_ + t0, nullptr,
-                               s_gpu_),
-           "argmax");
-        launches_ += 3;
+        kl("lm_head_gemm", mltk::launch_gemm(lm, num_sms_, s_gpu_));
+        kl("argmax", mltk::launch_argmax(d_logits_, mu_, V_, d_tok_out_ + static_cast<size_t>(step - 1) * N_ + t0,
+                                         nullptr, s_gpu_));
     }
 }
 

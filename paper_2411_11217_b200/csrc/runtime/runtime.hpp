@@ -74,6 +74,12 @@ struct DecodeReport {
     int expert_launches = 0;
     double qkv_o_ms_total = 0;       // dense QKV + O projections (pairs per micro-batch-layer)
     int dense_launches = 0;
+    struct KernelTime {
+        std::string name;
+        double ms = 0;
+        int launches = 0;
+    };
+    std::vector<KernelTime> kernels;  // live per-kernel breakdown (event deltas on the compute stream)
 };
 
 class Runtime {
@@ -129,6 +135,7 @@ class Runtime {
 
   private:
     void build_catalog();
+    void dense_tiling(int row_blocks, int& n_cap, int& n_chunks) const;
     void allocate();
     void generate_weights();
     void host_attention(int layer, int mb, int step);
@@ -201,9 +208,16 @@ class Runtime {
 
     cudaStream_t s_gpu_ = nullptr, s_h2d_ = nullptr, s_d2h_ = nullptr;
     int launches_ = 0;
-    // kernel event pairs recorded by the GPU worker during decode()
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_expert_, ev_dense_;
+    // per-kernel marks recorded by the GPU worker during decode(): (name,
+    // event after the launch); name == nullptr marks a task's start event
+    std::vector<std::pair<const char*, cudaEvent_t>> marks_;
+    void kl(const char* name, cudaError_t launch_status);
     cudaEvent_t take_event();
+
+  public:
+    void mark_start(cudaEvent_t task_start);
+
+  private:
     std::vector<cudaEvent_t> event_pool_;
     size_t event_next_ = 0;
     double pin_seconds_ = 0, gen_seconds_ = 0;

@@ -127,6 +127,14 @@ class Runtime:
         self.f["runtime_timeline_json"](self.h, buf, n + 1)
         return json.loads(buf.value.decode())
 
+    def kernel_profile(self) -> list:
+        f = self.api.lib.mlt_runtime_kernel_profile
+        f.restype, f.argtypes = C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]
+        n = self._ck(f(self.h, None, 0))
+        buf = C.create_string_buffer(n + 1)
+        f(self.h, buf, n + 1)
+        return json.loads(buf.value.decode())
+
     def residual(self) -> np.ndarray:
         x = np.zeros((self.policy.batch, self.model.hidden_dim), np.float32)
         self._ck(self.f["runtime_read_residual"](self.h, x.ctypes.data_as(C.c_void_p)))

@@ -1,19 +1,27 @@
 """End-to-end decode on the B200 through the runtime C ABI vs the CPU oracle
-(BASELINE.json correctness items 2 and 3; config 1 "Tiny": l=2, h1=1024,
-h2=3584, n_q=8, n_kv=2, n_e=8, k=2, vocab 32000, N=8, mu=4, prompt 16 +
-32 greedy steps, weights seed 1234, prompt seed 5678).
+(BASELINE.json correctness items 2 and 3).
+
+Configs: "Tiny" (BASELINE configs[0]: l=2, h1=1024, h2=3584, n_q=8, n_kv=2,
+n_e=8, k=2, vocab 32000) and the reduced-depth 8x7B-width model of SURVEY
+§8c (l=2, h1=4096, h2=14336, n_q=32, n_kv=8).  N=8 sequences, mu=4, a
+16-token prompt (seed 5678) + 32 greedy steps, weights seed 1234.
 
 Greedy parity.  The GPU keeps activations in bf16 between kernels and its
-tensor cores accumulate with ~4e-6 relative error (measured,
-tools/diag_gemm.py), so values sitting on a bf16 rounding boundary flip one
-ulp against any CPU reference; the resulting logit noise is ~1e-3 of the
-logit scale.  The test therefore runs both sides FREE-RUNNING for 32 steps
-and requires every divergence to start at a step whose oracle top1-top2
-margin is below NEAR_TIE (a genuine near-tie; a real bug diverges at large
-margins and fails), plus a sanity floor of half the sequences identical for
-all 32 steps (measured: 6/8 at seed 5678, both divergences at margins
-< 0.02).  The per-stage test below pins each kernel boundary bit-for-bit or
-to ~1e-5 on identical inputs.
+tensor cores accumulate with ~4e-6 relative error (tools/diag_gemm.py), so
+values on a bf16 rounding boundary flip one ulp against any CPU reference;
+the residual drifts ~3e-3 from the bf16-faithful oracle.  That flips two
+kinds of genuinely tied decisions: lm-head argmax near-ties and router
+top-k near-ties (a flipped expert moves that token's residual by 10-30%).
+So greedy parity is checked TEACHER-FORCED (the GPU decodes the oracle's own
+greedy tokens, so one tie cannot cascade) and every discrepancy must be
+attributable:
+  * each greedy id equals the oracle's, unless the oracle's top1-top2 logit
+    margin is < LM_TIE or a router near-tie (< ROUTER_TIE) occurred for that
+    sequence at that step;
+  * each per-step residual is within 1e-2 (relative) of the oracle, unless a
+    router near-tie occurred at that step.
+A real bug fails both (large margins, no ties).  The free-running 32-step
+comparison is printed for information.
 """
 import ctypes as C
 
@@ -29,16 +37,10 @@ from paper_2411_11217_b200 import capi  # noqa: E402
 from paper_2411_11217_b200.runtime import Runtime  # noqa: E402
 
 N, MU, PROMPT, GEN, VOCAB = 8, 4, 16, 32, 32000
-NEAR_TIE = 0.05  # logit units; logits have std ~4 (lm_head_scale 4)
-
-
-def tiny_model(layers=2):
-    return capi.ModelSpec(layers, 1024, 3584, 8, 2, 8, 2, 2.0, 2.0)
-
-
-def oracle_model(layers=2, batch=N):
-    from oracle import bind as orc
-    return orc.Model(layers, 1024, 3584, 8, 2, 8, 2, VOCAB, batch, 64, seed=1234)
+LM_TIE = 0.05      # logit units; logits have std ~4 (lm_head_scale 4)
+ROUTER_TIE = 0.02  # router logit units (std ~1)
+TINY = (1024, 3584, 8, 2)
+W8X7B = (4096, 14336, 32, 8)
 
 
 @pytest.fixture(scope="module")
@@ -46,60 +48,101 @@ def prompt():
     return np.random.default_rng(5678).integers(0, VOCAB, size=(PROMPT, N), dtype=np.int32)
 
 
-@pytest.fixture(scope="module")
-def oracle_run(prompt):
+def _model(dims, layers=2):
+    h1, h2, nq, nkv = dims
+    return capi.ModelSpec(layers, h1, h2, nq, nkv, 8, 2, 2.0, 2.0)
+
+
+def _oracle(dims, layers=2):
     from oracle import bind as orc
-    m = oracle_model()
-    ids, margins = [], []
+    h1, h2, nq, nkv = dims
+    return orc.Model(layers, h1, h2, nq, nkv, 8, 2, VOCAB, N, 64, seed=1234)
+
+
+def teacher_forced_parity(dims, prompt, r_w, a_g, budget):
+    from oracle import bind as orc
+    ref = _oracle(dims)
+    rt = Runtime(_model(dims), capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0),
+                 budget_bytes=budget, max_ctx=64, vocab=VOCAB, seed=1234)
+    steps = PROMPT + GEN - 1
+    tok = prompt[0]
+    events = {"lm_tie": 0, "router_tie": 0, "ids": 0}
+    worst_clean = 0.0
+    for s in range(steps):
+        tok = prompt[s] if s < PROMPT else tok
+        nxt, lm_margin, x_ref = ref.decode_step(tok, np.full(N, s, np.int32), orc.FAITHFUL, want_x=True)
+        r_margin = ref.router_margins()
+        out = rt.decode(tok, 1)
+        assert out.report.timeline_ok == 1
+        x = rt.residual()
+        rel = np.linalg.norm(x - x_ref, axis=1) / np.linalg.norm(x_ref, axis=1)
+        for q in range(N):
+            router_tie = r_margin[q] < ROUTER_TIE
+            events["router_tie"] += int(router_tie)
+            if not router_tie:
+                worst_clean = max(worst_clean, rel[q])
+                assert rel[q] <= 1e-2, (s, q, rel[q], r_margin[q])
+            if s >= PROMPT - 1 and out.ids[0][q] != nxt[q]:
+                events["ids"] += 1
+                explained = lm_margin[q] < LM_TIE or router_tie
+                events["lm_tie"] += int(lm_margin[q] < LM_TIE)
+                assert explained, (f"step {s} seq {q}: id {out.ids[0][q]} vs oracle {nxt[q]} at lm "
+                                   f"margin {lm_margin[q]:.3f}, router margin {r_margin[q]:.3f}")
+        tok = nxt
+    return rt, events, worst_clean
+
+
+def free_running(dims, prompt, r_w, a_g, budget):
+    from oracle import bind as orc
+    ref = _oracle(dims)
+    ids = []
     tok = prompt[0]
     for s in range(PROMPT + GEN - 1):
         tok = prompt[s] if s < PROMPT else tok
-        nxt, mg = m.decode_step(tok, np.full(N, s, np.int32), orc.FAITHFUL)
+        nxt, _ = ref.decode_step(tok, np.full(N, s, np.int32), orc.FAITHFUL)
         if s >= PROMPT - 1:
             ids.append(nxt)
-            margins.append(mg)
         tok = nxt
-    return np.array(ids), np.array(margins)
-
-
-def run_gpu(prompt, r_w, a_g):
-    pol = capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0)
-    rt = Runtime(tiny_model(), pol, budget_bytes=4e9, max_ctx=64, vocab=VOCAB, seed=1234)
+    rt = Runtime(_model(dims), capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0),
+                 budget_bytes=budget, max_ctx=64, vocab=VOCAB, seed=1234)
     first = rt.decode(prompt[0], PROMPT, forced=prompt)
     rest = rt.decode(first.ids[-1], GEN - 1)
-    return rt, first, rest, np.array([first.ids[-1]] + list(rest.ids))
+    gen = np.array([first.ids[-1]] + list(rest.ids))
+    ids = np.array(ids)
+    first_div = [int(np.nonzero(gen[:, q] != ids[:, q])[0][0]) if (gen[:, q] != ids[:, q]).any()
+                 else GEN for q in range(N)]
+    return rt, first, rest, first_div
 
 
 @pytest.mark.parametrize("r_w,a_g", [(0.0, 0), (0.5, 0), (1.0, 1)])
-def test_tiny_greedy_32_steps(prompt, oracle_run, r_w, a_g):
-    ref, margins = oracle_run
-    rt, first, rest, gen = run_gpu(prompt, r_w, a_g)
+def test_tiny_greedy(prompt, r_w, a_g):
+    rt, ev, worst = teacher_forced_parity(TINY, prompt, r_w, a_g, 4e9)
+    print(f"\n[tiny r_w={r_w} A_g={a_g}] teacher-forced: {ev}, worst residual "
+          f"(no router tie) {worst:.2e}")
+    assert ev["ids"] <= 4
+    rt2, first, rest, div = free_running(TINY, prompt, r_w, a_g, 4e9)
+    print(f"[tiny r_w={r_w} A_g={a_g}] free-running first divergence step per sequence: {div}")
     assert first.report.timeline_ok == 1 and rest.report.timeline_ok == 1
-    exact = 0
-    for s in range(N):
-        bad = np.nonzero(gen[:, s] != ref[:, s])[0]
-        if bad.size == 0:
-            exact += 1
-            continue
-        k = bad[0]
-        assert margins[k, s] < NEAR_TIE, (
-            f"seq {s} diverges at step {k} with oracle margin {margins[k, s]:.4f} >= {NEAR_TIE}")
-    print(f"\n[greedy] r_w={r_w} A_g={a_g}: {exact}/8 sequences identical for 32 steps; "
-          f"min oracle margin {margins.min():.4f}")
-    assert exact >= N // 2  # sanity floor; the near-tie check above is the real gate
     # paging volume: every step streams each layer's non-resident blocks once
-    info = rt.info
+    info = rt2.info
     layer_bytes = 2 * 1024 * 1536 + 2 * 1024 * 1024 + 8 * 3 * 1024 * 3584 * 2 + 8 * 1024 * 2
     # residency is decided per 128-row block: at most one block (128 x h2 x 2 B) short
     assert info.streamed_bytes_per_layer <= (1 - r_w) * layer_bytes + 128 * 3584 * 2
     assert rest.report.h2d_weight_bytes == pytest.approx((GEN - 1) * 2 * info.streamed_bytes_per_layer)
 
 
+def test_8x7b_width_reduced_depth_greedy(prompt):
+    """Reduced-depth 8x7B-width model paged at r_w=0.10 under a 7 GB cap."""
+    rt, ev, worst = teacher_forced_parity(W8X7B, prompt, 0.10, 0, 7e9)
+    print(f"\n[8x7B-width l=2] teacher-forced: {ev}, worst residual (no router tie) {worst:.2e}")
+    assert ev["ids"] <= 6
+
+
 def test_tiny_layer_output_within_2e2_of_fp32(prompt):
     """BASELINE item 2: layer outputs within 2e-2 relative (bf16 GPU vs fp32 CPU)."""
     from oracle import bind as orc
-    m = oracle_model()
-    rt = Runtime(tiny_model(), capi.Policy(N, MU, 0, 1, 0.25, 0.0), budget_bytes=4e9,
+    m = _oracle(TINY)
+    rt = Runtime(_model(TINY), capi.Policy(N, MU, 0, 1, 0.25, 0.0), budget_bytes=4e9,
                  max_ctx=64, vocab=VOCAB, seed=1234)
     worst = 0.0
     for s in range(4):
@@ -116,9 +159,9 @@ def test_one_layer_stage_by_stage():
     ulps, router indices exact, fp32 outputs ~1e-5."""
     from oracle import bind as orc
     KD = capi.load_kernels()
-    H, E, Kk = 1024, 8, 2
-    m = oracle_model(layers=1)
-    rt = Runtime(tiny_model(layers=1), capi.Policy(N, N, 0, 1, 0.0, 0.0), budget_bytes=4e9,
+    H, Kk = 1024, 2
+    m = _oracle(TINY, layers=1)
+    rt = Runtime(_model(TINY, layers=1), capi.Policy(N, N, 0, 1, 0.0, 0.0), budget_bytes=4e9,
                  max_ctx=64, vocab=VOCAB)
     toks = np.array([5, 17, 300, 4000, 12345, 31999, 7, 8], np.int32)
     rt.decode(toks, 1)
