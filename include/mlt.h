@@ -233,6 +233,8 @@ typedef struct mlt_gemm_args_t {
     void* out_packed;
     int32_t out_R;
     int32_t n_chunks;     /* token chunks per (group, row block) spread over CTAs; 0 -> 1 */
+    int32_t k_splits;     /* split-K: partial s written at out_f32 + s*split_stride; 0 -> 1 */
+    int64_t split_stride; /* floats between partial outputs (residual ignored when split) */
 } mlt_gemm_args_t;
 
 /* Grouped swap-AB tcgen05 GEMM (SURVEY.md §2c expert_gateup_silu /

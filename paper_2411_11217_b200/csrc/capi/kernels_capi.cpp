@@ -61,6 +61,8 @@ mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
     g.out_packed = reinterpret_cast<uint8_t*>(a->out_packed);
     g.out_R = a->out_R;
     g.n_chunks = a->n_chunks > 0 ? a->n_chunks : 1;
+    g.k_splits = a->k_splits > 0 ? a->k_splits : 1;
+    g.split_stride = a->split_stride;
     return g;
 }
 
@@ -125,7 +127,7 @@ int mlt_pack_rows(const uint16_t* src, int ld, int T, int K, void* dst, int R, v
 int mlt_rope_qkv(const float* qkv, const int32_t* pos, const void* rope, int T, int nq, int nkv,
                  int d, uint16_t* out, void* s) {
     return guard([&] {
-        ck(mltk::launch_rope_qkv(qkv, pos, reinterpret_cast<const float2*>(rope), T, nq, nkv, d, out,
+        ck(mltk::launch_rope_qkv(qkv, 1, 0, pos, reinterpret_cast<const float2*>(rope), T, nq, nkv, d, out,
                                  st(s)),
            "rope_qkv");
         return MLT_OK;

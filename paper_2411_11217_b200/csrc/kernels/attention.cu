@@ -8,15 +8,20 @@
 // contiguous 4 KiB run that a single cp.async.bulk moves into shared memory.
 // Page id = block_table[seq][pos / 16]; pool offset = (id*n_kv + h)*16*d.
 //
-// One CTA per (query token, kv head); warp g handles query head h*G + g, so
-// every K/V tile is read from HBM once for all G heads (GQA reuse).  Tiles of
-// 32 tokens (two pages of K and V, 16 KiB) flow through a kStages-deep ring
-// filled by one elected thread with 1-D bulk copies (mbarrier tx counts) —
-// the page gather is staged through shared memory.  QK^T: lane j owns token
-// j of the tile and walks the 128 dims in 16-byte chunks rotated by j
-// (conflict-free), against q held in shared memory pre-scaled by
-// log2(e)/sqrt(d); softmax runs in the exp2 domain with one warp max/sum per
-// tile; PV: lane l owns dims [4l, 4l+4) and takes p_j by shuffle.
+// One CTA per (query token, kv head).  Its kWarps warps split the pages
+// (warp w takes pages w, w+kWarps, ...: flash-decoding inside the CTA) and
+// each warp serves ALL G = n_q/n_kv query heads of the kv head, so every
+// K/V element is read once from HBM and once from shared memory for all G
+// heads (GQA reuse).  Each warp owns a kStagesW-deep ring of pages that its
+// lane 0 fills with 1-D bulk copies (mbarrier tx counts): the page gather is
+// staged through shared memory, ahead of the math.
+//   QK^T: 8 lanes per token (16 dims each, q in registers pre-scaled by
+//         log2(e)/sqrt(d)), 4 tokens per pass; lanes of the upper half read
+//         their two 16-byte chunks in swapped order so a pass is
+//         bank-conflict-free; 3 xor-shuffles reduce a score.
+//   softmax: exp2 domain, one 2-shuffle warp max/sum per page and head.
+//   PV: lane l owns dims [4l, 4l+4); p_j arrives by shuffle.
+// The warps' (m, l, acc) are merged through shared memory at the end.
 #include <cfloat>
 #include <cstdint>
 
@@ -27,134 +32,184 @@ namespace mltk {
 namespace {
 
 constexpr int kPage = 16;
-constexpr int kTile = 32;          // tokens per tile (2 pages)
 constexpr int kD = 128;
-constexpr int kStages = 4;
-constexpr int kTileBytes = kTile * kD * 2;  // one of K or V: 8 KiB
+constexpr int kWarps = 4;
+constexpr int kStagesW = 3;
+constexpr int kPageElems = kPage * kD;
+constexpr int kPageBytes = kPageElems * 2;  // 4 KiB (one of K or V)
+constexpr int kCombStride = 4 + kD;         // [m, l, pad, pad, acc[128]]: 16-byte aligned rows
 
-__global__ void __launch_bounds__(256) gqa_decode_kernel(const uint16_t* q, int ldq, const uint16_t* kp,
-                                                          const uint16_t* vp, const int32_t* bt,
-                                                          int max_pages, const int32_t* seq,
-                                                          const int32_t* ctx, int nq, int nkv,
-                                                          uint8_t* out_p, int R, float* out_f) {
+__device__ __forceinline__ float lo_bf16(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float hi_bf16(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+
+template <int G>
+__global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
+    const uint16_t* q, int ldq, const uint16_t* kp, const uint16_t* vp, const int32_t* bt,
+    int max_pages, const int32_t* seq, const int32_t* ctx, int nkv, uint8_t* out_p, int R,
+    float* out_f) {
     extern __shared__ __align__(128) uint8_t sm[];
-    __shared__ uint64_t full[kStages], empty[kStages];
+    __shared__ uint64_t full[kWarps][kStagesW];
     const int t = blockIdx.x, h = blockIdx.y;
-    const int G = nq / nkv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = ctx[t];
     const int s_id = seq[t];
     const int n_pages = (L + kPage - 1) / kPage;
-    const int n_tiles = (L + kTile - 1) / kTile;
-    uint16_t* sk = reinterpret_cast<uint16_t*>(sm);                               // [stages][32][128]
-    uint16_t* sv = reinterpret_cast<uint16_t*>(sm + kStages * kTileBytes);        // [stages][32][128]
-    float* sq = reinterpret_cast<float*>(sm + 2 * kStages * kTileBytes);          // [G][128]
+    // per-warp ring: [warp][stage][K page | V page]
+    uint16_t* ring = reinterpret_cast<uint16_t*>(sm) + static_cast<size_t>(warp) * kStagesW * 2 * kPageElems;
+    float* comb = reinterpret_cast<float*>(sm + kWarps * kStagesW * 2 * kPageBytes);  // [warp][G][2 + kD]
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], G);
-        }
+    if (lane == 0) {
+        for (int s = 0; s < kStagesW; ++s) mbar_init(&full[warp][s], 1);
         fence_mbar_init();
     }
-    // q for the G heads of this kv head, fp32, pre-scaled for exp2-domain softmax
-    const float qscale = 1.4426950408889634f * rsqrtf(static_cast<float>(kD));
-    for (int i = threadIdx.x; i < G * kD; i += blockDim.x)
-        sq[i] = bf16_bits_to_f32(q[static_cast<int64_t>(t) * ldq + (h * G) * kD + i]) * qscale;
-    __syncthreads();
-
+    __syncwarp();
     const uint64_t pol = l2_evict_first();
-    auto issue = [&](int tile) {
-        const int st = tile % kStages;
-        const int p0 = tile * 2;
-        const int np = min(2, n_pages - p0);
-        mbar_expect_tx(&full[st], np * 2 * kPage * kD * 2);
-        for (int i = 0; i < np; ++i) {
-            const int id = bt[static_cast<int64_t>(s_id) * max_pages + p0 + i];
-            const int64_t off = (static_cast<int64_t>(id) * nkv + h) * kPage * kD;
-            bulk_g2s(sk + (st * kTile + i * kPage) * kD, kp + off, kPage * kD * 2, &full[st], pol);
-            bulk_g2s(sv + (st * kTile + i * kPage) * kD, vp + off, kPage * kD * 2, &full[st], pol);
-        }
+    auto issue = [&](int page, int st) {
+        const int id = bt[static_cast<int64_t>(s_id) * max_pages + page];
+        const int64_t off = (static_cast<int64_t>(id) * nkv + h) * kPageElems;
+        uint16_t* dst = ring + st * 2 * kPageElems;
+        mbar_expect_tx(&full[warp][st], 2 * kPageBytes);
+        bulk_g2s(dst, kp + off, kPageBytes, &full[warp][st], pol);
+        bulk_g2s(dst + kPageElems, vp + off, kPageBytes, &full[warp][st], pol);
     };
-    if (threadIdx.x == 0)
-        for (int i = 0; i < n_tiles && i < kStages; ++i) issue(i);
+    if (lane == 0)
+        for (int k = 0; k < kStagesW && warp + k * kWarps < n_pages; ++k) issue(warp + k * kWarps, k);
 
-    const bool active = warp < G;
-    const float* qg = sq + warp * kD;
-    float m = -FLT_MAX, l = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-    uint32_t phase = 0;
-    for (int i = 0; i < n_tiles; ++i) {
-        const int st = i % kStages;
-        mbar_wait(&full[st], phase);
-        const int ntok = min(kTile, L - i * kTile);
-        if (active) {
-            // ---- scores: lane j <-> token j ----
-            float s = -FLT_MAX;
-            if (lane < ntok) {
-                const uint16_t* krow = sk + (st * kTile + lane) * kD;
-                float a0 = 0.f, a1 = 0.f;
+    // q slice: lane (grp = lane/8, r = lane%8) holds dims [16r, 16r+16) of each head
+    const int grp = lane >> 3, r = lane & 7;
+    const bool swap = (r >> 2) & 1;  // upper half reads its two chunks in swapped order
+    const float qscale = 1.4426950408889634f * rsqrtf(static_cast<float>(kD));
+    float qr[G][16];
 #pragma unroll
-                for (int c = 0; c < kD / 8; ++c) {
-                    const int cr = (c + lane) & (kD / 8 - 1);
-                    const uint4 kv = *reinterpret_cast<const uint4*>(krow + cr * 8);
-                    const float4 qa = *reinterpret_cast<const float4*>(qg + cr * 8);
-                    const float4 qb = *reinterpret_cast<const float4*>(qg + cr * 8 + 4);
-                    a0 = fmaf(qa.x, __uint_as_float(kv.x << 16), a0);
-                    a1 = fmaf(qa.y, __uint_as_float(kv.x & 0xffff0000u), a1);
-                    a0 = fmaf(qa.z, __uint_as_float(kv.y << 16), a0);
-                    a1 = fmaf(qa.w, __uint_as_float(kv.y & 0xffff0000u), a1);
-                    a0 = fmaf(qb.x, __uint_as_float(kv.z << 16), a0);
-                    a1 = fmaf(qb.y, __uint_as_float(kv.z & 0xffff0000u), a1);
-                    a0 = fmaf(qb.z, __uint_as_float(kv.w << 16), a0);
-                    a1 = fmaf(qb.w, __uint_as_float(kv.w & 0xffff0000u), a1);
-                }
-                s = a0 + a1;
-            }
-            // ---- online softmax (exp2 domain), one warp reduction per tile ----
-            float tmax = s;
+    for (int g = 0; g < G; ++g) {
+        const uint16_t* src = q + static_cast<int64_t>(t) * ldq + (h * G + g) * kD + r * 16;
+        const uint4 a = *reinterpret_cast<const uint4*>(src);
+        const uint4 b = *reinterpret_cast<const uint4*>(src + 8);
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-            const float m_new = fmaxf(m, tmax);
-            const float corr = exp2f(m - m_new);
-            const float p = lane < ntok ? exp2f(s - m_new) : 0.f;
-            float psum = p;
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
-            l = l * corr + psum;
-            m = m_new;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc[k] *= corr;
-            // ---- PV: lane l <-> dims [4l, 4l+4) ----
-            const uint16_t* vbase = sv + st * kTile * kD + lane * 4;
-#pragma unroll 8
-            for (int j = 0; j < kTile; ++j) {
-                const float pj = __shfl_sync(0xffffffffu, p, j);
-                const uint2 vv = *reinterpret_cast<const uint2*>(vbase + j * kD);
-                acc[0] = fmaf(pj, __uint_as_float(vv.x << 16), acc[0]);
-                acc[1] = fmaf(pj, __uint_as_float(vv.x & 0xffff0000u), acc[1]);
-                acc[2] = fmaf(pj, __uint_as_float(vv.y << 16), acc[2]);
-                acc[3] = fmaf(pj, __uint_as_float(vv.y & 0xffff0000u), acc[3]);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
+        for (int e = 0; e < 8; ++e) {
+            qr[g][2 * e] = lo_bf16(w[e]) * qscale;
+            qr[g][2 * e + 1] = hi_bf16(w[e]) * qscale;
         }
-        if (threadIdx.x == 0 && i + kStages < n_tiles) {
-            mbar_wait(&empty[st], phase);
-            issue(i + kStages);
-        }
-        if (st == kStages - 1) phase ^= 1;
     }
-    if (active) {
-        const float inv = 1.0f / l;
-        const int col = (h * G + warp) * kD + lane * 4;
-        uint2 o;
-        uint16_t* ob = reinterpret_cast<uint16_t*>(&o);
+    float m[G], l[G], acc[G][4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) ob[k] = f32_to_bf16_bits(acc[k] * inv);
-        if (out_p) *reinterpret_cast<uint2*>(out_p + b_packed_off(t, col, R)) = o;
-        if (out_f)
-            *reinterpret_cast<float4*>(out_f + static_cast<int64_t>(t) * nq * kD + col) =
-                make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    for (int g = 0; g < G; ++g) {
+        m[g] = -FLT_MAX;
+        l[g] = 0.f;
+        acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
+    }
+
+    uint32_t phase = 0;
+    for (int k = 0;; ++k) {
+        const int page = warp + k * kWarps;
+        if (page >= n_pages) break;
+        const int st = k % kStagesW;
+        mbar_wait(&full[warp][st], phase);
+        const uint16_t* sk = ring + st * 2 * kPageElems;
+        const uint16_t* sv = sk + kPageElems;
+        const int ntok = min(kPage, L - page * kPage);
+
+        // ---- QK^T: 4 passes x 4 tokens, 8 lanes per token ----
+        float sc[G][4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const int tok = p * 4 + grp;
+            const uint16_t* row = sk + tok * kD + r * 16;
+            float part[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) part[g] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int cc = swap ? (c ^ 1) : c;
+                const uint4 kv = *reinterpret_cast<const uint4*>(row + cc * 8);
+                const uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float q0 = swap ? qr[g][(c ^ 1) * 8 + 2 * e] : qr[g][c * 8 + 2 * e];
+                        const float q1 = swap ? qr[g][(c ^ 1) * 8 + 2 * e + 1] : qr[g][c * 8 + 2 * e + 1];
+                        part[g] = fmaf(q0, lo_bf16(w[e]), part[g]);
+                        part[g] = fmaf(q1, hi_bf16(w[e]), part[g]);
+                    }
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                float v = part[g];
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                sc[g][p] = tok < ntok ? v : -FLT_MAX;
+            }
+        }
+        // ---- online softmax per head (exp2 domain) ----
+        float pe[G][4];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float tmax = fmaxf(fmaxf(sc[g][0], sc[g][1]), fmaxf(sc[g][2], sc[g][3]));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
+            const float m_new = fmaxf(m[g], tmax);
+            const float corr = exp2f(m[g] - m_new);
+            float ps = 0.f;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                pe[g][p] = (p * 4 + grp) < ntok ? exp2f(sc[g][p] - m_new) : 0.f;
+                ps += pe[g][p];
+            }
+            ps += __shfl_xor_sync(0xffffffffu, ps, 8);
+            ps += __shfl_xor_sync(0xffffffffu, ps, 16);
+            l[g] = l[g] * corr + ps;
+            m[g] = m_new;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[g][e] *= corr;
+        }
+        // ---- PV: lane owns dims [4*lane, 4*lane + 4) ----
+#pragma unroll
+        for (int tok = 0; tok < kPage; ++tok) {
+            const uint2 vv = *reinterpret_cast<const uint2*>(sv + tok * kD + lane * 4);
+            const float v0 = lo_bf16(vv.x), v1 = hi_bf16(vv.x), v2 = lo_bf16(vv.y), v3 = hi_bf16(vv.y);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float pj = __shfl_sync(0xffffffffu, pe[g][tok >> 2], (tok & 3) * 8);
+                acc[g][0] = fmaf(pj, v0, acc[g][0]);
+                acc[g][1] = fmaf(pj, v1, acc[g][1]);
+                acc[g][2] = fmaf(pj, v2, acc[g][2]);
+                acc[g][3] = fmaf(pj, v3, acc[g][3]);
+            }
+        }
+        __syncwarp();  // every lane is done with this stage
+        if (lane == 0 && page + kStagesW * kWarps < n_pages) issue(page + kStagesW * kWarps, st);
+        if (st == kStagesW - 1) phase ^= 1;
+    }
+
+    // ---- merge the warps' partial softmax states ----
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        float* c = comb + (warp * G + g) * kCombStride;
+        if (lane == 0) {
+            c[0] = m[g];
+            c[1] = l[g];
+        }
+        *reinterpret_cast<float4*>(c + 4 + lane * 4) = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < G * kD; idx += blockDim.x) {
+        const int g = idx / kD, d = idx % kD;
+        float M = -FLT_MAX;
+        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, comb[(w * G + g) * kCombStride]);
+        float den = 0.f, num = 0.f;
+        for (int w = 0; w < kWarps; ++w) {
+            const float* c = comb + (w * G + g) * kCombStride;
+            const float f = c[1] > 0.f ? exp2f(c[0] - M) : 0.f;
+            den += c[1] * f;
+            num += c[4 + d] * f;
+        }
+        const float o = num / den;
+        const int col = (h * G + g) * kD + d;
+        if (out_p) *reinterpret_cast<uint16_t*>(out_p + b_packed_off(t, col, R)) = f32_to_bf16_bits(o);
+        if (out_f) out_f[static_cast<int64_t>(t) * (G * static_cast<int64_t>(nkv)) * kD + col] = o;
     }
 }
 
@@ -174,6 +229,23 @@ __global__ void kv_append_kernel(const uint16_t* qkv, int nq, int nkv, int d, co
     }
 }
 
+template <int G>
+cudaError_t launch_g(const uint16_t* q, int ldq, const uint16_t* kp, const uint16_t* vp,
+                     const int32_t* bt, int max_pages, const int32_t* seq, const int32_t* ctx, int T,
+                     int nkv, uint8_t* out_p, int R, float* out_f, cudaStream_t s) {
+    const int smem = kWarps * kStagesW * 2 * kPageBytes + kWarps * G * kCombStride * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(gqa_decode_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    dim3 grid(T, nkv);
+    gqa_decode_kernel<G><<<grid, kWarps * 32, smem, s>>>(q, ldq, kp, vp, bt, max_pages, seq, ctx, nkv,
+                                                         out_p, R, out_f);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_gqa_decode_paged(const uint16_t* q, int ldq, const uint16_t* k_pool,
@@ -182,21 +254,15 @@ cudaError_t launch_gqa_decode_paged(const uint16_t* q, int ldq, const uint16_t* 
                                     int nq, int nkv, int d, int page, uint8_t* out_packed, int R,
                                     float* out_rowmajor, cudaStream_t s) {
     if (T <= 0) return cudaSuccess;
-    if (d != kD || nq % nkv || nq / nkv > 8 || page != kPage) return cudaErrorInvalidValue;
-    const int G = nq / nkv;
-    const int threads = G * 32;
-    const int smem = 2 * kStages * kTileBytes + G * kD * 4;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(gqa_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             2 * kStages * kTileBytes + 8 * kD * 4);
-        if (e != cudaSuccess) return e;
-        attr = true;
+    if (d != kD || nq % nkv || page != kPage) return cudaErrorInvalidValue;
+    switch (nq / nkv) {
+        case 1: return launch_g<1>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, s);
+        case 2: return launch_g<2>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, s);
+        case 4: return launch_g<4>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, s);
+        case 6: return launch_g<6>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, s);
+        case 8: return launch_g<8>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, s);
+        default: return cudaErrorInvalidValue;
     }
-    dim3 grid(T, nkv);
-    gqa_decode_kernel<<<grid, threads, smem, s>>>(q, ldq, k_pool, v_pool, block_table, max_pages, seq,
-                                                  ctx, nq, nkv, out_packed, R, out_rowmajor);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_kv_append(const uint16_t* qkv_bf16, int nq, int nkv, int d, const int32_t* seq,

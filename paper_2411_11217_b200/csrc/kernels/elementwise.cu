@@ -77,25 +77,30 @@ __global__ void pack_rows_kernel(const uint16_t* src, int ld, int K, uint8_t* ds
 
 // One CTA per token; thread j < (nq+nkv)*half handles one rotation pair, the
 // v part is copied.
-__global__ void rope_qkv_kernel(const float* qkv, const int32_t* pos, const float2* rope, int nq,
-                                int nkv, int d, uint16_t* out) {
+// Sums the split-K partials of the QKV projection (parts >= 1) on the fly.
+__global__ void rope_qkv_kernel(const float* qkv, int parts, int64_t part_stride, const int32_t* pos,
+                                const float2* rope, int nq, int nkv, int d, uint16_t* out) {
     const int t = blockIdx.x;
     const int half = d / 2;
     const int W = (nq + 2 * nkv) * d;
     const float* src = qkv + static_cast<int64_t>(t) * W;
     uint16_t* dst = out + static_cast<int64_t>(t) * W;
     const float2* cs = rope + static_cast<int64_t>(pos[t]) * half;
+    auto at = [&](int j) {
+        float v = src[j];
+        for (int p = 1; p < parts; ++p) v += src[p * part_stride + j];
+        return v;
+    };
     const int pairs = (nq + nkv) * half;
     for (int j = threadIdx.x; j < pairs; j += blockDim.x) {
         const int head = j / half, i = j % half;
-        const float* v = src + head * d;
         const float c = cs[i].x, s = cs[i].y;
-        const float a = v[i], b = v[i + half];
+        const float a = at(head * d + i), b = at(head * d + i + half);
         dst[head * d + i] = f32_to_bf16_bits(a * c - b * s);
         dst[head * d + i + half] = f32_to_bf16_bits(b * c + a * s);
     }
     for (int j = (nq + nkv) * d + threadIdx.x; j < W; j += blockDim.x)
-        dst[j] = f32_to_bf16_bits(src[j]);
+        dst[j] = f32_to_bf16_bits(at(j));
 }
 
 __global__ void combine_kernel(const float* h, const float* y, int ldy, const int32_t* inv,
@@ -188,10 +193,12 @@ cudaError_t launch_pack_rows(const uint16_t* src, int ld, int T, int K, uint8_t*
     return cudaGetLastError();
 }
 
-cudaError_t launch_rope_qkv(const float* qkv, const int32_t* pos, const float2* rope, int T,
-                            int nq, int nkv, int d, uint16_t* out, cudaStream_t s) {
+cudaError_t launch_rope_qkv(const float* qkv, int parts, int64_t part_stride, const int32_t* pos,
+                            const float2* rope, int T, int nq, int nkv, int d, uint16_t* out,
+                            cudaStream_t s) {
     if (T <= 0) return cudaSuccess;
-    rope_qkv_kernel<<<T, 256, 0, s>>>(qkv, pos, rope, nq, nkv, d, out);
+    if (parts < 1) return cudaErrorInvalidValue;
+    rope_qkv_kernel<<<T, 256, 0, s>>>(qkv, parts, part_stride, pos, rope, nq, nkv, d, out);
     return cudaGetLastError();
 }
 

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
     tc_fence_after();
     const uint32_t tmem = ctl->tmem_base;
 
-    const int n_virtual = a.G * a.RB * a.n_chunks;  // (row block, group, N-chunk)
+    // virtual tile = (row block, group, N-chunk, K-split), K-split fastest
+    const int n_virtual = a.G * a.RB * a.n_chunks * a.k_splits;
     const int KB = a.K / kBlockK;
 
     if (warp == 0) {
@@ -83,7 +84,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
             int stage = 0;
             uint32_t phase = 0;
             for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-                const int c = v % a.n_chunks, g = (v / a.n_chunks) % a.G, rb = v / a.n_chunks / a.G;
+                const int ks = v % a.k_splits, u = v / a.k_splits;
+                const int c = u % a.n_chunks, g = (u / a.n_chunks) % a.G, rb = u / a.n_chunks / a.G;
+                const int kb0 = ks * KB / a.k_splits, kb1 = (ks + 1) * KB / a.k_splits;
                 const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
                 if (rows <= 0) continue;
                 const int row0 = a.b_off ? a.b_off[g] : 0;
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
                 for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
                     const int nt = min(a.n_cap, rows - n0);
                     const int ntp = (nt + 15) & ~15;
-                    for (int kb = 0; kb < KB; ++kb) {
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&ctl->empty[stage], phase ^ 1);
                         uint8_t* sa = smem + stage * stage_bytes;
                         uint8_t* sb = sa + a_bytes;
@@ -116,7 +119,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-            const int c = v % a.n_chunks, g = (v / a.n_chunks) % a.G;
+            const int ks = v % a.k_splits, u = v / a.k_splits;
+            const int c = u % a.n_chunks, g = (u / a.n_chunks) % a.G;
+            const int kb0 = ks * KB / a.k_splits, kb1 = (ks + 1) * KB / a.k_splits;
             const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
             if (rows <= 0) continue;
             for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
                 mbar_wait(&ctl->tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d0 = tmem + acc * acc_cols;
-                for (int kb = 0; kb < KB; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&ctl->full[stage], phase);
                     tc_fence_after();
                     if (elect_one()) {
@@ -137,10 +142,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
                             const uint64_t bd = sdesc_sw128(sb + k * 32);
                             for (int mt = 0; mt < a.n_mats; ++mt)
                                 umma_bf16(d0 + mt * a.n_cap, sdesc_sw128(sa + mt * kATileBytes + k * 32),
-                                          bd, idesc, (kb | k) != 0);
+                                          bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
                         }
                         umma_commit(&ctl->empty[stage]);
-                        if (kb == KB - 1) umma_commit(&ctl->tfull[acc]);
+                        if (kb == kb1 - 1) umma_commit(&ctl->tfull[acc]);
                     }
                     __syncwarp();
                     if (++stage == stages) { stage = 0; phase ^= 1; }
@@ -154,11 +159,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-            const int c = v % a.n_chunks, g = (v / a.n_chunks) % a.G, rb = v / a.n_chunks / a.G;
+            const int ks = v % a.k_splits, u = v / a.k_splits;
+            const int c = u % a.n_chunks, g = (u / a.n_chunks) % a.G, rb = u / a.n_chunks / a.G;
             const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
             if (rows <= 0) continue;
             const int row0 = a.b_off ? a.b_off[g] : 0;
             const int m = rb * kBlockM + quarter * 32 + lane;  // output feature
+            // K-split partials go to separate buffers, reduced by the consumer
+            float* const outp = a.out_f32 ? a.out_f32 + static_cast<int64_t>(ks) * a.split_stride : nullptr;
+            const float* const resid = a.k_splits == 1 ? a.residual : nullptr;
             for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
                 const int nt = min(a.n_cap, rows - n0);
                 mbar_wait(&ctl->tfull[acc], acc_phase);
@@ -174,8 +183,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
                             if (c + j < nt) {
                                 const int64_t row = row0 + n;
                                 float val = x0[j] * a.alpha;
-                                if (a.residual) val += a.residual[row * a.ldr + m];
-                                a.out_f32[row * a.ldo + m] = val;
+                                if (resid) val += resid[row * a.ldr + m];
+                                outp[row * a.ldo + m] = val;
                             }
                         }
                     } else {  // kEpiSiluPacked
@@ -214,7 +223,8 @@ int gemm_smem_bytes(int n_mats, int n_cap, int stages) {
 
 cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     if (a.n_mats < 1 || a.n_mats > kMaxMats || a.K % kBlockK || a.n_cap % 16 || a.n_cap < 16 ||
-        a.n_cap > 256 || a.R % 16 || a.n_chunks < 1)
+        a.n_cap > 256 || a.R % 16 || a.n_chunks < 1 || a.k_splits < 1 ||
+        a.k_splits > a.K / kBlockK || (a.k_splits > 1 && a.epi != kEpiF32))
         return cudaErrorInvalidValue;
     const int per_stage = a.n_mats * kATileBytes + a.n_cap * 128;
     const int budget = 227 * 1024 - 1024 - 256;
@@ -235,7 +245,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const int n_virtual = a.G * a.RB * a.n_chunks;
+    const int n_virtual = a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
     gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(a);

@@ -25,6 +25,8 @@ struct GemmArgs {
     int n_cap = 16;                  // max tokens per tile (16..256, multiple of 16)
     int n_chunks = 1;                // token chunks per (group, row block) spread over CTAs:
                                      // virtual tile (rb, g, c) handles tokens c*n_cap, +n_chunks*n_cap, ...
+    int k_splits = 1;                // split-K: partial s of the fp32 output goes to
+    int64_t split_stride = 0;        // out_f32 + s*split_stride (residual ignored; consumer reduces)
     // epilogue
     int epi = kEpiF32;
     float alpha = 1.0f;
@@ -55,17 +57,22 @@ cudaError_t launch_pack_rows(const uint16_t* src, int ld, int T, int K, uint8_t*
 
 // RoPE (rotate-half) on the q and k parts of qkv fp32 [T, (nq+2nkv)d] using
 // cos/sin table [max_pos][d/2] (float2), output bf16 [T, (nq+2nkv)d] rows
-// (q | k | v): the D1 offload layout.
-cudaError_t launch_rope_qkv(const float* qkv, const int32_t* pos, const float2* rope, int T,
-                            int nq, int nkv, int d, uint16_t* out, cudaStream_t s);
+// (q | k | v): the D1 offload layout.  qkv may hold `parts` split-K partials
+// at qkv + p*part_stride; they are summed first.
+cudaError_t launch_rope_qkv(const float* qkv, int parts, int64_t part_stride, const int32_t* pos,
+                            const float2* rope, int T, int nq, int nkv, int d, uint16_t* out,
+                            cudaStream_t s);
 
 // Router (SURVEY.md §2c router_topk_permute, first half): optional fused
 // RMSNorm (x fp32 + gamma) or direct bf16 input; logits with the fixed lane
 // tree of oracle orc_router; top-k + softmax over the selected logits.
+// With `parts` > 0 the input is split-K partials of the O projection:
+// h = residual + sum_p x[p*part_stride] is formed first and written to h_out.
 cudaError_t launch_router(const float* x, const uint16_t* gamma, float eps,
                           const uint16_t* hn_in, const uint16_t* w_router, int T, int H, int E,
                           int K, uint16_t* hn_out, float* logits, int32_t* topk_idx,
-                          float* topk_w, cudaStream_t s);
+                          float* topk_w, cudaStream_t s, int parts = 0, int64_t part_stride = 0,
+                          const float* residual = nullptr, float* h_out = nullptr);
 
 // Stable (expert, token, slot) permutation with per-expert 16-row padding
 // and gather of hn rows into the packed expert operand X (capacity R rows).

@@ -28,7 +28,8 @@ constexpr int kMaxSlots = 4096;
 
 __global__ void router_kernel(const float* x, const uint16_t* gamma, float eps,
                               const uint16_t* hn_in, const uint16_t* w, int H, int E, int K,
-                              uint16_t* hn_out, float* logits, int32_t* topk_idx, float* topk_w) {
+                              uint16_t* hn_out, float* logits, int32_t* topk_idx, float* topk_w,
+                              int parts, int64_t part_stride, const float* residual, float* h_out) {
     extern __shared__ __align__(16) uint8_t sm[];
     uint16_t* hn = reinterpret_cast<uint16_t*>(sm);                 // H bf16
     float* lg = reinterpret_cast<float*>(sm + ((H * 2 + 15) & ~15)); // E fp32
@@ -42,6 +43,23 @@ __global__ void router_kernel(const float* x, const uint16_t* gamma, float eps,
                 *reinterpret_cast<const uint4*>(hn_in + static_cast<int64_t>(t) * H + i);
     } else {
         const float* xr = x + static_cast<int64_t>(t) * H;
+        if (parts > 0) {
+            // h = residual + sum of the O-projection split-K partials (fixed
+            // order -> deterministic); h_out feeds the top-k combine
+            float* hr = h_out + static_cast<int64_t>(t) * H;
+            const float* rr = residual + static_cast<int64_t>(t) * H;
+            for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
+                float4 a = *reinterpret_cast<const float4*>(xr + i);
+                for (int p = 1; p < parts; ++p) {
+                    const float4 b = *reinterpret_cast<const float4*>(xr + p * part_stride + i);
+                    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+                }
+                const float4 r = *reinterpret_cast<const float4*>(rr + i);
+                *reinterpret_cast<float4*>(hr + i) = make_float4(a.x + r.x, a.y + r.y, a.z + r.z, a.w + r.w);
+            }
+            __syncthreads();
+            xr = hr;
+        }
         float ss = 0.0f;
         for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
             const float4 v = *reinterpret_cast<const float4*>(xr + i);
@@ -189,13 +207,15 @@ __global__ void permute_kernel(const int32_t* topk_idx, const uint16_t* hn, int 
 
 cudaError_t launch_router(const float* x, const uint16_t* gamma, float eps, const uint16_t* hn_in,
                           const uint16_t* w, int T, int H, int E, int K, uint16_t* hn_out,
-                          float* logits, int32_t* topk_idx, float* topk_w, cudaStream_t s) {
+                          float* logits, int32_t* topk_idx, float* topk_w, cudaStream_t s,
+                          int parts, int64_t part_stride, const float* residual, float* h_out) {
     if (T <= 0) return cudaSuccess;
-    if (H % 256 || E > kMaxE || K > 8 || K > E || (!hn_in && (!x || !gamma)))
+    if (H % 256 || E > kMaxE || K > 8 || K > E || (!hn_in && (!x || !gamma)) ||
+        (parts > 0 && (!residual || !h_out)))
         return cudaErrorInvalidValue;
     const int smem = ((H * 2 + 15) & ~15) + E * 4;
     router_kernel<<<T, 256, smem, s>>>(x, gamma, eps, hn_in, w, H, E, K, hn_out, logits, topk_idx,
-                                       topk_w);
+                                       topk_w, parts, part_stride, residual, h_out);
     return cudaGetLastError();
 }
 

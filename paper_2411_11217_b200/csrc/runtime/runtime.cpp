@@ -184,8 +184,9 @@ void Runtime::allocate() {
     d_qkv_bf16_ = static_cast<uint16_t*>(A.alloc(static_cast<size_t>(M_) * mu_ * W_ * 2, "qkv_bf16"));
     d_attn_in_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(M_) * Rmu_ * H_ * 2, "attn_in"));
     d_xn_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Rmu_) * H_ * 2, "xn"));
-    d_qkv_f32_ = static_cast<float*>(A.alloc(static_cast<size_t>(Rmu_) * W_ * 4, "qkv_f32"));
+    d_qkv_f32_ = static_cast<float*>(A.alloc(static_cast<size_t>(kMaxSplits) * Rmu_ * W_ * 4, "qkv_f32"));
     d_h_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * H_ * 4, "h"));
+    d_hparts_ = static_cast<float*>(A.alloc(static_cast<size_t>(kMaxSplits) * mu_ * H_ * 4, "h_parts"));
     d_hn_ = static_cast<uint16_t*>(A.alloc(static_cast<size_t>(mu_) * H_ * 2, "hn"));
     d_topk_ = static_cast<int32_t*>(A.alloc(mu_ * K_ * 4, "topk"));
     d_topw_ = static_cast<float*>(A.alloc(mu_ * K_ * 4, "topw"));
@@ -413,14 +414,15 @@ void Runtime::kl(const char* name, cudaError_t e) {
 
 void Runtime::mark_start(cudaEvent_t task_start) { marks_.push_back({nullptr, task_start}); }
 
-// Dense projections have few 128-row blocks (QKV 48, O 32 for 8x7B): split
-// the tokens into chunks so (row block x chunk) tiles cover all SMs; the
-// chunks of one row block run on neighbouring CTAs and share its weight tile
-// through L2.
-void Runtime::dense_tiling(int row_blocks, int& n_cap, int& n_chunks) const {
-    const int want = std::max(1, (num_sms_ + row_blocks - 1) / row_blocks);
-    n_cap = std::min(256, std::max(16, round_up((mu_ + want - 1) / want, 16)));
+// Dense projections have few 128-row blocks (QKV 48, O 32 for 8x7B), too
+// few to stream their weights over all SMs: split K so (row block x K-split)
+// tiles cover the chip (each weight byte is still read once).  The fp32
+// partials are reduced by the consumer (rope_qkv for QKV, the router kernel
+// for O), in fixed order.  Tokens stay in one chunk (<= 256).
+void Runtime::dense_tiling(int row_blocks, int& n_cap, int& n_chunks, int& k_splits) const {
+    n_cap = std::min(256, Rmu_);
     n_chunks = (mu_ + n_cap - 1) / n_cap;
+    k_splits = std::max(1, std::min(kMaxSplits, num_sms_ / (row_blocks * n_chunks)));
 }
 
 // ---------------------------------------------------------------------------
@@ -450,14 +452,16 @@ void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
     a.b = d_xn_;
     a.R = Rmu_;
     a.rows_dense = mu_;
-    dense_tiling(W_ / 128, a.n_cap, a.n_chunks);
+    dense_tiling(W_ / 128, a.n_cap, a.n_chunks, a.k_splits);
+    a.split_stride = static_cast<int64_t>(Rmu_) * W_;
     a.epi = mltk::kEpiF32;
     a.out_f32 = d_qkv_f32_;
     a.ldo = W_;
     kl("qkv_gemm", mltk::launch_gemm(a, num_sms_, s_gpu_));
     const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
     uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
-    kl("rope_qkv", mltk::launch_rope_qkv(d_qkv_f32_, pos, d_rope_, mu_, nq_, nkv_, d_, qkv, s_gpu_));
+    kl("rope_qkv", mltk::launch_rope_qkv(d_qkv_f32_, a.k_splits, a.split_stride, pos, d_rope_, mu_, nq_, nkv_,
+                                         d_, qkv, s_gpu_));
 }
 
 void Runtime::act_offload_qkv(int layer, int mb) {
@@ -507,15 +511,19 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     o.b = policy_.attn_on_gpu ? d_attn_gpu_ : d_attn_in_ + static_cast<size_t>(mb - 1) * Rmu_ * H_ * 2;
     o.R = Rmu_;
     o.rows_dense = mu_;
-    dense_tiling(H_ / 128, o.n_cap, o.n_chunks);
-    o.out_f32 = d_h_;
+    dense_tiling(H_ / 128, o.n_cap, o.n_chunks, o.k_splits);
+    const bool o_split = o.k_splits > 1;
+    o.split_stride = static_cast<int64_t>(mu_) * H_;
+    o.out_f32 = o_split ? d_hparts_ : d_h_;
     o.ldo = H_;
-    o.residual = x;
+    o.residual = x;  // added by the GEMM epilogue (unsplit) or by the router (split)
     o.ldr = H_;
     kl("o_gemm", mltk::launch_gemm(o, num_sms_, s_gpu_));
-    // RMSNorm + router + permute
-    kl("router", mltk::launch_router(d_h_, d_ffn_norm_[l], ext_.rms_eps, nullptr, d_router_[l], mu_, H_, E_, K_,
-                                     d_hn_, nullptr, d_topk_, d_topw_, s_gpu_));
+    // (split-K reduce + residual ->) RMSNorm + router + permute
+    kl("router", mltk::launch_router(o_split ? d_hparts_ : d_h_, d_ffn_norm_[l], ext_.rms_eps, nullptr,
+                                     d_router_[l], mu_, H_, E_, K_, d_hn_, nullptr, d_topk_, d_topw_, s_gpu_,
+                                     o_split ? o.k_splits : 0, o.split_stride, o_split ? x : nullptr,
+                                     o_split ? d_h_ : nullptr));
     kl("moe_permute", mltk::launch_moe_permute(d_topk_, d_hn_, mu_, H_, E_, K_, d_cnt_, d_off_, d_perm_, d_inv_,
                                                d_xe_, Re_, s_gpu_));
     // experts: gate/up (SiLU fused) -> down -> combine
@@ -557,7 +565,8 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
         lm.b = d_xn_;
         lm.R = Rmu_;
         lm.rows_dense = mu_;
-        dense_tiling(V_ / 128, lm.n_cap, lm.n_chunks);
+        lm.n_cap = std::min(256, Rmu_);  // 250+ row blocks already fill the chip
+        lm.n_chunks = (mu_ + lm.n_cap - 1) / lm.n_cap;
         lm.out_f32 = d_logits_;
         lm.ldo = V_;
         kl("lm_head_gemm", mltk::launch_gemm(lm, num_sms_, s_gpu_));

@@ -135,7 +135,8 @@ class Runtime {
 
   private:
     void build_catalog();
-    void dense_tiling(int row_blocks, int& n_cap, int& n_chunks) const;
+    void dense_tiling(int row_blocks, int& n_cap, int& n_chunks, int& k_splits) const;
+    static constexpr int kMaxSplits = 8;
     void allocate();
     void generate_weights();
     void host_attention(int layer, int mb, int step);
@@ -175,8 +176,9 @@ class Runtime {
     uint16_t* d_qkv_bf16_ = nullptr;    // [M][mu][W]
     uint8_t* d_attn_in_ = nullptr;      // [M][Rmu*H] packed
     uint8_t* d_xn_ = nullptr;           // [Rmu*H] packed
-    float* d_qkv_f32_ = nullptr;        // [Rmu, W]
+    float* d_qkv_f32_ = nullptr;        // [kMaxSplits][Rmu, W] split-K partials
     float* d_h_ = nullptr;              // [mu, H]
+    float* d_hparts_ = nullptr;         // [kMaxSplits][mu, H] O-projection split-K partials
     uint16_t* d_hn_ = nullptr;          // [mu, H]
     int32_t *d_topk_ = nullptr, *d_cnt_ = nullptr, *d_off_ = nullptr, *d_perm_ = nullptr, *d_inv_ = nullptr;
     float* d_topw_ = nullptr;

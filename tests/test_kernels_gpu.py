@@ -90,6 +90,29 @@ def test_dense_gemm_matches_torch(K, T, M, Kd, n_cap):
     assert err <= 2e-3 * max(1.0, ref.abs().max().item()), err
 
 
+@pytest.mark.parametrize("T,M,Kd,splits,chunks,n_cap", [(64, 384, 1024, 3, 1, 64),
+                                                         (256, 256, 4096, 4, 1, 256),
+                                                         (40, 128, 512, 8, 3, 16)])
+def test_split_k_and_chunked_gemm(K, T, M, Kd, splits, chunks, n_cap):
+    """Split-K partials (summed by the consumer) and N-chunked tiles."""
+    g = torch.Generator().manual_seed(T + splits)
+    w = rand_bf16(M, Kd, scale=Kd ** -0.5, gen=g)
+    x = rand_bf16(T, Kd, gen=g)
+    R = (T + 15) // 16 * 16
+    wdev, blocks = pack_weight_dev(K, w)
+    tab = table([blocks])
+    xp = pack_rows_dev(K, x, R)
+    parts = torch.zeros(splits, R, M, device="cuda")
+    a = capi.GemmArgs(a_table=tab.data_ptr(), n_mats=1, G=1, RB=M // 128, K=Kd, b=xp.data_ptr(),
+                      R=R, rows_dense=T, n_cap=n_cap, epi=0, alpha=1.0, out_f32=parts.data_ptr(),
+                      ldo=M, n_chunks=chunks, k_splits=splits, split_stride=R * M)
+    K.gemm(C.byref(a), stream())
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().T
+    got = parts.sum(0)[:T].cpu()
+    assert (got - ref).abs().max().item() <= 2e-3 * max(1.0, ref.abs().max().item())
+
+
 def _expert_setup(T, H, Fd, E, Kk, seed):
     g = torch.Generator().manual_seed(seed)
     hn = rand_bf16(T, H, gen=g)

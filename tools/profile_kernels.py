@@ -89,18 +89,45 @@ def main():
         KD.expert_ffn(ptr(xp), R, ptr(cnt), ptr(off), ptr(t13), ptr(t2), E, H, F, ncap,
                       ptr(inter), ptr(y), ptr(inv), ptr(wts), ptr(hbuf), mu, K, ptr(xo), s)
 
+    def tiling(rb):  # runtime.cpp dense_tiling
+        cap = min(256, Rmu)
+        ch = (mu + cap - 1) // cap
+        return cap, ch, max(1, min(8, 148 // (rb * ch)))
+
+    qkv_parts = torch.zeros(8 * Rmu * W, device="cuda")
+    h_parts = torch.zeros(8 * mu * H, device="cuda")
+
     def dense_qkv():
         KD.rmsnorm_pack(ptr(x), ptr(gamma), mu, H, 1e-5, ptr(xn), Rmu, s)
+        cap, ch, ks = tiling(W // 128)
         g = capi.GemmArgs(a_table=tqkv.data_ptr(), n_mats=1, G=1, RB=W // 128, K=H,
-                          b=xn.data_ptr(), R=Rmu, rows_dense=mu, n_cap=ncap, epi=0, alpha=1.0,
-                          out_f32=qkv.data_ptr(), ldo=W)
+                          b=xn.data_ptr(), R=Rmu, rows_dense=mu, n_cap=cap, epi=0, alpha=1.0,
+                          out_f32=qkv_parts.data_ptr(), ldo=W, n_chunks=ch, k_splits=ks,
+                          split_stride=Rmu * W)
         KD.gemm(C.byref(g), s)
 
     def dense_o():
+        cap, ch, ks = tiling(H // 128)
         g = capi.GemmArgs(a_table=to.data_ptr(), n_mats=1, G=1, RB=H // 128, K=H,
-                          b=xn.data_ptr(), R=Rmu, rows_dense=mu, n_cap=ncap, epi=0, alpha=1.0,
-                          out_f32=hbuf.data_ptr(), ldo=H, residual=x.data_ptr(), ldr=H)
+                          b=xn.data_ptr(), R=Rmu, rows_dense=mu, n_cap=cap, epi=0, alpha=1.0,
+                          out_f32=h_parts.data_ptr(), ldo=H, residual=x.data_ptr(), ldr=H,
+                          n_chunks=ch, k_splits=ks, split_stride=mu * H)
         KD.gemm(C.byref(g), s)
+
+    # paged GQA attention at ctx 528 (identity block table, 16-token pages)
+    CTX = 528
+    pages_per = (CTX + 15) // 16
+    kpool = (torch.randn(mu * pages_per * NKV * 16 * D, device="cuda")).to(torch.bfloat16)
+    vpool = (torch.randn(mu * pages_per * NKV * 16 * D, device="cuda")).to(torch.bfloat16)
+    bt = torch.arange(mu * pages_per, dtype=torch.int32, device="cuda")
+    seq = torch.arange(mu, dtype=torch.int32, device="cuda")
+    ctxs = torch.full((mu,), CTX, dtype=torch.int32, device="cuda")
+    qrows = (torch.randn(mu, W, device="cuda")).to(torch.bfloat16)
+    attn_out = torch.zeros(Rmu * H, dtype=torch.int16, device="cuda")
+
+    def attention():
+        KD.gqa_decode_paged(ptr(qrows), W, ptr(kpool), ptr(vpool), ptr(bt), pages_per, ptr(seq),
+                            ptr(ctxs), mu, NQ, NKV, D, 16, ptr(attn_out), Rmu, None, s)
 
     router()
     torch.cuda.synchronize()
@@ -111,6 +138,7 @@ def main():
          touched * 3 * H * F * 2 + mu * K * 2 * H * 2 + mu * H * 2),
         ("qkv (norm+gemm)", dense_qkv, W * H * 2 + mu * H * 4),
         ("o_proj (+residual)", dense_o, H * H * 2 + mu * H * 4 * 2),
+        ("gqa_decode_paged (ctx 528)", attention, mu * 2 * CTX * NKV * D * 2),
     ]
     reps = 2 if a.once else a.reps
     out = {}
