@@ -43,12 +43,19 @@ CONFIGS = {
     # GPU-bound regime a 180 GB B200 opens up (HRM bound is HBM, not PCIe)
     "mixtral8x7b-resident": dict(model=(32, 4096, 14336, 32, 8, 8, 2), N=256, mu=256, r_w=1.0,
                                  a_g=1, budget=140e9, prompt=512, gen=32, vocab=32000),
+    # BASELINE configs[3]/[4]: tensor-parallel over 2/4/8 B200 (torchrun), 16 GB per GPU;
+    # r_w per tp = the reference model's optimum
+    "mixtral8x22b-tp": dict(model=(56, 6144, 16384, 48, 8, 8, 2), N=256, mu=64,
+                            r_w={1: 0.0, 2: 0.05, 4: 0.15, 8: 0.40}, a_g=0, budget=16e9, prompt=512,
+                            gen=32, vocab=32000),
+    "dbrx-tp": dict(model=(40, 6144, 10752, 48, 8, 16, 4), N=256, mu=64,
+                    r_w={1: 0.0, 2: 0.05, 4: 0.20}, a_g=0, budget=16e9, prompt=512, gen=128,
+                    vocab=32000),
     "tiny": dict(model=(2, 1024, 3584, 8, 2, 8, 2), N=8, mu=4, r_w=0.0, a_g=0, budget=4e9,
                  prompt=16, gen=32, vocab=32000),
 }
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
-HOST_READ_GBS = 111.0   # measured on the GPU box, tools/pin_probe.cu (gpurun_out/pin_probe.txt)
 HOST_FLOPS = 2.0e12     # host-core fp32 estimate (16 SPR cores AVX-512); CPU attention never binds
 
 
@@ -125,17 +132,30 @@ def policy(cfg):
     return capi.Policy(cfg["N"], cfg["mu"], cfg["a_g"], 1, cfg["r_w"], 1.0 if cfg["a_g"] else 0.0)
 
 
-def hrm_bound(cfg, link_gbs, pk):
+def hrm_bound(cfg, link_gbs, host_gbs, pk, tp=1):
     """B200 HRM bound: the reference's own estimate_throughput (planner.cpp:129-162)
-    re-parameterised with measured B200 numbers."""
+    re-parameterised with measured B200 numbers; under TP the B200 rule of
+    apply_tensor_parallelism_b200 (GPU side x tp, link x tp capped by the host
+    DRAM read bandwidth: every B200 has its own PCIe link)."""
     from paper_2411_11217_b200 import capi
     api = capi.load_product()
-    hw = capi.HardwareSpec(cfg["budget"], 196e9, pk["hbm_gbs"] * 1e9, HOST_READ_GBS * 1e9,
+    hw = capi.HardwareSpec(cfg["budget"], 196e9, pk["hbm_gbs"] * 1e9, host_gbs * 1e9,
                            link_gbs * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12,
                            HOST_FLOPS)
+    if tp > 1:
+        hw = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=host_gbs * 1e9)
     w = capi.WorkloadSpec(cfg["prompt"], cfg["gen"])
     r = api.estimate_throughput(hw, model_spec(cfg), w, policy(cfg))
     return r
+
+
+def measure_host(api):
+    import ctypes as C
+    f = api.lib.mlt_measure_host_bw
+    f.restype, f.argtypes = C.c_int, [C.c_size_t, C.POINTER(C.c_double)]
+    out = (C.c_double * 2)()
+    api.check(f(4 << 30, out))
+    return out[0]
 
 
 def cpu_sample(cfg, samples, layers_sample=1):
@@ -183,20 +203,20 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def expert_roofline(cfg, rep, pk, traffic):
+def expert_roofline(cfg, rep, pk, traffic, tp=1):
     """Dominant GPU kernel = expert FFN (gate/up + down GEMM) per micro-batch.
     Algorithmic bytes per launch: sum over touched experts of
     3*h1*h2*dt (all n_e are touched at mu*k >= 128 slots, P(untouched) <
     1e-7) + mu*k*2*h1*dt + mu*h1*dt."""
     l, h1, h2, nq, nkv, ne, k = cfg["model"]
     mu = cfg["mu"]
-    bytes_launch = ne * 3 * h1 * h2 * 2 + mu * k * 2 * h1 * 2 + mu * h1 * 2
+    bytes_launch = ne * 3 * h1 * (h2 // tp) * 2 + mu * k * 2 * h1 * 2 + mu * h1 * 2
     avg_s = rep.expert_ms_total / max(rep.expert_launches, 1) / 1e3
     achieved = bytes_launch / avg_s / 1e9
     peak = pk["hbm_gbs"]
     return {"kernel": "expert_ffn (gemm_tc gate/up+SiLU, gemm_tc down)", "bound": "hbm",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "bytes_per_launch": bytes_launch,
+            "traffic": traffic if tp == 1 else None, "bytes_per_launch": bytes_launch,
             "avg_launch_ms": avg_s * 1e3, "launches": rep.expert_launches}
 
 
@@ -210,15 +230,25 @@ def load_traffic():
 
 def run_mlt(args, cfg):
     from paper_2411_11217_b200 import capi
-    from paper_2411_11217_b200.runtime import Runtime
+    from paper_2411_11217_b200.runtime import Runtime, nccl_unique_id
     import ctypes as C
     import numpy as np
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    nid = b""
     if world > 1:
-        raise SystemExit("multi-GPU tensor parallelism is not wired into bench.py yet")
+        # One process per GPU; tensor parallelism across the node: heads and
+        # expert h2 sharded, 2 NCCL all-reduces per layer per micro-batch.  The
+        # gloo group only ships the ncclUniqueId, barriers and the max-over-ranks.
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        idt = torch.tensor(list(nccl_unique_id() if rank == 0 else bytes(128)), dtype=torch.uint8)
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.tolist())
     pk, pk_src = peaks()
     api = capi.load_product()
     f = api.lib.mlt_measure_link
@@ -226,66 +256,83 @@ def run_mlt(args, cfg):
     link = (C.c_double * 3)()
     api.check(f(local, 1 << 30, 5, link))
     link_gbs = link[0]
-    log(f"[bench] link H2D {link[0]:.2f} GB/s, D2H {link[1]:.2f}, H2D with D2H {link[2]:.2f}")
+    host_gbs = measure_host(api)
+    log(f"[bench] rank {rank}: link H2D {link[0]:.2f} GB/s, D2H {link[1]:.2f}, H2D with D2H "
+        f"{link[2]:.2f}; host DRAM read {host_gbs:.1f} GB/s")
 
     t = time.perf_counter()
     rt = Runtime(model_spec(cfg), policy(cfg), budget_bytes=cfg["budget"],
                  max_ctx=cfg["prompt"] + args.warmup + args.steps + 8, vocab=cfg["vocab"],
-                 device=local, exact_gates=args.gates == "exact")
+                 device=local, exact_gates=args.gates == "exact", tp_rank=rank, tp_size=world,
+                 nccl_id=nid)
     info = rt.info
-    log(f"[bench] runtime ready in {time.perf_counter() - t:.1f}s (weights gen {info.gen_seconds:.1f}s,"
-        f" pin {info.pin_seconds:.1f}s), r_w achieved {info.achieved_weight_ratio:.4f}, "
-        f"streamed {info.streamed_bytes_per_layer / 1e9:.3f} GB/layer, arena {info.arena_used / 1e9:.2f} GB")
+    log(f"[bench] rank {rank}: runtime ready in {time.perf_counter() - t:.1f}s (weights gen "
+        f"{info.gen_seconds:.1f}s, pin {info.pin_seconds:.1f}s), r_w achieved "
+        f"{info.achieved_weight_ratio:.4f}, streamed {info.streamed_bytes_per_layer / 1e9:.3f} GB/layer, "
+        f"arena {info.arena_used / 1e9:.2f} GB")
     rt.prefill_synthetic(cfg["prompt"], 9012)
     toks = np.random.default_rng(5678).integers(0, cfg["vocab"], cfg["N"], dtype=np.int32)
     w = rt.decode(toks, args.warmup)
     last = w.ids[-1]
-    log(f"[bench] warm-up {args.warmup} steps: {w.report.tokens_per_second:.1f} tok/s")
+    log(f"[bench] rank {rank}: warm-up {args.warmup} steps: {w.report.tokens_per_second:.1f} tok/s")
 
+    if dist:
+        dist.barrier()
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
         d = rt.decode(last, args.steps)          # host ids in, host ids out (C ABI)
         t1 = time.perf_counter()
+    if dist:
+        dist.barrier()
     clocks = clk.summary()
     rep = d.report
+    dev_s, wall_s = rep.seconds, t1 - t0
+    if dist:  # time = max over ranks
+        import torch
+        tt = torch.tensor([dev_s, wall_s], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_s, wall_s = tt.tolist()
     if not rep.timeline_ok:
         log(f"[bench] measured timeline check: {api.error()}")
-    if args.timeline:
+    if args.timeline and rank == 0:
         with open(args.timeline, "w") as fh:
             json.dump(rt.timeline(), fh)
-    value = rep.tokens_per_second                # device-timed (CUDA events)
-    e2e = cfg["N"] * args.steps / (t1 - t0)      # wall clock around the C-ABI call
-    bound = hrm_bound(cfg, link_gbs, pk)
+    value = cfg["N"] * args.steps / dev_s        # device-timed (CUDA events), whole job
+    e2e = cfg["N"] * args.steps / wall_s         # wall clock around the C-ABI call
+    bound = hrm_bound(cfg, link_gbs, host_gbs, pk, tp=world)
     l = cfg["model"][0]
-    tl_layer_bytes = info.streamed_bytes_per_layer
     link_s = rep.measured.link_upload * l * args.steps
     h2d_gbs = rep.h2d_weight_bytes / link_s / 1e9 if link_s > 0 else 0.0
     bd = bound.breakdown
     binding = max([("host link (H2D)", bd.link_upload), ("host cores", bd.cpu_attention + bd.cpu_ffn),
                    ("GPU (HBM)", bd.gpu_attention + bd.gpu_ffn)], key=lambda kv: kv[1])[0]
+    names = {32: "Mixtral-8x7B shape", 56: "Mixtral-8x22B shape", 40: "DBRX shape", 2: "tiny"}
     line = {
         "metric": "decode tokens/sec at fixed GPU-mem budget",
-        "value": value, "unit": "tok/s", "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * rep.seconds / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (counter-PRNG weights seed 1234, prompt ids seed 5678, prompt KV seed 9012)",
-        "config": {"workload": args.config, "model": "Mixtral-8x7B shape" if l == 32 else "tiny",
+        "config": {"workload": args.config, "model": names.get(l, "custom"),
                    "global_batch": cfg["N"], "seq_len": cfg["prompt"], "micro_batch": cfg["mu"],
                    "gpu_budget_gb": cfg["budget"] / 1e9, "r_w": cfg["r_w"],
                    "r_w_achieved": info.achieved_weight_ratio, "A_g": cfg["a_g"],
-                   "parallelism": "single GPU, CGOPipe paging",
+                   "parallelism": (f"tp{world} (heads + expert h2 sharded, NCCL all-reduce x2/layer)"
+                                   if world > 1 else "single GPU, CGOPipe paging"),
                    "weight_gates": args.gates,
                    "l2": "weights streamed per step (>> 126 MB L2): no flush needed"},
         "hrm": {"bound_tok_s": bound.decode_throughput, "frac": value / bound.decode_throughput,
-                "binding": binding, "link_gbs_measured": link_gbs,
+                "binding": binding, "link_gbs_measured": link_gbs, "host_read_gbs_measured": host_gbs,
                 "modeled_layer_ms": bound.breakdown.layer_total * 1e3,
                 "measured_steady_layer_ms": rep.steady_layer_time * 1e3,
                 "h2d_weight_gbs_achieved": h2d_gbs,
-                "streamed_gb_per_layer": tl_layer_bytes / 1e9,
+                "streamed_gb_per_layer_per_gpu": info.streamed_bytes_per_layer / 1e9,
                 "utilization": dict(zip(["gpu", "cpu", "h2d", "d2h", "ctopin"], list(rep.utilization)))},
-        "roofline": expert_roofline(cfg, rep, pk, load_traffic()),
+        "roofline": expert_roofline(cfg, rep, pk, load_traffic(), world),
         "peaks_source": pk_src,
-        "e2e": {"value": e2e, "unit": "tok/s", "h2d_bytes_per_step": rep.h2d_bytes / args.steps + cfg["N"] * 4 * 2 / args.steps,
+        "e2e": {"value": e2e, "unit": "tok/s",
+                "h2d_bytes_per_step": rep.h2d_bytes / args.steps + cfg["N"] * 4 * 2,
                 "d2h_bytes_per_step": rep.d2h_bytes / args.steps + cfg["N"] * 4},
         "kernels_ms_per_step": {k["name"]: round(k["ms"] / args.steps, 4) for k in rt.kernel_profile()},
         "gpu_launches": rep.gpu_launches,
@@ -293,13 +340,16 @@ def run_mlt(args, cfg):
         "clocks": clocks,
     }
     del rt
-    if not args.no_cpu_baseline and rank == 0:
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
         tok_s, cores, times = cpu_sample(cfg, 3)
         line["cpu_baseline"] = {"value": tok_s, "unit": "tok/s", "cores": cores, "kind": "port",
                                 "sample": f"1 of {l} decoder layers, fp32 CPU oracle, N={cfg['N']} at ctx "
                                           f"{cfg['prompt']}, median of 3 (layer s: "
                                           f"{', '.join(f'{x:.2f}' for x in times)}), tok/s = N/(l*t_layer)"}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
 
 
 def main():
@@ -314,7 +364,12 @@ def main():
                     help="weight gates: data-exact (default) or the reference's all-pages gate")
     ap.add_argument("--timeline", default=None, help="write the measured timeline JSON here")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if isinstance(cfg["r_w"], dict):
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        if world not in cfg["r_w"]:
+            raise SystemExit(f"{args.config}: no policy for {world} GPUs (h2/tp must keep 128-row blocks)")
+        cfg["r_w"] = cfg["r_w"][world]
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

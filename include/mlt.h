@@ -289,6 +289,9 @@ int mlt_rope_table(int max_pos, int d, double theta, float* host_out);
  * `bytes` per copy, best of `reps`, CUDA events.  out[0] = H2D GB/s,
  * out[1] = D2H GB/s, out[2] = H2D GB/s with a concurrent D2H stream. */
 int mlt_measure_link(int device, size_t bytes, int reps, double out[3]);
+/* Host DRAM bandwidth (the b_c of the HardwareSpec), all host threads:
+ * out[0] = read GB/s (sum over `bytes`), out[1] = copy GB/s. */
+int mlt_measure_host_bw(size_t bytes, double out[2]);
 
 /* Host: synthetic weights, element i of tensor tid: splitmix64 counter PRNG
  * (DESIGN.md §3), bf16 RNE.  Multi-threaded. */
@@ -317,7 +320,26 @@ typedef struct mlt_runtime_options_t {
     int32_t exact_gates;   /* 1: data-exact weight gates (default); 0: reference gates,
                               every GPU task of layer g waits for all pages of g
                               (pipesim.cpp:131-148) */
+    int32_t tp_rank, tp_size; /* tensor parallelism, one process per GPU (tp_size 0/1: off):
+                                 heads + expert h2 sharded, 2 all-reduces per layer */
+    uint8_t nccl_id[128];     /* mlt_nccl_unique_id() of rank 0, identical on every rank */
 } mlt_runtime_options_t;
+
+/* ncclUniqueId for a tensor-parallel group (call on rank 0, broadcast). */
+int mlt_nccl_unique_id(uint8_t out[128]);
+
+/* Tensor-parallel shard of one rank (GPU-free): local head / h2 counts and
+ * the global rows / columns each local weight matrix covers. */
+typedef struct mlt_tp_shard_t {
+    int64_t q_heads, kv_heads, ffn, qkv_rows, o_k;
+} mlt_tp_shard_t;
+int mlt_tp_shard(const mlt_model_spec_t* model, int rank, int size, mlt_tp_shard_t* out);
+/* Host: this rank's local weight matrix `kind` (5 wqkv, 6 wo, 8 w1, 9 w3,
+ * 10 w2) of (layer, expert), row-major bf16 [rows, cols] exactly as the
+ * runtime generates it (packed, then unpacked here for inspection). */
+int mlt_synth_tp_weight(const mlt_model_spec_t* model, int rank, int size, uint64_t seed,
+                        int layer, int kind, int expert, uint16_t* host_out, int64_t* rows,
+                        int64_t* cols);
 
 typedef struct mlt_decode_report_t {
     double seconds, tokens_per_second;

@@ -2,7 +2,9 @@
 // points").  Thin: argument checks, cudaError -> MLT_ERR_CUDA, no hidden
 // allocation except mlt_expert_ffn's (none: all buffers caller-owned).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <vector>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -306,6 +308,30 @@ int mlt_measure_link(int device, size_t bytes, int reps, double out[3]) {
             throw;
         }
         cleanup();
+        return MLT_OK;
+    });
+}
+
+int mlt_measure_host_bw(size_t bytes, double out[2]) {
+    return guard([&] {
+        const size_t n = bytes / 8;
+        std::vector<double> a(n, 1.0), b(n, 0.0);
+        double best_read = 0, best_copy = 0;
+        for (int rep = 0; rep < 3; ++rep) {
+            double sum = 0;
+            auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for reduction(+ : sum) schedule(static)
+            for (int64_t i = 0; i < static_cast<int64_t>(n); ++i) sum += a[i];
+            auto t1 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < static_cast<int64_t>(n); ++i) b[i] = a[i];
+            auto t2 = std::chrono::steady_clock::now();
+            if (sum < 0) throw std::runtime_error("unreachable");
+            best_read = std::max(best_read, n * 8.0 / std::chrono::duration<double>(t1 - t0).count() / 1e9);
+            best_copy = std::max(best_copy, n * 16.0 / std::chrono::duration<double>(t2 - t1).count() / 1e9);
+        }
+        out[0] = best_read;
+        out[1] = best_copy;
         return MLT_OK;
     });
 }

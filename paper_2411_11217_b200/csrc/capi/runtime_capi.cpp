@@ -2,6 +2,11 @@
 #include <memory>
 #include <string>
 
+#include <cstring>
+#include <vector>
+
+#include "../kernels/common.cuh"
+#include "../runtime/host_layout.hpp"
 #include "../runtime/runtime.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
@@ -48,6 +53,9 @@ mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p
         opt.device = o->device; opt.budget_bytes = o->budget_bytes; opt.max_ctx = o->max_ctx;
         opt.host_threads = o->host_threads; opt.pin_weights = o->pin_weights;
         opt.exact_gates = o->exact_gates;
+        opt.tp_rank = o->tp_size > 1 ? o->tp_rank : 0;
+        opt.tp_size = o->tp_size > 1 ? o->tp_size : 1;
+        std::memcpy(opt.nccl_id, o->nccl_id, 128);
         auto hh = std::make_unique<Handle>();
         hh->rt = std::make_unique<mlt::Runtime>(ms, ext, pol, opt);
         h = hh.release();
@@ -57,6 +65,54 @@ mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p
 }
 
 void mlt_runtime_destroy(mlt_runtime* r) { delete H(r); }
+
+namespace {
+lightplan::ModelSpec model_in(const mlt_model_spec_t* m) {
+    lightplan::ModelSpec ms;
+    ms.layers = m->layers; ms.hidden_dim = m->hidden_dim; ms.ffn_dim = m->ffn_dim;
+    ms.q_heads = m->q_heads; ms.kv_heads = m->kv_heads; ms.experts = m->experts;
+    ms.top_k = m->top_k; ms.weight_dtype_bytes = m->weight_dtype_bytes;
+    ms.kv_dtype_bytes = m->kv_dtype_bytes;
+    return ms;
+}
+}  // namespace
+
+int mlt_tp_shard(const mlt_model_spec_t* m, int rank, int size, mlt_tp_shard_t* out) {
+    return guard([&] {
+        const mlt::Shard s = mlt::make_shard(model_in(m), rank, size);
+        *out = {s.q_heads, s.kv_heads, s.ffn, s.qkv_rows, s.o_k};
+        return MLT_OK;
+    });
+}
+
+int mlt_synth_tp_weight(const mlt_model_spec_t* m, int rank, int size, uint64_t seed, int layer,
+                        int kind, int expert, uint16_t* out, int64_t* rows, int64_t* cols) {
+    return guard([&] {
+        const lightplan::ModelSpec ms = model_in(m);
+        const mlt::Shard s = mlt::make_shard(ms, rank, size);
+        const mlt::ShardMap sm = mlt::shard_map(ms, s, kind);
+        const int64_t R = static_cast<int64_t>(sm.rows.size());
+        *rows = R;
+        *cols = sm.k_local;
+        if (!out) return MLT_OK;
+        std::vector<uint16_t> packed(static_cast<size_t>(R) * sm.k_local);
+        mlt::synth_shard_packed(seed, mlt::tensor_id(layer, kind, expert), sm.k_global, sm.rows.data(), sm.col0,
+                                sm.k_local, 0, R, sm.scale, packed.data());
+        // unpack [R, K] (block-major A layout) for inspection
+        const uint8_t* p = reinterpret_cast<const uint8_t*>(packed.data());
+        for (int64_t i = 0; i < R; ++i)
+            for (int64_t k = 0; k < sm.k_local; ++k)
+                std::memcpy(out + i * sm.k_local + k, p + mltk::a_packed_off(i, k, sm.k_local), 2);
+        return MLT_OK;
+    });
+}
+
+int mlt_nccl_unique_id(uint8_t out[128]) {
+    return guard([&] {
+        mlt::nccl_unique_id(out);
+        return MLT_OK;
+    });
+}
 
 mlt_dag* mlt_execution_dag(const mlt_dag* ref, const mlt_model_spec_t* m, const mlt_policy_t* p,
                            int exact_gates, mlt_runtime_info_t* info) {

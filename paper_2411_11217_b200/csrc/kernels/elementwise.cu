@@ -113,9 +113,29 @@ __global__ void combine_kernel(const float* h, const float* y, int ldy, const in
             const float4 v = *reinterpret_cast<const float4*>(y + static_cast<int64_t>(inv[t * K + s]) * ldy + i);
             acc.x += ws * v.x; acc.y += ws * v.y; acc.z += ws * v.z; acc.w += ws * v.w;
         }
-        const float4 r = *reinterpret_cast<const float4*>(h + static_cast<int64_t>(t) * H + i);
+        const float4 r = h ? *reinterpret_cast<const float4*>(h + static_cast<int64_t>(t) * H + i)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
         *reinterpret_cast<float4*>(x + static_cast<int64_t>(t) * H + i) =
             make_float4(r.x + acc.x, r.y + acc.y, r.z + acc.z, r.w + acc.w);
+    }
+}
+
+// out = sum_p parts[p*stride] (+ add): split-K reduction / residual add,
+// fixed order (deterministic).
+__global__ void sum_parts_kernel(const float* parts, int n_parts, int64_t stride, const float* add,
+                                 float* out, int64_t n4) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float4 a = reinterpret_cast<const float4*>(parts)[i];
+        for (int p = 1; p < n_parts; ++p) {
+            const float4 b = reinterpret_cast<const float4*>(parts + p * stride)[i];
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        }
+        if (add) {
+            const float4 b = reinterpret_cast<const float4*>(add)[i];
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        }
+        reinterpret_cast<float4*>(out)[i] = a;
     }
 }
 
@@ -207,6 +227,17 @@ cudaError_t launch_moe_combine(const float* h, const float* y, int ldy, const in
     if (T <= 0) return cudaSuccess;
     if (H % 4 || ldy % 4) return cudaErrorInvalidValue;
     combine_kernel<<<T, 256, 0, s>>>(h, y, ldy, inv, w, H, K, x);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sum_parts(const float* parts, int n_parts, int64_t stride, const float* add,
+                             float* out, int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (n % 4 || stride % 4 || n_parts < 1) return cudaErrorInvalidValue;
+    const int64_t n4 = n / 4;
+    int grid = static_cast<int>((n4 + 255) / 256);
+    if (grid > 1184) grid = 1184;
+    sum_parts_kernel<<<grid, 256, 0, s>>>(parts, n_parts, stride, add, out, n4);
     return cudaGetLastError();
 }
 

@@ -87,6 +87,10 @@ cudaError_t launch_moe_combine(const float* h, const float* y, int ldy, const in
                                const float* topk_w, int T, int H, int K, float* x_out,
                                cudaStream_t s);
 
+// out[i] = sum_p parts[p*stride + i] (+ add[i]); n % 4 == 0.  Fixed order.
+cudaError_t launch_sum_parts(const float* parts, int n_parts, int64_t stride, const float* add,
+                             float* out, int64_t n, cudaStream_t s);
+
 // Greedy ids: argmax (ties -> lower index) of fp32 logits [T, V]; margin =
 // top1 - top2 (optional).
 cudaError_t launch_argmax(const float* logits, int T, int V, int32_t* ids, float* margin,

@@ -2,6 +2,9 @@
 // reuse edges (see exec_plan.hpp and executor.cpp's file comment).
 #include "exec_plan.hpp"
 
+#include <cmath>
+#include <stdexcept>
+
 #include "host_layout.hpp"
 #include "lightplan/opcost.hpp"
 
@@ -12,22 +15,82 @@ using lightplan::sim::ScheduleDag;
 using lightplan::sim::Task;
 using lightplan::sim::TaskKind;
 
-Catalog build_catalog(const lightplan::ModelSpec& m, const lightplan::Policy& p) {
+Shard make_shard(const lightplan::ModelSpec& m, int rank, int size) {
+    if (size < 1 || rank < 0 || rank >= size) throw std::invalid_argument("bad tensor-parallel rank/size");
+    if (m.q_heads % size || m.kv_heads % size || m.ffn_dim % size)
+        throw std::invalid_argument("tp must divide n_q, n_kv and h2");
+    Shard s;
+    s.rank = rank;
+    s.size = size;
+    s.q_heads = m.q_heads / size;
+    s.kv_heads = m.kv_heads / size;
+    s.ffn = m.ffn_dim / size;
+    s.qkv_rows = (s.q_heads + 2 * s.kv_heads) * m.head_dim();
+    s.o_k = s.q_heads * m.head_dim();
+    if (s.qkv_rows % 128 || s.ffn % 128 || s.o_k % 64)
+        throw std::invalid_argument("tp shard must keep 128-row weight blocks (qkv rows, h2/tp)");
+    return s;
+}
+
+ShardMap shard_map(const lightplan::ModelSpec& m, const Shard& s, int kind) {
+    ShardMap out;
+    const int64_t H = m.hidden_dim, d = m.head_dim(), r = s.rank;
+    const double sH = 1.0 / std::sqrt(static_cast<double>(H));
+    const double sF = 1.0 / std::sqrt(static_cast<double>(m.ffn_dim));
+    switch (kind) {
+        case kWqkv: {
+            const int64_t qn = s.q_heads * d, kn = s.kv_heads * d;
+            for (int64_t i = 0; i < s.qkv_rows; ++i)
+                out.rows.push_back(i < qn ? r * qn + i
+                                   : i < qn + kn ? m.q_heads * d + r * kn + (i - qn)
+                                                 : (m.q_heads + m.kv_heads) * d + r * kn + (i - qn - kn));
+            out.k_local = out.k_global = H;
+            out.scale = static_cast<float>(sH);
+            break;
+        }
+        case kWo:
+            for (int64_t i = 0; i < H; ++i) out.rows.push_back(i);
+            out.col0 = r * s.o_k;
+            out.k_local = s.o_k;
+            out.k_global = m.q_heads * d;
+            out.scale = static_cast<float>(sH);
+            break;
+        case kW1:
+        case kW3:
+            for (int64_t i = 0; i < s.ffn; ++i) out.rows.push_back(r * s.ffn + i);
+            out.k_local = out.k_global = H;
+            out.scale = static_cast<float>(sH);
+            break;
+        case kW2:
+            for (int64_t i = 0; i < H; ++i) out.rows.push_back(i);
+            out.col0 = r * s.ffn;
+            out.k_local = s.ffn;
+            out.k_global = m.ffn_dim;
+            out.scale = static_cast<float>(sF);
+            break;
+        default:
+            throw std::invalid_argument("shard_map: not a sharded weight kind");
+    }
+    return out;
+}
+
+Catalog build_catalog(const lightplan::ModelSpec& m, const lightplan::Policy& p, const Shard& shard_in) {
     Catalog c;
-    const int H = static_cast<int>(m.hidden_dim), F = static_cast<int>(m.ffn_dim);
+    const Shard sh = shard_in.q_heads ? shard_in : make_shard(m, 0, 1);
+    const int H = static_cast<int>(m.hidden_dim), F = static_cast<int>(sh.ffn);
     const int E = static_cast<int>(m.experts);
-    const int W = static_cast<int>((m.q_heads + 2 * m.kv_heads) * m.head_dim());
+    const int W = static_cast<int>(sh.qkv_rows);
     auto add = [&](int kind, int expert, int rows, int64_t K) {
         for (int rb = 0; rb < rows / 128; ++rb) c.blocks.push_back({kind, expert, rb, K, 128 * K * 2, false, 0});
     };
     add(kWqkv, 0, W, H);
-    add(kWo, 0, H, H);
+    add(kWo, 0, H, sh.o_k);
     for (int e = 0; e < E; ++e) {
         add(kW1, e, F, H);
         add(kW3, e, F, H);
         add(kW2, e, H, F);
     }
-    const double layer_total = lightplan::layer_weight_bytes(m).total();
+    const double layer_total = lightplan::layer_weight_bytes(m).total() / sh.size;  // per GPU
     const double router = static_cast<double>(E) * H * 2;
     const double budget = p.weights_on_gpu * layer_total - router;
     bool open = true;

@@ -31,9 +31,34 @@ struct Catalog {
     double achieved_rw = 0;           // realised r_w (router counted resident)
 };
 
+// Tensor-parallel shard of one rank: heads and the expert hidden dim are
+// split tp ways (QKV / W1 / W3 by rows, O / W2 by columns); router, norms,
+// embedding and lm_head are replicated.
+struct Shard {
+    int rank = 0, size = 1;
+    int64_t q_heads = 0, kv_heads = 0, ffn = 0;  // local counts
+    int64_t qkv_rows = 0;                        // (q_heads + 2 kv_heads) * d
+    int64_t o_k = 0;                             // q_heads * d (O projection K)
+};
+Shard make_shard(const lightplan::ModelSpec& model, int rank, int size);
+
+// Which global rows / columns this rank's local matrix of `kind` covers:
+// local (m, k) is global (rows[m], col0 + k) of the [.., k_global] tensor.
+// QKV: this rank's q heads, then k heads, then v heads; O: all rows, the
+// columns of this rank's heads; W1/W3: rows [r*h2/tp, ...); W2: all rows,
+// columns [r*h2/tp, ...).  scale = the synthetic init scale (1/sqrt(fan_in)).
+struct ShardMap {
+    std::vector<int64_t> rows;
+    int64_t col0 = 0, k_local = 0, k_global = 0;
+    float scale = 0;
+};
+ShardMap shard_map(const lightplan::ModelSpec& model, const Shard& shard, int kind);
+
 // Resident first: QKV, O, then expert row blocks in (expert, W1, W3, W2)
-// order while resident + router <= r_w * W_layer.
-Catalog build_catalog(const lightplan::ModelSpec& model, const lightplan::Policy& policy);
+// order while resident + router <= r_w * (W_layer / tp) (SURVEY.md
+// Appendix B; the reference's uniform share, per GPU under TP).
+Catalog build_catalog(const lightplan::ModelSpec& model, const lightplan::Policy& policy,
+                      const Shard& shard = Shard{});
 
 // Byte range [begin, end) of page p (1..M) of a layer blob; p = 0: whole.
 std::pair<int64_t, int64_t> page_range(int64_t blob_bytes, int M, int page);

@@ -41,13 +41,15 @@ void Runtime::host_attention(int l, int mb, int step) {
     const int G = nq_ / nkv_;
     const int t0 = mb * mu_;
     const uint16_t* qkv = h_qkv_ + static_cast<size_t>(mb) * mu_ * W_;
-    uint8_t* out = h_attn_ + static_cast<size_t>(mb) * Rmu_ * H_ * 2;
+    uint8_t* out = h_attn_ + static_cast<size_t>(mb) * Rmu_ * Ho_ * 2;  // this rank's heads
     const int32_t* pos = step_pos_.data() + static_cast<size_t>(step - 1) * N_;
     const float scale = 1.0f / std::sqrt(static_cast<float>(kD));
     // Default: all cores but two, which stay free for the resource launcher
     // threads (a descheduled GPU launcher leaves the device idle between
     // kernels of one PostAttn).
-    const int threads = opt_.host_threads > 0 ? opt_.host_threads : std::max(1, omp_get_num_procs() - 2);
+    // Under TP every rank's process shares the host cores.
+    const int threads = opt_.host_threads > 0 ? opt_.host_threads
+                                              : std::max(1, (omp_get_num_procs() - 2) / shard_.size);
 
 #pragma omp parallel num_threads(threads)
     {

@@ -56,6 +56,22 @@ void synth_bf16_packed(uint64_t seed, uint64_t tid, int64_t M, int64_t K, int64_
                 draw(key, static_cast<uint64_t>(m * K + k), a, false);
 }
 
+void synth_shard_packed(uint64_t seed, uint64_t tid, int64_t K_global, const int64_t* rows,
+                        int64_t col0, int64_t K_local, int64_t row_begin, int64_t row_end,
+                        float scale, uint16_t* dst) {
+    const uint64_t key = mix64(seed ^ mix64(tid));
+    const float a = amplitude(scale);
+    uint8_t* base = reinterpret_cast<uint8_t*>(dst);
+    const uint64_t base_off = mltk::a_packed_off(row_begin, 0, K_local);
+#pragma omp parallel for schedule(static)
+    for (int64_t m = row_begin; m < row_end; ++m) {
+        const uint64_t g = static_cast<uint64_t>(rows[m]) * static_cast<uint64_t>(K_global) + static_cast<uint64_t>(col0);
+        for (int64_t k = 0; k < K_local; ++k)
+            *reinterpret_cast<uint16_t*>(base + mltk::a_packed_off(m, k, K_local) - base_off) =
+                draw(key, g + static_cast<uint64_t>(k), a, false);
+    }
+}
+
 void pack_weight(const uint16_t* src, int64_t M, int64_t K, uint16_t* dst) {
     uint8_t* d = reinterpret_cast<uint8_t*>(dst);
 #pragma omp parallel for schedule(static)

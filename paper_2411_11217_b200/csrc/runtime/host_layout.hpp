@@ -39,6 +39,15 @@ void synth_bf16(uint64_t seed, uint64_t tid, int64_t begin, int64_t end, float s
 void synth_bf16_packed(uint64_t seed, uint64_t tid, int64_t M, int64_t K, int64_t row_begin,
                        int64_t row_end, float scale, uint16_t* dst);
 
+// Tensor-parallel shard of a synthetic [M_global, K_global] tensor in packed
+// layout: local row m is global row rows[m] (rows.size() = M_local, a multiple
+// of 128), local column k is global column col0 + k (k < K_local).  Every
+// element equals the unsharded tensor's element, so the union of the shards
+// is bit-identical to the full model.  Local rows [row_begin, row_end).
+void synth_shard_packed(uint64_t seed, uint64_t tid, int64_t K_global, const int64_t* rows,
+                        int64_t col0, int64_t K_local, int64_t row_begin, int64_t row_end,
+                        float scale, uint16_t* dst);
+
 void pack_weight(const uint16_t* src, int64_t M, int64_t K, uint16_t* dst);
 void pack_rows(const uint16_t* src, int64_t rows, int64_t K, int64_t R, uint8_t* dst);
 void unpack_rows(const uint8_t* packed, int64_t R, int64_t rows, int64_t K, uint16_t* dst);

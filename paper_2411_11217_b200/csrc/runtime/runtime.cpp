@@ -98,6 +98,12 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     W_ = (nq_ + 2 * nkv_) * d_;
     V_ = ext.vocab;
     L_ = static_cast<int>(model.layers);
+    shard_ = make_shard(model, opt.tp_rank, opt.tp_size);
+    nq_ = static_cast<int>(shard_.q_heads);
+    nkv_ = static_cast<int>(shard_.kv_heads);
+    F_ = static_cast<int>(shard_.ffn);
+    W_ = static_cast<int>(shard_.qkv_rows);
+    Ho_ = static_cast<int>(shard_.o_k);
     if (model.weight_dtype_bytes != 2 || model.kv_dtype_bytes != 2)
         throw std::invalid_argument("runtime supports bf16 weights and KV (dt_w = dt_kv = 2)");
     if (H_ % 256 || F_ % 128 || W_ % 128 || V_ % 128 || d_ != 128 || E_ > 64 || K_ > 8)
@@ -118,6 +124,7 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     ck(cudaStreamCreateWithFlags(&s_gpu_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
+    if (opt.tp_size > 1) coll_ = make_nccl_collective(opt.nccl_id, opt.tp_rank, opt.tp_size, opt.device);
     arena_ = std::make_unique<Arena>(static_cast<size_t>(opt.budget_bytes));
     build_catalog();
     allocate();
@@ -151,7 +158,7 @@ cudaStream_t Runtime::stream(lightplan::sim::Resource r) const {
 
 // Residency split and blob layout: exec_plan.cpp build_catalog.
 void Runtime::build_catalog() {
-    cat_ = mlt::build_catalog(model_, policy_);
+    cat_ = mlt::build_catalog(model_, policy_, shard_);
     layer_res_bytes_ = cat_.resident_bytes;
     layer_blob_bytes_ = cat_.blob_bytes;
     achieved_rw_ = cat_.achieved_rw;
@@ -182,7 +189,8 @@ void Runtime::allocate() {
     // activations
     d_x_ = static_cast<float*>(A.alloc(T * H_ * 4, "x"));
     d_qkv_bf16_ = static_cast<uint16_t*>(A.alloc(static_cast<size_t>(M_) * mu_ * W_ * 2, "qkv_bf16"));
-    d_attn_in_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(M_) * Rmu_ * H_ * 2, "attn_in"));
+    d_attn_in_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(M_) * Rmu_ * Ho_ * 2, "attn_in"));
+    if (coll_) d_cbuf_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * H_ * 4, "tp_combine"));
     d_xn_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Rmu_) * H_ * 2, "xn"));
     d_qkv_f32_ = static_cast<float*>(A.alloc(static_cast<size_t>(kMaxSplits) * Rmu_ * W_ * 4, "qkv_f32"));
     d_h_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * H_ * 4, "h"));
@@ -209,7 +217,7 @@ void Runtime::allocate() {
         d_kpool_ = static_cast<uint16_t*>(A.alloc(bytes, "kv_pool_k"));
         d_vpool_ = static_cast<uint16_t*>(A.alloc(bytes, "kv_pool_v"));
         d_block_table_ = static_cast<int32_t*>(A.alloc(pages * 4, "block_table"));
-        d_attn_gpu_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Rmu_) * H_ * 2, "attn_gpu"));
+        d_attn_gpu_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Rmu_) * Ho_ * 2, "attn_gpu"));
         std::vector<int32_t> bt(pages);
         for (size_t i = 0; i < pages; ++i) bt[i] = static_cast<int32_t>(i);  // per (layer, seq) page runs
         ck(cudaMemcpy(d_block_table_, bt.data(), pages * 4, cudaMemcpyHostToDevice), "block table");
@@ -229,8 +237,8 @@ void Runtime::allocate() {
 
     // host side
     ck(cudaHostAlloc(reinterpret_cast<void**>(&h_qkv_), static_cast<size_t>(M_) * mu_ * W_ * 2, 0), "h_qkv");
-    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_attn_), static_cast<size_t>(M_) * Rmu_ * H_ * 2, 0), "h_attn");
-    std::memset(h_attn_, 0, static_cast<size_t>(M_) * Rmu_ * H_ * 2);
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_attn_), static_cast<size_t>(M_) * Rmu_ * Ho_ * 2, 0), "h_attn");
+    std::memset(h_attn_, 0, static_cast<size_t>(M_) * Rmu_ * Ho_ * 2);
     ck(cudaHostAlloc(reinterpret_cast<void**>(&h_tok_), static_cast<size_t>(max_steps_) * N_ * 4 * 4, 0), "h_tok");
     if (!policy_.attn_on_gpu) {
         const size_t kv = static_cast<size_t>(L_) * N_ * nkv_ * max_ctx_ * d_;
@@ -243,7 +251,12 @@ void Runtime::generate_weights() {
     const double t0 = now_s();
     const uint64_t seed = ext_.seed;
     const double sH = 1.0 / std::sqrt(static_cast<double>(H_));
-    const double sF = 1.0 / std::sqrt(static_cast<double>(F_));
+    // this rank's slice of every sharded matrix (exec_plan.cpp shard_map)
+    const ShardMap maps[] = {shard_map(model_, shard_, kWqkv), shard_map(model_, shard_, kWo),
+                             shard_map(model_, shard_, kW1), shard_map(model_, shard_, kW2)};
+    auto map_of = [&](int kind) -> const ShardMap& {
+        return kind == kWqkv ? maps[0] : kind == kWo ? maps[1] : kind == kW2 ? maps[3] : maps[2];
+    };
     host_blob_pinned_ = opt_.pin_weights != 0;
     if (layer_blob_bytes_) {
         host_blob_ = host_alloc(static_cast<size_t>(L_) * layer_blob_bytes_, host_blob_pinned_, &pin_seconds_);
@@ -254,13 +267,11 @@ void Runtime::generate_weights() {
     for (int l = 0; l < L_; ++l) {
         int idx_qkv = 0, idx_o = 0;
         for (const auto& b : cat_.blocks) {
-            const bool down = b.kind == kW2;
-            const int rows = b.kind == kWqkv ? W_ : (b.kind == kWo || down) ? H_ : F_;
-            const float scale = static_cast<float>(down ? sF : sH);
             uint8_t* dst = b.resident ? res.data() + b.offset
                                       : host_blob_ + static_cast<int64_t>(l) * layer_blob_bytes_ + b.offset;
-            synth_bf16_packed(seed, tensor_id(l, b.kind, b.expert), rows, b.K, b.rb * 128,
-                              (b.rb + 1) * 128, scale, reinterpret_cast<uint16_t*>(dst));
+            const ShardMap& sm = map_of(b.kind);
+            synth_shard_packed(seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0,
+                               b.K, b.rb * 128, (b.rb + 1) * 128, sm.scale, reinterpret_cast<uint16_t*>(dst));
             int entry;
             switch (b.kind) {
                 case kWqkv: entry = tab_qkv_ + idx_qkv++; break;
@@ -374,7 +385,7 @@ size_t Runtime::debug_read(const std::string& name, void* out, size_t cap) {
     else if (name == "topk") { src = d_topk_; bytes = static_cast<size_t>(mu_) * K_ * 4; }
     else if (name == "topw") { src = d_topw_; bytes = static_cast<size_t>(mu_) * K_ * 4; }
     else if (name == "qkv_bf16") { src = d_qkv_bf16_ + static_cast<size_t>(M_ - 1) * mu_ * W_; bytes = static_cast<size_t>(mu_) * W_ * 2; }
-    else if (name == "attn_in") { src = d_attn_in_ + static_cast<size_t>(M_ - 1) * Rmu_ * H_ * 2; bytes = static_cast<size_t>(Rmu_) * H_ * 2; }
+    else if (name == "attn_in") { src = d_attn_in_ + static_cast<size_t>(M_ - 1) * Rmu_ * Ho_ * 2; bytes = static_cast<size_t>(Rmu_) * Ho_ * 2; }
     else if (name == "y") { src = d_y_; bytes = static_cast<size_t>(Re_) * H_ * 4; }
     else if (name == "inv") { src = d_inv_; bytes = static_cast<size_t>(mu_) * K_ * 4; }
     else if (name == "counts") { src = d_cnt_; bytes = static_cast<size_t>(E_) * 4; }
@@ -476,8 +487,8 @@ void Runtime::act_cpu_attn(int step, int layer, int mb) { host_attention(layer -
 
 void Runtime::act_load_hidden(int layer, int mb) {
     (void)layer;
-    const size_t off = static_cast<size_t>(mb - 1) * Rmu_ * H_ * 2;
-    kk(cudaMemcpyAsync(d_attn_in_ + off, h_attn_ + off, static_cast<size_t>(Rmu_) * H_ * 2, cudaMemcpyHostToDevice,
+    const size_t off = static_cast<size_t>(mb - 1) * Rmu_ * Ho_ * 2;
+    kk(cudaMemcpyAsync(d_attn_in_ + off, h_attn_ + off, static_cast<size_t>(Rmu_) * Ho_ * 2, cudaMemcpyHostToDevice,
                        s_h2d_),
        "load hidden");
 }
@@ -507,8 +518,8 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     mltk::GemmArgs o;
     o.a_table = tab + tab_o_;
     o.RB = H_ / 128;
-    o.K = H_;
-    o.b = policy_.attn_on_gpu ? d_attn_gpu_ : d_attn_in_ + static_cast<size_t>(mb - 1) * Rmu_ * H_ * 2;
+    o.K = Ho_;  // this rank's heads (row-parallel O under TP)
+    o.b = policy_.attn_on_gpu ? d_attn_gpu_ : d_attn_in_ + static_cast<size_t>(mb - 1) * Rmu_ * Ho_ * 2;
     o.R = Rmu_;
     o.rows_dense = mu_;
     dense_tiling(H_ / 128, o.n_cap, o.n_chunks, o.k_splits);
@@ -516,14 +527,24 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     o.split_stride = static_cast<int64_t>(mu_) * H_;
     o.out_f32 = o_split ? d_hparts_ : d_h_;
     o.ldo = H_;
-    o.residual = x;  // added by the GEMM epilogue (unsplit) or by the router (split)
+    o.residual = coll_ ? nullptr : x;  // unsplit single GPU: residual in the GEMM epilogue
     o.ldr = H_;
     kl("o_gemm", mltk::launch_gemm(o, num_sms_, s_gpu_));
-    // (split-K reduce + residual ->) RMSNorm + router + permute
-    kl("router", mltk::launch_router(o_split ? d_hparts_ : d_h_, d_ffn_norm_[l], ext_.rms_eps, nullptr,
-                                     d_router_[l], mu_, H_, E_, K_, d_hn_, nullptr, d_topk_, d_topw_, s_gpu_,
-                                     o_split ? o.k_splits : 0, o.split_stride, o_split ? x : nullptr,
-                                     o_split ? d_h_ : nullptr));
+    if (coll_) {
+        // TP all-reduce #1: h = x + sum over ranks of this rank's O partial
+        if (o_split)
+            kl("sum_parts", mltk::launch_sum_parts(d_hparts_, o.k_splits, o.split_stride, nullptr, d_h_,
+                                                   static_cast<int64_t>(mu_) * H_, s_gpu_));
+        coll_->all_reduce_sum(d_h_, static_cast<size_t>(mu_) * H_, s_gpu_);
+        kl("router", mltk::launch_router(d_h_, d_ffn_norm_[l], ext_.rms_eps, nullptr, d_router_[l], mu_, H_, E_,
+                                         K_, d_hn_, nullptr, d_topk_, d_topw_, s_gpu_, 1, 0, x, d_h_));
+    } else {
+        // (split-K reduce + residual ->) RMSNorm + router
+        kl("router", mltk::launch_router(o_split ? d_hparts_ : d_h_, d_ffn_norm_[l], ext_.rms_eps, nullptr,
+                                         d_router_[l], mu_, H_, E_, K_, d_hn_, nullptr, d_topk_, d_topw_, s_gpu_,
+                                         o_split ? o.k_splits : 0, o.split_stride, o_split ? x : nullptr,
+                                         o_split ? d_h_ : nullptr));
+    }
     kl("moe_permute", mltk::launch_moe_permute(d_topk_, d_hn_, mu_, H_, E_, K_, d_cnt_, d_off_, d_perm_, d_inv_,
                                                d_xe_, Re_, s_gpu_));
     // experts: gate/up (SiLU fused) -> down -> combine
@@ -555,7 +576,14 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     dn.out_f32 = d_y_;
     dn.ldo = H_;
     kl("expert_down_gemm", mltk::launch_gemm(dn, num_sms_, s_gpu_));
-    kl("moe_combine", mltk::launch_moe_combine(d_h_, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, x, s_gpu_));
+    if (coll_) {
+        // TP all-reduce #2: x = h + sum over ranks of this rank's top-k combine (h2 shard)
+        kl("moe_combine", mltk::launch_moe_combine(nullptr, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, d_cbuf_, s_gpu_));
+        coll_->all_reduce_sum(d_cbuf_, static_cast<size_t>(mu_) * H_, s_gpu_);
+        kl("residual_add", mltk::launch_sum_parts(d_cbuf_, 1, 0, d_h_, x, static_cast<int64_t>(mu_) * H_, s_gpu_));
+    } else {
+        kl("moe_combine", mltk::launch_moe_combine(d_h_, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, x, s_gpu_));
+    }
     if (layer == L_) {  // step epilogue: final norm -> lm_head -> greedy ids
         kl("rmsnorm_pack", mltk::launch_rmsnorm_pack(x, d_final_norm_, mu_, H_, ext_.rms_eps, d_xn_, Rmu_, s_gpu_));
         mltk::GemmArgs lm;

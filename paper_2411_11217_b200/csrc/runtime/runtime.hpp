@@ -19,6 +19,7 @@
 
 #include <cuda_runtime.h>
 
+#include "collective.hpp"
 #include "exec_plan.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
@@ -40,6 +41,8 @@ struct RuntimeOptions {
     int host_threads = 0;        // CPU attention threads (0: all)
     int pin_weights = 1;         // 1: streamed blob pinned; 0: pageable + pinned staging ring
     int exact_gates = 1;         // 1: data-exact weight gates; 0: reference gates (all pages of g)
+    int tp_rank = 0, tp_size = 1;  // tensor parallelism (one process per GPU)
+    uint8_t nccl_id[128] = {};     // ncclUniqueId from rank 0 (tp_size > 1)
 };
 
 // Bump allocator over one cudaMalloc of the budget (SURVEY.md §7 hard part 5).
@@ -150,7 +153,12 @@ class Runtime {
     ModelExt ext_;
     lightplan::Policy policy_;
     RuntimeOptions opt_;
-    int N_, mu_, M_, H_, F_, E_, K_, nq_, nkv_, d_, W_, V_, L_;
+    // dims; under TP nq_, nkv_, F_, W_ and Ho_ (attention output width) are
+    // this rank's shard (exec_plan.hpp Shard)
+    int N_, mu_, M_, H_, F_, E_, K_, nq_, nkv_, d_, W_, V_, L_, Ho_;
+    Shard shard_;
+    std::unique_ptr<Collective> coll_;
+    float* d_cbuf_ = nullptr;  // [mu, H] TP expert-combine partial (all-reduced)
     int Rmu_, Re_, ncap_, ncap_e_;
     int num_sms_ = 148;
 
