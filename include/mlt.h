@@ -384,8 +384,10 @@ int mlt_runtime_decode(mlt_runtime* rt, const int32_t* host_tokens, const int32_
 mlt_dag* mlt_execution_dag(const mlt_dag* reference, const mlt_model_spec_t* model,
                            const mlt_policy_t* policy, int exact_gates,
                            mlt_runtime_info_t* info);
-/* Live per-kernel breakdown of the last decode (CUDA-event deltas on the
- * compute stream): JSON [{"name","ms","launches"}...]; returns length. */
+/* Live per-kernel breakdown of the last decode: JSON {"events": [...],
+ * "exec": [...]} of {"name","ms","launches"}; "events" are CUDA-event deltas
+ * on the compute stream (include host-launch gaps), "exec" the GEMMs'
+ * in-kernel first-CTA-start..last-CTA-end time.  Returns length. */
 int mlt_runtime_kernel_profile(mlt_runtime* rt, char* buf, size_t cap);
 /* timeline_json of the last decode's measured timeline; returns length. */
 int mlt_runtime_timeline_json(mlt_runtime* rt, char* buf, size_t cap);

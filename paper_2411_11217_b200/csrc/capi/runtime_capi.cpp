@@ -24,7 +24,7 @@ struct Handle {
     lightplan::sim::ScheduleDag dag;
     lightplan::sim::Timeline tl;
     bool has_tl = false;
-    std::vector<mlt::DecodeReport::KernelTime> kernels;
+    std::vector<mlt::DecodeReport::KernelTime> kernels, kernel_exec;
 };
 
 Handle* H(mlt_runtime* r) { return reinterpret_cast<Handle*>(r); }
@@ -176,6 +176,7 @@ int mlt_runtime_decode(mlt_runtime* r, const int32_t* tokens, const int32_t* for
         const mlt::DecodeReport d = h->rt->decode(tokens, forced, steps, out, &h->dag, &h->tl);
         h->has_tl = true;
         h->kernels = d.kernels;
+        h->kernel_exec = d.kernel_exec;
         if (rep) {
             rep->seconds = d.seconds;
             rep->tokens_per_second = d.tokens_per_second;
@@ -200,15 +201,21 @@ int mlt_runtime_decode(mlt_runtime* r, const int32_t* tokens, const int32_t* for
 
 int mlt_runtime_kernel_profile(mlt_runtime* r, char* buf, size_t cap) {
     return guard([&] {
-        std::string s = "[";
+        std::string s = "{";
         char line[256];
-        for (size_t i = 0; i < H(r)->kernels.size(); ++i) {
-            const auto& k = H(r)->kernels[i];
-            std::snprintf(line, sizeof line, "%s{\"name\":\"%s\",\"ms\":%.6f,\"launches\":%d}", i ? "," : "",
-                          k.name.c_str(), k.ms, k.launches);
-            s += line;
+        const char* keys[2] = {"events", "exec"};
+        const std::vector<mlt::DecodeReport::KernelTime>* lists[2] = {&H(r)->kernels, &H(r)->kernel_exec};
+        for (int L = 0; L < 2; ++L) {
+            s += std::string(L ? "," : "") + "\"" + keys[L] + "\":[";
+            for (size_t i = 0; i < lists[L]->size(); ++i) {
+                const auto& k = (*lists[L])[i];
+                std::snprintf(line, sizeof line, "%s{\"name\":\"%s\",\"ms\":%.6f,\"launches\":%d}", i ? "," : "",
+                              k.name.c_str(), k.ms, k.launches);
+                s += line;
+            }
+            s += "]";
         }
-        s += "]";
+        s += "}";
         if (buf && cap) {
             const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
             std::memcpy(buf, s.data(), n);

@@ -157,6 +157,13 @@ __device__ __forceinline__ uint32_t idesc_bf16(uint32_t M, uint32_t N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// Device-wide nanosecond timer (same timebase on every SM).
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ uint32_t warp_idx_sync() {
     return __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
 }

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
 
     const uint32_t warp = warp_idx_sync();
     const uint32_t lane = threadIdx.x & 31;
+    if (a.timing && threadIdx.x == 0) atomicMin(&a.timing[0], globaltimer());
     const int acc_cols = a.n_mats * a.n_cap;     // TMEM columns per accumulator stage
     const int acc_stages = a.acc_stages;          // 1 or 2
 
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
         tc_fence_after();
         tmem_dealloc(tmem, a.tmem_cols);
     }
+    if (a.timing && threadIdx.x == 0) atomicMin(&a.timing[1], ~globaltimer());
 }
 
 }  // namespace

@@ -27,6 +27,9 @@ struct GemmArgs {
                                      // virtual tile (rb, g, c) handles tokens c*n_cap, +n_chunks*n_cap, ...
     int k_splits = 1;                // split-K: partial s of the fp32 output goes to
     int64_t split_stride = 0;        // out_f32 + s*split_stride (residual ignored; consumer reduces)
+    // optional in-kernel timing: [0] = min over CTAs of the %globaltimer at
+    // entry, [1] = ~(max at exit); both pre-set to all ones by the caller
+    unsigned long long* timing = nullptr;
     // epilogue
     int epi = kEpiF32;
     float alpha = 1.0f;

@@ -177,6 +177,8 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
     launches_ = 0;
     marks_.clear();
     event_next_ = 0;
+    ktime_names_.clear();
+    ck(cudaMemsetAsync(d_ktime_, 0xFF, static_cast<size_t>(ktime_cap_) * 16, s_gpu_), "timer reset");
 
     std::array<std::vector<int>, lightplan::sim::kResourceCount> fifo;
     for (int i = 0; i < n; ++i) fifo[static_cast<int>(dag.tasks[i].resource)].push_back(i);
@@ -304,7 +306,24 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
         it->ms += ms;
         it->launches += 1;
     }
-    for (const auto& kt : rep.kernels) {
+    {  // in-kernel execution times of the GEMMs
+        std::vector<unsigned long long> tv(2 * ktime_names_.size());
+        if (!tv.empty())
+            ck(cudaMemcpy(tv.data(), d_ktime_, tv.size() * 8, cudaMemcpyDeviceToHost), "timers");
+        for (size_t k = 0; k < ktime_names_.size(); ++k) {
+            const unsigned long long t0 = tv[2 * k], t1 = ~tv[2 * k + 1];
+            if (t0 == ~0ull || t1 < t0) continue;  // launch had no work
+            auto it = std::find_if(rep.kernel_exec.begin(), rep.kernel_exec.end(),
+                                   [&](const DecodeReport::KernelTime& kt) { return kt.name == ktime_names_[k]; });
+            if (it == rep.kernel_exec.end()) {
+                rep.kernel_exec.push_back({ktime_names_[k], 0.0, 0});
+                it = rep.kernel_exec.end() - 1;
+            }
+            it->ms += (t1 - t0) * 1e-6;
+            it->launches += 1;
+        }
+    }
+    for (const auto& kt : rep.kernel_exec) {
         if (kt.name == "expert_gateup_gemm" || kt.name == "expert_down_gemm") rep.expert_ms_total += kt.ms;
         if (kt.name == "expert_gateup_gemm") rep.expert_launches = kt.launches;
         if (kt.name == "qkv_gemm" || kt.name == "o_gemm") {

@@ -210,6 +210,8 @@ void Runtime::allocate() {
     d_tok_out_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4, "tok_out"));
     d_pos_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4 * 2, "pos_ctx"));
     d_seq_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(N_) * 4, "seq"));
+    ktime_cap_ = max_steps_ * L_ * M_ * 4 + 16;
+    d_ktime_ = static_cast<unsigned long long*>(A.alloc(static_cast<size_t>(ktime_cap_) * 16, "kernel_timers"));
     if (policy_.attn_on_gpu) {
         max_pages_ = (max_ctx_ + page_ - 1) / page_;
         const size_t pages = static_cast<size_t>(L_) * N_ * max_pages_;
@@ -425,6 +427,12 @@ void Runtime::kl(const char* name, cudaError_t e) {
 
 void Runtime::mark_start(cudaEvent_t task_start) { marks_.push_back({nullptr, task_start}); }
 
+unsigned long long* Runtime::ktimer(const char* name) {
+    if (static_cast<int>(ktime_names_.size()) >= ktime_cap_) return nullptr;
+    ktime_names_.push_back(name);
+    return d_ktime_ + 2 * (ktime_names_.size() - 1);
+}
+
 // Dense projections have few 128-row blocks (QKV 48, O 32 for 8x7B), too
 // few to stream their weights over all SMs: split K so (row block x K-split)
 // tiles cover the chip (each weight byte is still read once).  The fp32
@@ -468,6 +476,7 @@ void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
     a.epi = mltk::kEpiF32;
     a.out_f32 = d_qkv_f32_;
     a.ldo = W_;
+    a.timing = ktimer("qkv_gemm");
     kl("qkv_gemm", mltk::launch_gemm(a, num_sms_, s_gpu_));
     const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
     uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
@@ -529,6 +538,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     o.ldo = H_;
     o.residual = coll_ ? nullptr : x;  // unsplit single GPU: residual in the GEMM epilogue
     o.ldr = H_;
+    o.timing = ktimer("o_gemm");
     kl("o_gemm", mltk::launch_gemm(o, num_sms_, s_gpu_));
     if (coll_) {
         // TP all-reduce #1: h = x + sum over ranks of this rank's O partial
@@ -562,6 +572,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     gu.epi = mltk::kEpiSiluPacked;
     gu.out_packed = d_inter_;
     gu.out_R = Re_;
+    gu.timing = ktimer("expert_gateup_gemm");
     kl("expert_gateup_gemm", mltk::launch_gemm(gu, num_sms_, s_gpu_));
     mltk::GemmArgs dn;
     dn.a_table = tab + tab_w2_;
@@ -575,6 +586,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     dn.n_cap = ncap_e_;
     dn.out_f32 = d_y_;
     dn.ldo = H_;
+    dn.timing = ktimer("expert_down_gemm");
     kl("expert_down_gemm", mltk::launch_gemm(dn, num_sms_, s_gpu_));
     if (coll_) {
         // TP all-reduce #2: x = h + sum over ranks of this rank's top-k combine (h2 shard)

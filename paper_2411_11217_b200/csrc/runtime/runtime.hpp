@@ -83,6 +83,7 @@ struct DecodeReport {
         int launches = 0;
     };
     std::vector<KernelTime> kernels;  // live per-kernel breakdown (event deltas on the compute stream)
+    std::vector<KernelTime> kernel_exec;  // in-kernel first-CTA-start to last-CTA-end (GEMMs)
 };
 
 class Runtime {
@@ -223,6 +224,12 @@ class Runtime {
     std::vector<std::pair<const char*, cudaEvent_t>> marks_;
     void kl(const char* name, cudaError_t launch_status);
     cudaEvent_t take_event();
+    // in-kernel %globaltimer slots (GEMMs): true execution time without the
+    // host-launch gaps that event deltas on an idle stream include
+    unsigned long long* d_ktime_ = nullptr;
+    std::vector<const char*> ktime_names_;
+    int ktime_cap_ = 0;
+    unsigned long long* ktimer(const char* name);
 
   public:
     void mark_start(cudaEvent_t task_start);

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--mu", type=int, default=64)
     ap.add_argument("--once", action="store_true")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--with-h2d", action="store_true", help="run a concurrent H2D copy stream")
     a = ap.parse_args()
     mu = a.mu
     KD = capi.load_kernels()
@@ -142,6 +143,13 @@ def main():
     ]
     reps = 2 if a.once else a.reps
     out = {}
+    if a.with_h2d:  # concurrent page-stream DMA into HBM, as during a paged decode
+        hsrc = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+        hdst = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+        cs = torch.cuda.Stream()
+        with torch.cuda.stream(cs):
+            for _ in range(12):
+                hdst.copy_(hsrc, non_blocking=True)
     for name, fn, nbytes in cases:
         for _ in range(2 if not a.once else 0):
             fn()
