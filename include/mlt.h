@@ -37,6 +37,7 @@ extern "C" {
 #define MLT_ERR_CUDA (-6)
 #define MLT_ERR_BUDGET (-7)
 #define MLT_ERR_INTERNAL (-8)
+#define MLT_ERR_NO_FEASIBLE (-9) /* NoFeasiblePolicyError (planner.hpp:16-18) */
 
 /* ---- spec structs: reference include/lightplan/config.hpp:12-56 ---------- */
 typedef struct mlt_hardware_spec_t {
@@ -129,6 +130,44 @@ int mlt_apply_tensor_parallelism(const mlt_hardware_spec_t* hw, int tp, int b200
 int mlt_estimate_throughput(const mlt_hardware_spec_t* hw, const mlt_model_spec_t* model,
                             const mlt_workload_spec_t* workload, const mlt_policy_t* policy,
                             mlt_plan_result_t* out);
+
+/* ---- policy search: reference planner.hpp:77-116 ------------------------- */
+typedef struct mlt_search_grid_t {
+    const int64_t* micro_batch_values;
+    int32_t n_micro_batch_values;
+    const int64_t* micro_batch_counts;
+    int32_t n_micro_batch_counts;
+    const double* weight_ratio_values;
+    int32_t n_weight_ratio_values;
+    const double* kv_ratio_values;
+    int32_t n_kv_ratio_values;
+    const int32_t* attn_on_gpu_values;
+    int32_t n_attn_on_gpu_values;
+    const int32_t* ffn_on_gpu_values;
+    int32_t n_ffn_on_gpu_values;
+} mlt_search_grid_t;
+
+/* search_policy (planner.hpp:110-116); grid NULL = SearchGrid::defaults();
+ * objective 0 = tokens/s, 1 = layer latency; ctx_override < 0 = s + n/2.
+ * MLT_ERR_NO_FEASIBLE when nothing fits (message names the constraint). */
+int mlt_search_policy(const mlt_hardware_spec_t* hw, const mlt_model_spec_t* model,
+                      const mlt_workload_spec_t* workload, const mlt_search_grid_t* grid,
+                      int objective, double ctx_override, mlt_plan_result_t* out);
+/* SearchGrid::candidate_count (grid NULL = defaults). */
+int64_t mlt_search_candidate_count(const mlt_search_grid_t* grid);
+
+/* ---- batcher: reference batcher.hpp:10-40 (Algorithm 2) ------------------ */
+typedef struct mlt_batch_params_t {
+    int64_t n_ub, ubs, gen_len, cache_size;
+    int32_t flush_partials;
+} mlt_batch_params_t;
+
+/* batch_requests: returns the number of micro-batches; out_batch[i] = the
+ * micro-batch of request i (-1 = aborted), out_slot[i] = its position there
+ * (for aborted requests: the abort order); -2 = left in an unsealed
+ * partition (only with flush_partials = 0, batcher.hpp:24-27). */
+int mlt_batch_requests(const char* const* ids, const int64_t* input_len, int32_t n,
+                       const mlt_batch_params_t* params, int32_t* out_batch, int32_t* out_slot);
 
 /* ---- CGOPipe scheduler: reference pipesim.hpp:23-136 --------------------- */
 enum { MLT_SCHED_CGOPIPE = 0, MLT_SCHED_S2 = 1, MLT_SCHED_S3 = 2, MLT_SCHED_S4 = 3 };

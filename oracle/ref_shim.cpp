@@ -13,7 +13,12 @@
 #include "lightplan/opcost.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
+#include "lightplan/batcher.hpp"
+#include <algorithm>
 #include "event_oracle.hpp"
+#include "search_reference.hpp"
+#include "batch_reference.hpp"
+#include <stdexcept>
 #include "latency_oracle.hpp"
 #include "../paper_2411_11217_b200/csrc/capi/status.hpp"
 
@@ -66,6 +71,50 @@ int ref_replay_simulate(const mlt_dag* d, mlt_timeline_entry_t* entries, double*
         *makespan = tl.makespan;
         for (int r = 0; r < 5; ++r) busy[r] = tl.busy[r];
         return MLT_OK;
+    });
+}
+
+// tests/support/search_reference.cpp — serial unpruned enumeration of the
+// grid.  Returns 1 with the winner in *policy/*objective, 0 when nothing fits.
+int ref_brute_force_search(const mlt_hardware_spec_t* hw, const mlt_model_spec_t* model,
+                           const mlt_workload_spec_t* w, const mlt_search_grid_t* grid,
+                           mlt_policy_t* policy, double* objective) {
+    return guard([&] {
+        const auto r = lightplan::testing::brute_force_search(glue::hw_in(hw), glue::model_in(model),
+                                                              glue::work_in(w), glue::grid_in(grid));
+        if (!r) return 0;
+        *policy = glue::policy_out(r->policy);
+        *objective = r->objective;
+        return 1;
+    });
+}
+
+// tests/support/batch_reference.cpp — literal replay of Algorithm 2 (no
+// flushing).  Same output convention as ref_batch_requests.
+int ref_replay_batching(const char* const* ids, const int64_t* input_len, int32_t n,
+                        const mlt_batch_params_t* p, int32_t* out_batch, int32_t* out_slot) {
+    return guard([&] {
+        std::vector<lightplan::Request> q;
+        for (int i = 0; i < n; ++i) q.push_back({ids[i], input_len[i]});
+        const auto plan = lightplan::testing::replay_batching(q, p->n_ub, p->ubs, p->gen_len, p->cache_size);
+        for (int i = 0; i < n; ++i) out_batch[i] = -2, out_slot[i] = -1;
+        auto index_of = [&](const std::string& id) {
+            for (int i = 0; i < n; ++i)
+                if (id == ids[i]) return i;
+            throw std::runtime_error("replay returned an unknown id");
+        };
+        for (size_t b = 0; b < plan.micro_batches.size(); ++b)
+            for (size_t s = 0; s < plan.micro_batches[b].size(); ++s) {
+                const int i = index_of(plan.micro_batches[b][s].id);
+                out_batch[i] = static_cast<int32_t>(b);
+                out_slot[i] = static_cast<int32_t>(s);
+            }
+        for (size_t a = 0; a < plan.aborted.size(); ++a) {
+            const int i = index_of(plan.aborted[a].id);
+            out_batch[i] = -1;
+            out_slot[i] = static_cast<int32_t>(a);
+        }
+        return static_cast<int>(plan.micro_batches.size());
     });
 }
 

@@ -43,8 +43,13 @@ class EmptyTimelineError(MltError):
     pass
 
 
+class NoFeasiblePolicyError(MltError):
+    pass
+
+
 _EXC = {-2: InfeasiblePolicyError, -3: UnsupportedCombinationError, -4: CycleDetectedError,
-        -5: EmptyTimelineError}
+        -5: EmptyTimelineError, -9: NoFeasiblePolicyError}
+ERRORS[-9] = "no feasible policy"
 
 
 class HardwareSpec(C.Structure):
@@ -134,6 +139,32 @@ class SimMetrics(C.Structure):
                 ("steady_layer_time", C.c_double)]
 
 
+class SearchGrid(C.Structure):
+    _fields_ = [("micro_batch_values", C.c_void_p), ("n_micro_batch_values", C.c_int32),
+                ("micro_batch_counts", C.c_void_p), ("n_micro_batch_counts", C.c_int32),
+                ("weight_ratio_values", C.c_void_p), ("n_weight_ratio_values", C.c_int32),
+                ("kv_ratio_values", C.c_void_p), ("n_kv_ratio_values", C.c_int32),
+                ("attn_on_gpu_values", C.c_void_p), ("n_attn_on_gpu_values", C.c_int32),
+                ("ffn_on_gpu_values", C.c_void_p), ("n_ffn_on_gpu_values", C.c_int32)]
+
+
+def make_grid(mu, counts, rw, rc, attn=(0, 1), ffn=(0, 1)):
+    """A SearchGrid over Python lists (the arrays are kept alive on the struct)."""
+    arrs = [(C.c_int64 * len(mu))(*mu), (C.c_int64 * len(counts))(*counts),
+            (C.c_double * len(rw))(*rw), (C.c_double * len(rc))(*rc),
+            (C.c_int32 * len(attn))(*attn), (C.c_int32 * len(ffn))(*ffn)]
+    g = SearchGrid(C.cast(arrs[0], C.c_void_p), len(mu), C.cast(arrs[1], C.c_void_p), len(counts),
+                   C.cast(arrs[2], C.c_void_p), len(rw), C.cast(arrs[3], C.c_void_p), len(rc),
+                   C.cast(arrs[4], C.c_void_p), len(attn), C.cast(arrs[5], C.c_void_p), len(ffn))
+    g._keep = arrs
+    return g
+
+
+class BatchParams(C.Structure):
+    _fields_ = [("n_ub", C.c_int64), ("ubs", C.c_int64), ("gen_len", C.c_int64),
+                ("cache_size", C.c_int64), ("flush_partials", C.c_int32)]
+
+
 SCHED = {"cgopipe": 0, "s2": 1, "s3": 2, "s4": 3}
 TASK_KINDS = ["pre_attn", "offload_qkv", "cpu_attn", "load_hidden", "post_attn",
               "weight_to_pinned", "weight_to_gpu", "kv_load", "gpu_attn"]
@@ -155,6 +186,13 @@ _SIGS = {
                                            P(HardwareSpec)]),
     "estimate_throughput": (C.c_int, [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(Policy),
                                       P(PlanResult)]),
+    "search_policy": (C.c_int, [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(SearchGrid),
+                                C.c_int, C.c_double, P(PlanResult)]),
+    "search_candidate_count": (C.c_int64, [P(SearchGrid)]),
+    "validate": (C.c_int, [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(Policy), C.c_char_p,
+                           C.c_size_t]),
+    "batch_requests": (C.c_int, [P(C.c_char_p), P(C.c_int64), C.c_int32, P(BatchParams),
+                                 P(C.c_int32), P(C.c_int32)]),
     "schedule_build": (C.c_void_p, [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(Policy),
                                     C.c_int, C.c_int, C.c_int]),
     "schedule_build_durations": (C.c_void_p, [P(StepDurations), C.c_int, C.c_int, C.c_int,
@@ -313,6 +351,44 @@ class Api:
                                                   C.byref(workload), C.byref(policy),
                                                   C.byref(out)))
         return out
+
+    def search_policy(self, hw, model, workload, grid=None, objective=0, ctx_override=-1.0):
+        out = PlanResult()
+        self.check(self.fn["search_policy"](C.byref(hw), C.byref(model), C.byref(workload),
+                                            C.byref(grid) if grid is not None else None, objective,
+                                            ctx_override, C.byref(out)))
+        return out
+
+    def validate(self, hw=None, model=None, workload=None, policy=None):
+        """Reference config.hpp validate(): the list of issue lines ([] = valid)."""
+        buf = C.create_string_buffer(4096)
+        ref = lambda x: C.byref(x) if x is not None else None  # noqa: E731
+        n = self.check(self.fn["validate"](ref(hw), ref(model), ref(workload), ref(policy), buf, 4096))
+        return buf.value.decode().splitlines() if n else []
+
+    def search_candidate_count(self, grid=None):
+        return self.fn["search_candidate_count"](C.byref(grid) if grid is not None else None)
+
+    def batch_requests(self, requests, n_ub, ubs, gen_len, cache_size, flush_partials=True,
+                       fn="batch_requests"):
+        """requests: list of (id, input_len).  Returns (micro_batches [[ids]], aborted [ids])."""
+        n = len(requests)
+        ids = (C.c_char_p * max(n, 1))(*[r[0].encode() for r in requests])
+        lens = (C.c_int64 * max(n, 1))(*[r[1] for r in requests])
+        ob, os_ = (C.c_int32 * max(n, 1))(), (C.c_int32 * max(n, 1))()
+        p = BatchParams(n_ub, ubs, gen_len, cache_size, int(flush_partials))
+        nb = self.check(self.fn[fn](ids, lens, n, C.byref(p), ob, os_))
+        batches = [[None] * 0 for _ in range(nb)]
+        slots = {}
+        aborted = {}
+        for i in range(n):
+            if ob[i] == -1:
+                aborted[os_[i]] = requests[i][0]
+            elif ob[i] >= 0:
+                slots[(ob[i], os_[i])] = requests[i][0]
+        for (b, s) in sorted(slots):
+            batches[b].append(slots[(b, s)])
+        return batches, [aborted[k] for k in sorted(aborted)]
 
     # --- scheduler -------------------------------------------------------
     def _dag(self, h):

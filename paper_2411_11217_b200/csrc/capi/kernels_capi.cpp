@@ -15,6 +15,7 @@
 #include "../runtime/host_layout.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
+#include "lightplan/batcher.hpp"
 #include "status.hpp"
 
 namespace {

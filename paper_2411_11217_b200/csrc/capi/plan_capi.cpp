@@ -7,6 +7,8 @@
 #include "lightplan/opcost.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
+#include "lightplan/batcher.hpp"
+#include <algorithm>
 #include "status.hpp"
 
 namespace mlt {

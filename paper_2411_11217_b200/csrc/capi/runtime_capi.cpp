@@ -10,6 +10,7 @@
 #include "../runtime/runtime.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
+#include "lightplan/batcher.hpp"
 #include "status.hpp"
 
 namespace {

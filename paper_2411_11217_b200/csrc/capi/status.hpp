@@ -33,6 +33,12 @@ int last_status();
     } catch (const NS::InfeasiblePolicyError& e) {                                   \
         mlt::set_error(e.what(), MLT_ERR_INFEASIBLE);                                                    \
         return MLT_ERR_INFEASIBLE;                                                   \
+    } catch (const NS::NoFeasiblePolicyError& e) {                                   \
+        mlt::set_error(e.what(), MLT_ERR_NO_FEASIBLE);                               \
+        return MLT_ERR_NO_FEASIBLE;                                                  \
+    } catch (const NS::InvalidBatchParametersError& e) {                             \
+        mlt::set_error(e.what(), MLT_ERR_INVALID);                                   \
+        return MLT_ERR_INVALID;                                                      \
     } catch (const NS::sim::UnsupportedCombinationError& e) {                        \
         mlt::set_error(e.what(), MLT_ERR_UNSUPPORTED);                                                    \
         return MLT_ERR_UNSUPPORTED;                                                  \

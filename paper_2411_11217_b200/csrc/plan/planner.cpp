@@ -61,6 +61,12 @@ double prefill_flops_per_layer(const ModelSpec& m, const Policy& p, const Worklo
 
 }  // namespace
 
+// Unchecked per-layer model, shared with the policy search (search.cpp).
+LatencyBreakdown layer_latency_model(const HardwareSpec& hw, const ModelSpec& m, const Policy& p,
+                                     double ctx) {
+    return model_layer(hw, m, p, ctx);
+}
+
 MemoryFootprint memory_footprint(const HardwareSpec& hw, const ModelSpec& m,
                                  const WorkloadSpec& w, const Policy& p) {
     const MemoryTotals tot = memory_totals(m, w, p.batch);

@@ -35,7 +35,13 @@ def ref():
                                                 C.POINTER(capi.Policy), C.c_double,
                                                 C.POINTER(C.c_double)]),
              "replay_simulate": (C.c_int, [C.c_void_p, C.POINTER(capi.TimelineEntry),
-                                           C.POINTER(C.c_double), C.POINTER(C.c_double)])}
+                                           C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+             "brute_force_search": (C.c_int, [C.POINTER(capi.HardwareSpec), C.POINTER(capi.ModelSpec),
+                                              C.POINTER(capi.WorkloadSpec), C.POINTER(capi.SearchGrid),
+                                              C.POINTER(capi.Policy), C.POINTER(C.c_double)]),
+             "replay_batching": (C.c_int, [C.POINTER(C.c_char_p), C.POINTER(C.c_int64), C.c_int32,
+                                           C.POINTER(capi.BatchParams), C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_int32)])}
     return capi.Api(C.CDLL(REF_SO), "ref_", extra)
 
 
