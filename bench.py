@@ -266,7 +266,7 @@ def run_mlt(args, cfg):
     rt = Runtime(model_spec(cfg), policy(cfg), budget_bytes=cfg["budget"],
                  max_ctx=cfg["prompt"] + args.warmup + args.steps + 8, vocab=cfg["vocab"],
                  device=local, exact_gates=args.gates == "exact", tp_rank=rank, tp_size=world,
-                 nccl_id=nid)
+                 nccl_id=nid, schedule=args.schedule)
     info = rt.info
     log(f"[bench] rank {rank}: runtime ready in {time.perf_counter() - t:.1f}s (weights gen "
         f"{info.gen_seconds:.1f}s, pin {info.pin_seconds:.1f}s), r_w achieved "
@@ -322,7 +322,9 @@ def run_mlt(args, cfg):
                    "gpu_budget_gb": cfg["budget"] / 1e9, "r_w": cfg["r_w"],
                    "r_w_achieved": info.achieved_weight_ratio, "A_g": cfg["a_g"],
                    "parallelism": (f"tp{world} (heads + expert h2 sharded, NCCL all-reduce x2/layer)"
-                                   if world > 1 else "single GPU, CGOPipe paging"),
+                                   if world > 1 else "single GPU, weight paging"),
+                   "schedule": ("CGOPipe" if cfg["a_g"] == 0 else "S4") if args.schedule == "auto"
+                   else args.schedule,
                    "weight_gates": args.gates,
                    "l2": "weights streamed per step (>> 126 MB L2): no flush needed"},
         "hrm": {"bound_tok_s": bound.decode_throughput, "frac": value / bound.decode_throughput,
@@ -366,6 +368,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gates", default="exact", choices=["exact", "reference"],
                     help="weight gates: data-exact (default) or the reference's all-pages gate")
+    ap.add_argument("--schedule", default="auto", choices=["auto", "cgopipe", "s2", "s3", "s4"],
+                    help="executed schedule: CGOPipe (S4 when A_g=1) or a baseline of pipesim.hpp")
     ap.add_argument("--timeline", default=None, help="write the measured timeline JSON here")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])

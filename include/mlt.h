@@ -362,6 +362,9 @@ typedef struct mlt_runtime_options_t {
     int32_t tp_rank, tp_size; /* tensor parallelism, one process per GPU (tp_size 0/1: off):
                                  heads + expert h2 sharded, 2 all-reduces per layer */
     uint8_t nccl_id[128];     /* mlt_nccl_unique_id() of rank 0, identical on every rank */
+    int32_t schedule;         /* -1: CGOPipe (S4 when A_g = 1); else an mlt_schedule_build
+                                 kind (0 CGOPipe, 1 S2, 2 S3, 3 S4; pipesim.hpp:20-21) to
+                                 execute a baseline schedule on the same kernels */
 } mlt_runtime_options_t;
 
 /* ncclUniqueId for a tensor-parallel group (call on rank 0, broadcast). */

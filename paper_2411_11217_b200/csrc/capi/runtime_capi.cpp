@@ -57,6 +57,7 @@ mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p
         opt.tp_rank = o->tp_size > 1 ? o->tp_rank : 0;
         opt.tp_size = o->tp_size > 1 ? o->tp_size : 1;
         std::memcpy(opt.nccl_id, o->nccl_id, 128);
+        opt.schedule = o->schedule;
         auto hh = std::make_unique<Handle>();
         hh->rt = std::make_unique<mlt::Runtime>(ms, ext, pol, opt);
         h = hh.release();

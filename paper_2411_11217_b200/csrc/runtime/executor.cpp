@@ -105,7 +105,7 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
     lightplan::WorkloadSpec wl;
     wl.prompt_len = pos_[0];
     wl.gen_len = steps;
-    const auto kind = policy_.attn_on_gpu ? lightplan::sim::ScheduleKind::S4 : lightplan::sim::ScheduleKind::CgoPipe;
+    const auto kind = schedule_kind();
     lightplan::Policy pol = policy_;
     ScheduleDag dag = lightplan::sim::build_schedule(
         [&](int step) {

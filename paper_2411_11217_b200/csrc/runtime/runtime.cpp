@@ -111,6 +111,8 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     if (!policy.ffn_on_gpu) throw lightplan::sim::UnsupportedCombinationError("F_g = 0 is not a B200 path");
     if (policy.attn_on_gpu && policy.kv_on_gpu < 1.0)
         throw lightplan::sim::UnsupportedCombinationError("A_g = 1 requires r_c = 1 (resident paged KV) in this build");
+    if (opt.schedule < -1 || opt.schedule > 3) throw std::invalid_argument("schedule must be -1 or 0..3");
+    schedule_kind();  // rejects S4 without A_g / CGOPipe,S2,S3 with A_g (pipesim.cpp:283-290)
     if (opt.max_ctx <= 0) throw std::invalid_argument("max_ctx must be > 0");
     max_ctx_ = opt.max_ctx;
     Rmu_ = round_up(mu_, 16);

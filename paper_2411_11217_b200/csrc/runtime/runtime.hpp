@@ -43,6 +43,7 @@ struct RuntimeOptions {
     int exact_gates = 1;         // 1: data-exact weight gates; 0: reference gates (all pages of g)
     int tp_rank = 0, tp_size = 1;  // tensor parallelism (one process per GPU)
     uint8_t nccl_id[128] = {};     // ncclUniqueId from rank 0 (tp_size > 1)
+    int schedule = -1;             // -1: CGOPipe (S4 when A_g = 1); else a ScheduleKind to execute
 };
 
 // Bump allocator over one cudaMalloc of the budget (SURVEY.md §7 hard part 5).
@@ -145,6 +146,16 @@ class Runtime {
     void generate_weights();
     void host_attention(int layer, int mb, int step);
     int slot_of(int global_layer) const { return global_layer & 1; }
+    // The schedule this runtime executes: opt_.schedule, or CGOPipe / S4 by A_g.
+    lightplan::sim::ScheduleKind schedule_kind() const {
+        using K = lightplan::sim::ScheduleKind;
+        if (opt_.schedule < 0) return policy_.attn_on_gpu ? K::S4 : K::CgoPipe;
+        const K k = static_cast<K>(opt_.schedule);
+        if ((k == K::S4) != policy_.attn_on_gpu)
+            throw lightplan::sim::UnsupportedCombinationError(std::string(lightplan::sim::to_string(k)) +
+                                                              (policy_.attn_on_gpu ? " needs A_g = 0" : " needs A_g = 1"));
+        return k;
+    }
     std::pair<int64_t, int64_t> page_range(int page) const {  // [begin, end) within layer blob
         return mlt::page_range(layer_blob_bytes_, M_, page);
     }

@@ -21,7 +21,7 @@ class RuntimeOptions(C.Structure):
                 ("host_threads", C.c_int32), ("pin_weights", C.c_int32), ("vocab", C.c_int32),
                 ("rms_eps", C.c_float), ("rope_theta", C.c_float), ("lm_head_scale", C.c_float),
                 ("seed", C.c_uint64), ("exact_gates", C.c_int32), ("tp_rank", C.c_int32),
-                ("tp_size", C.c_int32), ("nccl_id", C.c_uint8 * 128)]
+                ("tp_size", C.c_int32), ("nccl_id", C.c_uint8 * 128), ("schedule", C.c_int32)]
 
 
 def nccl_unique_id() -> bytes:
@@ -86,13 +86,14 @@ class Runtime:
                  max_ctx: int, vocab: int = 32000, seed: int = 1234, device: int = 0,
                  host_threads: int = 0, pin_weights: bool = True, rms_eps: float = 1e-5,
                  rope_theta: float = 1e6, lm_head_scale: float = 4.0, exact_gates: bool = True,
-                 tp_rank: int = 0, tp_size: int = 1, nccl_id: bytes = b""):
+                 tp_rank: int = 0, tp_size: int = 1, nccl_id: bytes = b"", schedule: str = "auto"):
         self.api, self.f = _fns()
         self.model, self.policy = model, policy
         nid = (C.c_uint8 * 128)(*(nccl_id.ljust(128, b"\0")[:128]))
         self.opts = RuntimeOptions(device, budget_bytes, max_ctx, host_threads, int(pin_weights),
                                    vocab, rms_eps, rope_theta, lm_head_scale, seed,
-                                   int(exact_gates), tp_rank, tp_size, nid)
+                                   int(exact_gates), tp_rank, tp_size, nid,
+                                   -1 if schedule == "auto" else capi.SCHED[schedule])
         self.h = self.f["runtime_create"](C.byref(model), C.byref(policy), C.byref(self.opts))
         if not self.h:
             code = self.api.fn["last_status"]()

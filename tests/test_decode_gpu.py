@@ -199,3 +199,24 @@ def test_one_layer_stage_by_stage():
                            m.tensor(0, orc.T_W2, e), True)
             out[t] += w[t, s] * y[0]
     assert rel(rt.residual(), out) < 1e-4
+
+
+def test_executed_baseline_schedules_match_cgopipe(prompt):
+    """S2 / S3 (pipesim.cpp s2/s3: whole-layer transfers, no page pipelining)
+    run through the same executor and kernels as CGOPipe: only the issue order
+    and dependencies change, so ids and the residual are bit-identical."""
+    outs = {}
+    for kind in ("cgopipe", "s2", "s3"):
+        rt = Runtime(_model(TINY), capi.Policy(N, MU, 0, 1, 0.25, 0.0), budget_bytes=4e9, max_ctx=64,
+                     vocab=VOCAB, seed=1234, schedule=kind)
+        first = rt.decode(prompt[0], PROMPT, forced=prompt)
+        rest = rt.decode(first.ids[-1], 8)
+        assert first.report.timeline_ok == 1 and rest.report.timeline_ok == 1
+        assert rest.report.h2d_weight_bytes == pytest.approx(8 * 2 * rt.info.streamed_bytes_per_layer)
+        outs[kind] = (np.asarray(first.ids), np.asarray(rest.ids), rt.residual())
+    for kind in ("s2", "s3"):
+        for a, b in zip(outs[kind], outs["cgopipe"]):
+            assert np.array_equal(a, b), kind
+    with pytest.raises(capi.UnsupportedCombinationError):
+        Runtime(_model(TINY), capi.Policy(N, MU, 0, 1, 0.25, 0.0), budget_bytes=4e9, max_ctx=64,
+                vocab=VOCAB, seed=1234, schedule="s4")
