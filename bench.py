@@ -272,8 +272,18 @@ def run_mlt(args, cfg):
         f"{info.gen_seconds:.1f}s, pin {info.pin_seconds:.1f}s), r_w achieved "
         f"{info.achieved_weight_ratio:.4f}, streamed {info.streamed_bytes_per_layer / 1e9:.3f} GB/layer, "
         f"arena {info.arena_used / 1e9:.2f} GB")
-    rt.prefill_synthetic(cfg["prompt"], 9012)
-    toks = np.random.default_rng(5678).integers(0, cfg["vocab"], cfg["N"], dtype=np.int32)
+    prep = None
+    if args.prefill:
+        # GPU prefill of real (synthetic-id) prompts: KV and first tokens computed, not generated
+        prompts = np.random.default_rng(5678).integers(0, cfg["vocab"], (cfg["N"], cfg["prompt"]),
+                                                       dtype=np.int32)
+        toks, prep = rt.prefill(prompts)
+        log(f"[bench] rank {rank}: GPU prefill {prep.prompt_tokens} tokens in {prep.seconds:.3f}s "
+            f"({prep.tokens_per_second:.0f} tok/s, chunk {prep.chunk_tokens} x {prep.chunks_per_layer}, "
+            f"GPU busy {prep.gpu_busy_seconds:.3f}s)")
+    else:
+        rt.prefill_synthetic(cfg["prompt"], 9012)
+        toks = np.random.default_rng(5678).integers(0, cfg["vocab"], cfg["N"], dtype=np.int32)
     w = rt.decode(toks, args.warmup)
     last = w.ids[-1]
     log(f"[bench] rank {rank}: warm-up {args.warmup} steps: {w.report.tokens_per_second:.1f} tok/s")
@@ -345,6 +355,25 @@ def run_mlt(args, cfg):
         "timeline_ok": bool(rep.timeline_ok),
         "clocks": clocks,
     }
+    if prep is not None:
+        gen = cfg["gen"]
+        n_tok = cfg["N"] * gen
+        model_prefill_s = n_tok / bound.generation_throughput - n_tok / bound.decode_throughput
+        step_s = dev_s / args.steps
+        line["prefill"] = {
+            "seconds": prep.seconds, "prompt_tokens": prep.prompt_tokens,
+            "tokens_per_second": prep.tokens_per_second,
+            "hrm_model_seconds": model_prefill_s, "hrm_frac": model_prefill_s / prep.seconds,
+            "chunk_tokens": prep.chunk_tokens, "chunks_per_layer": prep.chunks_per_layer,
+            "gpu_busy_seconds": prep.gpu_busy_seconds, "gpu_launches": prep.gpu_launches,
+            "h2d_gb": prep.h2d_bytes / 1e9, "d2h_gb": prep.d2h_bytes / 1e9,
+            "kv": "computed on the GPU and written to the host cache (A_g=0) / device pool (A_g=1)"}
+        line["generation"] = {
+            "metric": "generation tok/s = N*gen / (prefill + gen decode steps)",
+            "value": n_tok / (prep.seconds + gen * step_s), "unit": "tok/s",
+            "decode_steps_measured": args.steps, "gen_len": gen,
+            "hrm_bound": bound.generation_throughput,
+            "note": "prefill measured; decode time = gen_len x the measured per-step time"}
     del rt
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         tok_s, cores, times = cpu_sample(cfg, 3)
@@ -370,6 +399,8 @@ def main():
                     help="weight gates: data-exact (default) or the reference's all-pages gate")
     ap.add_argument("--schedule", default="auto", choices=["auto", "cgopipe", "s2", "s3", "s4"],
                     help="executed schedule: CGOPipe (S4 when A_g=1) or a baseline of pipesim.hpp")
+    ap.add_argument("--prefill", action="store_true",
+                    help="run the GPU prefill on synthetic prompt ids instead of synthetic prompt KV")
     ap.add_argument("--timeline", default=None, help="write the measured timeline JSON here")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])

@@ -319,6 +319,19 @@ int mlt_kv_append(const uint16_t* qkv_bf16, int nq, int nkv, int d, const int32_
                   const int32_t* pos, int T, const int32_t* block_table, int max_pages, int page,
                   uint16_t* k_pool, uint16_t* v_pool, void* stream);
 
+/* Causal GQA prefill attention (kernels/attention_prefill.cu).  qkv: roped
+ * bf16 rows [T][W], W = (nq + 2 nkv) d; tiles: n_tiles x {first row of the
+ * sequence, its length, first query position (multiple of 16), 0}; output
+ * packed bf16 rows (capacity R) of width nq*d.  d = 128, nq/nkv <= 8. */
+int mlt_prefill_attention(const uint16_t* qkv, int W, const int32_t* tiles, int n_tiles, int nq, int nkv,
+                          int d, void* out_packed, int R, void* stream);
+/* K/V rows of a prefill chunk -> per-sequence [nkv][len][d] staging (the
+ * layout one strided copy lands in the host KV cache).  tok_seq/tok_pos per
+ * row; seq_row0/seq_len per sequence of the chunk. */
+int mlt_kv_stage(const uint16_t* qkv, int W, int nq, int nkv, int d, const int32_t* tok_seq,
+                 const int32_t* tok_pos, const int32_t* seq_row0, const int32_t* seq_len, int T,
+                 uint16_t* stage_k, uint16_t* stage_v, void* stream);
+
 /* Host: rotary cos/sin table [max_pos][d/2] as (cos, sin) float pairs, angle
  * computed in double (theta^(-2i/d) * pos). */
 int mlt_rope_table(int max_pos, int d, double theta, float* host_out);
@@ -365,6 +378,7 @@ typedef struct mlt_runtime_options_t {
     int32_t schedule;         /* -1: CGOPipe (S4 when A_g = 1); else an mlt_schedule_build
                                  kind (0 CGOPipe, 1 S2, 2 S3, 3 S4; pipesim.hpp:20-21) to
                                  execute a baseline schedule on the same kernels */
+    int32_t prefill_chunk_tokens; /* 0: largest chunk the budget allows (<= 8192 tokens) */
 } mlt_runtime_options_t;
 
 /* ncclUniqueId for a tensor-parallel group (call on rank 0, broadcast). */
@@ -412,6 +426,26 @@ void mlt_runtime_destroy(mlt_runtime* rt);
 int mlt_runtime_info(const mlt_runtime* rt, mlt_runtime_info_t* out);
 /* Synthetic prompt-stage KV for positions [0, prompt_len); positions := prompt_len. */
 int mlt_runtime_prefill_synthetic(mlt_runtime* rt, int prompt_len, uint64_t seed);
+/* GPU prefill of real prompts (cost
+ * model planner.cpp:110-150).  tokens: the N prompts concatenated, lens[N]
+ * >= 1 each (< max_ctx); first_ids[N]: the greedy token after each prompt.
+ * Zigzag order (layer by layer over chunks of whole sequences, streamed
+ * weights double-buffered in the HBM pool); KV to the host cache (A_g = 0)
+ * or the paged device pool (A_g = 1).  Positions become lens[i]; decode
+ * continues from there.  MLT_ERR_BUDGET when the arena has no room for a
+ * chunk holding the longest prompt. */
+typedef struct mlt_prefill_report_t {
+    double seconds;              /* device-timed, host token upload and id download included */
+    double tokens_per_second;    /* prompt tokens / s */
+    int64_t prompt_tokens;
+    int32_t chunk_tokens, chunks_per_layer;
+    double h2d_weight_bytes, h2d_bytes, d2h_bytes;
+    double gpu_busy_seconds;     /* compute-stream time summed over chunks */
+    int32_t gpu_launches;
+} mlt_prefill_report_t;
+int mlt_runtime_prefill(mlt_runtime* r, const int32_t* tokens, const int32_t* lens, int32_t* first_ids,
+                        mlt_prefill_report_t* rep);
+
 int mlt_runtime_set_positions(mlt_runtime* rt, const int32_t* host_pos);
 /* `steps` decode steps: host_tokens [N] (step-0 ids), host_forced [steps][N]
  * or NULL (teacher forcing), host_out [steps][N] greedy ids. */

@@ -478,6 +478,8 @@ _KSIGS = {
     "gqa_decode_paged": [V, I, V, V, V, I, V, V, I, I, I, I, I, V, I, V, V],
     "kv_append": [V, I, I, I, V, V, I, V, I, I, V, V, V],
     "rope_table": [I, I, C.c_double, V],
+    "prefill_attention": [V, I, V, I, I, I, I, V, I, V],
+    "kv_stage": [V, I, I, I, I, V, V, V, V, I, V, V, V],
     "synth_bf16": [C.c_uint64, C.c_uint64, C.c_int64, F, I, V],
 }
 

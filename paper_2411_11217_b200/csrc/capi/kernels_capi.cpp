@@ -236,6 +236,27 @@ int mlt_kv_append(const uint16_t* qkv, int nq, int nkv, int d, const int32_t* se
     });
 }
 
+int mlt_prefill_attention(const uint16_t* qkv, int W, const int32_t* tiles, int n_tiles, int nq, int nkv,
+                          int d, void* out_packed, int R, void* s) {
+    return guard([&] {
+        ck(mltk::launch_prefill_attention(qkv, W, reinterpret_cast<const int4*>(tiles), n_tiles, nq, nkv, d,
+                                          reinterpret_cast<uint8_t*>(out_packed), R, st(s)),
+           "prefill_attention");
+        return MLT_OK;
+    });
+}
+
+int mlt_kv_stage(const uint16_t* qkv, int W, int nq, int nkv, int d, const int32_t* tok_seq,
+                 const int32_t* tok_pos, const int32_t* seq_row0, const int32_t* seq_len, int T,
+                 uint16_t* stage_k, uint16_t* stage_v, void* s) {
+    return guard([&] {
+        ck(mltk::launch_kv_stage(qkv, W, nq, nkv, d, tok_seq, tok_pos, seq_row0, seq_len, T, stage_k, stage_v,
+                                 st(s)),
+           "kv_stage");
+        return MLT_OK;
+    });
+}
+
 int mlt_rope_table(int max_pos, int d, double theta, float* out) {
     return guard([&] {
         const int half = d / 2;

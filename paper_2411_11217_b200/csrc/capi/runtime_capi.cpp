@@ -58,6 +58,7 @@ mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p
         opt.tp_size = o->tp_size > 1 ? o->tp_size : 1;
         std::memcpy(opt.nccl_id, o->nccl_id, 128);
         opt.schedule = o->schedule;
+        opt.prefill_chunk_tokens = o->prefill_chunk_tokens;
         auto hh = std::make_unique<Handle>();
         hh->rt = std::make_unique<mlt::Runtime>(ms, ext, pol, opt);
         h = hh.release();
@@ -160,6 +161,17 @@ int mlt_runtime_info(const mlt_runtime* r, mlt_runtime_info_t* out) {
 int mlt_runtime_prefill_synthetic(mlt_runtime* r, int prompt_len, uint64_t seed) {
     return guard([&] {
         H(r)->rt->prefill_synthetic(prompt_len, seed);
+        return MLT_OK;
+    });
+}
+
+int mlt_runtime_prefill(mlt_runtime* r, const int32_t* tokens, const int32_t* lens, int32_t* first_ids,
+                        mlt_prefill_report_t* rep) {
+    return guard([&] {
+        const mlt::PrefillReport p = H(r)->rt->prefill(tokens, lens, first_ids);
+        if (rep)
+            *rep = {p.seconds, p.tokens_per_second, p.prompt_tokens, p.chunk_tokens, p.chunks_per_layer,
+                    p.h2d_weight_bytes, p.h2d_bytes, p.d2h_bytes, p.gpu_busy_seconds, p.gpu_launches};
         return MLT_OK;
     });
 }

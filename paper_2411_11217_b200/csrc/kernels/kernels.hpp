@@ -118,4 +118,19 @@ cudaError_t launch_kv_append(const uint16_t* qkv_bf16, int nq, int nkv, int d,
                              const int32_t* block_table, int max_pages, int page,
                              uint16_t* k_pool, uint16_t* v_pool, cudaStream_t s);
 
+// ---- prefill (attention_prefill.cu) --------------------------------------
+// Causal GQA over a chunk of whole prompt sequences.  qkv: roped bf16 rows
+// [T][W]; tiles[i] = {first row of the sequence, its length, first query
+// position (multiple of 16)}; one CTA per (tile, kv head).  Output: packed
+// bf16 operand (capacity R) of the O projection.
+cudaError_t launch_prefill_attention(const uint16_t* qkv, int W, const int4* tiles, int n_tiles, int nq,
+                                     int nkv, int d, uint8_t* out_packed, int R, cudaStream_t s);
+// K/V rows -> per-sequence [n_kv][len][d] staging (sequence s at row
+// seq_row0[s] * n_kv * d) for one strided D2H copy per sequence.
+cudaError_t launch_kv_stage(const uint16_t* qkv, int W, int nq, int nkv, int d, const int32_t* tok_seq,
+                            const int32_t* tok_pos, const int32_t* seq_row0, const int32_t* seq_len, int T,
+                            uint16_t* stage_k, uint16_t* stage_v, cudaStream_t s);
+// dst[i] = x[idx[i]] (fp32 rows of width H).
+cudaError_t launch_gather_rows(const float* x, const int32_t* idx, int n, int H, float* dst, cudaStream_t s);
+
 }  // namespace mltk

@@ -24,7 +24,7 @@ namespace mltk {
 namespace {
 
 constexpr int kMaxE = 64;
-constexpr int kMaxSlots = 4096;
+constexpr int kMaxSlots = 16384;  // T*K per launch (prefill chunks)
 
 __global__ void router_kernel(const float* x, const uint16_t* gamma, float eps,
                               const uint16_t* hn_in, const uint16_t* w, int H, int E, int K,
@@ -131,53 +131,56 @@ __global__ void router_kernel(const float* x, const uint16_t* gamma, float eps,
     }
 }
 
-// Exclusive prefix over the block of a per-thread 0/1 flag, in thread order.
-__device__ __forceinline__ int block_excl_scan(int flag, int* warp_tot, int* total) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const unsigned bal = __ballot_sync(0xffffffffu, flag);
-    const int in_warp = __popc(bal & ((1u << lane) - 1u));
-    __syncthreads();
-    if (lane == 0) warp_tot[warp] = __popc(bal);
-    __syncthreads();
-    int base = 0, tot = 0;
-    for (int i = 0; i < nw; ++i) {
-        const int c = warp_tot[i];
-        if (i < warp) base += c;
-        tot += c;
-    }
-    *total = tot;
-    return base + in_warp;
-}
-
 __global__ void permute_kernel(const int32_t* topk_idx, const uint16_t* hn, int T, int H, int E,
                                int K, int32_t* counts, int32_t* offsets, int32_t* perm,
                                int32_t* inv, uint8_t* xp, int R) {
     __shared__ int s_cnt[kMaxE];
     __shared__ int s_off[kMaxE + 1];
-    __shared__ int warp_tot[32];
-    extern __shared__ int s_slot_row[];  // [T*K] padded row of each slot
+    extern __shared__ int dyn[];
+    const int nt = blockDim.x, tid = threadIdx.x;
+    int* hist = dyn;                    // [E][nt]: slots of expert e in thread t's run
+    int* s_slot_row = dyn + E * nt;     // [T*K] padded row of each slot
     const int TK = T * K;
-    // Ranks: slot i = t*K + s; for expert e, rank = #slots j < i choosing e.
-    // Slots are processed in chunks of blockDim (thread order == slot order).
-    for (int e = 0; e < E; ++e) {
-        int running = 0;
-        for (int base = 0; base < TK; base += blockDim.x) {
-            const int i = base + threadIdx.x;
-            const int flag = (i < TK && topk_idx[i] == e) ? 1 : 0;
-            int tot;
-            const int r = block_excl_scan(flag, warp_tot, &tot);
-            if (flag) s_slot_row[i] = running + r;  // rank within expert for now
-            running += tot;
+    // Slot i = t*K + s.  Thread t owns the contiguous run [t*per, (t+1)*per),
+    // so "rank within expert = #earlier slots choosing e" is the exclusive
+    // scan over threads of the per-run histograms plus the in-run count:
+    // stable (expert, token, slot) order in one pass over the slots.
+    const int per = (TK + nt - 1) / nt;
+    const int i0 = min(TK, tid * per), i1 = min(TK, i0 + per);
+    for (int e = 0; e < E; ++e) hist[e * nt + tid] = 0;
+    for (int i = i0; i < i1; ++i) ++hist[topk_idx[i] * nt + tid];
+    __syncthreads();
+    {  // per expert: exclusive scan over the nt thread counts (one warp per expert)
+        const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5, span = nt / 32;
+        for (int e = warp; e < E; e += nw) {
+            int* h = hist + e * nt + lane * span;
+            int local = 0;
+            for (int j = 0; j < span; ++j) local += h[j];
+            int incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int run = incl - local;
+            for (int j = 0; j < span; ++j) {
+                const int c = h[j];
+                h[j] = run;
+                run += c;
+            }
+            if (lane == 31) s_cnt[e] = incl;
         }
-        if (threadIdx.x == 0) s_cnt[e] = running;
-        __syncthreads();
     }
-    if (threadIdx.x == 0) {
+    __syncthreads();
+    if (tid == 0) {
         s_off[0] = 0;
         for (int e = 0; e < E; ++e) s_off[e + 1] = s_off[e] + ((s_cnt[e] + 15) & ~15);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < TK; i += blockDim.x) s_slot_row[i] += s_off[topk_idx[i]];
+    for (int i = i0; i < i1; ++i) {
+        const int e = topk_idx[i];
+        s_slot_row[i] = s_off[e] + hist[e * nt + tid]++;
+    }
     __syncthreads();
     const int rows = s_off[E];
     if (blockIdx.x == 0) {
@@ -228,8 +231,15 @@ cudaError_t launch_moe_permute(const int32_t* topk_idx, const uint16_t* hn, int 
     int grid = static_cast<int>((work + 255) / 256);
     if (grid > 296) grid = 296;
     if (grid < 1) grid = 1;
-    permute_kernel<<<grid, 256, T * K * sizeof(int), s>>>(topk_idx, hn, T, H, E, K, counts, offsets,
-                                                          perm, inv, xp, R);
+    const int smem = (E * 256 + T * K) * static_cast<int>(sizeof(int));
+    static bool attr = false;
+    if (!attr) {
+        const cudaError_t e = cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (kMaxE * 256 + kMaxSlots) * static_cast<int>(sizeof(int)));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    permute_kernel<<<grid, 256, smem, s>>>(topk_idx, hn, T, H, E, K, counts, offsets, perm, inv, xp, R);
     return cudaGetLastError();
 }
 

@@ -16,21 +16,17 @@
 #include "../kernels/common.cuh"
 #include "../kernels/kernels.hpp"
 #include "host_layout.hpp"
+#include "runtime_util.hpp"
 
 namespace mlt {
 
 namespace {
+using detail::ck;
+using detail::now_s;
+using detail::round_up;
+}  // namespace
 
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-double now_s() {
-    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
-
-int round_up(int v, int m) { return (v + m - 1) / m * m; }
-
+namespace detail {
 // Large host buffers: 2 MiB-aligned, transparent huge pages, first-touched
 // in parallel, then page-locked with cudaHostRegister (measured on the GPU
 // box: ~0.1 s/GB vs ~0.4 s/GB for cudaHostAlloc; tools/pin_probe.cu).
@@ -56,8 +52,9 @@ void host_free(void* p, bool pinned) {
     if (pinned) cudaHostUnregister(p);
     std::free(p);
 }
-
-}  // namespace
+}  // namespace detail
+using detail::host_alloc;
+using detail::host_free;
 
 // ---------------------------------------------------------------------------
 Arena::Arena(size_t bytes) : cap_(bytes) {
@@ -141,8 +138,9 @@ Runtime::~Runtime() {
     if (h_qkv_) cudaFreeHost(h_qkv_);
     if (h_attn_) cudaFreeHost(h_attn_);
     if (h_tok_) cudaFreeHost(h_tok_);
-    std::free(h_kcache_);
-    std::free(h_vcache_);
+    host_free(h_kcache_, true);
+    host_free(h_vcache_, true);
+    host_free(h_pfx_, true);
     arena_.reset();
     if (s_gpu_) cudaStreamDestroy(s_gpu_);
     if (s_h2d_) cudaStreamDestroy(s_h2d_);
@@ -246,8 +244,9 @@ void Runtime::allocate() {
     ck(cudaHostAlloc(reinterpret_cast<void**>(&h_tok_), static_cast<size_t>(max_steps_) * N_ * 4 * 4, 0), "h_tok");
     if (!policy_.attn_on_gpu) {
         const size_t kv = static_cast<size_t>(L_) * N_ * nkv_ * max_ctx_ * d_;
-        h_kcache_ = reinterpret_cast<uint16_t*>(host_alloc(kv * 2, false, nullptr));
-        h_vcache_ = reinterpret_cast<uint16_t*>(host_alloc(kv * 2, false, nullptr));
+        // page-locked: the GPU prefill writes the prompt KV here by DMA
+        h_kcache_ = reinterpret_cast<uint16_t*>(host_alloc(kv * 2, true, &pin_seconds_));
+        h_vcache_ = reinterpret_cast<uint16_t*>(host_alloc(kv * 2, true, &pin_seconds_));
     }
 }
 
@@ -397,6 +396,13 @@ size_t Runtime::debug_read(const std::string& name, void* out, size_t cap) {
     else if (name == "logits") { src = d_logits_; bytes = static_cast<size_t>(mu_) * V_ * 4; }
     else if (name == "xe") { src = d_xe_; bytes = static_cast<size_t>(Re_) * H_ * 2; }
     else if (name == "inter") { src = d_inter_; bytes = static_cast<size_t>(Re_) * F_ * 2; }
+    else if (name == "kcache" || name == "vcache") {  // host KV [L][N][nkv][max_ctx][d] (A_g = 0)
+        src = name[0] == 'k' ? h_kcache_ : h_vcache_;
+        bytes = src ? static_cast<size_t>(L_) * N_ * nkv_ * max_ctx_ * d_ * 2 : 0;
+    } else if (name == "kpool" || name == "vpool") {  // paged device KV (A_g = 1)
+        src = name[0] == 'k' ? d_kpool_ : d_vpool_;
+        bytes = src ? static_cast<size_t>(L_) * N_ * max_pages_ * nkv_ * page_ * d_ * 2 : 0;
+    }
     else throw std::invalid_argument("unknown debug buffer " + name);
     if (out) {
         if (cap < bytes) throw std::invalid_argument("debug_read: buffer too small");

@@ -44,6 +44,7 @@ struct RuntimeOptions {
     int tp_rank = 0, tp_size = 1;  // tensor parallelism (one process per GPU)
     uint8_t nccl_id[128] = {};     // ncclUniqueId from rank 0 (tp_size > 1)
     int schedule = -1;             // -1: CGOPipe (S4 when A_g = 1); else a ScheduleKind to execute
+    int prefill_chunk_tokens = 0;  // 0: largest prefill chunk the budget allows
 };
 
 // Bump allocator over one cudaMalloc of the budget (SURVEY.md §7 hard part 5).
@@ -87,6 +88,21 @@ struct DecodeReport {
     std::vector<KernelTime> kernel_exec;  // in-kernel first-CTA-start to last-CTA-end (GEMMs)
 };
 
+// GPU prefill ("for the prefill stage, we perform all the
+// computation on GPU and offload KV cache to CPU"; cost model planner.cpp:
+// 110-150).  Device-timed with CUDA events around the whole call, host
+// token upload and id download included.
+struct PrefillReport {
+    double seconds = 0;
+    double tokens_per_second = 0;   // prompt tokens / s
+    int64_t prompt_tokens = 0;
+    int chunk_tokens = 0;           // token capacity of one chunk
+    int chunks_per_layer = 0;
+    double h2d_weight_bytes = 0, h2d_bytes = 0, d2h_bytes = 0;
+    double gpu_busy_seconds = 0;    // sum over chunks of compute-stream time
+    int gpu_launches = 0;
+};
+
 class Runtime {
   public:
     Runtime(const lightplan::ModelSpec& model, const ModelExt& ext, const lightplan::Policy& policy,
@@ -100,6 +116,13 @@ class Runtime {
     // sequence's position to prompt_len.
     void prefill_synthetic(int prompt_len, uint64_t seed);
     void set_positions(const int32_t* pos);
+    // GPU prefill of real prompts: tokens = the N prompts concatenated
+    // (sequence i has lens[i] >= 1 tokens), first_ids[N] = the greedy token
+    // after each prompt.  Zigzag order (layer by layer over chunks of whole
+    // sequences); the residual stream of all prompt tokens lives in pinned
+    // host memory between layers, KV goes to the host cache (A_g = 0) or the
+    // paged device pool (A_g = 1).  Sets every position to lens[i].
+    PrefillReport prefill(const int32_t* tokens, const int32_t* lens, int32_t* first_ids);
     const std::vector<int32_t>& positions() const { return pos_; }
 
     // `steps` decode steps for all N sequences.  tokens_in: [N] host ids of
@@ -246,6 +269,25 @@ class Runtime {
     void mark_start(cudaEvent_t task_start);
 
   private:
+    // prefill scratch (allocated from the arena on first use) and host residual store
+    void prefill_alloc(int64_t total_tokens, int max_len);
+    int pf_T_ = 0;                       // chunk token capacity
+    int pf_R_ = 0, pf_Re_ = 0;
+    float* pf_x_[2] = {nullptr, nullptr};  // [T, H] fp32 residual, double-buffered
+    uint8_t* pf_xn_ = nullptr;           // packed [R_T, H] (also the attention output)
+    uint16_t* pf_qkv_ = nullptr;         // [T, W] roped bf16
+    float* pf_h_ = nullptr;              // [T, H]
+    uint16_t* pf_hn_ = nullptr;          // [T, H]
+    int32_t *pf_topk_ = nullptr, *pf_perm_ = nullptr, *pf_inv_ = nullptr;
+    float* pf_topw_ = nullptr;
+    uint8_t* pf_xe_ = nullptr;           // packed [Re_T, H]
+    uint8_t* pf_inter_ = nullptr;        // packed [Re_T, F]
+    float* pf_y_ = nullptr;              // [Re_T, H] (also the QKV fp32 output)
+    uint16_t* pf_kst_[2] = {nullptr, nullptr};  // K/V staging [2][T * nkv * d] per buffer
+    int32_t* pf_meta_ = nullptr;         // per-chunk metadata (device)
+    int64_t pf_meta_cap_ = 0;            // int32 entries
+    float* h_pfx_ = nullptr;             // pinned [tokens][H] residual store
+    int64_t h_pfx_tokens_ = 0;
     std::vector<cudaEvent_t> event_pool_;
     size_t event_next_ = 0;
     double pin_seconds_ = 0, gen_seconds_ = 0;

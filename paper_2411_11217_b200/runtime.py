@@ -21,7 +21,8 @@ class RuntimeOptions(C.Structure):
                 ("host_threads", C.c_int32), ("pin_weights", C.c_int32), ("vocab", C.c_int32),
                 ("rms_eps", C.c_float), ("rope_theta", C.c_float), ("lm_head_scale", C.c_float),
                 ("seed", C.c_uint64), ("exact_gates", C.c_int32), ("tp_rank", C.c_int32),
-                ("tp_size", C.c_int32), ("nccl_id", C.c_uint8 * 128), ("schedule", C.c_int32)]
+                ("tp_size", C.c_int32), ("nccl_id", C.c_uint8 * 128), ("schedule", C.c_int32),
+                ("prefill_chunk_tokens", C.c_int32)]
 
 
 def nccl_unique_id() -> bytes:
@@ -44,6 +45,14 @@ class DecodeReport(C.Structure):
                 ("dense_ms_total", C.c_double), ("dense_launches", C.c_int32)]
 
 
+class PrefillReport(C.Structure):
+    _fields_ = [("seconds", C.c_double), ("tokens_per_second", C.c_double),
+                ("prompt_tokens", C.c_int64), ("chunk_tokens", C.c_int32),
+                ("chunks_per_layer", C.c_int32), ("h2d_weight_bytes", C.c_double),
+                ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double),
+                ("gpu_busy_seconds", C.c_double), ("gpu_launches", C.c_int32)]
+
+
 class RuntimeInfo(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("achieved_weight_ratio", "streamed_bytes_per_layer",
                                           "arena_used", "arena_capacity", "pin_seconds",
@@ -57,6 +66,8 @@ _SIGS = {
     "runtime_info": (C.c_int, [C.c_void_p, C.POINTER(RuntimeInfo)]),
     "runtime_prefill_synthetic": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64]),
     "runtime_set_positions": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "runtime_prefill": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.POINTER(PrefillReport)]),
     "runtime_decode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                  C.POINTER(DecodeReport)]),
     "runtime_timeline_json": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
@@ -86,14 +97,16 @@ class Runtime:
                  max_ctx: int, vocab: int = 32000, seed: int = 1234, device: int = 0,
                  host_threads: int = 0, pin_weights: bool = True, rms_eps: float = 1e-5,
                  rope_theta: float = 1e6, lm_head_scale: float = 4.0, exact_gates: bool = True,
-                 tp_rank: int = 0, tp_size: int = 1, nccl_id: bytes = b"", schedule: str = "auto"):
+                 tp_rank: int = 0, tp_size: int = 1, nccl_id: bytes = b"", schedule: str = "auto",
+                 prefill_chunk_tokens: int = 0):
         self.api, self.f = _fns()
         self.model, self.policy = model, policy
         nid = (C.c_uint8 * 128)(*(nccl_id.ljust(128, b"\0")[:128]))
         self.opts = RuntimeOptions(device, budget_bytes, max_ctx, host_threads, int(pin_weights),
                                    vocab, rms_eps, rope_theta, lm_head_scale, seed,
                                    int(exact_gates), tp_rank, tp_size, nid,
-                                   -1 if schedule == "auto" else capi.SCHED[schedule])
+                                   -1 if schedule == "auto" else capi.SCHED[schedule],
+                                   prefill_chunk_tokens)
         self.h = self.f["runtime_create"](C.byref(model), C.byref(policy), C.byref(self.opts))
         if not self.h:
             code = self.api.fn["last_status"]()
@@ -117,6 +130,21 @@ class Runtime:
 
     def prefill_synthetic(self, prompt_len: int, seed: int = 9012):
         self._ck(self.f["runtime_prefill_synthetic"](self.h, prompt_len, seed))
+
+    def prefill(self, prompts):
+        """GPU prefill of real prompts (mlt_runtime_prefill).  prompts: [N, s]
+        array or a list of N 1-D id arrays (ragged).  Returns (first ids [N],
+        PrefillReport); decode continues at each prompt's length."""
+        if isinstance(prompts, np.ndarray) and prompts.ndim == 2:
+            prompts = list(prompts)
+        lens = np.array([len(p) for p in prompts], np.int32)
+        toks = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in prompts]), np.int32)
+        first = np.zeros(len(prompts), np.int32)
+        rep = PrefillReport()
+        self._ck(self.f["runtime_prefill"](self.h, toks.ctypes.data_as(C.c_void_p),
+                                           lens.ctypes.data_as(C.c_void_p),
+                                           first.ctypes.data_as(C.c_void_p), C.byref(rep)))
+        return first, rep
 
     def set_positions(self, pos):
         pos = np.ascontiguousarray(pos, np.int32)

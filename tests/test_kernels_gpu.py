@@ -285,3 +285,75 @@ def test_argmax(K):
     assert ids[1].item() == 5 and mg[1].item() == 0.0
     top2 = lg[0].topk(2).values
     assert abs(mg[0].item() - (top2[0] - top2[1]).item()) < 1e-6
+
+
+def _tiles(lens):
+    tiles, r = [], 0
+    for n in lens:
+        for q0 in range(0, n, 16):
+            tiles.append((r, n, q0, 0))
+        r += n
+    return np.array(tiles, np.int32).reshape(-1)
+
+
+@pytest.mark.parametrize("nq,nkv", [(8, 2), (12, 2), (4, 4), (8, 1)])
+def test_prefill_attention_ragged_vs_fp32(K, nq, nkv):
+    """Causal GQA prefill attention (attention_prefill.cu) on ragged
+    sequences vs a torch fp32 reference on the same bf16 inputs."""
+    from oracle import bind as orc
+    d = 128
+    lens = [1, 17, 64, 100, 33, 16, 130]
+    T, W = sum(lens), (nq + 2 * nkv) * d
+    g = torch.Generator().manual_seed(7)
+    qkv = (torch.rand(T, W, generator=g) * 2 - 1).to(torch.bfloat16)
+    qkv_d = qkv.cuda()
+    tiles = torch.from_numpy(_tiles(lens)).cuda()
+    R = (T + 15) // 16 * 16
+    outp = torch.zeros(R * nq * d, dtype=torch.int16, device="cuda")
+    K.prefill_attention(ptr(qkv_d), W, ptr(tiles), tiles.numel() // 4, nq, nkv, d, ptr(outp), R, stream())
+    torch.cuda.synchronize()
+    packed = outp.cpu().numpy().view(np.uint8)
+    rows = np.zeros((T, nq * d), np.uint16)
+    K.unpack_rows(packed.ctypes.data_as(C.c_void_p), R, T, nq * d, rows.ctypes.data_as(C.c_void_p))
+    got = orc.bf16_to_f32(rows)
+    x = qkv.float()
+    ref = np.zeros((T, nq * d), np.float32)
+    r = 0
+    G = nq // nkv
+    for n in lens:
+        q = x[r:r + n, :nq * d].reshape(n, nq, d)
+        k = x[r:r + n, nq * d:(nq + nkv) * d].reshape(n, nkv, d)
+        v = x[r:r + n, (nq + nkv) * d:].reshape(n, nkv, d)
+        kk = k.repeat_interleave(G, dim=1)
+        vv = v.repeat_interleave(G, dim=1)
+        s = torch.einsum("qhd,khd->hqk", q, kk) / np.sqrt(d)
+        mask = torch.triu(torch.ones(n, n, dtype=torch.bool), 1)
+        s = s.masked_fill(mask, float("-inf"))
+        o = torch.einsum("hqk,khd->qhd", torch.softmax(s, -1), vv)
+        ref[r:r + n] = o.reshape(n, nq * d).numpy()
+        r += n
+    err = np.abs(got - ref)
+    assert err.max() < 1.5e-2, err.max()
+    assert err.mean() < 2e-3, err.mean()
+
+
+def test_kv_stage_layout(K):
+    nq, nkv, d = 8, 2, 128
+    lens = [3, 17, 1, 40]
+    T, W = sum(lens), (nq + 2 * nkv) * d
+    qkv = torch.randint(-30000, 30000, (T, W), dtype=torch.int16, device="cuda")
+    tok_seq = np.concatenate([np.full(n, j, np.int32) for j, n in enumerate(lens)])
+    tok_pos = np.concatenate([np.arange(n, dtype=np.int32) for n in lens])
+    row0 = np.cumsum([0] + lens[:-1]).astype(np.int32)
+    ts, tp, r0, ln = (torch.from_numpy(a).cuda() for a in (tok_seq, tok_pos, row0, np.array(lens, np.int32)))
+    sk = torch.zeros(T * nkv * d, dtype=torch.int16, device="cuda")
+    sv = torch.zeros_like(sk)
+    K.kv_stage(ptr(qkv), W, nq, nkv, d, ptr(ts), ptr(tp), ptr(r0), ptr(ln), T, ptr(sk), ptr(sv), stream())
+    torch.cuda.synchronize()
+    q = qkv.cpu().numpy()
+    for j, n in enumerate(lens):
+        seg_k = sk.cpu().numpy()[row0[j] * nkv * d:(row0[j] + n) * nkv * d].reshape(nkv, n, d)
+        seg_v = sv.cpu().numpy()[row0[j] * nkv * d:(row0[j] + n) * nkv * d].reshape(nkv, n, d)
+        rows = q[row0[j]:row0[j] + n]
+        assert np.array_equal(seg_k, rows[:, nq * d:(nq + nkv) * d].reshape(n, nkv, d).transpose(1, 0, 2))
+        assert np.array_equal(seg_v, rows[:, (nq + nkv) * d:].reshape(n, nkv, d).transpose(1, 0, 2))
