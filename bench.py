@@ -239,6 +239,9 @@ def run_mlt(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # --tp-shard T: rank 0's shard of a T-way tensor-parallel job measured alone on
+    # this GPU (its own PCIe link, all-reduce elided): the per-GPU step of that job
+    tp = args.tp_shard if args.tp_shard > 1 else world
     dist = None
     nid = b""
     if world > 1:
@@ -265,8 +268,8 @@ def run_mlt(args, cfg):
     t = time.perf_counter()
     rt = Runtime(model_spec(cfg), policy(cfg), budget_bytes=cfg["budget"],
                  max_ctx=cfg["prompt"] + args.warmup + args.steps + 8, vocab=cfg["vocab"],
-                 device=local, exact_gates=args.gates == "exact", tp_rank=rank, tp_size=world,
-                 nccl_id=nid, schedule=args.schedule)
+                 device=local, exact_gates=args.gates == "exact", tp_rank=rank, tp_size=tp,
+                 nccl_id=nid, schedule=args.schedule, tp_shard_only=args.tp_shard > 1)
     info = rt.info
     log(f"[bench] rank {rank}: runtime ready in {time.perf_counter() - t:.1f}s (weights gen "
         f"{info.gen_seconds:.1f}s, pin {info.pin_seconds:.1f}s), r_w achieved "
@@ -311,7 +314,7 @@ def run_mlt(args, cfg):
             json.dump(rt.timeline(), fh)
     value = cfg["N"] * args.steps / dev_s        # device-timed (CUDA events), whole job
     e2e = cfg["N"] * args.steps / wall_s         # wall clock around the C-ABI call
-    bound = hrm_bound(cfg, link_gbs, host_gbs, pk, tp=world)
+    bound = hrm_bound(cfg, link_gbs, host_gbs, pk, tp=tp)
     prof = rt.kernel_profile()
     l = cfg["model"][0]
     link_s = rep.measured.link_upload * l * args.steps
@@ -332,7 +335,10 @@ def run_mlt(args, cfg):
                    "gpu_budget_gb": cfg["budget"] / 1e9, "r_w": cfg["r_w"],
                    "r_w_achieved": info.achieved_weight_ratio, "A_g": cfg["a_g"],
                    "parallelism": (f"tp{world} (heads + expert h2 sharded, NCCL all-reduce x2/layer)"
-                                   if world > 1 else "single GPU, weight paging"),
+                                   if world > 1 else
+                                   f"tp{tp} job, rank-0 shard measured alone on 1 GPU (own PCIe link; "
+                                   f"NVLink all-reduce elided, modeled ~0.5 MB/call)" if tp > 1
+                                   else "single GPU, weight paging"),
                    "schedule": ("CGOPipe" if cfg["a_g"] == 0 else "S4") if args.schedule == "auto"
                    else args.schedule,
                    "weight_gates": args.gates,
@@ -344,7 +350,7 @@ def run_mlt(args, cfg):
                 "h2d_weight_gbs_achieved": h2d_gbs,
                 "streamed_gb_per_layer_per_gpu": info.streamed_bytes_per_layer / 1e9,
                 "utilization": dict(zip(["gpu", "cpu", "h2d", "d2h", "ctopin"], list(rep.utilization)))},
-        "roofline": expert_roofline(cfg, rep, pk, load_traffic(), world),
+        "roofline": expert_roofline(cfg, rep, pk, load_traffic(), tp),
         "peaks_source": pk_src,
         "e2e": {"value": e2e, "unit": "tok/s",
                 "h2d_bytes_per_step": rep.h2d_bytes / args.steps + cfg["N"] * 4 * 2,
@@ -402,10 +408,12 @@ def main():
     ap.add_argument("--prefill", action="store_true",
                     help="run the GPU prefill on synthetic prompt ids instead of synthetic prompt KV")
     ap.add_argument("--timeline", default=None, help="write the measured timeline JSON here")
+    ap.add_argument("--tp-shard", type=int, default=0,
+                    help="measure rank 0's shard of a T-way TP job alone on one GPU (all-reduce elided)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if isinstance(cfg["r_w"], dict):
-        world = int(os.environ.get("WORLD_SIZE", "1"))
+        world = args.tp_shard if args.tp_shard > 1 else int(os.environ.get("WORLD_SIZE", "1"))
         if world not in cfg["r_w"]:
             raise SystemExit(f"{args.config}: no policy for {world} GPUs (h2/tp must keep 128-row blocks)")
         cfg["r_w"] = cfg["r_w"][world]

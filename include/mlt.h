@@ -379,6 +379,9 @@ typedef struct mlt_runtime_options_t {
                                  kind (0 CGOPipe, 1 S2, 2 S3, 3 S4; pipesim.hpp:20-21) to
                                  execute a baseline schedule on the same kernels */
     int32_t prefill_chunk_tokens; /* 0: largest chunk the budget allows (<= 8192 tokens) */
+    int32_t tp_shard_only;    /* 1 (with tp_size > 1): run rank tp_rank's shard ALONE on this GPU
+                                 with the all-reduce elided — a per-GPU throughput measurement
+                                 of a tp_size job on one device (values are partial sums) */
 } mlt_runtime_options_t;
 
 /* ncclUniqueId for a tensor-parallel group (call on rank 0, broadcast). */

@@ -59,6 +59,7 @@ mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p
         std::memcpy(opt.nccl_id, o->nccl_id, 128);
         opt.schedule = o->schedule;
         opt.prefill_chunk_tokens = o->prefill_chunk_tokens;
+        opt.tp_shard_only = o->tp_shard_only != 0;
         auto hh = std::make_unique<Handle>();
         hh->rt = std::make_unique<mlt::Runtime>(ms, ext, pol, opt);
         h = hh.release();

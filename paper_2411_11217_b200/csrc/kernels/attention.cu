@@ -1,27 +1,37 @@
 // GQA decode attention over a paged KV cache (north_star item 4; SURVEY.md
 // §2c gqa_decode_paged), used when the policy places attention on the GPU
 // (A_g = 1).  Memory-bound: attention intensity is 2*n_q/(n_kv*dt_kv) FLOP/B
-// (4 for 8x7B), so the kernel's job is to stream K/V pages at HBM rate.
+// (4 for 8x7B), so the kernel's job is to stream K/V pages at HBM rate with
+// as few instructions per byte as possible.
 //
-// Layout: a KV page holds kPage = 16 consecutive tokens of ONE kv head,
-// [16][d] bf16 (K and V in separate pools), so a (page, head) slice is one
-// contiguous 4 KiB run that a single cp.async.bulk moves into shared memory.
-// Page id = block_table[seq][pos / 16]; pool offset = (id*n_kv + h)*16*d.
+// Layout (common.cuh kv_page_off): a KV page holds kKvPage = 16 tokens of ONE
+// kv head, [16][128] bf16 with the 16-byte chunks of token r XOR-swizzled by
+// r & 7 (K and V in separate pools), so a (page, head) slice is one
+// contiguous 4 KiB run that a single cp.async.bulk moves into shared memory
+// and every ldmatrix phase on it is bank-conflict-free.
+// Page id = block_table[seq][pos / 16]; pool offset = (id*n_kv + h)*16*128.
 //
 // One CTA per (query token, kv head).  Its kWarps warps split the pages
-// (warp w takes pages w, w+kWarps, ...: flash-decoding inside the CTA) and
-// each warp serves ALL G = n_q/n_kv query heads of the kv head, so every
-// K/V element is read once from HBM and once from shared memory for all G
-// heads (GQA reuse).  Each warp owns a kStagesW-deep ring of pages that its
-// lane 0 fills with 1-D bulk copies (mbarrier tx counts): the page gather is
-// staged through shared memory, ahead of the math.
-//   QK^T: 8 lanes per token (16 dims each, q in registers pre-scaled by
-//         log2(e)/sqrt(d)), 4 tokens per pass; lanes of the upper half read
-//         their two 16-byte chunks in swapped order so a pass is
-//         bank-conflict-free; 3 xor-shuffles reduce a score.
-//   softmax: exp2 domain, one 2-shuffle warp max/sum per page and head.
-//   PV: lane l owns dims [4l, 4l+4); p_j arrives by shuffle.
-// The warps' (m, l, acc) are merged through shared memory at the end.
+// (warp w takes pages w, w+kWarps, ...: flash-decoding inside the CTA); each
+// warp owns a kStagesW-deep ring of pages that its elected lane fills with
+// 1-D bulk copies (mbarrier tx counts), so the page gather is staged through
+// shared memory ahead of the math.  The math runs on the tensor cores
+// (mma.sync m16n8k16 bf16 -> fp32) in the transposed orientation, which
+// wastes nothing on the token axis and at most half on the head axis:
+//   S^T[16 tok][8 heads] = K_page[16][128] . Q^T       (8 MMAs, K by ldmatrix,
+//                                                      Q^T fragments in regs,
+//                                                      heads >= G are zero)
+//   O^T[128][8 heads]   += V_page^T[128][16] . P^T     (V^T by ldmatrix.trans;
+//                                                      P^T from the S^T
+//                                                      accumulators by
+//                                                      movmatrix.trans)
+// P is split into bf16 hi + lo parts (two MMAs per tile), so the PV product
+// keeps ~16 mantissa bits — fp32-class accuracy at 16 extra MMAs per page.
+// Each thread's accumulator columns are heads 2*(lane%4)+{0,1} in both S^T
+// and O^T, so the online-softmax rescale is thread-local; the row max needs
+// 3 xor-shuffles per page, the row sum is reduced once at the end.  ~100
+// instructions per 8 KiB page and warp (vs ~1500 for CUDA-core FMAs).  The
+// warps' (m, l, O) are merged through shared memory at the end.
 #include <cfloat>
 #include <cstdint>
 
@@ -31,32 +41,65 @@
 namespace mltk {
 namespace {
 
-constexpr int kPage = 16;
+constexpr int kPage = kKvPage;
 constexpr int kD = 128;
 constexpr int kWarps = 4;
 constexpr int kStagesW = 3;
 constexpr int kPageElems = kPage * kD;
 constexpr int kPageBytes = kPageElems * 2;  // 4 KiB (one of K or V)
-constexpr int kCombStride = 4 + kD;         // [m, l, pad, pad, acc[128]]: 16-byte aligned rows
+constexpr int kCombStride = kD + 4;         // per (warp, head): acc[128], m, l, pad
 
-__device__ __forceinline__ float lo_bf16(uint32_t v) { return __uint_as_float(v << 16); }
-__device__ __forceinline__ float hi_bf16(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ uint32_t movm_t(uint32_t a) {
+    uint32_t d;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(d) : "r"(a));
+    return d;
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack2(uint16_t lo, uint16_t hi) {
+    return static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+}
+
+// byte offset of 16-byte chunk c of token row r inside a staged page
+__device__ __forceinline__ uint32_t pg_off(int r, int c) {
+    return static_cast<uint32_t>(r * 256 + ((c ^ (r & 7)) << 4));
+}
 
 template <int G>
 __global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
-    const uint16_t* q, int ldq, const uint16_t* kp, const uint16_t* vp, const int32_t* bt,
-    int max_pages, const int32_t* seq, const int32_t* ctx, int nkv, uint8_t* out_p, int R,
-    float* out_f) {
+    const uint16_t* __restrict__ q, int ldq, const uint16_t* __restrict__ kp, const uint16_t* __restrict__ vp,
+    const int32_t* __restrict__ bt, int max_pages, const int32_t* __restrict__ seq, const int32_t* __restrict__ ctx,
+    int nkv, uint8_t* out_p, int R, float* out_f) {
+    static_assert(G >= 1 && G <= 8, "heads per kv head must fit the MMA n = 8");
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ uint64_t full[kWarps][kStagesW];
     const int t = blockIdx.x, h = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, tg = lane & 3;
     const int L = ctx[t];
     const int s_id = seq[t];
     const int n_pages = (L + kPage - 1) / kPage;
     // per-warp ring: [warp][stage][K page | V page]
-    uint16_t* ring = reinterpret_cast<uint16_t*>(sm) + static_cast<size_t>(warp) * kStagesW * 2 * kPageElems;
-    float* comb = reinterpret_cast<float*>(sm + kWarps * kStagesW * 2 * kPageBytes);  // [warp][G][2 + kD]
+    uint8_t* ring = sm + static_cast<size_t>(warp) * kStagesW * 2 * kPageBytes;
+    const uint32_t ring_s = smem_u32(ring);
+    // after its loop, each warp's ring holds its partial state [8 heads][kCombStride]
+    auto comb = [&](int w) { return reinterpret_cast<float*>(sm + static_cast<size_t>(w) * kStagesW * 2 * kPageBytes); };
 
     if (lane == 0) {
         for (int s = 0; s < kStagesW; ++s) mbar_init(&full[warp][s], 1);
@@ -67,38 +110,36 @@ __global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
     auto issue = [&](int page, int st) {
         const int id = bt[static_cast<int64_t>(s_id) * max_pages + page];
         const int64_t off = (static_cast<int64_t>(id) * nkv + h) * kPageElems;
-        uint16_t* dst = ring + st * 2 * kPageElems;
+        uint8_t* dst = ring + st * 2 * kPageBytes;
         mbar_expect_tx(&full[warp][st], 2 * kPageBytes);
         bulk_g2s(dst, kp + off, kPageBytes, &full[warp][st], pol);
-        bulk_g2s(dst + kPageElems, vp + off, kPageBytes, &full[warp][st], pol);
+        bulk_g2s(dst + kPageBytes, vp + off, kPageBytes, &full[warp][st], pol);
     };
     if (lane == 0)
         for (int k = 0; k < kStagesW && warp + k * kWarps < n_pages; ++k) issue(warp + k * kWarps, k);
 
-    // q slice: lane (grp = lane/8, r = lane%8) holds dims [16r, 16r+16) of each head
-    const int grp = lane >> 3, r = lane & 7;
-    const bool swap = (r >> 2) & 1;  // upper half reads its two chunks in swapped order
-    const float qscale = 1.4426950408889634f * rsqrtf(static_cast<float>(kD));
-    float qr[G][16];
+    // Q^T as B fragments: b0 = q[head g][16kk + 2tg, +1], b1 = q[head g][16kk + 8 + 2tg, +1]
+    uint32_t qb[8][2];
+    {
+        const bool valid = g < G;
+        const uint16_t* src = q + static_cast<int64_t>(t) * ldq + (h * G + (valid ? g : 0)) * kD + 2 * tg;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const uint16_t* src = q + static_cast<int64_t>(t) * ldq + (h * G + g) * kD + r * 16;
-        const uint4 a = *reinterpret_cast<const uint4*>(src);
-        const uint4 b = *reinterpret_cast<const uint4*>(src + 8);
-        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            qr[g][2 * e] = lo_bf16(w[e]) * qscale;
-            qr[g][2 * e + 1] = hi_bf16(w[e]) * qscale;
+        for (int kk = 0; kk < 8; ++kk) {
+            qb[kk][0] = valid ? *reinterpret_cast<const uint32_t*>(src + kk * 16) : 0u;
+            qb[kk][1] = valid ? *reinterpret_cast<const uint32_t*>(src + kk * 16 + 8) : 0u;
         }
     }
-    float m[G], l[G], acc[G][4];
+    const float sl2 = 1.4426950408889634f * rsqrtf(static_cast<float>(kD));
+    // this thread's heads: c = 2tg + {0,1}
+    float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+    float acc[8][4];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        m[g] = -FLT_MAX;
-        l[g] = 0.f;
-        acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
-    }
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+
+    // ldmatrix lane addressing: matrix mi = lane/8, row-in-matrix lane%8
+    const int mi = lane >> 3, rr = lane & 7;
+    const int k_row = rr + (mi & 1) * 8, k_chunk = mi >> 1;   // K (A, non-trans): [tok][d] blocks
+    const int v_row = rr + (mi >> 1) * 8, v_chunk = mi & 1;   // V (A = V^T, trans)
 
     uint32_t phase = 0;
     for (int k = 0;; ++k) {
@@ -106,113 +147,105 @@ __global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
         if (page >= n_pages) break;
         const int st = k % kStagesW;
         mbar_wait(&full[warp][st], phase);
-        const uint16_t* sk = ring + st * 2 * kPageElems;
-        const uint16_t* sv = sk + kPageElems;
+        const uint32_t sk = ring_s + st * 2 * kPageBytes;
+        const uint32_t sv = sk + kPageBytes;
         const int ntok = min(kPage, L - page * kPage);
 
-        // ---- QK^T: 4 passes x 4 tokens, 8 lanes per token ----
-        float sc[G][4];
+        // ---- S^T = K Q^T: 16 tokens x 8 heads ----
+        float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const int tok = p * 4 + grp;
-            const uint16_t* row = sk + tok * kD + r * 16;
-            float part[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) part[g] = 0.f;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int cc = swap ? (c ^ 1) : c;
-                const uint4 kv = *reinterpret_cast<const uint4*>(row + cc * 8);
-                const uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w};
-#pragma unroll
-                for (int g = 0; g < G; ++g)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float q0 = swap ? qr[g][(c ^ 1) * 8 + 2 * e] : qr[g][c * 8 + 2 * e];
-                        const float q1 = swap ? qr[g][(c ^ 1) * 8 + 2 * e + 1] : qr[g][c * 8 + 2 * e + 1];
-                        part[g] = fmaf(q0, lo_bf16(w[e]), part[g]);
-                        part[g] = fmaf(q1, hi_bf16(w[e]), part[g]);
-                    }
-            }
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                float v = part[g];
-                v += __shfl_xor_sync(0xffffffffu, v, 1);
-                v += __shfl_xor_sync(0xffffffffu, v, 2);
-                v += __shfl_xor_sync(0xffffffffu, v, 4);
-                sc[g][p] = tok < ntok ? v : -FLT_MAX;
-            }
+        for (int kk = 0; kk < 8; ++kk) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4(sk + pg_off(k_row, 2 * kk + k_chunk), a0, a1, a2, a3);
+            mma16816(s, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
         }
-        // ---- online softmax per head (exp2 domain) ----
-        float pe[G][4];
+        // s[0], s[1]: token g, heads 2tg, 2tg+1; s[2], s[3]: token g+8
+        s[0] = g < ntok ? s[0] * sl2 : -INFINITY;
+        s[1] = g < ntok ? s[1] * sl2 : -INFINITY;
+        s[2] = g + 8 < ntok ? s[2] * sl2 : -INFINITY;
+        s[3] = g + 8 < ntok ? s[3] * sl2 : -INFINITY;
+        float mx0 = fmaxf(s[0], s[2]), mx1 = fmaxf(s[1], s[3]);
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            float tmax = fmaxf(fmaxf(sc[g][0], sc[g][1]), fmaxf(sc[g][2], sc[g][3]));
-            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
-            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
-            const float m_new = fmaxf(m[g], tmax);
-            const float corr = exp2f(m[g] - m_new);
-            float ps = 0.f;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                pe[g][p] = (p * 4 + grp) < ntok ? exp2f(sc[g][p] - m_new) : 0.f;
-                ps += pe[g][p];
-            }
-            ps += __shfl_xor_sync(0xffffffffu, ps, 8);
-            ps += __shfl_xor_sync(0xffffffffu, ps, 16);
-            l[g] = l[g] * corr + ps;
-            m[g] = m_new;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[g][e] *= corr;
+        for (int o = 4; o <= 16; o <<= 1) {
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
         }
-        // ---- PV: lane owns dims [4*lane, 4*lane + 4) ----
+        const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);  // finite: >= 1 valid token
+        const float c0 = exp2f(m[0] - mn0), c1 = exp2f(m[1] - mn1);
+        m[0] = mn0;
+        m[1] = mn1;
+        const float p00 = exp2f(s[0] - mn0), p01 = exp2f(s[1] - mn1);
+        const float p10 = exp2f(s[2] - mn0), p11 = exp2f(s[3] - mn1);
+        l[0] = l[0] * c0 + p00 + p10;  // this thread's tokens only; lanes reduced at the end
+        l[1] = l[1] * c1 + p01 + p11;
+        // P^T fragments (k = token, n = head) by transposing the two 8x8 halves
+        const uint16_t h00 = f32_to_bf16_bits(p00), h01 = f32_to_bf16_bits(p01);
+        const uint16_t h10 = f32_to_bf16_bits(p10), h11 = f32_to_bf16_bits(p11);
+        const uint32_t ph0 = movm_t(pack2(h00, h01)), ph1 = movm_t(pack2(h10, h11));
+        const uint32_t pl0 = movm_t(pack2(f32_to_bf16_bits(p00 - bf16_bits_to_f32(h00)),
+                                          f32_to_bf16_bits(p01 - bf16_bits_to_f32(h01))));
+        const uint32_t pl1 = movm_t(pack2(f32_to_bf16_bits(p10 - bf16_bits_to_f32(h10)),
+                                          f32_to_bf16_bits(p11 - bf16_bits_to_f32(h11))));
+        // ---- O^T += V^T P^T: 8 d-tiles of 16 ----
 #pragma unroll
-        for (int tok = 0; tok < kPage; ++tok) {
-            const uint2 vv = *reinterpret_cast<const uint2*>(sv + tok * kD + lane * 4);
-            const float v0 = lo_bf16(vv.x), v1 = hi_bf16(vv.x), v2 = lo_bf16(vv.y), v3 = hi_bf16(vv.y);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float pj = __shfl_sync(0xffffffffu, pe[g][tok >> 2], (tok & 3) * 8);
-                acc[g][0] = fmaf(pj, v0, acc[g][0]);
-                acc[g][1] = fmaf(pj, v1, acc[g][1]);
-                acc[g][2] = fmaf(pj, v2, acc[g][2]);
-                acc[g][3] = fmaf(pj, v3, acc[g][3]);
-            }
+        for (int mt = 0; mt < 8; ++mt) {
+            acc[mt][0] *= c0;
+            acc[mt][1] *= c1;
+            acc[mt][2] *= c0;
+            acc[mt][3] *= c1;
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4_t(sv + pg_off(v_row, 2 * mt + v_chunk), a0, a1, a2, a3);
+            mma16816(acc[mt], a0, a1, a2, a3, ph0, ph1);
+            mma16816(acc[mt], a0, a1, a2, a3, pl0, pl1);
         }
         __syncwarp();  // every lane is done with this stage
         if (lane == 0 && page + kStagesW * kWarps < n_pages) issue(page + kStagesW * kWarps, st);
         if (st == kStagesW - 1) phase ^= 1;
     }
-
-    // ---- merge the warps' partial softmax states ----
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        float* c = comb + (warp * G + g) * kCombStride;
-        if (lane == 0) {
-            c[0] = m[g];
-            c[1] = l[g];
+    for (int o = 4; o <= 16; o <<= 1) {
+        l[0] += __shfl_xor_sync(0xffffffffu, l[0], o);
+        l[1] += __shfl_xor_sync(0xffffffffu, l[1], o);
+    }
+
+    // ---- merge the warps' partial softmax states: comb[warp][head][d | m | l] ----
+    {
+        float* cw = comb(warp);  // every copy into this warp's ring has been consumed
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            float* ch = cw + (2 * tg + e) * kCombStride;
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                ch[mt * 16 + g] = acc[mt][e];
+                ch[mt * 16 + g + 8] = acc[mt][2 + e];
+            }
+            if (g == 0) {
+                ch[kD] = m[e];
+                ch[kD + 1] = l[e];
+            }
         }
-        *reinterpret_cast<float4*>(c + 4 + lane * 4) = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < G * kD; idx += blockDim.x) {
-        const int g = idx / kD, d = idx % kD;
-        float M = -FLT_MAX;
-        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, comb[(w * G + g) * kCombStride]);
+        const int hh = idx / kD, d = idx % kD;
+        float M = -INFINITY;
+        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, comb(w)[hh * kCombStride + kD]);
         float den = 0.f, num = 0.f;
         for (int w = 0; w < kWarps; ++w) {
-            const float* c = comb + (w * G + g) * kCombStride;
-            const float f = c[1] > 0.f ? exp2f(c[0] - M) : 0.f;
-            den += c[1] * f;
-            num += c[4 + d] * f;
+            const float* c = comb(w) + hh * kCombStride;
+            const float f = c[kD + 1] > 0.f ? exp2f(c[kD] - M) : 0.f;  // idle warps: l = 0
+            den += c[kD + 1] * f;
+            num += c[d] * f;
         }
         const float o = num / den;
-        const int col = (h * G + g) * kD + d;
+        const int col = (h * G + hh) * kD + d;
         if (out_p) *reinterpret_cast<uint16_t*>(out_p + b_packed_off(t, col, R)) = f32_to_bf16_bits(o);
         if (out_f) out_f[static_cast<int64_t>(t) * (G * static_cast<int64_t>(nkv)) * kD + col] = o;
     }
 }
 
+// One CTA per token: 16-byte chunks of this step's K and V rows into the
+// swizzled page slot of position pos[t].
 __global__ void kv_append_kernel(const uint16_t* qkv, int nq, int nkv, int d, const int32_t* seq,
                                  const int32_t* pos, const int32_t* bt, int max_pages, int page,
                                  uint16_t* kp, uint16_t* vp) {
@@ -221,19 +254,21 @@ __global__ void kv_append_kernel(const uint16_t* qkv, int nq, int nkv, int d, co
     const int p = pos[t];
     const int id = bt[static_cast<int64_t>(seq[t]) * max_pages + p / page];
     const int within = p % page;
-    for (int j = threadIdx.x; j < nkv * d; j += blockDim.x) {
-        const int h = j / d, i = j % d;
-        const int64_t off = ((static_cast<int64_t>(id) * nkv + h) * page + within) * d + i;
-        kp[off] = qkv[static_cast<int64_t>(t) * W + nq * d + j];
-        vp[off] = qkv[static_cast<int64_t>(t) * W + (nq + nkv) * d + j];
+    const int cpr = d / 8;
+    for (int j = threadIdx.x; j < 2 * nkv * cpr; j += blockDim.x) {
+        const int which = j / (nkv * cpr), jj = j % (nkv * cpr);
+        const int hh = jj / cpr, c = jj % cpr;
+        const int64_t off = (static_cast<int64_t>(id) * nkv + hh) * page * d + kv_page_off(within, c * 8);
+        const uint4 v = *reinterpret_cast<const uint4*>(qkv + static_cast<int64_t>(t) * W + (nq + which * nkv) * d + jj * 8);
+        *reinterpret_cast<uint4*>((which ? vp : kp) + off) = v;
     }
 }
-
 template <int G>
 cudaError_t launch_g(const uint16_t* q, int ldq, const uint16_t* kp, const uint16_t* vp,
                      const int32_t* bt, int max_pages, const int32_t* seq, const int32_t* ctx, int T,
                      int nkv, uint8_t* out_p, int R, float* out_f, cudaStream_t s) {
-    const int smem = kWarps * kStagesW * 2 * kPageBytes + kWarps * G * kCombStride * 4;
+    const int smem = kWarps * kStagesW * 2 * kPageBytes;
+    static_assert(8 * kCombStride * 4 <= kStagesW * 2 * kPageBytes, "merge state fits a warp's ring");
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(gqa_decode_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -41,6 +41,18 @@ __host__ __device__ inline uint64_t b_packed_off(uint64_t n, uint64_t k, uint64_
            ((((k & 63u) >> 3) ^ (n & 7u)) << 4) + (k & 7u) * 2u;
 }
 
+// Paged KV layout: one (page, kv head) slice is
+// kKvPage tokens x d = 128 bf16, 256 B per token row, with the 16-byte
+// chunks of token r XOR-swizzled by (r & 7).  The slice stays one contiguous
+// 4 KiB run (a single 1-D bulk copy), and 8 consecutive token rows at the
+// same logical chunk fall in 8 distinct bank groups, so ldmatrix (and its
+// .trans form for V) is conflict-free on the staged page.  Element offset of
+// (token-in-page tok, dim) inside a slice:
+constexpr int kKvPage = 16;
+__host__ __device__ inline uint32_t kv_page_off(uint32_t tok, uint32_t dim) {
+    return tok * 128u + (((dim >> 3) ^ (tok & 7u)) << 3) + (dim & 7u);
+}
+
 #if defined(__CUDACC__)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -62,9 +62,19 @@ cudaError_t launch_pack_rows(const uint16_t* src, int ld, int T, int K, uint8_t*
 // cos/sin table [max_pos][d/2] (float2), output bf16 [T, (nq+2nkv)d] rows
 // (q | k | v): the D1 offload layout.  qkv may hold `parts` split-K partials
 // at qkv + p*part_stride; they are summed first.
+// With kv (A_g = 1) the roped k and the v rows are also stored into the
+// swizzled paged pool at position pos[t] of sequence kv->seq[t] (fused
+// kv_append; d = 128, 16-token pages).
+struct KvAppend {
+    uint16_t* k_pool = nullptr;
+    uint16_t* v_pool = nullptr;
+    const int32_t* block_table = nullptr;  // [seq][max_pages]
+    int max_pages = 0;
+    const int32_t* seq = nullptr;          // [T]
+};
 cudaError_t launch_rope_qkv(const float* qkv, int parts, int64_t part_stride, const int32_t* pos,
                             const float2* rope, int T, int nq, int nkv, int d, uint16_t* out,
-                            cudaStream_t s);
+                            cudaStream_t s, const KvAppend* kv = nullptr);
 
 // Router (SURVEY.md §2c router_topk_permute, first half): optional fused
 // RMSNorm (x fp32 + gamma) or direct bf16 input; logits with the fixed lane
@@ -86,9 +96,12 @@ cudaError_t launch_moe_permute(const int32_t* topk_idx, const uint16_t* hn, int 
                                int32_t* inv, uint8_t* x_packed, int R, cudaStream_t s);
 
 // x_out[t] = h[t] + sum_s w[t,s] * y[inv[t*K+s]]  (fp32, slot order).
+// With gamma: also RMSNorm(x_out) * gamma -> packed bf16 xn (capacity R),
+// the operand of the next projection (fused next-layer / final norm).
 cudaError_t launch_moe_combine(const float* h, const float* y, int ldy, const int32_t* inv,
                                const float* topk_w, int T, int H, int K, float* x_out,
-                               cudaStream_t s);
+                               cudaStream_t s, const uint16_t* gamma = nullptr, float eps = 0.f,
+                               uint8_t* xn = nullptr, int R = 0);
 
 // out[i] = sum_p parts[p*stride + i] (+ add[i]); n % 4 == 0.  Fixed order.
 cudaError_t launch_sum_parts(const float* parts, int n_parts, int64_t stride, const float* add,

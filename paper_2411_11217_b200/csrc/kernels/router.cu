@@ -1,7 +1,7 @@
 // Top-k router + token permutation (north_star item 2; SURVEY.md §2c
 // router_topk_permute), warp-level.
 //
-// router_kernel: one CTA per token.  Optional fused RMSNorm of the fp32
+// router_kernel: one CTA (H/8 threads) per token.  Optional fused RMSNorm of the fp32
 // residual (the PostAttn norm), then one warp per expert computes the logit
 // with the FIXED reduction tree of oracle/oracle_numerics.c:orc_router —
 // lane l accumulates 8-element chunks c = l, l+32, ... with fmaf in element
@@ -26,70 +26,83 @@ namespace {
 constexpr int kMaxE = 64;
 constexpr int kMaxSlots = 16384;  // T*K per launch (prefill chunks)
 
-__global__ void router_kernel(const float* x, const uint16_t* gamma, float eps,
-                              const uint16_t* hn_in, const uint16_t* w, int H, int E, int K,
-                              uint16_t* hn_out, float* logits, int32_t* topk_idx, float* topk_w,
-                              int parts, int64_t part_stride, const float* residual, float* h_out) {
+// One CTA of H/8 threads per token; thread i owns elements [8i, 8i+8) and
+// issues every load of its slice (split-K partials + residual) up front.
+__global__ void __launch_bounds__(768) router_kernel(const float* x, const uint16_t* gamma, float eps,
+                                                      const uint16_t* hn_in, const uint16_t* w, int H, int E,
+                                                      int K, uint16_t* hn_out, float* logits, int32_t* topk_idx,
+                                                      float* topk_w, int parts, int64_t part_stride,
+                                                      const float* residual, float* h_out) {
     extern __shared__ __align__(16) uint8_t sm[];
     uint16_t* hn = reinterpret_cast<uint16_t*>(sm);                 // H bf16
     float* lg = reinterpret_cast<float*>(sm + ((H * 2 + 15) & ~15)); // E fp32
     __shared__ float red[32];
     const int t = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int i = threadIdx.x * 8;
 
     if (hn_in) {
-        for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8)
-            *reinterpret_cast<uint4*>(hn + i) =
-                *reinterpret_cast<const uint4*>(hn_in + static_cast<int64_t>(t) * H + i);
+        *reinterpret_cast<uint4*>(hn + i) = *reinterpret_cast<const uint4*>(hn_in + static_cast<int64_t>(t) * H + i);
     } else {
-        const float* xr = x + static_cast<int64_t>(t) * H;
+        const float* xr = x + static_cast<int64_t>(t) * H + i;
+        float v[8];
+        {
+            const float4 a = *reinterpret_cast<const float4*>(xr);
+            const float4 b = *reinterpret_cast<const float4*>(xr + 4);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        }
         if (parts > 0) {
             // h = residual + sum of the O-projection split-K partials (fixed
             // order -> deterministic); h_out feeds the top-k combine
-            float* hr = h_out + static_cast<int64_t>(t) * H;
-            const float* rr = residual + static_cast<int64_t>(t) * H;
-            for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
-                float4 a = *reinterpret_cast<const float4*>(xr + i);
-                for (int p = 1; p < parts; ++p) {
-                    const float4 b = *reinterpret_cast<const float4*>(xr + p * part_stride + i);
-                    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+            float pv[4][8];  // partials 1..3 in registers (the runtime uses <= 4 splits)
+#pragma unroll
+            for (int p = 1; p < 4; ++p)
+                if (p < parts) {
+                    const float4 a = *reinterpret_cast<const float4*>(xr + p * part_stride);
+                    const float4 b = *reinterpret_cast<const float4*>(xr + p * part_stride + 4);
+                    pv[p][0] = a.x; pv[p][1] = a.y; pv[p][2] = a.z; pv[p][3] = a.w;
+                    pv[p][4] = b.x; pv[p][5] = b.y; pv[p][6] = b.z; pv[p][7] = b.w;
                 }
-                const float4 r = *reinterpret_cast<const float4*>(rr + i);
-                *reinterpret_cast<float4*>(hr + i) = make_float4(a.x + r.x, a.y + r.y, a.z + r.z, a.w + r.w);
-            }
-            __syncthreads();
-            xr = hr;
+            const float* rr = residual + static_cast<int64_t>(t) * H + i;
+            const float4 ra = *reinterpret_cast<const float4*>(rr);
+            const float4 rb = *reinterpret_cast<const float4*>(rr + 4);
+            const float rv[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+            for (int p = 1; p < 4; ++p)
+                if (p < parts)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) v[j] += pv[p][j];
+            for (int p = 4; p < parts; ++p)  // further partials, same ascending order
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] += xr[p * part_stride + j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] += rv[j];
+            float* hr = h_out + static_cast<int64_t>(t) * H + i;
+            *reinterpret_cast<float4*>(hr) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4*>(hr + 4) = make_float4(v[4], v[5], v[6], v[7]);
         }
         float ss = 0.0f;
-        for (int i = threadIdx.x * 4; i < H; i += blockDim.x * 4) {
-            const float4 v = *reinterpret_cast<const float4*>(xr + i);
-            ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ss += v[j] * v[j];
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
         if (lane == 0) red[warp] = ss;
         __syncthreads();
         float tot = 0.0f;
-        for (int i = 0; i < nw; ++i) tot += red[i];
+        for (int k = 0; k < nw; ++k) tot += red[k];
         const float r = 1.0f / sqrtf(tot / static_cast<float>(H) + eps);
-        for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
-            const float4 a = *reinterpret_cast<const float4*>(xr + i);
-            const float4 b = *reinterpret_cast<const float4*>(xr + i + 4);
-            const uint4 gv = *reinterpret_cast<const uint4*>(gamma + i);
-            const uint16_t* g = reinterpret_cast<const uint16_t*>(&gv);
-            const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            uint4 o;
-            uint16_t* ob = reinterpret_cast<uint16_t*>(&o);
+        const uint4 gv = *reinterpret_cast<const uint4*>(gamma + i);
+        const uint16_t* g = reinterpret_cast<const uint16_t*>(&gv);
+        uint4 o;
+        uint16_t* ob = reinterpret_cast<uint16_t*>(&o);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) ob[j] = f32_to_bf16_bits(v[j] * r * bf16_bits_to_f32(g[j]));
-            *reinterpret_cast<uint4*>(hn + i) = o;
-        }
+        for (int j = 0; j < 8; ++j) ob[j] = f32_to_bf16_bits(v[j] * r * bf16_bits_to_f32(g[j]));
+        *reinterpret_cast<uint4*>(hn + i) = o;
     }
-    __syncthreads();
     if (hn_out)
-        for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8)
-            *reinterpret_cast<uint4*>(hn_out + static_cast<int64_t>(t) * H + i) =
-                *reinterpret_cast<const uint4*>(hn + i);
+        *reinterpret_cast<uint4*>(hn_out + static_cast<int64_t>(t) * H + i) = *reinterpret_cast<const uint4*>(hn + i);
+    __syncthreads();
 
     const int chunks = H / 8;
     for (int e = warp; e < E; e += nw) {
@@ -108,26 +121,34 @@ __global__ void router_kernel(const float* x, const uint16_t* gamma, float eps,
         if (lane == 0) lg[e] = acc;
     }
     __syncthreads();
+    if (logits)
+        for (int e = threadIdx.x; e < E; e += blockDim.x) logits[static_cast<int64_t>(t) * E + e] = lg[e];
     if (threadIdx.x == 0) {
-        if (logits)
-            for (int e = 0; e < E; ++e) logits[static_cast<int64_t>(t) * E + e] = lg[e];
+        // selection (ties -> lower index) and softmax over the k selected
+        // logits; fully unrolled over k <= 8 so everything stays in registers
         uint64_t used = 0;
-        int sel[8];
-        for (int s = 0; s < K; ++s) {
-            int best = -1;
-            for (int e = 0; e < E; ++e)
-                if (!((used >> e) & 1) && (best < 0 || lg[e] > lg[best])) best = e;
-            used |= 1ull << best;
-            sel[s] = best;
-            topk_idx[t * K + s] = best;
+        float* sv = red;  // K <= 8 selected exp values (red is free again here)
+        float top = 0.0f, sum = 0.0f;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            if (s < K) {
+                int best = -1;
+                float bv = 0.0f;
+                for (int e = 0; e < E; ++e)
+                    if (!((used >> e) & 1) && (best < 0 || lg[e] > bv)) {
+                        best = e;
+                        bv = lg[e];
+                    }
+                used |= 1ull << best;
+                topk_idx[t * K + s] = best;
+                if (s == 0) top = bv;
+                sv[s] = expf(bv - top);
+                sum += sv[s];
+            }
         }
-        const float top = lg[sel[0]];
-        float ws[8], sum = 0.0f;
-        for (int s = 0; s < K; ++s) {
-            ws[s] = expf(lg[sel[s]] - top);
-            sum += ws[s];
-        }
-        for (int s = 0; s < K; ++s) topk_w[t * K + s] = ws[s] / sum;
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            if (s < K) topk_w[t * K + s] = sv[s] / sum;
     }
 }
 
@@ -216,8 +237,9 @@ cudaError_t launch_router(const float* x, const uint16_t* gamma, float eps, cons
     if (H % 256 || E > kMaxE || K > 8 || K > E || (!hn_in && (!x || !gamma)) ||
         (parts > 0 && (!residual || !h_out)))
         return cudaErrorInvalidValue;
+    if (H > 6144) return cudaErrorInvalidValue;  // H/8 threads per token
     const int smem = ((H * 2 + 15) & ~15) + E * 4;
-    router_kernel<<<T, 256, smem, s>>>(x, gamma, eps, hn_in, w, H, E, K, hn_out, logits, topk_idx,
+    router_kernel<<<T, H / 8, smem, s>>>(x, gamma, eps, hn_in, w, H, E, K, hn_out, logits, topk_idx,
                                        topk_w, parts, part_stride, residual, h_out);
     return cudaGetLastError();
 }

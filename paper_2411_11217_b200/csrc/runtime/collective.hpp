@@ -21,5 +21,10 @@ class Collective {
 
 void nccl_unique_id(uint8_t out[128]);
 std::unique_ptr<Collective> make_nccl_collective(const uint8_t id[128], int rank, int size, int device);
+// Shard-only measurement: rank `rank` of a `size`-way job runs alone and the
+// all-reduce is elided (buffers keep this rank's partial sums).  Used to
+// measure a tensor-parallel job's per-GPU step on a single device; never a
+// numerical path.
+std::unique_ptr<Collective> make_elided_collective(int rank, int size);
 
 }  // namespace mlt

@@ -270,16 +270,22 @@ PrefillReport Runtime::prefill(const int32_t* tokens, const int32_t* lens, int32
                 a.out_f32 = pf_y_;
                 a.ldo = W_;
                 pl("qkv_gemm", mltk::launch_gemm(a, num_sms_, s_gpu_));
-                pl("rope_qkv", mltk::launch_rope_qkv(pf_y_, 1, 0, d_tpos, d_rope_, Tc, nq_, nkv_, d_, pf_qkv_, s_gpu_));
-                // KV: host cache (staged, one strided DMA per sequence) or the paged device pool
+                // KV: host cache (staged, one strided DMA per sequence) or the paged
+                // device pool (stored by rope_qkv itself)
+                mltk::KvAppend kv;
+                if (policy_.attn_on_gpu) {
+                    kv.k_pool = d_kpool_;
+                    kv.v_pool = d_vpool_;
+                    kv.block_table = d_block_table_ + static_cast<size_t>(l) * N_ * max_pages_;
+                    kv.max_pages = max_pages_;
+                    kv.seq = d_tseqg;
+                }
+                pl("rope_qkv", mltk::launch_rope_qkv(pf_y_, 1, 0, d_tpos, d_rope_, Tc, nq_, nkv_, d_, pf_qkv_, s_gpu_,
+                                                     policy_.attn_on_gpu ? &kv : nullptr));
                 uint16_t* sk = pf_kst_[b];
                 if (!policy_.attn_on_gpu)
                     pl("kv_stage", mltk::launch_kv_stage(pf_qkv_, W_, nq_, nkv_, d_, d_tseq, d_tpos, d_srow, d_slen,
                                                          Tc, sk, sk + kv_half, s_gpu_));
-                else
-                    pl("kv_append", mltk::launch_kv_append(pf_qkv_, nq_, nkv_, d_, d_tseqg, d_tpos, Tc,
-                                                           d_block_table_ + static_cast<size_t>(l) * N_ * max_pages_,
-                                                           max_pages_, page_, d_kpool_, d_vpool_, s_gpu_));
                 pl("prefill_attention", mltk::launch_prefill_attention(pf_qkv_, W_, d_tiles, c.n_tiles, nq_, nkv_, d_,
                                                                        pf_xn_, pf_R_, s_gpu_));
                 // PostAttn: O (+ residual) -> router -> permute -> experts -> combine

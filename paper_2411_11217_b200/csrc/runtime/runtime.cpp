@@ -123,7 +123,9 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     ck(cudaStreamCreateWithFlags(&s_gpu_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
-    if (opt.tp_size > 1) coll_ = make_nccl_collective(opt.nccl_id, opt.tp_rank, opt.tp_size, opt.device);
+    if (opt.tp_size > 1)
+        coll_ = opt.tp_shard_only ? make_elided_collective(opt.tp_rank, opt.tp_size)
+                                  : make_nccl_collective(opt.nccl_id, opt.tp_rank, opt.tp_size, opt.device);
     arena_ = std::make_unique<Arena>(static_cast<size_t>(opt.budget_bytes));
     build_catalog();
     allocate();
@@ -191,7 +193,10 @@ void Runtime::allocate() {
     d_qkv_bf16_ = static_cast<uint16_t*>(A.alloc(static_cast<size_t>(M_) * mu_ * W_ * 2, "qkv_bf16"));
     d_attn_in_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(M_) * Rmu_ * Ho_ * 2, "attn_in"));
     if (coll_) d_cbuf_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * H_ * 4, "tp_combine"));
-    d_xn_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Rmu_) * H_ * 2, "xn"));
+    // one normed-activation operand per micro-batch: the fused combine+norm of
+    // PostAttn(layer l, mb) produces PreAttn(layer l+1, mb)'s operand, and
+    // other micro-batches' PreAttn run in between (CGOPipe order)
+    d_xn_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(M_) * Rmu_ * H_ * 2, "xn"));
     d_qkv_f32_ = static_cast<float*>(A.alloc(static_cast<size_t>(kMaxSplits) * Rmu_ * W_ * 4, "qkv_f32"));
     d_h_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * H_ * 4, "h"));
     d_hparts_ = static_cast<float*>(A.alloc(static_cast<size_t>(kMaxSplits) * mu_ * H_ * 4, "h_parts"));
@@ -341,6 +346,7 @@ void Runtime::prefill_synthetic(int prompt_len, uint64_t seed) {
                             }
             } else {
                 // paged device cache: page id = (l*N + s)*max_pages + p/page, [nkv][page][d]
+                // with the token-row swizzle of common.cuh kv_page_off
                 const size_t per_seq = static_cast<size_t>(max_pages_) * nkv_ * page_ * d_;
                 tmp.assign(per_seq * N_, 0);
 #pragma omp parallel for collapse(2) schedule(static)
@@ -352,7 +358,8 @@ void Runtime::prefill_synthetic(int prompt_len, uint64_t seed) {
                                 const uint64_t hv = mix64(key + idx);
                                 const float r = 2.0f * (static_cast<float>(hv >> 40) * 0x1p-24f) - 1.0f;
                                 const size_t page = p / page_;
-                                tmp[static_cast<size_t>(s) * per_seq + ((page * nkv_ + h) * page_ + p % page_) * d_ + i] = f32_to_bf16(r);
+                                tmp[static_cast<size_t>(s) * per_seq + (page * nkv_ + h) * page_ * d_ +
+                                    mltk::kv_page_off(p % page_, i)] = f32_to_bf16(r);
                             }
                 uint16_t* pool = which ? d_vpool_ : d_kpool_;
                 ck(cudaMemcpy(pool + static_cast<size_t>(l) * N_ * per_seq, tmp.data(), tmp.size() * 2,
@@ -468,15 +475,17 @@ void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
                                                      : d_tok_out_ + static_cast<size_t>(step - 2) * N_ + t0;
         kl("embed", mltk::launch_embed(src, d_embed_, mu_, H_, d_x_ + static_cast<size_t>(t0) * H_, s_gpu_));
     }
-    kl("rmsnorm_pack", mltk::launch_rmsnorm_pack(d_x_ + static_cast<size_t>(t0) * H_, d_attn_norm_[l], mu_, H_,
-                                                 ext_.rms_eps, d_xn_, Rmu_, s_gpu_));
+    uint8_t* xn = d_xn_ + static_cast<size_t>(mb - 1) * Rmu_ * H_ * 2;
+    if (layer == 1 || coll_)  // otherwise the previous layer's combine produced it
+        kl("rmsnorm_pack", mltk::launch_rmsnorm_pack(d_x_ + static_cast<size_t>(t0) * H_, d_attn_norm_[l], mu_, H_,
+                                                     ext_.rms_eps, xn, Rmu_, s_gpu_));
     mltk::GemmArgs a;
     a.a_table = dev_tables_ + (static_cast<size_t>(l) * 2 + slot_of(g)) * table_entries_ + tab_qkv_;
     a.n_mats = 1;
     a.G = 1;
     a.RB = W_ / 128;
     a.K = H_;
-    a.b = d_xn_;
+    a.b = xn;
     a.R = Rmu_;
     a.rows_dense = mu_;
     dense_tiling(W_ / 128, a.n_cap, a.n_chunks, a.k_splits);
@@ -488,8 +497,16 @@ void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
     kl("qkv_gemm", mltk::launch_gemm(a, num_sms_, s_gpu_));
     const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
     uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
+    mltk::KvAppend kv;  // A_g = 1: this step's k/v go straight into the paged pool
+    if (policy_.attn_on_gpu) {
+        kv.k_pool = d_kpool_;
+        kv.v_pool = d_vpool_;
+        kv.block_table = d_block_table_ + static_cast<size_t>(l) * N_ * max_pages_;
+        kv.max_pages = max_pages_;
+        kv.seq = d_seq_ + t0;
+    }
     kl("rope_qkv", mltk::launch_rope_qkv(d_qkv_f32_, a.k_splits, a.split_stride, pos, d_rope_, mu_, nq_, nkv_,
-                                         d_, qkv, s_gpu_));
+                                         d_, qkv, s_gpu_, policy_.attn_on_gpu ? &kv : nullptr));
 }
 
 void Runtime::act_offload_qkv(int layer, int mb) {
@@ -514,11 +531,9 @@ void Runtime::act_gpu_attn(int step, int layer, int mb) {
     const int t0 = (mb - 1) * mu_;
     const int l = layer - 1;
     const uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
-    const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
+    // this step's k/v were stored into the pool by rope_qkv (PreAttn)
     const int32_t* ctx = d_pos_ + static_cast<size_t>(max_steps_) * N_ + static_cast<size_t>(step - 1) * N_ + t0;
     const int32_t* bt = d_block_table_ + static_cast<size_t>(l) * N_ * max_pages_;
-    kl("kv_append", mltk::launch_kv_append(qkv, nq_, nkv_, d_, d_seq_ + t0, pos, mu_, bt, max_pages_, page_,
-                                           d_kpool_, d_vpool_, s_gpu_));
     kl("gqa_decode_paged", mltk::launch_gqa_decode_paged(qkv, W_, d_kpool_, d_vpool_, bt, max_pages_, d_seq_ + t0,
                                                          ctx, mu_, nq_, nkv_, d_, page_, d_attn_gpu_, Rmu_,
                                                          nullptr, s_gpu_));
@@ -531,6 +546,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     const int l = layer - 1;
     const uint8_t** tab = dev_tables_ + (static_cast<size_t>(l) * 2 + slot_of(g)) * table_entries_;
     float* x = d_x_ + static_cast<size_t>(t0) * H_;
+    uint8_t* xn = d_xn_ + static_cast<size_t>(mb - 1) * Rmu_ * H_ * 2;  // next layer's normed operand
     // O projection + residual
     mltk::GemmArgs o;
     o.a_table = tab + tab_o_;
@@ -602,15 +618,19 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
         coll_->all_reduce_sum(d_cbuf_, static_cast<size_t>(mu_) * H_, s_gpu_);
         kl("residual_add", mltk::launch_sum_parts(d_cbuf_, 1, 0, d_h_, x, static_cast<int64_t>(mu_) * H_, s_gpu_));
     } else {
-        kl("moe_combine", mltk::launch_moe_combine(d_h_, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, x, s_gpu_));
+        // + the next layer's attention norm (or the final norm) fused
+        kl("moe_combine", mltk::launch_moe_combine(d_h_, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, x, s_gpu_,
+                                                   layer == L_ ? d_final_norm_ : d_attn_norm_[l + 1],
+                                                   ext_.rms_eps, xn, Rmu_));
     }
     if (layer == L_) {  // step epilogue: final norm -> lm_head -> greedy ids
-        kl("rmsnorm_pack", mltk::launch_rmsnorm_pack(x, d_final_norm_, mu_, H_, ext_.rms_eps, d_xn_, Rmu_, s_gpu_));
+        if (coll_)
+            kl("rmsnorm_pack", mltk::launch_rmsnorm_pack(x, d_final_norm_, mu_, H_, ext_.rms_eps, xn, Rmu_, s_gpu_));
         mltk::GemmArgs lm;
         lm.a_table = d_lm_table_;
         lm.RB = V_ / 128;
         lm.K = H_;
-        lm.b = d_xn_;
+        lm.b = xn;
         lm.R = Rmu_;
         lm.rows_dense = mu_;
         lm.n_cap = std::min(256, Rmu_);  // 250+ row blocks already fill the chip

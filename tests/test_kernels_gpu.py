@@ -212,9 +212,13 @@ def test_rmsnorm_pack_and_embed(K):
     assert np.abs(got - ref).max() <= 1e-2 * np.abs(ref).max()
 
 
-def test_rope_and_paged_attention(K):
+@pytest.mark.parametrize("nq,nkv", [(8, 2), (12, 2), (16, 2), (2, 2)])
+def test_rope_and_paged_attention(K, nq, nkv):
+    """rope_qkv + kv_append + gqa_decode_paged against the fp32 oracle for
+    G = n_q/n_kv in {4 (8x7B), 6 (8x22B/DBRX), 8, 1}; ragged contexts incl.
+    1, page-1, page, page+1 tokens."""
     from oracle import bind as orc
-    T, nq, nkv, d, page = 6, 8, 2, 128, 16
+    T, d, page = 6, 128, 16
     W = (nq + 2 * nkv) * d
     g = torch.Generator().manual_seed(5)
     ctx = np.array([1, 15, 16, 17, 100, 300], np.int32)
@@ -244,11 +248,14 @@ def test_rope_and_paged_attention(K):
     hist_v = orc.f32_to_bf16(np.random.default_rng(2).uniform(-1, 1, (T, cap, nkv, d)))
     kp = np.zeros((n_pages, nkv, page, d), np.uint16)
     vp = np.zeros_like(kp)
+    # swizzled page rows (common.cuh kv_page_off): chunk c of token r at c ^ (r & 7)
+    def swz(row, r):
+        return row.reshape(nkv, d // 8, 8)[:, np.arange(d // 8) ^ (r & 7)].reshape(nkv, d)
     for t in range(T):
         for j in range(pos[t]):
             pid = bt[t, j // page]
-            kp[pid, :, j % page] = hist_k[t, j]
-            vp[pid, :, j % page] = hist_v[t, j]
+            kp[pid, :, j % page] = swz(hist_k[t, j], j % page)
+            vp[pid, :, j % page] = swz(hist_v[t, j], j % page)
     kpool.copy_(torch.from_numpy(kp.reshape(-1).view(np.int16)))
     vpool.copy_(torch.from_numpy(vp.reshape(-1).view(np.int16)))
     bt_d = torch.from_numpy(bt).cuda()

@@ -78,6 +78,12 @@ def _kv_check(rt, ref, dims, lens, a_g, layers, rpos):
             page = 16
             mp = CTX // page
             pool = rt.debug_read(name + "pool", np.uint16).reshape(layers, N, mp, nkv, page, d)
+            # undo the token-row chunk swizzle (common.cuh kv_page_off): chunk c of
+            # token r is stored at c ^ (r & 7)
+            idx = np.arange(d // 8)[None, :] ^ (np.arange(page)[:, None] & 7)  # [page][chunk]
+            pool = np.take_along_axis(pool.reshape(layers, N, mp, nkv, page, d // 8, 8),
+                                      idx[None, None, None, None, :, :, None], axis=5).reshape(
+                layers, N, mp, nkv, page, d)
             kc = pool.transpose(0, 1, 3, 2, 4, 5).reshape(layers, N, nkv, mp * page, d)
         for l in range(layers):
             ok = ref.kv(l, which)  # [N][max_ctx][nkv][d]
