@@ -49,7 +49,7 @@ CONFIGS = {
                             r_w={1: 0.0, 2: 0.05, 4: 0.15, 8: 0.40}, a_g=0, budget=16e9, prompt=512,
                             gen=32, vocab=32000),
     "dbrx-tp": dict(model=(40, 6144, 10752, 48, 8, 16, 4), N=256, mu=64,
-                    r_w={1: 0.0, 2: 0.05, 4: 0.20}, a_g=0, budget=16e9, prompt=512, gen=128,
+                    r_w={1: 0.0, 2: 0.05, 4: 0.20, 8: 0.45}, a_g=0, budget=16e9, prompt=512, gen=128,
                     vocab=32000),
     "tiny": dict(model=(2, 1024, 3584, 8, 2, 8, 2), N=8, mu=4, r_w=0.0, a_g=0, budget=4e9,
                  prompt=16, gen=32, vocab=32000),

@@ -274,6 +274,10 @@ typedef struct mlt_gemm_args_t {
     int32_t n_chunks;     /* token chunks per (group, row block) spread over CTAs; 0 -> 1 */
     int32_t k_splits;     /* split-K: partial s written at out_f32 + s*split_stride; 0 -> 1 */
     int64_t split_stride; /* floats between partial outputs (residual ignored when split) */
+    unsigned long long* trace; /* optional [gridDim][8] %globaltimer phase stamps per CTA
+                                  (entry, setup done, first weight copy issued, first stage
+                                  full, last MMA issued, first accumulator ready, epilogue
+                                  done, exit) — a diagnostic, NULL in production */
 } mlt_gemm_args_t;
 
 /* Grouped swap-AB tcgen05 GEMM (SURVEY.md §2c expert_gateup_silu /
@@ -391,6 +395,8 @@ int mlt_nccl_unique_id(uint8_t out[128]);
  * the global rows / columns each local weight matrix covers. */
 typedef struct mlt_tp_shard_t {
     int64_t q_heads, kv_heads, ffn, qkv_rows, o_k;
+    int64_t ffn_off; /* first global h2 row of this rank's slice (128-row blocks, as even as
+                        blocks allow: DBRX h2=10752 at tp=8 -> 1408 or 1280 rows) */
 } mlt_tp_shard_t;
 int mlt_tp_shard(const mlt_model_spec_t* model, int rank, int size, mlt_tp_shard_t* out);
 /* Host: this rank's local weight matrix `kind` (5 wqkv, 6 wo, 8 w1, 9 w3,

@@ -457,7 +457,8 @@ class GemmArgs(C.Structure):
                 ("n_cap", C.c_int32), ("epi", C.c_int32), ("alpha", C.c_float),
                 ("out_f32", C.c_void_p), ("ldo", C.c_int32), ("residual", C.c_void_p),
                 ("ldr", C.c_int32), ("out_packed", C.c_void_p), ("out_R", C.c_int32),
-                ("n_chunks", C.c_int32), ("k_splits", C.c_int32), ("split_stride", C.c_int64)]
+                ("n_chunks", C.c_int32), ("k_splits", C.c_int32), ("split_stride", C.c_int64),
+                ("trace", C.c_void_p)]
 
 
 V, I, F = C.c_void_p, C.c_int, C.c_float

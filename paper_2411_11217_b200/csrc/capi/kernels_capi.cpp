@@ -66,6 +66,7 @@ mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
     g.n_chunks = a->n_chunks > 0 ? a->n_chunks : 1;
     g.k_splits = a->k_splits > 0 ? a->k_splits : 1;
     g.split_stride = a->split_stride;
+    g.trace = a->trace;
     return g;
 }
 

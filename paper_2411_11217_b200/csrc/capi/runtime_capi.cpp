@@ -84,7 +84,7 @@ lightplan::ModelSpec model_in(const mlt_model_spec_t* m) {
 int mlt_tp_shard(const mlt_model_spec_t* m, int rank, int size, mlt_tp_shard_t* out) {
     return guard([&] {
         const mlt::Shard s = mlt::make_shard(model_in(m), rank, size);
-        *out = {s.q_heads, s.kv_heads, s.ffn, s.qkv_rows, s.o_k};
+        *out = {s.q_heads, s.kv_heads, s.ffn, s.qkv_rows, s.o_k, s.ffn_off};
         return MLT_OK;
     });
 }

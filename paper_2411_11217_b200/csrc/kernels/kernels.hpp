@@ -30,6 +30,8 @@ struct GemmArgs {
     // optional in-kernel timing: [0] = min over CTAs of the %globaltimer at
     // entry, [1] = ~(max at exit); both pre-set to all ones by the caller
     unsigned long long* timing = nullptr;
+    // optional per-CTA phase stamps [gridDim][8] (diagnostic, see mlt.h)
+    unsigned long long* trace = nullptr;
     // epilogue
     int epi = kEpiF32;
     float alpha = 1.0f;

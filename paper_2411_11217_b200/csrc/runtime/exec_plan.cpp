@@ -17,14 +17,20 @@ using lightplan::sim::TaskKind;
 
 Shard make_shard(const lightplan::ModelSpec& m, int rank, int size) {
     if (size < 1 || rank < 0 || rank >= size) throw std::invalid_argument("bad tensor-parallel rank/size");
-    if (m.q_heads % size || m.kv_heads % size || m.ffn_dim % size)
-        throw std::invalid_argument("tp must divide n_q, n_kv and h2");
+    if (m.q_heads % size || m.kv_heads % size || m.ffn_dim % 128)
+        throw std::invalid_argument("tp must divide n_q and n_kv; h2 must be a multiple of 128");
     Shard s;
     s.rank = rank;
     s.size = size;
     s.q_heads = m.q_heads / size;
     s.kv_heads = m.kv_heads / size;
-    s.ffn = m.ffn_dim / size;
+    // h2 in 128-row blocks, as evenly as blocks allow (DBRX h2 = 10752 = 84
+    // blocks: tp=8 gives ranks 11 or 10 blocks); every rank keeps UMMA-sized
+    // row blocks and the all-reduce sums the uneven partial products exactly
+    const int64_t blocks = m.ffn_dim / 128;
+    const int64_t b0 = rank * blocks / size, b1 = (rank + 1) * blocks / size;
+    s.ffn = (b1 - b0) * 128;
+    s.ffn_off = b0 * 128;
     s.qkv_rows = (s.q_heads + 2 * s.kv_heads) * m.head_dim();
     s.o_k = s.q_heads * m.head_dim();
     if (s.qkv_rows % 128 || s.ffn % 128 || s.o_k % 64)
@@ -57,13 +63,13 @@ ShardMap shard_map(const lightplan::ModelSpec& m, const Shard& s, int kind) {
             break;
         case kW1:
         case kW3:
-            for (int64_t i = 0; i < s.ffn; ++i) out.rows.push_back(r * s.ffn + i);
+            for (int64_t i = 0; i < s.ffn; ++i) out.rows.push_back(s.ffn_off + i);
             out.k_local = out.k_global = H;
             out.scale = static_cast<float>(sH);
             break;
         case kW2:
             for (int64_t i = 0; i < H; ++i) out.rows.push_back(i);
-            out.col0 = r * s.ffn;
+            out.col0 = s.ffn_off;
             out.k_local = s.ffn;
             out.k_global = m.ffn_dim;
             out.scale = static_cast<float>(sF);

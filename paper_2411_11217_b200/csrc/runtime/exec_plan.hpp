@@ -37,6 +37,7 @@ struct Catalog {
 struct Shard {
     int rank = 0, size = 1;
     int64_t q_heads = 0, kv_heads = 0, ffn = 0;  // local counts
+    int64_t ffn_off = 0;                         // first global h2 row of this rank's slice
     int64_t qkv_rows = 0;                        // (q_heads + 2 kv_heads) * d
     int64_t o_k = 0;                             // q_heads * d (O projection K)
 };

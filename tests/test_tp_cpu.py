@@ -46,7 +46,7 @@ def _shard_weight(lib, model, rank, size, layer, kind, expert):
     return out
 
 
-def _worker(rank, size, port, outdir):
+def _worker(rank, size, port, outdir, ffn=CFG["ffn"]):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -54,7 +54,7 @@ def _worker(rank, size, port, outdir):
     from oracle import bind as orc
     from paper_2411_11217_b200 import capi
     lib = capi.load_product().lib
-    c = CFG
+    c = dict(CFG, ffn=ffn)
     H, d = c["hidden"], c["hidden"] // c["q_heads"]
     model = capi.ModelSpec(c["layers"], H, c["ffn"], c["q_heads"], c["kv_heads"], c["experts"],
                            c["top_k"], 2.0, 2.0)
@@ -107,8 +107,9 @@ def _worker(rank, size, port, outdir):
     dist.destroy_process_group()
 
 
-def test_tp2_layer_matches_unsharded_oracle(tmp_path):
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+@pytest.mark.parametrize("ffn", [512, 640])  # 640 = 5 blocks of 128: uneven h2 shards (2 + 3 blocks)
+def test_tp2_layer_matches_unsharded_oracle(tmp_path, ffn):
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), ffn), nprocs=2, join=True)
     assert all((tmp_path / f"ok_{r}").exists() for r in range(2))
 
 
@@ -135,3 +136,31 @@ def test_shards_tile_the_full_tensors(api):
     w1 = np.concatenate([_shard_weight(lib, model, r, 4, 0, 8, 0) for r in range(4)], axis=0)
     assert np.array_equal(w1, full_w1)
     del c
+
+
+def test_uneven_h2_shards_tile_the_full_tensors(api):
+    """h2 not divisible into tp x 128-row blocks (DBRX h2=10752 at tp=8): ranks
+    get floor/ceil block counts, and the union is still the full W1 / W2."""
+    from oracle import bind as orc
+    from paper_2411_11217_b200 import capi
+    model = capi.ModelSpec(1, 256, 640, 8, 4, 2, 2, 2.0, 2.0)  # 5 blocks over 2 ranks
+    lib = api.lib
+    w1p = [_shard_weight(lib, model, r, 2, 0, 8, 0) for r in range(2)]
+    assert [p.shape[0] for p in w1p] == [256, 384]
+    full_w1 = orc.gen_bf16(SEED, orc.tensor_id(0, 8, 0), 640 * 256, 256 ** -0.5).reshape(640, 256)
+    assert np.array_equal(np.concatenate(w1p, axis=0), full_w1)
+    full_w2 = orc.gen_bf16(SEED, orc.tensor_id(0, 10, 1), 256 * 640, 640 ** -0.5).reshape(256, 640)
+    w2 = np.concatenate([_shard_weight(lib, model, r, 2, 0, 10, 1) for r in range(2)], axis=1)
+    assert np.array_equal(w2, full_w2)
+    # DBRX at tp=8: 84 blocks -> 10 or 11 blocks per rank, covering h2 exactly
+    sh = C.c_int64 * 6
+    f = lib.mlt_tp_shard
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+    dbrx = capi.ModelSpec(40, 6144, 10752, 48, 8, 16, 4, 2.0, 2.0)
+    off = 0
+    for r in range(8):
+        out = sh()
+        assert f(C.byref(dbrx), r, 8, out) == 0
+        assert out[2] in (1280, 1408) and out[5] == off
+        off += out[2]
+    assert off == 10752

@@ -78,7 +78,7 @@ def main():
     xn = torch.zeros(Rmu * H, dtype=torch.int16, device="cuda")
     qkv = torch.zeros(Rmu, W, device="cuda")
     hbuf = torch.zeros(mu, H, device="cuda")
-    ncap = min(256, Rmu)
+    ncap = min(128, Rmu)  # runtime.cpp ncap_e_
 
     def router():
         KD.router_topk(ptr(x), ptr(gamma), 1e-5, None, ptr(wr), mu, H, E, K, ptr(hn), None,
