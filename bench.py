@@ -49,13 +49,16 @@ CONFIGS = {
                             r_w={1: 0.0, 2: 0.05, 4: 0.15, 8: 0.40}, a_g=0, budget=16e9, prompt=512,
                             gen=32, vocab=32000),
     "dbrx-tp": dict(model=(40, 6144, 10752, 48, 8, 16, 4), N=256, mu=64,
-                    r_w={1: 0.0, 2: 0.05, 4: 0.20, 8: 0.45}, a_g=0, budget=16e9, prompt=512, gen=128,
+                    # reference optimum r_w 0.05/0.20/0.45 less the arena's embedding + lm_head
+                    # (0.79 GB, not in ModelSpec): 0.04/0.18/0.42 fit 16 GB per GPU
+                    r_w={1: 0.0, 2: 0.04, 4: 0.18, 8: 0.42}, a_g=0, budget=16e9, prompt=512, gen=128,
                     vocab=32000),
     "tiny": dict(model=(2, 1024, 3584, 8, 2, 8, 2), N=8, mu=4, r_w=0.0, a_g=0, budget=4e9,
                  prompt=16, gen=32, vocab=32000),
 }
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+NVLINK_BW = 900e9       # B200 NVLink 5, bytes/s per direction (nominal; 1 GPU in this pool)
 HOST_FLOPS = 2.0e12     # host-core fp32 estimate (16 SPR cores AVX-512); CPU attention never binds
 
 
@@ -121,10 +124,34 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def model_spec(cfg):
+# bytes per weight as stored with --codec (12432 B per 8192-weight tile,
+# runtime/weight_codec.hpp); the runtime itself always computes in bf16
+CODEC_DT = 12432 / 8192
+ARENA_EXTRA = 0.75e9   # embedding + lm_head + activations: arena bytes outside ModelSpec
+
+
+def model_spec(cfg, stored=False):
+    """ModelSpec of the config; stored=True gives the bytes the weights occupy as
+    stored/streamed (dt_w = CODEC_DT with --codec), which is what the HRM bound of
+    the reference's cost model must see."""
     from paper_2411_11217_b200 import capi
     l, h1, h2, nq, nkv, ne, k = cfg["model"]
-    return capi.ModelSpec(l, h1, h2, nq, nkv, ne, k, 2.0, 2.0)
+    return capi.ModelSpec(l, h1, h2, nq, nkv, ne, k, CODEC_DT if stored and cfg.get("codec") else 2.0, 2.0)
+
+
+def search_rw(cfg, link_gbs, host_gbs, pk, tp=1):
+    """Best feasible r_w for the config's (N, mu, A_g) on the measured spec with
+    the stored weight bytes (product search_policy, planner.cpp:234-341)."""
+    from paper_2411_11217_b200 import capi
+    api = capi.load_product()
+    hw = capi.HardwareSpec(cfg["budget"] - ARENA_EXTRA, 196e9 * max(tp, 1), pk["hbm_gbs"] * 1e9, host_gbs * 1e9,
+                           link_gbs * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12, HOST_FLOPS)
+    if tp > 1:
+        hw = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=host_gbs * 1e9 * tp)
+    grid = capi.make_grid([cfg["mu"]], [cfg["N"] // cfg["mu"]], [round(0.01 * i, 2) for i in range(101)],
+                          [1.0] if cfg["a_g"] else [0.0], attn=(cfg["a_g"],), ffn=(1,))
+    return api.search_policy(hw, model_spec(cfg, stored=True), capi.WorkloadSpec(cfg["prompt"], cfg["gen"]),
+                             grid).policy.weights_on_gpu
 
 
 def policy(cfg):
@@ -132,20 +159,27 @@ def policy(cfg):
     return capi.Policy(cfg["N"], cfg["mu"], cfg["a_g"], 1, cfg["r_w"], 1.0 if cfg["a_g"] else 0.0)
 
 
-def hrm_bound(cfg, link_gbs, host_gbs, pk, tp=1):
+def hrm_bound(cfg, link_gbs, host_gbs, pk, tp=1, per_slice_host=False):
     """B200 HRM bound: the reference's own estimate_throughput (planner.cpp:129-162)
     re-parameterised with measured B200 numbers; under TP the B200 rule of
     apply_tensor_parallelism_b200 (GPU side x tp, link x tp capped by the host
     DRAM read bandwidth: every B200 has its own PCIe link)."""
     from paper_2411_11217_b200 import capi
     api = capi.load_product()
-    hw = capi.HardwareSpec(cfg["budget"], 196e9, pk["hbm_gbs"] * 1e9, host_gbs * 1e9,
+    # host RAM / DRAM read bandwidth of the job's node: with --tp-shard the
+    # measured box is one GPU's slice (16 cores, 196 GB, its own PCIe link), so a
+    # tp-way job has tp such slices
+    slices = tp if per_slice_host else 1
+    hw = capi.HardwareSpec(cfg["budget"], 196e9 * max(tp, 1), pk["hbm_gbs"] * 1e9, host_gbs * 1e9,
                            link_gbs * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12,
                            HOST_FLOPS)
     if tp > 1:
-        hw = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=host_gbs * 1e9)
+        hw = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=host_gbs * 1e9 * slices)
     w = capi.WorkloadSpec(cfg["prompt"], cfg["gen"])
-    r = api.estimate_throughput(hw, model_spec(cfg), w, policy(cfg))
+    m = model_spec(cfg, stored=True)
+    if tp > 1:  # + the NVLink roof of the 2 all-reduces / layer / micro-batch (nominal NVLink 5)
+        return api.estimate_throughput_b200(hw, m, w, policy(cfg), tp, NVLINK_BW)
+    r = api.estimate_throughput(hw, m, w, policy(cfg))
     return r
 
 
@@ -210,7 +244,12 @@ def expert_roofline(cfg, rep, pk, traffic, tp=1):
     1e-7) + mu*k*2*h1*dt + mu*h1*dt."""
     l, h1, h2, nq, nkv, ne, k = cfg["model"]
     mu = cfg["mu"]
-    bytes_launch = ne * 3 * h1 * (h2 // tp) * 2 + mu * k * 2 * h1 * 2 + mu * h1 * 2
+    wbytes = ne * 3 * h1 * (h2 // tp) * 2
+    tokens = mu * k * 2 * h1 * 2 + mu * h1 * 2
+    # --codec: the kernel must read the encoded tiles (CODEC_DT bytes/weight),
+    # so those are the bytes that bound it; the bf16 figure is reported beside
+    stored = wbytes * CODEC_DT / 2 if cfg.get("codec") else wbytes
+    bytes_launch = stored + tokens
     # in-kernel %globaltimer span of the gate/up and down GEMMs of each launch
     # (CUDA-event deltas on the mostly idle compute stream would add host-launch gaps)
     avg_s = rep.expert_ms_total / max(rep.expert_launches, 1) / 1e3
@@ -219,11 +258,12 @@ def expert_roofline(cfg, rep, pk, traffic, tp=1):
     return {"kernel": "expert_ffn (gemm_tc gate/up+SiLU, gemm_tc down)", "bound": "hbm",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic if tp == 1 else None, "bytes_per_launch": bytes_launch,
+            "bf16_equivalent_gbs": (wbytes + tokens) / avg_s / 1e9,
             "avg_launch_ms": avg_s * 1e3, "launches": rep.expert_launches}
 
 
-def load_traffic():
-    p = os.path.join(ROOT, "profiles", "expert_ffn_traffic.json")
+def load_traffic(codec=False):
+    p = os.path.join(ROOT, "profiles", "expert_ffn_traffic_codec.json" if codec else "expert_ffn_traffic.json")
     if os.path.exists(p):
         with open(p) as f:
             return json.load(f).get("traffic_bytes_per_launch")
@@ -239,9 +279,22 @@ def run_mlt(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # --tp-shard T: rank 0's shard of a T-way tensor-parallel job measured alone on
+    # --tp-shard T: the largest shard of a T-way tensor-parallel job measured alone on
     # this GPU (its own PCIe link, all-reduce elided): the per-GPU step of that job
     tp = args.tp_shard if args.tp_shard > 1 else world
+    if args.tp_shard > 1:  # measure the rank with the largest shard (uneven h2 blocks): the job's slowest
+        import ctypes as C
+        from paper_2411_11217_b200 import capi
+        f = capi.load_product().lib.mlt_tp_shard
+        f.restype, f.argtypes = C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+        sizes = []
+        for r in range(tp):
+            out = (C.c_int64 * 6)()
+            f(C.byref(model_spec(cfg)), r, tp, out)
+            sizes.append(out[2])
+        shard_rank = max(range(tp), key=lambda r: sizes[r])
+    else:
+        shard_rank = rank
     dist = None
     nid = b""
     if world > 1:
@@ -265,11 +318,16 @@ def run_mlt(args, cfg):
     log(f"[bench] rank {rank}: link H2D {link[0]:.2f} GB/s, D2H {link[1]:.2f}, H2D with D2H "
         f"{link[2]:.2f}; host DRAM read {host_gbs:.1f} GB/s")
 
+    raw_rw = cfg["r_w"]
+    if cfg.get("codec"):  # the stored bytes shrink: re-pick r_w for the budget
+        cfg["r_w"] = search_rw(cfg, link_gbs, host_gbs, pk, tp)
+        log(f"[bench] rank {rank}: weight codec on, r_w {cfg['r_w']:.2f} (search on {CODEC_DT:.4f} B/weight)")
     t = time.perf_counter()
     rt = Runtime(model_spec(cfg), policy(cfg), budget_bytes=cfg["budget"],
                  max_ctx=cfg["prompt"] + args.warmup + args.steps + 8, vocab=cfg["vocab"],
-                 device=local, exact_gates=args.gates == "exact", tp_rank=rank, tp_size=tp,
-                 nccl_id=nid, schedule=args.schedule, tp_shard_only=args.tp_shard > 1)
+                 device=local, exact_gates=args.gates == "exact", tp_rank=shard_rank, tp_size=tp,
+                 nccl_id=nid, schedule=args.schedule, tp_shard_only=args.tp_shard > 1,
+                 weight_codec=bool(cfg.get("codec")))
     info = rt.info
     log(f"[bench] rank {rank}: runtime ready in {time.perf_counter() - t:.1f}s (weights gen "
         f"{info.gen_seconds:.1f}s, pin {info.pin_seconds:.1f}s), r_w achieved "
@@ -314,7 +372,10 @@ def run_mlt(args, cfg):
             json.dump(rt.timeline(), fh)
     value = cfg["N"] * args.steps / dev_s        # device-timed (CUDA events), whole job
     e2e = cfg["N"] * args.steps / wall_s         # wall clock around the C-ABI call
-    bound = hrm_bound(cfg, link_gbs, host_gbs, pk, tp=tp)
+    bound = hrm_bound(cfg, link_gbs, host_gbs, pk, tp=tp, per_slice_host=args.tp_shard > 1)
+    # the bf16-weight bound at the raw policy: the best the unencoded stream could do
+    bound_bf16 = hrm_bound(dict(cfg, codec=False, r_w=raw_rw), link_gbs, host_gbs, pk, tp=tp,
+                           per_slice_host=args.tp_shard > 1) if cfg.get("codec") else bound
     prof = rt.kernel_profile()
     l = cfg["model"][0]
     link_s = rep.measured.link_upload * l * args.steps
@@ -333,10 +394,11 @@ def run_mlt(args, cfg):
         "config": {"workload": args.config, "model": names.get(l, "custom"),
                    "global_batch": cfg["N"], "seq_len": cfg["prompt"], "micro_batch": cfg["mu"],
                    "gpu_budget_gb": cfg["budget"] / 1e9, "r_w": cfg["r_w"],
+                   "weight_codec": "on" if cfg.get("codec") else "off",
                    "r_w_achieved": info.achieved_weight_ratio, "A_g": cfg["a_g"],
                    "parallelism": (f"tp{world} (heads + expert h2 sharded, NCCL all-reduce x2/layer)"
                                    if world > 1 else
-                                   f"tp{tp} job, rank-0 shard measured alone on 1 GPU (own PCIe link; "
+                                   f"tp{tp} job, its largest shard (rank {shard_rank}) measured alone on 1 GPU (own PCIe link; "
                                    f"NVLink all-reduce elided, modeled ~0.5 MB/call)" if tp > 1
                                    else "single GPU, weight paging"),
                    "schedule": ("CGOPipe" if cfg["a_g"] == 0 else "S4") if args.schedule == "auto"
@@ -344,13 +406,16 @@ def run_mlt(args, cfg):
                    "weight_gates": args.gates,
                    "l2": "weights streamed per step (>> 126 MB L2): no flush needed"},
         "hrm": {"bound_tok_s": bound.decode_throughput, "frac": value / bound.decode_throughput,
+                "weight_bytes_per_param": CODEC_DT if cfg.get("codec") else 2.0,
+                "bound_bf16_weights_tok_s": bound_bf16.decode_throughput,
+                "value_over_bf16_bound": value / bound_bf16.decode_throughput,
                 "binding": binding, "link_gbs_measured": link_gbs, "host_read_gbs_measured": host_gbs,
                 "modeled_layer_ms": bound.breakdown.layer_total * 1e3,
                 "measured_steady_layer_ms": rep.steady_layer_time * 1e3,
                 "h2d_weight_gbs_achieved": h2d_gbs,
                 "streamed_gb_per_layer_per_gpu": info.streamed_bytes_per_layer / 1e9,
                 "utilization": dict(zip(["gpu", "cpu", "h2d", "d2h", "ctopin"], list(rep.utilization)))},
-        "roofline": expert_roofline(cfg, rep, pk, load_traffic(), tp),
+        "roofline": expert_roofline(cfg, rep, pk, load_traffic(bool(cfg.get("codec"))), tp),
         "peaks_source": pk_src,
         "e2e": {"value": e2e, "unit": "tok/s",
                 "h2d_bytes_per_step": rep.h2d_bytes / args.steps + cfg["N"] * 4 * 2,
@@ -408,10 +473,15 @@ def main():
     ap.add_argument("--prefill", action="store_true",
                     help="run the GPU prefill on synthetic prompt ids instead of synthetic prompt KV")
     ap.add_argument("--timeline", default=None, help="write the measured timeline JSON here")
+    ap.add_argument("--codec", default="auto", choices=["auto", "on", "off"],
+                    help="store/stream/read weights as lossless encoded tiles (runtime/weight_codec.hpp); "
+                         "auto = on when weights are paged over the host link (r_w < 1), off when resident")
     ap.add_argument("--tp-shard", type=int, default=0,
-                    help="measure rank 0's shard of a T-way TP job alone on one GPU (all-reduce elided)")
+                    help="measure the largest shard of a T-way TP job alone on one GPU (all-reduce elided)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
+    rw0 = cfg["r_w"] if not isinstance(cfg["r_w"], dict) else min(cfg["r_w"].values())
+    cfg["codec"] = args.codec == "on" or (args.codec == "auto" and rw0 < 1.0)
     if isinstance(cfg["r_w"], dict):
         world = args.tp_shard if args.tp_shard > 1 else int(os.environ.get("WORLD_SIZE", "1"))
         if world not in cfg["r_w"]:

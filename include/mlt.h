@@ -126,6 +126,14 @@ int mlt_memory_footprint(const mlt_hardware_spec_t* hw, const mlt_model_spec_t* 
  * B200 deviation: link_bw := min(tp * link_bw, host_read_cap). */
 int mlt_apply_tensor_parallelism(const mlt_hardware_spec_t* hw, int tp, int b200_rule,
                                  double host_read_cap, mlt_hardware_spec_t* out);
+/* B200 HRM of a tp-way group: estimate_throughput on the TP-scaled spec
+ * (mlt_apply_tensor_parallelism with the B200 rule) plus the NVLink roof of
+ * the two fp32 all-reduces per layer per micro-batch (ring bytes
+ * 2(tp-1)/tp x mu*h1*4 at nvlink_bw B/s per direction) added to every
+ * layer's GPU FFN term (lightplan::estimate_throughput_b200). */
+int mlt_estimate_throughput_b200(const mlt_hardware_spec_t* tp_hw, const mlt_model_spec_t* model,
+                                 const mlt_workload_spec_t* workload, const mlt_policy_t* policy,
+                                 int tp, double nvlink_bw, mlt_plan_result_t* out);
 /* estimate_throughput, planner.hpp:74-75 */
 int mlt_estimate_throughput(const mlt_hardware_spec_t* hw, const mlt_model_spec_t* model,
                             const mlt_workload_spec_t* workload, const mlt_policy_t* policy,
@@ -248,6 +256,14 @@ int mlt_timeline_json(const mlt_dag* dag, const mlt_timeline_entry_t* entries, i
 /* Host: row-major bf16 [M, K] -> packed weight blocks (M % 128 == 0,
  * K % 64 == 0); dst holds M*K bf16. */
 int mlt_pack_weight(const uint16_t* host_src, int64_t M, int64_t K, uint16_t* host_dst);
+/* Lossless weight-tile codec: encode a packed [M, K] matrix
+ * (M/128 row blocks x K/64 tiles of 16 KiB) into M/128*K/64 tiles of
+ * mlt_codec_tile_bytes() = 12432 B each, same order (row block r starts at
+ * r*(K/64)*12432).  MLT_ERR_INVALID if a tile's high bytes do not fit the
+ * code (> 31 escapes). */
+int mlt_codec_encode(const uint8_t* host_packed, int64_t M, int64_t K, uint8_t* host_out);
+int mlt_codec_decode(const uint8_t* host_enc, int64_t tiles, uint8_t* host_packed);
+int mlt_codec_tile_bytes(void);
 /* Host: packed activation rows (capacity R) -> row-major bf16 [rows, K]. */
 int mlt_unpack_rows(const uint8_t* host_packed, int64_t R, int64_t rows, int64_t K,
                     uint16_t* host_dst);
@@ -278,6 +294,8 @@ typedef struct mlt_gemm_args_t {
                                   (entry, setup done, first weight copy issued, first stage
                                   full, last MMA issued, first accumulator ready, epilogue
                                   done, exit) — a diagnostic, NULL in production */
+    int32_t codec;             /* 1: every A row block is encoded (12432 B per 64-k tile, see
+                                  mlt_codec_encode_tile), expanded in smem by decoder warps */
 } mlt_gemm_args_t;
 
 /* Grouped swap-AB tcgen05 GEMM (SURVEY.md §2c expert_gateup_silu /
@@ -386,6 +404,9 @@ typedef struct mlt_runtime_options_t {
     int32_t tp_shard_only;    /* 1 (with tp_size > 1): run rank tp_rank's shard ALONE on this GPU
                                  with the all-reduce elided — a per-GPU throughput measurement
                                  of a tp_size job on one device (values are partial sums) */
+    int32_t weight_codec;     /* 1: projection + expert weights are stored, paged and read by the
+                                 GEMMs as encoded tiles (lossless, 24 % fewer bytes over PCIe and
+                                 from HBM; mlt_codec_encode); numerics unchanged bit for bit */
 } mlt_runtime_options_t;
 
 /* ncclUniqueId for a tensor-parallel group (call on rank 0, broadcast). */

@@ -352,6 +352,17 @@ class Api:
                                                   C.byref(out)))
         return out
 
+    def estimate_throughput_b200(self, tp_hw, model, workload, policy, tp, nvlink_bw=900e9):
+        """B200 HRM of a tp-way group incl. the NVLink all-reduce roof (product only)."""
+        f = self.lib.mlt_estimate_throughput_b200
+        f.restype = C.c_int
+        f.argtypes = [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(Policy), C.c_int, C.c_double,
+                      P(PlanResult)]
+        out = PlanResult()
+        self.check(f(C.byref(tp_hw), C.byref(model), C.byref(workload), C.byref(policy), tp, nvlink_bw,
+                     C.byref(out)))
+        return out
+
     def search_policy(self, hw, model, workload, grid=None, objective=0, ctx_override=-1.0):
         out = PlanResult()
         self.check(self.fn["search_policy"](C.byref(hw), C.byref(model), C.byref(workload),
@@ -458,12 +469,14 @@ class GemmArgs(C.Structure):
                 ("out_f32", C.c_void_p), ("ldo", C.c_int32), ("residual", C.c_void_p),
                 ("ldr", C.c_int32), ("out_packed", C.c_void_p), ("out_R", C.c_int32),
                 ("n_chunks", C.c_int32), ("k_splits", C.c_int32), ("split_stride", C.c_int64),
-                ("trace", C.c_void_p)]
+                ("trace", C.c_void_p), ("codec", C.c_int32)]
 
 
 V, I, F = C.c_void_p, C.c_int, C.c_float
 _KSIGS = {
     "pack_weight": [V, C.c_int64, C.c_int64, V],
+    "codec_encode": [V, C.c_int64, C.c_int64, V],
+    "codec_decode": [V, C.c_int64, V],
     "unpack_rows": [V, C.c_int64, C.c_int64, C.c_int64, V],
     "pack_rows_host": [V, C.c_int64, C.c_int64, C.c_int64, V],
     "gemm": [C.POINTER(GemmArgs), V],

@@ -13,6 +13,7 @@
 
 #include "../kernels/kernels.hpp"
 #include "../runtime/host_layout.hpp"
+#include "../runtime/weight_codec.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
 #include "lightplan/batcher.hpp"
@@ -67,6 +68,7 @@ mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
     g.k_splits = a->k_splits > 0 ? a->k_splits : 1;
     g.split_stride = a->split_stride;
     g.trace = a->trace;
+    g.codec = a->codec;
     return g;
 }
 
@@ -81,6 +83,30 @@ int mlt_pack_weight(const uint16_t* src, int64_t M, int64_t K, uint16_t* dst) {
         return MLT_OK;
     });
 }
+
+int mlt_codec_encode(const uint8_t* packed, int64_t M, int64_t K, uint8_t* out) {
+    return guard([&] {
+        if (M % 128 || K % 64 || M <= 0 || K <= 0) throw std::invalid_argument("codec_encode: M%128, K%64");
+        const int64_t tiles = M / 128 * (K / 64);
+        int bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+        for (int64_t t = 0; t < tiles; ++t)
+            bad += mlt::codec_encode_tile(packed + t * 16384, out + t * mlt::kCodecTileBytes) ? 0 : 1;
+        if (bad) throw std::invalid_argument("codec_encode: " + std::to_string(bad) + " tile(s) need > " +
+                                             std::to_string(mlt::kCodecMaxEscapes) + " escapes");
+        return MLT_OK;
+    });
+}
+
+int mlt_codec_decode(const uint8_t* enc, int64_t tiles, uint8_t* packed) {
+    return guard([&] {
+        for (int64_t t = 0; t < tiles; ++t)
+            mlt::codec_decode_tile(enc + t * mlt::kCodecTileBytes, packed + t * 16384);
+        return MLT_OK;
+    });
+}
+
+int mlt_codec_tile_bytes(void) { return mlt::kCodecTileBytes; }
 
 int mlt_unpack_rows(const uint8_t* packed, int64_t R, int64_t rows, int64_t K, uint16_t* dst) {
     return guard([&] {

@@ -41,6 +41,22 @@ int mlt_last_status(void) { return mlt::last_status(); }
 
 const char* mlt_version(void) { return "mlt-b200 0.1 (sm_100a)"; }
 
+int mlt_estimate_throughput_b200(const mlt_hardware_spec_t* tp_hw, const mlt_model_spec_t* model,
+                                 const mlt_workload_spec_t* w, const mlt_policy_t* p, int tp,
+                                 double nvlink_bw, mlt_plan_result_t* out) {
+    return guard([&] {
+        const auto r = lightplan::estimate_throughput_b200(glue::hw_in(tp_hw), glue::model_in(model),
+                                                           glue::work_in(w), glue::policy_in(p), tp, nvlink_bw);
+        out->policy = glue::policy_out(r.policy);
+        out->breakdown = glue::lat_out(r.breakdown);
+        out->memory = {r.memory.gpu_bytes, r.memory.cpu_bytes, r.memory.feasible ? 1 : 0};
+        out->decode_throughput = r.decode_throughput;
+        out->generation_throughput = r.generation_throughput;
+        out->objective = r.objective;
+        return MLT_OK;
+    });
+}
+
 int mlt_validate(const mlt_hardware_spec_t* hw, const mlt_model_spec_t* model,
                  const mlt_workload_spec_t* workload, const mlt_policy_t* policy, char* msg,
                  size_t cap) {

@@ -20,6 +20,7 @@
 // how the same kernel reads resident rows and rows paged into either pool
 // slot (runtime/weights.cpp).
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -27,8 +28,21 @@
 namespace mltk {
 namespace {
 
-constexpr int kThreads = 192;  // warp0 producer, warp1 MMA, warps2-5 epilogue
+constexpr int kThreadsRaw = 192;    // warp0 producer, warp1 MMA, warps2-5 epilogue
+constexpr int kDecWarps = 8;
+// Decoder group g owns the ring stages s with s % kDecGroups == g, so it
+// meets each of its stages round after round and never waits on a stage
+// barrier two phases ahead (mbarrier parity would alias).  Codec launches
+// round the stage count to a multiple of kDecGroups.
+constexpr int kDecGroups = 2;
+constexpr int kDecThreads = kDecWarps * 32 / kDecGroups;  // threads per group
+constexpr int kThreadsCodec = 192 + kDecWarps * 32;  // + warps 6-13: weight-tile decoders
+constexpr int kCodecTile = 12432;   // encoded tile bytes (runtime/weight_codec.hpp)
+// codec: an encoded tile lands at the END of its 16 KiB A slot and is
+// expanded in place (every input is in registers before any output store)
+constexpr int kCodecOff = kATileBytes - kCodecTile;  // 3952, 16-byte aligned
 constexpr int kMaxMats = 2;
+constexpr int kEpiChunks = 1;           // 16-token TMEM chunks per load wait in the epilogue
 constexpr int kCtlBytes = 256;           // barriers + TMEM base
 constexpr int kEpiScratch = 4 * 2048;    // per epilogue warp: 16 x 32 fp32 transpose tile
 
@@ -37,6 +51,7 @@ struct Smem {
     uint64_t empty[8];
     uint64_t tfull[2];
     uint64_t tempty[2];
+    uint64_t dfull[8];  // codec: decoders -> MMA, stage's A tiles decoded in place
     uint32_t tmem_base;
 };
 
@@ -44,13 +59,107 @@ static_assert(sizeof(Smem) <= kCtlBytes, "control block fits its reserved bytes"
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
-__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) {
+// named barrier of one decoder group (ids 1.. ; 0 is __syncthreads)
+__device__ __forceinline__ void decoders_sync(int grp) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kDecThreads) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Decode one encoded weight tile (weight_codec.hpp) into its 16 KiB bf16
+// smem image; decoder thread dt handles the 8-weight units dt, dt +
+// kDecThreads, ...  All of a thread's loads are issued first (ILP), then per
+// 4 weights: two PRMT table lookups (codes 0-7 / 8-15 of the 16-byte
+// table), a sign-replicating PRMT turning each code's bit 3 into a byte
+// mask, one LOP3 select, and two PRMTs interleaving the raw low bytes with
+// the looked-up high bytes: ~2.7 instructions per weight.
+// PTX prmt.b32 (default mode): selector nibble bit 3 = replicate the sign of
+// the selected byte (__byte_perm only documents the 3 low bits)
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+// high bytes of 4 weights: sel = their 3-bit table selectors (nibbles), m =
+// 0xFF per byte where the code's bit 3 is set (from sign-replicating PRMT)
+__device__ __forceinline__ uint32_t hi4(uint32_t sel, uint32_t m, const uint4& T) {
+    const uint32_t a = prmt(T.x, T.y, sel);  // table[code & 7]
+    const uint32_t b = prmt(T.z, T.w, sel);  // table[8 + (code & 7)]
+    return (a & ~m) | (b & m);
+}
+// shared-window accesses by 32-bit smem address (generic pointers into
+// dynamic smem compile to generic LD/ST, which cost extra latency and
+// address math in the decoder's inner loop)
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// One decoder thread's share of an encoded tile: its units u = dt + j *
+// kDecThreads (8 weights each), the table, and at most one escape entry.
+struct TileIn {
+    uint4 T;
+    uint2 lo[1024 / kDecThreads];
+    uint32_t cd[1024 / kDecThreads];
+    uint32_t n, esc;
+};
+__device__ __forceinline__ void load_tile(uint32_t c, int dt, TileIn& in) {
+    in.T = lds128(c + 12288);
+    in.n = lds32(c + 12304) & 0xffffu;
+    in.esc = static_cast<uint32_t>(dt) < in.n ? lds32(c + 12308 + 4 * dt) : 0u;  // {u16 index, u8 hi, 0}
+#pragma unroll
+    for (int j = 0; j < 1024 / kDecThreads; ++j) {
+        const uint32_t u = dt + j * kDecThreads;
+        in.lo[j] = lds64(c + u * 8);
+        in.cd[j] = lds32(c + 8192 + u * 4);
+    }
+}
+__device__ __forceinline__ void store_tile(const TileIn& in, uint32_t d, int dt) {
+#pragma unroll
+    for (int j = 0; j < 1024 / kDecThreads; ++j) {
+        // code bit 3 of weight k sits at bit 4k+3: byte msbs of cd (odd k) and
+        // of cd << 4 (even k) -> one sign-replicating PRMT per 4 weights
+        const uint32_t cd = in.cd[j], c4 = cd << 4;
+        const uint32_t h0 = hi4(cd & 0x7777u, prmt(c4, cd, 0xD9C8u), in.T);
+        const uint32_t h1 = hi4((cd >> 16) & 0x7777u, prmt(c4, cd, 0xFBEAu), in.T);
+        uint4 o;
+        o.x = prmt(in.lo[j].x, h0, 0x5140u);
+        o.y = prmt(in.lo[j].x, h0, 0x7362u);
+        o.z = prmt(in.lo[j].y, h1, 0x5140u);
+        o.w = prmt(in.lo[j].y, h1, 0x7362u);
+        sts128(d + (dt + j * kDecThreads) * 16, o);
+    }
+}
+
+__global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1 KiB alignment for the SWIZZLE_128B atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     const int a_bytes = a.n_mats * kATileBytes;
     const int b_bytes = a.n_cap * 128;
+    // stage = [A tiles (16 KiB slots) | B tile]; with the codec the encoded
+    // A tiles land at the end of their slots and are decoded in place
     const int stage_bytes = a_bytes + b_bytes;
     const int stages = a.stages;
     Smem* ctl = reinterpret_cast<Smem*>(smem + stages * stage_bytes);
@@ -72,6 +181,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
             mbar_init(&ctl->tfull[s], 1);
             mbar_init(&ctl->tempty[s], 4);
         }
+        if (a.codec)
+            for (int s = 0; s < stages; ++s) mbar_init(&ctl->dfull[s], 1);
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc(&ctl->tmem_base, a.tmem_cols);
@@ -106,14 +217,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
                     const int ntp = (nt + 15) & ~15;
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&ctl->empty[stage], phase ^ 1);
-                        uint8_t* sa = smem + stage * stage_bytes;
-                        uint8_t* sb = sa + a_bytes;
+                        uint8_t* const st = smem + stage * stage_bytes;
+                        uint8_t* sa = a.codec ? st + kCodecOff : st;
+                        uint8_t* sb = st + a_bytes;
+                        const int tile = a.codec ? kCodecTile : kATileBytes;
                         if (tr && v == static_cast<int>(blockIdx.x) && kb == kb0 && n0 == c * a.n_cap)
                             tr[2] = globaltimer();
-                        mbar_expect_tx(&ctl->full[stage], a.n_mats * kATileBytes + ntp * 128);
+                        mbar_expect_tx(&ctl->full[stage], a.n_mats * tile + ntp * 128);
                         for (int mt = 0; mt < a.n_mats; ++mt)
-                            bulk_g2s(sa + mt * kATileBytes, ab[mt] + static_cast<int64_t>(kb) * kATileBytes,
-                                     kATileBytes, &ctl->full[stage], pol_w);
+                            bulk_g2s(sa + mt * kATileBytes, ab[mt] + static_cast<int64_t>(kb) * tile, tile,
+                                     &ctl->full[stage], pol_w);
                         const uint8_t* src = a.b + static_cast<int64_t>(kb) * a.R * 128 +
                                              static_cast<int64_t>(row0 + n0) * 128;
                         bulk_g2s(sb, src, ntp * 128, &ctl->full[stage], pol_x);
@@ -143,12 +256,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
                 const uint32_t d0 = tmem + acc * acc_cols;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&ctl->full[stage], phase);
+                    if (a.codec) mbar_wait(&ctl->dfull[stage], phase);
                     tc_fence_after();
                     if (tr && lane == 0 && v == static_cast<int>(blockIdx.x) && kb == kb0 && n0 == c * a.n_cap)
                         tr[3] = globaltimer();
                     if (elect_one()) {
-                        const uint32_t sa = smem_u32(smem + stage * stage_bytes);
-                        const uint32_t sb = sa + a_bytes;
+                        const uint32_t st = smem_u32(smem + stage * stage_bytes);
+                        const uint32_t sa = st;
+                        const uint32_t sb = st + a_bytes;
 #pragma unroll
                         for (int k = 0; k < kBlockK / 16; ++k) {
                             const uint64_t bd = sdesc_sw128(sb + k * 32);
@@ -165,10 +280,53 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
                 if (++acc == acc_stages) { acc = 0; acc_phase ^= 1; }
             }
         }
+    } else if (warp >= 6) {
+        // ===== decoders (codec): encoded tiles -> bf16 smem images, in place =====
+        // kDecGroups groups of kDecThreads own alternate ring stages.  Per k-block:
+        // every input (and escape entry) of the group's tiles -> registers,
+        // group barrier, expanded 16-byte stores over the same slots, escape
+        // bytes, proxy fence (generic smem writes -> tcgen05.mma), barrier,
+        // one arrive on the stage's dfull.
+        const int grp = (static_cast<int>(threadIdx.x) - 192) / kDecThreads;
+        const int dt = (static_cast<int>(threadIdx.x) - 192) % kDecThreads;
+        const bool two = a.n_mats == 2;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
+            const int ks = v % a.k_splits, u = v / a.k_splits;
+            const int c = u % a.n_chunks, g = (u / a.n_chunks) % a.G;
+            const int kb0 = ks * KB / a.k_splits, kb1 = (ks + 1) * KB / a.k_splits;
+            const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
+            if (rows <= 0) continue;
+            for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    if (stage % kDecGroups == grp) {
+                        mbar_wait(&ctl->full[stage], phase);
+                        const uint32_t sa = smem_u32(smem + stage * stage_bytes);
+                        TileIn in0, in1;
+                        load_tile(sa + kCodecOff, dt, in0);
+                        if (two) load_tile(sa + kATileBytes + kCodecOff, dt, in1);
+                        decoders_sync(grp);  // all inputs read: the slots may be overwritten
+                        store_tile(in0, sa, dt);
+                        if (two) store_tile(in1, sa + kATileBytes, dt);
+                        if (in0.n + (two ? in1.n : 0u)) {  // rare: high bytes outside the table
+                            decoders_sync(grp);
+                            if (static_cast<uint32_t>(dt) < in0.n) sts8(sa + 2 * (in0.esc & 0xffffu) + 1, in0.esc >> 16);
+                            if (two && static_cast<uint32_t>(dt) < in1.n)
+                                sts8(sa + kATileBytes + 2 * (in1.esc & 0xffffu) + 1, in1.esc >> 16);
+                        }
+                        fence_proxy_async_smem();  // generic smem writes -> visible to tcgen05.mma
+                        decoders_sync(grp);
+                        if (dt == 0) mbar_arrive(&ctl->dfull[stage]);
+                    }
+                    if (++stage == stages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
     } else {
         // ===== epilogue: TMEM -> registers -> global =====
         const uint32_t quarter = warp & 3;  // TMEM lanes this warp may access
-        float* const scr = reinterpret_cast<float*>(smem + stages * stage_bytes + kCtlBytes) + quarter * 512;
+        float* const scr = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ctl) + kCtlBytes) + quarter * 512;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
@@ -192,10 +350,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
                 // a per-warp smem transpose -> 16-byte global stores along the
                 // feature axis (row-contiguous in the output), instead of 16
                 // scalar stores per thread (6x slower, tools/trace_gemm.py).
-                for (int c2 = 0; c2 < nt; c2 += 32) {
+                for (int c2 = 0; c2 < nt; c2 += 16 * kEpiChunks) {
                     // issue the TMEM loads of two 16-token chunks (both matrices
                     // for SiLU), then a single wait: one TMEM round trip per 32 tokens
-                    const bool two = c2 + 16 < nt;
+                    const bool two = kEpiChunks == 2 && c2 + 16 < nt;
                     uint32_t r0[2][16], r1[2][16];
                     tmem_ld16_async(t0 + c2, r0[0]);
                     if (two) tmem_ld16_async(t0 + c2 + 16, r0[1]);
@@ -211,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
                         if (two) tmem_regs_ready(r1[1]);
                     }
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    for (int h = 0; h < kEpiChunks; ++h) {
                         const int c = c2 + 16 * h;
                         if (c >= nt) break;
                         if (a.epi == kEpiF32) {
@@ -280,7 +438,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
 }  // namespace
 
 int gemm_smem_bytes(int n_mats, int n_cap, int stages) {
-    return stages * (n_mats * kATileBytes + n_cap * 128) + 1024 /*align*/ + kCtlBytes + kEpiScratch;
+    return stages * (n_mats * kATileBytes + n_cap * 128) +
+           1024 /*align*/ + kCtlBytes + kEpiScratch;
 }
 
 cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
@@ -293,6 +452,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     const int budget = 227 * 1024 - 1024 - kCtlBytes - kEpiScratch;
     a.stages = budget / per_stage;
     if (a.stages > 8) a.stages = 8;
+    if (a.codec) a.stages -= a.stages % kDecGroups;  // decoder groups own whole stages
     if (a.stages < 2) return cudaErrorInvalidValue;
     const int acc_cols = a.n_mats * a.n_cap;
     a.acc_stages = (2 * acc_cols <= 512) ? 2 : 1;
@@ -311,7 +471,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     const int n_virtual = a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
-    gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(a);
+    gemm_tc_kernel<<<grid, a.codec ? kThreadsCodec : kThreadsRaw, smem, stream>>>(a);
     return cudaGetLastError();
 }
 

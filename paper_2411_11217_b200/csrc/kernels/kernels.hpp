@@ -32,6 +32,9 @@ struct GemmArgs {
     unsigned long long* timing = nullptr;
     // optional per-CTA phase stamps [gridDim][8] (diagnostic, see mlt.h)
     unsigned long long* trace = nullptr;
+    // 1: A row blocks are encoded tiles (runtime/weight_codec.hpp, 12432 B
+    // per 64-k tile); decoder warps expand them in shared memory
+    int codec = 0;
     // epilogue
     int epi = kEpiF32;
     float alpha = 1.0f;

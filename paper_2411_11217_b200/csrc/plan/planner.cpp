@@ -5,6 +5,7 @@
 #include "lightplan/planner.hpp"
 
 #include <algorithm>
+#include <stdexcept>
 #include <string>
 
 namespace lightplan {
@@ -133,6 +134,42 @@ PlanResult estimate_throughput(const HardwareSpec& hw, const ModelSpec& m, const
     r.generation_throughput = generated / (prefill + decode);
     const double ctx_mid = d(w.prompt_len) + d(w.gen_len) / 2.0;
     r.breakdown = layer_latency(hw, m, w, p, ctx_mid);
+    r.objective = r.breakdown.layer_total / d(p.batch);
+    return r;
+}
+
+double nvlink_allreduce_seconds(const ModelSpec& m, const Policy& p, int tp, double nvlink_bw) {
+    if (tp <= 1) return 0.0;
+    if (nvlink_bw <= 0) throw std::invalid_argument("nvlink_bw must be > 0");
+    const double size = d(p.micro_batch) * d(m.hidden_dim) * 4.0;  // fp32 [mu, h1]
+    const double ring = 2.0 * (tp - 1.0) / tp;
+    return d(p.micro_batch_count()) * 2.0 * ring * size / nvlink_bw;
+}
+
+PlanResult estimate_throughput_b200(const HardwareSpec& hw, const ModelSpec& m, const WorkloadSpec& w,
+                                    const Policy& p, int tp, double nvlink_bw) {
+    if (tp <= 1) return estimate_throughput(hw, m, w, p);
+    const double t_nvl = nvlink_allreduce_seconds(m, p, tp, nvlink_bw);
+    PlanResult r;
+    r.policy = p;
+    r.memory = memory_footprint(hw, m, w, p);
+    if (!r.memory.feasible) throw InfeasiblePolicyError("policy exceeds device memory");
+    auto layer = [&](double ctx) {
+        LatencyBreakdown b = layer_latency(hw, m, w, p, ctx);
+        b.gpu_ffn += t_nvl;
+        b.layer_total = std::max({b.link_upload, b.cpu_total(), b.gpu_total()});
+        return b;
+    };
+    const double L = d(m.layers);
+    double decode = 0.0;
+    for (std::int64_t step = 1; step <= w.gen_len; ++step) decode += L * layer(d(w.prompt_len + step)).layer_total;
+    const double stream = transfer_sizes(m, p, 1.0).weight_stream / hw.link_bw;
+    const double compute = prefill_flops_per_layer(m, p, w) / hw.gpu_flops;
+    const double prefill = L * std::max(stream, compute);
+    const double generated = d(p.batch) * d(w.gen_len);
+    r.decode_throughput = generated / decode;
+    r.generation_throughput = generated / (prefill + decode);
+    r.breakdown = layer(d(w.prompt_len) + d(w.gen_len) / 2.0);
     r.objective = r.breakdown.layer_total / d(p.batch);
     return r;
 }

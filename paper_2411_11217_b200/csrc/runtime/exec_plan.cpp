@@ -6,6 +6,7 @@
 #include <stdexcept>
 
 #include "host_layout.hpp"
+#include "weight_codec.hpp"
 #include "lightplan/opcost.hpp"
 
 namespace mlt {
@@ -80,14 +81,16 @@ ShardMap shard_map(const lightplan::ModelSpec& m, const Shard& s, int kind) {
     return out;
 }
 
-Catalog build_catalog(const lightplan::ModelSpec& m, const lightplan::Policy& p, const Shard& shard_in) {
+Catalog build_catalog(const lightplan::ModelSpec& m, const lightplan::Policy& p, const Shard& shard_in,
+                      bool codec) {
     Catalog c;
     const Shard sh = shard_in.q_heads ? shard_in : make_shard(m, 0, 1);
     const int H = static_cast<int>(m.hidden_dim), F = static_cast<int>(sh.ffn);
     const int E = static_cast<int>(m.experts);
     const int W = static_cast<int>(sh.qkv_rows);
     auto add = [&](int kind, int expert, int rows, int64_t K) {
-        for (int rb = 0; rb < rows / 128; ++rb) c.blocks.push_back({kind, expert, rb, K, 128 * K * 2, false, 0});
+        const int64_t bytes = codec ? K / 64 * kCodecTileBytes : 128 * K * 2;
+        for (int rb = 0; rb < rows / 128; ++rb) c.blocks.push_back({kind, expert, rb, K, bytes, false, 0});
     };
     add(kWqkv, 0, W, H);
     add(kWo, 0, H, sh.o_k);
@@ -96,8 +99,11 @@ Catalog build_catalog(const lightplan::ModelSpec& m, const lightplan::Policy& p,
         add(kW3, e, F, H);
         add(kW2, e, H, F);
     }
-    const double layer_total = lightplan::layer_weight_bytes(m).total() / sh.size;  // per GPU
+    // per-GPU layer bytes as stored (= layer_weight_bytes(m).total() / tp for
+    // bf16 blocks, opcost.cpp:49-61); the router stays bf16 and resident
     const double router = static_cast<double>(E) * H * 2;
+    double layer_total = router;
+    for (const auto& b : c.blocks) layer_total += static_cast<double>(b.bytes);
     const double budget = p.weights_on_gpu * layer_total - router;
     bool open = true;
     for (auto& b : c.blocks) {

@@ -58,8 +58,11 @@ ShardMap shard_map(const lightplan::ModelSpec& model, const Shard& shard, int ki
 // Resident first: QKV, O, then expert row blocks in (expert, W1, W3, W2)
 // order while resident + router <= r_w * (W_layer / tp) (SURVEY.md
 // Appendix B; the reference's uniform share, per GPU under TP).
+// codec: blocks are stored encoded (weight_codec.hpp: 12432 B per 64-k tile
+// instead of 16384), so the same r_w share holds more weights and the pages
+// stream fewer bytes.
 Catalog build_catalog(const lightplan::ModelSpec& model, const lightplan::Policy& policy,
-                      const Shard& shard = Shard{});
+                      const Shard& shard = Shard{}, bool codec = false);
 
 // Byte range [begin, end) of page p (1..M) of a layer blob; p = 0: whole.
 std::pair<int64_t, int64_t> page_range(int64_t blob_bytes, int M, int page);

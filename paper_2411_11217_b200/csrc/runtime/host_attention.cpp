@@ -47,9 +47,11 @@ void Runtime::host_attention(int l, int mb, int step) {
     // Default: all cores but two, which stay free for the resource launcher
     // threads (a descheduled GPU launcher leaves the device idle between
     // kernels of one PostAttn).
-    // Under TP every rank's process shares the host cores.
+    // Under TP every rank's process shares the node's host cores; a
+    // shard-only measurement runs one rank alone on its slice of the node.
+    const int sharing = opt_.tp_shard_only ? 1 : shard_.size;
     const int threads = opt_.host_threads > 0 ? opt_.host_threads
-                                              : std::max(1, (omp_get_num_procs() - 2) / shard_.size);
+                                              : std::max(1, (omp_get_num_procs() - 2) / sharing);
 
 #pragma omp parallel num_threads(threads)
     {

@@ -16,6 +16,7 @@
 #include "../kernels/common.cuh"
 #include "../kernels/kernels.hpp"
 #include "host_layout.hpp"
+#include "weight_codec.hpp"
 #include "runtime_util.hpp"
 
 namespace mlt {
@@ -160,7 +161,7 @@ cudaStream_t Runtime::stream(lightplan::sim::Resource r) const {
 
 // Residency split and blob layout: exec_plan.cpp build_catalog.
 void Runtime::build_catalog() {
-    cat_ = mlt::build_catalog(model_, policy_, shard_);
+    cat_ = mlt::build_catalog(model_, policy_, shard_, opt_.weight_codec);
     layer_res_bytes_ = cat_.resident_bytes;
     layer_blob_bytes_ = cat_.blob_bytes;
     achieved_rw_ = cat_.achieved_rw;
@@ -271,6 +272,7 @@ void Runtime::generate_weights() {
         if (!opt_.pin_weights) staging_ = host_alloc(2 * static_cast<size_t>(layer_blob_bytes_), true, &pin_seconds_);
     }
     std::vector<uint8_t> res(static_cast<size_t>(layer_res_bytes_));
+    std::vector<uint16_t> tmp_block;
     std::vector<const uint8_t*> tab(static_cast<size_t>(L_) * 2 * table_entries_);
     for (int l = 0; l < L_; ++l) {
         int idx_qkv = 0, idx_o = 0;
@@ -278,8 +280,24 @@ void Runtime::generate_weights() {
             uint8_t* dst = b.resident ? res.data() + b.offset
                                       : host_blob_ + static_cast<int64_t>(l) * layer_blob_bytes_ + b.offset;
             const ShardMap& sm = map_of(b.kind);
-            synth_shard_packed(seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0,
-                               b.K, b.rb * 128, (b.rb + 1) * 128, sm.scale, reinterpret_cast<uint16_t*>(dst));
+            if (!opt_.weight_codec) {
+                synth_shard_packed(seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0,
+                                   b.K, b.rb * 128, (b.rb + 1) * 128, sm.scale, reinterpret_cast<uint16_t*>(dst));
+            } else {  // packed bf16 tiles -> encoded tiles (lossless, weight_codec.hpp)
+                tmp_block.resize(static_cast<size_t>(128) * b.K);
+                synth_shard_packed(seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0,
+                                   b.K, b.rb * 128, (b.rb + 1) * 128, sm.scale, tmp_block.data());
+                const int tiles = static_cast<int>(b.K / 64);
+                int bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+                for (int t = 0; t < tiles; ++t)
+                    bad += codec_encode_tile(reinterpret_cast<const uint8_t*>(tmp_block.data()) +
+                                                 static_cast<size_t>(t) * mltk::kATileBytes,
+                                             dst + static_cast<size_t>(t) * kCodecTileBytes)
+                               ? 0
+                               : 1;
+                if (bad) throw std::invalid_argument("weight_codec: a weight tile does not fit the code");
+            }
             int entry;
             switch (b.kind) {
                 case kWqkv: entry = tab_qkv_ + idx_qkv++; break;
@@ -494,6 +512,7 @@ void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
     a.out_f32 = d_qkv_f32_;
     a.ldo = W_;
     a.timing = ktimer("qkv_gemm");
+    a.codec = opt_.weight_codec ? 1 : 0;
     kl("qkv_gemm", mltk::launch_gemm(a, num_sms_, s_gpu_));
     const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
     uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
@@ -563,6 +582,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     o.residual = coll_ ? nullptr : x;  // unsplit single GPU: residual in the GEMM epilogue
     o.ldr = H_;
     o.timing = ktimer("o_gemm");
+    o.codec = opt_.weight_codec ? 1 : 0;
     kl("o_gemm", mltk::launch_gemm(o, num_sms_, s_gpu_));
     if (coll_) {
         // TP all-reduce #1: h = x + sum over ranks of this rank's O partial
@@ -597,6 +617,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     gu.out_packed = d_inter_;
     gu.out_R = Re_;
     gu.timing = ktimer("expert_gateup_gemm");
+    gu.codec = opt_.weight_codec ? 1 : 0;
     kl("expert_gateup_gemm", mltk::launch_gemm(gu, num_sms_, s_gpu_));
     mltk::GemmArgs dn;
     dn.a_table = tab + tab_w2_;
@@ -611,6 +632,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     dn.out_f32 = d_y_;
     dn.ldo = H_;
     dn.timing = ktimer("expert_down_gemm");
+    dn.codec = opt_.weight_codec ? 1 : 0;
     kl("expert_down_gemm", mltk::launch_gemm(dn, num_sms_, s_gpu_));
     if (coll_) {
         // TP all-reduce #2: x = h + sum over ranks of this rank's top-k combine (h2 shard)

@@ -44,6 +44,7 @@ struct RuntimeOptions {
     int tp_rank = 0, tp_size = 1;  // tensor parallelism (one process per GPU)
     uint8_t nccl_id[128] = {};     // ncclUniqueId from rank 0 (tp_size > 1)
     bool tp_shard_only = false;    // one shard alone on this GPU, all-reduce elided (measurement)
+    bool weight_codec = false;     // store/stream/read projection + expert weights encoded (weight_codec.hpp)
     int schedule = -1;             // -1: CGOPipe (S4 when A_g = 1); else a ScheduleKind to execute
     int prefill_chunk_tokens = 0;  // 0: largest prefill chunk the budget allows
 };

@@ -1,0 +1,62 @@
+// Host encoder / reference decoder of the weight-tile codec (weight_codec.hpp).
+#include "weight_codec.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace mlt {
+
+bool codec_encode_tile(const uint8_t* tile, uint8_t* out) {
+    uint32_t hist[256] = {};
+    for (int i = 0; i < 8192; ++i) ++hist[tile[2 * i + 1]];
+    // the 15 most frequent high bytes (ties -> smaller value: deterministic)
+    uint8_t order[256];
+    for (int v = 0; v < 256; ++v) order[v] = static_cast<uint8_t>(v);
+    std::stable_sort(order, order + 256, [&](uint8_t a, uint8_t b) { return hist[a] > hist[b]; });
+    uint8_t code_of[256];
+    std::memset(code_of, 15, sizeof(code_of));
+    uint8_t* table = out + 12288;
+    std::memset(table, 0, 16);
+    for (int c = 0; c < 15; ++c) {
+        if (!hist[order[c]]) break;
+        table[c] = order[c];
+        code_of[order[c]] = static_cast<uint8_t>(c);
+    }
+    uint8_t* codes = out + 8192;
+    std::memset(codes, 0, 4096);
+    int n = 0;
+    uint8_t* esc = out + 12308;
+    std::memset(out + 12304, 0, kCodecTileBytes - 12304);
+    for (int i = 0; i < 8192; ++i) {
+        out[i] = tile[2 * i];
+        const uint8_t hi = tile[2 * i + 1];
+        const uint8_t c = code_of[hi];
+        codes[i >> 1] |= static_cast<uint8_t>(c << ((i & 1) * 4));
+        if (c == 15) {
+            if (n == kCodecMaxEscapes) return false;
+            esc[4 * n] = static_cast<uint8_t>(i & 0xff);
+            esc[4 * n + 1] = static_cast<uint8_t>(i >> 8);
+            esc[4 * n + 2] = hi;
+            ++n;
+        }
+    }
+    out[12304] = static_cast<uint8_t>(n & 0xff);
+    out[12305] = static_cast<uint8_t>(n >> 8);
+    return true;
+}
+
+void codec_decode_tile(const uint8_t* enc, uint8_t* tile) {
+    const uint8_t* table = enc + 12288;
+    for (int i = 0; i < 8192; ++i) {
+        const int c = (enc[8192 + (i >> 1)] >> ((i & 1) * 4)) & 15;
+        tile[2 * i] = enc[i];
+        tile[2 * i + 1] = table[c];
+    }
+    const int n = enc[12304] | (enc[12305] << 8);
+    for (int e = 0; e < n; ++e) {
+        const int i = enc[12308 + 4 * e] | (enc[12309 + 4 * e] << 8);
+        tile[2 * i + 1] = enc[12310 + 4 * e];
+    }
+}
+
+}  // namespace mlt

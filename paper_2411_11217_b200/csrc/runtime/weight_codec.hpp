@@ -1,0 +1,37 @@
+// Lossless weight-tile codec ("hi-byte table" code).
+//
+// The unit is one 16 KiB packed weight tile (128 rows x 64 k, the exact
+// SWIZZLE_128B smem image the GEMM consumes, common.cuh): 8192 bf16 values
+// w_i at byte 2i.  A bf16 is [sign:1][exponent:8][mantissa:7]; its LOW byte
+// (exponent lsb + mantissa) is close to uniformly distributed, its HIGH byte
+// (sign + exponent msbs) takes a handful of values for trained or synthetic
+// weights (entropy ~2-3 bits).  The encoded tile keeps the low bytes raw and
+// replaces each high byte by a 4-bit index into a per-tile table of its 15
+// most frequent values; the rare rest are escapes (code 15) listed with
+// their position:
+//
+//   [0, 8192)        low byte of w_i
+//   [8192, 12288)    code of w_i in the low (even i) / high (odd i) nibble
+//   [12288, 12304)   table[16] of high bytes (entry 15 unused)
+//   [12304, 12306)   escape count n (u16), [12306, 12308) reserved
+//   [12308, 12432)   escapes: n <= 31 entries {u16 index, u8 high byte, u8 0}
+//
+// 12432 B instead of 16384 B (-24.1 %), a multiple of 16 so encoded tiles
+// pack back to back and stay cp.async.bulk-aligned.  Decoding is exact: the
+// tensor cores consume bit-identical bf16 tiles either way.
+#pragma once
+
+#include <cstdint>
+
+namespace mlt {
+
+constexpr int kCodecTileBytes = 12432;
+constexpr int kCodecMaxEscapes = 31;
+
+// Encode one 16 KiB tile; false if it needs more than kCodecMaxEscapes
+// escapes (its high bytes spread over > 15 values too evenly).
+bool codec_encode_tile(const uint8_t* tile16k, uint8_t* out);
+// Host reference decoder (tests; the GEMM decodes in shared memory).
+void codec_decode_tile(const uint8_t* enc, uint8_t* tile16k);
+
+}  // namespace mlt

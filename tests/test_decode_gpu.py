@@ -220,3 +220,26 @@ def test_executed_baseline_schedules_match_cgopipe(prompt):
     with pytest.raises(capi.UnsupportedCombinationError):
         Runtime(_model(TINY), capi.Policy(N, MU, 0, 1, 0.25, 0.0), budget_bytes=4e9, max_ctx=64,
                 vocab=VOCAB, seed=1234, schedule="s4")
+
+
+@pytest.mark.parametrize("dims,r_w,a_g,budget", [(TINY, 0.3, 0, 4e9), (TINY, 1.0, 1, 4e9), (W8X7B, 0.10, 0, 7e9)])
+def test_weight_codec_decode_bitwise_equal(prompt, dims, r_w, a_g, budget):
+    """Decoding with encoded weights (stored, paged and read as 12432-byte
+    tiles, expanded in smem by the GEMM's decoder warps) returns the same ids
+    and the same residual bits as decoding with raw bf16 tiles, while the
+    pages carry 24 % fewer bytes."""
+    out = []
+    for codec in (False, True):
+        rt = Runtime(_model(dims), capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0), budget_bytes=budget,
+                     max_ctx=64, vocab=VOCAB, seed=1234, weight_codec=codec)
+        first = rt.decode(prompt[0], PROMPT, forced=prompt)
+        rest = rt.decode(first.ids[-1], 8)
+        out.append((first.ids.copy(), rest.ids.copy(), rt.residual().copy(), rt.info.streamed_bytes_per_layer,
+                    rest.report.h2d_weight_bytes))
+        assert rest.report.timeline_ok == 1
+        rt.close()
+    (f0, r0, x0, s0, b0), (f1, r1, x1, s1, b1) = out
+    assert np.array_equal(f0, f1) and np.array_equal(r0, r1)
+    assert np.array_equal(x0.view(np.uint32), x1.view(np.uint32))
+    if r_w < 1.0:
+        assert s1 < 0.8 * s0 and b1 < 0.8 * b0

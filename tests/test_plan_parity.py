@@ -133,3 +133,26 @@ def test_b200_headline_bound_matches_reference(api, ref):
         a, b = api.estimate_throughput(hw, m, w, pol), ref.estimate_throughput(hw, m, w, pol)
         assert bytes(a) == bytes(b)
         assert 150 < a.decode_throughput < 190
+
+
+def test_b200_hrm_nvlink_roof(api):
+    """estimate_throughput_b200: tp=1 is estimate_throughput bit for bit; at tp>1
+    every layer's GPU FFN term grows by exactly the NVLink all-reduce time
+    (2 fp32 [mu, h1] all-reduces per micro-batch, ring 2(tp-1)/tp)."""
+    m = mixtral_8x22b_model()
+    w = capi.WorkloadSpec(512, 32)
+    p = capi.Policy(256, 64, 0, 1, 0.15, 0.0)
+    hw = capi.HardwareSpec(16e9, 1e13, 6.5e12, 1.1e11, 5.56e10, 1.39e15, 2e12)
+    big = capi.HardwareSpec(80e9, 1e13, 6.5e12, 1.1e11, 5.56e10, 1.39e15, 2e12)
+    a = api.estimate_throughput(big, m, w, p)
+    b = api.estimate_throughput_b200(big, m, w, p, 1, 900e9)
+    assert a.decode_throughput == b.decode_throughput and a.breakdown.gpu_ffn == b.breakdown.gpu_ffn
+    tp = 4
+    hw4 = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=0.0)
+    base = api.estimate_throughput(hw4, m, w, p)
+    ext = api.estimate_throughput_b200(hw4, m, w, p, tp, 900e9)
+    t_nvl = 4 * 2 * (2 * 3 / 4) * 64 * 6144 * 4 / 900e9
+    assert abs((ext.breakdown.gpu_ffn - base.breakdown.gpu_ffn) - t_nvl) < 1e-15
+    assert ext.decode_throughput <= base.decode_throughput
+    # link-bound here: the NVLink roof does not move the bound
+    assert ext.breakdown.layer_total == base.breakdown.layer_total

@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--once", action="store_true")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--with-h2d", action="store_true", help="run a concurrent H2D copy stream")
+    ap.add_argument("--codec", action="store_true", help="encoded weight tiles (decoder warps in the GEMM)")
     a = ap.parse_args()
     mu = a.mu
     KD = capi.load_kernels()
@@ -43,13 +44,28 @@ def main():
     torch.manual_seed(0)
 
     def blocks(rows, k, n_mats=1):
-        """n_mats x E packed weight matrices [rows, k] (random bytes are fine:
-        bandwidth does not depend on values; use small normals to avoid inf)."""
-        w = (torch.randn(n_mats * E * rows * k, device="cuda") * 0.02).to(torch.bfloat16)
-        per = rows * k * 2
-        tab = [w.data_ptr() + (m * E + e) * per + rb * 128 * k * 2
-               for m in range(n_mats) for e in range(E) for rb in range(rows // 128)]
-        return w, torch.tensor(tab, dtype=torch.int64, device="cuda")
+        """n_mats x E packed weight matrices [rows, k] (bandwidth does not depend on
+        values; small normals).  --codec: encoded tiles (runtime/weight_codec.hpp)."""
+        if not a.codec:
+            w = (torch.randn(n_mats * E * rows * k, device="cuda") * 0.02).to(torch.bfloat16)
+            per = rows * k * 2
+            tab = [w.data_ptr() + (m * E + e) * per + rb * 128 * k * 2
+                   for m in range(n_mats) for e in range(E) for rb in range(rows // 128)]
+            return w, torch.tensor(tab, dtype=torch.int64, device="cuda")
+        per = rows // 128 * (k // 64) * 12432
+        enc = np.zeros(n_mats * E * per, np.uint8)
+        g = torch.Generator().manual_seed(rows + k)
+        for i in range(n_mats * E):
+            w = (torch.randn(rows, k, generator=g) * k ** -0.5).to(torch.bfloat16)
+            src = w.view(torch.int16).numpy().view(np.uint16)
+            packed = np.empty_like(src)
+            KD.pack_weight(src.ctypes.data_as(C.c_void_p), rows, k, packed.ctypes.data_as(C.c_void_p))
+            KD.codec_encode(packed.ctypes.data_as(C.c_void_p), rows, k,
+                            enc[i * per:(i + 1) * per].ctypes.data_as(C.c_void_p))
+        dev = torch.from_numpy(enc).cuda()
+        tab = [dev.data_ptr() + i * per + rb * (k // 64) * 12432
+               for i in range(n_mats * E) for rb in range(rows // 128)]
+        return dev, torch.tensor(tab, dtype=torch.int64, device="cuda")
 
     w13, t13 = blocks(F, H, 2)
     w2, t2 = blocks(H, F, 1)
@@ -86,9 +102,17 @@ def main():
         KD.moe_permute(ptr(idx), ptr(hn), mu, H, E, K, ptr(cnt), ptr(off), ptr(perm), ptr(inv),
                        ptr(xp), R, s)
 
+    gu_args = capi.GemmArgs(a_table=t13.data_ptr(), n_mats=2, G=E, RB=F // 128, K=H, b=xp.data_ptr(), R=R,
+                            b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=1, alpha=1.0,
+                            out_packed=inter.data_ptr(), out_R=R, codec=int(a.codec))
+    dn_args = capi.GemmArgs(a_table=t2.data_ptr(), n_mats=1, G=E, RB=H // 128, K=F, b=inter.data_ptr(), R=R,
+                            b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=0, alpha=1.0,
+                            out_f32=y.data_ptr(), ldo=H, codec=int(a.codec))
+
     def expert():
-        KD.expert_ffn(ptr(xp), R, ptr(cnt), ptr(off), ptr(t13), ptr(t2), E, H, F, ncap,
-                      ptr(inter), ptr(y), ptr(inv), ptr(wts), ptr(hbuf), mu, K, ptr(xo), s)
+        KD.gemm(C.byref(gu_args), s)
+        KD.gemm(C.byref(dn_args), s)
+        KD.moe_combine(ptr(hbuf), ptr(y), H, ptr(inv), ptr(wts), mu, H, K, ptr(xo), s)
 
     def tiling(rb):  # runtime.cpp dense_tiling
         cap = min(256, Rmu)
@@ -163,8 +187,15 @@ def main():
         ms = st.elapsed_time(en) / reps
         gbs = nbytes / (ms * 1e-3) / 1e9
         out[name] = {"ms": ms, "alg_bytes": nbytes, "GBps": gbs, "frac_hbm": gbs / peak}
+        extra = ""
+        if a.codec and name.startswith("expert"):  # bytes actually read: encoded weight tiles
+            wb = touched * 3 * H * F * 2
+            stored = nbytes - wb + wb * 12432 // 16384
+            out[name].update(stored_bytes=stored, stored_GBps=stored / (ms * 1e-3) / 1e9,
+                             stored_frac_hbm=stored / (ms * 1e-3) / 1e9 / peak)
+            extra = f"  [encoded: {stored / 1e6:.1f} MB, {100 * out[name]['stored_frac_hbm']:.1f}% of HBM]"
         print(f"{name:36s} mu={mu:4d} {ms * 1e3:9.1f} us  {nbytes / 1e6:9.1f} MB  "
-              f"{gbs:8.1f} GB/s  {100 * gbs / peak:5.1f}% of {peak} GB/s", flush=True)
+              f"{gbs:8.1f} GB/s  {100 * gbs / peak:5.1f}% of {peak} GB/s{extra}", flush=True)
     print(json.dumps({"mu": mu, "touched_experts": touched, "kernels": out}))
 
 
