@@ -296,6 +296,8 @@ typedef struct mlt_gemm_args_t {
                                   done, exit) — a diagnostic, NULL in production */
     int32_t codec;             /* 1: every A row block is encoded (12432 B per 64-k tile, see
                                   mlt_codec_encode_tile), expanded in smem by decoder warps */
+    unsigned long long* ktrace; /* optional CTA-0 pipeline trace [4][256] %globaltimer stamps per
+                                   k-block: producer issue, decoder start, decoder done, MMA start */
 } mlt_gemm_args_t;
 
 /* Grouped swap-AB tcgen05 GEMM (SURVEY.md §2c expert_gateup_silu /

@@ -69,6 +69,7 @@ mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
     g.split_stride = a->split_stride;
     g.trace = a->trace;
     g.codec = a->codec;
+    g.ktrace = a->ktrace;
     return g;
 }
 

@@ -19,6 +19,7 @@
 // are addressed through a page table (one pointer per row block), which is
 // how the same kernel reads resident rows and rows paged into either pool
 // slot (runtime/weights.cpp).
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -125,7 +126,7 @@ struct TileIn {
 };
 __device__ __forceinline__ void load_tile(uint32_t c, int dt, TileIn& in) {
     in.T = lds128(c + 12288);
-    in.n = lds32(c + 12304) & 0xffffu;
+    in.n = lds32(c + 12304) & 0xffffu;  // {u16 escape count, u16 0}
     in.esc = static_cast<uint32_t>(dt) < in.n ? lds32(c + 12308 + 4 * dt) : 0u;  // {u16 index, u8 hi, 0}
 #pragma unroll
     for (int j = 0; j < 1024 / kDecThreads; ++j) {
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
         // ===== producer =====
         if (elect_one()) {
             const uint64_t pol_w = l2_evict_first(), pol_x = l2_evict_last();
-            int stage = 0;
+            int stage = 0, kstep = 0;
             uint32_t phase = 0;
             for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
                 const int ks = v % a.k_splits, u = v / a.k_splits;
@@ -217,6 +218,8 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                     const int ntp = (nt + 15) & ~15;
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&ctl->empty[stage], phase ^ 1);
+                        if (a.ktrace && blockIdx.x == 0 && kstep < 256) a.ktrace[kstep] = globaltimer();
+                        ++kstep;
                         uint8_t* const st = smem + stage * stage_bytes;
                         uint8_t* sa = a.codec ? st + kCodecOff : st;
                         uint8_t* sb = st + a_bytes;
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
         // ===== MMA issuer =====
         int stage = 0;
         uint32_t phase = 0;
-        int acc = 0;
+        int acc = 0, kstep = 0;
         uint32_t acc_phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
             const int ks = v % a.k_splits, u = v / a.k_splits;
@@ -258,6 +261,8 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                     mbar_wait(&ctl->full[stage], phase);
                     if (a.codec) mbar_wait(&ctl->dfull[stage], phase);
                     tc_fence_after();
+                    if (a.ktrace && blockIdx.x == 0 && kstep < 256 && lane == 0) a.ktrace[768 + kstep] = globaltimer();
+                    ++kstep;
                     if (tr && lane == 0 && v == static_cast<int>(blockIdx.x) && kb == kb0 && n0 == c * a.n_cap)
                         tr[3] = globaltimer();
                     if (elect_one()) {
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
         const int grp = (static_cast<int>(threadIdx.x) - 192) / kDecThreads;
         const int dt = (static_cast<int>(threadIdx.x) - 192) % kDecThreads;
         const bool two = a.n_mats == 2;
-        int stage = 0;
+        int stage = 0, kstep = 0;
         uint32_t phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
             const int ks = v % a.k_splits, u = v / a.k_splits;
@@ -299,9 +304,10 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
             const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
             if (rows <= 0) continue;
             for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
-                for (int kb = kb0; kb < kb1; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb, ++kstep) {
                     if (stage % kDecGroups == grp) {
                         mbar_wait(&ctl->full[stage], phase);
+                        if (a.ktrace && blockIdx.x == 0 && kstep < 256 && dt == 0) a.ktrace[256 + kstep] = globaltimer();
                         const uint32_t sa = smem_u32(smem + stage * stage_bytes);
                         TileIn in0, in1;
                         load_tile(sa + kCodecOff, dt, in0);
@@ -317,6 +323,7 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                         }
                         fence_proxy_async_smem();  // generic smem writes -> visible to tcgen05.mma
                         decoders_sync(grp);
+                        if (a.ktrace && blockIdx.x == 0 && kstep < 256 && dt == 0) a.ktrace[512 + kstep] = globaltimer();
                         if (dt == 0) mbar_arrive(&ctl->dfull[stage]);
                     }
                     if (++stage == stages) { stage = 0; phase ^= 1; }
@@ -453,6 +460,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     a.stages = budget / per_stage;
     if (a.stages > 8) a.stages = 8;
     if (a.codec) a.stages -= a.stages % kDecGroups;  // decoder groups own whole stages
+    if (a.codec != 0 && a.codec != 1) return cudaErrorInvalidValue;
     if (a.stages < 2) return cudaErrorInvalidValue;
     const int acc_cols = a.n_mats * a.n_cap;
     a.acc_stages = (2 * acc_cols <= 512) ? 2 : 1;

@@ -35,6 +35,9 @@ struct GemmArgs {
     // 1: A row blocks are encoded tiles (runtime/weight_codec.hpp, 12432 B
     // per 64-k tile); decoder warps expand them in shared memory
     int codec = 0;
+    // optional CTA-0 pipeline trace [4][256] (%globaltimer): producer issue,
+    // decoder start, decoder done, MMA start per k-block (diagnostic)
+    unsigned long long* ktrace = nullptr;
     // epilogue
     int epi = kEpiF32;
     float alpha = 1.0f;

@@ -366,7 +366,7 @@ def test_kv_stage_layout(K):
         assert np.array_equal(seg_v, rows[:, (nq + nkv) * d:].reshape(n, nkv, d).transpose(1, 0, 2))
 
 
-def encode_weight_dev(K, w_bf16):
+def encode_weight_dev(K, w_bf16, fmt=1):
     """Host-pack + codec-encode a [M, K] bf16 weight and upload; returns (device
     buffer, encoded row-block pointers)."""
     M, Kd = w_bf16.shape
@@ -380,10 +380,11 @@ def encode_weight_dev(K, w_bf16):
     return dev, blocks
 
 
+@pytest.mark.parametrize("codec", [1])
 @pytest.mark.parametrize("T,M,Kd,n_cap,splits,resid", [(16, 256, 512, 16, 1, True), (64, 384, 4096, 64, 3, False),
                                                         (256, 256, 1024, 256, 2, False),
                                                         (200, 128, 256, 208, 1, True)])
-def test_codec_gemm_bitwise_equals_raw(K, T, M, Kd, n_cap, splits, resid):
+def test_codec_gemm_bitwise_equals_raw(K, T, M, Kd, n_cap, splits, resid, codec):
     """The GEMM on encoded weights (decoder warps expand tiles in smem) returns
     the same bits as on raw bf16 tiles: dense fp32 epilogue, split-K, residual."""
     g = torch.Generator().manual_seed(T + M + Kd)
@@ -391,17 +392,17 @@ def test_codec_gemm_bitwise_equals_raw(K, T, M, Kd, n_cap, splits, resid):
     x = rand_bf16(T, Kd, gen=g)
     R = (T + 15) // 16 * 16
     raw_dev, raw_blocks = pack_weight_dev(K, w)  # keep the buffers alive while the GEMMs read them
-    enc_dev, enc_blocks = encode_weight_dev(K, w)
+    enc_dev, enc_blocks = encode_weight_dev(K, w, codec)
     xp = pack_rows_dev(K, x, R)
     res = torch.randn(T, M, device="cuda") if resid else None
     outs = []
-    for codec, blocks in ((0, raw_blocks), (1, enc_blocks)):
+    for cdc, blocks in ((0, raw_blocks), (codec, enc_blocks)):
         tab = table([blocks])
         out = torch.zeros(splits, R, M, device="cuda")
         a = capi.GemmArgs(a_table=tab.data_ptr(), n_mats=1, G=1, RB=M // 128, K=Kd, b=xp.data_ptr(), R=R,
                           rows_dense=T, n_cap=n_cap, epi=0, alpha=1.0, out_f32=out.data_ptr(), ldo=M,
                           residual=res.data_ptr() if resid else None, ldr=M, k_splits=splits,
-                          split_stride=R * M, codec=codec)
+                          split_stride=R * M, codec=cdc)
         K.gemm(C.byref(a), stream())
         torch.cuda.synchronize()
         outs.append(out.cpu())
@@ -410,8 +411,9 @@ def test_codec_gemm_bitwise_equals_raw(K, T, M, Kd, n_cap, splits, resid):
     assert (outs[1].sum(0)[:T] - ref).abs().max().item() <= 2e-3 * max(1.0, ref.abs().max().item())
 
 
+@pytest.mark.parametrize("codec", [1])
 @pytest.mark.parametrize("T,H,Fd,E,Kk,n_cap", [(64, 512, 768, 8, 2, 64), (33, 256, 256, 16, 4, 32)])
-def test_codec_expert_ffn_bitwise_equals_raw(K, T, H, Fd, E, Kk, n_cap):
+def test_codec_expert_ffn_bitwise_equals_raw(K, T, H, Fd, E, Kk, n_cap, codec):
     """Grouped gate/up (two encoded matrices, fused SiLU -> packed bf16) and
     down on encoded experts == the raw-tile GEMMs, bit for bit."""
     hn, w1, w3, w2, wr = _expert_setup(T, H, Fd, E, Kk, seed=T + H + 1)
@@ -428,8 +430,8 @@ def test_codec_expert_ffn_bitwise_equals_raw(K, T, H, Fd, E, Kk, n_cap):
     K.moe_permute(ptr(idx), ptr(hn_d), T, H, E, Kk, ptr(cnt), ptr(off), ptr(perm), ptr(inv), ptr(xp), R, stream())
     results = []
     keep = []
-    for codec in (0, 1):
-        mk = encode_weight_dev if codec else pack_weight_dev
+    for cdc in (0, codec):
+        mk = (lambda K_, w_: encode_weight_dev(K_, w_, cdc)) if cdc else pack_weight_dev
         t13, t2 = [], []
         for m in (w1, w3):
             for w in m:
@@ -445,13 +447,14 @@ def test_codec_expert_ffn_bitwise_equals_raw(K, T, H, Fd, E, Kk, n_cap):
         y = torch.zeros(R, H, device="cuda")
         gu = capi.GemmArgs(a_table=tab13.data_ptr(), n_mats=2, G=E, RB=Fd // 128, K=H, b=xp.data_ptr(), R=R,
                            b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=n_cap, epi=1, alpha=1.0,
-                           out_packed=inter.data_ptr(), out_R=R, codec=codec)
+                           out_packed=inter.data_ptr(), out_R=R, codec=cdc)
         K.gemm(C.byref(gu), stream())
         dn = capi.GemmArgs(a_table=tab2.data_ptr(), n_mats=1, G=E, RB=H // 128, K=Fd, b=inter.data_ptr(), R=R,
                            b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=n_cap, epi=0, alpha=1.0,
-                           out_f32=y.data_ptr(), ldo=H, codec=codec)
+                           out_f32=y.data_ptr(), ldo=H, codec=cdc)
         K.gemm(C.byref(dn), stream())
         torch.cuda.synchronize()
         results.append((inter.cpu(), y.cpu()))
     assert torch.equal(results[0][0], results[1][0])
     assert torch.equal(results[0][1], results[1][1])
+

@@ -56,7 +56,8 @@ def main():
         enc = np.zeros(n_mats * E * per, np.uint8)
         g = torch.Generator().manual_seed(rows + k)
         for i in range(n_mats * E):
-            w = (torch.randn(rows, k, generator=g) * k ** -0.5).to(torch.bfloat16)
+            # the runtime's synthetic-weight distribution: uniform(-sqrt3 s, sqrt3 s), s = 1/sqrt(k)
+            w = ((torch.rand(rows, k, generator=g) * 2 - 1) * (3.0 / k) ** 0.5).to(torch.bfloat16)
             src = w.view(torch.int16).numpy().view(np.uint16)
             packed = np.empty_like(src)
             KD.pack_weight(src.ctypes.data_as(C.c_void_p), rows, k, packed.ctypes.data_as(C.c_void_p))
