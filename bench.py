@@ -59,7 +59,7 @@ CONFIGS = {
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 NVLINK_BW = 900e9       # B200 NVLink 5, bytes/s per direction (nominal; 1 GPU in this pool)
-HOST_FLOPS = 2.0e12     # host-core fp32 estimate (16 SPR cores AVX-512); CPU attention never binds
+HOST_FLOPS = 2.0e12     # host-core fp32 estimate (16 SPR cores AVX-512); host DRAM bandwidth is measured
 
 
 def peaks():
@@ -127,7 +127,10 @@ class ClockSampler:
 # bytes per weight as stored with --codec (12432 B per 8192-weight tile,
 # runtime/weight_codec.hpp); the runtime itself always computes in bf16
 CODEC_DT = 12432 / 8192
-ARENA_EXTRA = 0.75e9   # embedding + lm_head + activations: arena bytes outside ModelSpec
+def arena_extra(cfg):
+    """Arena bytes outside ModelSpec: embedding + lm_head (vocab x h1 bf16 each),
+    activations, page tables and KV-independent buffers (0.5 GB)."""
+    return 2 * cfg["vocab"] * cfg["model"][1] * 2 + 0.5e9
 
 
 def model_spec(cfg, stored=False):
@@ -139,15 +142,17 @@ def model_spec(cfg, stored=False):
     return capi.ModelSpec(l, h1, h2, nq, nkv, ne, k, CODEC_DT if stored and cfg.get("codec") else 2.0, 2.0)
 
 
-def search_rw(cfg, link_gbs, host_gbs, pk, tp=1):
+def search_rw(cfg, link_gbs, host_gbs, pk, tp=1, per_slice_host=False):
     """Best feasible r_w for the config's (N, mu, A_g) on the measured spec with
     the stored weight bytes (product search_policy, planner.cpp:234-341)."""
     from paper_2411_11217_b200 import capi
     api = capi.load_product()
-    hw = capi.HardwareSpec(cfg["budget"] - ARENA_EXTRA, 196e9 * max(tp, 1), pk["hbm_gbs"] * 1e9, host_gbs * 1e9,
-                           link_gbs * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12, HOST_FLOPS)
+    slices = tp if per_slice_host else 1
+    hw = capi.HardwareSpec(cfg["budget"] - arena_extra(cfg), 196e9 * max(tp, 1), pk["hbm_gbs"] * 1e9,
+                           host_gbs * 1e9 * slices, link_gbs * 1e9,
+                           pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12, HOST_FLOPS * slices)
     if tp > 1:
-        hw = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=host_gbs * 1e9 * tp)
+        hw = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=host_gbs * 1e9 * slices)
     grid = capi.make_grid([cfg["mu"]], [cfg["N"] // cfg["mu"]], [round(0.01 * i, 2) for i in range(101)],
                           [1.0] if cfg["a_g"] else [0.0], attn=(cfg["a_g"],), ffn=(1,))
     return api.search_policy(hw, model_spec(cfg, stored=True), capi.WorkloadSpec(cfg["prompt"], cfg["gen"]),
@@ -170,9 +175,12 @@ def hrm_bound(cfg, link_gbs, host_gbs, pk, tp=1, per_slice_host=False):
     # measured box is one GPU's slice (16 cores, 196 GB, its own PCIe link), so a
     # tp-way job has tp such slices
     slices = tp if per_slice_host else 1
-    hw = capi.HardwareSpec(cfg["budget"], 196e9 * max(tp, 1), pk["hbm_gbs"] * 1e9, host_gbs * 1e9,
+    # a slice's host cores compute its own heads' attention: host DRAM bandwidth
+    # and FLOP/s of the job scale with the slices too (the reference keeps the
+    # CPU side fixed under TP, planner.cpp:101-108)
+    hw = capi.HardwareSpec(cfg["budget"], 196e9 * max(tp, 1), pk["hbm_gbs"] * 1e9, host_gbs * 1e9 * slices,
                            link_gbs * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12,
-                           HOST_FLOPS)
+                           HOST_FLOPS * slices)
     if tp > 1:
         hw = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=host_gbs * 1e9 * slices)
     w = capi.WorkloadSpec(cfg["prompt"], cfg["gen"])
@@ -320,14 +328,14 @@ def run_mlt(args, cfg):
 
     raw_rw = cfg["r_w"]
     if cfg.get("codec"):  # the stored bytes shrink: re-pick r_w for the budget
-        cfg["r_w"] = search_rw(cfg, link_gbs, host_gbs, pk, tp)
+        cfg["r_w"] = search_rw(cfg, link_gbs, host_gbs, pk, tp, per_slice_host=args.tp_shard > 1)
         log(f"[bench] rank {rank}: weight codec on, r_w {cfg['r_w']:.2f} (search on {CODEC_DT:.4f} B/weight)")
     t = time.perf_counter()
     rt = Runtime(model_spec(cfg), policy(cfg), budget_bytes=cfg["budget"],
                  max_ctx=cfg["prompt"] + args.warmup + args.steps + 8, vocab=cfg["vocab"],
                  device=local, exact_gates=args.gates == "exact", tp_rank=shard_rank, tp_size=tp,
                  nccl_id=nid, schedule=args.schedule, tp_shard_only=args.tp_shard > 1,
-                 weight_codec=bool(cfg.get("codec")))
+                 weight_codec=bool(cfg.get("codec")), pdl=not args.no_pdl)
     info = rt.info
     log(f"[bench] rank {rank}: runtime ready in {time.perf_counter() - t:.1f}s (weights gen "
         f"{info.gen_seconds:.1f}s, pin {info.pin_seconds:.1f}s), r_w achieved "
@@ -476,6 +484,8 @@ def main():
     ap.add_argument("--codec", default="auto", choices=["auto", "on", "off"],
                     help="store/stream/read weights as lossless encoded tiles (runtime/weight_codec.hpp); "
                          "auto = on when weights are paged over the host link (r_w < 1), off when resident")
+    ap.add_argument("--no-pdl", action="store_true",
+                    help="no programmatic dependent launch on all-GPU schedules (per-kernel event breakdown)")
     ap.add_argument("--tp-shard", type=int, default=0,
                     help="measure the largest shard of a T-way TP job alone on one GPU (all-reduce elided)")
     args = ap.parse_args()

@@ -409,6 +409,8 @@ typedef struct mlt_runtime_options_t {
     int32_t weight_codec;     /* 1: projection + expert weights are stored, paged and read by the
                                  GEMMs as encoded tiles (lossless, 24 % fewer bytes over PCIe and
                                  from HBM; mlt_codec_encode); numerics unchanged bit for bit */
+    int32_t disable_pdl;      /* 1: no programmatic dependent launch (all-GPU schedules use it by
+                                 default; per-kernel CUDA-event breakdowns need it off) */
 } mlt_runtime_options_t;
 
 /* ncclUniqueId for a tensor-parallel group (call on rank 0, broadcast). */

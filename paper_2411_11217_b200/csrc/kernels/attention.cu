@@ -86,6 +86,8 @@ __global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
     const uint16_t* __restrict__ q, int ldq, const uint16_t* __restrict__ kp, const uint16_t* __restrict__ vp,
     const int32_t* __restrict__ bt, int max_pages, const int32_t* __restrict__ seq, const int32_t* __restrict__ ctx,
     int nkv, uint8_t* out_p, int R, float* out_f) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     static_assert(G >= 1 && G <= 8, "heads per kv head must fit the MMA n = 8");
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ uint64_t full[kWarps][kStagesW];
@@ -249,6 +251,8 @@ __global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
 __global__ void kv_append_kernel(const uint16_t* qkv, int nq, int nkv, int d, const int32_t* seq,
                                  const int32_t* pos, const int32_t* bt, int max_pages, int page,
                                  uint16_t* kp, uint16_t* vp) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     const int t = blockIdx.x;
     const int W = (nq + 2 * nkv) * d;
     const int p = pos[t];
@@ -276,9 +280,8 @@ cudaError_t launch_g(const uint16_t* q, int ldq, const uint16_t* kp, const uint1
         attr = true;
     }
     dim3 grid(T, nkv);
-    gqa_decode_kernel<G><<<grid, kWarps * 32, smem, s>>>(q, ldq, kp, vp, bt, max_pages, seq, ctx, nkv,
+    return launch_k(gqa_decode_kernel<G>, dim3(grid), dim3(kWarps * 32), smem, s, q, ldq, kp, vp, bt, max_pages, seq, ctx, nkv,
                                                          out_p, R, out_f);
-    return cudaGetLastError();
 }
 
 }  // namespace
@@ -304,9 +307,8 @@ cudaError_t launch_kv_append(const uint16_t* qkv_bf16, int nq, int nkv, int d, c
                              const int32_t* pos, int T, const int32_t* block_table, int max_pages,
                              int page, uint16_t* k_pool, uint16_t* v_pool, cudaStream_t s) {
     if (T <= 0) return cudaSuccess;
-    kv_append_kernel<<<T, 256, 0, s>>>(qkv_bf16, nq, nkv, d, seq, pos, block_table, max_pages,
+    return launch_k(kv_append_kernel, dim3(T), dim3(256), 0, s, qkv_bf16, nq, nkv, d, seq, pos, block_table, max_pages,
                                        page, k_pool, v_pool);
-    return cudaGetLastError();
 }
 
 }  // namespace mltk

@@ -69,6 +69,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 __global__ void __launch_bounds__(256) prefill_attn_kernel(const uint16_t* __restrict__ qkv, int W,
                                                            const int4* __restrict__ tiles, int nq, int nkv,
                                                            float scale_log2, uint8_t* __restrict__ out, int R) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     extern __shared__ __align__(128) uint8_t smem[];
     const int4 tile = tiles[blockIdx.x];
     const int row0 = tile.x, len = tile.y, q0 = tile.z;
@@ -234,6 +236,8 @@ __global__ void kv_stage_kernel(const uint16_t* __restrict__ qkv, int W, int nq,
                                 const int32_t* __restrict__ tok_seq, const int32_t* __restrict__ tok_pos,
                                 const int32_t* __restrict__ seq_row0, const int32_t* __restrict__ seq_len,
                                 int T, uint16_t* __restrict__ sk, uint16_t* __restrict__ sv) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     const int chunks = nkv * kD / 8;  // 16-byte chunks per token for K (same for V)
     const int64_t work = static_cast<int64_t>(T) * chunks;
     for (int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < work;
@@ -251,6 +255,8 @@ __global__ void kv_stage_kernel(const uint16_t* __restrict__ qkv, int W, int nq,
 // x rows idx[i] -> dst row i (fp32), for the last-token lm_head of a chunk.
 __global__ void gather_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ idx, int n, int H,
                                    float* __restrict__ dst) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     const int i = blockIdx.x;
     if (i >= n) return;
     const float4* s = reinterpret_cast<const float4*>(x + static_cast<int64_t>(idx[i]) * H);
@@ -275,9 +281,8 @@ cudaError_t launch_prefill_attention(const uint16_t* qkv, int W, const int4* til
         attr = true;
     }
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(kD));
-    prefill_attn_kernel<<<dim3(n_tiles, nkv), 32 * (nq / nkv), prefill_attention_smem_bytes(), s>>>(
+    return launch_k(prefill_attn_kernel, dim3(n_tiles, nkv), dim3(32 * (nq / nkv)), prefill_attention_smem_bytes(), s,
         qkv, W, tiles, nq, nkv, scale_log2, out, R);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_kv_stage(const uint16_t* qkv, int W, int nq, int nkv, int d, const int32_t* tok_seq,
@@ -288,15 +293,13 @@ cudaError_t launch_kv_stage(const uint16_t* qkv, int W, int nq, int nkv, int d, 
     const int64_t work = static_cast<int64_t>(T) * nkv * kD / 8;
     int grid = static_cast<int>((work + 255) / 256);
     if (grid > 148 * 8) grid = 148 * 8;
-    kv_stage_kernel<<<grid, 256, 0, s>>>(qkv, W, nq, nkv, tok_seq, tok_pos, seq_row0, seq_len, T, stage_k, stage_v);
-    return cudaGetLastError();
+    return launch_k(kv_stage_kernel, dim3(grid), dim3(256), 0, s, qkv, W, nq, nkv, tok_seq, tok_pos, seq_row0, seq_len, T, stage_k, stage_v);
 }
 
 cudaError_t launch_gather_rows(const float* x, const int32_t* idx, int n, int H, float* dst, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     if (H % 4) return cudaErrorInvalidValue;
-    gather_rows_kernel<<<n, 256, 0, s>>>(x, idx, n, H, dst);
-    return cudaGetLastError();
+    return launch_k(gather_rows_kernel, dim3(n), dim3(256), 0, s, x, idx, n, H, dst);
 }
 
 }  // namespace mltk

@@ -187,6 +187,19 @@ __device__ __forceinline__ uint32_t idesc_bf16(uint32_t M, uint32_t N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// With set_pdl(true) every kernel of this build is launched with
+// programmatic stream serialization: it may be scheduled while its stream
+// predecessor drains; each kernel first lets its own dependents launch
+// (launch_dependents) and then waits for its predecessor's completion and
+// memory (griddepcontrol.wait) before touching any buffer the predecessor
+// may write or read.  Without PDL both instructions are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Device-wide nanosecond timer (same timebase on every SM).
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -217,6 +230,28 @@ __device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
     uint32_t u = __float_as_uint(f);
     u += 0x7fffu + ((u >> 16) & 1u);
     return static_cast<uint16_t>(u >> 16);
+}
+
+bool pdl_enabled();
+
+// Kernel launch through cudaLaunchKernelEx, with the PDL attribute when enabled.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    if (pdl_enabled()) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 #endif  // __CUDACC__

@@ -11,6 +11,13 @@
 #include "kernels.hpp"
 
 namespace mltk {
+
+namespace {
+bool g_pdl = false;
+}
+bool pdl_enabled() { return g_pdl; }
+void set_pdl(bool on) { g_pdl = on; }
+
 namespace {
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
@@ -27,6 +34,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 __global__ void embed_kernel(const int32_t* tokens, const uint16_t* table, int H, float* x) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     const int t = blockIdx.x;
     const uint16_t* src = table + static_cast<int64_t>(tokens[t]) * H;
     for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
@@ -82,6 +91,8 @@ __device__ __forceinline__ uint4 norm8(const float (&v)[8], float r, const uint1
 
 __global__ void __launch_bounds__(1024) rmsnorm_pack_kernel(const float* x, const uint16_t* gamma, int H,
                                                             float eps, uint8_t* out, int R) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     __shared__ float red[32];
     const int t = blockIdx.x, i = threadIdx.x * 8;
     float v[8];
@@ -95,6 +106,8 @@ __global__ void __launch_bounds__(1024) rmsnorm_pack_kernel(const float* x, cons
 }
 
 __global__ void pack_rows_kernel(const uint16_t* src, int ld, int K, uint8_t* dst, int R) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     const int t = blockIdx.x;
     for (int i = threadIdx.x * 8; i < K; i += blockDim.x * 8)
         *reinterpret_cast<uint4*>(dst + b_packed_off(t, i, R)) =
@@ -113,6 +126,8 @@ __global__ void __launch_bounds__(256) rope_qkv_kernel(const float* __restrict__
                                                        int64_t part_stride, const int32_t* __restrict__ pos,
                                                        const float2* __restrict__ rope, int T, int nq, int nkv,
                                                        uint16_t* __restrict__ out, KvAppend kv) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     constexpr int half = D / 2;
     constexpr int upr = half / 8;  // units per q/k head
     const int W = (nq + 2 * nkv) * D;
@@ -193,6 +208,8 @@ __global__ void __launch_bounds__(768) combine_kernel(const float* h, const floa
                                                       const int32_t* inv, const float* w, int H,
                                                       float* x, const uint16_t* gamma, float eps,
                                                       uint8_t* xn, int R) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     __shared__ float red[32];
     const int t = blockIdx.x, i = threadIdx.x * 8;
     float ys[K][8];  // every slot row's loads issued before the sum
@@ -224,6 +241,8 @@ __global__ void __launch_bounds__(768) combine_kernel(const float* h, const floa
 // fixed order (deterministic).
 __global__ void sum_parts_kernel(const float* parts, int n_parts, int64_t stride, const float* add,
                                  float* out, int64_t n4) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         float4 a = reinterpret_cast<const float4*>(parts)[i];
@@ -260,6 +279,8 @@ __device__ __forceinline__ void merge(Best2& a, const Best2& b) {
 }
 
 __global__ void argmax_kernel(const float* logits, int V, int32_t* ids, float* margin) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     __shared__ Best2 red[32];
     const int t = blockIdx.x;
     const float* r = logits + static_cast<int64_t>(t) * V;
@@ -293,24 +314,21 @@ cudaError_t launch_embed(const int32_t* tokens, const uint16_t* table, int T, in
                          cudaStream_t s) {
     if (T <= 0) return cudaSuccess;
     if (H % 8) return cudaErrorInvalidValue;
-    embed_kernel<<<T, 128, 0, s>>>(tokens, table, H, x);
-    return cudaGetLastError();
+    return launch_k(embed_kernel, dim3(T), dim3(128), 0, s, tokens, table, H, x);
 }
 
 cudaError_t launch_rmsnorm_pack(const float* x, const uint16_t* gamma, int T, int H, float eps,
                                 uint8_t* out, int R, cudaStream_t s) {
     if (T <= 0) return cudaSuccess;
     if (H % 256 || H > 8192 || R < T) return cudaErrorInvalidValue;
-    rmsnorm_pack_kernel<<<T, H / 8, 0, s>>>(x, gamma, H, eps, out, R);
-    return cudaGetLastError();
+    return launch_k(rmsnorm_pack_kernel, dim3(T), dim3(H / 8), 0, s, x, gamma, H, eps, out, R);
 }
 
 cudaError_t launch_pack_rows(const uint16_t* src, int ld, int T, int K, uint8_t* dst, int R,
                              cudaStream_t s) {
     if (T <= 0) return cudaSuccess;
     if (K % 64 || R < T) return cudaErrorInvalidValue;
-    pack_rows_kernel<<<T, 128, 0, s>>>(src, ld, K, dst, R);
-    return cudaGetLastError();
+    return launch_k(pack_rows_kernel, dim3(T), dim3(128), 0, s, src, ld, K, dst, R);
 }
 
 cudaError_t launch_rope_qkv(const float* qkv, int parts, int64_t part_stride, const int32_t* pos,
@@ -320,9 +338,8 @@ cudaError_t launch_rope_qkv(const float* qkv, int parts, int64_t part_stride, co
     if (parts < 1 || d != 128 || part_stride % 4) return cudaErrorInvalidValue;
     const int64_t total = static_cast<int64_t>(T) * ((nq + nkv) * 8 + nkv * 16);
     const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
-    rope_qkv_kernel<128><<<grid, 256, 0, s>>>(qkv, parts, part_stride, pos, rope, T, nq, nkv, out,
+    return launch_k(rope_qkv_kernel<128>, dim3(grid), dim3(256), 0, s, qkv, parts, part_stride, pos, rope, T, nq, nkv, out,
                                               kv ? *kv : KvAppend{});
-    return cudaGetLastError();
 }
 
 cudaError_t launch_moe_combine(const float* h, const float* y, int ldy, const int32_t* inv,
@@ -331,10 +348,10 @@ cudaError_t launch_moe_combine(const float* h, const float* y, int ldy, const in
     if (T <= 0) return cudaSuccess;
     if (H % 256 || H > 6144 || ldy % 4 || (gamma && (!xn || R < T))) return cudaErrorInvalidValue;
     switch (K) {  // x = h + sum of K slot rows (slot order)
-        case 1: combine_kernel<1><<<T, H / 8, 0, s>>>(h, y, ldy, inv, w, H, x, gamma, eps, xn, R); break;
-        case 2: combine_kernel<2><<<T, H / 8, 0, s>>>(h, y, ldy, inv, w, H, x, gamma, eps, xn, R); break;
-        case 4: combine_kernel<4><<<T, H / 8, 0, s>>>(h, y, ldy, inv, w, H, x, gamma, eps, xn, R); break;
-        case 8: combine_kernel<8><<<T, H / 8, 0, s>>>(h, y, ldy, inv, w, H, x, gamma, eps, xn, R); break;
+        case 1: return launch_k(combine_kernel<1>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R);
+        case 2: return launch_k(combine_kernel<2>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R);
+        case 4: return launch_k(combine_kernel<4>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R);
+        case 8: return launch_k(combine_kernel<8>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R);
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -347,15 +364,13 @@ cudaError_t launch_sum_parts(const float* parts, int n_parts, int64_t stride, co
     const int64_t n4 = n / 4;
     int grid = static_cast<int>((n4 + 255) / 256);
     if (grid > 1184) grid = 1184;
-    sum_parts_kernel<<<grid, 256, 0, s>>>(parts, n_parts, stride, add, out, n4);
-    return cudaGetLastError();
+    return launch_k(sum_parts_kernel, dim3(grid), dim3(256), 0, s, parts, n_parts, stride, add, out, n4);
 }
 
 cudaError_t launch_argmax(const float* logits, int T, int V, int32_t* ids, float* margin,
                           cudaStream_t s) {
     if (T <= 0) return cudaSuccess;
-    argmax_kernel<<<T, 512, 0, s>>>(logits, V, ids, margin);
-    return cudaGetLastError();
+    return launch_k(argmax_kernel, dim3(T), dim3(512), 0, s, logits, V, ids, margin);
 }
 
 }  // namespace mltk

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
 
     const uint32_t warp = warp_idx_sync();
     const uint32_t lane = threadIdx.x & 31;
-    if (a.timing && threadIdx.x == 0) atomicMin(&a.timing[0], globaltimer());
+
     unsigned long long* const tr = a.trace ? a.trace + blockIdx.x * 8 : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = globaltimer();
     const int acc_cols = a.n_mats * a.n_cap;     // TMEM columns per accumulator stage
@@ -187,9 +187,27 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc(&ctl->tmem_base, a.tmem_cols);
+    pdl_trigger();
+    if (warp == 0 && lane == 0 && static_cast<int>(blockIdx.x) < a.G * a.RB * a.n_chunks * a.k_splits) {
+        // immutable weights: warm L2 with this CTA's first A tiles while the
+        // predecessor kernel drains (PDL); activations only after the wait
+        const int u = static_cast<int>(blockIdx.x) / a.k_splits, ks = static_cast<int>(blockIdx.x) % a.k_splits;
+        const int g = (u / a.n_chunks) % a.G, rb = u / a.n_chunks / a.G;
+        const int KBt = a.K / kBlockK, kb0 = ks * KBt / a.k_splits;
+        const int tile = a.codec ? kCodecTile : kATileBytes;
+        const int nkb = min(4, (ks + 1) * KBt / a.k_splits - kb0);
+        for (int mt = 0; mt < a.n_mats; ++mt) {
+            const uint8_t* p = a.a_table[(static_cast<int64_t>(mt) * a.G + g) * a.RB + rb];
+            prefetch_l2(p + static_cast<int64_t>(kb0) * tile, static_cast<uint32_t>(nkb * tile));
+        }
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();
+    // in-kernel timing starts once the predecessor is done (with PDL the CTA
+    // may have been resident, prefetching weights, while it drained)
+    if (a.timing && threadIdx.x == 0) atomicMin(&a.timing[0], globaltimer());
     const uint32_t tmem = ctl->tmem_base;
     if (tr && threadIdx.x == 0) tr[1] = globaltimer();
 
@@ -479,8 +497,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     const int n_virtual = a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
-    gemm_tc_kernel<<<grid, a.codec ? kThreadsCodec : kThreadsRaw, smem, stream>>>(a);
-    return cudaGetLastError();
+    return launch_k(gemm_tc_kernel, dim3(grid), dim3(a.codec ? kThreadsCodec : kThreadsRaw), smem, stream, a);
 }
 
 }  // namespace mltk

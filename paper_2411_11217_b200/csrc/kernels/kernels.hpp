@@ -52,6 +52,10 @@ struct GemmArgs {
 };
 
 cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream);
+
+// Programmatic dependent launch for every kernel of this build (see
+// common.cuh); off by default; the runtime turns it on for all-GPU schedules.
+void set_pdl(bool on);
 int gemm_smem_bytes(int n_mats, int n_cap, int stages);
 
 // x_out[t][:] = float(table[tokens[t]][:])

@@ -33,6 +33,8 @@ __global__ void __launch_bounds__(768) router_kernel(const float* x, const uint1
                                                       int K, uint16_t* hn_out, float* logits, int32_t* topk_idx,
                                                       float* topk_w, int parts, int64_t part_stride,
                                                       const float* residual, float* h_out) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     extern __shared__ __align__(16) uint8_t sm[];
     uint16_t* hn = reinterpret_cast<uint16_t*>(sm);                 // H bf16
     float* lg = reinterpret_cast<float*>(sm + ((H * 2 + 15) & ~15)); // E fp32
@@ -155,6 +157,8 @@ __global__ void __launch_bounds__(768) router_kernel(const float* x, const uint1
 __global__ void permute_kernel(const int32_t* topk_idx, const uint16_t* hn, int T, int H, int E,
                                int K, int32_t* counts, int32_t* offsets, int32_t* perm,
                                int32_t* inv, uint8_t* xp, int R) {
+    pdl_trigger();  // dependents may launch; our inputs: after the wait
+    pdl_wait();
     __shared__ int s_cnt[kMaxE];
     __shared__ int s_off[kMaxE + 1];
     extern __shared__ int dyn[];
@@ -239,9 +243,8 @@ cudaError_t launch_router(const float* x, const uint16_t* gamma, float eps, cons
         return cudaErrorInvalidValue;
     if (H > 6144) return cudaErrorInvalidValue;  // H/8 threads per token
     const int smem = ((H * 2 + 15) & ~15) + E * 4;
-    router_kernel<<<T, H / 8, smem, s>>>(x, gamma, eps, hn_in, w, H, E, K, hn_out, logits, topk_idx,
+    return launch_k(router_kernel, dim3(T), dim3(H / 8), smem, s, x, gamma, eps, hn_in, w, H, E, K, hn_out, logits, topk_idx,
                                        topk_w, parts, part_stride, residual, h_out);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_moe_permute(const int32_t* topk_idx, const uint16_t* hn, int T, int H, int E,
@@ -261,8 +264,7 @@ cudaError_t launch_moe_permute(const int32_t* topk_idx, const uint16_t* hn, int 
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    permute_kernel<<<grid, 256, smem, s>>>(topk_idx, hn, T, H, E, K, counts, offsets, perm, inv, xp, R);
-    return cudaGetLastError();
+    return launch_k(permute_kernel, dim3(grid), dim3(256), smem, s, topk_idx, hn, T, H, E, K, counts, offsets, perm, inv, xp, R);
 }
 
 }  // namespace mltk

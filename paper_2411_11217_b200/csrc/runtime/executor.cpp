@@ -38,6 +38,7 @@
 #include "../capi/status.hpp"
 #include "host_layout.hpp"
 #include "runtime.hpp"
+#include "../kernels/kernels.hpp"
 
 namespace mlt {
 
@@ -137,6 +138,16 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
             step_pos_[static_cast<size_t>(s) * N_ + i] = pos_[i] + s;
             ctx[static_cast<size_t>(s) * N_ + i] = pos_[i] + s + 1;
         }
+    // All-GPU schedules (weights + KV resident, attention on the GPU) are
+    // launch-bound chains of kernels on one stream: launch them with PDL so a
+    // kernel's launch and setup (and its first weight tiles, prefetched to L2)
+    // overlap its predecessor's tail.  Per-kernel events would serialise the
+    // chain, so the per-kernel breakdown is taken without PDL (pdl_ false).
+    pdl_ = opt_.pdl && policy_.attn_on_gpu && cat_.blob_bytes == 0;
+    mltk::set_pdl(pdl_);
+    struct PdlOff {
+        ~PdlOff() { mltk::set_pdl(false); }
+    } pdl_off;
     cudaEvent_t e0, e_end;
     ck(cudaEventCreate(&e0), "event");
     ck(cudaEventCreate(&e_end), "event");

@@ -453,6 +453,7 @@ cudaEvent_t Runtime::take_event() {
 void Runtime::kl(const char* name, cudaError_t e) {
     ck(e, name);
     ++launches_;
+    if (pdl_) return;  // no per-kernel events inside a PDL chain
     cudaEvent_t ev = take_event();
     ck(cudaEventRecord(ev, s_gpu_), "event");
     marks_.push_back({name, ev});

@@ -45,6 +45,7 @@ struct RuntimeOptions {
     uint8_t nccl_id[128] = {};     // ncclUniqueId from rank 0 (tp_size > 1)
     bool tp_shard_only = false;    // one shard alone on this GPU, all-reduce elided (measurement)
     bool weight_codec = false;     // store/stream/read projection + expert weights encoded (weight_codec.hpp)
+    bool pdl = true;               // programmatic dependent launch on all-GPU (resident, A_g = 1) schedules
     int schedule = -1;             // -1: CGOPipe (S4 when A_g = 1); else a ScheduleKind to execute
     int prefill_chunk_tokens = 0;  // 0: largest prefill chunk the budget allows
 };
@@ -255,6 +256,7 @@ class Runtime {
 
     cudaStream_t s_gpu_ = nullptr, s_h2d_ = nullptr, s_d2h_ = nullptr;
     int launches_ = 0;
+    bool pdl_ = false;  // this decode runs its kernels as a PDL chain
     // per-kernel marks recorded by the GPU worker during decode(): (name,
     // event after the launch); name == nullptr marks a task's start event
     std::vector<std::pair<const char*, cudaEvent_t>> marks_;

@@ -24,9 +24,9 @@ import bench  # noqa: E402  (model/bound helpers, live link + host measurements)
 from paper_2411_11217_b200 import capi  # noqa: E402
 from paper_2411_11217_b200.runtime import Runtime  # noqa: E402
 
-# arena bytes outside ModelSpec (embedding + lm_head 0.52 GB, activations,
-# page tables): the search runs on m_g = budget - this, the runtime on budget
-RESERVE = 0.75e9
+# the search runs on m_g = budget - bench.arena_extra (embedding + lm_head +
+# activations, which ModelSpec does not model), the runtime on the budget
+RESERVE = 0.82e9  # bench.arena_extra for the 8x7B shape (reported)
 
 
 def main():
@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--codec", action="store_true", help="weights stored/streamed/read as encoded tiles")
     a = ap.parse_args()
     import ctypes as C
     api = capi.load_product()
@@ -51,8 +52,8 @@ def main():
     l = model_t[0]
     rows = []
     for budget_gb in [float(x) for x in a.budgets.split(",")]:
-        cfg0 = dict(model=model_t, N=N, prompt=prompt, gen=gen, budget=budget_gb * 1e9)
-        hw = capi.HardwareSpec(budget_gb * 1e9 - RESERVE, 196e9, pk["hbm_gbs"] * 1e9, host * 1e9,
+        cfg0 = dict(model=model_t, N=N, prompt=prompt, gen=gen, budget=budget_gb * 1e9, codec=a.codec)
+        hw = capi.HardwareSpec(budget_gb * 1e9 - bench.arena_extra(dict(cfg0, vocab=32000)), 196e9, pk["hbm_gbs"] * 1e9, host * 1e9,
                                link[0] * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12,
                                bench.HOST_FLOPS)
         w = capi.WorkloadSpec(prompt, gen)
@@ -61,7 +62,7 @@ def main():
                 grid = capi.make_grid([mu], [N // mu], [round(0.01 * i, 2) for i in range(101)],
                                       [1.0] if a_g else [0.0], attn=(a_g,), ffn=(1,))
                 try:
-                    plan = api.search_policy(hw, bench.model_spec(cfg0), w, grid)
+                    plan = api.search_policy(hw, bench.model_spec(cfg0, stored=True), w, grid)
                 except capi.MltError as e:
                     rows.append({"budget_gb": budget_gb, "mu": mu, "A_g": a_g, "feasible": False,
                                  "why": str(e)[:160]})
@@ -74,7 +75,7 @@ def main():
                 t = time.perf_counter()
                 try:
                     rt = Runtime(bench.model_spec(cfg), bench.policy(cfg), budget_bytes=cfg["budget"],
-                                 max_ctx=prompt + a.steps + a.warmup + 8, vocab=32000)
+                                 max_ctx=prompt + a.steps + a.warmup + 8, vocab=32000, weight_codec=a.codec)
                 except capi.MltError as e:  # e.g. the arena's extras push it over the cap
                     rows.append({"budget_gb": budget_gb, "mu": mu, "A_g": a_g, "r_w": r_w, "feasible": False,
                                  "why": "runtime: " + str(e)[:160]})
@@ -112,7 +113,8 @@ def main():
             "search_optimum": {k: best_model[k] for k in ("mu", "A_g", "r_w", "hrm_bound_tok_s", "measured_tok_s")},
             "measured_optimum": {k: best_meas[k] for k in ("mu", "A_g", "r_w", "hrm_bound_tok_s", "measured_tok_s")},
             "search_pick_within_pct_of_measured_best": 100 * best_model["measured_tok_s"] / best_meas["measured_tok_s"]}
-    out = {"what": "HRM policy sweep, Mixtral-8x7B shape, N=256, prompt 512, 1x B200 (tools/hrm_sweep.py)",
+    out = {"what": "HRM policy sweep, Mixtral-8x7B shape, N=256, prompt 512, 1x B200 (tools/hrm_sweep.py)"
+                   + (", weights encoded (weight codec, 12432 B per 16 KiB tile)" if a.codec else ""),
            "link_gbs": link[0], "host_read_gbs": host, "peaks_source": pk_src, "search_reserve_gb": RESERVE / 1e9,
            "decode_steps": a.steps, "rows": rows, "summary": summary}
     js = json.dumps(out, indent=1)
