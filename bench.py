@@ -129,8 +129,9 @@ class ClockSampler:
 CODEC_DT = 12432 / 8192
 def arena_extra(cfg):
     """Arena bytes outside ModelSpec: embedding + lm_head (vocab x h1 bf16 each),
-    activations, page tables and KV-independent buffers (0.5 GB)."""
-    return 2 * cfg["vocab"] * cfg["model"][1] * 2 + 0.5e9
+    activations, page tables and other KV-independent buffers (0.2 GB); the runtime
+    steps r_w down if the arena still overflows."""
+    return 2 * cfg["vocab"] * cfg["model"][1] * 2 + 0.2e9
 
 
 def model_spec(cfg, stored=False):
@@ -331,11 +332,21 @@ def run_mlt(args, cfg):
         cfg["r_w"] = search_rw(cfg, link_gbs, host_gbs, pk, tp, per_slice_host=args.tp_shard > 1)
         log(f"[bench] rank {rank}: weight codec on, r_w {cfg['r_w']:.2f} (search on {CODEC_DT:.4f} B/weight)")
     t = time.perf_counter()
-    rt = Runtime(model_spec(cfg), policy(cfg), budget_bytes=cfg["budget"],
-                 max_ctx=cfg["prompt"] + args.warmup + args.steps + 8, vocab=cfg["vocab"],
-                 device=local, exact_gates=args.gates == "exact", tp_rank=shard_rank, tp_size=tp,
-                 nccl_id=nid, schedule=args.schedule, tp_shard_only=args.tp_shard > 1,
-                 weight_codec=bool(cfg.get("codec")), pdl=not args.no_pdl)
+    while True:
+        try:
+            rt = Runtime(model_spec(cfg), policy(cfg), budget_bytes=cfg["budget"],
+                         max_ctx=cfg["prompt"] + args.warmup + args.steps + 8, vocab=cfg["vocab"],
+                         device=local, exact_gates=args.gates == "exact", tp_rank=shard_rank, tp_size=tp,
+                         nccl_id=nid, schedule=args.schedule, tp_shard_only=args.tp_shard > 1,
+                         weight_codec=bool(cfg.get("codec")), pdl=not args.no_pdl)
+            break
+        except capi.MltError as e:
+            # the searched r_w assumes an even shard; the largest uneven h2 shard
+            # (DBRX tp=8) or the arena extras may not fit: step r_w down
+            if not (cfg.get("codec") and "budget" in str(e) and cfg["r_w"] > 0.01):
+                raise
+            cfg["r_w"] = round(cfg["r_w"] - 0.01, 2)
+            log(f"[bench] rank {rank}: {e}; retrying with r_w {cfg['r_w']:.2f}")
     info = rt.info
     log(f"[bench] rank {rank}: runtime ready in {time.perf_counter() - t:.1f}s (weights gen "
         f"{info.gen_seconds:.1f}s, pin {info.pin_seconds:.1f}s), r_w achieved "
