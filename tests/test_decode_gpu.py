@@ -243,3 +243,20 @@ def test_weight_codec_decode_bitwise_equal(prompt, dims, r_w, a_g, budget):
     assert np.array_equal(x0.view(np.uint32), x1.view(np.uint32))
     if r_w < 1.0:
         assert s1 < 0.8 * s0 and b1 < 0.8 * b0
+
+
+def test_tp_shard_only_measurement_mode(prompt):
+    """tp_shard_only: one rank's shard of a tp=2 job runs alone (all-reduce
+    elided): it decodes, streams half of each layer's paged bytes, and its
+    measured timeline still verifies.  (Values are partial sums by design.)"""
+    model = _model(TINY)
+    full = Runtime(model, capi.Policy(N, MU, 0, 1, 0.0, 0.0), budget_bytes=4e9, max_ctx=64, vocab=VOCAB, seed=1234)
+    shard = Runtime(model, capi.Policy(N, MU, 0, 1, 0.0, 0.0), budget_bytes=4e9, max_ctx=64, vocab=VOCAB, seed=1234,
+                    tp_rank=1, tp_size=2, tp_shard_only=True)
+    for rt in (full, shard):
+        rt.prefill_synthetic(PROMPT, 9012)
+    d = shard.decode(prompt[0], 3)
+    assert d.report.timeline_ok == 1 and d.ids.shape == (3, N)
+    assert shard.info.streamed_bytes_per_layer == pytest.approx(full.info.streamed_bytes_per_layer / 2, rel=0.02)
+    full.close()
+    shard.close()

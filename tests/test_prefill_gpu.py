@@ -159,3 +159,30 @@ def test_prefill_small_chunks(a_g):
     residual/KV copies and chunk metadata alternate within a layer."""
     rep = _run(TINY, 0.25 if a_g == 0 else 0.0, a_g, 4e9, LENS, chunk=32)
     assert rep.chunk_tokens == 32 and rep.chunks_per_layer >= 4
+
+
+@pytest.mark.parametrize("a_g,r_w", [(0, 0.3), (1, 1.0)])
+def test_prefill_with_weight_codec_bitwise_equal(a_g, r_w):
+    """GPU prefill on encoded weights: same first tokens, same KV cache bits and
+    same decode continuation as on bf16 tiles."""
+    dims = (1024, 3584, 8, 2)
+    lens = [17, 40, 33, 8, 56, 1, 25, 48]
+    prompts = _prompts(lens)
+    outs = []
+    for codec in (False, True):
+        rt = Runtime(capi.ModelSpec(2, *dims, 8, 2, 2.0, 2.0), capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0),
+                     budget_bytes=4e9, max_ctx=CTX, vocab=VOCAB, seed=1234, weight_codec=codec)
+        first, _ = rt.prefill(prompts)
+        if a_g:  # paged pool [layer][seq][page][kv_head][16][d]: pages past a prompt hold stale bytes
+            kv = [rt.debug_read(n, np.uint16).reshape(2, N, CTX // 16, dims[3], 16, 128) for n in ("kpool", "vpool")]
+            kv = [np.concatenate([a[:, q, :(lens[q] + 15) // 16].reshape(2, -1) for q in range(N)], axis=1)
+                  for a in kv]
+        else:  # host cache [layer][seq][kv_head][ctx][d]: compare the prompt positions only
+            kv = [rt.debug_read(n, np.uint16).reshape(2, N, dims[3], CTX, 128) for n in ("kcache", "vcache")]
+            kv = [np.concatenate([a[:, q, :, :lens[q]].reshape(2, -1) for q in range(N)], axis=1) for a in kv]
+        nxt = rt.decode(first, 3)
+        outs.append((first.copy(), kv, nxt.ids.copy()))
+        rt.close()
+    (f0, kv0, n0), (f1, kv1, n1) = outs
+    assert np.array_equal(f0, f1) and np.array_equal(n0, n1)
+    assert all(np.array_equal(a, b) for a, b in zip(kv0, kv1))
