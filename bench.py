@@ -338,7 +338,8 @@ def run_mlt(args, cfg):
                          max_ctx=cfg["prompt"] + args.warmup + args.steps + 8, vocab=cfg["vocab"],
                          device=local, exact_gates=args.gates == "exact", tp_rank=shard_rank, tp_size=tp,
                          nccl_id=nid, schedule=args.schedule, tp_shard_only=args.tp_shard > 1,
-                         weight_codec=bool(cfg.get("codec")), pdl=not args.no_pdl)
+                         weight_codec=bool(cfg.get("codec")), pdl=not args.no_pdl,
+                         host_threads=args.host_threads)
             break
         except capi.MltError as e:
             # the searched r_w assumes an even shard; the largest uneven h2 shard
@@ -499,6 +500,8 @@ def main():
                     help="no programmatic dependent launch on all-GPU schedules (per-kernel event breakdown)")
     ap.add_argument("--tp-shard", type=int, default=0,
                     help="measure the largest shard of a T-way TP job alone on one GPU (all-reduce elided)")
+    ap.add_argument("--host-threads", type=int, default=0,
+                    help="host attention threads (0 = all cores but two, split across co-located ranks)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     rw0 = cfg["r_w"] if not isinstance(cfg["r_w"], dict) else min(cfg["r_w"].values())

@@ -264,6 +264,20 @@ int mlt_pack_weight(const uint16_t* host_src, int64_t M, int64_t K, uint16_t* ho
 int mlt_codec_encode(const uint8_t* host_packed, int64_t M, int64_t K, uint8_t* host_out);
 int mlt_codec_decode(const uint8_t* host_enc, int64_t tiles, uint8_t* host_packed);
 int mlt_codec_tile_bytes(void);
+/* Host-core GQA decode attention (A_g = 0: the CpuAttn task, pipesim.hpp:26,
+ * PAPER.md:390-392/553; cost model cpu_attention, planner.cpp:42-44) — the
+ * runtime's CpuAttn kernel on caller buffers.  q [T][nq][d] bf16 (roped);
+ * kc, vc [T][nkv][max_ctx][d] bf16 (one contiguous stream per sequence and
+ * kv head); ctx[t] in [1, max_ctx] valid rows; out [T][nq][d] bf16.  d must
+ * be 128, nq % nkv == 0, nq / nkv <= 16.  threads <= 0: all host cores. */
+int mlt_host_gqa_decode(const uint16_t* host_q, const uint16_t* host_k, const uint16_t* host_v,
+                        const int32_t* host_ctx, int T, int nq, int nkv, int d, int max_ctx,
+                        uint16_t* host_out, int threads);
+/* Select the host GQA path process-wide: enable != 0 -> the AMX tile path
+ * when the CPU has AMX-BF16 and the OS grants the tile state, else the
+ * AVX-512 path.  Returns 1 if AMX is in use afterwards, 0 otherwise (never
+ * an error).  Default: AMX when available (env MLT_HOST_AMX=0 disables). */
+int mlt_host_gqa_use_amx(int enable);
 /* Host: packed activation rows (capacity R) -> row-major bf16 [rows, K]. */
 int mlt_unpack_rows(const uint8_t* host_packed, int64_t R, int64_t rows, int64_t K,
                     uint16_t* host_dst);

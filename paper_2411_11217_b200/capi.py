@@ -477,6 +477,8 @@ _KSIGS = {
     "pack_weight": [V, C.c_int64, C.c_int64, V],
     "codec_encode": [V, C.c_int64, C.c_int64, V],
     "codec_decode": [V, C.c_int64, V],
+    "host_gqa_decode": [V, V, V, V, I, I, I, I, I, V, I],
+    "host_gqa_use_amx": [I],
     "unpack_rows": [V, C.c_int64, C.c_int64, C.c_int64, V],
     "pack_rows_host": [V, C.c_int64, C.c_int64, C.c_int64, V],
     "gemm": [C.POINTER(GemmArgs), V],

@@ -1,6 +1,8 @@
 // C ABI over the sm_100a kernels (include/mlt.h, "Kernel-level entry
 // points").  Thin: argument checks, cudaError -> MLT_ERR_CUDA, no hidden
 // allocation except mlt_expert_ffn's (none: all buffers caller-owned).
+#include <immintrin.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -13,6 +15,7 @@
 
 #include "../kernels/kernels.hpp"
 #include "../runtime/host_layout.hpp"
+#include "../runtime/host_gqa.hpp"
 #include "../runtime/weight_codec.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
@@ -108,6 +111,20 @@ int mlt_codec_decode(const uint8_t* enc, int64_t tiles, uint8_t* packed) {
 }
 
 int mlt_codec_tile_bytes(void) { return mlt::kCodecTileBytes; }
+
+int mlt_host_gqa_use_amx(int enable) { return mlt::host_gqa_set_amx(enable != 0) ? 1 : 0; }
+
+int mlt_host_gqa_decode(const uint16_t* q, const uint16_t* kc, const uint16_t* vc, const int32_t* ctx, int T,
+                        int nq, int nkv, int d, int max_ctx, uint16_t* out, int threads) {
+    return guard([&] {
+        if (d != 128 || nkv <= 0 || nq % nkv || nq / nkv > 16 || T < 0 || max_ctx <= 0)
+            throw std::invalid_argument("host_gqa_decode: d == 128, nq % nkv == 0, nq / nkv <= 16");
+        for (int t = 0; t < T; ++t)
+            if (ctx[t] < 1 || ctx[t] > max_ctx) throw std::invalid_argument("host_gqa_decode: 1 <= ctx[t] <= max_ctx");
+        mlt::host_gqa_decode(q, kc, vc, ctx, T, nq, nkv, max_ctx, out, threads);
+        return MLT_OK;
+    });
+}
 
 int mlt_unpack_rows(const uint8_t* packed, int64_t R, int64_t rows, int64_t K, uint16_t* dst) {
     return guard([&] {
@@ -362,24 +379,43 @@ int mlt_measure_link(int device, size_t bytes, int reps, double out[3]) {
     });
 }
 
+// Read: 64-byte vector loads into four independent accumulators per thread
+// (a scalar `sum += a[i]` chain is add-latency bound, not DRAM bound, and
+// under-reports the host by ~2x); copy: plain vectorised loop.  Pages are
+// first-touched by the threads that read them.
 int mlt_measure_host_bw(size_t bytes, double out[2]) {
     return guard([&] {
-        const size_t n = bytes / 8;
-        std::vector<double> a(n, 1.0), b(n, 0.0);
+        const size_t n = bytes / 64 * 16;  // floats, whole 64-byte lines
+        float* a = static_cast<float*>(std::aligned_alloc(64, n * 4));
+        float* b = static_cast<float*>(std::aligned_alloc(64, n * 4));
+        if (!a || !b) {
+            std::free(a);
+            std::free(b);
+            throw std::runtime_error("measure_host_bw: allocation failed");
+        }
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < static_cast<int64_t>(n); ++i) a[i] = 1.0f, b[i] = 0.0f;
         double best_read = 0, best_copy = 0;
         for (int rep = 0; rep < 3; ++rep) {
-            double sum = 0;
+            float sum = 0;
             auto t0 = std::chrono::steady_clock::now();
 #pragma omp parallel for reduction(+ : sum) schedule(static)
-            for (int64_t i = 0; i < static_cast<int64_t>(n); ++i) sum += a[i];
+            for (int64_t i = 0; i < static_cast<int64_t>(n); i += 64) {
+                __m512 s0 = _mm512_load_ps(a + i), s1 = _mm512_load_ps(a + i + 16);
+                s0 = _mm512_add_ps(s0, _mm512_load_ps(a + i + 32));
+                s1 = _mm512_add_ps(s1, _mm512_load_ps(a + i + 48));
+                sum += _mm512_reduce_add_ps(_mm512_add_ps(s0, s1));
+            }
             auto t1 = std::chrono::steady_clock::now();
 #pragma omp parallel for schedule(static)
-            for (int64_t i = 0; i < static_cast<int64_t>(n); ++i) b[i] = a[i];
+            for (int64_t i = 0; i < static_cast<int64_t>(n); i += 16) _mm512_store_ps(b + i, _mm512_load_ps(a + i));
             auto t2 = std::chrono::steady_clock::now();
             if (sum < 0) throw std::runtime_error("unreachable");
-            best_read = std::max(best_read, n * 8.0 / std::chrono::duration<double>(t1 - t0).count() / 1e9);
-            best_copy = std::max(best_copy, n * 16.0 / std::chrono::duration<double>(t2 - t1).count() / 1e9);
+            best_read = std::max(best_read, n * 4.0 / std::chrono::duration<double>(t1 - t0).count() / 1e9);
+            best_copy = std::max(best_copy, n * 8.0 / std::chrono::duration<double>(t2 - t1).count() / 1e9);
         }
+        std::free(a);
+        std::free(b);
         out[0] = best_read;
         out[1] = best_copy;
         return MLT_OK;

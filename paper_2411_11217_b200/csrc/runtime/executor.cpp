@@ -194,8 +194,10 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
     std::array<std::vector<int>, lightplan::sim::kResourceCount> fifo;
     for (int i = 0; i < n; ++i) fifo[static_cast<int>(dag.tasks[i].resource)].push_back(i);
 
+    host_cores_ = host_cores(shard_.rank, opt_.tp_shard_only ? 1 : shard_.size);
     auto worker = [&](Resource r) {
         try {
+            if (r != Resource::Cpu) pin_thread(host_cores_.launch);
             const cudaStream_t st = stream(r);
             ck(cudaSetDevice(opt_.device), "set device");
             for (int i : fifo[static_cast<int>(r)]) {

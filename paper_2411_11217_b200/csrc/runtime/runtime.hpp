@@ -21,6 +21,7 @@
 
 #include "collective.hpp"
 #include "exec_plan.hpp"
+#include "host_gqa.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
 
@@ -195,6 +196,7 @@ class Runtime {
     // this rank's shard (exec_plan.hpp Shard)
     int N_, mu_, M_, H_, F_, E_, K_, nq_, nkv_, d_, W_, V_, L_, Ho_;
     Shard shard_;
+    HostCores host_cores_;  // launcher / attention cores of the current decode
     std::unique_ptr<Collective> coll_;
     float* d_cbuf_ = nullptr;  // [mu, H] TP expert-combine partial (all-reduced)
     int Rmu_, Re_, ncap_, ncap_e_;
