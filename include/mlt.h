@@ -94,6 +94,24 @@ const char* mlt_last_error(void);
 int mlt_last_status(void);
 const char* mlt_version(void);
 
+/* ParsedConfig (config.hpp:89-94 of the reference). */
+typedef struct mlt_config_t {
+    mlt_hardware_spec_t hardware;
+    mlt_model_spec_t model;
+    mlt_workload_spec_t workload;
+    mlt_policy_t policy;
+    int32_t has_policy;
+} mlt_config_t;
+
+/* parse_config_text (config.hpp:116): INI text -> config.  MLT_OK, or
+ * MLT_ERR_INVALID with *err_line = the 1-based line of a parse error (0: not
+ * tied to a line, e.g. a missing section) or -1 for validation issues, and
+ * the message (ConfigParseError::message / format_issues) in msg. */
+int mlt_parse_config(const char* text, mlt_config_t* out, int32_t* err_line, char* msg, size_t msg_cap);
+/* serialize_config (config.hpp:121): writes at most cap bytes (NUL-terminated)
+ * and the full length to *len. */
+int mlt_serialize_config(const mlt_config_t* config, char* buf, size_t cap, size_t* len);
+
 /* validate(HardwareSpec/ModelSpec/WorkloadSpec/Policy), config.hpp:75-78.
  * Any pointer may be NULL (skipped).  Returns the number of issues (>= 0);
  * the formatted issue list (format_issues) is written to msg. */

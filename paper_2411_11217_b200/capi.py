@@ -171,9 +171,27 @@ TASK_KINDS = ["pre_attn", "offload_qkv", "cpu_attn", "load_hidden", "post_attn",
 RESOURCES = ["gpu", "cpu", "h2d", "d2h", "ctopin"]
 
 P = C.POINTER
+class Config(C.Structure):
+    """ParsedConfig (reference config.hpp:89-94); has_policy = the optional [policy]."""
+    _fields_ = [("hardware", HardwareSpec), ("model", ModelSpec), ("workload", WorkloadSpec),
+                ("policy", Policy), ("has_policy", C.c_int32)]
+
+
+class ConfigError(ValueError):
+    """parse_config_text failure: line >= 1 a parse error on that line, 0 a
+    file-level parse error (missing section/key), -1 validation issues."""
+
+    def __init__(self, line: int, message: str):
+        super().__init__(f"line {line}: {message}" if line > 0 else message)
+        self.line, self.message = line, message
+
+
 _SIGS = {
     "last_error": (C.c_char_p, []),
+    "parse_config": (C.c_int, [C.c_char_p, P(Config), P(C.c_int32), C.c_char_p, C.c_size_t]),
+    "serialize_config": (C.c_int, [P(Config), C.c_char_p, C.c_size_t, P(C.c_size_t)]),
     "last_status": (C.c_int, []),
+    "version": (C.c_char_p, []),
     "op_profiles": (C.c_int, [P(ModelSpec), C.c_double, C.c_double, C.c_double, P(OpProfile)]),
     "layer_weight_bytes": (C.c_int, [P(ModelSpec), P(LayerWeightBytes)]),
     "transfer_sizes": (C.c_int, [P(ModelSpec), P(Policy), C.c_double, P(TransferSizes)]),
@@ -300,6 +318,9 @@ class Api:
     def error(self) -> str:
         return (self.fn["last_error"]() or b"").decode()
 
+    def version(self) -> str:
+        return (self.fn["version"]() or b"").decode() if "version" in self.fn else ""
+
     def check(self, rc: int) -> int:
         if rc < 0:
             raise _EXC.get(rc, MltError)(rc, self.error())
@@ -369,6 +390,31 @@ class Api:
                                             C.byref(grid) if grid is not None else None, objective,
                                             ctx_override, C.byref(out)))
         return out
+
+    # --- INI config (config.hpp:80-121) -----------------------------------
+    def parse_config(self, text: str) -> Config:
+        out, line = Config(), C.c_int32(0)
+        buf = C.create_string_buffer(4096)
+        rc = self.fn["parse_config"](text.encode(), C.byref(out), C.byref(line), buf, 4096)
+        if rc == -1:
+            raise ConfigError(line.value, buf.value.decode())
+        self.check(rc)
+        return out
+
+    def parse_config_file(self, path: str) -> Config:
+        try:
+            with open(path, "rb") as fh:
+                text = fh.read().decode("utf-8", "surrogateescape")
+        except OSError:
+            raise ConfigError(0, "cannot open config file: " + path) from None
+        return self.parse_config(text)
+
+    def serialize_config(self, cfg: Config) -> str:
+        n = C.c_size_t(0)
+        self.check(self.fn["serialize_config"](C.byref(cfg), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self.check(self.fn["serialize_config"](C.byref(cfg), buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
 
     def validate(self, hw=None, model=None, workload=None, policy=None):
         """Reference config.hpp validate(): the list of issue lines ([] = valid)."""

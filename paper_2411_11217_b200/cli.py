@@ -1,0 +1,247 @@
+"""Command line over the planner and the B200 decode runtime, driven by the
+reference's own INI config files (the plan -> execute
+loop).
+
+  python -m paper_2411_11217_b200 plan    --config X.cfg [--out DIR] [--objective tokens-per-sec]
+                                          [--ctx C] [--mu-list 32,64] [--max-n-ub 8] [--tp T]
+  python -m paper_2411_11217_b200 latency --config X.cfg [--out DIR] [--ctx C] [--tp T]
+  python -m paper_2411_11217_b200 run     --config X.cfg [--out DIR] [--steps 8] [--codec auto|on|off]
+                                          [--mu-list 32,64,128,256] [--vocab 32000]
+
+`plan` and `latency` follow the reference subcommands (cli.cpp:262-324): the
+search / cost model on the config's [hardware], plan.json / latency.json with
+the same body (policy, latency{comm,t_cpu,t_gpu,t_layer}, memory, throughput,
+objective).  `run` is the B200 step: the same search on THIS machine's
+measured spec (host link and DRAM read measured live, HBM and tensor peaks
+from MEASURED_PEAKS.json) with the config's m_g as the GPU budget, restricted
+to the policies the runtime executes (F_g = 1; A_g = 1 keeps KV resident),
+then executes the picked policy on the GPU for a few decode steps and reports
+measured tok/s against the HRM bound of that policy.
+
+Exit status: 0 ok, 2 usage / config errors, 3 no feasible policy (as the
+reference CLI).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+from . import capi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0}  # B200_PROFILING.md fallback
+HOST_FLOPS = 2.0e12   # host-core estimate (the measured box: 16 SPR cores)
+CODEC_DT = 12432 / 8192  # stored bytes per weight with the weight codec
+
+
+class CliError(Exception):
+    def __init__(self, status: int, message: str):
+        super().__init__(message)
+        self.status = status
+
+
+def arena_extra_bytes(hidden: int, vocab: int) -> float:
+    """Arena bytes the ModelSpec does not model: embedding + lm_head (vocab x h1
+    bf16 each) and ~0.2 GB of activations, page tables and KV-independent buffers."""
+    return 2 * vocab * hidden * 2 + 0.2e9
+
+
+def _load(api, path):
+    try:
+        return api.parse_config_file(path)
+    except capi.ConfigError as e:
+        raise CliError(2, f"{path}: {e}") from None
+
+
+def _policy_json(p):
+    return {"N": p.batch, "mu": p.micro_batch, "A_g": int(p.attn_on_gpu), "F_g": int(p.ffn_on_gpu),
+            "r_w": p.weights_on_gpu, "r_c": p.kv_on_gpu}
+
+
+def plan_body(plan) -> dict:
+    """emit_plan_body (cli.cpp:92-111)."""
+    b = plan.breakdown
+    return {"policy": _policy_json(plan.policy),
+            "latency": {"comm": b.link_upload, "t_cpu": b.cpu_total(), "t_gpu": b.gpu_total(),
+                        "t_layer": b.layer_total},
+            "memory": {"gpu_bytes": plan.memory.gpu_bytes, "cpu_bytes": plan.memory.cpu_bytes,
+                       "feasible": bool(plan.memory.feasible)},
+            "throughput": {"decode": plan.decode_throughput, "generation": plan.generation_throughput},
+            "objective": plan.objective}
+
+
+def _grid(mu_list: str, max_n_ub: int, attn=(0, 1), ffn=(0, 1), rc=None, min_n_ub=1):
+    """grid_from_flags (cli.cpp:199-209) over SearchGrid::defaults (planner.cpp:164-180)."""
+    mu = sorted(set([1 << i for i in range(11)] + list(range(4, 257, 4))))
+    if mu_list:
+        try:
+            mu = [int(x) for x in mu_list.split(",") if x]
+        except ValueError:
+            raise CliError(2, f"expected a comma-separated list of positive integers, got '{mu_list}'") from None
+        if any(v < 1 for v in mu):
+            raise CliError(2, f"expected a comma-separated list of positive integers, got '{mu_list}'")
+    counts = list(range(min_n_ub, (max_n_ub if max_n_ub > 0 else 32) + 1))
+    ratios = [i * 0.05 for i in range(21)]
+    return capi.make_grid(mu, counts, ratios, ratios if rc is None else rc, attn=attn, ffn=ffn)
+
+
+def _objective(name: str) -> int:
+    if name == "tokens-per-sec":
+        return 0
+    if name == "layer-latency":
+        return 1
+    raise CliError(2, "--objective must be tokens-per-sec or layer-latency")
+
+
+def _write(out_dir, name, doc):
+    text = json.dumps(doc, indent=1) + "\n"
+    if out_dir:
+        os.makedirs(out_dir, exist_ok=True)
+        with open(os.path.join(out_dir, name), "w") as fh:
+            fh.write(text)
+    sys.stdout.write(text)
+
+
+def cmd_plan(a) -> int:
+    api = capi.load_product()
+    cfg = _load(api, a.config)
+    hw = api.apply_tensor_parallelism(cfg.hardware, a.tp) if a.tp > 1 else cfg.hardware
+    try:
+        plan = api.search_policy(hw, cfg.model, cfg.workload, _grid(a.mu, a.max_n_ub),
+                                 objective=_objective(a.objective), ctx_override=a.ctx)
+    except capi.NoFeasiblePolicyError as e:
+        raise CliError(3, str(e)) from None
+    except capi.MltError as e:
+        raise CliError(2, str(e)) from None
+    doc = {"manifest": {"command": "plan", "config": a.config, "objective": a.objective,
+                        "version": api.version()}}
+    doc.update(plan_body(plan))
+    _write(a.out, "plan.json", doc)
+    return 0
+
+
+def cmd_latency(a) -> int:
+    api = capi.load_product()
+    cfg = _load(api, a.config)
+    if not cfg.has_policy:
+        raise CliError(2, f"{a.config}: latency needs a [policy] section")
+    hw = api.apply_tensor_parallelism(cfg.hardware, a.tp) if a.tp > 1 else cfg.hardware
+    ctx = a.ctx if a.ctx > 0 else cfg.workload.prompt_len + cfg.workload.gen_len / 2.0
+    try:
+        plan = api.estimate_throughput(hw, cfg.model, cfg.workload, cfg.policy)
+        plan.breakdown = api.layer_latency(hw, cfg.model, cfg.workload, cfg.policy, ctx)
+    except capi.MltError as e:
+        raise CliError(2, str(e)) from None
+    doc = {"manifest": {"command": "latency", "config": a.config, "ctx": ctx, "version": api.version()}}
+    doc.update(plan_body(plan))
+    _write(a.out, "latency.json", doc)
+    return 0
+
+
+def measured_spec(api, budget: float, cpu_mem: float, hidden: int, vocab: int, device: int = 0):
+    """This machine as a HardwareSpec: link and host DRAM measured now, HBM and
+    tensor peaks from MEASURED_PEAKS.json (else the profiling guide's fallback)."""
+    link = (C.c_double * 3)()
+    f = api.lib.mlt_measure_link
+    f.restype, f.argtypes = C.c_int, [C.c_int, C.c_size_t, C.c_int, C.POINTER(C.c_double)]
+    api.check(f(device, 1 << 30, 5, link))
+    host = (C.c_double * 2)()
+    g = api.lib.mlt_measure_host_bw
+    g.restype, g.argtypes = C.c_int, [C.c_size_t, C.POINTER(C.c_double)]
+    api.check(g(4 << 30, host))
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    pk, src = (json.load(open(p)), "measured") if os.path.exists(p) else (PEAKS_FALLBACK, "fallback")
+    tflops = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    hw = capi.HardwareSpec(budget - arena_extra_bytes(hidden, vocab), cpu_mem, pk["hbm_gbs"] * 1e9,
+                           host[0] * 1e9, link[0] * 1e9, tflops * 1e12, HOST_FLOPS)
+    return hw, {"link_gbs": link[0], "host_read_gbs": host[0], "peaks": src}
+
+
+def cmd_run(a) -> int:
+    import numpy as np
+
+    from .runtime import Runtime
+    api = capi.load_product()
+    cfg = _load(api, a.config)
+    m = cfg.model
+    budget = cfg.hardware.gpu_mem_bytes
+    hw, meas = measured_spec(api, budget, cfg.hardware.cpu_mem_bytes, m.hidden_dim, a.vocab)
+    best, codec = None, None
+    for use_codec in ({"on": (True,), "off": (False,), "auto": (False, True)}[a.codec]):
+        stored = capi.ModelSpec(m.layers, m.hidden_dim, m.ffn_dim, m.q_heads, m.kv_heads, m.experts, m.top_k,
+                                CODEC_DT if use_codec else 2.0, m.kv_dtype_bytes)
+        # the runtime executes F_g = 1, and A_g = 1 only with the KV resident
+        # (r_c = 1).  Host attention needs >= 2 micro-batches: the HRM's max over
+        # resources assumes CpuAttn(j) overlaps GPU work of other micro-batches,
+        # which n_ub = 1 does not have (8x7B @64 GB codec, mu = 256, n_ub = 1:
+        # 63 % of its bound measured vs 94 % at mu = 64, profiles/r01_hrm_sweep_codec.json)
+        for attn, rc, n0 in ((0, [0.0], 2), (1, [1.0], 1)):
+            try:
+                g = _grid(a.mu, a.max_n_ub, attn=(attn,), ffn=(1,), rc=rc, min_n_ub=n0)
+                p = api.search_policy(hw, stored, cfg.workload, g)
+            except capi.MltError:
+                continue
+            if best is None or p.objective > best.objective:
+                best, codec = p, use_codec
+    if best is None:
+        raise CliError(3, "no feasible policy for this machine within the config's m_g")
+    pol = best.policy
+    steps = max(1, min(a.steps, cfg.workload.gen_len))
+    prompt = cfg.workload.prompt_len
+    model = capi.ModelSpec(m.layers, m.hidden_dim, m.ffn_dim, m.q_heads, m.kv_heads, m.experts, m.top_k,
+                           2.0, 2.0)
+    t = time.perf_counter()
+    rt = Runtime(model, pol, budget_bytes=budget, max_ctx=prompt + steps + a.warmup + 8, vocab=a.vocab,
+                 weight_codec=codec)
+    setup = time.perf_counter() - t
+    rt.prefill_synthetic(prompt, 9012)
+    toks = np.random.default_rng(5678).integers(0, a.vocab, pol.batch, dtype=np.int32)
+    w = rt.decode(toks, a.warmup) if a.warmup > 0 else None
+    d = rt.decode(w.ids[-1] if w is not None else toks, steps)
+    rep = d.report
+    measured = pol.batch * steps / rep.seconds
+    doc = {"manifest": {"command": "run", "config": a.config, "version": api.version(),
+                        "machine": meas, "weight_codec": bool(codec)}}
+    doc.update(plan_body(best))
+    doc["measured"] = {"decode_tok_s": measured, "frac_of_hrm_bound": measured / best.decode_throughput,
+                       "steps": steps, "warmup": a.warmup, "seconds": rep.seconds,
+                       "steady_layer_ms": rep.steady_layer_time * 1e3,
+                       "r_w_achieved": rt.info.achieved_weight_ratio, "timeline_ok": bool(rep.timeline_ok),
+                       "utilization": dict(zip(["gpu", "cpu", "h2d", "d2h", "ctopin"], list(rep.utilization))),
+                       "setup_s": setup, "data": "synthetic weights and prompt KV (no checkpoints offline)"}
+    rt.close()
+    _write(a.out, "run.json", doc)
+    return 0
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="python -m paper_2411_11217_b200", description=__doc__.split("\n\n")[0])
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    for name in ("plan", "latency", "run"):
+        s = sub.add_parser(name)
+        s.add_argument("--config", required=True)
+        s.add_argument("--out", default=None)
+        s.add_argument("--ctx", type=float, default=-1.0)
+        s.add_argument("--tp", type=int, default=1)
+        s.add_argument("--mu-list", "--mu", dest="mu", default="" if name != "run" else "32,64,128,256")
+        s.add_argument("--max-n-ub", type=int, default=0)
+        s.add_argument("--objective", default="tokens-per-sec")
+        if name == "run":
+            s.add_argument("--steps", type=int, default=8)
+            s.add_argument("--warmup", type=int, default=2)
+            s.add_argument("--codec", default="auto", choices=["auto", "on", "off"])
+            s.add_argument("--vocab", type=int, default=32000)
+    a = ap.parse_args(argv)
+    try:
+        return {"plan": cmd_plan, "latency": cmd_latency, "run": cmd_run}[a.cmd](a)
+    except CliError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return e.status
+
+
+if __name__ == "__main__":
+    sys.exit(main())
