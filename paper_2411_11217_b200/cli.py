@@ -7,6 +7,9 @@ loop).
   python -m paper_2411_11217_b200 latency --config X.cfg [--out DIR] [--ctx C] [--tp T]
   python -m paper_2411_11217_b200 run     --config X.cfg [--out DIR] [--steps 8] [--codec auto|on|off]
                                           [--mu-list 64,128,256] [--vocab 32000]
+  python -m paper_2411_11217_b200 batch   --requests R.csv|R.jsonl --n-ub U --ubs B --gen-len G
+                                          --cache-size C [--no-flush] [--out DIR]
+  python -m paper_2411_11217_b200 serve   --config X.cfg --requests R.csv|R.jsonl [--out DIR]
 
 `plan` and `latency` follow the reference subcommands (cli.cpp:262-324): the
 search / cost model on the config's [hardware], plan.json / latency.json with
@@ -17,6 +20,13 @@ from MEASURED_PEAKS.json) with the config's m_g as the GPU budget, restricted
 to the policies the runtime executes (F_g = 1; A_g = 1 keeps KV resident),
 then executes the picked policy on the GPU for a few decode steps and reports
 measured tok/s against the HRM bound of that policy.
+
+`batch` is the reference's balanced micro-batching (cli.cpp:398-442,
+batcher.cpp:7-57); `serve` feeds its variable-length micro-batches to the
+runtime: n_ub micro-batches of up to mu requests form
+one N-sequence batch (empty slots padded with 1-token prompts whose output is
+discarded), GPU prefill of the ragged prompts, then gen_len greedy tokens per
+request, and reports useful generated tokens per second.
 
 Exit status: 0 ok, 2 usage / config errors, 3 no feasible policy (as the
 reference CLI).
@@ -254,9 +264,151 @@ def cmd_run(a) -> int:
     return 0
 
 
+def load_requests(path: str):
+    """load_requests (cli.cpp:211-250): `id,input_len` CSV lines or JSONL
+    objects with "id" and "input_len"; blank lines skipped."""
+    out = []
+    try:
+        fh = open(path)
+    except OSError:
+        raise CliError(2, "cannot open requests file: " + path) from None
+    with fh:
+        for no, line in enumerate(fh, 1):
+            t = line.lstrip(" \t\r").rstrip("\n")
+            if not t.strip(" \t\r"):
+                continue
+            if t.startswith("{"):
+                try:
+                    row = json.loads(t)
+                    rid = row["id"] if isinstance(row["id"], str) else json.dumps(row["id"])
+                    out.append((rid, int(row["input_len"])))
+                except (ValueError, KeyError, TypeError):
+                    raise CliError(2, f'{path}:{no}: expected {{"id":..., "input_len":...}}') from None
+            else:
+                if "," not in t:
+                    raise CliError(2, f"{path}:{no}: expected `id,input_len`")
+                rid, n = t.split(",", 1)
+                try:
+                    if n != n.strip() or not n.lstrip("-").isdigit():
+                        raise ValueError
+                    out.append((rid, int(n)))
+                except ValueError:
+                    raise CliError(2, f"{path}:{no}: input_len must be an integer, got '{n}'") from None
+    return out
+
+
+def _batch(api, requests, n_ub, ubs, gen_len, cache_size, flush=True):
+    try:
+        return api.batch_requests(requests, n_ub, ubs, gen_len, cache_size, flush)
+    except capi.MltError as e:
+        raise CliError(2, str(e)) from None
+
+
+def cmd_batch(a) -> int:
+    api = capi.load_product()
+    reqs = load_requests(a.requests)
+    mbs, aborted = _batch(api, reqs, a.n_ub, a.ubs, a.gen_len, a.cache_size, not a.no_flush)
+    lens = dict(reqs)
+    doc = {"manifest": {"command": "batch", "requests": a.requests, "version": api.version()},
+           "micro_batches": mbs, "aborted": aborted, "sums": [sum(lens[r] for r in mb) for mb in mbs]}
+    _write(a.out, "batch.json", doc)
+    return 0
+
+
+def cmd_serve(a) -> int:
+    import numpy as np
+
+    from .runtime import Runtime
+    api = capi.load_product()
+    cfg = _load(api, a.config)
+    if not cfg.has_policy:
+        raise CliError(2, f"{a.config}: serve needs a [policy] section (N, mu, A_g, r_w; `run` picks one)")
+    pol, m = cfg.policy, cfg.model
+    if not pol.ffn_on_gpu or (pol.attn_on_gpu and pol.kv_on_gpu < 1.0):
+        raise CliError(2, "the runtime executes F_g = 1, and A_g = 1 only with r_c = 1")
+    reqs = load_requests(a.requests)
+    if not reqs:
+        raise CliError(2, f"{a.requests}: no requests")
+    gen = int(cfg.workload.gen_len)
+    lens = dict(reqs)
+    max_ctx = a.max_ctx if a.max_ctx > 0 else max(lens.values()) + gen + 8
+    mu, n_ub = int(pol.micro_batch), int(pol.micro_batch_count())
+    # a micro-batch holds at most mu requests whose prompts + generations fit
+    # mu KV streams of max_ctx slots
+    mbs, aborted = _batch(api, reqs, n_ub, mu, gen, mu * (max_ctx - 8))
+    over = [r for mb in mbs for r in mb if lens[r] + gen > max_ctx - 8]
+    aborted += over
+    mbs = [[r for r in mb if r not in over] for mb in mbs]
+    mbs = [mb for mb in mbs if mb]
+    model = capi.ModelSpec(m.layers, m.hidden_dim, m.ffn_dim, m.q_heads, m.kv_heads, m.experts, m.top_k, 2.0, 2.0)
+    t = time.perf_counter()
+    rt = Runtime(model, pol, budget_bytes=cfg.hardware.gpu_mem_bytes, max_ctx=max_ctx, vocab=a.vocab,
+                 weight_codec=a.codec == "on" or (a.codec == "auto" and pol.weights_on_gpu < 1.0))
+    setup = time.perf_counter() - t
+    import zlib
+    outputs, batches = {}, []
+    t_pre = t_dec = 0.0
+    for b0 in range(0, len(mbs), n_ub):
+        group = mbs[b0:b0 + n_ub]
+        slots = []  # request id or None per sequence, micro-batch major
+        for j in range(n_ub):
+            mb = group[j] if j < len(group) else []
+            slots += list(mb) + [None] * (mu - len(mb))
+        # prompt ids per request from (seed, crc32(id)): independent of batch composition
+        prompts = [np.random.default_rng([a.seed, zlib.crc32(r.encode())]).integers(0, a.vocab, lens[r], dtype=np.int32)
+                   if r else np.zeros(1, np.int32) for r in slots]
+        t0 = time.perf_counter()
+        first, prep = rt.prefill(prompts)
+        t1 = time.perf_counter()
+        ids = [first]
+        tok, left = first, gen - 1
+        while left > 0:
+            k = min(left, 64)
+            d = rt.decode(tok, k)
+            ids.append(d.ids)
+            tok, left = d.ids[-1], left - k
+        t2 = time.perf_counter()
+        t_pre += t1 - t0
+        t_dec += t2 - t1
+        allids = np.vstack([i.reshape(-1, len(slots)) for i in ids])  # [gen, N]
+        for q, r in enumerate(slots):
+            if r is not None:
+                outputs[r] = allids[:, q].tolist()
+        batches.append({"requests": sum(r is not None for r in slots), "prompt_tokens": int(prep.prompt_tokens),
+                        "prefill_s": t1 - t0, "decode_s": t2 - t1})
+    rt.close()
+    useful = gen * len(outputs)
+    doc = {"manifest": {"command": "serve", "config": a.config, "requests": a.requests, "version": api.version(),
+                        "policy": _policy_json(pol), "max_ctx": max_ctx, "setup_s": setup,
+                        "data": "synthetic weights; prompt ids per request from (seed %d, crc32(id))" % a.seed},
+           "served": len(outputs), "aborted": aborted, "batches": batches,
+           "generated_tokens": useful, "prefill_s": t_pre, "decode_s": t_dec,
+           "tok_s": useful / (t_pre + t_dec), "decode_tok_s": useful / t_dec if t_dec > 0 else None,
+           "outputs": outputs if a.keep_outputs else None}
+    _write(a.out, "serve.json", doc)
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2411_11217_b200", description=__doc__.split("\n\n")[0])
     sub = ap.add_subparsers(dest="cmd", required=True)
+    b = sub.add_parser("batch")
+    b.add_argument("--requests", required=True)
+    b.add_argument("--out", default=None)
+    b.add_argument("--n-ub", type=int, required=True)
+    b.add_argument("--ubs", type=int, required=True)
+    b.add_argument("--gen-len", type=int, required=True)
+    b.add_argument("--cache-size", type=int, required=True)
+    b.add_argument("--no-flush", action="store_true")
+    v = sub.add_parser("serve")
+    v.add_argument("--config", required=True)
+    v.add_argument("--requests", required=True)
+    v.add_argument("--out", default=None)
+    v.add_argument("--max-ctx", type=int, default=0)
+    v.add_argument("--vocab", type=int, default=32000)
+    v.add_argument("--seed", type=int, default=5678)
+    v.add_argument("--codec", default="auto", choices=["auto", "on", "off"])
+    v.add_argument("--keep-outputs", action="store_true")
     for name in ("plan", "latency", "run"):
         s = sub.add_parser(name)
         s.add_argument("--config", required=True)
@@ -277,7 +429,8 @@ def main(argv=None) -> int:
             s.add_argument("--vocab", type=int, default=32000)
     a = ap.parse_args(argv)
     try:
-        return {"plan": cmd_plan, "latency": cmd_latency, "run": cmd_run}[a.cmd](a)
+        return {"plan": cmd_plan, "latency": cmd_latency, "run": cmd_run, "batch": cmd_batch,
+                "serve": cmd_serve}[a.cmd](a)
     except CliError as e:
         print(f"error: {e}", file=sys.stderr)
         return e.status

@@ -72,3 +72,41 @@ def test_identical_runs_identical_artifacts(toy, tmp_path):
         assert rc == 0, err
         outs.append((tmp_path / d / "plan.json").read_bytes())
     assert outs[0] == outs[1]
+
+
+def test_batch_command_matches_reference_batcher(tmp_path, ref):
+    """`batch` (cli.cpp:398-442) on CSV and JSONL request files = the compiled
+    reference's batch_requests on the same queue."""
+    csv = tmp_path / "r.csv"
+    csv.write_text("a,77\nb,418\n\nc,242\n  d,256\ne,1693\n")
+    jl = tmp_path / "r.jsonl"
+    jl.write_text('{"id": "j1", "input_len": 40}\n{"id": 7, "input_len": 90}\n')
+    for path, reqs in ((csv, [("a", 77), ("b", 418), ("c", 242), ("d", 256), ("e", 1693)]),
+                       (jl, [("j1", 40), ("7", 90)])):
+        rc, _, err = run_cli("batch", "--requests", str(path), "--n-ub", "2", "--ubs", "2", "--gen-len", "8",
+                             "--cache-size", "1200", "--out", str(tmp_path / "o"))
+        assert rc == 0, err
+        doc = json.loads((tmp_path / "o" / "batch.json").read_text())
+        mbs, aborted = ref.batch_requests(reqs, 2, 2, 8, 1200, True)
+        assert doc["micro_batches"] == mbs and doc["aborted"] == aborted
+        lens = dict(reqs)
+        assert doc["sums"] == [sum(lens[r] for r in mb) for mb in mbs]
+
+
+def test_batch_command_errors(tmp_path):
+    bad = tmp_path / "bad.csv"
+    bad.write_text("a,77\nb;418\n")
+    rc, _, err = run_cli("batch", "--requests", str(bad), "--n-ub", "2", "--ubs", "2", "--gen-len", "8",
+                         "--cache-size", "1200")
+    assert rc == 2 and "bad.csv:2" in err
+    bad.write_text("a,7x\n")
+    rc, _, err = run_cli("batch", "--requests", str(bad), "--n-ub", "2", "--ubs", "2", "--gen-len", "8",
+                         "--cache-size", "1200")
+    assert rc == 2 and "input_len must be an integer" in err
+    assert run_cli("batch", "--requests", "/nonexistent", "--n-ub", "1", "--ubs", "1", "--gen-len", "1",
+                   "--cache-size", "4")[0] == 2
+    ok = tmp_path / "ok.csv"
+    ok.write_text("a,7\n")
+    rc, _, err = run_cli("batch", "--requests", str(ok), "--n-ub", "0", "--ubs", "1", "--gen-len", "1",
+                         "--cache-size", "4")
+    assert rc == 2  # InvalidBatchParametersError
