@@ -23,10 +23,12 @@ measured tok/s against the HRM bound of that policy.
 
 `batch` is the reference's balanced micro-batching (cli.cpp:398-442,
 batcher.cpp:7-57); `serve` feeds its variable-length micro-batches to the
-runtime: n_ub micro-batches of up to mu requests form
-one N-sequence batch (empty slots padded with 1-token prompts whose output is
-discarded), GPU prefill of the ragged prompts, then gen_len greedy tokens per
-request, and reports useful generated tokens per second.
+runtime: each batch_requests call fills the n_ub
+partitions (micro-batches of up to mu requests) of one N-sequence batch and
+the requests it could not place go to the next call; empty slots are padded
+with 1-token prompts whose output is discarded.  Per batch: GPU prefill of the
+ragged prompts, then gen_len greedy tokens per request; reports useful
+generated tokens per second.
 
 Exit status: 0 ok, 2 usage / config errors, 3 no feasible policy (as the
 reference CLI).
@@ -335,11 +337,20 @@ def cmd_serve(a) -> int:
     mu, n_ub = int(pol.micro_batch), int(pol.micro_batch_count())
     # a micro-batch holds at most mu requests whose prompts + generations fit
     # mu KV streams of max_ctx slots
-    mbs, aborted = _batch(api, reqs, n_ub, mu, gen, mu * (max_ctx - 8))
-    over = [r for mb in mbs for r in mb if lens[r] + gen > max_ctx - 8]
-    aborted += over
-    mbs = [[r for r in mb if r not in over] for mb in mbs]
-    mbs = [mb for mb in mbs if mb]
+    # requests whose prompt + generation exceed one KV stream are unservable
+    aborted = [r for r, n in reqs if n + gen > max_ctx - 8]
+    queue = [(r, n) for r, n in reqs if n + gen <= max_ctx - 8]
+    # one batch_requests call fills the n_ub open partitions of ONE batch and
+    # returns the rest as aborted (batcher.cpp:7-57): re-queue them per batch
+    rounds = []
+    while queue:
+        mbs, rest = _batch(api, queue, n_ub, mu, gen, mu * (max_ctx - 8))
+        if not mbs:
+            aborted += rest
+            break
+        rounds.append(mbs)
+        left = set(rest)
+        queue = [(r, n) for r, n in queue if r in left]
     model = capi.ModelSpec(m.layers, m.hidden_dim, m.ffn_dim, m.q_heads, m.kv_heads, m.experts, m.top_k, 2.0, 2.0)
     t = time.perf_counter()
     rt = Runtime(model, pol, budget_bytes=cfg.hardware.gpu_mem_bytes, max_ctx=max_ctx, vocab=a.vocab,
@@ -348,8 +359,7 @@ def cmd_serve(a) -> int:
     import zlib
     outputs, batches = {}, []
     t_pre = t_dec = 0.0
-    for b0 in range(0, len(mbs), n_ub):
-        group = mbs[b0:b0 + n_ub]
+    for group in rounds:
         slots = []  # request id or None per sequence, micro-batch major
         for j in range(n_ub):
             mb = group[j] if j < len(group) else []
