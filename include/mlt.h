@@ -443,6 +443,10 @@ typedef struct mlt_runtime_options_t {
                                  from HBM; mlt_codec_encode); numerics unchanged bit for bit */
     int32_t disable_pdl;      /* 1: no programmatic dependent launch (all-GPU schedules use it by
                                  default; per-kernel CUDA-event breakdowns need it off) */
+    int32_t expert_down_splits; /* K-splits of the expert down GEMM (fp32 partials summed in part
+                                 order by the combine): 0 = auto (with weight_codec, the split
+                                 in 1..8 that best fills the last wave of SMs; 1 without), else
+                                 explicit; results are bit-identical for equal splits */
 } mlt_runtime_options_t;
 
 /* ncclUniqueId for a tensor-parallel group (call on rank 0, broadcast). */

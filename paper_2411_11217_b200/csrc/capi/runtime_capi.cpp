@@ -62,6 +62,7 @@ mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p
         opt.tp_shard_only = o->tp_shard_only != 0;
         opt.weight_codec = o->weight_codec != 0;
         opt.pdl = o->disable_pdl == 0;
+        opt.expert_down_splits = o->expert_down_splits;
         auto hh = std::make_unique<Handle>();
         hh->rt = std::make_unique<mlt::Runtime>(ms, ext, pol, opt);
         h = hh.release();

@@ -207,7 +207,7 @@ template <int K>
 __global__ void __launch_bounds__(768) combine_kernel(const float* h, const float* y, int ldy,
                                                       const int32_t* inv, const float* w, int H,
                                                       float* x, const uint16_t* gamma, float eps,
-                                                      uint8_t* xn, int R) {
+                                                      uint8_t* xn, int R, int n_parts, int64_t pstride) {
     pdl_trigger();  // dependents may launch; our inputs: after the wait
     pdl_wait();
     __shared__ float red[32];
@@ -215,6 +215,16 @@ __global__ void __launch_bounds__(768) combine_kernel(const float* h, const floa
     float ys[K][8];  // every slot row's loads issued before the sum
 #pragma unroll
     for (int s = 0; s < K; ++s) load_row8(y + static_cast<int64_t>(inv[t * K + s]) * ldy + i, ys[s]);
+    // split-K partials of the down GEMM: summed in part order (deterministic)
+    for (int p = 1; p < n_parts; ++p) {
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            float v[8];
+            load_row8(y + p * pstride + static_cast<int64_t>(inv[t * K + s]) * ldy + i, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ys[s][j] += v[j];
+        }
+    }
     float r[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (h) load_row8(h + static_cast<int64_t>(t) * H + i, r);
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -344,14 +354,16 @@ cudaError_t launch_rope_qkv(const float* qkv, int parts, int64_t part_stride, co
 
 cudaError_t launch_moe_combine(const float* h, const float* y, int ldy, const int32_t* inv,
                                const float* w, int T, int H, int K, float* x, cudaStream_t s,
-                               const uint16_t* gamma, float eps, uint8_t* xn, int R) {
+                               const uint16_t* gamma, float eps, uint8_t* xn, int R, int n_parts,
+                               int64_t part_stride) {
     if (T <= 0) return cudaSuccess;
-    if (H % 256 || H > 6144 || ldy % 4 || (gamma && (!xn || R < T))) return cudaErrorInvalidValue;
+    if (H % 256 || H > 6144 || ldy % 4 || (gamma && (!xn || R < T)) || n_parts < 1 || part_stride % 4)
+        return cudaErrorInvalidValue;
     switch (K) {  // x = h + sum of K slot rows (slot order)
-        case 1: return launch_k(combine_kernel<1>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R);
-        case 2: return launch_k(combine_kernel<2>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R);
-        case 4: return launch_k(combine_kernel<4>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R);
-        case 8: return launch_k(combine_kernel<8>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R);
+        case 1: return launch_k(combine_kernel<1>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R, n_parts, part_stride);
+        case 2: return launch_k(combine_kernel<2>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R, n_parts, part_stride);
+        case 4: return launch_k(combine_kernel<4>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R, n_parts, part_stride);
+        case 8: return launch_k(combine_kernel<8>, dim3(T), dim3(H / 8), 0, s, h, y, ldy, inv, w, H, x, gamma, eps, xn, R, n_parts, part_stride);
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -113,7 +113,7 @@ cudaError_t launch_moe_permute(const int32_t* topk_idx, const uint16_t* hn, int 
 cudaError_t launch_moe_combine(const float* h, const float* y, int ldy, const int32_t* inv,
                                const float* topk_w, int T, int H, int K, float* x_out,
                                cudaStream_t s, const uint16_t* gamma = nullptr, float eps = 0.f,
-                               uint8_t* xn = nullptr, int R = 0);
+                               uint8_t* xn = nullptr, int R = 0, int n_parts = 1, int64_t part_stride = 0);
 
 // out[i] = sum_p parts[p*stride + i] (+ add[i]); n % 4 == 0.  Fixed order.
 cudaError_t launch_sum_parts(const float* parts, int n_parts, int64_t stride, const float* add,

@@ -210,7 +210,25 @@ void Runtime::allocate() {
     d_inv_ = static_cast<int32_t*>(A.alloc(mu_ * K_ * 4, "inv"));
     d_xe_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Re_) * H_ * 2, "expert_in"));
     d_inter_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Re_) * F_ * 2, "expert_inter"));
-    d_y_ = static_cast<float*>(A.alloc(static_cast<size_t>(Re_) * H_ * 4, "expert_out"));
+    // expert down GEMM split-K: with encoded weights each SM's tile rate is
+    // bound by its decoders, so the SMs idle in a partial last wave are lost
+    // time (8x7B: 8 x 32 row blocks = 1.73 waves of 148 SMs -> 86 % fill;
+    // 4 splits: 6.92 waves -> 99 %); bf16 tiles are HBM-bound and need none
+    down_splits_ = opt_.expert_down_splits;
+    if (down_splits_ <= 0) {
+        down_splits_ = 1;
+        if (opt_.weight_codec) {
+            const int tiles = E_ * (H_ / 128);
+            double best = 0;
+            for (int s = 1; s <= 8 && (F_ / 64) / s >= 8; ++s) {
+                const double waves = static_cast<double>(tiles) * s / num_sms_;
+                const double fill = waves / std::ceil(waves);
+                if (fill > best + 1e-9) best = fill, down_splits_ = s;
+            }
+        }
+    }
+    if (down_splits_ > 8 || (F_ / 64) < down_splits_) throw std::invalid_argument("expert_down_splits must be <= 8 and <= h2/64");
+    d_y_ = static_cast<float*>(A.alloc(static_cast<size_t>(down_splits_) * Re_ * H_ * 4, "expert_out"));
     d_logits_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * V_ * 4, "logits"));
     d_tok_in_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4, "tok_in"));
     d_tok_out_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4, "tok_out"));
@@ -632,19 +650,24 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     dn.n_cap = ncap_e_;
     dn.out_f32 = d_y_;
     dn.ldo = H_;
+    dn.k_splits = down_splits_;
+    dn.split_stride = static_cast<int64_t>(Re_) * H_;
     dn.timing = ktimer("expert_down_gemm");
     dn.codec = opt_.weight_codec ? 1 : 0;
     kl("expert_down_gemm", mltk::launch_gemm(dn, num_sms_, s_gpu_));
     if (coll_) {
         // TP all-reduce #2: x = h + sum over ranks of this rank's top-k combine (h2 shard)
-        kl("moe_combine", mltk::launch_moe_combine(nullptr, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, d_cbuf_, s_gpu_));
+        kl("moe_combine", mltk::launch_moe_combine(nullptr, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, d_cbuf_, s_gpu_,
+                                                   nullptr, 0.f, nullptr, 0, down_splits_,
+                                                   static_cast<int64_t>(Re_) * H_));
         coll_->all_reduce_sum(d_cbuf_, static_cast<size_t>(mu_) * H_, s_gpu_);
         kl("residual_add", mltk::launch_sum_parts(d_cbuf_, 1, 0, d_h_, x, static_cast<int64_t>(mu_) * H_, s_gpu_));
     } else {
         // + the next layer's attention norm (or the final norm) fused
         kl("moe_combine", mltk::launch_moe_combine(d_h_, d_y_, H_, d_inv_, d_topw_, mu_, H_, K_, x, s_gpu_,
                                                    layer == L_ ? d_final_norm_ : d_attn_norm_[l + 1],
-                                                   ext_.rms_eps, xn, Rmu_));
+                                                   ext_.rms_eps, xn, Rmu_, down_splits_,
+                                                   static_cast<int64_t>(Re_) * H_));
     }
     if (layer == L_) {  // step epilogue: final norm -> lm_head -> greedy ids
         if (coll_)

@@ -47,6 +47,7 @@ struct RuntimeOptions {
     bool tp_shard_only = false;    // one shard alone on this GPU, all-reduce elided (measurement)
     bool weight_codec = false;     // store/stream/read projection + expert weights encoded (weight_codec.hpp)
     bool pdl = true;               // programmatic dependent launch on all-GPU (resident, A_g = 1) schedules
+    int expert_down_splits = 0;    // 0: auto (codec: best last-wave fill in 1..8; raw: 1)
     int schedule = -1;             // -1: CGOPipe (S4 when A_g = 1); else a ScheduleKind to execute
     int prefill_chunk_tokens = 0;  // 0: largest prefill chunk the budget allows
 };
@@ -201,6 +202,7 @@ class Runtime {
     float* d_cbuf_ = nullptr;  // [mu, H] TP expert-combine partial (all-reduced)
     int Rmu_, Re_, ncap_, ncap_e_;
     int num_sms_ = 148;
+    int down_splits_ = 1;  // K-splits of the expert down GEMM (partials in d_y_)
 
     std::unique_ptr<Arena> arena_;
     // weights

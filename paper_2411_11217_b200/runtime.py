@@ -23,7 +23,7 @@ class RuntimeOptions(C.Structure):
                 ("seed", C.c_uint64), ("exact_gates", C.c_int32), ("tp_rank", C.c_int32),
                 ("tp_size", C.c_int32), ("nccl_id", C.c_uint8 * 128), ("schedule", C.c_int32),
                 ("prefill_chunk_tokens", C.c_int32), ("tp_shard_only", C.c_int32),
-                ("weight_codec", C.c_int32), ("disable_pdl", C.c_int32)]
+                ("weight_codec", C.c_int32), ("disable_pdl", C.c_int32), ("expert_down_splits", C.c_int32)]
 
 
 def nccl_unique_id() -> bytes:
@@ -100,7 +100,7 @@ class Runtime:
                  rope_theta: float = 1e6, lm_head_scale: float = 4.0, exact_gates: bool = True,
                  tp_rank: int = 0, tp_size: int = 1, nccl_id: bytes = b"", schedule: str = "auto",
                  prefill_chunk_tokens: int = 0, tp_shard_only: bool = False, weight_codec: bool = False,
-                 pdl: bool = True):
+                 pdl: bool = True, down_splits: int = 0):
         self.api, self.f = _fns()
         self.model, self.policy = model, policy
         nid = (C.c_uint8 * 128)(*(nccl_id.ljust(128, b"\0")[:128]))
@@ -108,7 +108,8 @@ class Runtime:
                                    vocab, rms_eps, rope_theta, lm_head_scale, seed,
                                    int(exact_gates), tp_rank, tp_size, nid,
                                    -1 if schedule == "auto" else capi.SCHED[schedule],
-                                   prefill_chunk_tokens, int(tp_shard_only), int(weight_codec), int(not pdl))
+                                   prefill_chunk_tokens, int(tp_shard_only), int(weight_codec), int(not pdl),
+                                   down_splits)
         self.h = self.f["runtime_create"](C.byref(model), C.byref(policy), C.byref(self.opts))
         if not self.h:
             code = self.api.fn["last_status"]()

@@ -231,7 +231,8 @@ def test_weight_codec_decode_bitwise_equal(prompt, dims, r_w, a_g, budget):
     out = []
     for codec in (False, True):
         rt = Runtime(_model(dims), capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0), budget_bytes=budget,
-                     max_ctx=64, vocab=VOCAB, seed=1234, weight_codec=codec)
+                     max_ctx=64, vocab=VOCAB, seed=1234, weight_codec=codec,
+                     down_splits=4)  # equal down-GEMM K-splits: the codec's auto split, forced on both
         first = rt.decode(prompt[0], PROMPT, forced=prompt)
         rest = rt.decode(first.ids[-1], 8)
         out.append((first.ids.copy(), rest.ids.copy(), rt.residual().copy(), rt.info.streamed_bytes_per_layer,

@@ -171,7 +171,8 @@ def test_prefill_with_weight_codec_bitwise_equal(a_g, r_w):
     outs = []
     for codec in (False, True):
         rt = Runtime(capi.ModelSpec(2, *dims, 8, 2, 2.0, 2.0), capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0),
-                     budget_bytes=4e9, max_ctx=CTX, vocab=VOCAB, seed=1234, weight_codec=codec)
+                     budget_bytes=4e9, max_ctx=CTX, vocab=VOCAB, seed=1234, weight_codec=codec,
+                     down_splits=4)  # equal down-GEMM K-splits: the codec's auto split, forced on both
         first, _ = rt.prefill(prompts)
         if a_g:  # paged pool [layer][seq][page][kv_head][16][d]: pages past a prompt hold stale bytes
             kv = [rt.debug_read(n, np.uint16).reshape(2, N, CTX // 16, dims[3], 16, 128) for n in ("kpool", "vpool")]
