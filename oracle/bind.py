@@ -1,8 +1,9 @@
 """TEST INFRASTRUCTURE — ctypes binding of the CPU numerical oracle
 (oracle/liboracle.so, oracle_numerics.c).  Importable only by tests/,
 __graft_entry__.smoke() and bench.py's CPU legs; the product never loads it.
-Numerics parity is UNPINNED (the reference has no numerical path; see
-oracle_numerics.h)."""
+The reference has no numerical path; the numerics are pinned against
+transformers' MixtralForCausalLM golden vectors (tests/test_oracle_golden_hf.py,
+see oracle_numerics.h)."""
 from __future__ import annotations
 
 import ctypes as C

@@ -1,7 +1,7 @@
 /*
  * TEST INFRASTRUCTURE — CPU numerical oracle (see oracle_numerics.h for the
- * scope statement: numerics parity is UNPINNED because the reference has no
- * numerical path).  Every function cites the paper / reference line it
+ * scope statement: the reference has no numerical path, so the numerics are
+ * pinned against transformers' Mixtral, tests/test_oracle_golden_hf.py).  Every function cites the paper / reference line it
  * restates.  Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may
  * load this library.
  */

@@ -1,10 +1,14 @@
 /*
  * TEST INFRASTRUCTURE — CPU numerical oracle for the MoE decode hot path.
  *
- * PARITY UNPINNED (numerics): the reference artifact (/root/reference/proj,
- * "lightplan") contains no numerical forward pass, no kernels and no golden
- * tensors (proj/README.md:25), and no third-party arithmetic
- * dependency is vendored.  This file restates the decode step from the
+ * NUMERICS PINNED EXTERNALLY, NOT BY THE REFERENCE: the reference artifact
+ * (/root/reference/proj, "lightplan") contains no numerical forward pass, no
+ * kernels and no golden tensors (proj/README.md:25), and no
+ * third-party arithmetic dependency is vendored.  The oracle is instead pinned
+ * against Hugging Face transformers' MixtralForCausalLM on its own synthetic
+ * weights (tests/golden/mixtral_hf_tiny.npz from tools/make_golden_mixtral.py,
+ * tests/test_oracle_golden_hf.py) and against numpy restatements per block
+ * (tests/test_oracle_pins.py).  This file restates the decode step from the
  * paper (PAPER.md:143-167 MoE semantics, :385-392 task split) plus public
  * Mixtral conventions (RMSNorm eps 1e-5, rotate-half RoPE theta 1e6, fp32
  * router softmax over the top-k logits, SiLU-gated experts).  It is only
