@@ -529,9 +529,14 @@ HostCores host_cores(int rank, int sharing) {
         hc.attn = all;
         return hc;
     }
-    hc.launch.assign(all.begin(), all.begin() + 2);
-    const int per = std::max(1, static_cast<int>(all.size() - 2) / std::max(1, sharing));
-    const int first = 2 + (rank % std::max(1, sharing)) * per;
+    static const int nl = [] {
+        const char* e = std::getenv("MLT_LAUNCH_CORES");
+        const int v = e ? std::atoi(e) : 2;
+        return v < 1 ? 1 : v > 4 ? 4 : v;
+    }();
+    hc.launch.assign(all.begin(), all.begin() + nl);
+    const int per = std::max(1, static_cast<int>(all.size() - nl) / std::max(1, sharing));
+    const int first = nl + (rank % std::max(1, sharing)) * per;
     for (int i = 0; i < per && first + i < static_cast<int>(all.size()); ++i) hc.attn.push_back(all[first + i]);
     hc.pinned = true;
     return hc;
