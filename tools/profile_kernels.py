@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--with-h2d", action="store_true", help="run a concurrent H2D copy stream")
     ap.add_argument("--codec", action="store_true", help="encoded weight tiles (decoder warps in the GEMM)")
+    ap.add_argument("--down-splits", type=int, default=0,
+                    help="K-splits of the down GEMM (0: the runtime's auto choice, 4 with --codec at 8x7B)")
     a = ap.parse_args()
     mu = a.mu
     KD = capi.load_kernels()
@@ -89,7 +91,8 @@ def main():
     inv = torch.zeros(mu * K, dtype=torch.int32, device="cuda")
     xp = torch.zeros(R * H, dtype=torch.int16, device="cuda")
     inter = torch.zeros(R * F, dtype=torch.int16, device="cuda")
-    y = torch.zeros(R, H, device="cuda")
+    ds = a.down_splits or (4 if a.codec else 1)  # runtime.cpp expert_down_splits auto (8 x 32 tiles, 148 SMs)
+    y = torch.zeros(ds * R, H, device="cuda")
     xo = torch.zeros(mu, H, device="cuda")
     Rmu = (mu + 15) // 16 * 16
     xn = torch.zeros(Rmu * H, dtype=torch.int16, device="cuda")
@@ -108,11 +111,12 @@ def main():
                             out_packed=inter.data_ptr(), out_R=R, codec=int(a.codec))
     dn_args = capi.GemmArgs(a_table=t2.data_ptr(), n_mats=1, G=E, RB=H // 128, K=F, b=inter.data_ptr(), R=R,
                             b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=0, alpha=1.0,
-                            out_f32=y.data_ptr(), ldo=H, codec=int(a.codec))
+                            out_f32=y.data_ptr(), ldo=H, codec=int(a.codec), k_splits=ds, split_stride=R * H)
 
     def expert():
         KD.gemm(C.byref(gu_args), s)
         KD.gemm(C.byref(dn_args), s)
+        # (timing tool: the C ABI's combine sums split 0 only; the runtime's sums all ds parts)
         KD.moe_combine(ptr(hbuf), ptr(y), H, ptr(inv), ptr(wts), mu, H, K, ptr(xo), s)
 
     def tiling(rb):  # runtime.cpp dense_tiling
