@@ -41,7 +41,8 @@ def main():
                 while not stop.is_set():
                     dst.copy_(src, non_blocking=True)
                     s.synchronize()
-        threading.Thread(target=pump, daemon=True).start()
+        pump_thread = threading.Thread(target=pump, daemon=True)
+        pump_thread.start()
         time.sleep(1.0)
     k = capi.load_kernels()
     T, nq, nkv, d, L = a.T, 32, 8, 128, a.ctx
@@ -68,6 +69,7 @@ def main():
               f"{kv_bytes / best / 1e9 / th:6.2f} GB/s/thread", flush=True)
     if stop is not None:
         stop.set()
+        pump_thread.join()
     return res
 
 
