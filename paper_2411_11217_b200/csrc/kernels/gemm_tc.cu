@@ -152,6 +152,42 @@ __device__ __forceinline__ void store_tile(const TileIn& in, uint32_t d, int dt)
     }
 }
 
+// Virtual task v -> (group, row block, token chunk, k-block range).  With
+// the stream-K tail enabled, tasks past sk_full are (tail tile, K part).
+struct VTask {
+    int g, rb, c, kb0, kb1, part, tile;
+};
+__device__ __forceinline__ VTask vtask(const GemmArgs& a, int v, int KB) {
+    VTask t;
+    int u, ks, S;
+    t.part = -1;
+    t.tile = 0;
+    if (a.sk_parts && v >= a.sk_full) {
+        const int w = v - a.sk_full;
+        t.tile = w / a.sk_parts;
+        t.part = w % a.sk_parts;
+        u = a.sk_full + t.tile;
+        ks = t.part;
+        S = a.sk_parts;
+    } else {
+        ks = v % a.k_splits;
+        u = v / a.k_splits;
+        S = a.k_splits;
+    }
+    t.c = u % a.n_chunks;
+    t.g = (u / a.n_chunks) % a.G;
+    t.rb = u / a.n_chunks / a.G;
+    t.kb0 = ks * KB / S;
+    t.kb1 = (ks + 1) * KB / S;
+    return t;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1 KiB alignment for the SWIZZLE_128B atoms.
@@ -212,7 +248,7 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
     if (tr && threadIdx.x == 0) tr[1] = globaltimer();
 
     // virtual tile = (row block, group, N-chunk, K-split), K-split fastest
-    const int n_virtual = a.G * a.RB * a.n_chunks * a.k_splits;
+    const int n_virtual = a.sk_parts ? a.sk_full + a.sk_tail * a.sk_parts : a.G * a.RB * a.n_chunks * a.k_splits;
     const int KB = a.K / kBlockK;
 
     if (warp == 0) {
@@ -222,9 +258,8 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
             int stage = 0, kstep = 0;
             uint32_t phase = 0;
             for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-                const int ks = v % a.k_splits, u = v / a.k_splits;
-                const int c = u % a.n_chunks, g = (u / a.n_chunks) % a.G, rb = u / a.n_chunks / a.G;
-                const int kb0 = ks * KB / a.k_splits, kb1 = (ks + 1) * KB / a.k_splits;
+                const VTask tk = vtask(a, v, KB);
+                const int c = tk.c, g = tk.g, rb = tk.rb, kb0 = tk.kb0, kb1 = tk.kb1;
                 const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
                 if (rows <= 0) continue;
                 const int row0 = a.b_off ? a.b_off[g] : 0;
@@ -263,9 +298,8 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
         int acc = 0, kstep = 0;
         uint32_t acc_phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-            const int ks = v % a.k_splits, u = v / a.k_splits;
-            const int c = u % a.n_chunks, g = (u / a.n_chunks) % a.G;
-            const int kb0 = ks * KB / a.k_splits, kb1 = (ks + 1) * KB / a.k_splits;
+            const VTask tk = vtask(a, v, KB);
+            const int c = tk.c, g = tk.g, kb0 = tk.kb0, kb1 = tk.kb1;
             const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
             if (rows <= 0) continue;
             for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
@@ -316,9 +350,8 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
         int stage = 0, kstep = 0;
         uint32_t phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-            const int ks = v % a.k_splits, u = v / a.k_splits;
-            const int c = u % a.n_chunks, g = (u / a.n_chunks) % a.G;
-            const int kb0 = ks * KB / a.k_splits, kb1 = (ks + 1) * KB / a.k_splits;
+            const VTask tk = vtask(a, v, KB);
+            const int c = tk.c, g = tk.g, kb0 = tk.kb0, kb1 = tk.kb1;
             const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
             if (rows <= 0) continue;
             for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
@@ -355,8 +388,9 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-            const int ks = v % a.k_splits, u = v / a.k_splits;
-            const int c = u % a.n_chunks, g = (u / a.n_chunks) % a.G, rb = u / a.n_chunks / a.G;
+            const VTask tk = vtask(a, v, KB);
+            const int ks = tk.part >= 0 ? 0 : v % a.k_splits;
+            const int c = tk.c, g = tk.g, rb = tk.rb;
             const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
             if (rows <= 0) continue;
             const int row0 = a.b_off ? a.b_off[g] : 0;
@@ -422,6 +456,26 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                                 }
                             }
                             __syncwarp();
+                        } else if (tk.part >= 0) {  // stream-K part: fp32 g and u to the scratch
+                            float* const pb = a.sk_scratch + static_cast<int64_t>(tk.tile * a.sk_parts + tk.part) *
+                                                                 a.n_mats * a.sk_rows * 128;
+#pragma unroll
+                            for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+                                for (int j = 0; j < 16; ++j)
+                                    scr[j * 32 + lane] = __uint_as_float(mt ? r1[h][j] : r0[h][j]);
+                                __syncwarp();
+                                const int f = (lane & 7) * 4;
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    const int j = q * 4 + (lane >> 3);
+                                    if (c + j < nt)
+                                        *reinterpret_cast<float4*>(
+                                            pb + (static_cast<int64_t>(mt) * a.sk_rows + n0 + c + j) * 128 + quarter * 32 + f) =
+                                            *reinterpret_cast<const float4*>(scr + j * 32 + f);
+                                }
+                                __syncwarp();
+                            }
                         } else {  // kEpiSiluPacked
                             uint16_t* sb = reinterpret_cast<uint16_t*>(scr);
 #pragma unroll
@@ -446,6 +500,49 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&ctl->tempty[acc]);
                 if (++acc == acc_stages) { acc = 0; acc_phase ^= 1; }
+            }
+            if (tk.part >= 0) {
+                // arrive, wait for the tile's other parts (monotonic counter:
+                // this launch's target is the next multiple of sk_parts), then
+                // finish rows [part*rows/S, (part+1)*rows/S): every part summed
+                // in part order (deterministic), SiLU, packed bf16
+                __threadfence();
+                asm volatile("bar.sync 4, 128;" ::: "memory");  // the 4 epilogue warps' stores are fenced
+                if (warp == 2 && lane == 0) {
+                    const int old = atomicAdd(a.sk_count + tk.tile, 1);
+                    const int target = (old / a.sk_parts + 1) * a.sk_parts;
+                    while (ld_acquire(a.sk_count + tk.tile) < target) __nanosleep(64);
+                }
+                asm volatile("bar.sync 4, 128;" ::: "memory");
+                __threadfence();
+                const int S = a.sk_parts;
+                const int r0s = tk.part * rows / S, r1s = (tk.part + 1) * rows / S;
+                const float* sb = a.sk_scratch + static_cast<int64_t>(tk.tile) * S * a.n_mats * a.sk_rows * 128 +
+                                  quarter * 32 + lane;
+                const int64_t pstride = static_cast<int64_t>(a.n_mats) * a.sk_rows * 128;
+                uint16_t* st16 = reinterpret_cast<uint16_t*>(scr);
+                for (int r = r0s; r < r1s; ++r) {
+                    float gs = 0.f, us = 0.f;
+                    constexpr int kB = 8;  // loads in flight before the ordered sums
+                    for (int p0 = 0; p0 < S; p0 += kB) {
+                        float gv[kB], uv[kB];
+#pragma unroll
+                        for (int q = 0; q < kB; ++q) {
+                            const float* bp = sb + (p0 + q) * pstride + static_cast<int64_t>(r) * 128;
+                            gv[q] = p0 + q < S ? __ldcg(bp) : 0.f;
+                            uv[q] = p0 + q < S ? __ldcg(bp + static_cast<int64_t>(a.sk_rows) * 128) : 0.f;
+                        }
+#pragma unroll
+                        for (int q = 0; q < kB; ++q)
+                            if (p0 + q < S) gs += gv[q], us += uv[q];
+                    }
+                    st16[lane] = f32_to_bf16_bits(silu(gs) * us);
+                    __syncwarp();
+                    if (lane < 4)
+                        *reinterpret_cast<uint4*>(a.out_packed + b_packed_off(row0 + r, mbase + 8 * lane, a.out_R)) =
+                            *reinterpret_cast<const uint4*>(st16 + 8 * lane);
+                    __syncwarp();
+                }
             }
         }
     }
@@ -494,7 +591,21 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const int n_virtual = a.G * a.RB * a.n_chunks * a.k_splits;
+    a.sk_full = a.sk_tail = a.sk_parts = 0;
+    if (a.sk_scratch && a.sk_count && a.sk_rows > 0 && a.epi == kEpiSiluPacked && a.n_mats == 2 &&
+        a.k_splits == 1 && a.n_chunks == 1) {
+        // stream-K tail: a partial last wave of `tail` tiles would leave
+        // num_sms - tail SMs idle for one whole tile time
+        const int nv = a.G * a.RB, tail = nv % num_sms;
+        int S = tail > 0 ? num_sms / tail : 0;
+        if (S > a.K / kBlockK / 2) S = a.K / kBlockK / 2;  // parts of >= 2 k-blocks
+        if (nv > num_sms && S >= 2) {
+            a.sk_full = nv - tail;
+            a.sk_tail = tail;
+            a.sk_parts = S;
+        }
+    }
+    const int n_virtual = a.sk_parts ? a.sk_full + a.sk_tail * a.sk_parts : a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
     return launch_k(gemm_tc_kernel, dim3(grid), dim3(a.codec ? kThreadsCodec : kThreadsRaw), smem, stream, a);

@@ -47,6 +47,18 @@ struct GemmArgs {
     int ldr = 0;
     uint8_t* out_packed = nullptr;  // kEpiSiluPacked: packed B layout, capacity out_R
     int out_R = 0;
+    // stream-K tail (kEpiSiluPacked, k_splits == n_chunks == 1, only when the
+    // caller provides the scratch): the G*RB % grid tiles of a partial last
+    // wave are split along K into sk_parts parts over the whole grid; each
+    // part stores its fp32 g/u accumulators to sk_scratch, waits for the
+    // tile's other parts (all CTAs are resident: grid = #SMs, one CTA per
+    // SM), then sums every part in part order for its slice of the tile's
+    // rows and runs the SiLU epilogue.  sk_full / sk_tail / sk_parts are set
+    // by launch_gemm.
+    float* sk_scratch = nullptr;  // [grid][n_mats][sk_rows][128] fp32
+    int* sk_count = nullptr;      // [grid] monotonic arrival counters, zero-initialised once
+    int sk_rows = 0;              // row capacity per (tile, part): max rows of one group
+    int sk_full = 0, sk_tail = 0, sk_parts = 0;
     // filled by launch_gemm
     int stages = 0, acc_stages = 0, tmem_cols = 0;
 };

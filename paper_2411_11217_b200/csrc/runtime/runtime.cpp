@@ -229,6 +229,10 @@ void Runtime::allocate() {
     }
     if (down_splits_ > 8 || (F_ / 64) < down_splits_) throw std::invalid_argument("expert_down_splits must be <= 8 and <= h2/64");
     d_y_ = static_cast<float*>(A.alloc(static_cast<size_t>(down_splits_) * Re_ * H_ * 4, "expert_out"));
+    // gate/up stream-K tail (gemm_tc.cu): parts of the partial last wave's tiles
+    d_sk_scratch_ = static_cast<float*>(A.alloc(static_cast<size_t>(num_sms_) * 2 * Rmu_ * 128 * 4, "sk_scratch"));
+    d_sk_count_ = static_cast<int*>(A.alloc(static_cast<size_t>(num_sms_) * 4, "sk_count"));
+    ck(cudaMemset(d_sk_count_, 0, static_cast<size_t>(num_sms_) * 4), "sk_count");
     d_logits_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * V_ * 4, "logits"));
     d_tok_in_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4, "tok_in"));
     d_tok_out_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4, "tok_out"));
@@ -635,6 +639,9 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     gu.epi = mltk::kEpiSiluPacked;
     gu.out_packed = d_inter_;
     gu.out_R = Re_;
+    gu.sk_scratch = d_sk_scratch_;
+    gu.sk_count = d_sk_count_;
+    gu.sk_rows = Rmu_;  // a token routes to an expert at most once: rows per group <= mu
     gu.timing = ktimer("expert_gateup_gemm");
     gu.codec = opt_.weight_codec ? 1 : 0;
     kl("expert_gateup_gemm", mltk::launch_gemm(gu, num_sms_, s_gpu_));

@@ -235,6 +235,8 @@ class Runtime {
     uint8_t* d_xe_ = nullptr;           // [Re*H] packed
     uint8_t* d_inter_ = nullptr;        // [Re*F] packed
     float* d_y_ = nullptr;              // [Re, H]
+    float* d_sk_scratch_ = nullptr;  // gate/up stream-K tail: fp32 parts [#SMs][2][Rmu][128]
+    int* d_sk_count_ = nullptr;       // [#SMs] monotonic arrival counters
     float* d_logits_ = nullptr;         // [Rmu, V]
     int32_t* d_tok_in_ = nullptr;       // [max_steps][N]
     int32_t* d_tok_out_ = nullptr;      // [max_steps][N]

@@ -138,6 +138,20 @@ def test_8x7b_width_reduced_depth_greedy(prompt):
     assert ev["ids"] <= 6
 
 
+SK = (1024, 2432, 8, 2)  # 8 experts x 19 row blocks = 152 gate/up tiles: a 4-tile last wave on 148 SMs
+
+
+@pytest.mark.parametrize("r_w,a_g", [(0.0, 0), (1.0, 1)])
+def test_gateup_stream_k_tail_parity(prompt, r_w, a_g):
+    """The gate/up GEMM's stream-K tail (gemm_tc.cu: the 4 tiles of the partial
+    last wave split 8 ways along K; every part sums all parts in order for its
+    slice of rows, SiLU after) against the fp32 oracle: residual within the
+    Tiny model's bar, greedy ids equal except at bf16-vs-fp32 near-ties."""
+    rt, ev, worst = teacher_forced_parity(SK, prompt, r_w, a_g, 4e9)
+    print(f"\n[stream-K tail r_w={r_w} A_g={a_g}] teacher-forced: {ev}, worst residual {worst:.2e}")
+    assert worst <= 1e-2 and ev["ids"] <= ev["lm_tie"] + ev["router_tie"]
+
+
 def test_tiny_layer_output_within_2e2_of_fp32(prompt):
     """BASELINE item 2: layer outputs within 2e-2 relative (bf16 GPU vs fp32 CPU)."""
     from oracle import bind as orc
@@ -222,7 +236,8 @@ def test_executed_baseline_schedules_match_cgopipe(prompt):
                 vocab=VOCAB, seed=1234, schedule="s4")
 
 
-@pytest.mark.parametrize("dims,r_w,a_g,budget", [(TINY, 0.3, 0, 4e9), (TINY, 1.0, 1, 4e9), (W8X7B, 0.10, 0, 7e9)])
+@pytest.mark.parametrize("dims,r_w,a_g,budget", [(TINY, 0.3, 0, 4e9), (TINY, 1.0, 1, 4e9), (SK, 0.5, 0, 4e9),
+                                                 (W8X7B, 0.10, 0, 7e9)])
 def test_weight_codec_decode_bitwise_equal(prompt, dims, r_w, a_g, budget):
     """Decoding with encoded weights (stored, paged and read as 12432-byte
     tiles, expanded in smem by the GEMM's decoder warps) returns the same ids
