@@ -339,7 +339,7 @@ def run_mlt(args, cfg):
                          device=local, exact_gates=args.gates == "exact", tp_rank=shard_rank, tp_size=tp,
                          nccl_id=nid, schedule=args.schedule, tp_shard_only=args.tp_shard > 1,
                          weight_codec=bool(cfg.get("codec")), pdl=not args.no_pdl,
-                         host_threads=args.host_threads)
+                         host_threads=args.host_threads, down_splits=args.down_splits)
             break
         except capi.MltError as e:
             # the searched r_w assumes an even shard; the largest uneven h2 shard
@@ -500,6 +500,8 @@ def main():
                     help="no programmatic dependent launch on all-GPU schedules (per-kernel event breakdown)")
     ap.add_argument("--tp-shard", type=int, default=0,
                     help="measure the largest shard of a T-way TP job alone on one GPU (all-reduce elided)")
+    ap.add_argument("--down-splits", type=int, default=0,
+                    help="K-splits of the expert down GEMM (0 = auto: wave fill with the codec, 1 raw)")
     ap.add_argument("--host-threads", type=int, default=0,
                     help="host attention threads (0 = all cores but two, split across co-located ranks)")
     args = ap.parse_args()
