@@ -330,6 +330,10 @@ typedef struct mlt_gemm_args_t {
                                   mlt_codec_encode_tile), expanded in smem by decoder warps */
     unsigned long long* ktrace; /* optional CTA-0 pipeline trace [4][256] %globaltimer stamps per
                                    k-block: producer issue, decoder start, decoder done, MMA start */
+    float* sk_scratch;         /* optional stream-K tail for epi = 1 (n_chunks = k_splits = 1): fp32
+                                  scratch [#SMs][2][sk_rows][128]; NULL disables it */
+    int32_t* sk_count;         /* [#SMs] int32 arrival counters, zeroed once by the caller */
+    int32_t sk_rows;           /* row capacity per group for the scratch (>= max rows of a group) */
 } mlt_gemm_args_t;
 
 /* Grouped swap-AB tcgen05 GEMM (SURVEY.md §2c expert_gateup_silu /

@@ -515,7 +515,8 @@ class GemmArgs(C.Structure):
                 ("out_f32", C.c_void_p), ("ldo", C.c_int32), ("residual", C.c_void_p),
                 ("ldr", C.c_int32), ("out_packed", C.c_void_p), ("out_R", C.c_int32),
                 ("n_chunks", C.c_int32), ("k_splits", C.c_int32), ("split_stride", C.c_int64),
-                ("trace", C.c_void_p), ("codec", C.c_int32), ("ktrace", C.c_void_p)]
+                ("trace", C.c_void_p), ("codec", C.c_int32), ("ktrace", C.c_void_p),
+                ("sk_scratch", C.c_void_p), ("sk_count", C.c_void_p), ("sk_rows", C.c_int32)]
 
 
 V, I, F = C.c_void_p, C.c_int, C.c_float

@@ -73,6 +73,9 @@ mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
     g.trace = a->trace;
     g.codec = a->codec;
     g.ktrace = a->ktrace;
+    g.sk_scratch = a->sk_scratch;
+    g.sk_count = a->sk_count;
+    g.sk_rows = a->sk_rows;
     return g;
 }
 

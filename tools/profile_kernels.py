@@ -106,9 +106,13 @@ def main():
         KD.moe_permute(ptr(idx), ptr(hn), mu, H, E, K, ptr(cnt), ptr(off), ptr(perm), ptr(inv),
                        ptr(xp), R, s)
 
+    # the runtime's stream-K tail for the last wave of gate/up tiles (runtime.cpp gu.sk_*)
+    sk_scratch = torch.zeros(148 * 2 * Rmu * 128, device="cuda")
+    sk_count = torch.zeros(148, dtype=torch.int32, device="cuda")
     gu_args = capi.GemmArgs(a_table=t13.data_ptr(), n_mats=2, G=E, RB=F // 128, K=H, b=xp.data_ptr(), R=R,
                             b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=1, alpha=1.0,
-                            out_packed=inter.data_ptr(), out_R=R, codec=int(a.codec))
+                            out_packed=inter.data_ptr(), out_R=R, codec=int(a.codec),
+                            sk_scratch=sk_scratch.data_ptr(), sk_count=sk_count.data_ptr(), sk_rows=Rmu)
     dn_args = capi.GemmArgs(a_table=t2.data_ptr(), n_mats=1, G=E, RB=H // 128, K=F, b=inter.data_ptr(), R=R,
                             b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=0, alpha=1.0,
                             out_f32=y.data_ptr(), ldo=H, codec=int(a.codec), k_splits=ds, split_stride=R * H)
