@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--with-h2d", action="store_true", help="run a concurrent H2D copy stream")
     ap.add_argument("--codec", action="store_true", help="encoded weight tiles (decoder warps in the GEMM)")
+    ap.add_argument("--no-stream-k", action="store_true", help="gate/up without the stream-K tail")
     ap.add_argument("--down-splits", type=int, default=0,
                     help="K-splits of the down GEMM (0: the runtime's auto choice, 4 with --codec at 8x7B)")
     a = ap.parse_args()
@@ -112,7 +113,8 @@ def main():
     gu_args = capi.GemmArgs(a_table=t13.data_ptr(), n_mats=2, G=E, RB=F // 128, K=H, b=xp.data_ptr(), R=R,
                             b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=1, alpha=1.0,
                             out_packed=inter.data_ptr(), out_R=R, codec=int(a.codec),
-                            sk_scratch=sk_scratch.data_ptr(), sk_count=sk_count.data_ptr(), sk_rows=Rmu)
+                            sk_scratch=None if a.no_stream_k else sk_scratch.data_ptr(),
+                            sk_count=sk_count.data_ptr(), sk_rows=Rmu)
     dn_args = capi.GemmArgs(a_table=t2.data_ptr(), n_mats=1, G=E, RB=H // 128, K=F, b=inter.data_ptr(), R=R,
                             b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=0, alpha=1.0,
                             out_f32=y.data_ptr(), ldo=H, codec=int(a.codec), k_splits=ds, split_stride=R * H)
