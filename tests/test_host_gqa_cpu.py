@@ -100,3 +100,15 @@ def test_amx_and_avx512_paths_agree():
     k.host_gqa_use_amx(1)
     a, b = outs
     assert np.all(np.abs(a - b) <= 2.0 ** -7 * np.maximum(np.abs(a), np.abs(b)) + 1e-6)
+
+
+def test_host_bandwidth_probe_is_vectorised():
+    """mlt_measure_host_bw (the b_c of the B200 HardwareSpec): a 4-accumulator
+    vector read, not an add-latency-bound scalar sum — it must beat one core's
+    scalar dependent-add rate (a few GB/s) by a wide margin on any AVX-512 host."""
+    api = capi.load_product()
+    f = api.lib.mlt_measure_host_bw
+    f.restype, f.argtypes = C.c_int, [C.c_size_t, C.POINTER(C.c_double)]
+    out = (C.c_double * 2)()
+    api.check(f(256 << 20, out))
+    assert out[0] > 10.0 and out[1] > 5.0, list(out)
