@@ -157,6 +157,32 @@ int mlt_estimate_throughput(const mlt_hardware_spec_t* hw, const mlt_model_spec_
                             const mlt_workload_spec_t* workload, const mlt_policy_t* policy,
                             mlt_plan_result_t* out);
 
+/* ---- hierarchical roofline: reference hrm.hpp:13-74 ---------------------- */
+#define MLT_LEVEL_GPU 0 /* MemoryLevel::Gpu */
+#define MLT_LEVEL_CPU 1 /* MemoryLevel::Cpu */
+/* attainable_local, hrm.hpp:17 (level: MLT_LEVEL_*) */
+int mlt_hrm_attainable_local(int level, double intensity, const mlt_hardware_spec_t* hw, double* out);
+/* attainable_cross, hrm.hpp:22 */
+int mlt_hrm_attainable_cross(double gpu_intensity, double cpu_intensity, const mlt_hardware_spec_t* hw,
+                             double* out);
+/* turning_point_p1 / turning_point_p2, hrm.hpp:26-30 */
+int mlt_hrm_turning_point_p1(double cpu_intensity, const mlt_hardware_spec_t* hw, double* out);
+int mlt_hrm_turning_point_p2(double gpu_intensity, const mlt_hardware_spec_t* hw, double* out);
+/* balance_gap, hrm.hpp:34 */
+int mlt_hrm_balance_gap(double gpu_intensity, double cpu_intensity, const mlt_hardware_spec_t* hw,
+                        double* out);
+/* RooflineGrid, hrm.hpp:57-61 */
+typedef struct mlt_roofline_grid_t {
+    double min_intensity, max_intensity;
+    int32_t points_per_decade;
+} mlt_roofline_grid_t;
+/* roofline_csv(roofline_series(profiles, names, hw, grid)), hrm.hpp:66-73.
+ * grid NULL = the defaults.  Writes at most cap bytes (NUL-terminated) and
+ * the full length to *len; MLT_ERR_INVALID on empty input (std::invalid_argument). */
+int mlt_roofline_csv(const mlt_op_profile_t* profiles, const char* const* names, int n,
+                     const mlt_hardware_spec_t* hw, const mlt_roofline_grid_t* grid, char* buf, size_t cap,
+                     size_t* len);
+
 /* ---- policy search: reference planner.hpp:77-116 ------------------------- */
 typedef struct mlt_search_grid_t {
     const int64_t* micro_batch_values;

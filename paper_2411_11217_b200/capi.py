@@ -160,6 +160,15 @@ def make_grid(mu, counts, rw, rc, attn=(0, 1), ffn=(0, 1)):
     return g
 
 
+class RooflineGrid(C.Structure):
+    """RooflineGrid (reference hrm.hpp:57-61)."""
+    _fields_ = [("min_intensity", C.c_double), ("max_intensity", C.c_double),
+                ("points_per_decade", C.c_int32)]
+
+
+LEVEL_GPU, LEVEL_CPU = 0, 1  # MemoryLevel (hrm.hpp:15)
+
+
 class BatchParams(C.Structure):
     _fields_ = [("n_ub", C.c_int64), ("ubs", C.c_int64), ("gen_len", C.c_int64),
                 ("cache_size", C.c_int64), ("flush_partials", C.c_int32)]
@@ -204,6 +213,13 @@ _SIGS = {
                                            P(HardwareSpec)]),
     "estimate_throughput": (C.c_int, [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(Policy),
                                       P(PlanResult)]),
+    "hrm_attainable_local": (C.c_int, [C.c_int, C.c_double, P(HardwareSpec), P(C.c_double)]),
+    "hrm_attainable_cross": (C.c_int, [C.c_double, C.c_double, P(HardwareSpec), P(C.c_double)]),
+    "hrm_turning_point_p1": (C.c_int, [C.c_double, P(HardwareSpec), P(C.c_double)]),
+    "hrm_turning_point_p2": (C.c_int, [C.c_double, P(HardwareSpec), P(C.c_double)]),
+    "hrm_balance_gap": (C.c_int, [C.c_double, C.c_double, P(HardwareSpec), P(C.c_double)]),
+    "roofline_csv": (C.c_int, [P(OpProfile), P(C.c_char_p), C.c_int, P(HardwareSpec), P(RooflineGrid),
+                               C.c_char_p, C.c_size_t, P(C.c_size_t)]),
     "search_policy": (C.c_int, [P(HardwareSpec), P(ModelSpec), P(WorkloadSpec), P(SearchGrid),
                                 C.c_int, C.c_double, P(PlanResult)]),
     "search_candidate_count": (C.c_int64, [P(SearchGrid)]),
@@ -383,6 +399,38 @@ class Api:
         self.check(f(C.byref(tp_hw), C.byref(model), C.byref(workload), C.byref(policy), tp, nvlink_bw,
                      C.byref(out)))
         return out
+
+    # --- hierarchical roofline (hrm.hpp:13-74) ---------------------------
+    def _d(self, name, *args):
+        out = C.c_double()
+        self.check(self.fn[name](*args, C.byref(out)))
+        return out.value
+
+    def attainable_local(self, level, intensity, hw):
+        return self._d("hrm_attainable_local", level, intensity, C.byref(hw))
+
+    def attainable_cross(self, gpu_intensity, cpu_intensity, hw):
+        return self._d("hrm_attainable_cross", gpu_intensity, cpu_intensity, C.byref(hw))
+
+    def turning_point_p1(self, cpu_intensity, hw):
+        return self._d("hrm_turning_point_p1", cpu_intensity, C.byref(hw))
+
+    def turning_point_p2(self, gpu_intensity, hw):
+        return self._d("hrm_turning_point_p2", gpu_intensity, C.byref(hw))
+
+    def balance_gap(self, gpu_intensity, cpu_intensity, hw):
+        return self._d("hrm_balance_gap", gpu_intensity, cpu_intensity, C.byref(hw))
+
+    def roofline_csv(self, profiles, names, hw, grid=None) -> str:
+        n = len(profiles)
+        arr = (OpProfile * max(n, 1))(*profiles)
+        nm = (C.c_char_p * max(n, 1))(*[x.encode() for x in names])
+        ln = C.c_size_t(0)
+        g = C.byref(grid) if grid is not None else None
+        self.check(self.fn["roofline_csv"](arr, nm, n, C.byref(hw), g, None, 0, C.byref(ln)))
+        buf = C.create_string_buffer(ln.value + 1)
+        self.check(self.fn["roofline_csv"](arr, nm, n, C.byref(hw), g, buf, ln.value + 1, C.byref(ln)))
+        return buf.value.decode()
 
     def search_policy(self, hw, model, workload, grid=None, objective=0, ctx_override=-1.0):
         out = PlanResult()

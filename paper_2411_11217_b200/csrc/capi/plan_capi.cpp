@@ -5,6 +5,7 @@
 
 #include "lightplan/config.hpp"
 #include "lightplan/opcost.hpp"
+#include "lightplan/hrm.hpp"
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
 #include "lightplan/batcher.hpp"
