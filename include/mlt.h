@@ -358,7 +358,7 @@ typedef struct mlt_gemm_args_t {
                                    k-block: producer issue, decoder start, decoder done, MMA start */
     float* sk_scratch;         /* optional stream-K tail for epi = 1 (n_chunks = k_splits = 1): fp32
                                   scratch [#SMs][2][sk_rows][128]; NULL disables it */
-    int32_t* sk_count;         /* [#SMs] int32 arrival counters, zeroed once by the caller */
+    int64_t* sk_count;         /* [#SMs] 64-bit arrival counters, zeroed once by the caller */
     int32_t sk_rows;           /* row capacity per group for the scratch (>= max rows of a group) */
 } mlt_gemm_args_t;
 

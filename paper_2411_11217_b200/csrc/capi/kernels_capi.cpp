@@ -4,6 +4,7 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <vector>
@@ -34,13 +35,15 @@ void ck(cudaError_t e, const char* what) {
         throw mlt::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// SM count of the calling thread's current device (cached per device)
 int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        ck(cudaGetDevice(&dev), "cudaGetDevice");
-        ck(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
-    }
+    static std::atomic<int> cache[64] = {};
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev >= 0 && dev < 64 && cache[dev].load()) return cache[dev].load();
+    int n = 0;
+    ck(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
+    if (dev >= 0 && dev < 64) cache[dev].store(n);
     return n;
 }
 
@@ -74,7 +77,7 @@ mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
     g.codec = a->codec;
     g.ktrace = a->ktrace;
     g.sk_scratch = a->sk_scratch;
-    g.sk_count = a->sk_count;
+    g.sk_count = reinterpret_cast<unsigned long long*>(a->sk_count);
     g.sk_rows = a->sk_rows;
     return g;
 }

@@ -273,12 +273,8 @@ cudaError_t launch_g(const uint16_t* q, int ldq, const uint16_t* kp, const uint1
                      int nkv, uint8_t* out_p, int R, float* out_f, cudaStream_t s) {
     const int smem = kWarps * kStagesW * 2 * kPageBytes;
     static_assert(8 * kCombStride * 4 <= kStagesW * 2 * kPageBytes, "merge state fits a warp's ring");
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(gqa_decode_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gqa_decode_kernel<G>), smem); e != cudaSuccess)
+        return e;
     dim3 grid(T, nkv);
     return launch_k(gqa_decode_kernel<G>, dim3(grid), dim3(kWarps * 32), smem, s, q, ldq, kp, vp, bt, max_pages, seq, ctx, nkv,
                                                          out_p, R, out_f);

@@ -273,13 +273,10 @@ cudaError_t launch_prefill_attention(const uint16_t* qkv, int W, const int4* til
     if (n_tiles <= 0) return cudaSuccess;
     if (d != kD || nkv <= 0 || nq % nkv || nq / nkv > 8 || W != (nq + 2 * nkv) * kD || R % 16)
         return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             prefill_attention_smem_bytes());
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(prefill_attn_kernel),
+                                         prefill_attention_smem_bytes());
+        e != cudaSuccess)
+        return e;
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(kD));
     return launch_k(prefill_attn_kernel, dim3(n_tiles, nkv), dim3(32 * (nq / nkv)), prefill_attention_smem_bytes(), s,
         qkv, W, tiles, nq, nkv, scale_log2, out, R);

@@ -233,6 +233,10 @@ __device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
 }
 
 bool pdl_enabled();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) once per (device,
+// kernel): function attributes are per device, so a process driving several
+// GPUs must set them on each.
+cudaError_t ensure_smem_attr(const void* kern, int bytes);
 
 // Kernel launch through cudaLaunchKernelEx, with the PDL attribute when enabled.
 template <typename... KArgs, typename... Args>
@@ -252,6 +256,29 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
     }
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
     return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// Cooperative launch (no PDL): the driver guarantees that every CTA of the
+// grid is co-resident, or refuses the launch (cudaErrorCooperativeLaunchTooLarge).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                 Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();  // a refused launch is not sticky: clear it for the fallback
+        return e;
+    }
+    return cudaGetLastError();
 }
 
 #endif  // __CUDACC__

@@ -6,6 +6,9 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -17,6 +20,19 @@ bool g_pdl = false;
 }
 bool pdl_enabled() { return g_pdl; }
 void set_pdl(bool on) { g_pdl = on; }
+
+cudaError_t ensure_smem_attr(const void* kern, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count({dev, kern})) return cudaSuccess;
+    if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); e != cudaSuccess)
+        return e;
+    done.insert({dev, kern});
+    return cudaSuccess;
+}
 
 namespace {
 

@@ -182,11 +182,15 @@ __device__ __forceinline__ VTask vtask(const GemmArgs& a, int v, int KB) {
     return t;
 }
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// A stream-K part spins for its peers; the launch is cooperative (every CTA
+// co-resident), so the wait always ends.  If it does not within this bound
+// something is badly wrong: trap (a launch error) instead of hanging the GPU.
+constexpr unsigned long long kSpinLimitNs = 2000000000ull;
 
 __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -509,9 +513,15 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                 __threadfence();
                 asm volatile("bar.sync 4, 128;" ::: "memory");  // the 4 epilogue warps' stores are fenced
                 if (warp == 2 && lane == 0) {
-                    const int old = atomicAdd(a.sk_count + tk.tile, 1);
-                    const int target = (old / a.sk_parts + 1) * a.sk_parts;
-                    while (ld_acquire(a.sk_count + tk.tile) < target) __nanosleep(64);
+                    // 64-bit monotonic counter: never wraps (2^64 / S launches)
+                    const unsigned long long S = static_cast<unsigned long long>(a.sk_parts);
+                    const unsigned long long old = atomicAdd(a.sk_count + tk.tile, 1ull);
+                    const unsigned long long target = (old / S + 1) * S;
+                    const unsigned long long t_start = globaltimer();
+                    while (ld_acquire(a.sk_count + tk.tile) < target) {
+                        __nanosleep(64);
+                        if (globaltimer() - t_start > kSpinLimitNs) __trap();
+                    }
                 }
                 asm volatile("bar.sync 4, 128;" ::: "memory");
                 __threadfence();
@@ -584,13 +594,8 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     while (cols < need) cols <<= 1;
     a.tmem_cols = cols;
     const int smem = gemm_smem_bytes(a.n_mats, a.n_cap, a.stages);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel), 227 * 1024); e != cudaSuccess)
+        return e;
     a.sk_full = a.sk_tail = a.sk_parts = 0;
     if (a.sk_scratch && a.sk_count && a.sk_rows > 0 && a.epi == kEpiSiluPacked && a.n_mats == 2 &&
         a.k_splits == 1 && a.n_chunks == 1) {
@@ -605,10 +610,30 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
             a.sk_parts = S;
         }
     }
+    if (a.sk_parts) {
+        // the tail's parts wait on each other: only with every CTA co-resident
+        // (1 CTA per SM at this smem size; fewer SMs under MPS / green
+        // contexts / a concurrent kernel) -> otherwise run without the tail
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_tc_kernel,
+                                                          a.codec ? kThreadsCodec : kThreadsRaw, smem) != cudaSuccess ||
+            per_sm < 1 || per_sm * num_sms < num_sms)
+            a.sk_full = a.sk_tail = a.sk_parts = 0;
+    }
     const int n_virtual = a.sk_parts ? a.sk_full + a.sk_tail * a.sk_parts : a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
-    return launch_k(gemm_tc_kernel, dim3(grid), dim3(a.codec ? kThreadsCodec : kThreadsRaw), smem, stream, a);
+    const dim3 block(a.codec ? kThreadsCodec : kThreadsRaw);
+    if (a.sk_parts) {
+        // cooperative: the driver guarantees co-residency of the whole grid or
+        // refuses the launch (then: the same GEMM without the stream-K tail)
+        const cudaError_t e = launch_k_coop(gemm_tc_kernel, dim3(grid), block, smem, stream, a);
+        if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported) return e;
+        a.sk_full = a.sk_tail = a.sk_parts = 0;
+        const int nv = a.G * a.RB * a.n_chunks * a.k_splits;
+        return launch_k(gemm_tc_kernel, dim3(nv < num_sms ? nv : num_sms), block, smem, stream, a);
+    }
+    return launch_k(gemm_tc_kernel, dim3(grid), block, smem, stream, a);
 }
 
 }  // namespace mltk

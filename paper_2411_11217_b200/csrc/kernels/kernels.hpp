@@ -56,7 +56,7 @@ struct GemmArgs {
     // rows and runs the SiLU epilogue.  sk_full / sk_tail / sk_parts are set
     // by launch_gemm.
     float* sk_scratch = nullptr;  // [grid][n_mats][sk_rows][128] fp32
-    int* sk_count = nullptr;      // [grid] monotonic arrival counters, zero-initialised once
+    unsigned long long* sk_count = nullptr;  // [grid] 64-bit monotonic arrival counters, zeroed once
     int sk_rows = 0;              // row capacity per (tile, part): max rows of one group
     int sk_full = 0, sk_tail = 0, sk_parts = 0;
     // filled by launch_gemm

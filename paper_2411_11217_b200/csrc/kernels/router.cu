@@ -257,13 +257,10 @@ cudaError_t launch_moe_permute(const int32_t* topk_idx, const uint16_t* hn, int 
     if (grid > 296) grid = 296;
     if (grid < 1) grid = 1;
     const int smem = (E * 256 + T * K) * static_cast<int>(sizeof(int));
-    static bool attr = false;
-    if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (kMaxE * 256 + kMaxSlots) * static_cast<int>(sizeof(int)));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(permute_kernel),
+                                               (kMaxE * 256 + kMaxSlots) * static_cast<int>(sizeof(int)));
+        e != cudaSuccess)
+        return e;
     return launch_k(permute_kernel, dim3(grid), dim3(256), smem, s, topk_idx, hn, T, H, E, K, counts, offsets, perm, inv, xp, R);
 }
 

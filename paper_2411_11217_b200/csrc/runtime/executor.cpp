@@ -54,6 +54,18 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+}  // namespace
+
+void check_token_ids(const int32_t* ids, int64_t n, int vocab, const char* what) {
+    if (!ids) throw std::invalid_argument(std::string(what) + ": null");
+    for (int64_t i = 0; i < n; ++i)
+        if (ids[i] < 0 || ids[i] >= vocab)
+            throw std::invalid_argument(std::string(what) + "[" + std::to_string(i) + "] = " + std::to_string(ids[i]) +
+                                        " is not a token id in [0, " + std::to_string(vocab) + ")");
+}
+
+namespace {
+
 bool on_device(Resource r) {
     return r == Resource::Gpu || r == Resource::HostToDevice || r == Resource::DeviceToHost;
 }
@@ -94,6 +106,9 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
     if (steps < 1 || steps > max_steps_) throw std::invalid_argument("steps must be in [1, 64]");
     for (int i = 0; i < N_; ++i)
         if (pos_[i] + steps > max_ctx_) throw std::invalid_argument("KV capacity exceeded (max_ctx)");
+    // token ids index the [vocab, h1] embedding on the device: reject bad ids here
+    check_token_ids(tokens_in, N_, V_, "tokens_in");
+    if (forced) check_token_ids(forced, static_cast<int64_t>(steps) * N_, V_, "forced");
     // ---- schedule: the reference DAG for this policy (durations modeled) ----
     lightplan::HardwareSpec hw;  // nominal B200 spec for the modeled durations only
     hw.gpu_mem_bytes = opt_.budget_bytes;
@@ -369,7 +384,7 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
             }
             case TaskKind::LoadHidden:
                 rep.measured.link_upload += t.duration / layers;
-                rep.h2d_bytes += static_cast<double>(Rmu_) * H_ * 2;
+                rep.h2d_bytes += static_cast<double>(Rmu_) * Ho_ * 2;  // this rank's heads (act_load_hidden)
                 break;
             case TaskKind::OffloadQkv: rep.d2h_bytes += static_cast<double>(mu_) * W_ * 2; break;
             default: break;

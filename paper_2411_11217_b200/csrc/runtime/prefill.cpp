@@ -109,6 +109,7 @@ PrefillReport Runtime::prefill(const int32_t* tokens, const int32_t* lens, int32
         total += lens[i];
         max_len = std::max(max_len, lens[i]);
     }
+    check_token_ids(tokens, total, V_, "prefill tokens");
     prefill_alloc(total, max_len);
     const int T = pf_T_;
 

@@ -112,6 +112,17 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     if (opt.schedule < -1 || opt.schedule > 3) throw std::invalid_argument("schedule must be -1 or 0..3");
     schedule_kind();  // rejects S4 without A_g / CGOPipe,S2,S3 with A_g (pipesim.cpp:283-290)
     if (opt.max_ctx <= 0) throw std::invalid_argument("max_ctx must be > 0");
+    {   // GQA group size this rank's attention kernels support (host: register
+        // blocking up to 16 heads per kv head; GPU decode: G in {1,2,4,6,8};
+        // the GPU prefill: G <= 8)
+        const int G = nkv_ > 0 ? nq_ / nkv_ : 0;
+        if (G < 1 || nq_ % nkv_) throw std::invalid_argument("q_heads / kv_heads must be a positive integer");
+        if (!policy.attn_on_gpu && G > 16)
+            throw std::invalid_argument("host attention supports q_heads / kv_heads <= 16 (got " + std::to_string(G) + ")");
+        if (policy.attn_on_gpu && G != 1 && G != 2 && G != 4 && G != 6 && G != 8)
+            throw std::invalid_argument("GPU decode attention supports q_heads / kv_heads in {1, 2, 4, 6, 8} (got " +
+                                        std::to_string(G) + ")");
+    }
     max_ctx_ = opt.max_ctx;
     Rmu_ = round_up(mu_, 16);
     Re_ = round_up(mu_ * K_ + 16 * E_, 16);
@@ -231,8 +242,8 @@ void Runtime::allocate() {
     d_y_ = static_cast<float*>(A.alloc(static_cast<size_t>(down_splits_) * Re_ * H_ * 4, "expert_out"));
     // gate/up stream-K tail (gemm_tc.cu): parts of the partial last wave's tiles
     d_sk_scratch_ = static_cast<float*>(A.alloc(static_cast<size_t>(num_sms_) * 2 * Rmu_ * 128 * 4, "sk_scratch"));
-    d_sk_count_ = static_cast<int*>(A.alloc(static_cast<size_t>(num_sms_) * 4, "sk_count"));
-    ck(cudaMemset(d_sk_count_, 0, static_cast<size_t>(num_sms_) * 4), "sk_count");
+    d_sk_count_ = static_cast<unsigned long long*>(A.alloc(static_cast<size_t>(num_sms_) * 8, "sk_count"));
+    ck(cudaMemset(d_sk_count_, 0, static_cast<size_t>(num_sms_) * 8), "sk_count");
     d_logits_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * V_ * 4, "logits"));
     d_tok_in_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4, "tok_in"));
     d_tok_out_ = static_cast<int32_t*>(A.alloc(static_cast<size_t>(max_steps_) * N_ * 4, "tok_out"));

@@ -52,6 +52,9 @@ struct RuntimeOptions {
     int prefill_chunk_tokens = 0;  // 0: largest prefill chunk the budget allows
 };
 
+// Throws std::invalid_argument unless every ids[i] is in [0, vocab).
+void check_token_ids(const int32_t* ids, int64_t n, int vocab, const char* what);
+
 // Bump allocator over one cudaMalloc of the budget (SURVEY.md §7 hard part 5).
 class Arena {
   public:
@@ -236,7 +239,7 @@ class Runtime {
     uint8_t* d_inter_ = nullptr;        // [Re*F] packed
     float* d_y_ = nullptr;              // [Re, H]
     float* d_sk_scratch_ = nullptr;  // gate/up stream-K tail: fp32 parts [#SMs][2][Rmu][128]
-    int* d_sk_count_ = nullptr;       // [#SMs] monotonic arrival counters
+    unsigned long long* d_sk_count_ = nullptr;  // [#SMs] 64-bit monotonic arrival counters
     float* d_logits_ = nullptr;         // [Rmu, V]
     int32_t* d_tok_in_ = nullptr;       // [max_steps][N]
     int32_t* d_tok_out_ = nullptr;      // [max_steps][N]

@@ -140,6 +140,8 @@ class Runtime:
         PrefillReport); decode continues at each prompt's length."""
         if isinstance(prompts, np.ndarray) and prompts.ndim == 2:
             prompts = list(prompts)
+        if len(prompts) != self.policy.batch:  # the C side reads exactly N lengths
+            raise ValueError(f"prefill needs {self.policy.batch} prompts (policy.batch), got {len(prompts)}")
         lens = np.array([len(p) for p in prompts], np.int32)
         toks = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in prompts]), np.int32)
         first = np.zeros(len(prompts), np.int32)
@@ -155,7 +157,10 @@ class Runtime:
 
     def decode(self, tokens, steps: int, forced=None) -> Decoded:
         N = self.policy.batch
-        tokens = np.ascontiguousarray(tokens, np.int32).reshape(N)
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        if tokens.size != N:
+            raise ValueError(f"decode needs {N} token ids (policy.batch), got {tokens.size}")
+        tokens = tokens.reshape(N)
         out = np.zeros((steps, N), np.int32)
         rep = DecodeReport()
         fp = None

@@ -276,3 +276,33 @@ def test_tp_shard_only_measurement_mode(prompt):
     assert shard.info.streamed_bytes_per_layer == pytest.approx(full.info.streamed_bytes_per_layer / 2, rel=0.02)
     full.close()
     shard.close()
+
+
+def test_bad_inputs_rejected_before_the_device(prompt):
+    """Token ids outside [0, vocab) (decode inputs, teacher-forced ids and
+    prefill prompts) and unsupported GQA group sizes fail loudly with
+    invalid-argument instead of reaching the kernels."""
+    rt = Runtime(_model(TINY), capi.Policy(N, MU, 0, 1, 0.0, 0.0), budget_bytes=4e9, max_ctx=64, vocab=VOCAB,
+                 seed=1234)
+    bad = prompt[0].copy()
+    bad[3] = VOCAB
+    with pytest.raises(capi.MltError, match="token id"):
+        rt.decode(bad, 1)
+    bad[3] = -1
+    with pytest.raises(capi.MltError, match="token id"):
+        rt.decode(prompt[0], 2, forced=np.stack([prompt[0], bad]))
+    with pytest.raises(capi.MltError, match="token id"):
+        rt.prefill([np.array([1, 2, VOCAB + 5], np.int32)] * N)
+    with pytest.raises(ValueError):
+        rt.prefill([np.array([1, 2], np.int32)] * (N - 1))
+    d = rt.decode(prompt[0], 1)  # the runtime is still usable
+    assert d.report.timeline_ok == 1
+    rt.close()
+    # G = 32 / 1 = 32 query heads per kv head: beyond the host kernel's 16
+    with pytest.raises(capi.MltError, match="q_heads / kv_heads"):
+        Runtime(capi.ModelSpec(2, 4096, 3584, 32, 1, 8, 2, 2.0, 2.0), capi.Policy(N, MU, 0, 1, 0.0, 0.0),
+                budget_bytes=4e9, max_ctx=64, vocab=VOCAB)
+    # G = 3 on the GPU attention path (templated for 1/2/4/6/8)
+    with pytest.raises(capi.MltError, match="q_heads / kv_heads"):
+        Runtime(capi.ModelSpec(2, 768, 3584, 6, 2, 8, 2, 2.0, 2.0), capi.Policy(N, MU, 1, 1, 1.0, 1.0),
+                budget_bytes=4e9, max_ctx=64, vocab=VOCAB)

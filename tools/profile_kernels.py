@@ -109,7 +109,7 @@ def main():
 
     # the runtime's stream-K tail for the last wave of gate/up tiles (runtime.cpp gu.sk_*)
     sk_scratch = torch.zeros(148 * 2 * Rmu * 128, device="cuda")
-    sk_count = torch.zeros(148, dtype=torch.int32, device="cuda")
+    sk_count = torch.zeros(148, dtype=torch.int64, device="cuda")
     gu_args = capi.GemmArgs(a_table=t13.data_ptr(), n_mats=2, G=E, RB=F // 128, K=H, b=xp.data_ptr(), R=R,
                             b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=1, alpha=1.0,
                             out_packed=inter.data_ptr(), out_R=R, codec=int(a.codec),
