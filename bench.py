@@ -60,6 +60,13 @@ CONFIGS = {
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 NVLINK_BW = 900e9       # B200 NVLink 5, bytes/s per direction (nominal; 1 GPU in this pool)
 HOST_FLOPS = 2.0e12     # host-core fp32 estimate (16 SPR cores AVX-512); host DRAM bandwidth is measured
+# An 8-GPU B200 node's host DRAM feeds every GPU's PCIe stream and the host
+# attention together.  This pool leases one GPU with a 16-core slice of a
+# host (its DRAM read bandwidth is measured live); a tp-way job's node is
+# modeled as tp such slices but never above this node limit: 2 sockets x 8
+# channels of DDR5-5600 (716.8 GB/s peak) at the ~80 % a read stream
+# sustains (DGX B200 class host).  Documented assumption.
+NODE_HOST_READ_GBS = 573.0
 
 
 def peaks():
@@ -143,17 +150,36 @@ def model_spec(cfg, stored=False):
     return capi.ModelSpec(l, h1, h2, nq, nkv, ne, k, CODEC_DT if stored and cfg.get("codec") else 2.0, 2.0)
 
 
+def node_host(host_gbs, tp, per_slice_host):
+    """(host DRAM read B/s, host FLOP/s) of the job's node: the measured slice,
+    x tp slices for a --tp-shard extrapolation, capped at NODE_HOST_READ_GBS."""
+    slices = tp if per_slice_host else 1
+    bw = host_gbs * slices
+    if slices > 1:
+        bw = min(bw, NODE_HOST_READ_GBS)
+    return bw * 1e9, HOST_FLOPS * slices
+
+
+def b200_hw(cfg, link_gbs, host_gbs, pk, tp=1, per_slice_host=False, budget=None):
+    """The measured B200 HardwareSpec (TP-scaled with the B200 rule for tp > 1:
+    GPU side x tp, link x tp capped by the node's host read bandwidth)."""
+    from paper_2411_11217_b200 import capi
+    api = capi.load_product()
+    host_bw, host_fl = node_host(host_gbs, tp, per_slice_host)
+    hw = capi.HardwareSpec(cfg["budget"] if budget is None else budget, 196e9 * max(tp, 1), pk["hbm_gbs"] * 1e9,
+                           host_bw, link_gbs * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12,
+                           host_fl)
+    if tp > 1:
+        hw = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=host_bw)
+    return hw
+
+
 def search_rw(cfg, link_gbs, host_gbs, pk, tp=1, per_slice_host=False):
     """Best feasible r_w for the config's (N, mu, A_g) on the measured spec with
     the stored weight bytes (product search_policy, planner.cpp:234-341)."""
     from paper_2411_11217_b200 import capi
     api = capi.load_product()
-    slices = tp if per_slice_host else 1
-    hw = capi.HardwareSpec(cfg["budget"] - arena_extra(cfg), 196e9 * max(tp, 1), pk["hbm_gbs"] * 1e9,
-                           host_gbs * 1e9 * slices, link_gbs * 1e9,
-                           pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12, HOST_FLOPS * slices)
-    if tp > 1:
-        hw = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=host_gbs * 1e9 * slices)
+    hw = b200_hw(cfg, link_gbs, host_gbs, pk, tp, per_slice_host, budget=cfg["budget"] - arena_extra(cfg))
     grid = capi.make_grid([cfg["mu"]], [cfg["N"] // cfg["mu"]], [round(0.01 * i, 2) for i in range(101)],
                           [1.0] if cfg["a_g"] else [0.0], attn=(cfg["a_g"],), ffn=(1,))
     return api.search_policy(hw, model_spec(cfg, stored=True), capi.WorkloadSpec(cfg["prompt"], cfg["gen"]),
@@ -172,18 +198,11 @@ def hrm_bound(cfg, link_gbs, host_gbs, pk, tp=1, per_slice_host=False):
     DRAM read bandwidth: every B200 has its own PCIe link)."""
     from paper_2411_11217_b200 import capi
     api = capi.load_product()
-    # host RAM / DRAM read bandwidth of the job's node: with --tp-shard the
-    # measured box is one GPU's slice (16 cores, 196 GB, its own PCIe link), so a
-    # tp-way job has tp such slices
-    slices = tp if per_slice_host else 1
-    # a slice's host cores compute its own heads' attention: host DRAM bandwidth
-    # and FLOP/s of the job scale with the slices too (the reference keeps the
-    # CPU side fixed under TP, planner.cpp:101-108)
-    hw = capi.HardwareSpec(cfg["budget"], 196e9 * max(tp, 1), pk["hbm_gbs"] * 1e9, host_gbs * 1e9 * slices,
-                           link_gbs * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12,
-                           HOST_FLOPS * slices)
-    if tp > 1:
-        hw = api.apply_tensor_parallelism(hw, tp, b200_rule=True, host_read_cap=host_gbs * 1e9 * slices)
+    # with --tp-shard the measured box is one GPU's slice of a node (16 cores,
+    # 196 GB, its own PCIe link): a tp-way job has tp slices, whose host cores
+    # compute their own heads' attention (the reference keeps the CPU side
+    # fixed under TP, planner.cpp:101-108), capped at the node's DRAM read limit
+    hw = b200_hw(cfg, link_gbs, host_gbs, pk, tp, per_slice_host)
     w = capi.WorkloadSpec(cfg["prompt"], cfg["gen"])
     m = model_spec(cfg, stored=True)
     if tp > 1:  # + the NVLink roof of the 2 all-reduces / layer / micro-batch (nominal NVLink 5)
@@ -201,46 +220,74 @@ def measure_host(api):
     return out[0]
 
 
-def cpu_sample(cfg, samples, layers_sample=1):
-    """Oracle (CPU restatement) on a bounded sample of the same workload: one
-    decoder layer for all N sequences at ctx = prompt, repeated `samples`
-    times; tok/s = N / (l * t_layer)."""
+def host_info():
+    """CPU model and usable cores of this box (stated in both arms' lines)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cores": len(os.sched_getaffinity(0))}
+
+
+def config_obj(args, cfg, world):
+    """The workload description, printed identically by both arms."""
+    names = {32: "Mixtral-8x7B shape", 56: "Mixtral-8x22B shape", 40: "DBRX shape", 2: "tiny"}
+    l = cfg["model"][0]
+    return {"workload": args.config, "model": names.get(l, "custom"), "global_batch": cfg["N"],
+            "seq_len": cfg["prompt"], "gen_len": cfg["gen"], "micro_batch": cfg["mu"],
+            "gpu_budget_gb": cfg["budget"] / 1e9, "A_g": cfg["a_g"],
+            "parallelism": f"tp{world}" if world > 1 else "single GPU, weight paging",
+            "data": "synthetic weights seed 1234, prompt ids seed 5678, prompt KV seed 9012"}
+
+
+def cpu_decode(cfg, warmup, steps):
+    """The CPU restatement of the decode path (oracle/, fp32 activations,
+    OpenMP over all host cores) run for WHOLE decode steps: all l layers for
+    all N sequences, greedy, from the synthetic prompt KV at ctx = prompt.
+    Returns (per-step seconds of the timed steps, threads, setup seconds)."""
     import numpy as np
     from oracle import bind as orc
     l, h1, h2, nq, nkv, ne, k = cfg["model"]
     N, s = cfg["N"], cfg["prompt"]
-    m = orc.Model(layers_sample, h1, h2, nq, nkv, ne, k, cfg["vocab"], N, s + samples + 2)
+    t0 = time.perf_counter()
+    m = orc.Model(l, h1, h2, nq, nkv, ne, k, cfg["vocab"], N, s + warmup + steps + 2)
     m.fill_kv(9012, s)
-    x = np.random.default_rng(0).standard_normal((N, h1)).astype(np.float32)
+    setup = time.perf_counter() - t0
+    tok = np.random.default_rng(5678).integers(0, cfg["vocab"], N, dtype=np.int32)
     times = []
-    for i in range(samples):
+    for i in range(warmup + steps):
         t = time.perf_counter()
-        x, _ = m.layer_forward(0, x, np.full(N, s + i, np.int32), orc.FP32)
+        tok, _ = m.decode_step(tok, np.full(N, s + i, np.int32), orc.FP32)
         times.append(time.perf_counter() - t)
-    t_layer = statistics.median(times)
-    return N / (l * t_layer), orc.lib().orc_num_threads(), times
+    del m
+    return times[warmup:], orc.lib().orc_num_threads(), setup
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    samples = args.warmup + args.steps
-    tok_s, cores, times = cpu_sample(cfg, samples)
-    timed = times[args.warmup:]
-    t_layer = statistics.median(timed)
+    times, cores, setup = cpu_decode(cfg, args.warmup, args.steps)
+    total = sum(times)
     l = cfg["model"][0]
-    value = cfg["N"] / (l * t_layer)
-    sample = (f"1 of {l} decoder layers (fp32 CPU oracle, N={cfg['N']} sequences at ctx "
-              f"{cfg['prompt']}), {args.steps} timed samples after {args.warmup} warm-up; "
-              f"tok/s = N / ({l} x median layer time)")
+    value = cfg["N"] * len(times) / total
+    sample = (f"{len(times)} whole decode steps (all {l} layers, N={cfg['N']} sequences, ctx "
+              f"{cfg['prompt']}..{cfg['prompt'] + args.warmup + args.steps - 1}) of the fp32 CPU oracle "
+              f"after {args.warmup} warm-up steps; model build + prompt KV {setup:.1f} s untimed")
     line = {"impl": "reference", "metric": "decode tokens/sec at fixed GPU-mem budget",
             "value": value, "unit": "tok/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * l * t_layer, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.config, "N": cfg["N"], "prompt": cfg["prompt"]},
+            "config": config_obj(args, cfg, args.tp_shard if args.tp_shard > 1 else world), "host": host_info(),
             "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port",
                              "sample": sample},
+            "step_seconds": [round(t, 3) for t in times],
             "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -269,6 +316,59 @@ def expert_roofline(cfg, rep, pk, traffic, tp=1):
             "traffic": traffic if tp == 1 else None, "bytes_per_launch": bytes_launch,
             "bf16_equivalent_gbs": (wbytes + tokens) / avg_s / 1e9,
             "avg_launch_ms": avg_s * 1e3, "launches": rep.expert_launches}
+
+
+def hrm_kernels(cfg, hw, rep, prof, steps, tp=1, csv_path=None):
+    """Each hot kernel on the B200 hierarchical roofline (lightplan::hrm on the
+    measured spec hw, Eq. 7-11): operator FLOPs/bytes per micro-batch
+    launch from the reference cost model (opcost.cpp:5-47, stored weight
+    bytes, /tp under TP), its operational intensities, attainable_local /
+    attainable_cross, the turning points P1/P2, the balance gap, and the FLOP/s
+    it achieved in this run (live per-launch timings)."""
+    from paper_2411_11217_b200 import capi
+    api = capi.load_product()
+    mu = cfg["mu"]
+    ctx = cfg["prompt"] + steps / 2.0  # mean context over the timed steps
+    pr = api.op_profiles(model_spec(cfg, stored=True), mu, ctx, cfg["r_w"])
+    for p in pr.values():  # this rank's share
+        p.flops, p.gpu_bytes, p.cpu_bytes, p.link_bytes = (p.flops / tp, p.gpu_bytes / tp, p.cpu_bytes / tp,
+                                                           p.link_bytes / tp)
+    ex = {k["name"]: k for k in prof.get("exec", [])}
+    ev = {k["name"]: k for k in prof.get("events", [])}
+
+    def per_launch(d, name):
+        k = d.get(name)
+        return k["ms"] / k["launches"] / 1e3 if k and k.get("launches") else None
+
+    M = cfg["N"] // mu
+    t_ffn = rep.expert_ms_total / rep.expert_launches / 1e3 if rep.expert_launches else None
+    t_attn = (per_launch(ev, "gqa_decode_paged") if cfg["a_g"]
+              else (rep.measured.cpu_attention / M if rep.measured.cpu_attention > 0 else None))
+    items = [("expert_ffn", pr["ffn"], t_ffn, capi.LEVEL_GPU),
+             ("attention", pr["attention"], t_attn, capi.LEVEL_GPU if cfg["a_g"] else capi.LEVEL_CPU),
+             ("qkv_proj", pr["qkv"], per_launch(ex, "qkv_gemm"), capi.LEVEL_GPU),
+             ("o_proj", pr["output"], per_launch(ex, "o_gemm"), capi.LEVEL_GPU)]
+    out = {}
+    for name, p, t, lv in items:
+        gi = p.flops / p.gpu_bytes if p.gpu_bytes else 0.0
+        ci = p.flops / p.cpu_bytes if p.cpu_bytes else 0.0
+        li = p.flops / p.link_bytes if p.link_bytes else None
+        local = api.attainable_local(lv, gi if lv == capi.LEVEL_GPU else ci, hw)
+        r = {"where": "gpu" if lv == capi.LEVEL_GPU else "host cores", "flops": p.flops,
+             "bytes": p.gpu_bytes if lv == capi.LEVEL_GPU else p.cpu_bytes, "intensity": gi if lv == capi.LEVEL_GPU else ci,
+             "attainable_local_tflops": local / 1e12, "p2": api.turning_point_p2(gi, hw)}
+        if li is not None:  # streamed over the link: the cross roof binds
+            r.update({"link_intensity": li, "attainable_cross_tflops": api.attainable_cross(gi, li, hw) / 1e12,
+                      "p1": api.turning_point_p1(li, hw), "balance_gap": api.balance_gap(gi, li, hw)})
+        if t:
+            r["seconds_per_launch"] = t
+            r["achieved_tflops"] = p.flops / t / 1e12
+            r["frac_of_attainable_local"] = p.flops / t / local if local else None
+        out[name] = r
+    if csv_path:
+        with open(csv_path, "w") as fh:
+            fh.write(api.roofline_csv([p for _, p, _, _ in items], [n for n, _, _, _ in items], hw))
+    return out
 
 
 def load_traffic(codec=False):
@@ -403,7 +503,6 @@ def run_mlt(args, cfg):
     bd = bound.breakdown
     binding = max([("host link (H2D)", bd.link_upload), ("host cores", bd.cpu_attention + bd.cpu_ffn),
                    ("GPU (HBM)", bd.gpu_attention + bd.gpu_ffn)], key=lambda kv: kv[1])[0]
-    names = {32: "Mixtral-8x7B shape", 56: "Mixtral-8x22B shape", 40: "DBRX shape", 2: "tiny"}
     line = {
         "metric": "decode tokens/sec at fixed GPU-mem budget",
         "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
@@ -411,20 +510,19 @@ def run_mlt(args, cfg):
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (counter-PRNG weights seed 1234, prompt ids seed 5678, prompt KV seed 9012)",
-        "config": {"workload": args.config, "model": names.get(l, "custom"),
-                   "global_batch": cfg["N"], "seq_len": cfg["prompt"], "micro_batch": cfg["mu"],
-                   "gpu_budget_gb": cfg["budget"] / 1e9, "r_w": cfg["r_w"],
-                   "weight_codec": "on" if cfg.get("codec") else "off",
-                   "r_w_achieved": info.achieved_weight_ratio, "A_g": cfg["a_g"],
-                   "parallelism": (f"tp{world} (heads + expert h2 sharded, NCCL all-reduce x2/layer)"
-                                   if world > 1 else
-                                   f"tp{tp} job, its largest shard (rank {shard_rank}) measured alone on 1 GPU (own PCIe link; "
-                                   f"NVLink all-reduce elided, modeled ~0.5 MB/call)" if tp > 1
-                                   else "single GPU, weight paging"),
-                   "schedule": ("CGOPipe" if cfg["a_g"] == 0 else "S4") if args.schedule == "auto"
-                   else args.schedule,
-                   "weight_gates": args.gates,
-                   "l2": "weights streamed per step (>> 126 MB L2): no flush needed"},
+        "config": config_obj(args, cfg, tp),
+        "host": host_info(),
+        "run": {"r_w": cfg["r_w"], "weight_codec": "on" if cfg.get("codec") else "off",
+                "r_w_achieved": info.achieved_weight_ratio,
+                "parallelism_detail": (f"tp{world} (heads + expert h2 sharded, all-reduce x2/layer)"
+                                       if world > 1 else
+                                       f"tp{tp} job, its largest shard (rank {shard_rank}) measured alone on 1 GPU "
+                                       f"(own PCIe link; NVLink all-reduce elided, modeled ~0.5 MB/call)" if tp > 1
+                                       else "single GPU, weight paging"),
+                "schedule": ("CGOPipe" if cfg["a_g"] == 0 else "S4") if args.schedule == "auto"
+                else args.schedule,
+                "weight_gates": args.gates,
+                "l2": "weights streamed per step (>> 126 MB L2): no flush needed"},
         "hrm": {"bound_tok_s": bound.decode_throughput, "frac": value / bound.decode_throughput,
                 "weight_bytes_per_param": CODEC_DT if cfg.get("codec") else 2.0,
                 "bound_bf16_weights_tok_s": bound_bf16.decode_throughput,
@@ -436,6 +534,8 @@ def run_mlt(args, cfg):
                 "streamed_gb_per_layer_per_gpu": info.streamed_bytes_per_layer / 1e9,
                 "utilization": dict(zip(["gpu", "cpu", "h2d", "d2h", "ctopin"], list(rep.utilization)))},
         "roofline": expert_roofline(cfg, rep, pk, load_traffic(bool(cfg.get("codec"))), tp),
+        "hrm_kernels": hrm_kernels(cfg, b200_hw(cfg, link_gbs, host_gbs, pk, tp, args.tp_shard > 1), rep, prof,
+                                   args.steps, tp, args.roofline_csv),
         "peaks_source": pk_src,
         "e2e": {"value": e2e, "unit": "tok/s",
                 "h2d_bytes_per_step": rep.h2d_bytes / args.steps + cfg["N"] * 4 * 2,
@@ -467,11 +567,13 @@ def run_mlt(args, cfg):
             "note": "prefill measured; decode time = gen_len x the measured per-step time"}
     del rt
     if not args.no_cpu_baseline and rank == 0 and world == 1:
-        tok_s, cores, times = cpu_sample(cfg, 3)
-        line["cpu_baseline"] = {"value": tok_s, "unit": "tok/s", "cores": cores, "kind": "port",
-                                "sample": f"1 of {l} decoder layers, fp32 CPU oracle, N={cfg['N']} at ctx "
-                                          f"{cfg['prompt']}, median of 3 (layer s: "
-                                          f"{', '.join(f'{x:.2f}' for x in times)}), tok/s = N/(l*t_layer)"}
+        # >= 2 whole decode steps of the CPU path on this box's cores
+        times, cores, setup = cpu_decode(cfg, 0, 2)
+        line["cpu_baseline"] = {"value": cfg["N"] * len(times) / sum(times), "unit": "tok/s", "cores": cores,
+                                "kind": "port",
+                                "sample": f"2 whole decode steps (all {l} layers, N={cfg['N']}, ctx {cfg['prompt']}"
+                                          f"..{cfg['prompt'] + 1}) of the fp32 CPU oracle (step s: "
+                                          f"{', '.join(f'{x:.2f}' for x in times)}; build {setup:.1f} s untimed)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -493,6 +595,8 @@ def main():
     ap.add_argument("--prefill", action="store_true",
                     help="run the GPU prefill on synthetic prompt ids instead of synthetic prompt KV")
     ap.add_argument("--timeline", default=None, help="write the measured timeline JSON here")
+    ap.add_argument("--roofline-csv", default=None,
+                    help="write the hot kernels' roofline series (lightplan::roofline_csv) here")
     ap.add_argument("--codec", default="auto", choices=["auto", "on", "off"],
                     help="store/stream/read weights as lossless encoded tiles (runtime/weight_codec.hpp); "
                          "auto = on when weights are paged over the host link (r_w < 1), off when resident")

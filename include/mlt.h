@@ -572,6 +572,13 @@ int mlt_runtime_read_residual(mlt_runtime* rt, float* host_out);
  * "topk", "topw", "qkv_bf16", "attn_in", "y", "inv", "counts", "offsets",
  * "logits") to host; returns the byte count (host_out may be NULL). */
 int mlt_runtime_debug_read(mlt_runtime* rt, const char* name, void* host_out, size_t cap);
+/* Parity probe: arm a router tap for decode step `step` (1-based) of the next
+ * mlt_runtime_decode call (0 = off).  Every layer's router input (bf16
+ * [N, h1]) and top-k choice are then readable with mlt_runtime_debug_read
+ * names "cap_hn" ([L][N][h1] u16), "cap_topk" ([L][N][k] i32), "cap_topw"
+ * ([L][N][k] f32), so a caller can re-run the CPU router on identical inputs
+ * at every layer (BASELINE: router top-k bit-exact). */
+int mlt_runtime_capture_router(mlt_runtime* rt, int step);
 
 #ifdef __cplusplus
 }

@@ -34,6 +34,7 @@ _SIGS = {
     "orc_rmsnorm": (None, [V, V, I, I, F, I, V]),
     "orc_attention": (None, [V, V, V, V, I, I, I, I, I, V]),
     "orc_linear": (None, [V, V, I, I, I, V]),
+    "orc_linear_scalar": (None, [V, V, I, I, I, V]),
     "orc_expert": (None, [V, V, V, V, I, I, I, I, V]),
     "orc_rope": (None, [V, V, I, I, I, F]),
     "orc_model_create": (V, [C.POINTER(OrcConfig)]),
@@ -45,6 +46,8 @@ _SIGS = {
     "orc_model_kv": (V, [V, I, I]),
     "orc_num_threads": (I, []),
     "orc_router_margins": (None, [V, V]),
+    "orc_model_force_routes": (None, [V, V]),
+    "orc_model_route_info": (None, [V, V, V]),
 }
 
 _lib = None
@@ -194,6 +197,25 @@ class Model:
         out = np.zeros(self.cfg.batch, np.float32)
         lib().orc_router_margins(self.h, p(out))
         return out
+
+    def force_routes(self, topk):
+        """Take these routes ([L, N, K] int32) in every following step (None: own routing)."""
+        if topk is None:
+            self._routes = None
+            lib().orc_model_force_routes(self.h, None)
+            return
+        self._routes = np.ascontiguousarray(topk, np.int32)  # kept alive while borrowed
+        c = self.cfg
+        assert self._routes.shape == (c.layers, c.batch, c.top_k)
+        lib().orc_model_force_routes(self.h, p(self._routes))
+
+    def route_info(self):
+        """(own top-k [L, N, K], gap [L, N]) of the last step."""
+        c = self.cfg
+        idx = np.zeros((c.layers, c.batch, c.top_k), np.int32)
+        gap = np.zeros((c.layers, c.batch), np.float32)
+        lib().orc_model_route_info(self.h, p(idx), p(gap))
+        return idx, gap
 
     def fill_kv(self, seed, upto):
         lib().orc_fill_kv(self.h, seed, upto)

@@ -7,6 +7,7 @@
  */
 #include "oracle_numerics.h"
 
+#include <immintrin.h>
 #include <math.h>
 #include <omp.h>
 #include <stdlib.h>
@@ -59,31 +60,77 @@ void orc_gen_bf16(uint64_t seed, uint64_t tid, int64_t n, float scale, int is_no
 /* kernels                                                                  */
 /* ---------------------------------------------------------------------- */
 
-/* dot of fp32 x with fp32 w (16 independent partial sums -> vectorizes
- * without reassociation flags). */
+/* Every dot product of the oracle has one fixed summation structure: 16
+ * lane partials p_j = sum over k = j (mod 16), in k order, each step one
+ * fused multiply-add (fp32, single rounding); then s = p_0 + p_1 + ... +
+ * p_15 left to right; then the K % 16 tail in order.  dot16 is the scalar
+ * statement of it; the blocked AVX-512 paths below evaluate exactly the same
+ * operations (one zmm lane per partial), so they are bit-identical to it and
+ * to each other for any blocking and thread count. */
 static inline float dot16(const float* x, const float* w, int n) {
     float acc[16] = {0};
     int k = 0;
     for (; k + 16 <= n; k += 16)
-        for (int j = 0; j < 16; ++j) acc[j] += x[k + j] * w[k + j];
+        for (int j = 0; j < 16; ++j) acc[j] = fmaf(x[k + j], w[k + j], acc[j]);
     float s = 0.0f;
     for (int j = 0; j < 16; ++j) s += acc[j];
-    for (; k < n; ++k) s += x[k] * w[k];
+    for (; k < n; ++k) s = fmaf(x[k], w[k], s);
     return s;
 }
 
+static inline float hsum16(__m512 v) {
+    float a[16];
+    _mm512_storeu_ps(a, v);
+    float s = 0.0f;
+    for (int j = 0; j < 16; ++j) s += a[j];
+    return s;
+}
+
+static inline __m512 ld_bf16x16(const uint16_t* p) {
+    const __m256i h = _mm256_loadu_si256((const __m256i*)p);
+    return _mm512_castsi512_ps(_mm512_slli_epi32(_mm512_cvtepu16_epi32(h), 16));
+}
+
+/* y[t][m] = dot(x[t], w[m]) for 4 weight rows x 4 tokens per register
+ * block (16 zmm accumulators; weights widened from bf16 in registers). */
 void orc_linear(const float* x, const uint16_t* w, int T, int K, int M, float* y) {
-#pragma omp parallel
-    {
-        float* row = (float*)malloc(sizeof(float) * (size_t)K);
-#pragma omp for schedule(static)
-        for (int m = 0; m < M; ++m) {
-            const uint16_t* wr = w + (size_t)m * K;
-            for (int k = 0; k < K; ++k) row[k] = orc_bf16_to_f32(wr[k]);
-            for (int t = 0; t < T; ++t) y[(size_t)t * M + m] = dot16(x + (size_t)t * K, row, K);
+    const int K16 = K & ~15;
+#pragma omp parallel for schedule(static)
+    for (int m0 = 0; m0 < M; m0 += 4) {
+        const uint16_t* wr[4];
+        for (int r = 0; r < 4; ++r) wr[r] = w + (size_t)(m0 + r < M ? m0 + r : M - 1) * K;
+        for (int t0 = 0; t0 < T; t0 += 4) {
+            const float* xr[4];
+            for (int t = 0; t < 4; ++t) xr[t] = x + (size_t)(t0 + t < T ? t0 + t : T - 1) * K;
+            __m512 acc[4][4];
+            for (int r = 0; r < 4; ++r)
+                for (int t = 0; t < 4; ++t) acc[r][t] = _mm512_setzero_ps();
+            for (int k = 0; k < K16; k += 16) {
+                __m512 wv[4];
+                for (int r = 0; r < 4; ++r) wv[r] = ld_bf16x16(wr[r] + k);
+                for (int t = 0; t < 4; ++t) {
+                    const __m512 xv = _mm512_loadu_ps(xr[t] + k);
+                    for (int r = 0; r < 4; ++r) acc[r][t] = _mm512_fmadd_ps(xv, wv[r], acc[r][t]);
+                }
+            }
+            for (int r = 0; r < 4 && m0 + r < M; ++r)
+                for (int t = 0; t < 4 && t0 + t < T; ++t) {
+                    float s = hsum16(acc[r][t]);
+                    for (int k = K16; k < K; ++k) s = fmaf(xr[t][k], orc_bf16_to_f32(wr[r][k]), s);
+                    y[(size_t)(t0 + t) * M + m0 + r] = s;
+                }
         }
-        free(row);
     }
+}
+
+/* Reference statement of orc_linear (tests pin the blocked path to it). */
+void orc_linear_scalar(const float* x, const uint16_t* w, int T, int K, int M, float* y) {
+    float* row = (float*)malloc(sizeof(float) * (size_t)K);
+    for (int m = 0; m < M; ++m) {
+        for (int k = 0; k < K; ++k) row[k] = orc_bf16_to_f32(w[(size_t)m * K + k]);
+        for (int t = 0; t < T; ++t) y[(size_t)t * M + m] = dot16(x + (size_t)t * K, row, K);
+    }
+    free(row);
 }
 
 /* RMSNorm, Mixtral convention: y = x / sqrt(mean(x^2) + eps) * gamma. */
@@ -125,18 +172,31 @@ void orc_attention(const float* q, const uint16_t* k, const uint16_t* v, const i
                    int T, int n_q, int n_kv, int d, int ctx_cap, float* out) {
     const int group = n_q / n_kv;
     const float scale = 1.0f / sqrtf((float)d);
+    /* one work item per (token, query head): scores s_j = dot16(q, k_j) (the
+     * oracle's dot structure; d % 16 == 0 is vectorised, else scalar), fp32
+     * softmax with expf, o = sum_j p_j v_j accumulated in key order, / l */
 #pragma omp parallel for collapse(2) schedule(static)
     for (int t = 0; t < T; ++t)
         for (int h = 0; h < n_q; ++h) {
             const int kh = h / group;
             const int L = ctx[t];
             const float* qv = q + ((size_t)t * n_q + h) * d;
-            float* p = (float*)malloc(sizeof(float) * (size_t)(L > 0 ? L : 1));
+            float* p = (float*)malloc(sizeof(float) * (size_t)(L > 0 ? L : 1) + sizeof(float) * (size_t)d * 2);
+            float* kf = p + (L > 0 ? L : 1);
+            float* o = out + ((size_t)t * n_q + h) * d;
             float mx = -INFINITY;
             for (int j = 0; j < L; ++j) {
                 const uint16_t* kr = k + (((size_t)t * ctx_cap + j) * n_kv + kh) * d;
-                float s = 0.0f;
-                for (int i = 0; i < d; ++i) s += qv[i] * orc_bf16_to_f32(kr[i]);
+                float s;
+                if ((d & 15) == 0) {
+                    __m512 acc = _mm512_setzero_ps();
+                    for (int i = 0; i < d; i += 16)
+                        acc = _mm512_fmadd_ps(_mm512_loadu_ps(qv + i), ld_bf16x16(kr + i), acc);
+                    s = hsum16(acc);
+                } else {
+                    for (int i = 0; i < d; ++i) kf[i] = orc_bf16_to_f32(kr[i]);
+                    s = dot16(qv, kf, d);
+                }
                 p[j] = s * scale;
                 if (p[j] > mx) mx = p[j];
             }
@@ -145,11 +205,16 @@ void orc_attention(const float* q, const uint16_t* k, const uint16_t* v, const i
                 p[j] = expf(p[j] - mx);
                 l += p[j];
             }
-            float* o = out + ((size_t)t * n_q + h) * d;
             for (int i = 0; i < d; ++i) o[i] = 0.0f;
             for (int j = 0; j < L; ++j) {
                 const uint16_t* vr = v + (((size_t)t * ctx_cap + j) * n_kv + kh) * d;
-                for (int i = 0; i < d; ++i) o[i] += p[j] * orc_bf16_to_f32(vr[i]);
+                int i = 0;
+                if ((d & 15) == 0) {
+                    const __m512 pj = _mm512_set1_ps(p[j]);
+                    for (; i < d; i += 16)
+                        _mm512_storeu_ps(o + i, _mm512_fmadd_ps(pj, ld_bf16x16(vr + i), _mm512_loadu_ps(o + i)));
+                }
+                for (; i < d; ++i) o[i] = fmaf(p[j], orc_bf16_to_f32(vr[i]), o[i]);
             }
             const float inv = L > 0 ? 1.0f / l : 0.0f;
             for (int i = 0; i < d; ++i) o[i] *= inv;
@@ -163,11 +228,9 @@ void orc_attention(const float* q, const uint16_t* k, const uint16_t* v, const i
  * logits (softmax is monotone), ties to the lower expert index; weights =
  * softmax over the k selected logits; permutation = stable sort by
  * (expert, token, slot).  The GPU kernel (router.cu) mirrors this exactly. */
-void orc_router(const uint16_t* hn, const uint16_t* w, int T, int H, int E, int K,
-                float* logits, int32_t* topk_idx, float* topk_w, int32_t* perm,
-                int32_t* offsets) {
+void orc_router_logits(const uint16_t* hn, const uint16_t* w, int T, int H, int E, float* logits) {
     const int chunks = H / 8;
-    for (int t = 0; t < T; ++t) {
+    for (int t = 0; t < T; ++t)
         for (int e = 0; e < E; ++e) {
             float lane[32];
             for (int l = 0; l < 32; ++l) {
@@ -185,15 +248,14 @@ void orc_router(const uint16_t* hn, const uint16_t* w, int T, int H, int E, int 
             }
             logits[(size_t)t * E + e] = lane[0];
         }
+}
+
+/* Weights (softmax over the k chosen logits, slot order) and the stable
+ * (expert, token, slot) permutation for given top-k choices. */
+void orc_route(const float* logits, const int32_t* topk_idx, int T, int E, int K, float* topk_w,
+               int32_t* perm, int32_t* offsets) {
+    for (int t = 0; t < T; ++t) {
         const float* lg = logits + (size_t)t * E;
-        int used[64] = {0};
-        for (int s = 0; s < K; ++s) {
-            int best = -1;
-            for (int e = 0; e < E; ++e)
-                if (!used[e] && (best < 0 || lg[e] > lg[best])) best = e;
-            used[best] = 1;
-            topk_idx[(size_t)t * K + s] = best;
-        }
         const float top = lg[topk_idx[(size_t)t * K]];
         float sum = 0.0f;
         for (int s = 0; s < K; ++s) {
@@ -210,6 +272,24 @@ void orc_router(const uint16_t* hn, const uint16_t* w, int T, int H, int E, int 
     for (int e = 0; e < E; ++e) fill[e] = offsets[e];
     for (int t = 0; t < T; ++t)
         for (int s = 0; s < K; ++s) perm[fill[topk_idx[(size_t)t * K + s]]++] = t * K + s;
+}
+
+void orc_router(const uint16_t* hn, const uint16_t* w, int T, int H, int E, int K,
+                float* logits, int32_t* topk_idx, float* topk_w, int32_t* perm,
+                int32_t* offsets) {
+    orc_router_logits(hn, w, T, H, E, logits);
+    for (int t = 0; t < T; ++t) {
+        const float* lg = logits + (size_t)t * E;
+        int used[64] = {0};
+        for (int s = 0; s < K; ++s) {
+            int best = -1;
+            for (int e = 0; e < E; ++e)
+                if (!used[e] && (best < 0 || lg[e] > lg[best])) best = e;
+            used[best] = 1;
+            topk_idx[(size_t)t * K + s] = best;
+        }
+    }
+    orc_route(logits, topk_idx, T, E, K, topk_w, perm, offsets);
 }
 
 /* Expert FFN: W2 (silu(x W1^T) * (x W3^T)). */
@@ -239,6 +319,9 @@ struct orc_model {
     uint16_t ***w1, ***w3, ***w2;
     uint16_t **kc, **vc; /* [layer] -> [N][max_ctx][n_kv][d] */
     float* rmargin;      /* [N]: min over layers of the router's k-th minus (k+1)-th logit */
+    const int32_t* force_topk; /* [L][N][K] routes to take instead of the own top-k (borrowed) */
+    int32_t* own_topk;   /* [L][N][K] the oracle's own top-k of the last step */
+    float* own_gap;      /* [L][N] its k-th selected minus best unselected logit */
 };
 
 static uint16_t* gen(const orc_model* m, int layer, int kind, int expert, int64_t n, double scale,
@@ -269,6 +352,8 @@ orc_model* orc_model_create(const orc_config* cfg) {
     m->kc = calloc(L, sizeof(void*));
     m->vc = calloc(L, sizeof(void*));
     m->rmargin = calloc(cfg->batch, sizeof(float));
+    m->own_topk = calloc((size_t)L * cfg->batch * cfg->top_k, sizeof(int32_t));
+    m->own_gap = calloc((size_t)L * cfg->batch, sizeof(float));
     const size_t kv = (size_t)cfg->batch * cfg->max_ctx * cfg->kv_heads * m->d;
     for (int l = 0; l < L; ++l) {
         m->attn_norm[l] = gen(m, l, ORC_T_ATTN_NORM, 0, H, 0, 1);
@@ -303,11 +388,20 @@ void orc_model_free(orc_model* m) {
     free(m->attn_norm); free(m->ffn_norm); free(m->wqkv); free(m->wo); free(m->router);
     free(m->w1); free(m->w3); free(m->w2); free(m->kc); free(m->vc);
     free(m->embed); free(m->lm_head); free(m->final_norm); free(m->rmargin);
+    free(m->own_topk); free(m->own_gap);
     free(m);
 }
 
 void orc_router_margins(const orc_model* m, float* out) {
     memcpy(out, m->rmargin, sizeof(float) * (size_t)m->c.batch);
+}
+
+void orc_model_force_routes(orc_model* m, const int32_t* topk) { m->force_topk = topk; }
+
+void orc_model_route_info(const orc_model* m, int32_t* own_topk, float* own_gap) {
+    const size_t rows = (size_t)m->c.layers * m->c.batch;
+    if (own_topk) memcpy(own_topk, m->own_topk, sizeof(int32_t) * rows * m->c.top_k);
+    if (own_gap) memcpy(own_gap, m->own_gap, sizeof(float) * rows);
 }
 
 const uint16_t* orc_model_tensor(const orc_model* m, int layer, int kind, int expert) {
@@ -406,7 +500,7 @@ int orc_layer_forward(orc_model* m, int layer, float* x, const int32_t* pos, int
     int32_t* perm = malloc(sizeof(int32_t) * (size_t)N * K);
     int32_t* off = malloc(sizeof(int32_t) * (E + 1));
     orc_router(hb, m->router[layer], N, H, E, K, logits, idx, wts, perm, off);
-    if (topk_out) memcpy(topk_out, idx, sizeof(int32_t) * N * K);
+    memcpy(m->own_topk + (size_t)layer * N * K, idx, sizeof(int32_t) * N * K);
     for (int t = 0; t < N; ++t) { /* routing robustness: gap between selected and next logit */
         const float kth = logits[(size_t)t * E + idx[t * K + K - 1]];
         float next = -INFINITY;
@@ -416,8 +510,20 @@ int orc_layer_forward(orc_model* m, int layer, float* x, const int32_t* pos, int
             if (!sel && logits[(size_t)t * E + e] > next) next = logits[(size_t)t * E + e];
         }
         const float gap = kth - next;
+        m->own_gap[(size_t)layer * N + t] = gap;
         if (layer == 0 || gap < m->rmargin[t]) m->rmargin[t] = gap;
     }
+    if (m->force_topk) { /* take the given routes (e.g. the GPU's) on the oracle's own logits */
+        memcpy(idx, m->force_topk + (size_t)layer * N * K, sizeof(int32_t) * N * K);
+        for (int i = 0; i < N * K; ++i)
+            if (idx[i] < 0 || idx[i] >= E) {
+                free(xn); free(qkv); free(q); free(kk); free(o); free(h); free(ctx); free(hb);
+                free(logits); free(idx); free(wts); free(perm); free(off);
+                return -1;
+            }
+        orc_route(logits, idx, N, E, K, wts, perm, off);
+    }
+    if (topk_out) memcpy(topk_out, idx, sizeof(int32_t) * N * K);
 
     float* y = malloc(sizeof(float) * (size_t)N * K * H); /* per (t, s) */
     for (int e = 0; e < E; ++e) {

@@ -67,6 +67,12 @@ void orc_router(const uint16_t* hn, const uint16_t* w, int T, int H, int E, int 
                 float* logits, int32_t* topk_idx, float* topk_w, int32_t* perm,
                 int32_t* offsets);
 
+/* The two halves of orc_router: logits (fixed tree) and, for given top-k
+ * choices, the softmax weights + stable permutation. */
+void orc_router_logits(const uint16_t* hn, const uint16_t* w, int T, int H, int E, float* logits);
+void orc_route(const float* logits, const int32_t* topk_idx, int T, int E, int K, float* topk_w,
+               int32_t* perm, int32_t* offsets);
+
 void orc_rmsnorm(const float* x, const uint16_t* gamma, int T, int H, float eps, int round_bf16,
                  float* out);
 
@@ -75,8 +81,13 @@ void orc_rmsnorm(const float* x, const uint16_t* gamma, int T, int H, float eps,
 void orc_attention(const float* q, const uint16_t* k, const uint16_t* v, const int32_t* ctx,
                    int T, int n_q, int n_kv, int d, int ctx_cap, float* out);
 
-/* Dense y = x W^T, x fp32 [T,K], W bf16 [M,K] -> fp32 [T,M]. */
+/* Dense y = x W^T, x fp32 [T,K], W bf16 [M,K] -> fp32 [T,M].  Each output
+ * is one dot product in the oracle's fixed structure (16 lane partials of
+ * fused multiply-adds in k order, then summed left to right, then the tail);
+ * orc_linear (blocked AVX-512, OpenMP) and orc_linear_scalar (the plain
+ * statement) are bit-identical. */
 void orc_linear(const float* x, const uint16_t* w, int T, int K, int M, float* y);
+void orc_linear_scalar(const float* x, const uint16_t* w, int T, int K, int M, float* y);
 
 /* One expert FFN over T rows: W2 (silu(x W1^T) * (x W3^T)); faithful rounds
  * the intermediate to bf16. */
@@ -108,6 +119,14 @@ void orc_fill_kv(orc_model* m, uint64_t seed, int upto);
  * (a routing near-tie indicator). */
 void orc_router_margins(const orc_model* m, float* out);
 uint16_t* orc_model_kv(orc_model* m, int layer, int which); /* which: 0=K 1=V */
+/* Forced routing (parity probe): with topk != NULL ([L][N][K], borrowed until
+ * reset with NULL) every layer takes these experts instead of its own top-k,
+ * weighted by the softmax of the ORACLE's logits at those experts.  Lets the
+ * residual be compared against a GPU run on the identical route even where a
+ * router near-tie flipped; the oracle's own choice is still recorded. */
+void orc_model_force_routes(orc_model* m, const int32_t* topk);
+/* The last step's own (unforced) top-k [L][N][K] and its gap [L][N]. */
+void orc_model_route_info(const orc_model* m, int32_t* own_topk, float* own_gap);
 int orc_num_threads(void);
 
 #ifdef __cplusplus

@@ -264,6 +264,13 @@ int mlt_runtime_read_residual(mlt_runtime* r, float* out) {
     });
 }
 
+int mlt_runtime_capture_router(mlt_runtime* r, int step) {
+    return guard([&] {
+        H(r)->rt->capture_router(step);
+        return MLT_OK;
+    });
+}
+
 int mlt_runtime_debug_read(mlt_runtime* r, const char* name, void* out, size_t cap) {
     return guard([&] { return static_cast<int>(H(r)->rt->debug_read(name, out, cap)); });
 }

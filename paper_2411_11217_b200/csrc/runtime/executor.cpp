@@ -287,6 +287,7 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
     const double host_end = std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count();
     std::memcpy(out, h_tok_ + static_cast<size_t>(max_steps_) * N_ * 3, static_cast<size_t>(steps) * N_ * 4);
     for (int i = 0; i < N_; ++i) pos_[i] += steps;
+    capture_step_ = 0;  // the router tap covers one decode call
 
     // ---- measured timeline ----
     // Host (steady_clock) and GPU timers drift by tens of ppm; map host times

@@ -152,6 +152,9 @@ Runtime::~Runtime() {
     if (h_qkv_) cudaFreeHost(h_qkv_);
     if (h_attn_) cudaFreeHost(h_attn_);
     if (h_tok_) cudaFreeHost(h_tok_);
+    if (h_cap_hn_) cudaFreeHost(h_cap_hn_);
+    if (h_cap_topk_) cudaFreeHost(h_cap_topk_);
+    if (h_cap_topw_) cudaFreeHost(h_cap_topw_);
     host_free(h_kcache_, true);
     host_free(h_vcache_, true);
     host_free(h_pfx_, true);
@@ -438,10 +441,26 @@ void Runtime::read_last_topk(int32_t* out) {
     ck(cudaMemcpy(out, d_topk_, static_cast<size_t>(mu_) * K_ * 4, cudaMemcpyDeviceToHost), "read topk");
 }
 
+void Runtime::capture_router(int step) {
+    if (step < 0 || step > max_steps_) throw std::invalid_argument("capture_router: step out of range");
+    if (step && !h_cap_hn_) {
+        const size_t rows = static_cast<size_t>(L_) * N_;
+        ck(cudaHostAlloc(reinterpret_cast<void**>(&h_cap_hn_), rows * H_ * 2, 0), "cap_hn");
+        ck(cudaHostAlloc(reinterpret_cast<void**>(&h_cap_topk_), rows * K_ * 4, 0), "cap_topk");
+        ck(cudaHostAlloc(reinterpret_cast<void**>(&h_cap_topw_), rows * K_ * 4, 0), "cap_topw");
+    }
+    capture_step_ = step;
+}
+
 size_t Runtime::debug_read(const std::string& name, void* out, size_t cap) {
     const void* src = nullptr;
     size_t bytes = 0;
-    if (name == "h") { src = d_h_; bytes = static_cast<size_t>(mu_) * H_ * 4; }
+    if (name == "cap_hn" || name == "cap_topk" || name == "cap_topw") {  // router tap (host, pinned)
+        const size_t rows = static_cast<size_t>(L_) * N_;
+        src = name == "cap_hn" ? static_cast<const void*>(h_cap_hn_)
+              : name == "cap_topk" ? static_cast<const void*>(h_cap_topk_) : static_cast<const void*>(h_cap_topw_);
+        bytes = src ? rows * (name == "cap_hn" ? H_ * 2 : K_ * 4) : 0;
+    } else if (name == "h") { src = d_h_; bytes = static_cast<size_t>(mu_) * H_ * 4; }
     else if (name == "hn") { src = d_hn_; bytes = static_cast<size_t>(mu_) * H_ * 2; }
     else if (name == "topk") { src = d_topk_; bytes = static_cast<size_t>(mu_) * K_ * 4; }
     else if (name == "topw") { src = d_topw_; bytes = static_cast<size_t>(mu_) * K_ * 4; }
@@ -465,7 +484,7 @@ size_t Runtime::debug_read(const std::string& name, void* out, size_t cap) {
     if (out) {
         if (cap < bytes) throw std::invalid_argument("debug_read: buffer too small");
         ck(cudaStreamSynchronize(s_gpu_), "sync");
-        ck(cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost), "debug read");
+        ck(cudaMemcpy(out, src, bytes, cudaMemcpyDefault), "debug read");
     }
     return bytes;
 }
@@ -632,6 +651,15 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
                                          d_router_[l], mu_, H_, E_, K_, d_hn_, nullptr, d_topk_, d_topw_, s_gpu_,
                                          o_split ? o.k_splits : 0, o.split_stride, o_split ? x : nullptr,
                                          o_split ? d_h_ : nullptr));
+    }
+    if (capture_step_ == step) {  // router tap: this layer's router input and choice (parity probe)
+        const size_t row = static_cast<size_t>(l) * N_ + t0;
+        kk(cudaMemcpyAsync(h_cap_hn_ + row * H_, d_hn_, static_cast<size_t>(mu_) * H_ * 2, cudaMemcpyDeviceToHost,
+                           s_gpu_), "capture hn");
+        kk(cudaMemcpyAsync(h_cap_topk_ + row * K_, d_topk_, static_cast<size_t>(mu_) * K_ * 4, cudaMemcpyDeviceToHost,
+                           s_gpu_), "capture topk");
+        kk(cudaMemcpyAsync(h_cap_topw_ + row * K_, d_topw_, static_cast<size_t>(mu_) * K_ * 4, cudaMemcpyDeviceToHost,
+                           s_gpu_), "capture topw");
     }
     kl("moe_permute", mltk::launch_moe_permute(d_topk_, d_hn_, mu_, H_, E_, K_, d_cnt_, d_off_, d_perm_, d_inv_,
                                                d_xe_, Re_, s_gpu_));

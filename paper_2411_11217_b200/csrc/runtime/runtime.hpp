@@ -145,6 +145,12 @@ class Runtime {
     void read_residual(float* host_out);          // x [N, H] fp32
     void read_last_topk(int32_t* host_idx);       // last micro-batch's topk [mu, K]
     size_t debug_read(const std::string& name, void* host_out, size_t cap);
+    // Router tap: during decode step `step` (1-based, of the next decode()
+    // call; 0 = off) every layer's router input hn (bf16 [N, H]), top-k ids
+    // and weights are copied to host buffers on the compute stream (readable
+    // via debug_read "cap_hn" [L][N][H] u16, "cap_topk" [L][N][K] i32,
+    // "cap_topw" [L][N][K] f32).  A parity probe, off on measured paths.
+    void capture_router(int step);
 
     double achieved_weight_ratio() const { return achieved_rw_; }
     int64_t streamed_bytes_per_layer() const { return layer_blob_bytes_; }
@@ -258,6 +264,10 @@ class Runtime {
     uint16_t* h_kcache_ = nullptr;  // [L][N][nkv][max_ctx][d]
     uint16_t* h_vcache_ = nullptr;
     int32_t* h_tok_ = nullptr;    // pinned [max_steps][N] in / out staging
+    int capture_step_ = 0;        // router tap (capture_router)
+    uint16_t* h_cap_hn_ = nullptr;
+    int32_t* h_cap_topk_ = nullptr;
+    float* h_cap_topw_ = nullptr;
     std::vector<int32_t> pos_;
     int max_ctx_ = 0;
     int cur_forced_ = 0, cur_steps_ = 0;

@@ -74,6 +74,7 @@ _SIGS = {
     "runtime_timeline_json": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
     "runtime_read_residual": (C.c_int, [C.c_void_p, C.c_void_p]),
     "runtime_debug_read": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
+    "runtime_capture_router": (C.c_int, [C.c_void_p, C.c_int]),
 }
 
 
@@ -195,3 +196,15 @@ class Runtime:
         out = np.zeros(n // np.dtype(dtype).itemsize, dtype)
         self._ck(self.f["runtime_debug_read"](self.h, name.encode(), out.ctypes.data_as(C.c_void_p), n))
         return out
+
+    def capture_router(self, step: int):
+        """Arm the router tap for decode step `step` (1-based) of the next decode()."""
+        self._ck(self.f["runtime_capture_router"](self.h, step))
+
+    def captured_router(self):
+        """(hn [L, N, H] u16, topk [L, N, K] i32, topw [L, N, K] f32) of the tapped step."""
+        L, N = self.model.layers, self.policy.batch
+        H, K = self.model.hidden_dim, self.model.top_k
+        return (self.debug_read("cap_hn", np.uint16).reshape(L, N, H),
+                self.debug_read("cap_topk", np.int32).reshape(L, N, K),
+                self.debug_read("cap_topw", np.float32).reshape(L, N, K))

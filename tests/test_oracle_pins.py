@@ -104,3 +104,51 @@ def test_tiny_model_decode_runs_and_is_deterministic(mode):
         nb, mb = b.decode_step(toks, np.full(3, s, np.int32), mode)
         assert (na == nb).all() and (ma == mb).all() and (ma >= 0).all()
         toks = na
+
+
+@pytest.mark.parametrize("T,K,M", [(1, 16, 1), (5, 4096, 14), (64, 1024, 37), (3, 100, 7), (17, 33, 9)])
+def test_blocked_linear_is_the_scalar_dot_structure(T, K, M):
+    """orc_linear (4x4 register-blocked AVX-512, OpenMP) evaluates exactly the
+    oracle's one dot-product structure (16 lane partials of fused
+    multiply-adds, summed left to right, then the tail): bit-identical to the
+    plain statement orc_linear_scalar for any shape, including M/T/K tails."""
+    rng = np.random.default_rng(T * 1000 + K + M)
+    x = rng.standard_normal((T, K)).astype(np.float32)
+    w = bf(rng.standard_normal((M, K)) * 0.05)
+    a = np.zeros((T, M), np.float32)
+    b = np.zeros((T, M), np.float32)
+    orc.lib().orc_linear(orc.p(x), orc.p(w), T, K, M, orc.p(a))
+    orc.lib().orc_linear_scalar(orc.p(x), orc.p(w), T, K, M, orc.p(b))
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_forced_routes_reproduce_own_routes_bitwise():
+    """orc_model_force_routes with the oracle's own top-k reproduces the
+    unforced step bit for bit (same weights, same permutation); a different
+    route changes the residual; out-of-range experts are rejected."""
+    def model():
+        return orc.Model(2, 256, 384, 2, 1, 8, 2, 512, 4, 8, seed=77)
+
+    toks = np.array([1, 7, 300, 511], np.int32)
+    pos = np.zeros(4, np.int32)
+    a = model()
+    _, _, xa = a.decode_step(toks, pos, orc.FP32, want_x=True)
+    own, gap = a.route_info()
+    assert own.shape == (2, 4, 2) and np.all(gap >= 0)
+    b = model()
+    b.force_routes(own)
+    _, _, xb = b.decode_step(toks, pos, orc.FP32, want_x=True)
+    assert np.array_equal(xa.view(np.uint32), xb.view(np.uint32))
+    alt = own.copy()
+    alt[1, 2] = [(own[1, 2, 0] + 1) % 8 if (own[1, 2, 0] + 1) % 8 != own[1, 2, 1] else (own[1, 2, 0] + 2) % 8,
+                 own[1, 2, 1]]
+    c = model()
+    c.force_routes(alt)
+    _, _, xc = c.decode_step(toks, pos, orc.FP32, want_x=True)
+    assert np.array_equal(xc[[0, 1, 3]], xa[[0, 1, 3]]) and not np.array_equal(xc[2], xa[2])
+    bad = own.copy()
+    bad[0, 0, 0] = 8
+    d = model()
+    d.force_routes(bad)
+    with pytest.raises(AssertionError):
+        d.decode_step(toks, pos, orc.FP32)
