@@ -473,6 +473,10 @@ typedef struct mlt_runtime_options_t {
                                  from HBM; mlt_codec_encode); numerics unchanged bit for bit */
     int32_t disable_pdl;      /* 1: no programmatic dependent launch (all-GPU schedules use it by
                                  default; per-kernel CUDA-event breakdowns need it off) */
+    int32_t collective;       /* tp_size > 1: 0 = NCCL (nccl_id = ncclUniqueId); 1 = host-staged
+                                 all-reduce through POSIX shared memory (ranks on one host, any
+                                 number per GPU; nccl_id = a NUL-terminated rendezvous name,
+                                 identical on every rank and unique per job) */
     int32_t expert_down_splits; /* K-splits of the expert down GEMM (fp32 partials summed in part
                                  order by the combine): 0 = auto (with weight_codec, the split
                                  in 1..8 that best fills the last wave of SMs; 1 without), else

@@ -63,6 +63,7 @@ mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p
         opt.weight_codec = o->weight_codec != 0;
         opt.pdl = o->disable_pdl == 0;
         opt.expert_down_splits = o->expert_down_splits;
+        opt.collective = o->collective;
         auto hh = std::make_unique<Handle>();
         hh->rt = std::make_unique<mlt::Runtime>(ms, ext, pol, opt);
         h = hh.release();

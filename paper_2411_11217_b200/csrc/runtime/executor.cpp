@@ -284,6 +284,7 @@ DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, in
        "ids d2h");
     ck(cudaEventRecord(e_end, s_gpu_), "record");
     ck(cudaEventSynchronize(e_end), "sync");
+    if (coll_) coll_->check();  // an asynchronous collective failure surfaces here
     const double host_end = std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count();
     std::memcpy(out, h_tok_ + static_cast<size_t>(max_steps_) * N_ * 3, static_cast<size_t>(steps) * N_ * 4);
     for (int i = 0; i < N_; ++i) pos_[i] += steps;

@@ -135,9 +135,18 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     ck(cudaStreamCreateWithFlags(&s_gpu_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
-    if (opt.tp_size > 1)
-        coll_ = opt.tp_shard_only ? make_elided_collective(opt.tp_rank, opt.tp_size)
-                                  : make_nccl_collective(opt.nccl_id, opt.tp_rank, opt.tp_size, opt.device);
+    if (opt.tp_size > 1) {
+        if (opt.tp_shard_only)
+            coll_ = make_elided_collective(opt.tp_rank, opt.tp_size);
+        else if (opt.collective == 1)  // host-staged: the rendezvous name travels in nccl_id
+            coll_ = make_host_collective(std::string(reinterpret_cast<const char*>(opt.nccl_id),
+                                                     strnlen(reinterpret_cast<const char*>(opt.nccl_id), 127)),
+                                         opt.tp_rank, opt.tp_size, static_cast<size_t>(mu_) * H_);
+        else if (opt.collective == 0)
+            coll_ = make_nccl_collective(opt.nccl_id, opt.tp_rank, opt.tp_size, opt.device);
+        else
+            throw std::invalid_argument("collective must be 0 (NCCL) or 1 (host-staged)");
+    }
     arena_ = std::make_unique<Arena>(static_cast<size_t>(opt.budget_bytes));
     build_catalog();
     allocate();

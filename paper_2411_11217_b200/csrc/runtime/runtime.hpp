@@ -45,6 +45,7 @@ struct RuntimeOptions {
     int tp_rank = 0, tp_size = 1;  // tensor parallelism (one process per GPU)
     uint8_t nccl_id[128] = {};     // ncclUniqueId from rank 0 (tp_size > 1)
     bool tp_shard_only = false;    // one shard alone on this GPU, all-reduce elided (measurement)
+    int collective = 0;            // tp_size > 1: 0 NCCL, 1 host-staged shared memory (collective_host.cpp)
     bool weight_codec = false;     // store/stream/read projection + expert weights encoded (weight_codec.hpp)
     bool pdl = true;               // programmatic dependent launch on all-GPU (resident, A_g = 1) schedules
     int expert_down_splits = 0;    // 0: auto (codec: best last-wave fill in 1..8; raw: 1)

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -23,7 +24,15 @@ class RuntimeOptions(C.Structure):
                 ("seed", C.c_uint64), ("exact_gates", C.c_int32), ("tp_rank", C.c_int32),
                 ("tp_size", C.c_int32), ("nccl_id", C.c_uint8 * 128), ("schedule", C.c_int32),
                 ("prefill_chunk_tokens", C.c_int32), ("tp_shard_only", C.c_int32),
-                ("weight_codec", C.c_int32), ("disable_pdl", C.c_int32), ("expert_down_splits", C.c_int32)]
+                ("weight_codec", C.c_int32), ("disable_pdl", C.c_int32), ("collective", C.c_int32),
+                ("expert_down_splits", C.c_int32)]
+
+
+def host_collective_name() -> bytes:
+    """Rendezvous key of a host-staged collective group (collective="host"):
+    rank 0 creates it, the launcher broadcasts it like an ncclUniqueId."""
+    import secrets
+    return f"mlt_coll_{os.getpid()}_{secrets.token_hex(8)}".encode()
 
 
 def nccl_unique_id() -> bytes:
@@ -101,7 +110,7 @@ class Runtime:
                  rope_theta: float = 1e6, lm_head_scale: float = 4.0, exact_gates: bool = True,
                  tp_rank: int = 0, tp_size: int = 1, nccl_id: bytes = b"", schedule: str = "auto",
                  prefill_chunk_tokens: int = 0, tp_shard_only: bool = False, weight_codec: bool = False,
-                 pdl: bool = True, down_splits: int = 0):
+                 pdl: bool = True, down_splits: int = 0, collective: str = "nccl"):
         self.api, self.f = _fns()
         self.model, self.policy = model, policy
         nid = (C.c_uint8 * 128)(*(nccl_id.ljust(128, b"\0")[:128]))
@@ -110,7 +119,7 @@ class Runtime:
                                    int(exact_gates), tp_rank, tp_size, nid,
                                    -1 if schedule == "auto" else capi.SCHED[schedule],
                                    prefill_chunk_tokens, int(tp_shard_only), int(weight_codec), int(not pdl),
-                                   down_splits)
+                                   {"nccl": 0, "host": 1}[collective], down_splits)
         self.h = self.f["runtime_create"](C.byref(model), C.byref(policy), C.byref(self.opts))
         if not self.h:
             code = self.api.fn["last_status"]()
