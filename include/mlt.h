@@ -360,6 +360,7 @@ typedef struct mlt_gemm_args_t {
                                   scratch [#SMs][2][sk_rows][128]; NULL disables it */
     int64_t* sk_count;         /* [#SMs] 64-bit arrival counters, zeroed once by the caller */
     int32_t sk_rows;           /* row capacity per group for the scratch (>= max rows of a group) */
+    int32_t dec_groups;        /* codec: decoder groups of 4 warps (2..4; 0 -> the default) */
 } mlt_gemm_args_t;
 
 /* Grouped swap-AB tcgen05 GEMM (SURVEY.md §2c expert_gateup_silu /
@@ -401,6 +402,15 @@ int mlt_gqa_decode_paged(const uint16_t* q, int ldq, const uint16_t* k_pool,
                          const uint16_t* v_pool, const int32_t* block_table, int max_pages,
                          const int32_t* seq, const int32_t* ctx, int T, int nq, int nkv, int d,
                          int page, void* out_packed, int R, float* out_rowmajor, void* stream);
+/* Split-KV variant: each (token, kv head)'s pages are split over `splits`
+ * CTAs (0 = auto: the count in 1..max_splits that best fills whole waves of
+ * SMs); scratch >= T*nq*max_splits*130 floats; counters >= T*nkv int32,
+ * zeroed once by the caller (every launch leaves them zero).  Same output. */
+int mlt_gqa_decode_paged_split(const uint16_t* q, int ldq, const uint16_t* k_pool, const uint16_t* v_pool,
+                               const int32_t* block_table, int max_pages, const int32_t* seq,
+                               const int32_t* ctx, int T, int nq, int nkv, int d, int page, void* out_packed,
+                               int R, float* out_rowmajor, int splits, int max_splits, float* scratch,
+                               int32_t* counters, void* stream);
 int mlt_kv_append(const uint16_t* qkv_bf16, int nq, int nkv, int d, const int32_t* seq,
                   const int32_t* pos, int T, const int32_t* block_table, int max_pages, int page,
                   uint16_t* k_pool, uint16_t* v_pool, void* stream);

@@ -564,7 +564,8 @@ class GemmArgs(C.Structure):
                 ("ldr", C.c_int32), ("out_packed", C.c_void_p), ("out_R", C.c_int32),
                 ("n_chunks", C.c_int32), ("k_splits", C.c_int32), ("split_stride", C.c_int64),
                 ("trace", C.c_void_p), ("codec", C.c_int32), ("ktrace", C.c_void_p),
-                ("sk_scratch", C.c_void_p), ("sk_count", C.c_void_p), ("sk_rows", C.c_int32)]
+                ("sk_scratch", C.c_void_p), ("sk_count", C.c_void_p), ("sk_rows", C.c_int32),
+                ("dec_groups", C.c_int32)]
 
 
 V, I, F = C.c_void_p, C.c_int, C.c_float
@@ -587,6 +588,7 @@ _KSIGS = {
     "expert_ffn": [V, I, V, V, V, V, I, I, I, I, V, V, V, V, V, I, I, V, V],
     "argmax": [V, I, I, V, V, V],
     "gqa_decode_paged": [V, I, V, V, V, I, V, V, I, I, I, I, I, V, I, V, V],
+    "gqa_decode_paged_split": [V, I, V, V, V, I, V, V, I, I, I, I, I, V, I, V, I, I, V, V, V],
     "kv_append": [V, I, I, I, V, V, I, V, I, I, V, V, V],
     "rope_table": [I, I, C.c_double, V],
     "prefill_attention": [V, I, V, I, I, I, I, V, I, V],

@@ -79,6 +79,7 @@ mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
     g.sk_scratch = a->sk_scratch;
     g.sk_count = reinterpret_cast<unsigned long long*>(a->sk_count);
     g.sk_rows = a->sk_rows;
+    if (a->dec_groups > 0) g.dec_groups = a->dec_groups;
     return g;
 }
 
@@ -273,6 +274,25 @@ int mlt_gqa_decode_paged(const uint16_t* q, int ldq, const uint16_t* kp, const u
         ck(mltk::launch_gqa_decode_paged(q, ldq, kp, vp, bt, max_pages, seq, ctx, T, nq, nkv, d, page,
                                          reinterpret_cast<uint8_t*>(out_packed), R, out_f, st(s)),
            "gqa_decode_paged");
+        return MLT_OK;
+    });
+}
+
+int mlt_gqa_decode_paged_split(const uint16_t* q, int ldq, const uint16_t* kp, const uint16_t* vp,
+                               const int32_t* bt, int max_pages, const int32_t* seq, const int32_t* ctx, int T,
+                               int nq, int nkv, int d, int page, void* out_packed, int R, float* out_f,
+                               int splits, int max_splits, float* scratch, int32_t* counters, void* s) {
+    return guard([&] {
+        if (splits < 0 || max_splits < 1 || !scratch || !counters)
+            throw std::invalid_argument("gqa_decode_paged_split: splits >= 0, max_splits >= 1, scratch + counters");
+        mltk::GqaSplit sp;
+        sp.splits = splits;
+        sp.max_splits = max_splits;
+        sp.scratch = scratch;
+        sp.counters = counters;
+        ck(mltk::launch_gqa_decode_paged(q, ldq, kp, vp, bt, max_pages, seq, ctx, T, nq, nkv, d, page,
+                                         reinterpret_cast<uint8_t*>(out_packed), R, out_f, st(s), &sp),
+           "gqa_decode_paged_split");
         return MLT_OK;
     });
 }

@@ -32,7 +32,16 @@
 // 3 xor-shuffles per page, the row sum is reduced once at the end.  ~100
 // instructions per 8 KiB page and warp (vs ~1500 for CUDA-core FMAs).  The
 // warps' (m, l, O) are merged through shared memory at the end.
+//
+// Split-KV (flash-decoding across CTAs): with few (token, kv head) pairs the
+// grid is a fraction of a wave (mu = 64: 512 CTAs = 1.73 waves of 2 CTAs x
+// 148 SMs), so a token's pages are split S ways over blockIdx.z.  Each split
+// CTA stores its unnormalised partial (O, m, l) per head to a scratch, and
+// the last split to arrive (a per-(token, head) counter it resets to 0)
+// merges all S partials in split order — deterministic for any arrival
+// order — and writes the output.
 #include <cfloat>
+#include <cmath>
 #include <cstdint>
 
 #include "common.cuh"
@@ -85,18 +94,22 @@ template <int G>
 __global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
     const uint16_t* __restrict__ q, int ldq, const uint16_t* __restrict__ kp, const uint16_t* __restrict__ vp,
     const int32_t* __restrict__ bt, int max_pages, const int32_t* __restrict__ seq, const int32_t* __restrict__ ctx,
-    int nkv, uint8_t* out_p, int R, float* out_f) {
+    int nkv, uint8_t* out_p, int R, float* out_f, int S, float* __restrict__ part, int* __restrict__ cnt) {
     pdl_trigger();  // dependents may launch; our inputs: after the wait
     pdl_wait();
     static_assert(G >= 1 && G <= 8, "heads per kv head must fit the MMA n = 8");
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ uint64_t full[kWarps][kStagesW];
-    const int t = blockIdx.x, h = blockIdx.y;
+    __shared__ int last_split;
+    const int t = blockIdx.x, h = blockIdx.y, sp = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, tg = lane & 3;
     const int L = ctx[t];
     const int s_id = seq[t];
-    const int n_pages = (L + kPage - 1) / kPage;
+    const int n_all = (L + kPage - 1) / kPage;
+    // this split's pages [p0, p1) of the token's n_all
+    const int p0 = static_cast<int>(static_cast<int64_t>(sp) * n_all / S);
+    const int n_pages = static_cast<int>(static_cast<int64_t>(sp + 1) * n_all / S);
     // per-warp ring: [warp][stage][K page | V page]
     uint8_t* ring = sm + static_cast<size_t>(warp) * kStagesW * 2 * kPageBytes;
     const uint32_t ring_s = smem_u32(ring);
@@ -118,7 +131,7 @@ __global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
         bulk_g2s(dst + kPageBytes, vp + off, kPageBytes, &full[warp][st], pol);
     };
     if (lane == 0)
-        for (int k = 0; k < kStagesW && warp + k * kWarps < n_pages; ++k) issue(warp + k * kWarps, k);
+        for (int k = 0; k < kStagesW && p0 + warp + k * kWarps < n_pages; ++k) issue(p0 + warp + k * kWarps, k);
 
     // Q^T as B fragments: b0 = q[head g][16kk + 2tg, +1], b1 = q[head g][16kk + 8 + 2tg, +1]
     uint32_t qb[8][2];
@@ -145,7 +158,7 @@ __global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
 
     uint32_t phase = 0;
     for (int k = 0;; ++k) {
-        const int page = warp + k * kWarps;
+        const int page = p0 + warp + k * kWarps;
         if (page >= n_pages) break;
         const int st = k % kStagesW;
         mbar_wait(&full[warp][st], phase);
@@ -228,6 +241,9 @@ __global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
         }
     }
     __syncthreads();
+    // partial of split sp: [t][h][sp][head][O(128) | m | l]
+    constexpr int kPart = kD + 2;
+    float* const mine = S > 1 ? part + ((static_cast<int64_t>(t) * nkv + h) * S + sp) * (G * kPart) : nullptr;
     for (int idx = threadIdx.x; idx < G * kD; idx += blockDim.x) {
         const int hh = idx / kD, d = idx % kD;
         float M = -INFINITY;
@@ -239,11 +255,45 @@ __global__ void __launch_bounds__(kWarps * 32) gqa_decode_kernel(
             den += c[kD + 1] * f;
             num += c[d] * f;
         }
+        if (S > 1) {  // unnormalised partial; the last split merges
+            mine[hh * kPart + d] = num;
+            if (d == 0) {
+                mine[hh * kPart + kD] = M;
+                mine[hh * kPart + kD + 1] = den;
+            }
+            continue;
+        }
         const float o = num / den;
         const int col = (h * G + hh) * kD + d;
         if (out_p) *reinterpret_cast<uint16_t*>(out_p + b_packed_off(t, col, R)) = f32_to_bf16_bits(o);
         if (out_f) out_f[static_cast<int64_t>(t) * (G * static_cast<int64_t>(nkv)) * kD + col] = o;
     }
+    if (S == 1) return;
+    __threadfence();  // this split's partial is visible device-wide before it is counted
+    __syncthreads();
+    if (threadIdx.x == 0) last_split = atomicAdd(cnt + t * nkv + h, 1) == S - 1;
+    __syncthreads();
+    if (!last_split) return;
+    __threadfence();  // acquire: every other split's partial
+    const float* base = part + (static_cast<int64_t>(t) * nkv + h) * S * (G * kPart);
+    for (int idx = threadIdx.x; idx < G * kD; idx += blockDim.x) {
+        const int hh = idx / kD, d = idx % kD;
+        float M = -INFINITY;
+        for (int s2 = 0; s2 < S; ++s2) M = fmaxf(M, __ldcg(base + s2 * (G * kPart) + hh * kPart + kD));
+        float den = 0.f, num = 0.f;
+        for (int s2 = 0; s2 < S; ++s2) {  // split order: deterministic whoever merges
+            const float* c = base + s2 * (G * kPart) + hh * kPart;
+            const float l2 = __ldcg(c + kD + 1);
+            const float f = l2 > 0.f ? exp2f(__ldcg(c + kD) - M) : 0.f;  // empty splits: l = 0
+            den += l2 * f;
+            num += __ldcg(c + d) * f;
+        }
+        const float o = num / den;
+        const int col = (h * G + hh) * kD + d;
+        if (out_p) *reinterpret_cast<uint16_t*>(out_p + b_packed_off(t, col, R)) = f32_to_bf16_bits(o);
+        if (out_f) out_f[static_cast<int64_t>(t) * (G * static_cast<int64_t>(nkv)) * kD + col] = o;
+    }
+    if (threadIdx.x == 0) cnt[t * nkv + h] = 0;  // every split has arrived: ready for the next launch
 }
 
 // One CTA per token: 16-byte chunks of this step's K and V rows into the
@@ -270,14 +320,35 @@ __global__ void kv_append_kernel(const uint16_t* qkv, int nq, int nkv, int d, co
 template <int G>
 cudaError_t launch_g(const uint16_t* q, int ldq, const uint16_t* kp, const uint16_t* vp,
                      const int32_t* bt, int max_pages, const int32_t* seq, const int32_t* ctx, int T,
-                     int nkv, uint8_t* out_p, int R, float* out_f, cudaStream_t s) {
+                     int nkv, uint8_t* out_p, int R, float* out_f, const GqaSplit* split, cudaStream_t s) {
     const int smem = kWarps * kStagesW * 2 * kPageBytes;
     static_assert(8 * kCombStride * 4 <= kStagesW * 2 * kPageBytes, "merge state fits a warp's ring");
     if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gqa_decode_kernel<G>), smem); e != cudaSuccess)
         return e;
-    dim3 grid(T, nkv);
+    int S = 1;
+    if (split && split->scratch && split->counters) {
+        S = split->splits;
+        if (S <= 0) {  // auto: the split count in 1..max whose grid best fills whole waves
+            int per_sm = 0, sms = 0, dev = 0;
+            if (cudaGetDevice(&dev) != cudaSuccess ||
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gqa_decode_kernel<G>, kWarps * 32, smem) !=
+                    cudaSuccess)
+                return cudaErrorInvalidValue;
+            const double slots = static_cast<double>(sms) * (per_sm > 0 ? per_sm : 1);
+            double best = 0;
+            for (int c = 1; c <= split->max_splits && c <= max_pages; ++c) {
+                const double w = static_cast<double>(T) * nkv * c / slots;
+                const double fill = w / std::ceil(w);
+                if (fill > best + 0.02) best = fill, S = c;  // more splits only for a clearly better fill
+            }
+        }
+        if (S > split->max_splits) return cudaErrorInvalidValue;
+    }
+    if (S < 1) S = 1;
+    dim3 grid(T, nkv, S);
     return launch_k(gqa_decode_kernel<G>, dim3(grid), dim3(kWarps * 32), smem, s, q, ldq, kp, vp, bt, max_pages, seq, ctx, nkv,
-                                                         out_p, R, out_f);
+                    out_p, R, out_f, S, S > 1 ? split->scratch : nullptr, S > 1 ? split->counters : nullptr);
 }
 
 }  // namespace
@@ -286,15 +357,15 @@ cudaError_t launch_gqa_decode_paged(const uint16_t* q, int ldq, const uint16_t* 
                                     const uint16_t* v_pool, const int32_t* block_table,
                                     int max_pages, const int32_t* seq, const int32_t* ctx, int T,
                                     int nq, int nkv, int d, int page, uint8_t* out_packed, int R,
-                                    float* out_rowmajor, cudaStream_t s) {
+                                    float* out_rowmajor, cudaStream_t s, const GqaSplit* split) {
     if (T <= 0) return cudaSuccess;
     if (d != kD || nq % nkv || page != kPage) return cudaErrorInvalidValue;
     switch (nq / nkv) {
-        case 1: return launch_g<1>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, s);
-        case 2: return launch_g<2>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, s);
-        case 4: return launch_g<4>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, s);
-        case 6: return launch_g<6>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, s);
-        case 8: return launch_g<8>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, s);
+        case 1: return launch_g<1>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, split, s);
+        case 2: return launch_g<2>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, split, s);
+        case 4: return launch_g<4>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, split, s);
+        case 6: return launch_g<6>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, split, s);
+        case 8: return launch_g<8>(q, ldq, k_pool, v_pool, block_table, max_pages, seq, ctx, T, nkv, out_packed, R, out_rowmajor, split, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -30,14 +30,14 @@ namespace mltk {
 namespace {
 
 constexpr int kThreadsRaw = 192;    // warp0 producer, warp1 MMA, warps2-5 epilogue
-constexpr int kDecWarps = 8;
-// Decoder group g owns the ring stages s with s % kDecGroups == g, so it
-// meets each of its stages round after round and never waits on a stage
+// Decoder group g (4 warps) owns the ring stages s with s % groups == g, so
+// it meets each of its stages round after round and never waits on a stage
 // barrier two phases ahead (mbarrier parity would alias).  Codec launches
-// round the stage count to a multiple of kDecGroups.
-constexpr int kDecGroups = 2;
-constexpr int kDecThreads = kDecWarps * 32 / kDecGroups;  // threads per group
-constexpr int kThreadsCodec = 192 + kDecWarps * 32;  // + warps 6-13: weight-tile decoders
+// round the stage count to a multiple of the group count (GemmArgs::dec_groups,
+// 2..kMaxDecGroups: more groups = more tiles decoding concurrently).
+constexpr int kMaxDecGroups = 4;
+constexpr int kDecThreads = 128;  // threads per decoder group
+constexpr int kThreadsCodec = 192 + kMaxDecGroups * kDecThreads;  // launch bound; warps 6+: decoders
 constexpr int kCodecTile = 12432;   // encoded tile bytes (runtime/weight_codec.hpp)
 // codec: an encoded tile lands at the END of its 16 KiB A slot and is
 // expanded in place (every input is in registers before any output store)
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
             if (rows <= 0) continue;
             for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
                 for (int kb = kb0; kb < kb1; ++kb, ++kstep) {
-                    if (stage % kDecGroups == grp) {
+                    if (stage % a.dec_groups == grp) {
                         mbar_wait(&ctl->full[stage], phase);
                         if (a.ktrace && blockIdx.x == 0 && kstep < 256 && dt == 0) a.ktrace[256 + kstep] = globaltimer();
                         const uint32_t sa = smem_u32(smem + stage * stage_bytes);
@@ -584,7 +584,10 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     const int budget = 227 * 1024 - 1024 - kCtlBytes - kEpiScratch;
     a.stages = budget / per_stage;
     if (a.stages > 8) a.stages = 8;
-    if (a.codec) a.stages -= a.stages % kDecGroups;  // decoder groups own whole stages
+    if (a.codec) {
+        if (a.dec_groups < 2 || a.dec_groups > kMaxDecGroups) return cudaErrorInvalidValue;
+        a.stages -= a.stages % a.dec_groups;  // decoder groups own whole stages
+    }
     if (a.codec != 0 && a.codec != 1) return cudaErrorInvalidValue;
     if (a.stages < 2) return cudaErrorInvalidValue;
     const int acc_cols = a.n_mats * a.n_cap;
@@ -616,14 +619,15 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         // contexts / a concurrent kernel) -> otherwise run without the tail
         int per_sm = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_tc_kernel,
-                                                          a.codec ? kThreadsCodec : kThreadsRaw, smem) != cudaSuccess ||
+                                                          a.codec ? 192 + a.dec_groups * kDecThreads : kThreadsRaw,
+                                                          smem) != cudaSuccess ||
             per_sm < 1 || per_sm * num_sms < num_sms)
             a.sk_full = a.sk_tail = a.sk_parts = 0;
     }
     const int n_virtual = a.sk_parts ? a.sk_full + a.sk_tail * a.sk_parts : a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
-    const dim3 block(a.codec ? kThreadsCodec : kThreadsRaw);
+    const dim3 block(a.codec ? 192 + a.dec_groups * kDecThreads : kThreadsRaw);
     if (a.sk_parts) {
         // cooperative: the driver guarantees co-residency of the whole grid or
         // refuses the launch (then: the same GEMM without the stream-K tail)

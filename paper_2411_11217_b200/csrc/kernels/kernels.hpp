@@ -35,6 +35,7 @@ struct GemmArgs {
     // 1: A row blocks are encoded tiles (runtime/weight_codec.hpp, 12432 B
     // per 64-k tile); decoder warps expand them in shared memory
     int codec = 0;
+    int dec_groups = 2;  // codec: decoder groups of 4 warps (2..4), each owning every dec_groups-th stage
     // optional CTA-0 pipeline trace [4][256] (%globaltimer): producer issue,
     // decoder start, decoder done, MMA start per k-block (diagnostic)
     unsigned long long* ktrace = nullptr;
@@ -142,11 +143,20 @@ cudaError_t launch_argmax(const float* logits, int T, int V, int32_t* ids, float
 // of sequence seq[t].  q bf16 rows with leading dimension ldq (the rope
 // output [T, (nq+2nkv)d] works directly); output written in packed B layout
 // (capacity R) for the O projection and/or fp32 row-major.
+// Split-KV scratch: splits = S (0: auto, the count in 1..max_splits that best
+// fills whole waves), scratch >= T * nq * max_splits * 130 floats, counters
+// >= T * nkv ints zeroed once (each launch leaves them zero).
+struct GqaSplit {
+    int splits = 0;
+    int max_splits = 8;
+    float* scratch = nullptr;
+    int* counters = nullptr;
+};
 cudaError_t launch_gqa_decode_paged(const uint16_t* q, int ldq, const uint16_t* k_pool,
                                     const uint16_t* v_pool, const int32_t* block_table,
                                     int max_pages, const int32_t* seq, const int32_t* ctx, int T,
                                     int nq, int nkv, int d, int page, uint8_t* out_packed, int R,
-                                    float* out_rowmajor, cudaStream_t s);
+                                    float* out_rowmajor, cudaStream_t s, const GqaSplit* split = nullptr);
 
 // Append this step's k/v (bf16 rows from the rope output [T, (nq+2nkv)d])
 // into the paged cache at position ctx[t]-1 of sequence seq[t].

@@ -12,13 +12,20 @@ depth on the same weights, KV and tokens (teacher-forced with the GPU's own
 greedy ids, so one near-tie cannot cascade):
   (i)   router top-k indices at every layer and step are BIT-EXACT against
         the oracle's router on the identical bf16 inputs (weights to 1e-6);
-  (ii)  the oracle is forced onto the GPU's routes (orc_model_force_routes)
-        and every sequence's residual after every step is within 2e-2
-        relative (bf16 GPU vs fp32 CPU) — no sequence is excused;
-  (iii) greedy ids equal the oracle's except where the oracle's top1-top2
-        logit margin is below LM_TIE (margins reported).
-The oracle's own free routing is compared too: every layer where it picks
-other experts than the GPU must be a router near-tie (gap < ROUTER_TIE).
+  (ii)  the fp32 oracle (ORC_FP32) is forced onto the GPU's routes
+        (orc_model_force_routes) and every sequence's residual after every
+        step is within 2e-2 relative (bf16 GPU vs fp32 CPU) — no sequence is
+        excused;
+  (iii) a second pass of the oracle in bf16-faithful mode (activations
+        rounded to bf16 where the GPU stores bf16) on the GPU's routes: greedy
+        ids equal except where that oracle's top1-top2 logit margin is below
+        LM_TIE (margins reported).  At 32 layers the fp32 oracle's residual
+        sits ~1 % from any bf16 pipeline, which moves logits by ~0.1; the
+        faithful mode isolates the kernels' own error;
+  (iv)  the oracle's own free routing (faithful pass): every layer where it
+        picks other experts than the GPU is a router near-tie (gap <
+        ROUTER_TIE); the fp32 pass's flips are reported.
+The two oracle passes run one after the other (each holds the 93 GB model).
 """
 import json
 import os
@@ -76,36 +83,42 @@ def test_headline_config_parity():
     t_gpu = time.perf_counter() - t0
 
     t0 = time.perf_counter()
-    m = orc.Model(l, h1, h2, nq, nkv, ne, k, V, N, max_ctx, seed=1234)
-    m.fill_kv(9012, prompt)
-    w_router = [m.tensor(j, orc.T_ROUTER) for j in range(l)]
     report = {"config": "mixtral8x7b-16g", "r_w": cfg["r_w"], "r_w_achieved": info.achieved_weight_ratio,
-              "steps": []}
-    for s, g in enumerate(gpu):
-        # (i) router bit-exact on identical inputs, every layer
-        for j in range(l):
-            _, idx, wts, _, _ = orc.router(g["hn"][j], w_router[j], k)
-            assert np.array_equal(idx, g["topk"][j]), f"step {s} layer {j}: router indices differ"
-            np.testing.assert_allclose(g["topw"][j], wts, rtol=1e-6, atol=1e-7)
-        # (ii) + (iii): oracle on the GPU's routes, teacher-forced tokens
-        m.force_routes(g["topk"])
-        nxt, margin, x_ref = m.decode_step(g["tok"], np.full(N, prompt + s, np.int32), orc.FP32, want_x=True)
-        own, gap = m.route_info()
-        rel = np.linalg.norm(g["x"] - x_ref, axis=1) / np.linalg.norm(x_ref, axis=1)
-        diff = np.nonzero(g["ids"] != nxt)[0]
-        flips = np.argwhere((np.sort(own, axis=2) != np.sort(g["topk"], axis=2)).any(axis=2))
-        flip_gaps = [float(gap[a, b]) for a, b in flips]
-        st = {"step": s, "pos": prompt + s, "max_rel_residual": float(rel.max()),
-              "median_rel_residual": float(np.median(rel)), "id_mismatches": int(diff.size),
-              "id_mismatch_margins": [float(margin[q]) for q in diff],
-              "min_lm_margin": float(margin.min()),
-              "router_free_choice_flips": int(len(flips)), "flip_gaps": flip_gaps}
-        report["steps"].append(st)
-        print(f"\n[headline parity] step {s}: {json.dumps(st)}")
-        assert rel.max() <= RES_TOL, (s, float(rel.max()))
-        for q in diff:
-            assert margin[q] < LM_TIE, f"step {s} seq {q}: id {g['ids'][q]} vs {nxt[q]} at margin {margin[q]:.3f}"
-        assert all(x < ROUTER_TIE for x in flip_gaps), flip_gaps
+              "steps": [{"step": s, "pos": prompt + s} for s in range(STEPS)]}
+    for mode in (orc.FP32, orc.FAITHFUL):
+        tag = "fp32" if mode == orc.FP32 else "faithful"
+        m = orc.Model(l, h1, h2, nq, nkv, ne, k, V, N, max_ctx, seed=1234)
+        m.fill_kv(9012, prompt)
+        if mode == orc.FP32:  # (i) router bit-exact on identical inputs, every layer and step
+            w_router = [m.tensor(j, orc.T_ROUTER) for j in range(l)]
+            for s, g in enumerate(gpu):
+                for j in range(l):
+                    _, idx, wts, _, _ = orc.router(g["hn"][j], w_router[j], k)
+                    assert np.array_equal(idx, g["topk"][j]), f"step {s} layer {j}: router indices differ"
+                    np.testing.assert_allclose(g["topw"][j], wts, rtol=1e-6, atol=1e-7)
+            report["router_bit_exact_layers"] = l * len(gpu)
+            del w_router
+        for s, g in enumerate(gpu):  # the oracle on the GPU's routes, teacher-forced tokens
+            m.force_routes(g["topk"])
+            nxt, margin, x_ref = m.decode_step(g["tok"], np.full(N, prompt + s, np.int32), mode, want_x=True)
+            own, gap = m.route_info()
+            rel = np.linalg.norm(g["x"] - x_ref, axis=1) / np.linalg.norm(x_ref, axis=1)
+            diff = np.nonzero(g["ids"] != nxt)[0]
+            flips = np.argwhere((np.sort(own, axis=2) != np.sort(g["topk"], axis=2)).any(axis=2))
+            flip_gaps = sorted(float(gap[a, b]) for a, b in flips)
+            st = {"max_rel_residual": float(rel.max()), "median_rel_residual": float(np.median(rel)),
+                  "id_mismatches": int(diff.size), "id_mismatch_margins": sorted(float(margin[q]) for q in diff),
+                  "min_lm_margin": float(margin.min()), "router_free_choice_flips": int(len(flips)),
+                  "max_flip_gap": max(flip_gaps, default=0.0)}
+            report["steps"][s][tag] = st
+            print(f"\n[headline parity] step {s} {tag}: {json.dumps(st)}")
+            if mode == orc.FP32:  # (ii)
+                assert rel.max() <= RES_TOL, (s, float(rel.max()))
+            else:  # (iii), (iv)
+                for q in diff:
+                    assert margin[q] < LM_TIE, f"step {s} seq {q}: id {g['ids'][q]} vs {nxt[q]} at margin {margin[q]:.3f}"
+                assert all(x < ROUTER_TIE for x in flip_gaps), flip_gaps
+        del m
     report["gpu_seconds"], report["oracle_seconds"] = t_gpu, time.perf_counter() - t0
     report["oracle_threads"] = orc.lib().orc_num_threads()
     out = os.environ.get("MLT_PARITY_OUT")

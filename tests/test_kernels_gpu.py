@@ -276,6 +276,20 @@ def test_rope_and_paged_attention(K, nq, nkv):
     q = orc.bf16_to_f32(rbn[:, :nq * d])
     ref = orc.attention(q, hist_k, hist_v, ctx, nq, nkv, d)
     assert np.abs(out.cpu().numpy() - ref).max() < 2e-3
+    # split-KV (flash-decoding over CTAs): splits > pages of the short
+    # contexts included (empty splits), auto choice, and the counters must be
+    # left at zero for the next launch
+    scratch = torch.zeros(T * nq * 8 * 130, device="cuda")
+    counters = torch.zeros(T * nkv, dtype=torch.int32, device="cuda")
+    for splits in (2, 3, 8, 0, 8):
+        out2 = torch.zeros_like(out)
+        outp2 = torch.zeros_like(outp)
+        K.gqa_decode_paged_split(ptr(rb), W, ptr(kpool), ptr(vpool), ptr(bt_d), max_pages, ptr(seq),
+                                 ptr(ctx_d), T, nq, nkv, d, page, ptr(outp2), R, ptr(out2), splits, 8,
+                                 ptr(scratch), ptr(counters), stream())
+        torch.cuda.synchronize()
+        assert np.abs(out2.cpu().numpy() - ref).max() < 2e-3, splits
+        assert int(counters.abs().sum()) == 0
 
 
 def test_argmax(K):

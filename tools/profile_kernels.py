@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--with-h2d", action="store_true", help="run a concurrent H2D copy stream")
     ap.add_argument("--codec", action="store_true", help="encoded weight tiles (decoder warps in the GEMM)")
     ap.add_argument("--no-stream-k", action="store_true", help="gate/up without the stream-K tail")
+    ap.add_argument("--dec-groups", type=int, default=0, help="codec decoder groups (0: default)")
     ap.add_argument("--down-splits", type=int, default=0,
                     help="K-splits of the down GEMM (0: the runtime's auto choice, 4 with --codec at 8x7B)")
     a = ap.parse_args()
@@ -114,10 +115,11 @@ def main():
                             b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=1, alpha=1.0,
                             out_packed=inter.data_ptr(), out_R=R, codec=int(a.codec),
                             sk_scratch=None if a.no_stream_k else sk_scratch.data_ptr(),
-                            sk_count=sk_count.data_ptr(), sk_rows=Rmu)
+                            sk_count=sk_count.data_ptr(), sk_rows=Rmu, dec_groups=a.dec_groups)
     dn_args = capi.GemmArgs(a_table=t2.data_ptr(), n_mats=1, G=E, RB=H // 128, K=F, b=inter.data_ptr(), R=R,
                             b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=0, alpha=1.0,
-                            out_f32=y.data_ptr(), ldo=H, codec=int(a.codec), k_splits=ds, split_stride=R * H)
+                            out_f32=y.data_ptr(), ldo=H, codec=int(a.codec), k_splits=ds, split_stride=R * H,
+                            dec_groups=a.dec_groups)
 
     def expert():
         KD.gemm(C.byref(gu_args), s)
@@ -165,6 +167,14 @@ def main():
         KD.gqa_decode_paged(ptr(qrows), W, ptr(kpool), ptr(vpool), ptr(bt), pages_per, ptr(seq),
                             ptr(ctxs), mu, NQ, NKV, D, 16, ptr(attn_out), Rmu, None, s)
 
+    att_scratch = torch.zeros(mu * NQ * 8 * 130, device="cuda")
+    att_cnt = torch.zeros(mu * NKV, dtype=torch.int32, device="cuda")
+
+    def attention_split():  # the runtime's call: split-KV, auto split count
+        KD.gqa_decode_paged_split(ptr(qrows), W, ptr(kpool), ptr(vpool), ptr(bt), pages_per, ptr(seq),
+                                  ptr(ctxs), mu, NQ, NKV, D, 16, ptr(attn_out), Rmu, None, 0, 8,
+                                  ptr(att_scratch), ptr(att_cnt), s)
+
     router()
     torch.cuda.synchronize()
     touched = int((cnt > 0).sum().item())
@@ -172,9 +182,12 @@ def main():
         ("router+permute", router, mu * H * 4 + E * H * 2 + mu * K * 2 * H * 2),
         ("expert_ffn (gate/up+down+combine)", expert,
          touched * 3 * H * F * 2 + mu * K * 2 * H * 2 + mu * H * 2),
+        ("expert gate/up gemm", lambda: KD.gemm(C.byref(gu_args), s), touched * 2 * H * F * 2 + mu * K * H * 2),
+        ("expert down gemm", lambda: KD.gemm(C.byref(dn_args), s), touched * H * F * 2 + mu * K * F * 2),
         ("qkv (norm+gemm)", dense_qkv, W * H * 2 + mu * H * 4),
         ("o_proj (+residual)", dense_o, H * H * 2 + mu * H * 4 * 2),
         ("gqa_decode_paged (ctx 528)", attention, mu * 2 * CTX * NKV * D * 2),
+        ("gqa_decode_paged split-KV (ctx 528)", attention_split, mu * 2 * CTX * NKV * D * 2),
     ]
     reps = 2 if a.once else a.reps
     out = {}
@@ -200,7 +213,7 @@ def main():
         out[name] = {"ms": ms, "alg_bytes": nbytes, "GBps": gbs, "frac_hbm": gbs / peak}
         extra = ""
         if a.codec and name.startswith("expert"):  # bytes actually read: encoded weight tiles
-            wb = touched * 3 * H * F * 2
+            wb = touched * {"expert_ffn": 3, "expert gate/up gemm": 2, "expert down gemm": 1}[name.split(" (")[0]] * H * F * 2
             stored = nbytes - wb + wb * 12432 // 16384
             out[name].update(stored_bytes=stored, stored_GBps=stored / (ms * 1e-3) / 1e9,
                              stored_frac_hbm=stored / (ms * 1e-3) / 1e9 / peak)
