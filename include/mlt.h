@@ -565,6 +565,14 @@ int mlt_runtime_set_positions(mlt_runtime* rt, const int32_t* host_pos);
  * or NULL (teacher forcing), host_out [steps][N] greedy ids. */
 int mlt_runtime_decode(mlt_runtime* rt, const int32_t* host_tokens, const int32_t* host_forced,
                        int steps, int32_t* host_out, mlt_decode_report_t* report);
+/* sim::execute (lightplan/runtime.hpp; replaces sim::simulate, reference
+ * pipesim.hpp:114): run a caller-built schedule — a build_schedule DAG
+ * (mlt_schedule_build*) of this runtime's kind, layers and micro-batches —
+ * instead of the runtime's own.  Decode steps = the DAG's step count;
+ * host_forced / host_out are [steps][N].  MLT_ERR_INVALID for a DAG that does
+ * not match the runtime, MLT_ERR_CYCLE for a cyclic one. */
+int mlt_runtime_execute(mlt_runtime* rt, const mlt_dag* dag, const int32_t* host_tokens,
+                        const int32_t* host_forced, int32_t* host_out, mlt_decode_report_t* report);
 /* The graph the executor runs for `reference` (a build_schedule DAG of this
  * model/policy): same tasks and issue order; with exact_gates the
  * all-pages weight gates (pipesim.cpp:131-148) are replaced by the pages a

@@ -218,6 +218,37 @@ int mlt_runtime_decode(mlt_runtime* r, const int32_t* tokens, const int32_t* for
     });
 }
 
+int mlt_runtime_execute(mlt_runtime* r, const mlt_dag* dag, const int32_t* tokens, const int32_t* forced,
+                        int32_t* out, mlt_decode_report_t* rep) {
+    return guard([&] {
+        if (!dag) throw std::invalid_argument("execute: null dag");
+        Handle* h = H(r);
+        const auto& d0 = *reinterpret_cast<const lightplan::sim::ScheduleDag*>(dag);
+        const mlt::DecodeReport d = h->rt->execute(d0, tokens, forced, out, &h->dag, &h->tl);
+        h->has_tl = true;
+        h->kernels = d.kernels;
+        h->kernel_exec = d.kernel_exec;
+        if (rep) {
+            rep->seconds = d.seconds;
+            rep->tokens_per_second = d.tokens_per_second;
+            rep->measured = {d.measured.link_upload, d.measured.gpu_attention, d.measured.gpu_ffn,
+                             d.measured.cpu_attention, d.measured.cpu_ffn, d.measured.layer_total};
+            rep->h2d_weight_bytes = d.h2d_weight_bytes;
+            rep->h2d_bytes = d.h2d_bytes;
+            rep->d2h_bytes = d.d2h_bytes;
+            rep->steady_layer_time = d.steady_layer_time;
+            for (int i = 0; i < 5; ++i) rep->utilization[i] = d.utilization[i];
+            rep->gpu_launches = d.gpu_launches;
+            rep->timeline_ok = d.verify.empty() ? 1 : 0;
+            rep->expert_ms_total = d.expert_ms_total;
+            rep->expert_launches = d.expert_launches;
+            rep->dense_ms_total = d.qkv_o_ms_total;
+            rep->dense_launches = d.dense_launches;
+        }
+        return MLT_OK;
+    });
+}
+
 int mlt_runtime_kernel_profile(mlt_runtime* r, char* buf, size_t cap) {
     return guard([&] {
         std::string s = "{";

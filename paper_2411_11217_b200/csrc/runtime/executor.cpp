@@ -101,40 +101,61 @@ struct Flags {
 
 }  // namespace
 
+// The reference DAG (lightplan::sim::build_schedule, pipesim.cpp:294-348) of
+// this runtime's schedule kind for `steps` decode steps.  Durations are
+// placeholders: the executor runs in issue order and dependency order only
+// (the weight-upload estimate uses the page bytes at a nominal PCIe rate; it
+// orders nothing).
+ScheduleDag Runtime::schedule(int steps) const {
+    const double link = 55e9;  // nominal; measured durations replace every modeled one
+    return lightplan::sim::build_schedule(
+        [&](int) {
+            lightplan::sim::StepDurations d;
+            d.pre_attn = d.post_attn = d.cpu_attn = d.gpu_attn = 1e-4;
+            d.offload_qkv = d.load_hidden = d.kv_load = 1e-5;
+            d.weight_upload = static_cast<double>(layer_blob_bytes_) / link;
+            d.weight_stage = opt_.pin_weights ? 0.0 : static_cast<double>(layer_blob_bytes_) / link;
+            return d;
+        },
+        schedule_kind(), L_, steps, M_);
+}
+
 DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, int steps, int32_t* out,
                              ScheduleDag* dag_out, Timeline* tl_out) {
     if (steps < 1 || steps > max_steps_) throw std::invalid_argument("steps must be in [1, 64]");
+    return run(schedule(steps), tokens_in, forced, steps, out, dag_out, tl_out);
+}
+
+DecodeReport Runtime::execute(const ScheduleDag& dag, const int32_t* tokens_in, const int32_t* forced, int32_t* out,
+                              ScheduleDag* dag_out, Timeline* tl_out) {
+    // A caller-built DAG must describe THIS runtime's decode: tasks of its
+    // schedule kind over its layers, micro-batches and pages; the step count
+    // is the DAG's.
+    using lightplan::sim::TaskKind;
+    if (dag.tasks.empty()) throw lightplan::sim::EmptyTimelineError("execute: empty schedule");
+    int steps = 0;
+    for (const Task& t : dag.tasks) {
+        steps = std::max(steps, t.step);
+        const bool gpu_attn = t.kind == TaskKind::GpuAttn || t.kind == TaskKind::KvLoad;
+        const bool host_attn = t.kind == TaskKind::CpuAttn || t.kind == TaskKind::OffloadQkv ||
+                               t.kind == TaskKind::LoadHidden;
+        if (t.step < 1 || t.layer < 1 || t.layer > L_ || t.microbatch < 0 || t.microbatch > M_ || t.page < 0 ||
+            t.page > M_ || (gpu_attn && !policy_.attn_on_gpu) || (host_attn && policy_.attn_on_gpu))
+            throw std::invalid_argument("execute: the schedule does not match this runtime's model/policy "
+                                        "(build it with build_schedule for the same layers, micro-batches and A_g)");
+    }
+    if (steps > max_steps_) throw std::invalid_argument("execute: at most 64 decode steps per call");
+    lightplan::sim::simulate(dag);  // acyclic (CycleDetectedError otherwise)
+    return run(dag, tokens_in, forced, steps, out, dag_out, tl_out);
+}
+
+DecodeReport Runtime::run(ScheduleDag dag, const int32_t* tokens_in, const int32_t* forced, int steps, int32_t* out,
+                          ScheduleDag* dag_out, Timeline* tl_out) {
     for (int i = 0; i < N_; ++i)
         if (pos_[i] + steps > max_ctx_) throw std::invalid_argument("KV capacity exceeded (max_ctx)");
     // token ids index the [vocab, h1] embedding on the device: reject bad ids here
     check_token_ids(tokens_in, N_, V_, "tokens_in");
     if (forced) check_token_ids(forced, static_cast<int64_t>(steps) * N_, V_, "forced");
-    // ---- schedule: the reference DAG for this policy (durations modeled) ----
-    lightplan::HardwareSpec hw;  // nominal B200 spec for the modeled durations only
-    hw.gpu_mem_bytes = opt_.budget_bytes;
-    hw.cpu_mem_bytes = 1e15;
-    hw.gpu_bw = 6548.5e9;
-    hw.cpu_bw = 111e9;
-    hw.link_bw = 55.6e9;
-    hw.gpu_flops = 1393e12;
-    hw.cpu_flops = 2e12;
-    lightplan::WorkloadSpec wl;
-    wl.prompt_len = pos_[0];
-    wl.gen_len = steps;
-    const auto kind = schedule_kind();
-    lightplan::Policy pol = policy_;
-    ScheduleDag dag = lightplan::sim::build_schedule(
-        [&](int step) {
-            lightplan::sim::StepDurations d;
-            (void)step;
-            d.pre_attn = d.post_attn = d.cpu_attn = d.gpu_attn = 1e-4;
-            d.offload_qkv = d.load_hidden = d.kv_load = 1e-5;
-            d.weight_upload = static_cast<double>(layer_blob_bytes_) / hw.link_bw;
-            d.weight_stage = opt_.pin_weights ? 0.0 : static_cast<double>(layer_blob_bytes_) / 87e9;
-            return d;
-        },
-        kind, L_, steps, M_);
-    (void)pol;
     const int n = static_cast<int>(dag.tasks.size());
     if (opt_.exact_gates) apply_exact_gates(dag, cat_, M_);
     const auto extra = reuse_edges(dag);

@@ -141,6 +141,14 @@ class Runtime {
     DecodeReport decode(const int32_t* tokens_in, const int32_t* forced, int steps, int32_t* out,
                         lightplan::sim::ScheduleDag* dag_out = nullptr,
                         lightplan::sim::Timeline* timeline_out = nullptr);
+    // The same on a caller-built schedule: `dag` must be a build_schedule DAG
+    // of this runtime's schedule kind, layers and micro-batches (checked);
+    // the number of decode steps is the DAG's (forced/out are [steps][N]).
+    DecodeReport execute(const lightplan::sim::ScheduleDag& dag, const int32_t* tokens_in, const int32_t* forced,
+                         int32_t* out, lightplan::sim::ScheduleDag* dag_out = nullptr,
+                         lightplan::sim::Timeline* timeline_out = nullptr);
+    // The reference DAG this runtime executes for `steps` decode steps.
+    lightplan::sim::ScheduleDag schedule(int steps) const;
 
     // Debug/test taps (device -> host copies, synchronous).
     void read_residual(float* host_out);          // x [N, H] fp32
@@ -177,6 +185,8 @@ class Runtime {
     int launches() const { return launches_; }
 
   private:
+    DecodeReport run(lightplan::sim::ScheduleDag dag, const int32_t* tokens_in, const int32_t* forced, int steps,
+                     int32_t* out, lightplan::sim::ScheduleDag* dag_out, lightplan::sim::Timeline* timeline_out);
     void build_catalog();
     void dense_tiling(int row_blocks, int& n_cap, int& n_chunks, int& k_splits) const;
     static constexpr int kMaxSplits = 8;

@@ -84,6 +84,8 @@ _SIGS = {
     "runtime_read_residual": (C.c_int, [C.c_void_p, C.c_void_p]),
     "runtime_debug_read": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
     "runtime_capture_router": (C.c_int, [C.c_void_p, C.c_int]),
+    "runtime_execute": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.POINTER(DecodeReport)]),
 }
 
 
@@ -179,6 +181,22 @@ class Runtime:
             fp = forced.ctypes.data_as(C.c_void_p)
         self._ck(self.f["runtime_decode"](self.h, tokens.ctypes.data_as(C.c_void_p), fp, steps,
                                           out.ctypes.data_as(C.c_void_p), C.byref(rep)))
+        return Decoded(out, rep)
+
+    def execute(self, dag, tokens, forced=None) -> Decoded:
+        """sim::execute: run a caller-built schedule (a capi.Dag from
+        Api.schedule_build for this model/policy) instead of the runtime's own."""
+        N = self.policy.batch
+        steps = max(t.step for t, _ in dag.tasks())
+        tokens = np.ascontiguousarray(tokens, np.int32).reshape(N)
+        out = np.zeros((steps, N), np.int32)
+        rep = DecodeReport()
+        fp = None
+        if forced is not None:
+            forced = np.ascontiguousarray(forced, np.int32).reshape(steps, N)
+            fp = forced.ctypes.data_as(C.c_void_p)
+        self._ck(self.f["runtime_execute"](self.h, dag.h, tokens.ctypes.data_as(C.c_void_p), fp,
+                                           out.ctypes.data_as(C.c_void_p), C.byref(rep)))
         return Decoded(out, rep)
 
     def timeline(self) -> dict:
