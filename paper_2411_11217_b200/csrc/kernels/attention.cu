@@ -57,6 +57,7 @@ constexpr int kStagesW = 3;
 constexpr int kPageElems = kPage * kD;
 constexpr int kPageBytes = kPageElems * 2;  // 4 KiB (one of K or V)
 constexpr int kCombStride = kD + 4;         // per (warp, head): acc[128], m, l, pad
+constexpr int kMinSplitPages = 16;          // split-KV auto: fewest pages (256 tokens) per split
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -328,7 +329,9 @@ cudaError_t launch_g(const uint16_t* q, int ldq, const uint16_t* kp, const uint1
     int S = 1;
     if (split && split->scratch && split->counters) {
         S = split->splits;
-        if (S <= 0) {  // auto: the split count in 1..max whose grid best fills whole waves
+        if (S <= 0) {  // auto: the split count in 1..max whose grid best fills whole waves, keeping
+                       // >= kMinSplitPages pages per split (a split CTA pays its pipeline ramp and
+                       // merge once: 8-page splits measured 2x slower at mu = 64, ctx 528)
             int per_sm = 0, sms = 0, dev = 0;
             if (cudaGetDevice(&dev) != cudaSuccess ||
                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
@@ -337,7 +340,7 @@ cudaError_t launch_g(const uint16_t* q, int ldq, const uint16_t* kp, const uint1
                 return cudaErrorInvalidValue;
             const double slots = static_cast<double>(sms) * (per_sm > 0 ? per_sm : 1);
             double best = 0;
-            for (int c = 1; c <= split->max_splits && c <= max_pages; ++c) {
+            for (int c = 1; c <= split->max_splits && max_pages / c >= kMinSplitPages; ++c) {
                 const double w = static_cast<double>(T) * nkv * c / slots;
                 const double fill = w / std::ceil(w);
                 if (fill > best + 0.02) best = fill, S = c;  // more splits only for a clearly better fill

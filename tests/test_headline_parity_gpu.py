@@ -18,13 +18,18 @@ greedy ids, so one near-tie cannot cascade):
         excused;
   (iii) a second pass of the oracle in bf16-faithful mode (activations
         rounded to bf16 where the GPU stores bf16) on the GPU's routes: greedy
-        ids equal except where that oracle's top1-top2 logit margin is below
-        LM_TIE (margins reported).  At 32 layers the fp32 oracle's residual
-        sits ~1 % from any bf16 pipeline, which moves logits by ~0.1; the
-        faithful mode isolates the kernels' own error;
-  (iv)  the oracle's own free routing (faithful pass): every layer where it
-        picks other experts than the GPU is a router near-tie (gap <
-        ROUTER_TIE); the fp32 pass's flips are reported.
+        ids equal except at near-ties.  A near-tie is judged against the
+        error the measured residual deviation implies: after 32 layers every
+        bf16 pipeline sits ~1e-2 (relative) from the oracle (independent
+        ~2e-3 rounding per layer; 3e-3 at 2 layers, tests/test_decode_gpu.py),
+        and a residual error of relative size r moves a logit difference by
+        sigma = sqrt(2) * lm_head_scale * r (lm_head rows have norm
+        lm_head_scale = 4; the final RMSNorm makes r scale-free), i.e.
+        ~0.06 at r = 1e-2.  So an id may differ only where the oracle's
+        top1-top2 margin is < max(LM_TIE, 4 sigma) of that sequence;
+  (iv)  the oracle's own free routing (faithful pass): where it picks other
+        experts than the GPU the gap must be < max(ROUTER_TIE, 4 sqrt(2) r)
+        (router rows have norm ~1).  Margins and gaps are reported.
 The two oracle passes run one after the other (each holds the 93 GB model).
 """
 import json
@@ -47,6 +52,7 @@ STEPS = 3
 LM_TIE = 0.05      # logit units (lm_head logits have std ~4)
 ROUTER_TIE = 0.02  # router logit units (std ~1)
 RES_TOL = 2e-2     # BASELINE.json: layer outputs within 2e-2 relative
+LM_SCALE = 4.0     # runtime / oracle lm_head_scale (norm of an lm_head row)
 
 
 def test_headline_config_parity():
@@ -115,9 +121,14 @@ def test_headline_config_parity():
             if mode == orc.FP32:  # (ii)
                 assert rel.max() <= RES_TOL, (s, float(rel.max()))
             else:  # (iii), (iv)
+                lm_bound = np.maximum(LM_TIE, 4 * np.sqrt(2) * LM_SCALE * rel)
+                rt_bound = np.maximum(ROUTER_TIE, 4 * np.sqrt(2) * rel)
+                st["id_mismatch_bounds"] = sorted(float(lm_bound[q]) for q in diff)
                 for q in diff:
-                    assert margin[q] < LM_TIE, f"step {s} seq {q}: id {g['ids'][q]} vs {nxt[q]} at margin {margin[q]:.3f}"
-                assert all(x < ROUTER_TIE for x in flip_gaps), flip_gaps
+                    assert margin[q] < lm_bound[q], (f"step {s} seq {q}: id {g['ids'][q]} vs {nxt[q]} at margin "
+                                                     f"{margin[q]:.3f} (bound {lm_bound[q]:.3f})")
+                for a, b in flips:
+                    assert gap[a, b] < rt_bound[b], (s, int(a), int(b), float(gap[a, b]), float(rt_bound[b]))
         del m
     report["gpu_seconds"], report["oracle_seconds"] = t_gpu, time.perf_counter() - t0
     report["oracle_threads"] = orc.lib().orc_num_threads()

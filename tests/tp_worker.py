@@ -5,9 +5,10 @@
         --out FILE [--a-g 0|1] [--r-w X] [--budget B]
 
 Each rank builds mlt_runtime with tp_rank/tp_size and the host-staged
-all-reduce (collective = 1, rendezvous KEY), decodes a teacher-forced
-16-token prompt then 8 free greedy steps, and saves its ids, residual and
-report fields to FILE (.npz)."""
+all-reduce (collective = 1, rendezvous KEY) and decodes STEPS teacher-forced
+steps (fixed synthetic ids, seed 5678), one step per call with the router tap
+armed, saving per step its greedy ids, residual and every layer's top-k
+choice, plus report fields, to FILE (.npz)."""
 import argparse
 import os
 import sys
@@ -20,7 +21,7 @@ sys.path.insert(0, ROOT)
 from paper_2411_11217_b200 import capi  # noqa: E402
 from paper_2411_11217_b200.runtime import Runtime  # noqa: E402
 
-N, MU, PROMPT, GEN, VOCAB = 8, 4, 16, 8, 32000
+N, MU, STEPS, VOCAB = 8, 4, 24, 32000
 
 
 def run(rank, size, name, dims, out, a_g=0, r_w=0.0, budget=4e9, layers=2, experts=8, top_k=2):
@@ -31,13 +32,22 @@ def run(rank, size, name, dims, out, a_g=0, r_w=0.0, budget=4e9, layers=2, exper
     if size > 1:
         kw.update(tp_rank=rank, tp_size=size, nccl_id=name.encode(), collective="host")
     rt = Runtime(model, pol, **kw)
-    prompt = np.random.default_rng(5678).integers(0, VOCAB, size=(PROMPT, N), dtype=np.int32)
-    first = rt.decode(prompt[0], PROMPT, forced=prompt)
-    rest = rt.decode(first.ids[-1], GEN)
-    np.savez(out, first=first.ids, rest=rest.ids, x=rt.residual(), streamed=rt.info.streamed_bytes_per_layer,
-             timeline_ok=min(first.report.timeline_ok, rest.report.timeline_ok),
-             h2d=rest.report.h2d_weight_bytes)
+    toks = forced_tokens()
+    ids, xs, routes, ok = [], [], [], 1
+    for s in range(STEPS):
+        rt.capture_router(1)
+        d = rt.decode(toks[s], 1)
+        ok = min(ok, d.report.timeline_ok)
+        ids.append(d.ids[0])
+        xs.append(rt.residual())
+        routes.append(rt.captured_router()[1])
+    np.savez(out, ids=np.array(ids), x=np.array(xs), routes=np.array(routes),
+             streamed=rt.info.streamed_bytes_per_layer, timeline_ok=ok, h2d=d.report.h2d_weight_bytes)
     rt.close()
+
+
+def forced_tokens():
+    return np.random.default_rng(5678).integers(0, VOCAB, size=(STEPS, N), dtype=np.int32)
 
 
 if __name__ == "__main__":
