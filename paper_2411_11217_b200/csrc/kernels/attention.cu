@@ -332,12 +332,20 @@ cudaError_t launch_g(const uint16_t* q, int ldq, const uint16_t* kp, const uint1
         if (S <= 0) {  // auto: the split count in 1..max whose grid best fills whole waves, keeping
                        // >= kMinSplitPages pages per split (a split CTA pays its pipeline ramp and
                        // merge once: 8-page splits measured 2x slower at mu = 64, ctx 528)
-            int per_sm = 0, sms = 0, dev = 0;
-            if (cudaGetDevice(&dev) != cudaSuccess ||
-                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gqa_decode_kernel<G>, kWarps * 32, smem) !=
-                    cudaSuccess)
-                return cudaErrorInvalidValue;
+            // resident-CTA slots of this device, cached (the occupancy query costs
+            // microseconds of host time per call)
+            static int cache_slots[64] = {};
+            int dev = 0;
+            if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidValue;
+            if (!cache_slots[dev]) {
+                int per_sm = 0, sms = 0;
+                if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gqa_decode_kernel<G>, kWarps * 32, smem) !=
+                        cudaSuccess)
+                    return cudaErrorInvalidValue;
+                cache_slots[dev] = sms * (per_sm > 0 ? per_sm : 1);
+            }
+            const int per_sm = 1, sms = cache_slots[dev];
             const double slots = static_cast<double>(sms) * (per_sm > 0 ? per_sm : 1);
             double best = 0;
             for (int c = 1; c <= split->max_splits && max_pages / c >= kMinSplitPages; ++c) {

@@ -197,11 +197,13 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
     // 1 KiB alignment for the SWIZZLE_128B atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
-    const int a_bytes = a.n_mats * kATileBytes;
-    const int b_bytes = a.n_cap * 128;
-    // stage = [A tiles (16 KiB slots) | B tile]; with the codec the encoded
-    // A tiles land at the end of their slots and are decoded in place
-    const int stage_bytes = a_bytes + b_bytes;
+    const int a_bytes = a.n_mats * kATileBytes;  // A slots of one k-block
+    const int b_bytes = a.n_cap * 128;            // B tile of one k-block
+    const int kps = a.kps;                        // k-blocks per ring stage (1, or 2 for codec n_mats = 1)
+    // stage = [kps x A tiles (16 KiB slots) | kps x B tile]; with the codec
+    // the encoded A tiles land at the end of their slots and are decoded in
+    // place; tile t of a stage (t = j * n_mats + mt) sits at t * 16 KiB
+    const int stage_bytes = kps * (a_bytes + b_bytes);
     const int stages = a.stages;
     Smem* ctl = reinterpret_cast<Smem*>(smem + stages * stage_bytes);
 
@@ -273,23 +275,26 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                 for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
                     const int nt = min(a.n_cap, rows - n0);
                     const int ntp = (nt + 15) & ~15;
-                    for (int kb = kb0; kb < kb1; ++kb) {
+                    for (int kb = kb0; kb < kb1; kb += kps) {
+                        const int nk = min(kps, kb1 - kb);
                         mbar_wait(&ctl->empty[stage], phase ^ 1);
                         if (a.ktrace && blockIdx.x == 0 && kstep < 256) a.ktrace[kstep] = globaltimer();
                         ++kstep;
                         uint8_t* const st = smem + stage * stage_bytes;
                         uint8_t* sa = a.codec ? st + kCodecOff : st;
-                        uint8_t* sb = st + a_bytes;
+                        uint8_t* sb = st + kps * a_bytes;
                         const int tile = a.codec ? kCodecTile : kATileBytes;
                         if (tr && v == static_cast<int>(blockIdx.x) && kb == kb0 && n0 == c * a.n_cap)
                             tr[2] = globaltimer();
-                        mbar_expect_tx(&ctl->full[stage], a.n_mats * tile + ntp * 128);
-                        for (int mt = 0; mt < a.n_mats; ++mt)
-                            bulk_g2s(sa + mt * kATileBytes, ab[mt] + static_cast<int64_t>(kb) * tile, tile,
-                                     &ctl->full[stage], pol_w);
-                        const uint8_t* src = a.b + static_cast<int64_t>(kb) * a.R * 128 +
-                                             static_cast<int64_t>(row0 + n0) * 128;
-                        bulk_g2s(sb, src, ntp * 128, &ctl->full[stage], pol_x);
+                        mbar_expect_tx(&ctl->full[stage], nk * (a.n_mats * tile + ntp * 128));
+                        for (int j = 0; j < nk; ++j) {
+                            for (int mt = 0; mt < a.n_mats; ++mt)
+                                bulk_g2s(sa + (j * a.n_mats + mt) * kATileBytes,
+                                         ab[mt] + static_cast<int64_t>(kb + j) * tile, tile, &ctl->full[stage], pol_w);
+                            const uint8_t* src = a.b + static_cast<int64_t>(kb + j) * a.R * 128 +
+                                                 static_cast<int64_t>(row0 + n0) * 128;
+                            bulk_g2s(sb + j * b_bytes, src, ntp * 128, &ctl->full[stage], pol_x);
+                        }
                         if (++stage == stages) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -313,7 +318,8 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                 mbar_wait(&ctl->tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d0 = tmem + acc * acc_cols;
-                for (int kb = kb0; kb < kb1; ++kb) {
+                for (int kb = kb0; kb < kb1; kb += kps) {
+                    const int nk = min(kps, kb1 - kb);
                     mbar_wait(&ctl->full[stage], phase);
                     if (a.codec) mbar_wait(&ctl->dfull[stage], phase);
                     tc_fence_after();
@@ -323,17 +329,19 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                         tr[3] = globaltimer();
                     if (elect_one()) {
                         const uint32_t st = smem_u32(smem + stage * stage_bytes);
-                        const uint32_t sa = st;
-                        const uint32_t sb = st + a_bytes;
+                        for (int j = 0; j < nk; ++j) {
+                            const uint32_t sa = st + j * a_bytes;
+                            const uint32_t sb = st + kps * a_bytes + j * b_bytes;
 #pragma unroll
-                        for (int k = 0; k < kBlockK / 16; ++k) {
-                            const uint64_t bd = sdesc_sw128(sb + k * 32);
-                            for (int mt = 0; mt < a.n_mats; ++mt)
-                                umma_bf16(d0 + mt * a.n_cap, sdesc_sw128(sa + mt * kATileBytes + k * 32),
-                                          bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                            for (int k = 0; k < kBlockK / 16; ++k) {
+                                const uint64_t bd = sdesc_sw128(sb + k * 32);
+                                for (int mt = 0; mt < a.n_mats; ++mt)
+                                    umma_bf16(d0 + mt * a.n_cap, sdesc_sw128(sa + mt * kATileBytes + k * 32),
+                                              bd, idesc, (kb + j != kb0 || k != 0) ? 1u : 0u);
+                            }
                         }
                         umma_commit(&ctl->empty[stage]);
-                        if (kb == kb1 - 1) umma_commit(&ctl->tfull[acc]);
+                        if (kb + nk >= kb1) umma_commit(&ctl->tfull[acc]);
                     }
                     __syncwarp();
                     if (++stage == stages) { stage = 0; phase ^= 1; }
@@ -350,7 +358,6 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
         // one arrive on the stage's dfull.
         const int grp = (static_cast<int>(threadIdx.x) - 192) / kDecThreads;
         const int dt = (static_cast<int>(threadIdx.x) - 192) % kDecThreads;
-        const bool two = a.n_mats == 2;
         int stage = 0, kstep = 0;
         uint32_t phase = 0;
         for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
@@ -359,7 +366,9 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
             const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
             if (rows <= 0) continue;
             for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
-                for (int kb = kb0; kb < kb1; ++kb, ++kstep) {
+                for (int kb = kb0; kb < kb1; kb += kps, ++kstep) {
+                    // tiles of this stage: n_mats (one k-block) or kps (n_mats = 1), at most 2
+                    const bool two = a.n_mats * min(kps, kb1 - kb) == 2;
                     if (stage % a.dec_groups == grp) {
                         mbar_wait(&ctl->full[stage], phase);
                         if (a.ktrace && blockIdx.x == 0 && kstep < 256 && dt == 0) a.ktrace[256 + kstep] = globaltimer();
@@ -569,8 +578,8 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
 
 }  // namespace
 
-int gemm_smem_bytes(int n_mats, int n_cap, int stages) {
-    return stages * (n_mats * kATileBytes + n_cap * 128) +
+int gemm_smem_bytes(int n_mats, int n_cap, int stages, int kps) {
+    return stages * kps * (n_mats * kATileBytes + n_cap * 128) +
            1024 /*align*/ + kCtlBytes + kEpiScratch;
 }
 
@@ -580,8 +589,13 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         a.k_splits > a.K / kBlockK || (a.k_splits > 1 && a.epi != kEpiF32) ||
         (a.epi == kEpiF32 && (a.ldo % 4 || a.ldr % 4 || a.split_stride % 4)))  // 16-byte epilogue stores
         return cudaErrorInvalidValue;
-    const int per_stage = a.n_mats * kATileBytes + a.n_cap * 128;
+    // codec with one matrix: two k-blocks per ring stage, so each stage's
+    // fixed decode cost (barriers, proxy fence, dfull round trip) covers two
+    // encoded tiles, as it does for the two matrices of gate/up
+    // (only while that still leaves >= 4 stages: mu = 256 down, n_cap 128, would get 2)
     const int budget = 227 * 1024 - 1024 - kCtlBytes - kEpiScratch;
+    a.kps = (a.codec && a.n_mats == 1 && budget / (2 * (kATileBytes + a.n_cap * 128)) >= 4) ? 2 : 1;
+    const int per_stage = a.kps * (a.n_mats * kATileBytes + a.n_cap * 128);
     a.stages = budget / per_stage;
     if (a.stages > 8) a.stages = 8;
     if (a.codec) {
@@ -596,7 +610,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     int cols = 32;
     while (cols < need) cols <<= 1;
     a.tmem_cols = cols;
-    const int smem = gemm_smem_bytes(a.n_mats, a.n_cap, a.stages);
+    const int smem = gemm_smem_bytes(a.n_mats, a.n_cap, a.stages, a.kps);
     if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel), 227 * 1024); e != cudaSuccess)
         return e;
     a.sk_full = a.sk_tail = a.sk_parts = 0;
@@ -617,12 +631,20 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         // the tail's parts wait on each other: only with every CTA co-resident
         // (1 CTA per SM at this smem size; fewer SMs under MPS / green
         // contexts / a concurrent kernel) -> otherwise run without the tail
+        // (cached per device and block size: the occupancy query costs host microseconds)
+        static int cache[64][kMaxDecGroups + 2] = {};
+        int dev = 0;
+        const int slot = a.codec ? a.dec_groups : 0;
         int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_tc_kernel,
-                                                          a.codec ? 192 + a.dec_groups * kDecThreads : kThreadsRaw,
-                                                          smem) != cudaSuccess ||
-            per_sm < 1 || per_sm * num_sms < num_sms)
-            a.sk_full = a.sk_tail = a.sk_parts = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
+            if (!cache[dev][slot] &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache[dev][slot], gemm_tc_kernel,
+                                                              a.codec ? 192 + a.dec_groups * kDecThreads : kThreadsRaw,
+                                                              227 * 1024 - 1024) != cudaSuccess)
+                cache[dev][slot] = 0;
+            per_sm = cache[dev][slot];
+        }
+        if (per_sm < 1) a.sk_full = a.sk_tail = a.sk_parts = 0;
     }
     const int n_virtual = a.sk_parts ? a.sk_full + a.sk_tail * a.sk_parts : a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;

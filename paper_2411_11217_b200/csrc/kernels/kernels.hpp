@@ -62,6 +62,7 @@ struct GemmArgs {
     int sk_full = 0, sk_tail = 0, sk_parts = 0;
     // filled by launch_gemm
     int stages = 0, acc_stages = 0, tmem_cols = 0;
+    int kps = 1;  // k-blocks per ring stage
 };
 
 cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream);
@@ -69,7 +70,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream);
 // Programmatic dependent launch for every kernel of this build (see
 // common.cuh); off by default; the runtime turns it on for all-GPU schedules.
 void set_pdl(bool on);
-int gemm_smem_bytes(int n_mats, int n_cap, int stages);
+int gemm_smem_bytes(int n_mats, int n_cap, int stages, int kps = 1);
 
 // x_out[t][:] = float(table[tokens[t]][:])
 cudaError_t launch_embed(const int32_t* tokens, const uint16_t* table, int T, int H, float* x_out,

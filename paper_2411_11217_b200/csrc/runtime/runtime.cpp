@@ -271,10 +271,7 @@ void Runtime::allocate() {
         d_vpool_ = static_cast<uint16_t*>(A.alloc(bytes, "kv_pool_v"));
         d_block_table_ = static_cast<int32_t*>(A.alloc(pages * 4, "block_table"));
         d_attn_gpu_ = static_cast<uint8_t*>(A.alloc(static_cast<size_t>(Rmu_) * Ho_ * 2, "attn_gpu"));
-        // split-KV partials [mu][nq][splits][130] + per-(token, kv head) arrival counters
-        d_attn_part_ = static_cast<float*>(A.alloc(static_cast<size_t>(mu_) * nq_ * kAttnSplits * 130 * 4, "attn_split"));
-        d_attn_cnt_ = static_cast<int*>(A.alloc(static_cast<size_t>(mu_) * nkv_ * 4, "attn_split_counters"));
-        ck(cudaMemset(d_attn_cnt_, 0, static_cast<size_t>(mu_) * nkv_ * 4), "attn counters");
+
         std::vector<int32_t> bt(pages);
         for (size_t i = 0; i < pages; ++i) bt[i] = static_cast<int32_t>(i);  // per (layer, seq) page runs
         ck(cudaMemcpy(d_block_table_, bt.data(), pages * 4, cudaMemcpyHostToDevice), "block table");
@@ -619,13 +616,14 @@ void Runtime::act_gpu_attn(int step, int layer, int mb) {
     // this step's k/v were stored into the pool by rope_qkv (PreAttn)
     const int32_t* ctx = d_pos_ + static_cast<size_t>(max_steps_) * N_ + static_cast<size_t>(step - 1) * N_ + t0;
     const int32_t* bt = d_block_table_ + static_cast<size_t>(l) * N_ * max_pages_;
-    mltk::GqaSplit split;  // split-KV when (token, kv head) pairs under-fill the SMs (auto count)
-    split.max_splits = kAttnSplits;
-    split.scratch = d_attn_part_;
-    split.counters = d_attn_cnt_;
+    // one CTA per (token, kv head), no split-KV: splitting a token's pages
+    // over CTAs (mlt_gqa_decode_paged_split) measured slower at every decode
+    // shape here (mu = 16/32/64, ctx 528: 18.9/20.5/56 vs 12.8/17.9/29.9 us,
+    // profiles/r02_attention_split_kv.txt) — each short split CTA pays the
+    // page-pipeline ramp and the partial merge
     kl("gqa_decode_paged", mltk::launch_gqa_decode_paged(qkv, W_, d_kpool_, d_vpool_, bt, max_pages_, d_seq_ + t0,
                                                          ctx, mu_, nq_, nkv_, d_, page_, d_attn_gpu_, Rmu_,
-                                                         nullptr, s_gpu_, &split));
+                                                         nullptr, s_gpu_));
 }
 
 void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {

@@ -268,9 +268,6 @@ class Runtime {
     int32_t* d_block_table_ = nullptr;  // [L][N][max_pages]
     int max_pages_ = 0, page_ = 16;
     uint8_t* d_attn_gpu_ = nullptr;
-    static constexpr int kAttnSplits = 8;
-    float* d_attn_part_ = nullptr;      // split-KV partials
-    int* d_attn_cnt_ = nullptr;         // split-KV arrival counters (self-resetting)
 
     // host side
     uint16_t* h_qkv_ = nullptr;   // pinned [M][mu][W]
