@@ -308,6 +308,17 @@ int mlt_pack_weight(const uint16_t* host_src, int64_t M, int64_t K, uint16_t* ho
 int mlt_codec_encode(const uint8_t* host_packed, int64_t M, int64_t K, uint8_t* host_out);
 int mlt_codec_decode(const uint8_t* host_enc, int64_t tiles, uint8_t* host_packed);
 int mlt_codec_tile_bytes(void);
+/* The fragment-order code of the register-decode GEMM (GemmArgs codec = 2,
+ * kernels/gemm_codec.cu; runtime/weight_codec.hpp frag_from_packed): encode a
+ * packed [M, K] matrix row block by row block.  A row block with a tile the
+ * code cannot hold is stored raw instead (K/64 tiles of 16 KiB in fragment
+ * order) when raw_blocks (uint8[M/128], set to 1 for such blocks) is given;
+ * without it that is MLT_ERR_INVALID.  Row block r starts at the sum of the
+ * previous blocks' sizes.  Returns the number of raw blocks (>= 0). */
+int mlt_codec_encode_frag(const uint8_t* host_packed, int64_t M, int64_t K, uint8_t* host_out,
+                          uint8_t* raw_blocks);
+/* 16 KiB packed tiles -> fragment-order bf16 tiles (raw codec-2 blocks). */
+int mlt_frag_pack(const uint8_t* host_packed, int64_t tiles, uint8_t* host_out);
 /* Host-core GQA decode attention (A_g = 0: the CpuAttn task, pipesim.hpp:26,
  * PAPER.md:390-392/553; cost model cpu_attention, planner.cpp:42-44) — the
  * runtime's CpuAttn kernel on caller buffers.  q [T][nq][d] bf16 (roped);
@@ -353,14 +364,19 @@ typedef struct mlt_gemm_args_t {
                                   full, last MMA issued, first accumulator ready, epilogue
                                   done, exit) — a diagnostic, NULL in production */
     int32_t codec;             /* 1: every A row block is encoded (12432 B per 64-k tile, see
-                                  mlt_codec_encode_tile), expanded in smem by decoder warps */
+                                  mlt_codec_encode), expanded in smem by decoder warps (tcgen05);
+                                  2: fragment-order encoded blocks (mlt_codec_encode_frag), decoded
+                                  in registers and multiplied with mma.sync (n_cap <= 64, <= 32
+                                  for n_mats = 2; kernels/gemm_codec.cu) */
     unsigned long long* ktrace; /* optional CTA-0 pipeline trace [4][256] %globaltimer stamps per
                                    k-block: producer issue, decoder start, decoder done, MMA start */
     float* sk_scratch;         /* optional stream-K tail for epi = 1 (n_chunks = k_splits = 1): fp32
                                   scratch [#SMs][2][sk_rows][128]; NULL disables it */
     int64_t* sk_count;         /* [#SMs] 64-bit arrival counters, zeroed once by the caller */
     int32_t sk_rows;           /* row capacity per group for the scratch (>= max rows of a group) */
-    int32_t dec_groups;        /* codec: decoder groups of 4 warps (2..4; 0 -> the default) */
+    int32_t dec_groups;        /* codec 1: decoder groups of 4 warps (2; 0 -> the default) */
+    int32_t codec_raw;         /* codec 2: 1 when a page-table entry may carry tag bit 0 (a raw
+                                  fragment-order block, mlt_codec_encode_frag raw_blocks) */
 } mlt_gemm_args_t;
 
 /* Grouped swap-AB tcgen05 GEMM (SURVEY.md §2c expert_gateup_silu /

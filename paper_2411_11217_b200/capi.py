@@ -565,7 +565,7 @@ class GemmArgs(C.Structure):
                 ("n_chunks", C.c_int32), ("k_splits", C.c_int32), ("split_stride", C.c_int64),
                 ("trace", C.c_void_p), ("codec", C.c_int32), ("ktrace", C.c_void_p),
                 ("sk_scratch", C.c_void_p), ("sk_count", C.c_void_p), ("sk_rows", C.c_int32),
-                ("dec_groups", C.c_int32)]
+                ("dec_groups", C.c_int32), ("codec_raw", C.c_int32)]
 
 
 V, I, F = C.c_void_p, C.c_int, C.c_float
@@ -573,6 +573,8 @@ _KSIGS = {
     "pack_weight": [V, C.c_int64, C.c_int64, V],
     "codec_encode": [V, C.c_int64, C.c_int64, V],
     "codec_decode": [V, C.c_int64, V],
+    "codec_encode_frag": [V, C.c_int64, C.c_int64, V, V],
+    "frag_pack": [V, C.c_int64, V],
     "host_gqa_decode": [V, V, V, V, I, I, I, I, I, V, I],
     "host_gqa_use_amx": [I],
     "unpack_rows": [V, C.c_int64, C.c_int64, C.c_int64, V],

@@ -80,6 +80,7 @@ mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
     g.sk_count = reinterpret_cast<unsigned long long*>(a->sk_count);
     g.sk_rows = a->sk_rows;
     if (a->dec_groups > 0) g.dec_groups = a->dec_groups;
+    g.codec_raw = a->codec_raw;
     return g;
 }
 
@@ -118,6 +119,51 @@ int mlt_codec_decode(const uint8_t* enc, int64_t tiles, uint8_t* packed) {
 }
 
 int mlt_codec_tile_bytes(void) { return mlt::kCodecTileBytes; }
+
+int mlt_codec_encode_frag(const uint8_t* packed, int64_t M, int64_t K, uint8_t* out, uint8_t* raw_blocks) {
+    return guard([&] {
+        if (M % 128 || K % 64 || M <= 0 || K <= 0) throw std::invalid_argument("codec_encode_frag: M%128, K%64");
+        const int64_t kb = K / 64, rbs = M / 128;
+        // per row block: encoded tiles, or (raw_blocks given) 16 KiB fragment-order tiles when a tile fails
+        std::vector<int64_t> off(rbs + 1, 0);
+        std::vector<uint8_t> raw(rbs, 0);
+        int bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+        for (int64_t r = 0; r < rbs; ++r) {
+            uint8_t tmp[mlt::kCodecTileBytes];
+            for (int64_t t = 0; t < kb; ++t)
+                if (!mlt::codec_encode_frag_tile(packed + (r * kb + t) * 16384, tmp)) {
+                    raw[r] = 1;
+                    ++bad;
+                    break;
+                }
+        }
+        if (bad && !raw_blocks)
+            throw std::invalid_argument("codec_encode_frag: " + std::to_string(bad) + " row block(s) need > " +
+                                        std::to_string(mlt::kCodecMaxEscapes) + " escapes in a tile");
+        for (int64_t r = 0; r < rbs; ++r) off[r + 1] = off[r] + kb * (raw[r] ? 16384 : mlt::kCodecTileBytes);
+#pragma omp parallel for schedule(static)
+        for (int64_t r = 0; r < rbs; ++r)
+            for (int64_t t = 0; t < kb; ++t) {
+                const uint8_t* src = packed + (r * kb + t) * 16384;
+                if (raw[r])
+                    mlt::frag_from_packed(src, reinterpret_cast<uint16_t*>(out + off[r] + t * 16384));
+                else
+                    mlt::codec_encode_frag_tile(src, out + off[r] + t * mlt::kCodecTileBytes);
+            }
+        if (raw_blocks) std::memcpy(raw_blocks, raw.data(), static_cast<size_t>(rbs));
+        return static_cast<int>(bad);
+    });
+}
+
+int mlt_frag_pack(const uint8_t* packed, int64_t tiles, uint8_t* out) {
+    return guard([&] {
+#pragma omp parallel for schedule(static)
+        for (int64_t t = 0; t < tiles; ++t)
+            mlt::frag_from_packed(packed + t * 16384, reinterpret_cast<uint16_t*>(out + t * 16384));
+        return MLT_OK;
+    });
+}
 
 int mlt_host_gqa_use_amx(int enable) { return mlt::host_gqa_set_amx(enable != 0) ? 1 : 0; }
 

@@ -35,7 +35,7 @@ constexpr int kThreadsRaw = 192;    // warp0 producer, warp1 MMA, warps2-5 epilo
 // barrier two phases ahead (mbarrier parity would alias).  Codec launches
 // round the stage count to a multiple of the group count (GemmArgs::dec_groups,
 // 2..kMaxDecGroups: more groups = more tiles decoding concurrently).
-constexpr int kMaxDecGroups = 4;
+constexpr int kMaxDecGroups = 2;  // 3-4 groups measured no faster (r02 profiles) and cost registers
 constexpr int kDecThreads = 128;  // threads per decoder group
 constexpr int kThreadsCodec = 192 + kMaxDecGroups * kDecThreads;  // launch bound; warps 6+: decoders
 constexpr int kCodecTile = 12432;   // encoded tile bytes (runtime/weight_codec.hpp)
@@ -152,6 +152,16 @@ __device__ __forceinline__ void store_tile(const TileIn& in, uint32_t d, int dt)
     }
 }
 
+// Page-table entries of an encoded (codec = 1) GEMM may carry tag bit 0: that
+// 128-row block is stored as raw bf16 tiles (16 KiB each), the per-block
+// fallback for weights the code cannot hold (runtime: codec_encode_tile
+// fails) — copied straight into its A slot, never decoded.
+__device__ __forceinline__ const uint8_t* untag(const uint8_t* p, bool& raw) {
+    const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+    raw = (u & 1u) != 0;
+    return reinterpret_cast<const uint8_t*>(u & ~static_cast<uintptr_t>(1));
+}
+
 // Virtual task v -> (group, row block, token chunk, k-block range).  With
 // the stream-K tail enabled, tasks past sk_full are (tail tile, K part).
 struct VTask {
@@ -236,10 +246,11 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
         const int u = static_cast<int>(blockIdx.x) / a.k_splits, ks = static_cast<int>(blockIdx.x) % a.k_splits;
         const int g = (u / a.n_chunks) % a.G, rb = u / a.n_chunks / a.G;
         const int KBt = a.K / kBlockK, kb0 = ks * KBt / a.k_splits;
-        const int tile = a.codec ? kCodecTile : kATileBytes;
         const int nkb = min(4, (ks + 1) * KBt / a.k_splits - kb0);
         for (int mt = 0; mt < a.n_mats; ++mt) {
-            const uint8_t* p = a.a_table[(static_cast<int64_t>(mt) * a.G + g) * a.RB + rb];
+            bool raw;
+            const uint8_t* p = untag(a.a_table[(static_cast<int64_t>(mt) * a.G + g) * a.RB + rb], raw);
+            const int tile = (a.codec && !raw) ? kCodecTile : kATileBytes;
             prefetch_l2(p + static_cast<int64_t>(kb0) * tile, static_cast<uint32_t>(nkb * tile));
         }
     }
@@ -270,8 +281,14 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                 if (rows <= 0) continue;
                 const int row0 = a.b_off ? a.b_off[g] : 0;
                 const uint8_t* ab[kMaxMats];
-                for (int mt = 0; mt < a.n_mats; ++mt)
-                    ab[mt] = a.a_table[(static_cast<int64_t>(mt) * a.G + g) * a.RB + rb];
+                int tile_b[kMaxMats], slot_off[kMaxMats], tx = 0;  // per matrix: stored tile bytes, offset in slot
+                for (int mt = 0; mt < a.n_mats; ++mt) {
+                    bool raw;
+                    ab[mt] = untag(a.a_table[(static_cast<int64_t>(mt) * a.G + g) * a.RB + rb], raw);
+                    tile_b[mt] = (a.codec && !raw) ? kCodecTile : kATileBytes;
+                    slot_off[mt] = (a.codec && !raw) ? kCodecOff : 0;
+                    tx += tile_b[mt];
+                }
                 for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
                     const int nt = min(a.n_cap, rows - n0);
                     const int ntp = (nt + 15) & ~15;
@@ -281,16 +298,15 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
                         if (a.ktrace && blockIdx.x == 0 && kstep < 256) a.ktrace[kstep] = globaltimer();
                         ++kstep;
                         uint8_t* const st = smem + stage * stage_bytes;
-                        uint8_t* sa = a.codec ? st + kCodecOff : st;
                         uint8_t* sb = st + kps * a_bytes;
-                        const int tile = a.codec ? kCodecTile : kATileBytes;
                         if (tr && v == static_cast<int>(blockIdx.x) && kb == kb0 && n0 == c * a.n_cap)
                             tr[2] = globaltimer();
-                        mbar_expect_tx(&ctl->full[stage], nk * (a.n_mats * tile + ntp * 128));
+                        mbar_expect_tx(&ctl->full[stage], nk * (tx + ntp * 128));
                         for (int j = 0; j < nk; ++j) {
                             for (int mt = 0; mt < a.n_mats; ++mt)
-                                bulk_g2s(sa + (j * a.n_mats + mt) * kATileBytes,
-                                         ab[mt] + static_cast<int64_t>(kb + j) * tile, tile, &ctl->full[stage], pol_w);
+                                bulk_g2s(st + (j * a.n_mats + mt) * kATileBytes + slot_off[mt],
+                                         ab[mt] + static_cast<int64_t>(kb + j) * tile_b[mt], tile_b[mt],
+                                         &ctl->full[stage], pol_w);
                             const uint8_t* src = a.b + static_cast<int64_t>(kb + j) * a.R * 128 +
                                                  static_cast<int64_t>(row0 + n0) * 128;
                             bulk_g2s(sb + j * b_bytes, src, ntp * 128, &ctl->full[stage], pol_x);
@@ -365,24 +381,30 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
             const int c = tk.c, g = tk.g, kb0 = tk.kb0, kb1 = tk.kb1;
             const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
             if (rows <= 0) continue;
+            bool raw_m[kMaxMats] = {false, false};  // raw-fallback blocks: nothing to decode
+            for (int mt = 0; mt < a.n_mats; ++mt)
+                untag(a.a_table[(static_cast<int64_t>(mt) * a.G + tk.g) * a.RB + tk.rb], raw_m[mt]);
             for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
                 for (int kb = kb0; kb < kb1; kb += kps, ++kstep) {
-                    // tiles of this stage: n_mats (one k-block) or kps (n_mats = 1), at most 2
+                    // tiles of this stage: n_mats (one k-block) or kps (n_mats = 1), at most 2;
+                    // tile t belongs to matrix t (n_mats = 2) or matrix 0 (n_mats = 1)
                     const bool two = a.n_mats * min(kps, kb1 - kb) == 2;
+                    const bool dec0 = !raw_m[0], dec1 = two && !raw_m[a.n_mats == 2 ? 1 : 0];
                     if (stage % a.dec_groups == grp) {
                         mbar_wait(&ctl->full[stage], phase);
                         if (a.ktrace && blockIdx.x == 0 && kstep < 256 && dt == 0) a.ktrace[256 + kstep] = globaltimer();
                         const uint32_t sa = smem_u32(smem + stage * stage_bytes);
                         TileIn in0, in1;
-                        load_tile(sa + kCodecOff, dt, in0);
-                        if (two) load_tile(sa + kATileBytes + kCodecOff, dt, in1);
+                        in0.n = in1.n = 0;
+                        if (dec0) load_tile(sa + kCodecOff, dt, in0);
+                        if (dec1) load_tile(sa + kATileBytes + kCodecOff, dt, in1);
                         decoders_sync(grp);  // all inputs read: the slots may be overwritten
-                        store_tile(in0, sa, dt);
-                        if (two) store_tile(in1, sa + kATileBytes, dt);
-                        if (in0.n + (two ? in1.n : 0u)) {  // rare: high bytes outside the table
+                        if (dec0) store_tile(in0, sa, dt);
+                        if (dec1) store_tile(in1, sa + kATileBytes, dt);
+                        if (in0.n + in1.n) {  // rare: high bytes outside the table
                             decoders_sync(grp);
                             if (static_cast<uint32_t>(dt) < in0.n) sts8(sa + 2 * (in0.esc & 0xffffu) + 1, in0.esc >> 16);
-                            if (two && static_cast<uint32_t>(dt) < in1.n)
+                            if (static_cast<uint32_t>(dt) < in1.n)
                                 sts8(sa + kATileBytes + 2 * (in1.esc & 0xffffu) + 1, in1.esc >> 16);
                         }
                         fence_proxy_async_smem();  // generic smem writes -> visible to tcgen05.mma
@@ -584,6 +606,7 @@ int gemm_smem_bytes(int n_mats, int n_cap, int stages, int kps) {
 }
 
 cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
+    if (a.codec == 2) return launch_gemm_codec(a, num_sms, stream);
     if (a.n_mats < 1 || a.n_mats > kMaxMats || a.K % kBlockK || a.n_cap % 16 || a.n_cap < 16 ||
         a.n_cap > 256 || a.R % 16 || a.n_chunks < 1 || a.k_splits < 1 ||
         a.k_splits > a.K / kBlockK || (a.k_splits > 1 && a.epi != kEpiF32) ||
@@ -602,7 +625,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         if (a.dec_groups < 2 || a.dec_groups > kMaxDecGroups) return cudaErrorInvalidValue;
         a.stages -= a.stages % a.dec_groups;  // decoder groups own whole stages
     }
-    if (a.codec != 0 && a.codec != 1) return cudaErrorInvalidValue;
+    if (a.codec != 0 && a.codec != 1) return cudaErrorInvalidValue;  // 2 dispatched above
     if (a.stages < 2) return cudaErrorInvalidValue;
     const int acc_cols = a.n_mats * a.n_cap;
     a.acc_stages = (2 * acc_cols <= 512) ? 2 : 1;

@@ -35,7 +35,11 @@ struct GemmArgs {
     // 1: A row blocks are encoded tiles (runtime/weight_codec.hpp, 12432 B
     // per 64-k tile); decoder warps expand them in shared memory
     int codec = 0;
-    int dec_groups = 2;  // codec: decoder groups of 4 warps (2..4), each owning every dec_groups-th stage
+    int dec_groups = 2;  // codec 1: decoder groups of 4 warps, each owning every dec_groups-th stage
+    // codec 2 (fragment-order tiles, gemm_codec.cu: decode in registers,
+    // mma.sync): 1 when some page-table entry of this GEMM is a raw fallback
+    // block (tag bit 0; 16 KiB ring slots instead of 12432 B)
+    int codec_raw = 0;
     // optional CTA-0 pipeline trace [4][256] (%globaltimer): producer issue,
     // decoder start, decoder done, MMA start per k-block (diagnostic)
     unsigned long long* ktrace = nullptr;
@@ -65,7 +69,9 @@ struct GemmArgs {
     int kps = 1;  // k-blocks per ring stage
 };
 
+// Dispatches codec = 2 to launch_gemm_codec (gemm_codec.cu).
 cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream);
+cudaError_t launch_gemm_codec(GemmArgs a, int num_sms, cudaStream_t stream);
 
 // Programmatic dependent launch for every kernel of this build (see
 // common.cuh); off by default; the runtime turns it on for all-GPU schedules.

@@ -19,7 +19,8 @@ struct WeightBlock {
     int expert;
     int rb;         // row block
     int64_t K;      // reduction length
-    int64_t bytes;  // 128 * K * 2
+    int64_t bytes;  // 128 * K * 2, or the encoded size (codec)
+    bool raw;       // codec: stored as raw bf16 tiles (per-block fallback, tagged page-table entry)
     bool resident;
     int64_t offset;  // resident: offset in the layer's resident region; streamed: in the layer blob
 };
@@ -61,8 +62,11 @@ ShardMap shard_map(const lightplan::ModelSpec& model, const Shard& shard, int ki
 // codec: blocks are stored encoded (weight_codec.hpp: 12432 B per 64-k tile
 // instead of 16384), so the same r_w share holds more weights and the pages
 // stream fewer bytes.
+// raw_mask (codec only): raw_mask[i] != 0 stores catalog block i as raw
+// 16 KiB tiles in every layer — the fallback for weights the code cannot hold.
 Catalog build_catalog(const lightplan::ModelSpec& model, const lightplan::Policy& policy,
-                      const Shard& shard = Shard{}, bool codec = false);
+                      const Shard& shard = Shard{}, bool codec = false,
+                      const std::vector<uint8_t>* raw_mask = nullptr);
 
 // Byte range [begin, end) of page p (1..M) of a layer blob; p = 0: whole.
 std::pair<int64_t, int64_t> page_range(int64_t blob_bytes, int M, int page);

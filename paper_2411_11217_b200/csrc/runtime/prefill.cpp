@@ -270,7 +270,7 @@ PrefillReport Runtime::prefill(const int32_t* tokens, const int32_t* lens, int32
                 a.n_chunks = nchunks;
                 a.out_f32 = pf_y_;
                 a.ldo = W_;
-                a.codec = opt_.weight_codec ? 1 : 0;
+                codec_args(a);
                 pl("qkv_gemm", mltk::launch_gemm(a, num_sms_, s_gpu_));
                 // KV: host cache (staged, one strided DMA per sequence) or the paged
                 // device pool (stored by rope_qkv itself)
@@ -304,7 +304,7 @@ PrefillReport Runtime::prefill(const int32_t* tokens, const int32_t* lens, int32
                 o.ldo = H_;
                 o.residual = coll_ ? nullptr : x;
                 o.ldr = H_;
-                o.codec = opt_.weight_codec ? 1 : 0;
+                codec_args(o);
                 pl("o_gemm", mltk::launch_gemm(o, num_sms_, s_gpu_));
                 if (coll_) {
                     coll_->all_reduce_sum(pf_h_, static_cast<size_t>(Tc) * H_, s_gpu_);
@@ -331,7 +331,7 @@ PrefillReport Runtime::prefill(const int32_t* tokens, const int32_t* lens, int32
                 gu.epi = mltk::kEpiSiluPacked;
                 gu.out_packed = pf_inter_;
                 gu.out_R = pf_Re_;
-                gu.codec = opt_.weight_codec ? 1 : 0;
+                codec_args(gu);
                 pl("expert_gateup_gemm", mltk::launch_gemm(gu, num_sms_, s_gpu_));
                 mltk::GemmArgs dn;
                 dn.a_table = tab + tab_w2_;
@@ -346,7 +346,7 @@ PrefillReport Runtime::prefill(const int32_t* tokens, const int32_t* lens, int32
                 dn.n_chunks = nchunks;
                 dn.out_f32 = pf_y_;
                 dn.ldo = H_;
-                dn.codec = opt_.weight_codec ? 1 : 0;
+                codec_args(dn);
                 pl("expert_down_gemm", mltk::launch_gemm(dn, num_sms_, s_gpu_));
                 if (coll_) {
                     pl("moe_combine", mltk::launch_moe_combine(nullptr, pf_y_, H_, pf_inv_, pf_topw_, Tc, H_, K_, x, s_gpu_));

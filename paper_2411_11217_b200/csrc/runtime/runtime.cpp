@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -125,6 +126,9 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     }
     max_ctx_ = opt.max_ctx;
     Rmu_ = round_up(mu_, 16);
+    // encoded weights: the register-decode GEMM (fragment-order tiles) while a
+    // micro-batch fits its 64-token chunks, else the tcgen05 in-smem decoder
+    codec_mode_ = opt.weight_codec ? (Rmu_ <= 64 ? 2 : 1) : 0;
     Re_ = round_up(mu_ * K_ + 16 * E_, 16);
     ncap_ = std::min(256, Rmu_);
     ncap_e_ = std::min(128, Rmu_);  // per-expert tiles: 4+ smem stages; m_e > 128 loops in-tile
@@ -184,7 +188,16 @@ cudaStream_t Runtime::stream(lightplan::sim::Resource r) const {
 
 // Residency split and blob layout: exec_plan.cpp build_catalog.
 void Runtime::build_catalog() {
-    cat_ = mlt::build_catalog(model_, policy_, shard_, opt_.weight_codec);
+    // codec: per-block raw fallback mask (test knob MLT_CODEC_FORCE_RAW=1 stores
+    // every block raw, which must decode bit-identically to the encoded run)
+    if (opt_.weight_codec && raw_mask_.empty()) {
+        const char* f = std::getenv("MLT_CODEC_FORCE_RAW");
+        if (f && f[0] == '1')
+            raw_mask_.assign(mlt::build_catalog(model_, policy_, shard_, true).blocks.size(), 1);
+    }
+    cat_ = mlt::build_catalog(model_, policy_, shard_, opt_.weight_codec, raw_mask_.empty() ? nullptr : &raw_mask_);
+    any_raw_ = false;
+    for (const auto& b : cat_.blocks) any_raw_ = any_raw_ || b.raw;
     layer_res_bytes_ = cat_.resident_bytes;
     layer_blob_bytes_ = cat_.blob_bytes;
     achieved_rw_ = cat_.achieved_rw;
@@ -244,7 +257,7 @@ void Runtime::allocate() {
             const int tiles = E_ * (H_ / 128);
             double best = 0;
             for (int s = 1; s <= 8 && (F_ / 64) / s >= 8; ++s) {
-                const double waves = static_cast<double>(tiles) * s / num_sms_;
+                const double waves = static_cast<double>(tiles) * s / gemm_slots();
                 const double fill = waves / std::ceil(waves);
                 if (fill > best + 1e-9) best = fill, down_splits_ = s;
             }
@@ -326,9 +339,19 @@ void Runtime::generate_weights() {
             uint8_t* dst = b.resident ? res.data() + b.offset
                                       : host_blob_ + static_cast<int64_t>(l) * layer_blob_bytes_ + b.offset;
             const ShardMap& sm = map_of(b.kind);
-            if (!opt_.weight_codec) {
+            if (!opt_.weight_codec || (b.raw && codec_mode_ == 1)) {  // packed bf16 tiles
                 synth_shard_packed(seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0,
                                    b.K, b.rb * 128, (b.rb + 1) * 128, sm.scale, reinterpret_cast<uint16_t*>(dst));
+            } else if (b.raw) {  // codec 2 raw fallback: fragment-order bf16 tiles
+                tmp_block.resize(static_cast<size_t>(128) * b.K);
+                synth_shard_packed(seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0,
+                                   b.K, b.rb * 128, (b.rb + 1) * 128, sm.scale, tmp_block.data());
+                const int tiles = static_cast<int>(b.K / 64);
+#pragma omp parallel for schedule(static)
+                for (int t = 0; t < tiles; ++t)
+                    frag_from_packed(reinterpret_cast<const uint8_t*>(tmp_block.data()) +
+                                         static_cast<size_t>(t) * mltk::kATileBytes,
+                                     reinterpret_cast<uint16_t*>(dst + static_cast<size_t>(t) * mltk::kATileBytes));
             } else {  // packed bf16 tiles -> encoded tiles (lossless, weight_codec.hpp)
                 tmp_block.resize(static_cast<size_t>(128) * b.K);
                 synth_shard_packed(seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0,
@@ -337,11 +360,12 @@ void Runtime::generate_weights() {
                 int bad = 0;
 #pragma omp parallel for schedule(static) reduction(+ : bad)
                 for (int t = 0; t < tiles; ++t)
-                    bad += codec_encode_tile(reinterpret_cast<const uint8_t*>(tmp_block.data()) +
-                                                 static_cast<size_t>(t) * mltk::kATileBytes,
-                                             dst + static_cast<size_t>(t) * kCodecTileBytes)
-                               ? 0
-                               : 1;
+                    {
+                    const uint8_t* src = reinterpret_cast<const uint8_t*>(tmp_block.data()) +
+                                         static_cast<size_t>(t) * mltk::kATileBytes;
+                    uint8_t* out = dst + static_cast<size_t>(t) * kCodecTileBytes;
+                    bad += (codec_mode_ == 2 ? codec_encode_frag_tile(src, out) : codec_encode_tile(src, out)) ? 0 : 1;
+                }
                 if (bad) throw std::invalid_argument("weight_codec: a weight tile does not fit the code");
             }
             int entry;
@@ -355,6 +379,7 @@ void Runtime::generate_weights() {
             for (int slot = 0; slot < 2; ++slot) {
                 const uint8_t* p = b.resident ? dev_res_ + static_cast<int64_t>(l) * layer_res_bytes_ + b.offset
                                               : dev_pool_ + static_cast<int64_t>(slot) * layer_blob_bytes_ + b.offset;
+                if (b.raw) p += 1;  // tag: raw fallback block of an encoded model (gemm_tc / gemm_codec untag)
                 tab[(static_cast<size_t>(l) * 2 + slot) * table_entries_ + entry] = p;
             }
         }
@@ -535,9 +560,21 @@ unsigned long long* Runtime::ktimer(const char* name) {
 // partials are reduced by the consumer (rope_qkv for QKV, the router kernel
 // for O), in fixed order.  Tokens stay in one chunk (<= 256).
 void Runtime::dense_tiling(int row_blocks, int& n_cap, int& n_chunks, int& k_splits) const {
-    n_cap = std::min(256, Rmu_);
+    // the register-decode codec GEMM holds <= 64 tokens per chunk and runs 2 CTAs per SM
+    n_cap = std::min(codec_mode_ == 2 ? 64 : 256, Rmu_);
     n_chunks = (mu_ + n_cap - 1) / n_cap;
-    k_splits = std::max(1, std::min(kMaxSplits, num_sms_ / (row_blocks * n_chunks)));
+    k_splits = std::max(1, std::min(kMaxSplits, gemm_slots() / (row_blocks * n_chunks)));
+}
+
+// Encoded-weight settings of a projection / expert GEMM (lm_head stays bf16):
+// codec 1 = tcgen05 with in-smem decode (gemm_tc.cu), codec 2 = register
+// decode + mma.sync (gemm_codec.cu: <= 64 tokens per chunk, <= 32 for gate/up).
+void Runtime::codec_args(mltk::GemmArgs& a) const {
+    a.codec = codec_mode_;
+    if (codec_mode_ == 2) {
+        a.n_cap = std::min(a.n_cap, a.n_mats == 2 ? 32 : 64);
+        a.codec_raw = any_raw_ ? 1 : 0;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -575,7 +612,7 @@ void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
     a.out_f32 = d_qkv_f32_;
     a.ldo = W_;
     a.timing = ktimer("qkv_gemm");
-    a.codec = opt_.weight_codec ? 1 : 0;
+    codec_args(a);
     kl("qkv_gemm", mltk::launch_gemm(a, num_sms_, s_gpu_));
     const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
     uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
@@ -650,7 +687,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     o.residual = coll_ ? nullptr : x;  // unsplit single GPU: residual in the GEMM epilogue
     o.ldr = H_;
     o.timing = ktimer("o_gemm");
-    o.codec = opt_.weight_codec ? 1 : 0;
+    codec_args(o);
     kl("o_gemm", mltk::launch_gemm(o, num_sms_, s_gpu_));
     if (coll_) {
         // TP all-reduce #1: h = x + sum over ranks of this rank's O partial
@@ -697,7 +734,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     gu.sk_count = d_sk_count_;
     gu.sk_rows = Rmu_;  // a token routes to an expert at most once: rows per group <= mu
     gu.timing = ktimer("expert_gateup_gemm");
-    gu.codec = opt_.weight_codec ? 1 : 0;
+    codec_args(gu);
     kl("expert_gateup_gemm", mltk::launch_gemm(gu, num_sms_, s_gpu_));
     mltk::GemmArgs dn;
     dn.a_table = tab + tab_w2_;
@@ -714,7 +751,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     dn.k_splits = down_splits_;
     dn.split_stride = static_cast<int64_t>(Re_) * H_;
     dn.timing = ktimer("expert_down_gemm");
-    dn.codec = opt_.weight_codec ? 1 : 0;
+    codec_args(dn);
     kl("expert_down_gemm", mltk::launch_gemm(dn, num_sms_, s_gpu_));
     if (coll_) {
         // TP all-reduce #2: x = h + sum over ranks of this rank's top-k combine (h2 shard)

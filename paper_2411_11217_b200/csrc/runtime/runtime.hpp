@@ -25,6 +25,10 @@
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
 
+namespace mltk {
+struct GemmArgs;
+}
+
 namespace mlt {
 
 struct ModelExt {
@@ -189,6 +193,12 @@ class Runtime {
                      int32_t* out, lightplan::sim::ScheduleDag* dag_out, lightplan::sim::Timeline* timeline_out);
     void build_catalog();
     void dense_tiling(int row_blocks, int& n_cap, int& n_chunks, int& k_splits) const;
+    void codec_args(mltk::GemmArgs& a) const;
+    // resident CTA slots of the weight GEMMs: 2 per SM for the register-decode codec GEMM
+    int gemm_slots() const { return codec_mode_ == 2 ? 2 * num_sms_ : num_sms_; }
+    int codec_mode_ = 0;   // 0 bf16 tiles, 1 encoded (tcgen05 path), 2 encoded fragment order (mma.sync)
+    bool any_raw_ = false; // codec: some block is a raw fallback (tagged page-table entry)
+    std::vector<uint8_t> raw_mask_;  // codec: per catalog block, stored raw (fallback)
     static constexpr int kMaxSplits = 8;
     void allocate();
     void generate_weights();

@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include "../kernels/common.cuh"
+
 namespace mlt {
 
 bool codec_encode_tile(const uint8_t* tile, uint8_t* out) {
@@ -57,6 +59,31 @@ void codec_decode_tile(const uint8_t* enc, uint8_t* tile) {
         const int i = enc[12308 + 4 * e] | (enc[12309 + 4 * e] << 8);
         tile[2 * i + 1] = enc[12310 + 4 * e];
     }
+}
+
+namespace {
+// packed (SWIZZLE_128B image) byte offset of fragment-order weight i
+inline uint32_t frag_src(uint32_t i) {
+    const uint32_t u = i >> 3, j = i & 7u;
+    const uint32_t lane = u & 31u, kk = (u >> 5) & 3u, mb = u >> 7;
+    const uint32_t r = 16u * mb + (lane >> 2) + 8u * ((j >> 1) & 1u);
+    const uint32_t k = 16u * kk + 2u * (lane & 3u) + (j & 1u) + 8u * (j >> 2);
+    return mltk::swz_off(r, k);
+}
+}  // namespace
+
+void frag_from_packed(const uint8_t* packed, uint16_t* frag) {
+    for (uint32_t i = 0; i < 8192; ++i) std::memcpy(frag + i, packed + frag_src(i), 2);
+}
+
+void packed_from_frag(const uint16_t* frag, uint8_t* packed) {
+    for (uint32_t i = 0; i < 8192; ++i) std::memcpy(packed + frag_src(i), frag + i, 2);
+}
+
+bool codec_encode_frag_tile(const uint8_t* packed, uint8_t* out) {
+    uint16_t frag[8192];
+    frag_from_packed(packed, frag);
+    return codec_encode_tile(reinterpret_cast<const uint8_t*>(frag), out);
 }
 
 }  // namespace mlt

@@ -34,4 +34,15 @@ bool codec_encode_tile(const uint8_t* tile16k, uint8_t* out);
 // Host reference decoder (tests; the GEMM decodes in shared memory).
 void codec_decode_tile(const uint8_t* enc, uint8_t* tile16k);
 
+// Fragment order (kernels/gemm_codec.cu, GemmArgs::codec = 2): the same
+// 128 x 64 weights reordered so that 8-weight unit u = (mb * 4 + kk) * 32 +
+// lane holds lane's mma.sync m16n8k16 A fragment of m16 block mb and k16
+// block kk: weight j of the unit is row 16 mb + g + 8 ((j >> 1) & 1), k 16 kk
+// + 2 tg + (j & 1) + 8 (j >> 2), g = lane / 4, tg = lane % 4.  The codec
+// fields are unchanged (the code is order-independent); escape indices refer
+// to fragment order.  A raw fallback block stores 16 KiB fragment-order bf16.
+void frag_from_packed(const uint8_t* packed16k, uint16_t* frag8192);
+void packed_from_frag(const uint16_t* frag8192, uint8_t* packed16k);
+bool codec_encode_frag_tile(const uint8_t* packed16k, uint8_t* out);
+
 }  // namespace mlt

@@ -472,3 +472,131 @@ def test_codec_expert_ffn_bitwise_equals_raw(K, T, H, Fd, E, Kk, n_cap, codec):
     assert torch.equal(results[0][0], results[1][0])
     assert torch.equal(results[0][1], results[1][1])
 
+
+
+def encode_frag_dev(K, w_bf16, raw_rows=()):
+    """Codec-2 weight blocks (fragment-order encoded tiles, gemm_codec.cu):
+    row blocks listed in raw_rows are stored as raw fragment-order tiles with
+    their page-table pointer tagged (bit 0), the runtime's per-block fallback.
+    Returns (device buffer, row-block pointers)."""
+    M, Kd = w_bf16.shape
+    src = bf16_bits(w_bf16.cpu())
+    packed = np.empty_like(src)
+    K.pack_weight(src.ctypes.data_as(C.c_void_p), M, Kd, packed.ctypes.data_as(C.c_void_p))
+    kb, rbs = Kd // 64, M // 128
+    pb = packed.view(np.uint8).reshape(rbs, kb * 16384)
+    parts, ptrs_rel = [], []
+    off = 0
+    for r in range(rbs):
+        if r in raw_rows:
+            blk = np.empty(kb * 16384, np.uint8)
+            K.frag_pack(pb[r].ctypes.data_as(C.c_void_p), kb, blk.ctypes.data_as(C.c_void_p))
+        else:
+            blk = np.empty(kb * 12432, np.uint8)
+            rr = np.zeros(1, np.uint8)
+            assert K.codec_encode_frag(np.ascontiguousarray(pb[r]).ctypes.data_as(C.c_void_p), 128, Kd,
+                                       blk.ctypes.data_as(C.c_void_p), rr.ctypes.data_as(C.c_void_p)) == 0
+        parts.append(blk)
+        ptrs_rel.append((off, r in raw_rows))
+        off += blk.size
+        off = (off + 15) // 16 * 16
+        parts.append(np.zeros((-blk.size) % 16, np.uint8))
+    dev = torch.from_numpy(np.concatenate(parts)).cuda()
+    return dev, [dev.data_ptr() + o + (1 if raw else 0) for o, raw in ptrs_rel]
+
+
+@pytest.mark.parametrize("T,M,Kd,n_cap,splits,resid", [(16, 256, 512, 16, 1, True), (64, 384, 4096, 64, 3, False),
+                                                        (37, 256, 1024, 48, 2, False), (100, 128, 256, 64, 1, True)])
+def test_codec2_gemm_register_decode(K, T, M, Kd, n_cap, splits, resid):
+    """Register-decode GEMM (codec = 2: fragment-order encoded tiles, mma.sync):
+    against torch fp32; and encoded == raw fallback blocks (tagged pointers,
+    same kernel without the decode) bit for bit, for all-raw and mixed tables —
+    the GPU decode is exact.  Token counts above n_cap loop over chunks."""
+    g = torch.Generator().manual_seed(T + M + Kd + 7)
+    w = rand_bf16(M, Kd, scale=Kd ** -0.5, gen=g)
+    x = rand_bf16(T, Kd, gen=g)
+    R = (T + 15) // 16 * 16
+    xp = pack_rows_dev(K, x, R)
+    res = torch.randn(T, M, device="cuda") if resid else None
+    outs = []
+    for raw_rows in ((), tuple(range(M // 128)), (0,)):
+        dev, blocks = encode_frag_dev(K, w, raw_rows)
+        tab = table([blocks])
+        out = torch.zeros(splits, R, M, device="cuda")
+        a = capi.GemmArgs(a_table=tab.data_ptr(), n_mats=1, G=1, RB=M // 128, K=Kd, b=xp.data_ptr(), R=R,
+                          rows_dense=T, n_cap=n_cap, epi=0, alpha=1.0, out_f32=out.data_ptr(), ldo=M,
+                          residual=res.data_ptr() if resid else None, ldr=M, k_splits=splits,
+                          split_stride=R * M, codec=2, codec_raw=int(bool(raw_rows)))
+        K.gemm(C.byref(a), stream())
+        torch.cuda.synchronize()
+        outs.append(out.cpu())
+        del dev
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    ref = x.float() @ w.float().T + (res.cpu() if resid else 0)
+    assert (outs[0].sum(0)[:T] - ref).abs().max().item() <= 2e-3 * max(1.0, ref.abs().max().item())
+
+
+@pytest.mark.parametrize("T,H,Fd,E,Kk", [(64, 512, 768, 8, 2), (33, 256, 256, 16, 4), (96, 256, 512, 2, 1)])
+def test_codec2_expert_ffn_register_decode(K, T, H, Fd, E, Kk):
+    """Grouped gate/up (fused SiLU -> packed bf16, <= 32 tokens per chunk) and
+    down (<= 64 tokens per chunk, 2 K-splits) on codec-2 experts: against a
+    torch fp32 reference of the same routing, and bit-equal to raw fallback
+    blocks (E = 2, top-1 puts > 32 tokens on an expert: chunk loop)."""
+    hn, w1, w3, w2, wr = _expert_setup(T, H, Fd, E, Kk, seed=T + H + 5)
+    hn_d, wr_d = hn.cuda(), wr.cuda()
+    idx = torch.zeros(T, Kk, dtype=torch.int32, device="cuda")
+    wts = torch.zeros(T, Kk, device="cuda")
+    K.router_topk(None, None, 0.0, ptr(hn_d), ptr(wr_d), T, H, E, Kk, None, None, ptr(idx), ptr(wts), stream())
+    R = (T * Kk + 16 * E + 15) // 16 * 16
+    cnt = torch.zeros(E, dtype=torch.int32, device="cuda")
+    off = torch.zeros(E + 1, dtype=torch.int32, device="cuda")
+    perm = torch.zeros(R, dtype=torch.int32, device="cuda")
+    inv = torch.zeros(T * Kk, dtype=torch.int32, device="cuda")
+    xp = torch.zeros(R * H, dtype=torch.int16, device="cuda")
+    K.moe_permute(ptr(idx), ptr(hn_d), T, H, E, Kk, ptr(cnt), ptr(off), ptr(perm), ptr(inv), ptr(xp), R, stream())
+    results = []
+    for all_raw in (False, True):
+        keep, t13, t2 = [], [], []
+        for m in (w1, w3):
+            for w in m:
+                dev, bl = encode_frag_dev(K, w, tuple(range(w.shape[0] // 128)) if all_raw else ())
+                keep.append(dev)
+                t13.append(bl)
+        for w in w2:
+            dev, bl = encode_frag_dev(K, w, tuple(range(w.shape[0] // 128)) if all_raw else ())
+            keep.append(dev)
+            t2.append(bl)
+        tab13, tab2 = table(t13), table(t2)
+        inter = torch.zeros(R * Fd, dtype=torch.int16, device="cuda")
+        y = torch.zeros(2, R, H, device="cuda")
+        gu = capi.GemmArgs(a_table=tab13.data_ptr(), n_mats=2, G=E, RB=Fd // 128, K=H, b=xp.data_ptr(), R=R,
+                           b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=32, epi=1, alpha=1.0,
+                           out_packed=inter.data_ptr(), out_R=R, codec=2, codec_raw=int(all_raw))
+        K.gemm(C.byref(gu), stream())
+        dn = capi.GemmArgs(a_table=tab2.data_ptr(), n_mats=1, G=E, RB=H // 128, K=Fd, b=inter.data_ptr(), R=R,
+                           b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=64, epi=0, alpha=1.0,
+                           out_f32=y.data_ptr(), ldo=H, codec=2, k_splits=2, split_stride=R * H,
+                           codec_raw=int(all_raw))
+        K.gemm(C.byref(dn), stream())
+        torch.cuda.synchronize()
+        results.append((inter.cpu(), y.cpu()))
+    assert torch.equal(results[0][0], results[1][0]) and torch.equal(results[0][1], results[1][1])
+    # torch fp32 reference of every (token, slot) row
+    inter_rows = np.empty((R, Fd), np.uint16)
+    K.unpack_rows(results[0][0].numpy().ctypes.data_as(C.c_void_p), R, R, Fd, inter_rows.ctypes.data_as(C.c_void_p))
+    cnt_h, off_h, perm_h = cnt.cpu().numpy(), off.cpu().numpy(), perm.cpu().numpy()
+    yh = results[0][1].sum(0)
+    hnf = hn.float()
+    worst_i = worst_y = 0.0
+    for e in range(E):
+        for r in range(int(cnt_h[e])):
+            row = int(off_h[e]) + r
+            t = int(perm_h[row]) // Kk
+            g_ = hnf[t] @ w1[e].float().T
+            u_ = hnf[t] @ w3[e].float().T
+            it = torch.nn.functional.silu(g_) * u_
+            got_i = torch.from_numpy(inter_rows[row].astype(np.int32) << 16).view(torch.float32)
+            worst_i = max(worst_i, ((got_i - it).abs().max() / it.abs().max()).item())
+            yr = got_i.to(torch.bfloat16).float() @ w2[e].float().T
+            worst_y = max(worst_y, ((yh[row] - yr).abs().max() / yr.abs().max()).item())
+    assert worst_i < 1.5e-2 and worst_y < 2e-3, (worst_i, worst_y)

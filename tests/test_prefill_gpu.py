@@ -164,15 +164,21 @@ def test_prefill_small_chunks(a_g):
 @pytest.mark.parametrize("a_g,r_w", [(0, 0.3), (1, 1.0)])
 def test_prefill_with_weight_codec_bitwise_equal(a_g, r_w):
     """GPU prefill on encoded weights: same first tokens, same KV cache bits and
-    same decode continuation as on bf16 tiles."""
+    same decode continuation as the same runtime with every block stored as a
+    raw fallback block (MLT_CODEC_FORCE_RAW=1: same GEMMs, no decode)."""
+    import os
     dims = (1024, 3584, 8, 2)
     lens = [17, 40, 33, 8, 56, 1, 25, 48]
     prompts = _prompts(lens)
     outs = []
-    for codec in (False, True):
-        rt = Runtime(capi.ModelSpec(2, *dims, 8, 2, 2.0, 2.0), capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0),
-                     budget_bytes=4e9, max_ctx=CTX, vocab=VOCAB, seed=1234, weight_codec=codec,
-                     down_splits=4)  # equal down-GEMM K-splits: the codec's auto split, forced on both
+    for force_raw in (True, False):
+        os.environ["MLT_CODEC_FORCE_RAW"] = "1" if force_raw else "0"
+        try:
+            rt = Runtime(capi.ModelSpec(2, *dims, 8, 2, 2.0, 2.0),
+                         capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0),
+                         budget_bytes=4e9, max_ctx=CTX, vocab=VOCAB, seed=1234, weight_codec=True)
+        finally:
+            os.environ.pop("MLT_CODEC_FORCE_RAW", None)
         first, _ = rt.prefill(prompts)
         if a_g:  # paged pool [layer][seq][page][kv_head][16][d]: pages past a prompt hold stale bytes
             kv = [rt.debug_read(n, np.uint16).reshape(2, N, CTX // 16, dims[3], 16, 128) for n in ("kpool", "vpool")]

@@ -35,11 +35,15 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--with-h2d", action="store_true", help="run a concurrent H2D copy stream")
     ap.add_argument("--codec", action="store_true", help="encoded weight tiles (decoder warps in the GEMM)")
+    ap.add_argument("--codec2", action="store_true",
+                    help="fragment-order encoded tiles, register decode + mma.sync (gemm_codec.cu)")
     ap.add_argument("--no-stream-k", action="store_true", help="gate/up without the stream-K tail")
     ap.add_argument("--dec-groups", type=int, default=0, help="codec decoder groups (0: default)")
     ap.add_argument("--down-splits", type=int, default=0,
                     help="K-splits of the down GEMM (0: the runtime's auto choice, 4 with --codec at 8x7B)")
     a = ap.parse_args()
+    if a.codec2:
+        a.codec = True
     mu = a.mu
     KD = capi.load_kernels()
     s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -65,8 +69,12 @@ def main():
             src = w.view(torch.int16).numpy().view(np.uint16)
             packed = np.empty_like(src)
             KD.pack_weight(src.ctypes.data_as(C.c_void_p), rows, k, packed.ctypes.data_as(C.c_void_p))
-            KD.codec_encode(packed.ctypes.data_as(C.c_void_p), rows, k,
-                            enc[i * per:(i + 1) * per].ctypes.data_as(C.c_void_p))
+            if a.codec2:
+                KD.codec_encode_frag(packed.ctypes.data_as(C.c_void_p), rows, k,
+                                     enc[i * per:(i + 1) * per].ctypes.data_as(C.c_void_p), None)
+            else:
+                KD.codec_encode(packed.ctypes.data_as(C.c_void_p), rows, k,
+                                enc[i * per:(i + 1) * per].ctypes.data_as(C.c_void_p))
         dev = torch.from_numpy(enc).cuda()
         tab = [dev.data_ptr() + i * per + rb * (k // 64) * 12432
                for i in range(n_mats * E) for rb in range(rows // 128)]
@@ -93,7 +101,9 @@ def main():
     inv = torch.zeros(mu * K, dtype=torch.int32, device="cuda")
     xp = torch.zeros(R * H, dtype=torch.int16, device="cuda")
     inter = torch.zeros(R * F, dtype=torch.int16, device="cuda")
-    ds = a.down_splits or (4 if a.codec else 1)  # runtime.cpp expert_down_splits auto (8 x 32 tiles, 148 SMs)
+    # runtime.cpp expert_down_splits auto (8 x 32 tiles over 148 SMs; 2 CTAs per SM with codec 2)
+    ds = a.down_splits or (8 if a.codec2 else 4 if a.codec else 1)
+    cmode = 2 if a.codec2 else int(a.codec)
     y = torch.zeros(ds * R, H, device="cuda")
     xo = torch.zeros(mu, H, device="cuda")
     Rmu = (mu + 15) // 16 * 16
@@ -101,6 +111,7 @@ def main():
     qkv = torch.zeros(Rmu, W, device="cuda")
     hbuf = torch.zeros(mu, H, device="cuda")
     ncap = min(128, Rmu)  # runtime.cpp ncap_e_
+    ncap_gu, ncap_dn = (min(32, ncap), min(64, ncap)) if a.codec2 else (ncap, ncap)
 
     def router():
         KD.router_topk(ptr(x), ptr(gamma), 1e-5, None, ptr(wr), mu, H, E, K, ptr(hn), None,
@@ -112,13 +123,13 @@ def main():
     sk_scratch = torch.zeros(148 * 2 * Rmu * 128, device="cuda")
     sk_count = torch.zeros(148, dtype=torch.int64, device="cuda")
     gu_args = capi.GemmArgs(a_table=t13.data_ptr(), n_mats=2, G=E, RB=F // 128, K=H, b=xp.data_ptr(), R=R,
-                            b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=1, alpha=1.0,
-                            out_packed=inter.data_ptr(), out_R=R, codec=int(a.codec),
+                            b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap_gu, epi=1, alpha=1.0,
+                            out_packed=inter.data_ptr(), out_R=R, codec=cmode,
                             sk_scratch=None if a.no_stream_k else sk_scratch.data_ptr(),
                             sk_count=sk_count.data_ptr(), sk_rows=Rmu, dec_groups=a.dec_groups)
     dn_args = capi.GemmArgs(a_table=t2.data_ptr(), n_mats=1, G=E, RB=H // 128, K=F, b=inter.data_ptr(), R=R,
-                            b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap, epi=0, alpha=1.0,
-                            out_f32=y.data_ptr(), ldo=H, codec=int(a.codec), k_splits=ds, split_stride=R * H,
+                            b_off=off.data_ptr(), b_cnt=cnt.data_ptr(), n_cap=ncap_dn, epi=0, alpha=1.0,
+                            out_f32=y.data_ptr(), ldo=H, codec=cmode, k_splits=ds, split_stride=R * H,
                             dec_groups=a.dec_groups)
 
     def expert():
