@@ -546,6 +546,8 @@ typedef struct mlt_runtime_info_t {
     double streamed_bytes_per_layer;
     double arena_used, arena_capacity;
     double pin_seconds, gen_seconds;
+    double bytes_per_weight;  /* projection + expert weights as stored (2 = bf16; codec ~1.52) */
+    double raw_blocks;        /* codec: 128-row blocks per layer stored raw (per-block fallback) */
 } mlt_runtime_info_t;
 
 typedef struct mlt_runtime mlt_runtime;
@@ -553,6 +555,20 @@ typedef struct mlt_runtime mlt_runtime;
 mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* model, const mlt_policy_t* policy,
                                 const mlt_runtime_options_t* options);
 void mlt_runtime_destroy(mlt_runtime* rt);
+/* Caller-owned weights instead of the synthetic ones (e.g. a real checkpoint).
+ * get(ctx, layer, kind, expert) returns the FULL (unsharded) tensor as
+ * row-major bf16 bits; layer = -1 for the model-level tensors.  kind:
+ *   0 embed [vocab][h1]      1 lm_head [vocab][h1]   2 final_norm [h1]
+ *   3 attn_norm [h1]         4 ffn_norm [h1]         5 wqkv [(n_q+2n_kv)d][h1]
+ *     (q heads, then k heads, then v heads)          6 wo [h1][n_q d]
+ *   7 router [n_e][h1]       8 w1 [h2][h1]  9 w3 [h2][h1]  10 w2 [h1][h2]
+ * (expert = 0 for non-expert tensors).  Called only during this call, from
+ * the calling thread; pointers need not outlive it; NULL = MLT_ERR_INVALID.
+ * With weight_codec, row blocks the code cannot hold are stored raw (per-block
+ * fallback, see mlt_runtime_info raw_blocks). */
+typedef const uint16_t* (*mlt_weight_fn)(void* ctx, int layer, int kind, int expert);
+mlt_runtime* mlt_runtime_create_with_weights(const mlt_model_spec_t* model, const mlt_policy_t* policy,
+                                             const mlt_runtime_options_t* options, mlt_weight_fn get, void* ctx);
 int mlt_runtime_info(const mlt_runtime* rt, mlt_runtime_info_t* out);
 /* Synthetic prompt-stage KV for positions [0, prompt_len); positions := prompt_len. */
 int mlt_runtime_prefill_synthetic(mlt_runtime* rt, int prompt_len, uint64_t seed);

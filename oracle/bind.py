@@ -47,6 +47,7 @@ _SIGS = {
     "orc_num_threads": (I, []),
     "orc_router_margins": (None, [V, V]),
     "orc_model_force_routes": (None, [V, V]),
+    "orc_model_set_tensor": (I, [V, I, I, I, V]),
     "orc_model_route_info": (None, [V, V, V]),
 }
 
@@ -197,6 +198,11 @@ class Model:
         out = np.zeros(self.cfg.batch, np.float32)
         lib().orc_router_margins(self.h, p(out))
         return out
+
+    def set_tensor(self, layer, kind, expert, data):
+        """Overwrite a model tensor with caller weights (bf16 bits, same shape)."""
+        a = np.ascontiguousarray(data, np.uint16)
+        assert lib().orc_model_set_tensor(self.h, layer, kind, expert, p(a)) == 0
 
     def force_routes(self, topk):
         """Take these routes ([L, N, K] int32) in every following step (None: own routing)."""

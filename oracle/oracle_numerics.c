@@ -421,6 +421,29 @@ const uint16_t* orc_model_tensor(const orc_model* m, int layer, int kind, int ex
     return 0;
 }
 
+/* Element count of a model tensor (the shapes of orc_model_create). */
+static int64_t tensor_elems(const orc_model* m, int kind) {
+    const orc_config* c = &m->c;
+    const int64_t H = c->hidden, F = c->ffn, qkv = (int64_t)(c->q_heads + 2 * c->kv_heads) * m->d;
+    switch (kind) {
+        case ORC_T_EMBED: case ORC_T_LM_HEAD: return (int64_t)c->vocab * H;
+        case ORC_T_FINAL_NORM: case ORC_T_ATTN_NORM: case ORC_T_FFN_NORM: return H;
+        case ORC_T_WQKV: return qkv * H;
+        case ORC_T_WO: return H * H;
+        case ORC_T_ROUTER: return (int64_t)c->experts * H;
+        case ORC_T_W1: case ORC_T_W3: case ORC_T_W2: return F * H;
+    }
+    return 0;
+}
+
+int orc_model_set_tensor(orc_model* m, int layer, int kind, int expert, const uint16_t* data) {
+    uint16_t* dst = (uint16_t*)orc_model_tensor(m, layer, kind, expert);
+    const int64_t n = tensor_elems(m, kind);
+    if (!dst || n <= 0) return -1;
+    memcpy(dst, data, sizeof(uint16_t) * (size_t)n);
+    return 0;
+}
+
 uint16_t* orc_model_kv(orc_model* m, int layer, int which) {
     return which ? m->vc[layer] : m->kc[layer];
 }

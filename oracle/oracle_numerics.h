@@ -119,6 +119,9 @@ void orc_fill_kv(orc_model* m, uint64_t seed, int upto);
  * (a routing near-tie indicator). */
 void orc_router_margins(const orc_model* m, float* out);
 uint16_t* orc_model_kv(orc_model* m, int layer, int which); /* which: 0=K 1=V */
+/* Replace a generated tensor with caller weights (same shape, bf16 bits):
+ * parity of caller-weight runs (mlt_runtime_create_with_weights). */
+int orc_model_set_tensor(orc_model* m, int layer, int kind, int expert, const uint16_t* data);
 /* Forced routing (parity probe): with topk != NULL ([L][N][K], borrowed until
  * reset with NULL) every layer takes these experts instead of its own top-k,
  * weighted by the softmax of the ORACLE's logits at those experts.  Lets the

@@ -34,8 +34,16 @@ Handle* H(mlt_runtime* r) { return reinterpret_cast<Handle*>(r); }
 
 extern "C" {
 
+mlt_runtime* mlt_runtime_create_with_weights(const mlt_model_spec_t* m, const mlt_policy_t* p,
+                                             const mlt_runtime_options_t* o, mlt_weight_fn get, void* ctx);
+
 mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p,
                                 const mlt_runtime_options_t* o) {
+    return mlt_runtime_create_with_weights(m, p, o, nullptr, nullptr);
+}
+
+mlt_runtime* mlt_runtime_create_with_weights(const mlt_model_spec_t* m, const mlt_policy_t* p,
+                                             const mlt_runtime_options_t* o, mlt_weight_fn get, void* ctx) {
     Handle* h = nullptr;
     guard([&] {
         lightplan::ModelSpec ms;
@@ -64,6 +72,8 @@ mlt_runtime* mlt_runtime_create(const mlt_model_spec_t* m, const mlt_policy_t* p
         opt.pdl = o->disable_pdl == 0;
         opt.expert_down_splits = o->expert_down_splits;
         opt.collective = o->collective;
+        opt.weight_fn = get;
+        opt.weight_ctx = ctx;
         auto hh = std::make_unique<Handle>();
         hh->rt = std::make_unique<mlt::Runtime>(ms, ext, pol, opt);
         h = hh.release();
@@ -159,6 +169,8 @@ int mlt_runtime_info(const mlt_runtime* r, mlt_runtime_info_t* out) {
         out->arena_capacity = 0;
         out->pin_seconds = rt.pin_seconds();
         out->gen_seconds = rt.gen_seconds();
+        out->bytes_per_weight = rt.bytes_per_weight();
+        out->raw_blocks = static_cast<double>(rt.raw_blocks());
         return MLT_OK;
     });
 }

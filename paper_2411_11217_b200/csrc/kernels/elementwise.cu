@@ -6,8 +6,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <map>
 #include <mutex>
-#include <set>
 #include <utility>
 
 #include "common.cuh"
@@ -22,15 +22,17 @@ bool pdl_enabled() { return g_pdl; }
 void set_pdl(bool on) { g_pdl = on; }
 
 cudaError_t ensure_smem_attr(const void* kern, int bytes) {
+    // the largest size set so far per (device, kernel); raised when a launch needs more
     static std::mutex mu;
-    static std::set<std::pair<int, const void*>> done;
+    static std::map<std::pair<int, const void*>, int> done;
     int dev = 0;
     if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
     std::lock_guard<std::mutex> g(mu);
-    if (done.count({dev, kern})) return cudaSuccess;
+    auto it = done.find({dev, kern});
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
     if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); e != cudaSuccess)
         return e;
-    done.insert({dev, kern});
+    done[{dev, kern}] = bytes;
     return cudaSuccess;
 }
 

@@ -235,52 +235,61 @@ __global__ void __launch_bounds__(kCThreads, 2) gemm_codec_kernel(const GemmArgs
                     mbar_wait(&ctl->full[stage], phase);
                     const uint32_t st = smem_u32(smem + stage * stage_bytes);
                     const uint32_t sb = st + NMATS * slot;
-                    // per matrix: table + escape count (encoded) of this stage's tile
+                    // Every shared load of the stage first (this warp's 4 fragments per
+                    // matrix, the tables, the escape list), then the decode + MMA chains:
+                    // independent work in flight instead of one load latency per fragment.
                     uint4 T[NMATS];
+                    uint2 lo[NMATS][4];
+                    uint32_t cd[NMATS][4];
                     uint32_t esc[NMATS];  // this lane's escape entry {u16 idx, u8 hi} or ~0
-                    uint32_t nesc[NMATS];
 #pragma unroll
                     for (int mt = 0; mt < NMATS; ++mt) {
                         const uint32_t ta = st + mt * slot;
                         if (!raw[mt]) {
                             T[mt] = lds128(ta + 12288);
-                            nesc[mt] = lds32(ta + 12304) & 0xffffu;
-                            esc[mt] = static_cast<uint32_t>(lane) < nesc[mt] ? lds32(ta + 12308 + 4 * lane) : ~0u;
+                            const uint32_t n = lds32(ta + 12304) & 0xffffu;
+                            esc[mt] = static_cast<uint32_t>(lane) < n ? lds32(ta + 12308 + 4 * lane) : ~0u;
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const int unit = (cw * 4 + kk) * 32 + lane;
+                                lo[mt][kk] = lds64(ta + unit * 8);
+                                cd[mt][kk] = lds32(ta + 8192 + unit * 4);
+                            }
                         } else {
-                            nesc[mt] = 0;
                             esc[mt] = ~0u;
                         }
                     }
+                    // escapes that fall into this warp's fragments (weight index >> 10 = warp):
+                    // one ballot per matrix and stage, the patch loop only when there are some
+                    unsigned emask[NMATS];
+#pragma unroll
+                    for (int mt = 0; mt < NMATS; ++mt)
+                        emask[mt] = __ballot_sync(0xffffffffu, esc[mt] != ~0u &&
+                                                                   static_cast<int>((esc[mt] & 0xffffu) >> 10) == cw);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        const int unit = (cw * 4 + kk) * 32 + lane;  // this lane's fragment
                         uint4 A[NMATS];
 #pragma unroll
                         for (int mt = 0; mt < NMATS; ++mt) {
-                            const uint32_t ta = st + mt * slot;
                             if (raw[mt]) {
-                                A[mt] = lds128(ta + unit * 16);
-                            } else {
-                                A[mt] = decode_unit(lds64(ta + unit * 8), lds32(ta + 8192 + unit * 4), T[mt]);
-                                if (nesc[mt]) {  // high bytes outside the table: patch this warp's fragments
-                                    const uint32_t eu = esc[mt] & 0xffffu;  // weight index
-                                    unsigned m = __ballot_sync(0xffffffffu, esc[mt] != ~0u &&
-                                                                            static_cast<int>(eu >> 8) == cw * 4 + kk);
-                                    while (m) {
-                                        const int src = __ffs(m) - 1;
-                                        m &= m - 1;
-                                        const uint32_t e = __shfl_sync(0xffffffffu, esc[mt], src);
-                                        const uint32_t idx = e & 0xffffu, hi = (e >> 16) & 0xffu;
-                                        if (static_cast<int>((idx >> 3) & 31u) == lane) {
-                                            const uint32_t j = idx & 7u;  // weight j of the unit: reg j/2, byte 2(j&1)+1
-                                            const uint32_t sh = ((j & 1u) * 2u + 1u) * 8u;
-                                            const uint32_t keep = ~(0xffu << sh), put = hi << sh, q = j >> 1;
-                                            if (q == 0) A[mt].x = (A[mt].x & keep) | put;
-                                            else if (q == 1) A[mt].y = (A[mt].y & keep) | put;
-                                            else if (q == 2) A[mt].z = (A[mt].z & keep) | put;
-                                            else A[mt].w = (A[mt].w & keep) | put;
-                                        }
-                                    }
+                                A[mt] = lds128(st + mt * slot + ((cw * 4 + kk) * 32 + lane) * 16);
+                                continue;
+                            }
+                            A[mt] = decode_unit(lo[mt][kk], cd[mt][kk], T[mt]);
+                            unsigned m = emask[mt];
+                            while (m) {  // rare: high bytes outside the table
+                                const int src = __ffs(m) - 1;
+                                m &= m - 1;
+                                const uint32_t e = __shfl_sync(0xffffffffu, esc[mt], src);
+                                const uint32_t idx = e & 0xffffu, hi = (e >> 16) & 0xffu;
+                                if (static_cast<int>((idx >> 8) & 3u) == kk && static_cast<int>((idx >> 3) & 31u) == lane) {
+                                    const uint32_t j = idx & 7u;  // weight j of the unit: reg j/2, byte 2(j&1)+1
+                                    const uint32_t sh = ((j & 1u) * 2u + 1u) * 8u;
+                                    const uint32_t keep = ~(0xffu << sh), put = hi << sh, q = j >> 1;
+                                    if (q == 0) A[mt].x = (A[mt].x & keep) | put;
+                                    else if (q == 1) A[mt].y = (A[mt].y & keep) | put;
+                                    else if (q == 2) A[mt].z = (A[mt].z & keep) | put;
+                                    else A[mt].w = (A[mt].w & keep) | put;
                                 }
                             }
                         }

@@ -72,6 +72,18 @@ void synth_shard_packed(uint64_t seed, uint64_t tid, int64_t K_global, const int
     }
 }
 
+void pack_shard_rows(const uint16_t* full, int64_t K_global, const int64_t* rows, int64_t col0, int64_t K_local,
+                     int64_t row_begin, int64_t row_end, uint16_t* dst) {
+    uint8_t* base = reinterpret_cast<uint8_t*>(dst);
+    const uint64_t base_off = mltk::a_packed_off(row_begin, 0, K_local);
+#pragma omp parallel for schedule(static)
+    for (int64_t m = row_begin; m < row_end; ++m) {
+        const uint16_t* src = full + rows[m] * K_global + col0;
+        for (int64_t k = 0; k < K_local; k += 8)
+            std::memcpy(base + mltk::a_packed_off(m, k, K_local) - base_off, src + k, 16);
+    }
+}
+
 void pack_weight(const uint16_t* src, int64_t M, int64_t K, uint16_t* dst) {
     uint8_t* d = reinterpret_cast<uint8_t*>(dst);
 #pragma omp parallel for schedule(static)

@@ -49,6 +49,11 @@ void synth_shard_packed(uint64_t seed, uint64_t tid, int64_t K_global, const int
                         float scale, uint16_t* dst);
 
 void pack_weight(const uint16_t* src, int64_t M, int64_t K, uint16_t* dst);
+// The caller-weights counterpart of synth_shard_packed: local rows [row_begin,
+// row_end) of this rank's shard of the row-major [M_global, K_global] tensor
+// `full` (local row m = global row rows[m], local column k = col0 + k).
+void pack_shard_rows(const uint16_t* full, int64_t K_global, const int64_t* rows, int64_t col0, int64_t K_local,
+                     int64_t row_begin, int64_t row_end, uint16_t* dst);
 void pack_rows(const uint16_t* src, int64_t rows, int64_t K, int64_t R, uint8_t* dst);
 void unpack_rows(const uint8_t* packed, int64_t R, int64_t rows, int64_t K, uint16_t* dst);
 

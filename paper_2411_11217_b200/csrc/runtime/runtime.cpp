@@ -98,6 +98,11 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     V_ = ext.vocab;
     L_ = static_cast<int>(model.layers);
     shard_ = make_shard(model, opt.tp_rank, opt.tp_size);
+    // this rank's slice of every sharded matrix (exec_plan.cpp shard_map): QKV, O, W1/W3, W2
+    maps_[0] = shard_map(model, shard_, kWqkv);
+    maps_[1] = shard_map(model, shard_, kWo);
+    maps_[2] = shard_map(model, shard_, kW1);
+    maps_[3] = shard_map(model, shard_, kW2);
     nq_ = static_cast<int>(shard_.q_heads);
     nkv_ = static_cast<int>(shard_.kv_heads);
     F_ = static_cast<int>(shard_.ffn);
@@ -152,6 +157,10 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
             throw std::invalid_argument("collective must be 0 (NCCL) or 1 (host-staged)");
     }
     arena_ = std::make_unique<Arena>(static_cast<size_t>(opt.budget_bytes));
+    if (opt.weight_codec && opt.weight_fn) {
+        const char* f = std::getenv("MLT_CODEC_FORCE_RAW");
+        if (!(f && f[0] == '1')) scan_raw_blocks();
+    }
     build_catalog();
     allocate();
     generate_weights();
@@ -190,7 +199,7 @@ cudaStream_t Runtime::stream(lightplan::sim::Resource r) const {
 void Runtime::build_catalog() {
     // codec: per-block raw fallback mask (test knob MLT_CODEC_FORCE_RAW=1 stores
     // every block raw, which must decode bit-identically to the encoded run)
-    if (opt_.weight_codec && raw_mask_.empty()) {
+    if (opt_.weight_codec) {
         const char* f = std::getenv("MLT_CODEC_FORCE_RAW");
         if (f && f[0] == '1')
             raw_mask_.assign(mlt::build_catalog(model_, policy_, shard_, true).blocks.size(), 1);
@@ -315,16 +324,64 @@ void Runtime::allocate() {
     }
 }
 
+const uint16_t* Runtime::ext_tensor(int l, int kind, int expert) const {
+    const uint16_t* p = opt_.weight_fn(opt_.weight_ctx, l, kind, expert);
+    if (!p)
+        throw std::invalid_argument("weights: no tensor for layer " + std::to_string(l) + " kind " +
+                                    std::to_string(kind) + " expert " + std::to_string(expert));
+    return p;
+}
+
+void Runtime::packed_block(int l, const WeightBlock& b, uint16_t* dst) const {
+    const ShardMap& sm = maps_[b.kind == kWqkv ? 0 : b.kind == kWo ? 1 : b.kind == kW2 ? 3 : 2];
+    if (opt_.weight_fn)
+        pack_shard_rows(ext_tensor(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0, b.K, b.rb * 128,
+                        (b.rb + 1) * 128, dst);
+    else
+        synth_shard_packed(ext_.seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0, b.K,
+                           b.rb * 128, (b.rb + 1) * 128, sm.scale, dst);
+}
+
+void Runtime::plain_tensor(int l, int kind, int64_t n, float scale, bool is_norm, uint16_t* dst) const {
+    if (opt_.weight_fn)
+        std::memcpy(dst, ext_tensor(l, kind, 0), static_cast<size_t>(n) * 2);
+    else
+        synth_bf16(ext_.seed, tensor_id(l, kind, 0), 0, n, scale, is_norm, dst);
+}
+
+// Caller weights with the codec: a 128-row block whose tiles the code cannot
+// hold (more than 31 escapes in a tile: heavy tails, outlier rows) is stored
+// raw in every layer (one catalog layout for all layers, so the page pool
+// and page table stay uniform).  Synthetic weights always fit.
+void Runtime::scan_raw_blocks() {
+    const Catalog probe = mlt::build_catalog(model_, policy_, shard_, true);
+    raw_mask_.assign(probe.blocks.size(), 0);
+    std::vector<uint16_t> tmp;
+    for (int l = 0; l < L_; ++l)
+        for (size_t i = 0; i < probe.blocks.size(); ++i) {
+            if (raw_mask_[i]) continue;
+            const WeightBlock& b = probe.blocks[i];
+            tmp.resize(static_cast<size_t>(128) * b.K);
+            packed_block(l, b, tmp.data());
+            const int tiles = static_cast<int>(b.K / 64);
+            int bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+            for (int t = 0; t < tiles; ++t) {
+                uint8_t out[kCodecTileBytes];
+                bad += codec_encode_tile(reinterpret_cast<const uint8_t*>(tmp.data()) +
+                                             static_cast<size_t>(t) * mltk::kATileBytes,
+                                         out)
+                           ? 0
+                           : 1;
+            }
+            if (bad) raw_mask_[i] = 1;
+        }
+}
+
 void Runtime::generate_weights() {
     const double t0 = now_s();
     const uint64_t seed = ext_.seed;
     const double sH = 1.0 / std::sqrt(static_cast<double>(H_));
-    // this rank's slice of every sharded matrix (exec_plan.cpp shard_map)
-    const ShardMap maps[] = {shard_map(model_, shard_, kWqkv), shard_map(model_, shard_, kWo),
-                             shard_map(model_, shard_, kW1), shard_map(model_, shard_, kW2)};
-    auto map_of = [&](int kind) -> const ShardMap& {
-        return kind == kWqkv ? maps[0] : kind == kWo ? maps[1] : kind == kW2 ? maps[3] : maps[2];
-    };
     host_blob_pinned_ = opt_.pin_weights != 0;
     if (layer_blob_bytes_) {
         host_blob_ = host_alloc(static_cast<size_t>(L_) * layer_blob_bytes_, host_blob_pinned_, &pin_seconds_);
@@ -338,14 +395,11 @@ void Runtime::generate_weights() {
         for (const auto& b : cat_.blocks) {
             uint8_t* dst = b.resident ? res.data() + b.offset
                                       : host_blob_ + static_cast<int64_t>(l) * layer_blob_bytes_ + b.offset;
-            const ShardMap& sm = map_of(b.kind);
             if (!opt_.weight_codec || (b.raw && codec_mode_ == 1)) {  // packed bf16 tiles
-                synth_shard_packed(seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0,
-                                   b.K, b.rb * 128, (b.rb + 1) * 128, sm.scale, reinterpret_cast<uint16_t*>(dst));
+                packed_block(l, b, reinterpret_cast<uint16_t*>(dst));
             } else if (b.raw) {  // codec 2 raw fallback: fragment-order bf16 tiles
                 tmp_block.resize(static_cast<size_t>(128) * b.K);
-                synth_shard_packed(seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0,
-                                   b.K, b.rb * 128, (b.rb + 1) * 128, sm.scale, tmp_block.data());
+                packed_block(l, b, tmp_block.data());
                 const int tiles = static_cast<int>(b.K / 64);
 #pragma omp parallel for schedule(static)
                 for (int t = 0; t < tiles; ++t)
@@ -354,8 +408,7 @@ void Runtime::generate_weights() {
                                      reinterpret_cast<uint16_t*>(dst + static_cast<size_t>(t) * mltk::kATileBytes));
             } else {  // packed bf16 tiles -> encoded tiles (lossless, weight_codec.hpp)
                 tmp_block.resize(static_cast<size_t>(128) * b.K);
-                synth_shard_packed(seed, tensor_id(l, b.kind, b.expert), sm.k_global, sm.rows.data(), sm.col0,
-                                   b.K, b.rb * 128, (b.rb + 1) * 128, sm.scale, tmp_block.data());
+                packed_block(l, b, tmp_block.data());
                 const int tiles = static_cast<int>(b.K / 64);
                 int bad = 0;
 #pragma omp parallel for schedule(static) reduction(+ : bad)
@@ -366,7 +419,8 @@ void Runtime::generate_weights() {
                     uint8_t* out = dst + static_cast<size_t>(t) * kCodecTileBytes;
                     bad += (codec_mode_ == 2 ? codec_encode_frag_tile(src, out) : codec_encode_tile(src, out)) ? 0 : 1;
                 }
-                if (bad) throw std::invalid_argument("weight_codec: a weight tile does not fit the code");
+                if (bad)  // caller weights were scanned (scan_raw_blocks); synthetic ones always fit
+                    throw std::invalid_argument("weight_codec: a weight tile does not fit the code");
             }
             int entry;
             switch (b.kind) {
@@ -388,27 +442,30 @@ void Runtime::generate_weights() {
                           cudaMemcpyHostToDevice),
                "resident upload");
         std::vector<uint16_t> v(static_cast<size_t>(E_) * H_);
-        synth_bf16(seed, tensor_id(l, kRouter, 0), 0, static_cast<int64_t>(E_) * H_, static_cast<float>(sH), false, v.data());
+        plain_tensor(l, kRouter, static_cast<int64_t>(E_) * H_, static_cast<float>(sH), false, v.data());
         ck(cudaMemcpy(d_router_[l], v.data(), v.size() * 2, cudaMemcpyHostToDevice), "router");
-        synth_bf16(seed, tensor_id(l, kAttnNorm, 0), 0, H_, 0.f, true, v.data());
+        plain_tensor(l, kAttnNorm, H_, 0.f, true, v.data());
         ck(cudaMemcpy(d_attn_norm_[l], v.data(), H_ * 2, cudaMemcpyHostToDevice), "attn_norm");
-        synth_bf16(seed, tensor_id(l, kFfnNorm, 0), 0, H_, 0.f, true, v.data());
+        plain_tensor(l, kFfnNorm, H_, 0.f, true, v.data());
         ck(cudaMemcpy(d_ffn_norm_[l], v.data(), H_ * 2, cudaMemcpyHostToDevice), "ffn_norm");
     }
     ck(cudaMemcpy(dev_tables_, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice), "tables");
     {
         std::vector<uint16_t> big(static_cast<size_t>(V_) * H_);
-        synth_bf16(seed, tensor_id(-1, kEmbed, 0), 0, static_cast<int64_t>(V_) * H_, 1.0f, false, big.data());
+        plain_tensor(-1, kEmbed, static_cast<int64_t>(V_) * H_, 1.0f, false, big.data());
         ck(cudaMemcpy(d_embed_, big.data(), big.size() * 2, cudaMemcpyHostToDevice), "embed");
         const float s_lm = static_cast<float>(static_cast<double>(ext_.lm_head_scale) * sH);
-        synth_bf16_packed(seed, tensor_id(-1, kLmHead, 0), V_, H_, 0, V_, s_lm, big.data());
+        if (opt_.weight_fn)
+            pack_weight(ext_tensor(-1, kLmHead, 0), V_, H_, big.data());
+        else
+            synth_bf16_packed(seed, tensor_id(-1, kLmHead, 0), V_, H_, 0, V_, s_lm, big.data());
         ck(cudaMemcpy(d_lm_, big.data(), big.size() * 2, cudaMemcpyHostToDevice), "lm_head");
         std::vector<const uint8_t*> lt(V_ / 128);
         for (int rb = 0; rb < V_ / 128; ++rb)
             lt[rb] = reinterpret_cast<const uint8_t*>(d_lm_) + static_cast<int64_t>(rb) * 128 * H_ * 2;
         ck(cudaMemcpy(d_lm_table_, lt.data(), lt.size() * sizeof(void*), cudaMemcpyHostToDevice), "lm table");
         std::vector<uint16_t> g(H_);
-        synth_bf16(seed, tensor_id(-1, kFinalNorm, 0), 0, H_, 0.f, true, g.data());
+        plain_tensor(-1, kFinalNorm, H_, 0.f, true, g.data());
         ck(cudaMemcpy(d_final_norm_, g.data(), H_ * 2, cudaMemcpyHostToDevice), "final_norm");
     }
     gen_seconds_ = now_s() - t0;

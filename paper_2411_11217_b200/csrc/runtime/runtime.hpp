@@ -50,6 +50,11 @@ struct RuntimeOptions {
     uint8_t nccl_id[128] = {};     // ncclUniqueId from rank 0 (tp_size > 1)
     bool tp_shard_only = false;    // one shard alone on this GPU, all-reduce elided (measurement)
     int collective = 0;            // tp_size > 1: 0 NCCL, 1 host-staged shared memory (collective_host.cpp)
+    // Caller-owned weights instead of the synthetic PRNG: get(ctx, layer,
+    // kind, expert) returns the FULL row-major bf16 tensor (TensorKind;
+    // layer -1 for embed / lm_head / final norm).  Used during construction only.
+    const uint16_t* (*weight_fn)(void* ctx, int layer, int kind, int expert) = nullptr;
+    void* weight_ctx = nullptr;
     bool weight_codec = false;     // store/stream/read projection + expert weights encoded (weight_codec.hpp)
     bool pdl = true;               // programmatic dependent launch on all-GPU (resident, A_g = 1) schedules
     int expert_down_splits = 0;    // 0: auto (codec: best last-wave fill in 1..8; raw: 1)
@@ -173,6 +178,19 @@ class Runtime {
     const lightplan::ModelSpec& model() const { return model_; }
     double pin_seconds() const { return pin_seconds_; }
     double gen_seconds() const { return gen_seconds_; }
+    double bytes_per_weight() const {
+        double bytes = 0, weights = 0;
+        for (const auto& b : cat_.blocks) {
+            bytes += static_cast<double>(b.bytes);
+            weights += 128.0 * static_cast<double>(b.K);
+        }
+        return weights > 0 ? bytes / weights : 0.0;
+    }
+    int raw_blocks() const {
+        int n = 0;
+        for (const auto& b : cat_.blocks) n += b.raw ? 1 : 0;
+        return n;
+    }
 
     // --- task actions (called by the executor) ---
     struct Ctx;
@@ -192,6 +210,12 @@ class Runtime {
     DecodeReport run(lightplan::sim::ScheduleDag dag, const int32_t* tokens_in, const int32_t* forced, int steps,
                      int32_t* out, lightplan::sim::ScheduleDag* dag_out, lightplan::sim::Timeline* timeline_out);
     void build_catalog();
+    // this rank's packed (SW128) rows of catalog block b of layer l
+    void packed_block(int l, const WeightBlock& b, uint16_t* dst) const;
+    // the first n elements of an unsharded tensor (router, norms, embedding)
+    void plain_tensor(int l, int kind, int64_t n, float scale, bool is_norm, uint16_t* dst) const;
+    const uint16_t* ext_tensor(int l, int kind, int expert) const;
+    void scan_raw_blocks();  // codec + caller weights: blocks the code cannot hold -> raw_mask_
     void dense_tiling(int row_blocks, int& n_cap, int& n_chunks, int& k_splits) const;
     void codec_args(mltk::GemmArgs& a) const;
     // resident CTA slots of the weight GEMMs: 2 per SM for the register-decode codec GEMM
@@ -227,6 +251,7 @@ class Runtime {
     // this rank's shard (exec_plan.hpp Shard)
     int N_, mu_, M_, H_, F_, E_, K_, nq_, nkv_, d_, W_, V_, L_, Ho_;
     Shard shard_;
+    ShardMap maps_[4];
     HostCores host_cores_;  // launcher / attention cores of the current decode
     std::unique_ptr<Collective> coll_;
     float* d_cbuf_ = nullptr;  // [mu, H] TP expert-combine partial (all-reduced)

@@ -66,10 +66,18 @@ class PrefillReport(C.Structure):
 class RuntimeInfo(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("achieved_weight_ratio", "streamed_bytes_per_layer",
                                           "arena_used", "arena_capacity", "pin_seconds",
-                                          "gen_seconds")]
+                                          "gen_seconds", "bytes_per_weight", "raw_blocks")]
+
+
+# mlt_weight_fn: const uint16_t* get(void* ctx, int layer, int kind, int expert)
+WEIGHT_FN = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int)
+# tensor kinds of mlt_runtime_create_with_weights (runtime/host_layout.hpp TensorKind)
+W_EMBED, W_LM_HEAD, W_FINAL_NORM, W_ATTN_NORM, W_FFN_NORM, W_QKV, W_O, W_ROUTER, W_W1, W_W3, W_W2 = range(11)
 
 
 _SIGS = {
+    "runtime_create_with_weights": (C.c_void_p, [C.POINTER(capi.ModelSpec), C.POINTER(capi.Policy),
+                                                 C.POINTER(RuntimeOptions), WEIGHT_FN, C.c_void_p]),
     "runtime_create": (C.c_void_p, [C.POINTER(capi.ModelSpec), C.POINTER(capi.Policy),
                                     C.POINTER(RuntimeOptions)]),
     "runtime_destroy": (None, [C.c_void_p]),
@@ -112,7 +120,10 @@ class Runtime:
                  rope_theta: float = 1e6, lm_head_scale: float = 4.0, exact_gates: bool = True,
                  tp_rank: int = 0, tp_size: int = 1, nccl_id: bytes = b"", schedule: str = "auto",
                  prefill_chunk_tokens: int = 0, tp_shard_only: bool = False, weight_codec: bool = False,
-                 pdl: bool = True, down_splits: int = 0, collective: str = "nccl"):
+                 pdl: bool = True, down_splits: int = 0, collective: str = "nccl", weights=None):
+        """weights: optional callable (layer, kind, expert) -> bf16 bits (uint16
+        ndarray, the FULL row-major tensor; kinds W_*) replacing the synthetic
+        weights (mlt_runtime_create_with_weights)."""
         self.api, self.f = _fns()
         self.model, self.policy = model, policy
         nid = (C.c_uint8 * 128)(*(nccl_id.ljust(128, b"\0")[:128]))
@@ -122,7 +133,22 @@ class Runtime:
                                    -1 if schedule == "auto" else capi.SCHED[schedule],
                                    prefill_chunk_tokens, int(tp_shard_only), int(weight_codec), int(not pdl),
                                    {"nccl": 0, "host": 1}[collective], down_splits)
-        self.h = self.f["runtime_create"](C.byref(model), C.byref(policy), C.byref(self.opts))
+        if weights is None:
+            self.h = self.f["runtime_create"](C.byref(model), C.byref(policy), C.byref(self.opts))
+        else:
+            held = []  # arrays handed to the C side stay alive until the call returns
+
+            def get(_ctx, layer, kind, expert):
+                try:
+                    a = np.ascontiguousarray(weights(layer, kind, expert), dtype=np.uint16)
+                except Exception:  # noqa: BLE001 - reported as a NULL tensor (MLT_ERR_INVALID)
+                    return None
+                held.append(a)
+                return a.ctypes.data
+            cb = WEIGHT_FN(get)
+            self.h = self.f["runtime_create_with_weights"](C.byref(model), C.byref(policy), C.byref(self.opts),
+                                                           cb, None)
+            del held
         if not self.h:
             code = self.api.fn["last_status"]()
             raise capi._EXC.get(code, capi.MltError)(code, self.api.error())

@@ -1,0 +1,101 @@
+"""BASELINE.md §3 / SURVEY §8(d) Config 1: the Tiny model (l=2, h1=1024,
+h2=3584, n_q=8, n_kv=2, 8 experts top-2, vocab 32000), N=8 sequences with a
+16-token prompt (ids seed 5678) and 32 greedy decode steps — end to end on the
+CPU oracle (fp32 activations, OpenMP over the host cores) and on the B200
+(GPU prefill + decode through the C ABI), tokens/sec of both, with the parity
+of the greedy ids (equal up to each sequence's first oracle near-tie).
+
+  python tools/tiny_cpu_gpu.py [--out FILE]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from oracle import bind as orc  # noqa: E402  (tool: the CPU side of the comparison)
+from paper_2411_11217_b200 import capi  # noqa: E402
+from paper_2411_11217_b200.runtime import Runtime  # noqa: E402
+
+N, MU, PROMPT, GEN, VOCAB = 8, 4, 16, 32, 32000
+DIMS = (2, 1024, 3584, 8, 2, 8, 2)
+LM_TIE = 0.05
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    prompts = np.random.default_rng(5678).integers(0, VOCAB, size=(N, PROMPT), dtype=np.int32)
+    l, h1, h2, nq, nkv, ne, k = DIMS
+
+    # ---- CPU oracle: prompt tokens one position at a time (its prefill), then greedy decode
+    t0 = time.perf_counter()
+    m = orc.Model(l, h1, h2, nq, nkv, ne, k, VOCAB, N, PROMPT + GEN + 1, seed=1234)
+    build_cpu = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for s in range(PROMPT):
+        nxt, _ = m.decode_step(prompts[:, s], np.full(N, s, np.int32), orc.FP32)
+    t_pref_cpu = time.perf_counter() - t0
+    ids_cpu, margins = [nxt], []
+    t0 = time.perf_counter()
+    tok = nxt
+    for s in range(GEN - 1):
+        tok, mg = m.decode_step(tok, np.full(N, PROMPT + s, np.int32), orc.FP32)
+        ids_cpu.append(tok)
+        margins.append(mg)
+    t_dec_cpu = time.perf_counter() - t0
+    del m
+
+    # ---- GPU: prefill + decode through the C ABI (device-timed reports; wall clock beside)
+    rt = Runtime(capi.ModelSpec(*DIMS, 2.0, 2.0), capi.Policy(N, MU, 0, 1, 0.0, 0.0), budget_bytes=4e9,
+                 max_ctx=PROMPT + GEN + 8, vocab=VOCAB)
+    rt.prefill(prompts)  # warm-up: kernels / attributes
+    rt.close()
+    rt = Runtime(capi.ModelSpec(*DIMS, 2.0, 2.0), capi.Policy(N, MU, 0, 1, 0.0, 0.0), budget_bytes=4e9,
+                 max_ctx=PROMPT + GEN + 8, vocab=VOCAB)
+    t0 = time.perf_counter()
+    first, prep = rt.prefill(prompts)
+    d = rt.decode(first, GEN - 1)
+    wall_gpu = time.perf_counter() - t0
+    ids_gpu = np.concatenate([first[None], d.ids])
+    rt.close()
+
+    ids_cpu = np.array(ids_cpu)
+    div = [int(np.nonzero(ids_gpu[:, q] != ids_cpu[:, q])[0][0]) if (ids_gpu[:, q] != ids_cpu[:, q]).any()
+           else GEN for q in range(N)]
+    margins = np.array(margins)
+    out = {
+        "workload": "tiny (BASELINE configs[0]): l=2 h1=1024 h2=3584 n_q=8 n_kv=2 8 experts top-2, N=8, "
+                    "prompt 16, gen 32, synthetic weights seed 1234",
+        "host": bench.host_info(),
+        "cpu_oracle": {"threads": orc.lib().orc_num_threads(), "build_s": build_cpu, "prefill_s": t_pref_cpu,
+                       "decode_s": t_dec_cpu,
+                       "prefill_tok_s": N * PROMPT / t_pref_cpu, "decode_tok_s": N * (GEN - 1) / t_dec_cpu,
+                       "generation_tok_s": N * GEN / (t_pref_cpu + t_dec_cpu)},
+        "gpu": {"prefill_s": prep.seconds, "decode_s": d.report.seconds,
+                "prefill_tok_s": prep.tokens_per_second, "decode_tok_s": d.report.tokens_per_second,
+                "generation_tok_s": N * GEN / (prep.seconds + d.report.seconds),
+                "wall_generation_tok_s": N * GEN / wall_gpu},
+        "parity": {"first_divergence_step_per_sequence": div,
+                   "sequences_identical_32_steps": int(sum(x == GEN for x in div)),
+                   "min_lm_margin": float(margins.min()),
+                   "note": "GPU bf16 vs CPU fp32, free running: a divergence is expected only at an oracle "
+                           "near-tie (tests/test_decode_gpu.py asserts it)"},
+    }
+    out["gpu_over_cpu_generation"] = out["gpu"]["generation_tok_s"] / out["cpu_oracle"]["generation_tok_s"]
+    js = json.dumps(out, indent=1)
+    if a.out:
+        with open(a.out, "w") as fh:
+            fh.write(js)
+    print(js)
+
+
+if __name__ == "__main__":
+    main()
