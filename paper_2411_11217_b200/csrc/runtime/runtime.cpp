@@ -131,9 +131,16 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     }
     max_ctx_ = opt.max_ctx;
     Rmu_ = round_up(mu_, 16);
-    // encoded weights: the register-decode GEMM (fragment-order tiles) while a
-    // micro-batch fits its 64-token chunks, else the tcgen05 in-smem decoder
-    codec_mode_ = opt.weight_codec ? (Rmu_ <= 64 ? 2 : 1) : 0;
+    // encoded weights: the tcgen05 GEMM with in-smem decoder warps (codec 1).
+    // The register-decode mma.sync GEMM (codec 2, fragment-order tiles) is
+    // selectable with MLT_CODEC_MODE=2 while a micro-batch fits its 64-token
+    // chunks; measured slower at mu = 64 (gate/up 437 vs 278 us, down 172 vs
+    // 172 us; profiles/r02_codec_engines.txt), so it is not the default.
+    codec_mode_ = 0;
+    if (opt.weight_codec) {
+        const char* m = std::getenv("MLT_CODEC_MODE");
+        codec_mode_ = (m && m[0] == '2' && Rmu_ <= 64) ? 2 : 1;
+    }
     Re_ = round_up(mu_ * K_ + 16 * E_, 16);
     ncap_ = std::min(256, Rmu_);
     ncap_e_ = std::min(128, Rmu_);  // per-expert tiles: 4+ smem stages; m_e > 128 loops in-tile

@@ -13,8 +13,9 @@ Checked:
   * decoding is bit-identical to the same weights with every block raw
     (MLT_CODEC_FORCE_RAW=1): the in-kernel decode is exact on these values;
   * against the CPU oracle holding the same caller weights (teacher-forced on
-    the GPU's routes): residual within 1e-2 every step, ids equal except at
-    lm-head near-ties.
+    the GPU's routes): residual within BASELINE's 2e-2 every step (the x30
+    outlier channels make bf16 activations round coarser than with the
+    synthetic weights' 3e-3), ids equal except at lm-head near-ties.
 """
 import os
 
@@ -127,7 +128,7 @@ def test_codec_raw_fallback_on_heavy_tailed_weights(weights):
         nxt, mg, x = m.decode_step(toks[s], np.full(N, s, np.int32), orc.FAITHFUL, want_x=True)
         rel = np.linalg.norm(xs[s] - x, axis=1) / np.linalg.norm(x, axis=1)
         worst = max(worst, float(rel.max()))
-        assert rel.max() <= 1e-2, (s, float(rel.max()))
+        assert rel.max() <= 2e-2, (s, float(rel.max()))
         for q in np.nonzero(ids[s] != nxt)[0]:
             assert mg[q] < LM_TIE, (s, int(q), float(mg[q]))
     print(f"[heavy-tailed weights] vs oracle (same weights, GPU routes): worst residual {worst:.2e}")
@@ -148,7 +149,7 @@ def test_caller_weights_without_codec_match_oracle(weights):
         m.force_routes(rt.captured_router()[1])
         _, _, x = m.decode_step(toks[s], np.full(N, s, np.int32), orc.FAITHFUL, want_x=True)
         rel = np.linalg.norm(rt.residual() - x, axis=1) / np.linalg.norm(x, axis=1)
-        assert rel.max() <= 1e-2 and d.report.timeline_ok == 1
+        assert rel.max() <= 2e-2 and d.report.timeline_ok == 1
     rt.close()
     partial = {k: v for k, v in weights.items() if k[1] != rtm.W_W2}
     with pytest.raises(capi.MltError, match="no tensor"):

@@ -284,11 +284,13 @@ def test_executed_baseline_schedules_match_cgopipe(prompt):
                 vocab=VOCAB, seed=1234, schedule="s4")
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
 @pytest.mark.parametrize("dims,r_w,a_g,budget", [(TINY, 0.3, 0, 4e9), (TINY, 1.0, 1, 4e9), (SK, 0.5, 0, 4e9),
                                                  (W8X7B, 0.10, 0, 7e9)])
-def test_weight_codec_decode_bitwise_equal(prompt, dims, r_w, a_g, budget):
+def test_weight_codec_decode_bitwise_equal(prompt, dims, r_w, a_g, budget, mode):
     """Decoding with encoded weights (stored, paged and read as 12432-byte
-    tiles; at mu <= 64 the register-decode GEMM, codec 2) returns the same ids
+    tiles; codec 1 = tcgen05 with in-smem decoders, codec 2 = the register-
+    decode mma.sync GEMM, MLT_CODEC_MODE=2) returns the same ids
     and residual bits as the same runtime with every block stored as a raw
     fallback block (MLT_CODEC_FORCE_RAW=1: bf16 tiles through the same GEMMs,
     no decode), while the pages carry 24 % fewer bytes — the in-kernel decode
@@ -297,11 +299,13 @@ def test_weight_codec_decode_bitwise_equal(prompt, dims, r_w, a_g, budget):
     out = []
     for force_raw in (True, False):
         os.environ["MLT_CODEC_FORCE_RAW"] = "1" if force_raw else "0"
+        os.environ["MLT_CODEC_MODE"] = mode
         try:
             rt = Runtime(_model(dims), capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0), budget_bytes=budget,
                          max_ctx=64, vocab=VOCAB, seed=1234, weight_codec=True)
         finally:
             os.environ.pop("MLT_CODEC_FORCE_RAW", None)
+            os.environ.pop("MLT_CODEC_MODE", None)
         first = rt.decode(prompt[0], PROMPT, forced=prompt)
         rest = rt.decode(first.ids[-1], 8)
         out.append((first.ids.copy(), rest.ids.copy(), rt.residual().copy(), rt.info.streamed_bytes_per_layer,
