@@ -222,16 +222,18 @@ def measure_host(api):
 
 def host_info():
     """CPU model and usable cores of this box (stated in both arms' lines)."""
-    model = None
+    model, flags = None, set()
     try:
         with open("/proc/cpuinfo") as fh:
             for ln in fh:
-                if ln.startswith("model name"):
+                if ln.startswith("model name") and model is None:
                     model = ln.split(":", 1)[1].strip()
-                    break
+                elif ln.startswith("flags") and not flags:
+                    flags = set(ln.split(":", 1)[1].split())
     except OSError:
         pass
-    return {"cpu_model": model, "cores": len(os.sched_getaffinity(0))}
+    isa = [f for f in ("avx512f", "avx512_bf16", "amx_bf16", "amx_tile") if f in flags]
+    return {"cpu_model": model, "cores": len(os.sched_getaffinity(0)), "isa": isa}
 
 
 def config_obj(args, cfg, world):
@@ -293,12 +295,13 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def expert_roofline(cfg, rep, pk, traffic, tp=1):
+def expert_roofline(cfg, rep, pk, traffic_src, tp=1):
     """Dominant GPU kernel = expert FFN (gate/up + down GEMM) per micro-batch.
     Algorithmic bytes per launch: sum over touched experts of
     3*h1*h2*dt (all n_e are touched at mu*k >= 128 slots, P(untouched) <
     1e-7) + mu*k*2*h1*dt + mu*h1*dt."""
     l, h1, h2, nq, nkv, ne, k = cfg["model"]
+    traffic, traffic_file = traffic_src
     mu = cfg["mu"]
     wbytes = ne * 3 * h1 * (h2 // tp) * 2
     tokens = mu * k * 2 * h1 * 2 + mu * h1 * 2
@@ -313,7 +316,10 @@ def expert_roofline(cfg, rep, pk, traffic, tp=1):
     peak = pk["hbm_gbs"]
     return {"kernel": "expert_ffn (gemm_tc gate/up+SiLU, gemm_tc down)", "bound": "hbm",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic if tp == 1 else None, "bytes_per_launch": bytes_launch,
+            "traffic": traffic if tp == 1 else None,
+            "traffic_source": (f"ncu dram__bytes_read+write per launch, {traffic_file} (same kernels and shape, "
+                               f"captured outside the timed run)") if tp == 1 and traffic else None,
+            "bytes_per_launch": bytes_launch,
             "bf16_equivalent_gbs": (wbytes + tokens) / avg_s / 1e9,
             "avg_launch_ms": avg_s * 1e3, "launches": rep.expert_launches}
 
@@ -372,11 +378,14 @@ def hrm_kernels(cfg, hw, rep, prof, steps, tp=1, csv_path=None):
 
 
 def load_traffic(codec=False):
-    p = os.path.join(ROOT, "profiles", "expert_ffn_traffic_codec.json" if codec else "expert_ffn_traffic.json")
+    """ncu dram read+write bytes per expert-FFN launch of the same kernels at the
+    same shape (an ncu capture cannot run inside the timed bench): (bytes, file)."""
+    name = "expert_ffn_traffic_codec.json" if codec else "expert_ffn_traffic.json"
+    p = os.path.join(ROOT, "profiles", name)
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f).get("traffic_bytes_per_launch")
-    return None
+            return json.load(f).get("traffic_bytes_per_launch"), "profiles/" + name
+    return None, None
 
 
 def run_mlt(args, cfg):
