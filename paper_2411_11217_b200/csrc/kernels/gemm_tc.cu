@@ -35,9 +35,13 @@ constexpr int kThreadsRaw = 192;    // warp0 producer, warp1 MMA, warps2-5 epilo
 // barrier two phases ahead (mbarrier parity would alias).  Codec launches
 // round the stage count to a multiple of the group count (GemmArgs::dec_groups,
 // 2..kMaxDecGroups: more groups = more tiles decoding concurrently).
-constexpr int kMaxDecGroups = 2;  // 3-4 groups measured no faster (r02 profiles) and cost registers
-constexpr int kDecThreads = 128;  // threads per decoder group
-constexpr int kThreadsCodec = 192 + kMaxDecGroups * kDecThreads;  // launch bound; warps 6+: decoders
+// 8 decoder warps (warps 6-13) form dec_groups groups: 2 groups of 128 threads
+// alternate stages (each group decodes a whole stage), or 1 group of 256
+// threads decodes every stage (half the per-stage decode latency).  3-4
+// groups of 4 warps measured no faster (r02 profiles) and cost registers.
+constexpr int kMaxDecGroups = 2;
+constexpr int kDecWarpThreads = 256;
+constexpr int kThreadsCodec = 192 + kDecWarpThreads;  // launch bound
 constexpr int kCodecTile = 12432;   // encoded tile bytes (runtime/weight_codec.hpp)
 // codec: an encoded tile lands at the END of its 16 KiB A slot and is
 // expanded in place (every input is in registers before any output store)
@@ -61,8 +65,9 @@ static_assert(sizeof(Smem) <= kCtlBytes, "control block fits its reserved bytes"
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
 // named barrier of one decoder group (ids 1.. ; 0 is __syncthreads)
+template <int THR>
 __device__ __forceinline__ void decoders_sync(int grp) {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kDecThreads) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(THR) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -116,28 +121,31 @@ __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// One decoder thread's share of an encoded tile: its units u = dt + j *
-// kDecThreads (8 weights each), the table, and at most one escape entry.
+// One decoder thread's share of an encoded tile: its units u = dt + j * THR
+// (8 weights each), the table, and at most one escape entry.
+template <int THR>
 struct TileIn {
     uint4 T;
-    uint2 lo[1024 / kDecThreads];
-    uint32_t cd[1024 / kDecThreads];
+    uint2 lo[1024 / THR];
+    uint32_t cd[1024 / THR];
     uint32_t n, esc;
 };
-__device__ __forceinline__ void load_tile(uint32_t c, int dt, TileIn& in) {
+template <int THR>
+__device__ __forceinline__ void load_tile(uint32_t c, int dt, TileIn<THR>& in) {
     in.T = lds128(c + 12288);
     in.n = lds32(c + 12304) & 0xffffu;  // {u16 escape count, u16 0}
     in.esc = static_cast<uint32_t>(dt) < in.n ? lds32(c + 12308 + 4 * dt) : 0u;  // {u16 index, u8 hi, 0}
 #pragma unroll
-    for (int j = 0; j < 1024 / kDecThreads; ++j) {
-        const uint32_t u = dt + j * kDecThreads;
+    for (int j = 0; j < 1024 / THR; ++j) {
+        const uint32_t u = dt + j * THR;
         in.lo[j] = lds64(c + u * 8);
         in.cd[j] = lds32(c + 8192 + u * 4);
     }
 }
-__device__ __forceinline__ void store_tile(const TileIn& in, uint32_t d, int dt) {
+template <int THR>
+__device__ __forceinline__ void store_tile(const TileIn<THR>& in, uint32_t d, int dt) {
 #pragma unroll
-    for (int j = 0; j < 1024 / kDecThreads; ++j) {
+    for (int j = 0; j < 1024 / THR; ++j) {
         // code bit 3 of weight k sits at bit 4k+3: byte msbs of cd (odd k) and
         // of cd << 4 (even k) -> one sign-replicating PRMT per 4 weights
         const uint32_t cd = in.cd[j], c4 = cd << 4;
@@ -148,7 +156,7 @@ __device__ __forceinline__ void store_tile(const TileIn& in, uint32_t d, int dt)
         o.y = prmt(in.lo[j].x, h0, 0x7362u);
         o.z = prmt(in.lo[j].y, h1, 0x5140u);
         o.w = prmt(in.lo[j].y, h1, 0x7362u);
-        sts128(d + (dt + j * kDecThreads) * 16, o);
+        sts128(d + (dt + j * THR) * 16, o);
     }
 }
 
@@ -201,6 +209,61 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // co-resident), so the wait always ends.  If it does not within this bound
 // something is badly wrong: trap (a launch error) instead of hanging the GPU.
 constexpr unsigned long long kSpinLimitNs = 2000000000ull;
+
+// Decoder warps of a codec launch (warps 6-13): groups of THR threads own
+// every (256 / THR)-th ring stage.  Per stage: every input (and escape entry)
+// of the group's tiles -> registers, group barrier, expanded 16-byte stores
+// over the same slots, escape bytes, proxy fence (generic smem writes ->
+// tcgen05.mma), barrier, one arrive on the stage's dfull.
+template <int THR>
+__device__ __forceinline__ void decoder_role(const GemmArgs& a, uint8_t* smem, Smem* ctl, int stages, int stage_bytes,
+                                             int kps, int n_virtual, int KB) {
+    constexpr int kGroups = kDecWarpThreads / THR;
+    const int grp = (static_cast<int>(threadIdx.x) - 192) / THR;
+    const int dt = (static_cast<int>(threadIdx.x) - 192) % THR;
+    int stage = 0, kstep = 0;
+    uint32_t phase = 0;
+    for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
+        const VTask tk = vtask(a, v, KB);
+        const int c = tk.c, g = tk.g, kb0 = tk.kb0, kb1 = tk.kb1;
+        const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
+        if (rows <= 0) continue;
+        bool raw_m[kMaxMats] = {false, false};  // raw-fallback blocks: nothing to decode
+        for (int mt = 0; mt < a.n_mats; ++mt)
+            untag(a.a_table[(static_cast<int64_t>(mt) * a.G + tk.g) * a.RB + tk.rb], raw_m[mt]);
+        for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
+            for (int kb = kb0; kb < kb1; kb += kps, ++kstep) {
+                // tiles of this stage: n_mats (one k-block) or kps (n_mats = 1), at most 2;
+                // tile t belongs to matrix t (n_mats = 2) or matrix 0 (n_mats = 1)
+                const bool two = a.n_mats * min(kps, kb1 - kb) == 2;
+                const bool dec0 = !raw_m[0], dec1 = two && !raw_m[a.n_mats == 2 ? 1 : 0];
+                if (stage % kGroups == grp) {
+                    mbar_wait(&ctl->full[stage], phase);
+                    if (a.ktrace && blockIdx.x == 0 && kstep < 256 && dt == 0) a.ktrace[256 + kstep] = globaltimer();
+                    const uint32_t sa = smem_u32(smem + stage * stage_bytes);
+                    TileIn<THR> in0, in1;
+                    in0.n = in1.n = 0;
+                    if (dec0) load_tile<THR>(sa + kCodecOff, dt, in0);
+                    if (dec1) load_tile<THR>(sa + kATileBytes + kCodecOff, dt, in1);
+                    decoders_sync<THR>(grp);  // all inputs read: the slots may be overwritten
+                    if (dec0) store_tile<THR>(in0, sa, dt);
+                    if (dec1) store_tile<THR>(in1, sa + kATileBytes, dt);
+                    if (in0.n + in1.n) {  // rare: high bytes outside the table
+                        decoders_sync<THR>(grp);
+                        if (static_cast<uint32_t>(dt) < in0.n) sts8(sa + 2 * (in0.esc & 0xffffu) + 1, in0.esc >> 16);
+                        if (static_cast<uint32_t>(dt) < in1.n)
+                            sts8(sa + kATileBytes + 2 * (in1.esc & 0xffffu) + 1, in1.esc >> 16);
+                    }
+                    fence_proxy_async_smem();  // generic smem writes -> visible to tcgen05.mma
+                    decoders_sync<THR>(grp);
+                    if (a.ktrace && blockIdx.x == 0 && kstep < 256 && dt == 0) a.ktrace[512 + kstep] = globaltimer();
+                    if (dt == 0) mbar_arrive(&ctl->dfull[stage]);
+                }
+                if (++stage == stages) { stage = 0; phase ^= 1; }
+            }
+        }
+    }
+}
 
 __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -367,55 +430,10 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
         }
     } else if (warp >= 6) {
         // ===== decoders (codec): encoded tiles -> bf16 smem images, in place =====
-        // kDecGroups groups of kDecThreads own alternate ring stages.  Per k-block:
-        // every input (and escape entry) of the group's tiles -> registers,
-        // group barrier, expanded 16-byte stores over the same slots, escape
-        // bytes, proxy fence (generic smem writes -> tcgen05.mma), barrier,
-        // one arrive on the stage's dfull.
-        const int grp = (static_cast<int>(threadIdx.x) - 192) / kDecThreads;
-        const int dt = (static_cast<int>(threadIdx.x) - 192) % kDecThreads;
-        int stage = 0, kstep = 0;
-        uint32_t phase = 0;
-        for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
-            const VTask tk = vtask(a, v, KB);
-            const int c = tk.c, g = tk.g, kb0 = tk.kb0, kb1 = tk.kb1;
-            const int rows = a.b_cnt ? a.b_cnt[g] : a.rows_dense;
-            if (rows <= 0) continue;
-            bool raw_m[kMaxMats] = {false, false};  // raw-fallback blocks: nothing to decode
-            for (int mt = 0; mt < a.n_mats; ++mt)
-                untag(a.a_table[(static_cast<int64_t>(mt) * a.G + tk.g) * a.RB + tk.rb], raw_m[mt]);
-            for (int n0 = c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
-                for (int kb = kb0; kb < kb1; kb += kps, ++kstep) {
-                    // tiles of this stage: n_mats (one k-block) or kps (n_mats = 1), at most 2;
-                    // tile t belongs to matrix t (n_mats = 2) or matrix 0 (n_mats = 1)
-                    const bool two = a.n_mats * min(kps, kb1 - kb) == 2;
-                    const bool dec0 = !raw_m[0], dec1 = two && !raw_m[a.n_mats == 2 ? 1 : 0];
-                    if (stage % a.dec_groups == grp) {
-                        mbar_wait(&ctl->full[stage], phase);
-                        if (a.ktrace && blockIdx.x == 0 && kstep < 256 && dt == 0) a.ktrace[256 + kstep] = globaltimer();
-                        const uint32_t sa = smem_u32(smem + stage * stage_bytes);
-                        TileIn in0, in1;
-                        in0.n = in1.n = 0;
-                        if (dec0) load_tile(sa + kCodecOff, dt, in0);
-                        if (dec1) load_tile(sa + kATileBytes + kCodecOff, dt, in1);
-                        decoders_sync(grp);  // all inputs read: the slots may be overwritten
-                        if (dec0) store_tile(in0, sa, dt);
-                        if (dec1) store_tile(in1, sa + kATileBytes, dt);
-                        if (in0.n + in1.n) {  // rare: high bytes outside the table
-                            decoders_sync(grp);
-                            if (static_cast<uint32_t>(dt) < in0.n) sts8(sa + 2 * (in0.esc & 0xffffu) + 1, in0.esc >> 16);
-                            if (static_cast<uint32_t>(dt) < in1.n)
-                                sts8(sa + kATileBytes + 2 * (in1.esc & 0xffffu) + 1, in1.esc >> 16);
-                        }
-                        fence_proxy_async_smem();  // generic smem writes -> visible to tcgen05.mma
-                        decoders_sync(grp);
-                        if (a.ktrace && blockIdx.x == 0 && kstep < 256 && dt == 0) a.ktrace[512 + kstep] = globaltimer();
-                        if (dt == 0) mbar_arrive(&ctl->dfull[stage]);
-                    }
-                    if (++stage == stages) { stage = 0; phase ^= 1; }
-                }
-            }
-        }
+        if (a.dec_groups == 1)
+            decoder_role<256>(a, smem, ctl, stages, stage_bytes, kps, n_virtual, KB);
+        else
+            decoder_role<128>(a, smem, ctl, stages, stage_bytes, kps, n_virtual, KB);
     } else {
         // ===== epilogue: TMEM -> registers -> global =====
         const uint32_t quarter = warp & 3;  // TMEM lanes this warp may access
@@ -622,7 +640,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     a.stages = budget / per_stage;
     if (a.stages > 8) a.stages = 8;
     if (a.codec) {
-        if (a.dec_groups < 2 || a.dec_groups > kMaxDecGroups) return cudaErrorInvalidValue;
+        if (a.dec_groups < 1 || a.dec_groups > kMaxDecGroups) return cudaErrorInvalidValue;
         a.stages -= a.stages % a.dec_groups;  // decoder groups own whole stages
     }
     if (a.codec != 0 && a.codec != 1) return cudaErrorInvalidValue;  // 2 dispatched above
@@ -662,7 +680,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
             if (!cache[dev][slot] &&
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache[dev][slot], gemm_tc_kernel,
-                                                              a.codec ? 192 + a.dec_groups * kDecThreads : kThreadsRaw,
+                                                              a.codec ? kThreadsCodec : kThreadsRaw,
                                                               227 * 1024 - 1024) != cudaSuccess)
                 cache[dev][slot] = 0;
             per_sm = cache[dev][slot];
@@ -672,7 +690,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     const int n_virtual = a.sk_parts ? a.sk_full + a.sk_tail * a.sk_parts : a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
-    const dim3 block(a.codec ? 192 + a.dec_groups * kDecThreads : kThreadsRaw);
+    const dim3 block(a.codec ? kThreadsCodec : kThreadsRaw);
     if (a.sk_parts) {
         // cooperative: the driver guarantees co-residency of the whole grid or
         // refuses the launch (then: the same GEMM without the stream-K tail)
