@@ -23,6 +23,7 @@
 
 #include <atomic>
 #include <chrono>
+#include <memory>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -122,8 +123,10 @@ class HostStagedCollective final : public Collective {
         check();
         if (count > max_count_) throw std::invalid_argument("host collective: count exceeds capacity");
         cuda_ck(cudaMemcpyAsync(stage_, buf, count * sizeof(float), cudaMemcpyDeviceToHost, s), "collective d2h");
-        cuda_ck(cudaLaunchHostFunc(s, &HostStagedCollective::host_fn, new Call{this, calls_++, count}),
-                "collective host fn");
+        auto call = std::make_unique<Call>(Call{this, calls_, count});
+        cuda_ck(cudaLaunchHostFunc(s, &HostStagedCollective::host_fn, call.get()), "collective host fn");
+        call.release();  // owned by host_fn from here on
+        ++calls_;
         cuda_ck(cudaMemcpyAsync(buf, stage_, count * sizeof(float), cudaMemcpyHostToDevice, s), "collective h2d");
     }
 

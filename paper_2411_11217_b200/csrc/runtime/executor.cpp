@@ -122,7 +122,8 @@ ScheduleDag Runtime::schedule(int steps) const {
 
 DecodeReport Runtime::decode(const int32_t* tokens_in, const int32_t* forced, int steps, int32_t* out,
                              ScheduleDag* dag_out, Timeline* tl_out) {
-    if (steps < 1 || steps > max_steps_) throw std::invalid_argument("steps must be in [1, 64]");
+    if (steps < 1 || steps > max_steps_)
+        throw std::invalid_argument("steps must be in [1, " + std::to_string(max_steps_) + "]");
     return run(schedule(steps), tokens_in, forced, steps, out, dag_out, tl_out);
 }
 
@@ -144,7 +145,8 @@ DecodeReport Runtime::execute(const ScheduleDag& dag, const int32_t* tokens_in, 
             throw std::invalid_argument("execute: the schedule does not match this runtime's model/policy "
                                         "(build it with build_schedule for the same layers, micro-batches and A_g)");
     }
-    if (steps > max_steps_) throw std::invalid_argument("execute: at most 64 decode steps per call");
+    if (steps > max_steps_)
+        throw std::invalid_argument("execute: at most " + std::to_string(max_steps_) + " decode steps per call");
     lightplan::sim::simulate(dag);  // acyclic (CycleDetectedError otherwise)
     return run(dag, tokens_in, forced, steps, out, dag_out, tl_out);
 }
@@ -184,6 +186,14 @@ DecodeReport Runtime::run(ScheduleDag dag, const int32_t* tokens_in, const int32
     struct PdlOff {
         ~PdlOff() { mltk::set_pdl(false); }
     } pdl_off;
+    // task events are created before the measured region opens (tens of
+    // thousands for a long decode; creating them is host work, not decode)
+    std::vector<cudaEvent_t> ev_start(n, nullptr), ev_end(n, nullptr);
+    for (int i = 0; i < n; ++i)
+        if (on_device(dag.tasks[i].resource)) {
+            ck(cudaEventCreate(&ev_start[i]), "event");
+            ck(cudaEventCreate(&ev_end[i]), "event");
+        }
     cudaEvent_t e0, e_end;
     ck(cudaEventCreate(&e0), "event");
     ck(cudaEventCreate(&e_end), "event");
@@ -210,12 +220,6 @@ DecodeReport Runtime::run(ScheduleDag dag, const int32_t* tokens_in, const int32
     ck(cudaStreamWaitEvent(s_d2h_, e_inputs, 0), "wait");
 
     // ---- execute ----
-    std::vector<cudaEvent_t> ev_start(n, nullptr), ev_end(n, nullptr);
-    for (int i = 0; i < n; ++i)
-        if (on_device(dag.tasks[i].resource)) {
-            ck(cudaEventCreate(&ev_start[i]), "event");
-            ck(cudaEventCreate(&ev_end[i]), "event");
-        }
     std::vector<double> h_start(n, 0), h_end(n, 0);
     Flags flags;
     flags.ready.assign(n, 0);

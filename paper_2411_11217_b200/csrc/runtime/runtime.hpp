@@ -297,7 +297,7 @@ class Runtime {
     int32_t* d_tok_out_ = nullptr;      // [max_steps][N]
     int32_t* d_pos_ = nullptr;          // [max_steps][N]
     int32_t* d_seq_ = nullptr;          // [N]
-    int max_steps_ = 64;
+    int max_steps_ = 256;  // decode steps per call (DBRX gen 128 runs in one call)
     // GPU attention (A_g = 1): paged KV pool
     uint16_t *d_kpool_ = nullptr, *d_vpool_ = nullptr;
     int32_t* d_block_table_ = nullptr;  // [L][N][max_pages]
