@@ -53,7 +53,9 @@ CONFIGS = {
                     # (0.79 GB, not in ModelSpec): 0.04/0.18/0.42 fit 16 GB per GPU
                     r_w={1: 0.0, 2: 0.04, 4: 0.18, 8: 0.42}, a_g=0, budget=16e9, prompt=512, gen=128,
                     vocab=32000),
-    "tiny": dict(model=(2, 1024, 3584, 8, 2, 8, 2), N=8, mu=4, r_w=0.0, a_g=0, budget=4e9,
+    # BASELINE configs[0] (the CPU reference's own case): 181 MB of weights per layer fit
+    # any budget, so weights and KV are resident and attention runs on the GPU (S4)
+    "tiny": dict(model=(2, 1024, 3584, 8, 2, 8, 2), N=8, mu=4, r_w=1.0, a_g=1, budget=4e9,
                  prompt=16, gen=32, vocab=32000),
 }
 
