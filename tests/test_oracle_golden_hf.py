@@ -43,3 +43,35 @@ def test_oracle_matches_transformers_mixtral():
         if s >= prompt.shape[1] - 1:
             assert np.array_equal(nxt, ids[:, s + 1])  # = HF's greedy continuation
     assert worst < 1e-3, worst
+
+
+GOLD_BT = os.path.join(os.path.dirname(__file__), "golden", "mixtral_hf_baseline_tiny.npz")
+
+
+def test_oracle_matches_transformers_mixtral_at_baseline_tiny_dims():
+    """The same pin at BASELINE.json configs[0] dimensions (2 layers, h1 1024,
+    h2 3584, 8 query / 2 kv heads, 8 experts top-2, vocab 32000): at every
+    position the oracle's logits at HF's top-64 ids agree to 1e-3 of the
+    logit range, the oracle's argmax is HF's, and HF's greedy continuation is
+    reproduced (tools/make_golden_mixtral.py --config baseline_tiny)."""
+    g = np.load(GOLD_BT)
+    L, H, F, NQ, NKV, E, K, V = (int(g[k]) for k in ("layers", "hidden", "ffn", "q_heads", "kv_heads",
+                                                     "experts", "top_k", "vocab"))
+    ids, prompt = g["ids"], g["prompt"]
+    top_ids, top_logits, rng = g["top_ids"], g["top_logits"], g["logit_range"]
+    N, S = prompt.shape[0], ids.shape[1] - 1
+    m = orc.Model(L, H, F, NQ, NKV, E, K, V, N, S + 2, seed=int(g["seed"]))
+    lm = orc.bf16_to_f32(m.tensor(-1, orc.T_LM_HEAD)).astype(np.float64)
+    gamma = orc.bf16_to_f32(m.tensor(-1, orc.T_FINAL_NORM)).astype(np.float64)
+    worst = 0.0
+    for s in range(S):
+        nxt, _, x = m.decode_step(ids[:, s], np.full(N, s, np.int32), orc.FP32, want_x=True)
+        x = x.astype(np.float64)
+        logits = (x / np.sqrt((x * x).mean(1, keepdims=True) + 1e-5) * gamma) @ lm.T
+        for q in range(N):
+            got = logits[q, top_ids[q, s]]
+            worst = max(worst, float(np.abs(got - top_logits[q, s]).max() / rng[q, s]))
+        assert np.array_equal(nxt, top_ids[:, s, 0])
+        if s >= prompt.shape[1] - 1:
+            assert np.array_equal(nxt, ids[:, s + 1])
+    assert worst < 1e-3, worst

@@ -7,7 +7,12 @@ oracle's "per public Mixtral" semantics (RMSNorm eps 1e-5,
 rotate-half RoPE theta 1e6, GQA, softmax top-2 router renormalised over the
 k, SiLU-gated experts, weighted combine) against the canonical model code.
 
-  python tools/make_golden_mixtral.py      # writes tests/golden/mixtral_hf_tiny.npz
+  python tools/make_golden_mixtral.py [--config toy|baseline_tiny]
+      toy           -> tests/golden/mixtral_hf_tiny.npz (2 layers, h1 512, 4 experts, vocab 1000:
+                       every position's full logits)
+      baseline_tiny -> tests/golden/mixtral_hf_baseline_tiny.npz (BASELINE configs[0]: 2 layers,
+                       h1 1024, h2 3584, n_q 8, n_kv 2, 8 experts top-2, vocab 32000: every
+                       position's top-64 logits with their ids, to keep the fixture small)
 
 The committed fixture is what tests/test_oracle_golden_hf.py checks; this
 script needs transformers (in this container) and is not run by the tests.
@@ -22,8 +27,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from oracle import bind as orc  # noqa: E402
 
-CFG = dict(layers=2, hidden=512, ffn=384, q_heads=4, kv_heads=2, experts=4, top_k=2, vocab=1000)
+CONFIGS = {
+    "toy": dict(layers=2, hidden=512, ffn=384, q_heads=4, kv_heads=2, experts=4, top_k=2, vocab=1000),
+    "baseline_tiny": dict(layers=2, hidden=1024, ffn=3584, q_heads=8, kv_heads=2, experts=8, top_k=2, vocab=32000),
+}
+CFG = dict(CONFIGS["toy"])
 N, PROMPT, GEN, SEED = 3, 10, 6, 1234
+TOPK = 64
 
 
 def oracle_model(max_ctx=PROMPT + GEN + 2):
@@ -82,6 +92,12 @@ def bf16_kv_cache(hf):
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="toy", choices=sorted(CONFIGS))
+    a = ap.parse_args()
+    CFG.clear()
+    CFG.update(CONFIGS[a.config])
     torch.manual_seed(0)
     m = oracle_model()
     hf = hf_model(m)
@@ -93,11 +109,18 @@ def main():
             nxt = hf(ids).logits[:, -1].argmax(-1, keepdim=True)
             ids = torch.cat([ids, nxt], 1)
         logits = hf(ids[:, :-1]).logits.float().numpy()  # every position's next-token logits
-    out = os.path.join(ROOT, "tests", "golden", "mixtral_hf_tiny.npz")
     import transformers
-    np.savez_compressed(out, prompt=prompt.astype(np.int32), ids=ids.numpy().astype(np.int32),
-                        logits=logits.astype(np.float32), seed=SEED, transformers=transformers.__version__,
-                        torch=torch.__version__, **{k: v for k, v in CFG.items()})
+    meta = dict(prompt=prompt.astype(np.int32), ids=ids.numpy().astype(np.int32), seed=SEED,
+                transformers=transformers.__version__, torch=torch.__version__, **{k: v for k, v in CFG.items()})
+    if a.config == "toy":
+        out = os.path.join(ROOT, "tests", "golden", "mixtral_hf_tiny.npz")
+        np.savez_compressed(out, logits=logits.astype(np.float32), **meta)
+    else:  # top-64 logits per position (+ their ids) and each position's logit range
+        out = os.path.join(ROOT, "tests", "golden", f"mixtral_hf_{a.config}.npz")
+        top = np.argsort(-logits, axis=-1)[..., :TOPK]
+        np.savez_compressed(out, top_ids=top.astype(np.int32),
+                            top_logits=np.take_along_axis(logits, top, -1).astype(np.float32),
+                            logit_range=np.abs(logits).max(-1).astype(np.float32), **meta)
     print("wrote", out, logits.shape, "greedy", ids[:, PROMPT:].tolist())
 
 
