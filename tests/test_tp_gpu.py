@@ -43,7 +43,7 @@ LM_TIE = 0.05
 ROUTER_TIE = 0.02
 
 
-def _launch(tmp_path, dims, size, a_g, r_w, budget):
+def _launch(tmp_path, dims, size, a_g, r_w, budget, codec=False):
     from paper_2411_11217_b200.runtime import host_collective_name
     name = host_collective_name().decode()
     procs, outs = [], []
@@ -53,7 +53,8 @@ def _launch(tmp_path, dims, size, a_g, r_w, budget):
         outs.append(out)
         procs.append(subprocess.Popen([sys.executable, WORKER, "--rank", str(r), "--size", str(size), "--name", name,
                                        "--dims", ",".join(map(str, dims)), "--out", out, "--a-g", str(a_g),
-                                       "--r-w", str(r_w), "--budget", str(budget)], env=env))
+                                       "--r-w", str(r_w), "--budget", str(budget)] + (["--codec"] if codec else []),
+                                      env=env))
     for p in procs:
         assert p.wait(timeout=900) == 0
     return [dict(np.load(o)) for o in outs]
@@ -85,17 +86,17 @@ def _oracle_check(dims, run, tag):
     return {"worst_rel_residual": worst, "id_mismatches_at_lm_ties": id_diff, "router_flips_at_ties": flips}
 
 
-@pytest.mark.parametrize("dims,a_g,r_w,budget", [(TINY, 0, 0.0, 4e9), (TINY, 1, 1.0, 4e9),
-                                                 (W8X22B, 0, 0.05, 8e9)])
-def test_tp2_two_ranks_one_gpu(tmp_path, dims, a_g, r_w, budget):
-    r0, r1 = _launch(tmp_path, dims, 2, a_g, r_w, budget)
+@pytest.mark.parametrize("dims,a_g,r_w,budget,codec", [(TINY, 0, 0.0, 4e9, False), (TINY, 1, 1.0, 4e9, False),
+                                                       (W8X22B, 0, 0.05, 8e9, False), (TINY, 0, 0.3, 4e9, True)])
+def test_tp2_two_ranks_one_gpu(tmp_path, dims, a_g, r_w, budget, codec):
+    r0, r1 = _launch(tmp_path, dims, 2, a_g, r_w, budget, codec)
     assert r0["timeline_ok"] == 1 and r1["timeline_ok"] == 1
     for k in ("ids", "routes"):  # replicated routing: identical on every rank
         assert np.array_equal(r0[k], r1[k]), k
     assert np.array_equal(r0["x"].view(np.uint32), r1["x"].view(np.uint32))
     one = tmp_path / "one"
     one.mkdir()
-    (u,) = _launch(one, dims, 1, a_g, r_w, 2 * budget)  # the unsharded model needs both ranks' budget
+    (u,) = _launch(one, dims, 1, a_g, r_w, 2 * budget, codec)  # the unsharded model needs both ranks' budget
     if r_w < 1.0:
         assert float(r0["streamed"]) == pytest.approx(float(u["streamed"]) / 2, rel=0.03)
     same_route = (r0["routes"] == u["routes"]).all(axis=(0, 1, 3))  # per sequence, every step and layer

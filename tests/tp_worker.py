@@ -24,11 +24,11 @@ from paper_2411_11217_b200.runtime import Runtime  # noqa: E402
 N, MU, STEPS, VOCAB = 8, 4, 24, 32000
 
 
-def run(rank, size, name, dims, out, a_g=0, r_w=0.0, budget=4e9, layers=2, experts=8, top_k=2):
+def run(rank, size, name, dims, out, a_g=0, r_w=0.0, budget=4e9, layers=2, experts=8, top_k=2, codec=False):
     h1, h2, nq, nkv = dims
     model = capi.ModelSpec(layers, h1, h2, nq, nkv, experts, top_k, 2.0, 2.0)
     pol = capi.Policy(N, MU, a_g, 1, r_w, 1.0 if a_g else 0.0)
-    kw = dict(budget_bytes=budget, max_ctx=64, vocab=VOCAB, seed=1234)
+    kw = dict(budget_bytes=budget, max_ctx=64, vocab=VOCAB, seed=1234, weight_codec=codec)
     if size > 1:
         kw.update(tp_rank=rank, tp_size=size, nccl_id=name.encode(), collective="host")
     rt = Runtime(model, pol, **kw)
@@ -60,5 +60,7 @@ if __name__ == "__main__":
     ap.add_argument("--a-g", type=int, default=0)
     ap.add_argument("--r-w", type=float, default=0.0)
     ap.add_argument("--budget", type=float, default=4e9)
+    ap.add_argument("--codec", action="store_true")
     a = ap.parse_args()
-    run(a.rank, a.size, a.name, tuple(int(x) for x in a.dims.split(",")), a.out, a.a_g, a.r_w, a.budget)
+    run(a.rank, a.size, a.name, tuple(int(x) for x in a.dims.split(",")), a.out, a.a_g, a.r_w, a.budget,
+        codec=a.codec)
