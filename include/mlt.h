@@ -427,6 +427,15 @@ int mlt_gqa_decode_paged_split(const uint16_t* q, int ldq, const uint16_t* k_poo
                                const int32_t* ctx, int T, int nq, int nkv, int d, int page, void* out_packed,
                                int R, float* out_rowmajor, int splits, int max_splits, float* scratch,
                                int32_t* counters, void* stream);
+/* Stream-K variant (gqa_decode_flat_kernel): `ctas` resident CTAs (0 = 2 per
+ * SM) split the flattened (token, kv head, page) space evenly, partial
+ * softmax states of shared (token, head) segments merged in warp order by the
+ * last arriver.  scratch >= ctas*4*2*(nq/nkv)*130 floats; counters >= T*nkv
+ * int32 zeroed once (left zero).  T <= 4096.  Same output. */
+int mlt_gqa_decode_paged_flat(const uint16_t* q, int ldq, const uint16_t* k_pool, const uint16_t* v_pool,
+                              const int32_t* block_table, int max_pages, const int32_t* seq, const int32_t* ctx, int T,
+                              int nq, int nkv, int d, int page, void* out_packed, int R, float* out_rowmajor, int ctas,
+                              float* scratch, int32_t* counters, void* stream);
 int mlt_kv_append(const uint16_t* qkv_bf16, int nq, int nkv, int d, const int32_t* seq,
                   const int32_t* pos, int T, const int32_t* block_table, int max_pages, int page,
                   uint16_t* k_pool, uint16_t* v_pool, void* stream);

@@ -591,6 +591,7 @@ _KSIGS = {
     "argmax": [V, I, I, V, V, V],
     "gqa_decode_paged": [V, I, V, V, V, I, V, V, I, I, I, I, I, V, I, V, V],
     "gqa_decode_paged_split": [V, I, V, V, V, I, V, V, I, I, I, I, I, V, I, V, I, I, V, V, V],
+    "gqa_decode_paged_flat": [V, I, V, V, V, I, V, V, I, I, I, I, I, V, I, V, I, V, V, V],
     "kv_append": [V, I, I, I, V, V, I, V, I, I, V, V, V],
     "rope_table": [I, I, C.c_double, V],
     "prefill_attention": [V, I, V, I, I, I, I, V, I, V],

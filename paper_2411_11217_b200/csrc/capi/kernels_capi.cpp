@@ -343,6 +343,22 @@ int mlt_gqa_decode_paged_split(const uint16_t* q, int ldq, const uint16_t* kp, c
     });
 }
 
+int mlt_gqa_decode_paged_flat(const uint16_t* q, int ldq, const uint16_t* kp, const uint16_t* vp, const int32_t* bt,
+                              int max_pages, const int32_t* seq, const int32_t* ctx, int T, int nq, int nkv, int d,
+                              int page, void* out_packed, int R, float* out_f, int ctas, float* scratch,
+                              int32_t* counters, void* s) {
+    return guard([&] {
+        mltk::GqaFlat fl;
+        fl.ctas = ctas > 0 ? ctas : mltk::gqa_flat_ctas(sm_count());
+        fl.scratch = scratch;
+        fl.counters = counters;
+        ck(mltk::launch_gqa_decode_flat(q, ldq, kp, vp, bt, max_pages, seq, ctx, T, nq, nkv, d, page,
+                                        reinterpret_cast<uint8_t*>(out_packed), R, out_f, fl, st(s)),
+           "gqa_decode_paged_flat");
+        return MLT_OK;
+    });
+}
+
 int mlt_kv_append(const uint16_t* qkv, int nq, int nkv, int d, const int32_t* seq,
                   const int32_t* pos, int T, const int32_t* bt, int max_pages, int page,
                   uint16_t* kp, uint16_t* vp, void* s) {

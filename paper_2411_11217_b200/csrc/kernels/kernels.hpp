@@ -159,6 +159,20 @@ struct GqaSplit {
     float* scratch = nullptr;
     int* counters = nullptr;
 };
+// Stream-K decode (attention.cu gqa_decode_flat_kernel): ctas = gqa_flat_ctas(#SMs)
+// resident CTAs split the flattened (token, kv head, page) space evenly;
+// scratch >= ctas * 4 warps * 2 slots * G * 130 floats, counters >= T * nkv
+// ints zeroed once (every launch leaves them zero).  Same output.
+struct GqaFlat {
+    int ctas = 0;
+    float* scratch = nullptr;
+    int* counters = nullptr;
+};
+int gqa_flat_ctas(int num_sms);
+cudaError_t launch_gqa_decode_flat(const uint16_t* q, int ldq, const uint16_t* k_pool, const uint16_t* v_pool,
+                                   const int32_t* block_table, int max_pages, const int32_t* seq, const int32_t* ctx,
+                                   int T, int nq, int nkv, int d, int page, uint8_t* out_packed, int R,
+                                   float* out_rowmajor, const GqaFlat& fl, cudaStream_t s);
 cudaError_t launch_gqa_decode_paged(const uint16_t* q, int ldq, const uint16_t* k_pool,
                                     const uint16_t* v_pool, const int32_t* block_table,
                                     int max_pages, const int32_t* seq, const int32_t* ctx, int T,

@@ -281,6 +281,19 @@ def test_rope_and_paged_attention(K, nq, nkv):
     # left at zero for the next launch
     scratch = torch.zeros(T * nq * 8 * 130, device="cuda")
     counters = torch.zeros(T * nkv, dtype=torch.int32, device="cuda")
+    # stream-K decode over the flattened (token, head, page) space: the default
+    # grid (2 CTAs per SM: more warps than pages here, so single-page ranges and
+    # many-part merges) and small grids (multi-segment ranges)
+    fscratch = torch.zeros(296 * 4 * 2 * (nq // nkv) * 130, device="cuda")
+    fcount = torch.zeros(T * nkv, dtype=torch.int32, device="cuda")
+    for ctas in (0, 1, 3, 7):
+        out3 = torch.zeros_like(out)
+        outp3 = torch.zeros_like(outp)
+        K.gqa_decode_paged_flat(ptr(rb), W, ptr(kpool), ptr(vpool), ptr(bt_d), max_pages, ptr(seq), ptr(ctx_d), T,
+                                nq, nkv, d, page, ptr(outp3), R, ptr(out3), ctas, ptr(fscratch), ptr(fcount), stream())
+        torch.cuda.synchronize()
+        assert np.abs(out3.cpu().numpy() - ref).max() < 2e-3, ctas
+        assert int(fcount.abs().sum()) == 0
     for splits in (2, 3, 8, 0, 8):
         out2 = torch.zeros_like(out)
         outp2 = torch.zeros_like(outp)

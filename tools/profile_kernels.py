@@ -181,6 +181,13 @@ def main():
     att_scratch = torch.zeros(mu * NQ * 8 * 130, device="cuda")
     att_cnt = torch.zeros(mu * NKV, dtype=torch.int32, device="cuda")
 
+    flat_scratch = torch.zeros(296 * 4 * 2 * (NQ // NKV) * 130, device="cuda")
+
+    def attention_flat():  # stream-K over the flattened (token, head, page) space
+        KD.gqa_decode_paged_flat(ptr(qrows), W, ptr(kpool), ptr(vpool), ptr(bt), pages_per, ptr(seq),
+                                 ptr(ctxs), mu, NQ, NKV, D, 16, ptr(attn_out), Rmu, None, 0,
+                                 ptr(flat_scratch), ptr(att_cnt), s)
+
     def attention_split():  # the runtime's call: split-KV, auto split count
         KD.gqa_decode_paged_split(ptr(qrows), W, ptr(kpool), ptr(vpool), ptr(bt), pages_per, ptr(seq),
                                   ptr(ctxs), mu, NQ, NKV, D, 16, ptr(attn_out), Rmu, None, 0, 8,
@@ -199,6 +206,7 @@ def main():
         ("o_proj (+residual)", dense_o, H * H * 2 + mu * H * 4 * 2),
         ("gqa_decode_paged (ctx 528)", attention, mu * 2 * CTX * NKV * D * 2),
         ("gqa_decode_paged split-KV (ctx 528)", attention_split, mu * 2 * CTX * NKV * D * 2),
+        ("gqa_decode_paged stream-K (ctx 528)", attention_flat, mu * 2 * CTX * NKV * D * 2),
     ]
     reps = 2 if a.once else a.reps
     out = {}
