@@ -360,10 +360,12 @@ __global__ void __launch_bounds__(kWarps * 32) gqa_decode_flat_kernel(
         __syncthreads();
     }
     const int64_t P = static_cast<int64_t>(nkv) * pre[T];
-    const int64_t W = static_cast<int64_t>(gridDim.x) * kWarps;
+    // W <= P working warps, so every range is non-empty and the warps covering
+    // a segment are exactly owner(s0) .. owner(s1 - 1)
+    const int64_t W = min(static_cast<int64_t>(gridDim.x) * kWarps, P);
     const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+    if (gw >= W) return;  // no barriers below: idle warps may leave
     const int64_t f0 = gw * P / W, f1 = (gw + 1) * P / W;
-    if (f0 >= f1) return;  // no barriers below: idle warps may leave
 
     uint8_t* ring = sm + static_cast<size_t>(warp) * kStagesW * 2 * kPageBytes;
     const uint32_t ring_s = smem_u32(ring);
@@ -456,23 +458,49 @@ __global__ void __launch_bounds__(kWarps * 32) gqa_decode_flat_kernel(
         last = __shfl_sync(0xffffffffu, last, 0);
         if (!last) return;
         __threadfence();  // acquire the other parts
-        for (int idx = lane; idx < G * kD; idx += 32) {
-            const int hh = idx / kD, d = idx % kD;
-            auto slot_of = [&](int64_t w) {  // as the writer chose: 0 if the segment began before w's range
-                return s0 < w * P / W ? 0 : 1;
-            };
-            float M = -INFINITY;
-            for (int64_t w = w_first; w <= w_last; ++w)
-                M = fmaxf(M, __ldcg(part + (w * 2 + slot_of(w)) * kPartF + hh * (kD + 2) + kD));
-            float den = 0.f, num = 0.f;
-            for (int64_t w = w_first; w <= w_last; ++w) {  // warp order: deterministic
-                const float* c = part + (w * 2 + slot_of(w)) * kPartF + hh * (kD + 2);
-                const float l2 = __ldcg(c + kD + 1);
-                const float f = l2 > 0.f ? exp2f(__ldcg(c + kD) - M) : 0.f;
-                den += l2 * f;
-                num += __ldcg(c + d) * f;
+        // merge in warp order (deterministic), 8 parts at a time with every
+        // load of a batch in flight before the arithmetic (one L2 round trip
+        // per batch and head instead of one per part)
+        auto slot_of = [&](int64_t w) { return s0 < w * P / W ? 0 : 1; };  // as the writer chose
+        for (int hh = 0; hh < G; ++hh) {
+            float M = -INFINITY, den = 0.f, num[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int64_t w0 = w_first; w0 <= w_last; w0 += 8) {
+                float mv[8], lv[8], ov[8][4];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int64_t w = w0 + j;
+                    if (w <= w_last) {
+                        const float* c = part + (w * 2 + slot_of(w)) * kPartF + hh * (kD + 2);
+                        mv[j] = __ldcg(c + kD);
+                        lv[j] = __ldcg(c + kD + 1);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) ov[j][i] = __ldcg(c + lane + 32 * i);
+                    } else {
+                        mv[j] = -INFINITY;
+                        lv[j] = 0.f;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) ov[j][i] = 0.f;
+                    }
+                }
+                float Mn = M;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (lv[j] > 0.f) Mn = fmaxf(Mn, mv[j]);
+                const float sc = den > 0.f ? exp2f(M - Mn) : 0.f;  // rescale what is merged so far
+                den *= sc;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) num[i] *= sc;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float f = lv[j] > 0.f ? exp2f(mv[j] - Mn) : 0.f;
+                    den += lv[j] * f;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) num[i] += ov[j][i] * f;
+                }
+                M = Mn;
             }
-            store(hh, d, num / den);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) store(hh, lane + 32 * i, num[i] / den);
         }
         if (lane == 0) cnt[cur_t * nkv + cur_h] = 0;
     };
