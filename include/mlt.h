@@ -317,6 +317,11 @@ int mlt_codec_tile_bytes(void);
  * previous blocks' sizes.  Returns the number of raw blocks (>= 0). */
 int mlt_codec_encode_frag(const uint8_t* host_packed, int64_t M, int64_t K, uint8_t* host_out,
                           uint8_t* raw_blocks);
+/* The row-plane code of the TMEM-operand GEMM (GemmArgs codec = 3, kernels/
+ * gemm_tc.cu; runtime/weight_codec.hpp rows_from_packed): same contract as
+ * mlt_codec_encode_frag; raw fallback blocks are plain 16 KiB packed tiles. */
+int mlt_codec_encode_rows(const uint8_t* host_packed, int64_t M, int64_t K, uint8_t* host_out,
+                          uint8_t* raw_blocks);
 /* 16 KiB packed tiles -> fragment-order bf16 tiles (raw codec-2 blocks). */
 int mlt_frag_pack(const uint8_t* host_packed, int64_t tiles, uint8_t* host_out);
 /* Host-core GQA decode attention (A_g = 0: the CpuAttn task, pipesim.hpp:26,
@@ -367,9 +372,14 @@ typedef struct mlt_gemm_args_t {
                                   mlt_codec_encode), expanded in smem by decoder warps (tcgen05);
                                   2: fragment-order encoded blocks (mlt_codec_encode_frag), decoded
                                   in registers and multiplied with mma.sync (n_cap <= 64, <= 32
-                                  for n_mats = 2; kernels/gemm_codec.cu) */
+                                  for n_mats = 2; kernels/gemm_codec.cu);
+                                  3: row-plane encoded blocks (mlt_codec_encode_rows), each decoder
+                                  thread expands one weight row into tensor memory and the
+                                  tcgen05.mma reads A from TMEM (raw fallback blocks: tag bit 0) */
     unsigned long long* ktrace; /* optional CTA-0 pipeline trace [4][256] %globaltimer stamps per
-                                   k-block: producer issue, decoder start, decoder done, MMA start */
+                                   k-block: producer issue, decoder start, decoder done, MMA start;
+                                   codec 3: [6][256] per weight tile: producer issue, landed,
+                                   decoded, TMEM slot granted, stored, MMA start */
     float* sk_scratch;         /* optional stream-K tail for epi = 1 (n_chunks = k_splits = 1): fp32
                                   scratch [#SMs][2][sk_rows][128]; NULL disables it */
     int64_t* sk_count;         /* [#SMs] 64-bit arrival counters, zeroed once by the caller */

@@ -574,6 +574,7 @@ _KSIGS = {
     "codec_encode": [V, C.c_int64, C.c_int64, V],
     "codec_decode": [V, C.c_int64, V],
     "codec_encode_frag": [V, C.c_int64, C.c_int64, V, V],
+    "codec_encode_rows": [V, C.c_int64, C.c_int64, V, V],
     "frag_pack": [V, C.c_int64, V],
     "host_gqa_decode": [V, V, V, V, I, I, I, I, I, V, I],
     "host_gqa_use_amx": [I],

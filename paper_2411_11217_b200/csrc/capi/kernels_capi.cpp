@@ -120,39 +120,59 @@ int mlt_codec_decode(const uint8_t* enc, int64_t tiles, uint8_t* packed) {
 
 int mlt_codec_tile_bytes(void) { return mlt::kCodecTileBytes; }
 
+// Encode an [M, K] packed matrix in a reordered code (fragment / row-plane
+// order) with the per-block raw fallback: a 128-row block with a tile the
+// code cannot hold is stored as 16 KiB raw tiles (raw_tile: packed -> the
+// engine's raw layout), its flag set in raw_blocks; without raw_blocks such
+// a block is an error.  Returns the number of raw blocks.
+static int encode_blocks(const char* what, const uint8_t* packed, int64_t M, int64_t K, uint8_t* out,
+                         uint8_t* raw_blocks, bool (*enc)(const uint8_t*, uint8_t*),
+                         void (*raw_tile)(const uint8_t*, uint8_t*)) {
+    if (M % 128 || K % 64 || M <= 0 || K <= 0) throw std::invalid_argument(std::string(what) + ": M%128, K%64");
+    const int64_t kb = K / 64, rbs = M / 128;
+    std::vector<int64_t> off(rbs + 1, 0);
+    std::vector<uint8_t> raw(rbs, 0);
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+    for (int64_t r = 0; r < rbs; ++r) {
+        uint8_t tmp[mlt::kCodecTileBytes];
+        for (int64_t t = 0; t < kb; ++t)
+            if (!enc(packed + (r * kb + t) * 16384, tmp)) {
+                raw[r] = 1;
+                ++bad;
+                break;
+            }
+    }
+    if (bad && !raw_blocks)
+        throw std::invalid_argument(std::string(what) + ": " + std::to_string(bad) + " row block(s) need > " +
+                                    std::to_string(mlt::kCodecMaxEscapes) + " escapes in a tile");
+    for (int64_t r = 0; r < rbs; ++r) off[r + 1] = off[r] + kb * (raw[r] ? 16384 : mlt::kCodecTileBytes);
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < rbs; ++r)
+        for (int64_t t = 0; t < kb; ++t) {
+            const uint8_t* src = packed + (r * kb + t) * 16384;
+            if (raw[r])
+                raw_tile(src, out + off[r] + t * 16384);
+            else
+                enc(src, out + off[r] + t * mlt::kCodecTileBytes);
+        }
+    if (raw_blocks) std::memcpy(raw_blocks, raw.data(), static_cast<size_t>(rbs));
+    return bad;
+}
+
 int mlt_codec_encode_frag(const uint8_t* packed, int64_t M, int64_t K, uint8_t* out, uint8_t* raw_blocks) {
     return guard([&] {
-        if (M % 128 || K % 64 || M <= 0 || K <= 0) throw std::invalid_argument("codec_encode_frag: M%128, K%64");
-        const int64_t kb = K / 64, rbs = M / 128;
-        // per row block: encoded tiles, or (raw_blocks given) 16 KiB fragment-order tiles when a tile fails
-        std::vector<int64_t> off(rbs + 1, 0);
-        std::vector<uint8_t> raw(rbs, 0);
-        int bad = 0;
-#pragma omp parallel for schedule(static) reduction(+ : bad)
-        for (int64_t r = 0; r < rbs; ++r) {
-            uint8_t tmp[mlt::kCodecTileBytes];
-            for (int64_t t = 0; t < kb; ++t)
-                if (!mlt::codec_encode_frag_tile(packed + (r * kb + t) * 16384, tmp)) {
-                    raw[r] = 1;
-                    ++bad;
-                    break;
-                }
-        }
-        if (bad && !raw_blocks)
-            throw std::invalid_argument("codec_encode_frag: " + std::to_string(bad) + " row block(s) need > " +
-                                        std::to_string(mlt::kCodecMaxEscapes) + " escapes in a tile");
-        for (int64_t r = 0; r < rbs; ++r) off[r + 1] = off[r] + kb * (raw[r] ? 16384 : mlt::kCodecTileBytes);
-#pragma omp parallel for schedule(static)
-        for (int64_t r = 0; r < rbs; ++r)
-            for (int64_t t = 0; t < kb; ++t) {
-                const uint8_t* src = packed + (r * kb + t) * 16384;
-                if (raw[r])
-                    mlt::frag_from_packed(src, reinterpret_cast<uint16_t*>(out + off[r] + t * 16384));
-                else
-                    mlt::codec_encode_frag_tile(src, out + off[r] + t * mlt::kCodecTileBytes);
-            }
-        if (raw_blocks) std::memcpy(raw_blocks, raw.data(), static_cast<size_t>(rbs));
-        return static_cast<int>(bad);
+        return encode_blocks("codec_encode_frag", packed, M, K, out, raw_blocks, mlt::codec_encode_frag_tile,
+                             [](const uint8_t* src, uint8_t* dst) {
+                                 mlt::frag_from_packed(src, reinterpret_cast<uint16_t*>(dst));
+                             });
+    });
+}
+
+int mlt_codec_encode_rows(const uint8_t* packed, int64_t M, int64_t K, uint8_t* out, uint8_t* raw_blocks) {
+    return guard([&] {
+        return encode_blocks("codec_encode_rows", packed, M, K, out, raw_blocks, mlt::codec_encode_rows_tile,
+                             [](const uint8_t* src, uint8_t* dst) { std::memcpy(dst, src, 16384); });
     });
 }
 

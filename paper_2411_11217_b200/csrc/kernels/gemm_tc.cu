@@ -41,22 +41,31 @@ constexpr int kThreadsRaw = 192;    // warp0 producer, warp1 MMA, warps2-5 epilo
 // groups of 4 warps measured no faster (r02 profiles) and cost registers.
 constexpr int kMaxDecGroups = 2;
 constexpr int kDecWarpThreads = 256;
-constexpr int kThreadsCodec = 192 + kDecWarpThreads;  // launch bound
+constexpr int kThreadsCodec = 192 + kDecWarpThreads;
+// codec 3: + warp 14, the token-tile (B) producer
+// codec 3: kTsGroups decoder groups of 4 warps (warps 6 .. 6 + 4 kTsGroups - 1)
+// + the token-tile (B) producer warp after them
+constexpr int kTsGroups = 3;
+constexpr int kTsBWarp = 6 + 4 * kTsGroups;
+constexpr int kThreadsCodec3 = 32 * (kTsBWarp + 1);
 constexpr int kCodecTile = 12432;   // encoded tile bytes (runtime/weight_codec.hpp)
 // codec: an encoded tile lands at the END of its 16 KiB A slot and is
 // expanded in place (every input is in registers before any output store)
 constexpr int kCodecOff = kATileBytes - kCodecTile;  // 3952, 16-byte aligned
 constexpr int kMaxMats = 2;
 constexpr int kEpiChunks = 1;           // 16-token TMEM chunks per load wait in the epilogue
-constexpr int kCtlBytes = 256;           // barriers + TMEM base
+constexpr int kCtlBytes = 1024;          // barriers + TMEM base
+constexpr int kMaxRing = 16;             // codec 3: encoded-A ring slots / TMEM A slots
 constexpr int kEpiScratch = 4 * 2048;    // per epilogue warp: 16 x 32 fp32 transpose tile
 
 struct Smem {
-    uint64_t full[8];
-    uint64_t empty[8];
+    uint64_t full[kMaxRing];   // stage landed (codec 3: encoded A slot landed)
+    uint64_t empty[kMaxRing];  // stage free (codec 3: encoded A slot read by its decoders)
     uint64_t tfull[2];
     uint64_t tempty[2];
-    uint64_t dfull[8];  // codec: decoders -> MMA, stage's A tiles decoded in place
+    uint64_t dfull[kMaxRing];  // codec 1: stage's A tiles decoded in place; codec 3: TMEM A slot written
+    uint64_t aslot_empty[kMaxRing];  // codec 3: TMEM A slot consumed by the MMA
+    uint64_t bfull[8], bempty[8];    // codec 3: token-tile ring
     uint32_t tmem_base;
 };
 
@@ -265,7 +274,253 @@ __device__ __forceinline__ void decoder_role(const GemmArgs& a, uint8_t* smem, S
     }
 }
 
-__global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArgs a) {
+// ---- codec 3: decode into tensor memory -----------------------------------
+// Decoder thread (warp w, lane) owns row r = 32 (w % 4) + lane of a tile —
+// the TMEM lane quarter warp w may access — and expands that row's 64
+// weights (row-plane order, weight_codec.hpp rows_from_packed: 4 x 16-byte
+// low-byte words + 4 x 8-byte code words, lane-consecutive) into the 32 TMEM
+// columns of lane r (k pairs per 32-bit column, the A-operand layout of
+// tcgen05.mma with A in TMEM).  No shared-memory writes: the A operand
+// never returns to smem, the MMA reads it from TMEM.
+__device__ __forceinline__ void decode_row_ts(uint32_t c, uint32_t r, uint32_t (&o)[32]) {
+    const uint4 T = lds128(c + 12288);
+    const uint32_t n = lds32(c + 12304) & 0xffffu;
+    uint4 lo[4];
+    uint2 cd[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        lo[j] = lds128(c + (j * 128u + r) * 16u);
+        cd[j] = lds64(c + 8192u + (j * 128u + r) * 8u);
+    }
+    // escapes (n <= 31): lane e holds entry e {u16 index, u8 high byte}
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t my_ent = lane < n ? lds32(c + 12308u + 4u * lane) : 0u;
+    // branch-free expansion of the 8 units (independent: full ILP)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t cw = h ? cd[j].y : cd[j].x, c4 = cw << 4;
+            const uint32_t h0 = hi4(cw & 0x7777u, prmt(c4, cw, 0xD9C8u), T);
+            const uint32_t h1 = hi4((cw >> 16) & 0x7777u, prmt(c4, cw, 0xFBEAu), T);
+            const uint32_t l0 = h ? lo[j].z : lo[j].x, l1 = h ? lo[j].w : lo[j].y;
+            o[8 * j + 4 * h + 0] = prmt(l0, h0, 0x5140u);
+            o[8 * j + 4 * h + 1] = prmt(l0, h0, 0x7362u);
+            o[8 * j + 4 * h + 2] = prmt(l1, h1, 0x5140u);
+            o[8 * j + 4 * h + 3] = prmt(l1, h1, 0x7362u);
+        }
+    }
+    // patch escaped high bytes (rare; n is tile-uniform, so the loop is warp-uniform):
+    // weight k of row r is the (k & 1) half of column k / 2
+    for (uint32_t e = 0; e < n; ++e) {
+        const uint32_t ent = __shfl_sync(0xffffffffu, my_ent, e), i = ent & 0xffffu;
+        if (((i >> 4) & 127u) == r) {
+            const uint32_t k = (i >> 11) * 16u + (i & 15u), col = k >> 1, sh = (k & 1u) * 16u + 8u;
+            const uint32_t m = ~(0xffu << sh), hv = ((ent >> 16) & 0xffu) << sh;
+#pragma unroll
+            for (uint32_t q = 0; q < 32; ++q)
+                if (q == col) o[q] = (o[q] & m) | hv;
+        }
+    }
+}
+// raw fallback tile (16 KiB SWIZZLE_128B image): row r's logical 16-byte
+// chunk q sits at chunk position q ^ (r % 8) of its 128-byte line
+__device__ __forceinline__ void raw_row_ts(uint32_t sa, uint32_t r, uint32_t (&o)[32]) {
+    const uint32_t base = sa + (r >> 3) * 1024u + (r & 7u) * 128u;
+#pragma unroll
+    for (uint32_t q = 0; q < 8; ++q) {
+        const uint4 v = lds128(base + ((q ^ (r & 7u)) << 4));
+        o[4 * q] = v.x, o[4 * q + 1] = v.y, o[4 * q + 2] = v.z, o[4 * q + 3] = v.w;
+    }
+}
+// ---- codec 3 roles: three decoupled rings ---------------------------------
+// (1) encoded-A ring in smem (A3 slots of 12432 B, 16 KiB when the GEMM has
+//     raw fallback blocks): warp 0 streams every weight tile of the CTA's
+//     task list into it, gated only by its decoders having READ the slot;
+// (2) TMEM A slots (32 columns per tile): decoders -> MMA;
+// (3) token-tile (B) ring in smem: warp 14 streams one B tile per k-block,
+//     freed by the MMA's commit.
+// Weight tile t of the CTA (all tasks, k-blocks, matrices in order) uses A
+// slot t % A3 and TMEM slot t % T3, and is decoded by warps 6-9 (t even) or
+// 10-13 (t odd).  The HBM stream is thus bounded by the smem ring depth and
+// decoder speed, not by MMA completion as in a shared per-stage ring.
+struct Ring3 {
+    int a_slots, t_slots, b_slots, a_slot_bytes, b_bytes;
+    uint8_t* a_ring;
+    uint8_t* b_ring;
+};
+
+__device__ __forceinline__ void producer_a_ts(const GemmArgs& a, const Ring3& R, Smem* ctl, int n_virtual, int KB) {
+    const uint64_t pol_w = l2_evict_first();
+    int s = 0, t = 0;
+    uint32_t ph = 0;
+    for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
+        const VTask tk = vtask(a, v, KB);
+        const int rows = a.b_cnt ? a.b_cnt[tk.g] : a.rows_dense;
+        if (rows <= 0) continue;
+        const uint8_t* ab[kMaxMats];
+        int tile_b[kMaxMats];
+        for (int mt = 0; mt < a.n_mats; ++mt) {
+            bool raw;
+            ab[mt] = untag(a.a_table[(static_cast<int64_t>(mt) * a.G + tk.g) * a.RB + tk.rb], raw);
+            tile_b[mt] = raw ? kATileBytes : kCodecTile;
+        }
+        for (int n0 = tk.c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap)
+            for (int kb = tk.kb0; kb < tk.kb1; ++kb)
+                for (int mt = 0; mt < a.n_mats; ++mt, ++t) {
+                    mbar_wait(&ctl->empty[s], ph ^ 1);
+                    if (a.ktrace && blockIdx.x == 0 && t < 256) a.ktrace[t] = globaltimer();
+                    mbar_expect_tx(&ctl->full[s], tile_b[mt]);
+                    bulk_g2s(R.a_ring + s * R.a_slot_bytes, ab[mt] + static_cast<int64_t>(kb) * tile_b[mt],
+                             tile_b[mt], &ctl->full[s], pol_w);
+                    if (++s == R.a_slots) { s = 0; ph ^= 1; }
+                }
+    }
+}
+
+__device__ __forceinline__ void producer_b_ts(const GemmArgs& a, const Ring3& R, Smem* ctl, int n_virtual, int KB) {
+    const uint64_t pol_x = l2_evict_last();
+    int s = 0;
+    uint32_t ph = 0;
+    for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
+        const VTask tk = vtask(a, v, KB);
+        const int rows = a.b_cnt ? a.b_cnt[tk.g] : a.rows_dense;
+        if (rows <= 0) continue;
+        const int row0 = a.b_off ? a.b_off[tk.g] : 0;
+        for (int n0 = tk.c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
+            const int ntp = (min(a.n_cap, rows - n0) + 15) & ~15;
+            for (int kb = tk.kb0; kb < tk.kb1; ++kb) {
+                mbar_wait(&ctl->bempty[s], ph ^ 1);
+                mbar_expect_tx(&ctl->bfull[s], ntp * 128);
+                bulk_g2s(R.b_ring + s * R.b_bytes,
+                         a.b + static_cast<int64_t>(kb) * a.R * 128 + static_cast<int64_t>(row0 + n0) * 128, ntp * 128,
+                         &ctl->bfull[s], pol_x);
+                if (++s == R.b_slots) { s = 0; ph ^= 1; }
+            }
+        }
+    }
+}
+
+// Decoder warps 6-13: warp w decodes rows 32 (w % 4) .. +31 (its TMEM lane
+// quarter) of every tile t with t % 2 == (w - 6) / 4: smem -> registers ->
+// release the A slot (one arrival per warp) -> wait for the TMEM slot ->
+// tcgen05.st -> wait::st -> one arrival per warp on the slot's dfull.
+__device__ __forceinline__ void decoder_role_ts(const GemmArgs& a, const Ring3& R, Smem* ctl, int n_virtual, int KB,
+                                                uint32_t tmem) {
+    const int w = static_cast<int>(threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31u;
+    const int grp = (w - 6) >> 2;    // tile t is decoded by group t % kTsGroups
+    const uint32_t q = static_cast<uint32_t>(w) & 3u;  // TMEM lane quarter
+    const uint32_t r = q * 32u + lane;
+    const uint32_t tl = tmem + ((q * 32u) << 16) + static_cast<uint32_t>(a.acc_stages * a.n_mats * a.n_cap);
+    int t = 0, s = 0, ts = 0, tg = 0;  // tile counter, its A slot, TMEM slot and decoder group
+    uint32_t ph = 0, tph = 0;        // ring phases
+    for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
+        const VTask tk = vtask(a, v, KB);
+        const int rows = a.b_cnt ? a.b_cnt[tk.g] : a.rows_dense;
+        if (rows <= 0) continue;
+        bool raw0 = false, raw1 = false;
+        untag(a.a_table[static_cast<int64_t>(tk.g) * a.RB + tk.rb], raw0);
+        if (a.n_mats == 2) untag(a.a_table[(static_cast<int64_t>(a.G) + tk.g) * a.RB + tk.rb], raw1);
+        for (int n0 = tk.c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap)
+            for (int kb = tk.kb0; kb < tk.kb1; ++kb)
+                for (int mt = 0; mt < a.n_mats; ++mt) {
+                    if (tg == grp) {
+                        // CTA-0 trace (warp of lane quarter 0): rows 1-4 = landed, decoded, slot granted, stored
+                        unsigned long long* const kt =
+                            (a.ktrace && blockIdx.x == 0 && t < 256 && q == 0 && lane == 0) ? a.ktrace + t : nullptr;
+                        mbar_wait(&ctl->full[s], ph);
+                        if (kt) kt[256] = globaltimer();
+                        const uint32_t sa = smem_u32(R.a_ring + s * R.a_slot_bytes);
+                        uint32_t o[32];
+                        if (mt ? raw1 : raw0)
+                            raw_row_ts(sa, r, o);
+                        else
+                            decode_row_ts(sa, r, o);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&ctl->empty[s]);
+                        if (kt) kt[512] = globaltimer();
+                        mbar_wait(&ctl->aslot_empty[ts], tph ^ 1);
+                        if (kt) kt[768] = globaltimer();
+                        tc_fence_after();
+                        tmem_st32(tl + static_cast<uint32_t>(ts * 32), o);
+                        tmem_wait_st();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&ctl->dfull[ts]);
+                        if (kt) kt[1024] = globaltimer();
+                    }
+                    ++t;
+                    if (++tg == kTsGroups) tg = 0;
+                    if (++s == R.a_slots) { s = 0; ph ^= 1; }
+                    if (++ts == R.t_slots) { ts = 0; tph ^= 1; }
+                }
+    }
+}
+
+// MMA warp (lane 0 issues): per k-block wait its B tile, per matrix wait the
+// decoded TMEM A slot, 4 x (M128 N ntp K16) with A from TMEM, commit the A
+// slot; after the k-block commit the B slot; after the last k-block commit
+// the accumulator stage to the epilogue.
+__device__ __forceinline__ void mma_role_ts(const GemmArgs& a, const Ring3& R, Smem* ctl, int n_virtual, int KB,
+                                            uint32_t tmem) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const int acc_cols = a.n_mats * a.n_cap;
+    const uint32_t ta0 = tmem + static_cast<uint32_t>(a.acc_stages * acc_cols);
+    int ts = 0, sb = 0, acc = 0, t = 0;
+    uint32_t tph = 0, bph = 0, acc_phase = 0;
+    for (int v = blockIdx.x; v < n_virtual; v += gridDim.x) {
+        const VTask tk = vtask(a, v, KB);
+        const int rows = a.b_cnt ? a.b_cnt[tk.g] : a.rows_dense;
+        if (rows <= 0) continue;
+        for (int n0 = tk.c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap) {
+            const int ntp = (min(a.n_cap, rows - n0) + 15) & ~15;
+            const uint32_t idesc = idesc_bf16(128, ntp);
+            mbar_wait(&ctl->tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d0 = tmem + acc * acc_cols;
+            for (int kb = tk.kb0; kb < tk.kb1; ++kb) {
+                // the k-block's B tile and its n_mats decoded A tiles (TMEM slots ts, ts+1 mod t_slots)
+                mbar_wait(&ctl->bfull[sb], bph);
+                int ts1 = ts + 1;
+                uint32_t tph1 = tph;
+                if (ts1 == R.t_slots) { ts1 = 0; tph1 ^= 1; }
+                mbar_wait(&ctl->dfull[ts], tph);
+                if (a.ktrace && blockIdx.x == 0 && t < 256 && lane == 0) a.ktrace[1280 + t] = globaltimer();
+                if (a.n_mats == 2) mbar_wait(&ctl->dfull[ts1], tph1);
+                tc_fence_after();
+                if (elect_one()) {  // warp-uniform operands: no per-MMA register -> uniform moves
+                    const uint32_t bs = smem_u32(R.b_ring + sb * R.b_bytes);
+                    const uint32_t a0 = ta0 + ts * 32, a1 = ta0 + ts1 * 32;
+#pragma unroll
+                    for (int k = 0; k < kBlockK / 16; ++k) {
+                        const uint64_t bd = sdesc_sw128(bs + k * 32);
+                        const uint32_t accf = (kb != tk.kb0 || k != 0) ? 1u : 0u;
+                        umma_bf16_ts(d0, a0 + k * 8, bd, idesc, accf);
+                        if (a.n_mats == 2) umma_bf16_ts(d0 + a.n_cap, a1 + k * 8, bd, idesc, accf);
+                    }
+                    umma_commit(&ctl->aslot_empty[ts]);
+                    if (a.n_mats == 2) umma_commit(&ctl->aslot_empty[ts1]);
+                    umma_commit(&ctl->bempty[sb]);
+                    if (kb + 1 == tk.kb1) umma_commit(&ctl->tfull[acc]);
+                }
+                __syncwarp();
+                t += a.n_mats;
+                if (a.n_mats == 2) {
+                    ts = ts1 + 1, tph = tph1;
+                    if (ts == R.t_slots) { ts = 0; tph ^= 1; }
+                } else {
+                    ts = ts1, tph = tph1;
+                }
+                if (++sb == R.b_slots) { sb = 0; bph ^= 1; }
+            }
+            if (++acc == a.acc_stages) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+}
+
+template <bool kTs>
+__global__ void __launch_bounds__(kTs ? kThreadsCodec3 : kThreadsCodec, 1) gemm_tc_kernel(const GemmArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1 KiB alignment for the SWIZZLE_128B atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -278,7 +533,11 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
     // place; tile t of a stage (t = j * n_mats + mt) sits at t * 16 KiB
     const int stage_bytes = kps * (a_bytes + b_bytes);
     const int stages = a.stages;
-    Smem* ctl = reinterpret_cast<Smem*>(smem + stages * stage_bytes);
+    // codec 3: [A ring: stages x a3_slot_bytes][B ring: b3_slots x b_bytes][ctl]
+    // (the B ring's SWIZZLE_128B atoms need 1 KiB alignment)
+    Ring3 R3{stages, a.t3_slots, a.b3_slots, a.a3_slot_bytes, b_bytes, smem,
+             smem + ((stages * a.a3_slot_bytes + 1023) & ~1023)};
+    Smem* ctl = reinterpret_cast<Smem*>(kTs ? R3.b_ring + a.b3_slots * b_bytes : smem + stages * stage_bytes);
 
     const uint32_t warp = warp_idx_sync();
     const uint32_t lane = threadIdx.x & 31;
@@ -297,8 +556,19 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
             mbar_init(&ctl->tfull[s], 1);
             mbar_init(&ctl->tempty[s], 4);
         }
-        if (a.codec)
+        if (a.codec == 1)
             for (int s = 0; s < stages; ++s) mbar_init(&ctl->dfull[s], 1);
+        if (kTs) {  // A slots are read / written by the 4 warps of one decoder group
+            for (int s = 0; s < stages; ++s) mbar_init(&ctl->empty[s], 4);
+            for (int s = 0; s < a.t3_slots; ++s) {
+                mbar_init(&ctl->dfull[s], 4);
+                mbar_init(&ctl->aslot_empty[s], 1);
+            }
+            for (int s = 0; s < a.b3_slots; ++s) {
+                mbar_init(&ctl->bfull[s], 1);
+                mbar_init(&ctl->bempty[s], 1);
+            }
+        }
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc(&ctl->tmem_base, a.tmem_cols);
@@ -331,7 +601,18 @@ __global__ void __launch_bounds__(kThreadsCodec, 1) gemm_tc_kernel(const GemmArg
     const int n_virtual = a.sk_parts ? a.sk_full + a.sk_tail * a.sk_parts : a.G * a.RB * a.n_chunks * a.k_splits;
     const int KB = a.K / kBlockK;
 
-    if (warp == 0) {
+    if (kTs && (warp < 2 || warp >= 6)) {
+        // ===== codec 3: decoupled rings (the epilogue below is shared) =====
+        if (warp == 0) {
+            if (lane == 0) producer_a_ts(a, R3, ctl, n_virtual, KB);
+        } else if (warp == kTsBWarp) {
+            if (lane == 0) producer_b_ts(a, R3, ctl, n_virtual, KB);
+        } else if (warp == 1) {
+            mma_role_ts(a, R3, ctl, n_virtual, KB, tmem);
+        } else {
+            decoder_role_ts(a, R3, ctl, n_virtual, KB, tmem);
+        }
+    } else if (warp == 0) {
         // ===== producer =====
         if (elect_one()) {
             const uint64_t pol_w = l2_evict_first(), pol_x = l2_evict_last();
@@ -634,25 +915,47 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     // fixed decode cost (barriers, proxy fence, dfull round trip) covers two
     // encoded tiles, as it does for the two matrices of gate/up
     // (only while that still leaves >= 4 stages: mu = 256 down, n_cap 128, would get 2)
+    // codec 3 keeps A slots in TMEM next to the accumulators: at most 256
+    // accumulator columns (a wide prefill tile loops over more token chunks)
+    if (a.codec == 3 && a.n_mats * a.n_cap > 256) a.n_cap = 256 / a.n_mats;
     const int budget = 227 * 1024 - 1024 - kCtlBytes - kEpiScratch;
     a.kps = (a.codec && a.n_mats == 1 && budget / (2 * (kATileBytes + a.n_cap * 128)) >= 4) ? 2 : 1;
     const int per_stage = a.kps * (a.n_mats * kATileBytes + a.n_cap * 128);
     a.stages = budget / per_stage;
     if (a.stages > 8) a.stages = 8;
-    if (a.codec) {
+    if (a.codec == 1) {
         if (a.dec_groups < 1 || a.dec_groups > kMaxDecGroups) return cudaErrorInvalidValue;
         a.stages -= a.stages % a.dec_groups;  // decoder groups own whole stages
     }
-    if (a.codec != 0 && a.codec != 1) return cudaErrorInvalidValue;  // 2 dispatched above
-    if (a.stages < 2) return cudaErrorInvalidValue;
+    if (a.codec != 0 && a.codec != 1 && a.codec != 3) return cudaErrorInvalidValue;  // 2 dispatched above
     const int acc_cols = a.n_mats * a.n_cap;
     a.acc_stages = (2 * acc_cols <= 512) ? 2 : 1;
     int need = a.acc_stages * acc_cols;
+    if (a.codec == 3) {
+        // decoupled rings (Ring3): token tiles (3-4 slots), encoded A slots
+        // (12432 B, or 16 KiB when raw fallback blocks may appear) in the rest
+        // of smem, TMEM A slots (32 columns per tile) next to the accumulators
+        a.kps = 1;
+        a.b3_slots = a.n_cap * 128 <= 16384 ? 4 : 3;
+        a.a3_slot_bytes = a.codec_raw ? kATileBytes : kCodecTile;
+        a.stages = std::min(kMaxRing, (budget - 1024 - a.b3_slots * a.n_cap * 128) / a.a3_slot_bytes);
+        if ((512 - need) / 32 < 4 && a.acc_stages == 2) {
+            a.acc_stages = 1;
+            need = acc_cols;
+        }
+        a.t3_slots = std::min(kMaxRing, (512 - need) / 32);
+        if (a.t3_slots < 2) return cudaErrorInvalidValue;
+        need += a.t3_slots * 32;
+    }
+    if (a.stages < 2) return cudaErrorInvalidValue;
     int cols = 32;
     while (cols < need) cols <<= 1;
     a.tmem_cols = cols;
-    const int smem = gemm_smem_bytes(a.n_mats, a.n_cap, a.stages, a.kps);
-    if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel), 227 * 1024); e != cudaSuccess)
+    const int smem = a.codec == 3 ? ((a.stages * a.a3_slot_bytes + 1023) & ~1023) + a.b3_slots * a.n_cap * 128 +
+                                        1024 + kCtlBytes + kEpiScratch
+                                  : gemm_smem_bytes(a.n_mats, a.n_cap, a.stages, a.kps);
+    void (*const kern)(const GemmArgs) = a.codec == 3 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>;
+    if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), 227 * 1024); e != cudaSuccess)
         return e;
     a.sk_full = a.sk_tail = a.sk_parts = 0;
     if (a.sk_scratch && a.sk_count && a.sk_rows > 0 && a.epi == kEpiSiluPacked && a.n_mats == 2 &&
@@ -675,12 +978,14 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         // (cached per device and block size: the occupancy query costs host microseconds)
         static int cache[64][kMaxDecGroups + 2] = {};
         int dev = 0;
-        const int slot = a.codec ? a.dec_groups : 0;
+        const int slot = a.codec == 3 ? kMaxDecGroups + 1 : a.codec ? a.dec_groups : 0;
         int per_sm = 0;
         if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
             if (!cache[dev][slot] &&
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache[dev][slot], gemm_tc_kernel,
-                                                              a.codec ? kThreadsCodec : kThreadsRaw,
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache[dev][slot], kern,
+                                                              a.codec == 3 ? kThreadsCodec3
+                                                              : a.codec    ? kThreadsCodec
+                                                                           : kThreadsRaw,
                                                               227 * 1024 - 1024) != cudaSuccess)
                 cache[dev][slot] = 0;
             per_sm = cache[dev][slot];
@@ -690,17 +995,17 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     const int n_virtual = a.sk_parts ? a.sk_full + a.sk_tail * a.sk_parts : a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
-    const dim3 block(a.codec ? kThreadsCodec : kThreadsRaw);
+    const dim3 block(a.codec == 3 ? kThreadsCodec3 : a.codec ? kThreadsCodec : kThreadsRaw);
     if (a.sk_parts) {
         // cooperative: the driver guarantees co-residency of the whole grid or
         // refuses the launch (then: the same GEMM without the stream-K tail)
-        const cudaError_t e = launch_k_coop(gemm_tc_kernel, dim3(grid), block, smem, stream, a);
+        const cudaError_t e = launch_k_coop(kern, dim3(grid), block, smem, stream, a);
         if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported) return e;
         a.sk_full = a.sk_tail = a.sk_parts = 0;
         const int nv = a.G * a.RB * a.n_chunks * a.k_splits;
-        return launch_k(gemm_tc_kernel, dim3(nv < num_sms ? nv : num_sms), block, smem, stream, a);
+        return launch_k(kern, dim3(nv < num_sms ? nv : num_sms), block, smem, stream, a);
     }
-    return launch_k(gemm_tc_kernel, dim3(grid), block, smem, stream, a);
+    return launch_k(kern, dim3(grid), block, smem, stream, a);
 }
 
 }  // namespace mltk

@@ -33,7 +33,9 @@ struct GemmArgs {
     // optional per-CTA phase stamps [gridDim][8] (diagnostic, see mlt.h)
     unsigned long long* trace = nullptr;
     // 1: A row blocks are encoded tiles (runtime/weight_codec.hpp, 12432 B
-    // per 64-k tile); decoder warps expand them in shared memory
+    // per 64-k tile); decoder warps expand them in shared memory.
+    // 3: row-plane encoded tiles; decoder warps expand them into tensor
+    // memory, the MMA reads its A operand from TMEM (gemm_tc.cu)
     int codec = 0;
     int dec_groups = 2;  // codec 1: decoder groups of 4 warps, each owning every dec_groups-th stage
     // codec 2 (fragment-order tiles, gemm_codec.cu: decode in registers,
@@ -67,6 +69,8 @@ struct GemmArgs {
     // filled by launch_gemm
     int stages = 0, acc_stages = 0, tmem_cols = 0;
     int kps = 1;  // k-blocks per ring stage
+    // codec 3 rings (stages = encoded-A smem slots): TMEM A slots, token-tile slots, A slot bytes
+    int t3_slots = 0, b3_slots = 0, a3_slot_bytes = 0;
 };
 
 // Dispatches codec = 2 to launch_gemm_codec (gemm_codec.cu).

@@ -139,7 +139,7 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     codec_mode_ = 0;
     if (opt.weight_codec) {
         const char* m = std::getenv("MLT_CODEC_MODE");
-        codec_mode_ = (m && m[0] == '2' && Rmu_ <= 64) ? 2 : 1;
+        codec_mode_ = (m && m[0] == '2' && Rmu_ <= 64) ? 2 : (m && m[0] == '3') ? 3 : 1;
     }
     Re_ = round_up(mu_ * K_ + 16 * E_, 16);
     ncap_ = std::min(256, Rmu_);
@@ -402,7 +402,7 @@ void Runtime::generate_weights() {
         for (const auto& b : cat_.blocks) {
             uint8_t* dst = b.resident ? res.data() + b.offset
                                       : host_blob_ + static_cast<int64_t>(l) * layer_blob_bytes_ + b.offset;
-            if (!opt_.weight_codec || (b.raw && codec_mode_ == 1)) {  // packed bf16 tiles
+            if (!opt_.weight_codec || (b.raw && codec_mode_ != 2)) {  // packed bf16 tiles
                 packed_block(l, b, reinterpret_cast<uint16_t*>(dst));
             } else if (b.raw) {  // codec 2 raw fallback: fragment-order bf16 tiles
                 tmp_block.resize(static_cast<size_t>(128) * b.K);
@@ -424,7 +424,11 @@ void Runtime::generate_weights() {
                     const uint8_t* src = reinterpret_cast<const uint8_t*>(tmp_block.data()) +
                                          static_cast<size_t>(t) * mltk::kATileBytes;
                     uint8_t* out = dst + static_cast<size_t>(t) * kCodecTileBytes;
-                    bad += (codec_mode_ == 2 ? codec_encode_frag_tile(src, out) : codec_encode_tile(src, out)) ? 0 : 1;
+                    bad += (codec_mode_ == 2   ? codec_encode_frag_tile(src, out)
+                            : codec_mode_ == 3 ? codec_encode_rows_tile(src, out)
+                                               : codec_encode_tile(src, out))
+                               ? 0
+                               : 1;
                 }
                 if (bad)  // caller weights were scanned (scan_raw_blocks); synthetic ones always fit
                     throw std::invalid_argument("weight_codec: a weight tile does not fit the code");
@@ -632,13 +636,12 @@ void Runtime::dense_tiling(int row_blocks, int& n_cap, int& n_chunks, int& k_spl
 
 // Encoded-weight settings of a projection / expert GEMM (lm_head stays bf16):
 // codec 1 = tcgen05 with in-smem decode (gemm_tc.cu), codec 2 = register
-// decode + mma.sync (gemm_codec.cu: <= 64 tokens per chunk, <= 32 for gate/up).
+// decode + mma.sync (gemm_codec.cu: <= 64 tokens per chunk, <= 32 for gate/up),
+// codec 3 = tcgen05 with A decoded into TMEM (gemm_tc.cu, decoupled rings).
 void Runtime::codec_args(mltk::GemmArgs& a) const {
     a.codec = codec_mode_;
-    if (codec_mode_ == 2) {
-        a.n_cap = std::min(a.n_cap, a.n_mats == 2 ? 32 : 64);
-        a.codec_raw = any_raw_ ? 1 : 0;
-    }
+    if (codec_mode_ == 2) a.n_cap = std::min(a.n_cap, a.n_mats == 2 ? 32 : 64);
+    if (codec_mode_ >= 2) a.codec_raw = any_raw_ ? 1 : 0;  // raw fallback tiles need 16 KiB ring slots
 }
 
 // ---------------------------------------------------------------------------

@@ -86,4 +86,26 @@ bool codec_encode_frag_tile(const uint8_t* packed, uint8_t* out) {
     return codec_encode_tile(reinterpret_cast<const uint8_t*>(frag), out);
 }
 
+namespace {
+// packed (SWIZZLE_128B image) byte offset of row-plane weight i
+inline uint32_t rows_src(uint32_t i) {
+    const uint32_t t = i & 15u, r = (i >> 4) & 127u, j = i >> 11;
+    return mltk::swz_off(r, 16u * j + t);
+}
+}  // namespace
+
+void rows_from_packed(const uint8_t* packed, uint16_t* rows) {
+    for (uint32_t i = 0; i < 8192; ++i) std::memcpy(rows + i, packed + rows_src(i), 2);
+}
+
+void packed_from_rows(const uint16_t* rows, uint8_t* packed) {
+    for (uint32_t i = 0; i < 8192; ++i) std::memcpy(packed + rows_src(i), rows + i, 2);
+}
+
+bool codec_encode_rows_tile(const uint8_t* packed, uint8_t* out) {
+    uint16_t rows[8192];
+    rows_from_packed(packed, rows);
+    return codec_encode_tile(reinterpret_cast<const uint8_t*>(rows), out);
+}
+
 }  // namespace mlt

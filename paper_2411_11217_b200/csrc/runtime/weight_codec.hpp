@@ -45,4 +45,16 @@ void frag_from_packed(const uint8_t* packed16k, uint16_t* frag8192);
 void packed_from_frag(const uint16_t* frag8192, uint8_t* packed16k);
 bool codec_encode_frag_tile(const uint8_t* packed16k, uint8_t* out);
 
+// Row-plane order (kernels/gemm_tc.cu, GemmArgs::codec = 3: decoded rows go
+// to tensor memory, the MMA reads A from TMEM): weight (r, k) of the tile is
+// i = ((k / 16) * 128 + r) * 16 + k % 16, so the 16 low bytes (and 8 code
+// bytes) of one row's 16-k chunk are one 16-byte (8-byte) word and a warp's
+// 32 rows read 32 consecutive words (bank-conflict-free).  Decoder thread r
+// expands its row's 64 weights into the 32 TMEM columns of lane r (k pairs
+// per 32-bit column).  The codec fields are unchanged; escape indices refer to
+// this order.  A raw fallback block stays 16 KiB packed (SWIZZLE_128B) tiles.
+void rows_from_packed(const uint8_t* packed16k, uint16_t* rows8192);
+void packed_from_rows(const uint16_t* rows8192, uint8_t* packed16k);
+bool codec_encode_rows_tile(const uint8_t* packed16k, uint8_t* out);
+
 }  // namespace mlt

@@ -107,3 +107,38 @@ def test_product_synthetic_weights_encode(K):
     back = np.zeros_like(packed)
     K.codec_decode(enc.ctypes.data_as(C.c_void_p), tiles, back.ctypes.data_as(C.c_void_p))
     assert np.array_equal(back, packed)
+
+
+def np_swz_off(r, k):
+    """Byte offset of element (r, k) in a packed 16 KiB tile (SWIZZLE_128B image)."""
+    return (r >> 3) * 1024 + (r & 7) * 128 + ((((k & 63) >> 3) ^ (r & 7)) << 4) + (k & 7) * 2
+
+
+def test_row_plane_order_roundtrip(K):
+    """Codec-3 tiles (mlt_codec_encode_rows): the spec decoder yields the tile's
+    weights in row-plane order i = ((k // 16) * 128 + r) * 16 + k % 16; mapped
+    back through the swizzle they equal the packed tile, escapes included; a
+    block that cannot be coded is reported raw and copied as packed tiles."""
+    rng = np.random.default_rng(11)
+    M, Kd = 256, 256
+    w = bf16(rng.normal(0, Kd ** -0.5, (M, Kd)))
+    w[3, 17] = bf16(np.array([2.0 ** -40]))[0]          # an escape in block 0
+    w[128:] = bf16(rng.normal(0, 1, (128, Kd)) * np.exp(rng.normal(0, 4, (128, Kd))))  # block 1: raw
+    packed = pack(K, w, M, Kd)
+    out = np.zeros(M * Kd * 2, np.uint8)
+    raw = np.zeros(M // 128, np.uint8)
+    n_raw = K.codec_encode_rows(packed.ctypes.data_as(C.c_void_p), M, Kd, out.ctypes.data_as(C.c_void_p),
+                                raw.ctypes.data_as(C.c_void_p))
+    assert n_raw == 1 and list(raw) == [0, 1]
+    r_i, k_i = np.meshgrid(np.arange(128), np.arange(64), indexing="ij")
+    row_plane = ((k_i // 16) * 128 + r_i) * 16 + k_i % 16
+    src = np_swz_off(r_i, k_i)
+    kb = Kd // 64
+    for t in range(kb):
+        dec = np_decode(out[t * TILE:(t + 1) * TILE].tobytes())
+        vals = dec.view(np.uint16)[row_plane]
+        ref = packed[t * 16384:(t + 1) * 16384].view(np.uint16)[src // 2]
+        assert np.array_equal(vals, ref)
+    assert int(out[12304]) >= 1 or any(int(out[t * TILE + 12304]) for t in range(kb))
+    off = kb * TILE
+    assert np.array_equal(out[off:off + kb * 16384], packed[kb * 16384:2 * kb * 16384])

@@ -284,7 +284,7 @@ def test_executed_baseline_schedules_match_cgopipe(prompt):
                 vocab=VOCAB, seed=1234, schedule="s4")
 
 
-@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("mode", ["1", "2", "3"])
 @pytest.mark.parametrize("dims,r_w,a_g,budget", [(TINY, 0.3, 0, 4e9), (TINY, 1.0, 1, 4e9), (SK, 0.5, 0, 4e9),
                                                  (W8X7B, 0.10, 0, 7e9)])
 def test_weight_codec_decode_bitwise_equal(prompt, dims, r_w, a_g, budget, mode):

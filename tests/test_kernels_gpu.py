@@ -395,7 +395,12 @@ def test_kv_stage_layout(K):
 
 def encode_weight_dev(K, w_bf16, fmt=1):
     """Host-pack + codec-encode a [M, K] bf16 weight and upload; returns (device
-    buffer, encoded row-block pointers)."""
+    buffer, encoded row-block pointers).  fmt 3: the row-plane code of the
+    TMEM-operand engine (see encode_rows_dev)."""
+    if fmt == 3:
+        dev, blocks, flags = encode_rows_dev(K, w_bf16)
+        assert not any(flags)  # 12432-byte ring slots (codec_raw = 0)
+        return dev, blocks
     M, Kd = w_bf16.shape
     src = bf16_bits(w_bf16.cpu())
     packed = np.empty_like(src)
@@ -407,7 +412,35 @@ def encode_weight_dev(K, w_bf16, fmt=1):
     return dev, blocks
 
 
-@pytest.mark.parametrize("codec", [1])
+def encode_rows_dev(K, w_bf16, force_raw=()):
+    """Codec-3 weight blocks (row-plane encoded tiles, mlt_codec_encode_rows):
+    a row block the code cannot hold (> 31 escapes in a tile), or listed in
+    force_raw, is stored as raw packed tiles with its pointer tagged (bit 0).
+    Returns (device buffer, row-block pointers, raw flags)."""
+    M, Kd = w_bf16.shape
+    src = bf16_bits(w_bf16.cpu())
+    packed = np.empty_like(src)
+    K.pack_weight(src.ctypes.data_as(C.c_void_p), M, Kd, packed.ctypes.data_as(C.c_void_p))
+    kb, rbs = Kd // 64, M // 128
+    pb = packed.view(np.uint8).reshape(rbs, kb * 16384)
+    parts, rel, flags = [], [], []
+    off = 0
+    for r in range(rbs):
+        blk = np.empty(kb * 16384, np.uint8)
+        rr = np.zeros(1, np.uint8)
+        assert K.codec_encode_rows(np.ascontiguousarray(pb[r]).ctypes.data_as(C.c_void_p), 128, Kd,
+                                   blk.ctypes.data_as(C.c_void_p), rr.ctypes.data_as(C.c_void_p)) >= 0
+        raw = bool(rr[0]) or r in force_raw
+        blk = pb[r].copy() if raw else blk[:kb * 12432]
+        parts.append(blk)
+        rel.append((off, raw))
+        flags.append(raw)
+        off += blk.size
+    dev = torch.from_numpy(np.concatenate(parts)).cuda()
+    return dev, [dev.data_ptr() + o + (1 if raw else 0) for o, raw in rel], flags
+
+
+@pytest.mark.parametrize("codec", [1, 3])
 @pytest.mark.parametrize("T,M,Kd,n_cap,splits,resid", [(16, 256, 512, 16, 1, True), (64, 384, 4096, 64, 3, False),
                                                         (256, 256, 1024, 256, 2, False),
                                                         (200, 128, 256, 208, 1, True)])
@@ -438,7 +471,7 @@ def test_codec_gemm_bitwise_equals_raw(K, T, M, Kd, n_cap, splits, resid, codec)
     assert (outs[1].sum(0)[:T] - ref).abs().max().item() <= 2e-3 * max(1.0, ref.abs().max().item())
 
 
-@pytest.mark.parametrize("codec", [1])
+@pytest.mark.parametrize("codec", [1, 3])
 @pytest.mark.parametrize("T,H,Fd,E,Kk,n_cap", [(64, 512, 768, 8, 2, 64), (33, 256, 256, 16, 4, 32)])
 def test_codec_expert_ffn_bitwise_equals_raw(K, T, H, Fd, E, Kk, n_cap, codec):
     """Grouped gate/up (two encoded matrices, fused SiLU -> packed bf16) and
@@ -485,6 +518,40 @@ def test_codec_expert_ffn_bitwise_equals_raw(K, T, H, Fd, E, Kk, n_cap, codec):
     assert torch.equal(results[0][0], results[1][0])
     assert torch.equal(results[0][1], results[1][1])
 
+
+
+@pytest.mark.parametrize("T,M,Kd,n_cap,splits", [(16, 512, 1024, 16, 1), (80, 384, 2048, 96, 2)])
+def test_codec3_escapes_and_raw_blocks(K, T, M, Kd, n_cap, splits):
+    """Codec 3 (row-plane tiles decoded into TMEM, MMA with A from TMEM) on
+    heavy-tailed weights: tiles with escapes (patched per row in registers),
+    row blocks the code cannot hold stored raw (tagged pointers), plus a
+    forced raw block — bit-equal to the raw-tile GEMM."""
+    g = torch.Generator().manual_seed(M + Kd + 3)
+    w = rand_bf16(M, Kd, scale=Kd ** -0.5, gen=g)
+    # sparse outliers: a few per tile in rows 0..127 -> escapes; a wide
+    # spread in the last row block -> more than 31 escapes -> raw
+    nout = M * Kd // 2048
+    ri = torch.randint(0, M - 128, (nout,), generator=g)
+    ci = torch.randint(0, Kd, (nout,), generator=g)
+    w[ri, ci] = (torch.rand(nout, generator=g) * 64 + 1).to(torch.bfloat16)
+    w[M - 128:] = (torch.randn(128, Kd, generator=g) * torch.exp(torch.randn(128, Kd, generator=g) * 4)).to(torch.bfloat16)
+    x = rand_bf16(T, Kd, gen=g)
+    R = (T + 15) // 16 * 16
+    raw_dev, raw_blocks = pack_weight_dev(K, w)
+    enc_dev, enc_blocks, flags = encode_rows_dev(K, w, force_raw=(1,))
+    assert flags[-1] and flags[1] and not flags[0], flags
+    xp = pack_rows_dev(K, x, R)
+    outs = []
+    for cdc, blocks in ((0, raw_blocks), (3, enc_blocks)):
+        tab = table([blocks])
+        out = torch.zeros(splits, R, M, device="cuda")
+        a = capi.GemmArgs(a_table=tab.data_ptr(), n_mats=1, G=1, RB=M // 128, K=Kd, b=xp.data_ptr(), R=R,
+                          rows_dense=T, n_cap=n_cap, epi=0, alpha=1.0, out_f32=out.data_ptr(), ldo=M,
+                          k_splits=splits, split_stride=R * M, codec=cdc, codec_raw=int(cdc == 3))
+        K.gemm(C.byref(a), stream())
+        torch.cuda.synchronize()
+        outs.append(out.cpu())
+    assert torch.equal(outs[0], outs[1])
 
 
 def encode_frag_dev(K, w_bf16, raw_rows=()):

@@ -37,12 +37,15 @@ def main():
     ap.add_argument("--codec", action="store_true", help="encoded weight tiles (decoder warps in the GEMM)")
     ap.add_argument("--codec2", action="store_true",
                     help="fragment-order encoded tiles, register decode + mma.sync (gemm_codec.cu)")
+    ap.add_argument("--codec3", action="store_true",
+                    help="row-plane encoded tiles decoded into TMEM, MMA with A from TMEM (gemm_tc codec 3)")
+    ap.add_argument("--ncap-e", type=int, default=0, help="expert GEMM token tile (0: the runtime's min(128, Rmu))")
     ap.add_argument("--no-stream-k", action="store_true", help="gate/up without the stream-K tail")
     ap.add_argument("--dec-groups", type=int, default=0, help="codec decoder groups (0: default)")
     ap.add_argument("--down-splits", type=int, default=0,
                     help="K-splits of the down GEMM (0: the runtime's auto choice, 4 with --codec at 8x7B)")
     a = ap.parse_args()
-    if a.codec2:
+    if a.codec2 or a.codec3:
         a.codec = True
     mu = a.mu
     KD = capi.load_kernels()
@@ -69,7 +72,10 @@ def main():
             src = w.view(torch.int16).numpy().view(np.uint16)
             packed = np.empty_like(src)
             KD.pack_weight(src.ctypes.data_as(C.c_void_p), rows, k, packed.ctypes.data_as(C.c_void_p))
-            if a.codec2:
+            if a.codec3:
+                assert KD.codec_encode_rows(packed.ctypes.data_as(C.c_void_p), rows, k,
+                                            enc[i * per:(i + 1) * per].ctypes.data_as(C.c_void_p), None) == 0
+            elif a.codec2:
                 KD.codec_encode_frag(packed.ctypes.data_as(C.c_void_p), rows, k,
                                      enc[i * per:(i + 1) * per].ctypes.data_as(C.c_void_p), None)
             else:
@@ -103,14 +109,14 @@ def main():
     inter = torch.zeros(R * F, dtype=torch.int16, device="cuda")
     # runtime.cpp expert_down_splits auto (8 x 32 tiles over 148 SMs; 2 CTAs per SM with codec 2)
     ds = a.down_splits or (8 if a.codec2 else 4 if a.codec else 1)
-    cmode = 2 if a.codec2 else int(a.codec)
+    cmode = 2 if a.codec2 else 3 if a.codec3 else int(a.codec)
     y = torch.zeros(ds * R, H, device="cuda")
     xo = torch.zeros(mu, H, device="cuda")
     Rmu = (mu + 15) // 16 * 16
     xn = torch.zeros(Rmu * H, dtype=torch.int16, device="cuda")
     qkv = torch.zeros(Rmu, W, device="cuda")
     hbuf = torch.zeros(mu, H, device="cuda")
-    ncap = min(128, Rmu)  # runtime.cpp ncap_e_
+    ncap = a.ncap_e or min(128, Rmu)  # runtime.cpp ncap_e_
     ncap_gu, ncap_dn = (min(32, ncap), min(64, ncap)) if a.codec2 else (ncap, ncap)
 
     def router():
