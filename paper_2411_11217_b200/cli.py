@@ -48,12 +48,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0}  # B200_PROFILING.md fallback
 HOST_FLOPS = 2.0e12   # host-core estimate (the measured box: 16 SPR cores)
 CODEC_DT = 12432 / 8192  # stored bytes per weight with the weight codec
-# The codec GEMM moves its stored bytes at 64 % of the HBM peak (smem-bound
-# in-place decode; roofline.frac of profiles/r01_bench_mixtral8x7b-64g_codec.txt,
-# the bf16 GEMM: 97 %), i.e. the same time per weight as bf16 pages: the
-# search sees the codec's GPU term at that rate, or it would trade GPU time it
-# does not have for link bytes it saves.
-CODEC_GEMM_HBM_FRAC = 0.64
+# The codec GEMM moves its stored bytes at ~75-84 % of the HBM peak (codec 3,
+# decode into TMEM: expert FFN 83.8 % at mu = 64, 74.4 % at mu = 256,
+# profiles/r02s2_codec_engines.txt; the bf16 GEMM: ~97 %), i.e. about the time
+# per weight of bf16 pages or less: the search sees the codec's GPU term at the
+# lower of those rates, or it would trade GPU time it does not have for link
+# bytes it saves.
+CODEC_GEMM_HBM_FRAC = 0.74
 
 
 class CliError(Exception):

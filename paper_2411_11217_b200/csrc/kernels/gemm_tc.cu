@@ -341,9 +341,10 @@ __device__ __forceinline__ void raw_row_ts(uint32_t sa, uint32_t r, uint32_t (&o
 // (3) token-tile (B) ring in smem: warp 14 streams one B tile per k-block,
 //     freed by the MMA's commit.
 // Weight tile t of the CTA (all tasks, k-blocks, matrices in order) uses A
-// slot t % A3 and TMEM slot t % T3, and is decoded by warps 6-9 (t even) or
-// 10-13 (t odd).  The HBM stream is thus bounded by the smem ring depth and
-// decoder speed, not by MMA completion as in a shared per-stage ring.
+// slot t % A3 and TMEM slot t % T3, and is decoded by group t % kTsGroups
+// (warps 6 + 4g .. 9 + 4g; A3 and T3 are multiples of kTsGroups).  The HBM
+// stream is thus bounded by the smem ring depth and decoder speed, not by MMA
+// completion as in a shared per-stage ring.
 struct Ring3 {
     int a_slots, t_slots, b_slots, a_slot_bytes, b_bytes;
     uint8_t* a_ring;
@@ -944,7 +945,13 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
             need = acc_cols;
         }
         a.t3_slots = std::min(kMaxRing, (512 - need) / 32);
-        if (a.t3_slots < 2) return cudaErrorInvalidValue;
+        // tile t goes to decoder group t % kTsGroups, so both rings' slot counts
+        // are multiples of the group count: every slot then belongs to one group,
+        // which meets it phase after phase (a group skipping a phase of a slot it
+        // shares could pass a parity wait one phase early: mbarrier parity aliases)
+        a.stages -= a.stages % kTsGroups;
+        a.t3_slots -= a.t3_slots % kTsGroups;
+        if (a.t3_slots < kTsGroups || a.stages < kTsGroups) return cudaErrorInvalidValue;
         need += a.t3_slots * 32;
     }
     if (a.stages < 2) return cudaErrorInvalidValue;

@@ -131,15 +131,16 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     }
     max_ctx_ = opt.max_ctx;
     Rmu_ = round_up(mu_, 16);
-    // encoded weights: the tcgen05 GEMM with in-smem decoder warps (codec 1).
-    // The register-decode mma.sync GEMM (codec 2, fragment-order tiles) is
-    // selectable with MLT_CODEC_MODE=2 while a micro-batch fits its 64-token
-    // chunks; measured slower at mu = 64 (gate/up 437 vs 278 us, down 172 vs
-    // 172 us; profiles/r02_codec_engines.txt), so it is not the default.
+    // encoded weights: the tcgen05 GEMM with the A operand decoded into tensor
+    // memory (codec 3, row-plane tiles, three decoupled rings): expert FFN at
+    // mu = 64 391 us vs 451 us for the in-smem decoder (codec 1) and 450 us for
+    // raw bf16 (profiles/r02s2_codec_engines.txt).  MLT_CODEC_MODE=1 selects the
+    // in-smem decoder, MLT_CODEC_MODE=2 the register-decode mma.sync GEMM
+    // (fragment-order tiles, while a micro-batch fits its 64-token chunks).
     codec_mode_ = 0;
     if (opt.weight_codec) {
         const char* m = std::getenv("MLT_CODEC_MODE");
-        codec_mode_ = (m && m[0] == '2' && Rmu_ <= 64) ? 2 : (m && m[0] == '3') ? 3 : 1;
+        codec_mode_ = (m && m[0] == '2' && Rmu_ <= 64) ? 2 : (m && m[0] == '1') ? 1 : 3;
     }
     Re_ = round_up(mu_ * K_ + 16 * E_, 16);
     ncap_ = std::min(256, Rmu_);
@@ -608,6 +609,11 @@ cudaEvent_t Runtime::take_event() {
 void Runtime::kl(const char* name, cudaError_t e) {
     ck(e, name);
     ++launches_;
+    static const bool sync_each = [] {  // diagnostic knob: MLT_SYNC_EACH=1 names the kernel that faults
+        const char* v = std::getenv("MLT_SYNC_EACH");
+        return v && v[0] == '1';
+    }();
+    if (sync_each) ck(cudaStreamSynchronize(s_gpu_), name);
     if (pdl_) return;  // no per-kernel events inside a PDL chain
     cudaEvent_t ev = take_event();
     ck(cudaEventRecord(ev, s_gpu_), "event");
@@ -797,7 +803,11 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     gu.epi = mltk::kEpiSiluPacked;
     gu.out_packed = d_inter_;
     gu.out_R = Re_;
-    gu.sk_scratch = d_sk_scratch_;
+    static const bool no_sk = [] {  // diagnostic knob: MLT_NO_STREAM_K=1 runs gate/up without the tail
+        const char* e = std::getenv("MLT_NO_STREAM_K");
+        return e && e[0] == '1';
+    }();
+    gu.sk_scratch = no_sk ? nullptr : d_sk_scratch_;
     gu.sk_count = d_sk_count_;
     gu.sk_rows = Rmu_;  // a token routes to an expert at most once: rows per group <= mu
     gu.timing = ktimer("expert_gateup_gemm");
