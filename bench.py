@@ -133,9 +133,11 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# bytes per weight as stored with --codec (12432 B per 8192-weight tile,
-# runtime/weight_codec.hpp); the runtime itself always computes in bf16
-CODEC_DT = 12432 / 8192
+# bytes per weight as stored with --codec: the runtime's default 3-bit code
+# (codec 4, 11600 B per 8192-weight tile, runtime/weight_codec.hpp), or the
+# 4-bit code's 12432 B when MLT_CODEC_MODE selects engine 1-3; the runtime
+# itself always computes in bf16
+CODEC_DT = (12432 if os.environ.get("MLT_CODEC_MODE", "4")[:1] in ("1", "2", "3") else 11600) / 8192
 def arena_extra(cfg):
     """Arena bytes outside ModelSpec: embedding + lm_head (vocab x h1 bf16 each),
     activations, page tables and other KV-independent buffers (0.2 GB); the runtime

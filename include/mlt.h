@@ -322,6 +322,16 @@ int mlt_codec_encode_frag(const uint8_t* host_packed, int64_t M, int64_t K, uint
  * mlt_codec_encode_frag; raw fallback blocks are plain 16 KiB packed tiles. */
 int mlt_codec_encode_rows(const uint8_t* host_packed, int64_t M, int64_t K, uint8_t* host_out,
                           uint8_t* raw_blocks);
+/* The 3-bit row-plane code (GemmArgs codec = 4; runtime/weight_codec.hpp
+ * codec4_encode_rows_tile): 11 stored bits per weight, mlt_codec4_tile_bytes()
+ * = 11600 B per 64-k tile (8-entry high-byte table with a per-tile exponent
+ * phase, a per-row override of table slot 7, <= 48 escapes); same contract as
+ * mlt_codec_encode_rows.  mlt_codec4_decode_rows is the host reference
+ * decoder (encoded tiles -> 16 KiB packed tiles). */
+int mlt_codec4_encode_rows(const uint8_t* host_packed, int64_t M, int64_t K, uint8_t* host_out,
+                           uint8_t* raw_blocks);
+int mlt_codec4_decode_rows(const uint8_t* host_enc, int64_t tiles, uint8_t* host_packed);
+int mlt_codec4_tile_bytes(void);
 /* 16 KiB packed tiles -> fragment-order bf16 tiles (raw codec-2 blocks). */
 int mlt_frag_pack(const uint8_t* host_packed, int64_t tiles, uint8_t* host_out);
 /* Host-core GQA decode attention (A_g = 0: the CpuAttn task, pipesim.hpp:26,
@@ -375,7 +385,9 @@ typedef struct mlt_gemm_args_t {
                                   for n_mats = 2; kernels/gemm_codec.cu);
                                   3: row-plane encoded blocks (mlt_codec_encode_rows), each decoder
                                   thread expands one weight row into tensor memory and the
-                                  tcgen05.mma reads A from TMEM (raw fallback blocks: tag bit 0) */
+                                  tcgen05.mma reads A from TMEM (raw fallback blocks: tag bit 0);
+                                  4: the same engine on 3-bit row-plane blocks
+                                  (mlt_codec4_encode_rows, 11600 B per tile) */
     unsigned long long* ktrace; /* optional CTA-0 pipeline trace [4][256] %globaltimer stamps per
                                    k-block: producer issue, decoder start, decoder done, MMA start;
                                    codec 3: [6][256] per weight tile: producer issue, landed,

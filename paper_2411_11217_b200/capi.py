@@ -575,6 +575,9 @@ _KSIGS = {
     "codec_decode": [V, C.c_int64, V],
     "codec_encode_frag": [V, C.c_int64, C.c_int64, V, V],
     "codec_encode_rows": [V, C.c_int64, C.c_int64, V, V],
+    "codec4_encode_rows": [V, C.c_int64, C.c_int64, V, V],
+    "codec4_decode_rows": [V, C.c_int64, V],
+    "codec4_tile_bytes": [],
     "frag_pack": [V, C.c_int64, V],
     "host_gqa_decode": [V, V, V, V, I, I, I, I, I, V, I],
     "host_gqa_use_amx": [I],

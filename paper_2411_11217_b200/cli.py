@@ -47,7 +47,9 @@ from . import capi
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0}  # B200_PROFILING.md fallback
 HOST_FLOPS = 2.0e12   # host-core estimate (the measured box: 16 SPR cores)
-CODEC_DT = 12432 / 8192  # stored bytes per weight with the weight codec
+# stored bytes per weight with the weight codec (the runtime's default 3-bit
+# code, 11600 B per tile; 12432 B when MLT_CODEC_MODE selects engine 1-3)
+CODEC_DT = (12432 if os.environ.get("MLT_CODEC_MODE", "4")[:1] in ("1", "2", "3") else 11600) / 8192
 # The codec GEMM moves its stored bytes at ~75-84 % of the HBM peak (codec 3,
 # decode into TMEM: expert FFN 83.8 % at mu = 64, 74.4 % at mu = 256,
 # profiles/r02s2_codec_engines.txt; the bf16 GEMM: ~97 %), i.e. about the time

@@ -127,7 +127,8 @@ int mlt_codec_tile_bytes(void) { return mlt::kCodecTileBytes; }
 // a block is an error.  Returns the number of raw blocks.
 static int encode_blocks(const char* what, const uint8_t* packed, int64_t M, int64_t K, uint8_t* out,
                          uint8_t* raw_blocks, bool (*enc)(const uint8_t*, uint8_t*),
-                         void (*raw_tile)(const uint8_t*, uint8_t*)) {
+                         void (*raw_tile)(const uint8_t*, uint8_t*), int tile_bytes = mlt::kCodecTileBytes,
+                         int max_escapes = mlt::kCodecMaxEscapes) {
     if (M % 128 || K % 64 || M <= 0 || K <= 0) throw std::invalid_argument(std::string(what) + ": M%128, K%64");
     const int64_t kb = K / 64, rbs = M / 128;
     std::vector<int64_t> off(rbs + 1, 0);
@@ -135,7 +136,7 @@ static int encode_blocks(const char* what, const uint8_t* packed, int64_t M, int
     int bad = 0;
 #pragma omp parallel for schedule(static) reduction(+ : bad)
     for (int64_t r = 0; r < rbs; ++r) {
-        uint8_t tmp[mlt::kCodecTileBytes];
+        uint8_t tmp[mlt::kCodecTileBytes > mlt::kCodec4TileBytes ? mlt::kCodecTileBytes : mlt::kCodec4TileBytes];
         for (int64_t t = 0; t < kb; ++t)
             if (!enc(packed + (r * kb + t) * 16384, tmp)) {
                 raw[r] = 1;
@@ -145,8 +146,8 @@ static int encode_blocks(const char* what, const uint8_t* packed, int64_t M, int
     }
     if (bad && !raw_blocks)
         throw std::invalid_argument(std::string(what) + ": " + std::to_string(bad) + " row block(s) need > " +
-                                    std::to_string(mlt::kCodecMaxEscapes) + " escapes in a tile");
-    for (int64_t r = 0; r < rbs; ++r) off[r + 1] = off[r] + kb * (raw[r] ? 16384 : mlt::kCodecTileBytes);
+                                    std::to_string(max_escapes) + " escapes in a tile");
+    for (int64_t r = 0; r < rbs; ++r) off[r + 1] = off[r] + kb * (raw[r] ? 16384 : tile_bytes);
 #pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < rbs; ++r)
         for (int64_t t = 0; t < kb; ++t) {
@@ -154,7 +155,7 @@ static int encode_blocks(const char* what, const uint8_t* packed, int64_t M, int
             if (raw[r])
                 raw_tile(src, out + off[r] + t * 16384);
             else
-                enc(src, out + off[r] + t * mlt::kCodecTileBytes);
+                enc(src, out + off[r] + t * tile_bytes);
         }
     if (raw_blocks) std::memcpy(raw_blocks, raw.data(), static_cast<size_t>(rbs));
     return bad;
@@ -175,6 +176,24 @@ int mlt_codec_encode_rows(const uint8_t* packed, int64_t M, int64_t K, uint8_t* 
                              [](const uint8_t* src, uint8_t* dst) { std::memcpy(dst, src, 16384); });
     });
 }
+
+int mlt_codec4_encode_rows(const uint8_t* packed, int64_t M, int64_t K, uint8_t* out, uint8_t* raw_blocks) {
+    return guard([&] {
+        return encode_blocks("codec4_encode_rows", packed, M, K, out, raw_blocks, mlt::codec4_encode_rows_tile,
+                             [](const uint8_t* src, uint8_t* dst) { std::memcpy(dst, src, 16384); },
+                             mlt::kCodec4TileBytes, mlt::kCodec4MaxEscapes);
+    });
+}
+
+int mlt_codec4_decode_rows(const uint8_t* enc, int64_t tiles, uint8_t* packed) {
+    return guard([&] {
+        for (int64_t t = 0; t < tiles; ++t)
+            mlt::codec4_decode_rows_tile(enc + t * mlt::kCodec4TileBytes, packed + t * 16384);
+        return MLT_OK;
+    });
+}
+
+int mlt_codec4_tile_bytes(void) { return mlt::kCodec4TileBytes; }
 
 int mlt_frag_pack(const uint8_t* packed, int64_t tiles, uint8_t* out) {
     return guard([&] {

@@ -49,6 +49,8 @@ constexpr int kTsGroups = 3;
 constexpr int kTsBWarp = 6 + 4 * kTsGroups;
 constexpr int kThreadsCodec3 = 32 * (kTsBWarp + 1);
 constexpr int kCodecTile = 12432;   // encoded tile bytes (runtime/weight_codec.hpp)
+constexpr int kCodec4Tile = 11600;  // codec 4: 3-bit code (kCodec4TileBytes)
+__host__ __device__ constexpr int enc_tile_bytes(int codec) { return codec == 4 ? kCodec4Tile : kCodecTile; }
 // codec: an encoded tile lands at the END of its 16 KiB A slot and is
 // expanded in place (every input is in registers before any output store)
 constexpr int kCodecOff = kATileBytes - kCodecTile;  // 3952, 16-byte aligned
@@ -323,6 +325,88 @@ __device__ __forceinline__ void decode_row_ts(uint32_t c, uint32_t r, uint32_t (
         }
     }
 }
+// ---- codec 4: 3-bit codes (runtime/weight_codec.hpp codec4_encode_rows_tile) ----
+// Same row ownership and TMEM layout as decode_row_ts.  Per 32 weights of a
+// row: words A, B, C hold 24 codes in nibbles (bits 0-2; selector = word &
+// 0x7777) and, in their nibble bit 3, the 3 bits of the last 8 codes,
+// gathered into a fourth selector word by 3 shifts and 3 masked ORs.  One
+// PRMT looks up 4 high bytes in the 8-entry table (slot 7 = this row's
+// override byte), two PRMTs interleave them with the raw low bytes, and with
+// phase 1 one subtraction per 2 weights undoes the tile's exponent shift:
+// ~1.25 (phase 0) / 1.75 (phase 1) instructions per weight.  The escapes of
+// the warp's row quarter are then patched by their owning lanes.
+__device__ __forceinline__ void patch_col(uint32_t (&o)[32], uint32_t col, uint32_t v, uint32_t sel) {
+    switch (col) {
+#define MLT_PATCH(q) case q: o[q] = prmt(o[q], v, sel); break;
+        MLT_PATCH(0) MLT_PATCH(1) MLT_PATCH(2) MLT_PATCH(3) MLT_PATCH(4) MLT_PATCH(5) MLT_PATCH(6) MLT_PATCH(7)
+        MLT_PATCH(8) MLT_PATCH(9) MLT_PATCH(10) MLT_PATCH(11) MLT_PATCH(12) MLT_PATCH(13) MLT_PATCH(14)
+        MLT_PATCH(15) MLT_PATCH(16) MLT_PATCH(17) MLT_PATCH(18) MLT_PATCH(19) MLT_PATCH(20) MLT_PATCH(21)
+        MLT_PATCH(22) MLT_PATCH(23) MLT_PATCH(24) MLT_PATCH(25) MLT_PATCH(26) MLT_PATCH(27) MLT_PATCH(28)
+        MLT_PATCH(29) MLT_PATCH(30) MLT_PATCH(31)
+#undef MLT_PATCH
+        default: break;
+    }
+}
+
+template <bool kPhase>
+__device__ __forceinline__ void expand_row_c4(const uint4 (&lo)[4], const uint32_t (&cw)[6], uint32_t t0,
+                                              uint32_t t1, uint32_t (&o)[32]) {
+#pragma unroll
+    for (int H = 0; H < 2; ++H) {
+        const uint32_t A = cw[3 * H], B = cw[3 * H + 1], C = cw[3 * H + 2];
+        const uint32_t S = ((A >> 3) & 0x11111111u) | ((B >> 2) & 0x22222222u) | ((C >> 1) & 0x44444444u);
+        const uint32_t sel[8] = {A & 0x7777u, (A >> 16) & 0x7777u, B & 0x7777u, (B >> 16) & 0x7777u,
+                                 C & 0x7777u, (C >> 16) & 0x7777u, S, S >> 16};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // weights k = 32H + 4u .. +3
+            const uint32_t h4 = prmt(t0, t1, sel[u]);
+            const uint4& l = lo[2 * H + (u >> 2)];
+            const uint32_t lw = (u & 3) == 0 ? l.x : (u & 3) == 1 ? l.y : (u & 3) == 2 ? l.z : l.w;
+            uint32_t a = prmt(lw, h4, 0x5140u), b = prmt(lw, h4, 0x7362u);
+            if (kPhase) a -= 0x00800080u, b -= 0x00800080u;
+            o[16 * H + 2 * u] = a;
+            o[16 * H + 2 * u + 1] = b;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void decode_row_c4(uint32_t c, uint32_t r, uint32_t (&o)[32]) {
+    const uint2 T = lds64(c + 11392);
+    const uint32_t hdr = lds32(c + 11400), n = lds32(c + 11404) & 0xffu;
+    const uint32_t rb = lds8(c + 11264 + r);
+    uint4 lo[4];
+    uint32_t cw[6];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) lo[j] = lds128(c + (j * 128u + r) * 16u);
+#pragma unroll
+    for (int m = 0; m < 6; ++m) cw[m] = lds32(c + 8192u + (m * 128u + r) * 4u);
+    const uint32_t t1 = prmt(T.y, rb, 0x4210u);  // slot 7 <- this row's byte
+    if (hdr & 0xffu)
+        expand_row_c4<true>(lo, cw, T.x, t1, o);
+    else
+        expand_row_c4<false>(lo, cw, T.x, t1, o);
+    // escapes of this warp's quarter q = r / 32 (warp-uniform count)
+    const uint32_t lane = threadIdx.x & 31u, q = r >> 5;
+    const uint32_t b0 = q ? (hdr >> (8 * q)) & 0xffu : 0u, b1 = q < 3 ? (hdr >> (8 * (q + 1))) & 0xffu : n;
+    for (uint32_t base = b0; base < b1; base += 32) {
+        const uint32_t cnt = min(32u, b1 - base);
+        const uint32_t my = lane < cnt ? lds32(c + 11408u + 4u * (base + lane)) : 0u;
+        for (uint32_t e = 0; e < cnt; ++e) {
+            const uint32_t ent = __shfl_sync(0xffffffffu, my, e), i = ent & 0xffffu;
+            if (((i >> 4) & 127u) == r) {
+                const uint32_t k = (i >> 11) * 16u + (i & 15u);
+                patch_col(o, k >> 1, ent >> 16, (k & 1u) ? 0x5410u : 0x3254u);
+            }
+        }
+    }
+}
+
 // raw fallback tile (16 KiB SWIZZLE_128B image): row r's logical 16-byte
 // chunk q sits at chunk position q ^ (r % 8) of its 128-byte line
 __device__ __forceinline__ void raw_row_ts(uint32_t sa, uint32_t r, uint32_t (&o)[32]) {
@@ -364,7 +448,7 @@ __device__ __forceinline__ void producer_a_ts(const GemmArgs& a, const Ring3& R,
         for (int mt = 0; mt < a.n_mats; ++mt) {
             bool raw;
             ab[mt] = untag(a.a_table[(static_cast<int64_t>(mt) * a.G + tk.g) * a.RB + tk.rb], raw);
-            tile_b[mt] = raw ? kATileBytes : kCodecTile;
+            tile_b[mt] = raw ? kATileBytes : enc_tile_bytes(a.codec);
         }
         for (int n0 = tk.c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap)
             for (int kb = tk.kb0; kb < tk.kb1; ++kb)
@@ -436,6 +520,8 @@ __device__ __forceinline__ void decoder_role_ts(const GemmArgs& a, const Ring3& 
                         uint32_t o[32];
                         if (mt ? raw1 : raw0)
                             raw_row_ts(sa, r, o);
+                        else if (a.codec == 4)
+                            decode_row_c4(sa, r, o);
                         else
                             decode_row_ts(sa, r, o);
                         __syncwarp();
@@ -584,7 +670,7 @@ __global__ void __launch_bounds__(kTs ? kThreadsCodec3 : kThreadsCodec, 1) gemm_
         for (int mt = 0; mt < a.n_mats; ++mt) {
             bool raw;
             const uint8_t* p = untag(a.a_table[(static_cast<int64_t>(mt) * a.G + g) * a.RB + rb], raw);
-            const int tile = (a.codec && !raw) ? kCodecTile : kATileBytes;
+            const int tile = (a.codec && !raw) ? enc_tile_bytes(a.codec) : kATileBytes;
             prefetch_l2(p + static_cast<int64_t>(kb0) * tile, static_cast<uint32_t>(nkb * tile));
         }
     }
@@ -918,7 +1004,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     // (only while that still leaves >= 4 stages: mu = 256 down, n_cap 128, would get 2)
     // codec 3 keeps A slots in TMEM next to the accumulators: at most 256
     // accumulator columns (a wide prefill tile loops over more token chunks)
-    if (a.codec == 3 && a.n_mats * a.n_cap > 256) a.n_cap = 256 / a.n_mats;
+    if (a.codec >= 3 && a.n_mats * a.n_cap > 256) a.n_cap = 256 / a.n_mats;
     const int budget = 227 * 1024 - 1024 - kCtlBytes - kEpiScratch;
     a.kps = (a.codec && a.n_mats == 1 && budget / (2 * (kATileBytes + a.n_cap * 128)) >= 4) ? 2 : 1;
     const int per_stage = a.kps * (a.n_mats * kATileBytes + a.n_cap * 128);
@@ -928,17 +1014,17 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         if (a.dec_groups < 1 || a.dec_groups > kMaxDecGroups) return cudaErrorInvalidValue;
         a.stages -= a.stages % a.dec_groups;  // decoder groups own whole stages
     }
-    if (a.codec != 0 && a.codec != 1 && a.codec != 3) return cudaErrorInvalidValue;  // 2 dispatched above
+    if (a.codec < 0 || a.codec > 4) return cudaErrorInvalidValue;  // 2 dispatched above
     const int acc_cols = a.n_mats * a.n_cap;
     a.acc_stages = (2 * acc_cols <= 512) ? 2 : 1;
     int need = a.acc_stages * acc_cols;
-    if (a.codec == 3) {
+    if (a.codec >= 3) {
         // decoupled rings (Ring3): token tiles (3-4 slots), encoded A slots
         // (12432 B, or 16 KiB when raw fallback blocks may appear) in the rest
         // of smem, TMEM A slots (32 columns per tile) next to the accumulators
         a.kps = 1;
         a.b3_slots = a.n_cap * 128 <= 16384 ? 4 : 3;
-        a.a3_slot_bytes = a.codec_raw ? kATileBytes : kCodecTile;
+        a.a3_slot_bytes = a.codec_raw ? kATileBytes : enc_tile_bytes(a.codec);
         a.stages = std::min(kMaxRing, (budget - 1024 - a.b3_slots * a.n_cap * 128) / a.a3_slot_bytes);
         if ((512 - need) / 32 < 4 && a.acc_stages == 2) {
             a.acc_stages = 1;
@@ -958,10 +1044,10 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     int cols = 32;
     while (cols < need) cols <<= 1;
     a.tmem_cols = cols;
-    const int smem = a.codec == 3 ? ((a.stages * a.a3_slot_bytes + 1023) & ~1023) + a.b3_slots * a.n_cap * 128 +
+    const int smem = a.codec >= 3 ? ((a.stages * a.a3_slot_bytes + 1023) & ~1023) + a.b3_slots * a.n_cap * 128 +
                                         1024 + kCtlBytes + kEpiScratch
                                   : gemm_smem_bytes(a.n_mats, a.n_cap, a.stages, a.kps);
-    void (*const kern)(const GemmArgs) = a.codec == 3 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>;
+    void (*const kern)(const GemmArgs) = a.codec >= 3 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>;
     if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), 227 * 1024); e != cudaSuccess)
         return e;
     a.sk_full = a.sk_tail = a.sk_parts = 0;
@@ -985,12 +1071,12 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         // (cached per device and block size: the occupancy query costs host microseconds)
         static int cache[64][kMaxDecGroups + 2] = {};
         int dev = 0;
-        const int slot = a.codec == 3 ? kMaxDecGroups + 1 : a.codec ? a.dec_groups : 0;
+        const int slot = a.codec >= 3 ? kMaxDecGroups + 1 : a.codec ? a.dec_groups : 0;
         int per_sm = 0;
         if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
             if (!cache[dev][slot] &&
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache[dev][slot], kern,
-                                                              a.codec == 3 ? kThreadsCodec3
+                                                              a.codec >= 3 ? kThreadsCodec3
                                                               : a.codec    ? kThreadsCodec
                                                                            : kThreadsRaw,
                                                               227 * 1024 - 1024) != cudaSuccess)
@@ -1002,7 +1088,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     const int n_virtual = a.sk_parts ? a.sk_full + a.sk_tail * a.sk_parts : a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
-    const dim3 block(a.codec == 3 ? kThreadsCodec3 : a.codec ? kThreadsCodec : kThreadsRaw);
+    const dim3 block(a.codec >= 3 ? kThreadsCodec3 : a.codec ? kThreadsCodec : kThreadsRaw);
     if (a.sk_parts) {
         // cooperative: the driver guarantees co-residency of the whole grid or
         // refuses the launch (then: the same GEMM without the stream-K tail)

@@ -10,6 +10,7 @@
 
 #include "lightplan/config.hpp"
 #include "lightplan/pipesim.hpp"
+#include "weight_codec.hpp"
 
 namespace mlt {
 
@@ -66,7 +67,7 @@ ShardMap shard_map(const lightplan::ModelSpec& model, const Shard& shard, int ki
 // 16 KiB tiles in every layer — the fallback for weights the code cannot hold.
 Catalog build_catalog(const lightplan::ModelSpec& model, const lightplan::Policy& policy,
                       const Shard& shard = Shard{}, bool codec = false,
-                      const std::vector<uint8_t>* raw_mask = nullptr);
+                      const std::vector<uint8_t>* raw_mask = nullptr, int codec_tile_bytes = kCodecTileBytes);
 
 // Byte range [begin, end) of page p (1..M) of a layer blob; p = 0: whole.
 std::pair<int64_t, int64_t> page_range(int64_t blob_bytes, int M, int page);

@@ -137,10 +137,14 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     // raw bf16 (profiles/r02s2_codec_engines.txt).  MLT_CODEC_MODE=1 selects the
     // in-smem decoder, MLT_CODEC_MODE=2 the register-decode mma.sync GEMM
     // (fragment-order tiles, while a micro-batch fits its 64-token chunks).
+    // Codec 4 (the default) is the same engine on the 3-bit code: 11600 B per
+    // tile instead of 12432 (weight_codec.hpp); MLT_CODEC_MODE=3 keeps the
+    // 4-bit code.  Weights whose tiles overflow the 3-bit code's escapes in
+    // more than 5 % of the 128-row blocks fall back to codec 3 (scan_raw_blocks).
     codec_mode_ = 0;
     if (opt.weight_codec) {
         const char* m = std::getenv("MLT_CODEC_MODE");
-        codec_mode_ = (m && m[0] == '2' && Rmu_ <= 64) ? 2 : (m && m[0] == '1') ? 1 : 3;
+        codec_mode_ = (m && m[0] == '2' && Rmu_ <= 64) ? 2 : (m && m[0] == '1') ? 1 : (m && m[0] == '3') ? 3 : 4;
     }
     Re_ = round_up(mu_ * K_ + 16 * E_, 16);
     ncap_ = std::min(256, Rmu_);
@@ -165,9 +169,20 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
             throw std::invalid_argument("collective must be 0 (NCCL) or 1 (host-staged)");
     }
     arena_ = std::make_unique<Arena>(static_cast<size_t>(opt.budget_bytes));
-    if (opt.weight_codec && opt.weight_fn) {
+    // every block of every layer is test-encoded once when some tile may not
+    // fit: caller weights (any code), and the 3-bit code even for the
+    // synthetic weights (~14 of its 48 escapes per tile on average)
+    if (opt.weight_codec && (opt.weight_fn || codec_mode_ == 4)) {
         const char* f = std::getenv("MLT_CODEC_FORCE_RAW");
-        if (!(f && f[0] == '1')) scan_raw_blocks();
+        if (!(f && f[0] == '1')) {
+            scan_raw_blocks();
+            int raw = 0;
+            for (uint8_t b : raw_mask_) raw += b;
+            if (codec_mode_ == 4 && raw * 20 > static_cast<int>(raw_mask_.size())) {
+                codec_mode_ = 3;
+                scan_raw_blocks();
+            }
+        }
     }
     build_catalog();
     allocate();
@@ -212,7 +227,8 @@ void Runtime::build_catalog() {
         if (f && f[0] == '1')
             raw_mask_.assign(mlt::build_catalog(model_, policy_, shard_, true).blocks.size(), 1);
     }
-    cat_ = mlt::build_catalog(model_, policy_, shard_, opt_.weight_codec, raw_mask_.empty() ? nullptr : &raw_mask_);
+    cat_ = mlt::build_catalog(model_, policy_, shard_, opt_.weight_codec, raw_mask_.empty() ? nullptr : &raw_mask_,
+                              codec_tile_bytes(codec_mode_));
     any_raw_ = false;
     for (const auto& b : cat_.blocks) any_raw_ = any_raw_ || b.raw;
     layer_res_bytes_ = cat_.resident_bytes;
@@ -373,14 +389,13 @@ void Runtime::scan_raw_blocks() {
             packed_block(l, b, tmp.data());
             const int tiles = static_cast<int>(b.K / 64);
             int bad = 0;
+            const bool c4 = codec_mode_ == 4;
 #pragma omp parallel for schedule(static) reduction(+ : bad)
             for (int t = 0; t < tiles; ++t) {
                 uint8_t out[kCodecTileBytes];
-                bad += codec_encode_tile(reinterpret_cast<const uint8_t*>(tmp.data()) +
-                                             static_cast<size_t>(t) * mltk::kATileBytes,
-                                         out)
-                           ? 0
-                           : 1;
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(tmp.data()) +
+                                     static_cast<size_t>(t) * mltk::kATileBytes;
+                bad += (c4 ? codec4_encode_rows_tile(src, out) : codec_encode_tile(src, out)) ? 0 : 1;
             }
             if (bad) raw_mask_[i] = 1;
         }
@@ -424,14 +439,15 @@ void Runtime::generate_weights() {
                     {
                     const uint8_t* src = reinterpret_cast<const uint8_t*>(tmp_block.data()) +
                                          static_cast<size_t>(t) * mltk::kATileBytes;
-                    uint8_t* out = dst + static_cast<size_t>(t) * kCodecTileBytes;
+                    uint8_t* out = dst + static_cast<size_t>(t) * codec_tile_bytes(codec_mode_);
                     bad += (codec_mode_ == 2   ? codec_encode_frag_tile(src, out)
                             : codec_mode_ == 3 ? codec_encode_rows_tile(src, out)
+                            : codec_mode_ == 4 ? codec4_encode_rows_tile(src, out)
                                                : codec_encode_tile(src, out))
                                ? 0
                                : 1;
                 }
-                if (bad)  // caller weights were scanned (scan_raw_blocks); synthetic ones always fit
+                if (bad)  // scanned (scan_raw_blocks) unless the code always fits (synthetic, 4-bit)
                     throw std::invalid_argument("weight_codec: a weight tile does not fit the code");
             }
             int entry;

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "../kernels/common.cuh"
 
@@ -106,6 +107,140 @@ bool codec_encode_rows_tile(const uint8_t* packed, uint8_t* out) {
     uint16_t rows[8192];
     rows_from_packed(packed, rows);
     return codec_encode_tile(reinterpret_cast<const uint8_t*>(rows), out);
+}
+
+}  // namespace mlt
+
+namespace mlt {
+namespace {
+constexpr int kC4Codes = 8192, kC4Rows = 11264, kC4Table = 11392, kC4Hdr = 11400, kC4Esc = 11408;
+inline uint32_t c4_index(uint32_t r, uint32_t k) { return ((k >> 4) * 128u + r) * 16u + (k & 15u); }
+// (code word m, bit shift) of the 3-bit code of weight k of a row; bits 0-2
+// of a direct code are contiguous, a spare-bit code is spread over words
+// 3H, 3H+1, 3H+2 at bit 4n+3 (see weight_codec.hpp)
+inline void c4_put(uint32_t* words, uint32_t k, uint32_t code) {
+    const uint32_t H = k >> 5, kk = k & 31u, n = kk & 7u;
+    if (kk < 24) {
+        words[3 * H + (kk >> 3)] |= code << (4 * n);
+    } else {
+        for (uint32_t b = 0; b < 3; ++b) words[3 * H + b] |= ((code >> b) & 1u) << (4 * n + 3);
+    }
+}
+inline uint32_t c4_get(const uint32_t* words, uint32_t k) {
+    const uint32_t H = k >> 5, kk = k & 31u, n = kk & 7u;
+    if (kk < 24) return (words[3 * H + (kk >> 3)] >> (4 * n)) & 7u;
+    uint32_t c = 0;
+    for (uint32_t b = 0; b < 3; ++b) c |= ((words[3 * H + b] >> (4 * n + 3)) & 1u) << b;
+    return c;
+}
+}  // namespace
+
+bool codec4_encode_rows_tile(const uint8_t* packed, uint8_t* out) {
+    uint16_t w[8192];
+    rows_from_packed(packed, w);
+    bool can_shift = true;  // w + 0x80 must not carry out of the exponent (e = 255)
+    for (int i = 0; i < 8192; ++i) can_shift = can_shift && ((w[i] >> 7) & 0xFF) != 0xFF;
+    int ph = 0, best_cov = -1;
+    uint8_t table[8] = {};
+    int n_tab = 0;
+    for (int p = 0; p < (can_shift ? 2 : 1); ++p) {
+        uint32_t hist[256] = {};
+        for (int i = 0; i < 8192; ++i) ++hist[((w[i] + p * 0x80) >> 8) & 0xFF];
+        uint8_t order[256];
+        for (int v = 0; v < 256; ++v) order[v] = static_cast<uint8_t>(v);
+        std::stable_sort(order, order + 256, [&](uint8_t a, uint8_t b) { return hist[a] > hist[b]; });
+        int cov = 0, nt = 0;
+        for (int s = 0; s < 8 && hist[order[s]]; ++s) cov += static_cast<int>(hist[order[s]]), ++nt;
+        if (cov > best_cov) {
+            best_cov = cov, ph = p, n_tab = nt;
+            for (int s = 0; s < 8; ++s) table[s] = order[s];  // descending frequency: slot 7 the rarest
+        }
+    }
+    std::memset(out, 0, kCodec4TileBytes);
+    int code_of[256];
+    for (int v = 0; v < 256; ++v) code_of[v] = -1;
+    for (int s = 0; s < n_tab; ++s) code_of[table[s]] = s;
+    const int t7 = n_tab == 8 ? table[7] : -1;  // slot 7 free in every row when the table is short
+    struct Esc { uint32_t q, i; uint16_t v; };
+    std::vector<Esc> esc;
+    for (uint32_t r = 0; r < 128; ++r) {
+        uint8_t hi[64];
+        uint32_t cnt[256] = {};
+        int n_out = 0, uses7 = 0;
+        for (uint32_t k = 0; k < 64; ++k) {
+            const uint32_t i = c4_index(r, k);
+            const uint16_t x = static_cast<uint16_t>(w[i] + ph * 0x80);
+            out[i] = static_cast<uint8_t>(x & 0xFF);
+            hi[k] = static_cast<uint8_t>(x >> 8);
+            const int c = code_of[hi[k]];
+            if (c < 0) ++cnt[hi[k]], ++n_out;
+            else if (c == 7) ++uses7;
+        }
+        // slot 7 of this row: keep the table's, or take the most frequent
+        // out-of-table byte if that leaves fewer escapes
+        int ov = t7;
+        if (n_out) {
+            int vbest = -1;
+            for (int v = 0; v < 256; ++v)
+                if (cnt[v] && (vbest < 0 || cnt[v] > cnt[vbest])) vbest = v;
+            if (static_cast<int>(cnt[vbest]) > uses7) ov = vbest;
+        }
+        out[kC4Rows + r] = static_cast<uint8_t>(ov < 0 ? 0 : ov);
+        uint32_t words[6] = {};
+        for (uint32_t k = 0; k < 64; ++k) {
+            int c = code_of[hi[k]];
+            if (c == 7 && ov != t7) c = -1;   // slot 7 given to the row's override
+            if (c < 0 && hi[k] == ov) c = 7;
+            if (c < 0) {
+                const uint32_t i = c4_index(r, k);
+                esc.push_back({r / 32, i, w[i]});
+                c = 0;
+            }
+            c4_put(words, k, static_cast<uint32_t>(c));
+        }
+        for (uint32_t m = 0; m < 6; ++m) std::memcpy(out + kC4Codes + (m * 128 + r) * 4, &words[m], 4);
+    }
+    if (esc.size() > static_cast<size_t>(kCodec4MaxEscapes)) return false;
+    // rows were visited in order, so esc is already sorted by quarter, then row
+    std::memcpy(out + kC4Table, table, 8);
+    uint8_t start[4] = {0, 0, 0, 0};
+    for (uint32_t q = 1; q < 4; ++q) {
+        uint8_t s = 0;
+        while (s < esc.size() && esc[s].q < q) ++s;
+        start[q] = s;
+    }
+    out[kC4Hdr] = static_cast<uint8_t>(ph);
+    out[kC4Hdr + 1] = start[1], out[kC4Hdr + 2] = start[2], out[kC4Hdr + 3] = start[3];
+    out[kC4Hdr + 4] = static_cast<uint8_t>(esc.size());
+    for (size_t e = 0; e < esc.size(); ++e) {
+        const uint16_t i16 = static_cast<uint16_t>(esc[e].i);
+        std::memcpy(out + kC4Esc + 4 * e, &i16, 2);
+        std::memcpy(out + kC4Esc + 4 * e + 2, &esc[e].v, 2);
+    }
+    return true;
+}
+
+void codec4_decode_rows_tile(const uint8_t* enc, uint8_t* packed) {
+    uint16_t w[8192];
+    const uint8_t* table = enc + kC4Table;
+    const int ph = enc[kC4Hdr];
+    for (uint32_t r = 0; r < 128; ++r) {
+        uint32_t words[6];
+        for (uint32_t m = 0; m < 6; ++m) std::memcpy(&words[m], enc + kC4Codes + (m * 128 + r) * 4, 4);
+        for (uint32_t k = 0; k < 64; ++k) {
+            const uint32_t i = c4_index(r, k), c = c4_get(words, k);
+            const uint32_t hb = c == 7 ? enc[kC4Rows + r] : table[c];
+            w[i] = static_cast<uint16_t>(((hb << 8) | enc[i]) - ph * 0x80);
+        }
+    }
+    const int n = enc[kC4Hdr + 4];
+    for (int e = 0; e < n; ++e) {
+        uint16_t i16, v;
+        std::memcpy(&i16, enc + kC4Esc + 4 * e, 2);
+        std::memcpy(&v, enc + kC4Esc + 4 * e + 2, 2);
+        w[i16] = v;
+    }
+    packed_from_rows(w, packed);
 }
 
 }  // namespace mlt

@@ -58,3 +58,36 @@ void packed_from_rows(const uint16_t* rows8192, uint8_t* packed16k);
 bool codec_encode_rows_tile(const uint8_t* packed16k, uint8_t* out);
 
 }  // namespace mlt
+
+namespace mlt {
+
+// ---- codec 4: 3-bit code (GemmArgs::codec = 4, kernels/gemm_tc.cu) --------
+// Same row-plane weight order and TMEM-operand engine as codec 3, 11 stored
+// bits per weight instead of 12.  A per-tile phase ph in {0, 1} shifts every
+// weight by ph * 0x80 (one exponent step; ph = 1 pairs binades (2m-1, 2m)
+// instead of (2m, 2m+1), whichever leaves fewer weights outside the table):
+// w' = w + ph * 0x80.  Stored: w' low byte raw, a 3-bit index of w' high
+// byte into an 8-entry table whose slot 7 each row may override with its own
+// byte (the row's most frequent out-of-table high byte), and the weights that
+// still miss ("slow escapes") as {index, bf16} entries.  Layout:
+//   [0, 8192)       low byte of w'_i (i = ((k / 16) * 128 + r) * 16 + k % 16)
+//   [8192, 11264)   codes: u32 word m (0..5) of row r at 8192 + (m * 128 + r) * 4;
+//                   for H = m / 3, words A, B, C = 3H, 3H+1, 3H+2: nibble n
+//                   (bits 4n..4n+2) holds the code of k = 32H + n (A),
+//                   32H + 8 + n (B), 32H + 16 + n (C); bit 4n+3 of A, B, C
+//                   holds bit 0, 1, 2 of the code of k = 32H + 24 + n
+//   [11264, 11392)  per-row byte for slot 7
+//   [11392, 11400)  table[8] of high bytes
+//   [11400, 11404)  {phase, start of quarter 1, 2, 3} (u8; escapes sorted by quarter r / 32)
+//   [11404, 11408)  {n escapes (u8), 0, 0, 0}
+//   [11408, 11600)  n <= 48 escapes {u16 index i, u16 bf16 value w_i}
+// Decoding: w_i = (table'[code] << 8 | low) - ph * 0x80, then escapes.
+constexpr int kCodec4TileBytes = 11600;
+constexpr int kCodec4MaxEscapes = 48;
+bool codec4_encode_rows_tile(const uint8_t* packed16k, uint8_t* out);
+void codec4_decode_rows_tile(const uint8_t* enc, uint8_t* packed16k);
+
+// stored bytes of one encoded 64-k tile in GemmArgs::codec mode m (1-4)
+inline int codec_tile_bytes(int mode) { return mode == 4 ? kCodec4TileBytes : kCodecTileBytes; }
+
+}  // namespace mlt

@@ -42,11 +42,12 @@ def test_tp_bounds_match_baseline_md(name, tp, expect):
 def test_codec_bound_uses_stored_bytes():
     raw = bench.hrm_bound(_cfg("mixtral8x7b-16g"), 55.6, 125.0, PK)
     cfg = _cfg("mixtral8x7b-16g", codec=True)
-    assert bench.model_spec(cfg, stored=True).weight_dtype_bytes == pytest.approx(12432 / 8192)
+    assert bench.model_spec(cfg, stored=True).weight_dtype_bytes == pytest.approx(bench.CODEC_DT)
+    assert bench.CODEC_DT == pytest.approx(11600 / 8192)  # the default 3-bit code (codec 4)
     assert bench.model_spec(cfg).weight_dtype_bytes == 2.0  # the runtime always computes in bf16
     same_rw = bench.hrm_bound(cfg, 55.6, 125.0, PK)
-    # same residency, 24.1 % fewer streamed bytes: link-bound layer time shrinks by the byte ratio
-    assert same_rw.breakdown.link_upload == pytest.approx(raw.breakdown.link_upload * 12432 / 16384, rel=2e-3)
+    # same residency, 29.2 % fewer streamed bytes: link-bound layer time shrinks by the byte ratio
+    assert same_rw.breakdown.link_upload == pytest.approx(raw.breakdown.link_upload * bench.CODEC_DT / 2, rel=2e-3)
     cfg["r_w"] = bench.search_rw(cfg, 55.6, 125.0, PK)
     assert cfg["r_w"] > 0.10  # the same budget holds more encoded weights
     assert bench.hrm_bound(cfg, 55.6, 125.0, PK).decode_throughput > 1.35 * raw.decode_throughput

@@ -1,0 +1,160 @@
+"""Codec 4, the 3-bit row-plane weight code (runtime/weight_codec.hpp
+codec4_encode_rows_tile), on the host.
+
+A numpy decoder written from the format description pins the byte layout:
+3-bit codes (nibbles of words A, B, C, and their spare bits for the last 8
+weights of each 32), the 8-entry high-byte table with the per-row slot-7
+override, the per-tile exponent phase, and the quarter-sorted escapes.
+Encode -> decode restores every tile bit for bit (synthetic Mixtral weights,
+uniform and Gaussian tiles, zeros, tiles with e = 255); blocks that need more
+than 48 escapes are reported raw.  Also the stored size against codec 3.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2411_11217_b200 import capi
+
+TILE4 = 11600
+
+
+@pytest.fixture(scope="module")
+def K():
+    return capi.load_kernels()
+
+
+def bf16(x):
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def pack(K, w16, M, Kd):
+    out = np.zeros(M * Kd, np.uint16)
+    K.pack_weight(np.ascontiguousarray(w16).ctypes.data_as(C.c_void_p), M, Kd, out.ctypes.data_as(C.c_void_p))
+    return out.view(np.uint8)
+
+
+def np_swz_off(r, k):
+    return (r >> 3) * 1024 + (r & 7) * 128 + ((((k & 63) >> 3) ^ (r & 7)) << 4) + (k & 7) * 2
+
+
+R_I, K_I = np.meshgrid(np.arange(128), np.arange(64), indexing="ij")
+ROW_PLANE = ((K_I // 16) * 128 + R_I) * 16 + K_I % 16    # [r, k] -> index i
+
+
+def np_decode4(enc):
+    """Spec decoder -> [128, 64] bf16 (row r, column k of the tile)."""
+    enc = np.frombuffer(enc, np.uint8)
+    words = enc[8192:11264].view(np.uint32).reshape(6, 128)      # [m, r]
+    codes = np.zeros((128, 64), np.uint32)
+    for k in range(64):
+        H, kk = k // 32, k % 32
+        n = kk % 8
+        if kk < 24:
+            codes[:, k] = (words[3 * H + kk // 8] >> (4 * n)) & 7
+        else:
+            for b in range(3):
+                codes[:, k] |= ((words[3 * H + b] >> (4 * n + 3)) & 1) << b
+    table = enc[11392:11400]
+    ph = int(enc[11400])
+    rowb = enc[11264:11392]
+    hi = np.where(codes == 7, rowb[:, None], table[np.minimum(codes, 7)]).astype(np.uint32)
+    lo = enc[:8192][ROW_PLANE].astype(np.uint32)
+    w = ((hi << 8 | lo) - ph * 0x80).astype(np.uint16)
+    n = int(enc[11404])
+    starts = [0, int(enc[11401]), int(enc[11402]), int(enc[11403]), n]
+    assert starts == sorted(starts)
+    for e in range(n):
+        i = int(enc[11408 + 4 * e:11410 + 4 * e].view(np.uint16)[0])
+        v = enc[11410 + 4 * e:11412 + 4 * e].view(np.uint16)[0]
+        r, k = (i >> 4) & 127, (i >> 11) * 16 + (i & 15)
+        q = r // 32
+        assert starts[q] <= e < starts[q + 1]       # quarter-sorted
+        w[r, k] = v
+    return w
+
+
+def tile_weights(packed_tile):
+    """[128, 64] bf16 of a packed 16 KiB tile."""
+    return packed_tile.view(np.uint16)[np_swz_off(R_I, K_I) // 2]
+
+
+def encode4(K, packed, M, Kd):
+    out = np.zeros(M // 128 * (Kd // 64) * 16384, np.uint8)
+    raw = np.zeros(M // 128, np.uint8)
+    n_raw = K.codec4_encode_rows(packed.ctypes.data_as(C.c_void_p), M, Kd, out.ctypes.data_as(C.c_void_p),
+                                 raw.ctypes.data_as(C.c_void_p))
+    return out, raw, n_raw
+
+
+@pytest.mark.parametrize("fan", [4096, 14336])
+def test_roundtrip_synthetic_mixtral(K, fan):
+    """The runtime's synthetic weights (counter PRNG, uniform(+-sqrt3/sqrt(fan))):
+    every block codes, escapes well under the cap, bit-exact round trip."""
+    from oracle import bind as orc
+    Kd = 1024
+    w = orc.gen_bf16(1234, orc.tensor_id(0, 8 if fan == 4096 else 10, 3), 256 * Kd, fan ** -0.5).reshape(256, Kd)
+    packed = pack(K, w, 256, Kd)
+    out, raw, n_raw = encode4(K, packed, 256, Kd)
+    assert n_raw == 0 and not raw.any()
+    tiles = 256 // 128 * Kd // 64
+    esc = []
+    for t in range(tiles):
+        enc = out[t * TILE4:(t + 1) * TILE4]
+        esc.append(int(enc[11404]))
+        assert np.array_equal(np_decode4(enc.tobytes()), tile_weights(packed[t * 16384:(t + 1) * 16384]))
+    assert max(esc) <= 36, esc
+    back = np.zeros_like(packed)
+    K.codec4_decode_rows(out.ctypes.data_as(C.c_void_p), tiles, back.ctypes.data_as(C.c_void_p))
+    assert np.array_equal(back, packed)
+    assert K.codec4_tile_bytes() == TILE4 and TILE4 % 16 == 0
+    assert TILE4 / 12432 < 0.934      # >= 6.6 % fewer stored bytes than codec 3
+
+
+def test_edge_tiles(K):
+    """Zeros, signed zeros, denormals, e = 255 (inf / nan: phase 0 forced),
+    tiny outliers (escapes), and a block whose tiles overflow -> raw."""
+    rng = np.random.default_rng(5)
+    M, Kd = 384, 128
+    w = bf16(rng.uniform(-0.02, 0.02, (M, Kd)))
+    w[0, :64] = 0
+    w[1, :8] = 0x8000
+    w[2, :4] = [1, 2, 0x8003, 0x0040]                  # denormals
+    w[3, 5] = 0x7F80; w[3, 6] = 0xFF80; w[3, 7] = 0x7FC1   # inf, -inf, nan
+    w[5, 3] = bf16(np.array([2.0 ** -60]))[0]
+    w[100, 60] = bf16(np.array([-(2.0 ** -50)]))[0]
+    w[256:] = bf16(rng.normal(0, 1, (128, Kd)) * np.exp(rng.normal(0, 4, (128, Kd))))   # block 2: raw
+    packed = pack(K, w, M, Kd)
+    out, raw, n_raw = encode4(K, packed, M, Kd)
+    assert n_raw == 1 and list(raw) == [0, 0, 1]
+    kb = Kd // 64
+    for t in range(2 * kb):
+        enc = out[t * TILE4:(t + 1) * TILE4]
+        assert np.array_equal(np_decode4(enc.tobytes()), tile_weights(packed[t * 16384:(t + 1) * 16384]))
+    assert int(out[11400]) == 0                      # tile 0 holds e = 255: no phase shift
+    off = 2 * kb * TILE4
+    assert np.array_equal(out[off:off + kb * 16384], packed[2 * kb * 16384:])
+
+
+def test_phase_and_row_override(K):
+    """A tile whose binades straddle the high-byte pairing picks phase 1, and a
+    row whose out-of-table weights share one high byte codes them through its
+    slot-7 override instead of escapes."""
+    rng = np.random.default_rng(8)
+    a = 1.5 * 2.0 ** -7                      # top binade alone in its pair at phase 0
+    w = bf16(rng.uniform(-a, a, (128, 64)))
+    packed = pack(K, w, 128, 64)
+    out, raw, n_raw = encode4(K, packed, 128, 64)
+    enc = out[:TILE4]
+    assert int(enc[11400]) == 1
+    assert np.array_equal(np_decode4(enc.tobytes()), tile_weights(packed[:16384]))
+    w2 = bf16(rng.uniform(-0.02, 0.02, (128, 64)))
+    w2[9, :6] = bf16(np.full(6, 2.0 ** -30))          # six equal tiny weights in row 9
+    packed2 = pack(K, w2, 128, 64)
+    out2, _, _ = encode4(K, packed2, 128, 64)
+    enc2 = out2[:TILE4]
+    assert np.array_equal(np_decode4(enc2.tobytes()), tile_weights(packed2[:16384]))
+    n = int(enc2[11404])
+    rows = [((int(enc2[11408 + 4 * e]) | int(enc2[11409 + 4 * e]) << 8) >> 4) & 127 for e in range(n)]
+    assert 9 not in rows

@@ -397,9 +397,9 @@ def encode_weight_dev(K, w_bf16, fmt=1):
     """Host-pack + codec-encode a [M, K] bf16 weight and upload; returns (device
     buffer, encoded row-block pointers).  fmt 3: the row-plane code of the
     TMEM-operand engine (see encode_rows_dev)."""
-    if fmt == 3:
-        dev, blocks, flags = encode_rows_dev(K, w_bf16)
-        assert not any(flags)  # 12432-byte ring slots (codec_raw = 0)
+    if fmt in (3, 4):
+        dev, blocks, flags = encode_rows_dev(K, w_bf16, fmt=fmt)
+        assert not any(flags)  # encoded-size ring slots (codec_raw = 0)
         return dev, blocks
     M, Kd = w_bf16.shape
     src = bf16_bits(w_bf16.cpu())
@@ -412,11 +412,13 @@ def encode_weight_dev(K, w_bf16, fmt=1):
     return dev, blocks
 
 
-def encode_rows_dev(K, w_bf16, force_raw=()):
-    """Codec-3 weight blocks (row-plane encoded tiles, mlt_codec_encode_rows):
-    a row block the code cannot hold (> 31 escapes in a tile), or listed in
+def encode_rows_dev(K, w_bf16, force_raw=(), fmt=3):
+    """Codec-3 weight blocks (row-plane encoded tiles, mlt_codec_encode_rows),
+    or with fmt 4 the 3-bit code (mlt_codec4_encode_rows, 11600 B tiles):
+    a row block the code cannot hold (too many escapes in a tile), or listed in
     force_raw, is stored as raw packed tiles with its pointer tagged (bit 0).
     Returns (device buffer, row-block pointers, raw flags)."""
+    enc_fn, tb = (K.codec4_encode_rows, 11600) if fmt == 4 else (K.codec_encode_rows, 12432)
     M, Kd = w_bf16.shape
     src = bf16_bits(w_bf16.cpu())
     packed = np.empty_like(src)
@@ -428,10 +430,10 @@ def encode_rows_dev(K, w_bf16, force_raw=()):
     for r in range(rbs):
         blk = np.empty(kb * 16384, np.uint8)
         rr = np.zeros(1, np.uint8)
-        assert K.codec_encode_rows(np.ascontiguousarray(pb[r]).ctypes.data_as(C.c_void_p), 128, Kd,
-                                   blk.ctypes.data_as(C.c_void_p), rr.ctypes.data_as(C.c_void_p)) >= 0
+        assert enc_fn(np.ascontiguousarray(pb[r]).ctypes.data_as(C.c_void_p), 128, Kd,
+                      blk.ctypes.data_as(C.c_void_p), rr.ctypes.data_as(C.c_void_p)) >= 0
         raw = bool(rr[0]) or r in force_raw
-        blk = pb[r].copy() if raw else blk[:kb * 12432]
+        blk = pb[r].copy() if raw else blk[:kb * tb]
         parts.append(blk)
         rel.append((off, raw))
         flags.append(raw)
@@ -440,7 +442,7 @@ def encode_rows_dev(K, w_bf16, force_raw=()):
     return dev, [dev.data_ptr() + o + (1 if raw else 0) for o, raw in rel], flags
 
 
-@pytest.mark.parametrize("codec", [1, 3])
+@pytest.mark.parametrize("codec", [1, 3, 4])
 @pytest.mark.parametrize("T,M,Kd,n_cap,splits,resid", [(16, 256, 512, 16, 1, True), (64, 384, 4096, 64, 3, False),
                                                         (256, 256, 1024, 256, 2, False),
                                                         (200, 128, 256, 208, 1, True)])
@@ -471,7 +473,7 @@ def test_codec_gemm_bitwise_equals_raw(K, T, M, Kd, n_cap, splits, resid, codec)
     assert (outs[1].sum(0)[:T] - ref).abs().max().item() <= 2e-3 * max(1.0, ref.abs().max().item())
 
 
-@pytest.mark.parametrize("codec", [1, 3])
+@pytest.mark.parametrize("codec", [1, 3, 4])
 @pytest.mark.parametrize("T,H,Fd,E,Kk,n_cap", [(64, 512, 768, 8, 2, 64), (33, 256, 256, 16, 4, 32)])
 def test_codec_expert_ffn_bitwise_equals_raw(K, T, H, Fd, E, Kk, n_cap, codec):
     """Grouped gate/up (two encoded matrices, fused SiLU -> packed bf16) and
@@ -520,8 +522,9 @@ def test_codec_expert_ffn_bitwise_equals_raw(K, T, H, Fd, E, Kk, n_cap, codec):
 
 
 
+@pytest.mark.parametrize("codec", [3, 4])
 @pytest.mark.parametrize("T,M,Kd,n_cap,splits", [(16, 512, 1024, 16, 1), (80, 384, 2048, 96, 2)])
-def test_codec3_escapes_and_raw_blocks(K, T, M, Kd, n_cap, splits):
+def test_codec3_escapes_and_raw_blocks(K, T, M, Kd, n_cap, splits, codec):
     """Codec 3 (row-plane tiles decoded into TMEM, MMA with A from TMEM) on
     heavy-tailed weights: tiles with escapes (patched per row in registers),
     row blocks the code cannot hold stored raw (tagged pointers), plus a
@@ -538,17 +541,54 @@ def test_codec3_escapes_and_raw_blocks(K, T, M, Kd, n_cap, splits):
     x = rand_bf16(T, Kd, gen=g)
     R = (T + 15) // 16 * 16
     raw_dev, raw_blocks = pack_weight_dev(K, w)
-    enc_dev, enc_blocks, flags = encode_rows_dev(K, w, force_raw=(1,))
+    enc_dev, enc_blocks, flags = encode_rows_dev(K, w, force_raw=(1,), fmt=codec)
     assert flags[-1] and flags[1] and not flags[0], flags
     xp = pack_rows_dev(K, x, R)
     outs = []
-    for cdc, blocks in ((0, raw_blocks), (3, enc_blocks)):
+    for cdc, blocks in ((0, raw_blocks), (codec, enc_blocks)):
         tab = table([blocks])
         out = torch.zeros(splits, R, M, device="cuda")
         a = capi.GemmArgs(a_table=tab.data_ptr(), n_mats=1, G=1, RB=M // 128, K=Kd, b=xp.data_ptr(), R=R,
                           rows_dense=T, n_cap=n_cap, epi=0, alpha=1.0, out_f32=out.data_ptr(), ldo=M,
-                          k_splits=splits, split_stride=R * M, codec=cdc, codec_raw=int(cdc == 3))
+                          k_splits=splits, split_stride=R * M, codec=cdc, codec_raw=int(cdc != 0))
         K.gemm(C.byref(a), stream())
+        torch.cuda.synchronize()
+        outs.append(out.cpu())
+    assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("T,n_cap", [(48, 48), (130, 144)])
+def test_codec4_phase_override_escapes(K, T, n_cap):
+    """Codec 4 tiles of every kind the encoder emits: phase 0 and phase 1
+    tiles (top binade alone in its high-byte pair), rows whose out-of-table
+    weights go through the row's slot-7 override, escapes in every row quarter
+    up to the 48-entry cap, a raw block — the TMEM-operand GEMM equals the
+    raw-tile GEMM bit for bit."""
+    g = torch.Generator().manual_seed(T + 17)
+    M, Kd = 512, 512
+    a = 1.5 * 2.0 ** -7
+    w = ((torch.rand(M, Kd, generator=g) * 2 - 1) * a)
+    w[128:256] *= 2                        # the other binade alignment (phase 0)
+    w[256:384, :8] = 2.0 ** -30            # rows with one repeated tiny value: slot-7 overrides
+    # tiles with many escapes: distinct tiny values spread over rows of every quarter
+    idx = torch.randperm(128 * Kd, generator=g)[:26 * (Kd // 64)]
+    vals = torch.pow(2.0, -torch.randint(20, 60, (idx.numel(),), generator=g).float())
+    w[:128].view(-1)[idx] = vals * torch.sign(torch.rand(idx.numel(), generator=g) - 0.5)
+    w = w.to(torch.bfloat16)
+    x = rand_bf16(T, Kd, gen=g)
+    R = (T + 15) // 16 * 16
+    raw_dev, raw_blocks = pack_weight_dev(K, w)
+    enc_dev, enc_blocks, flags = encode_rows_dev(K, w, force_raw=(3,), fmt=4)
+    assert flags == [False, False, False, True], flags
+    xp = pack_rows_dev(K, x, R)
+    outs = []
+    for cdc, blocks in ((0, raw_blocks), (4, enc_blocks)):
+        tab = table([blocks])
+        out = torch.zeros(1, R, M, device="cuda")
+        args = capi.GemmArgs(a_table=tab.data_ptr(), n_mats=1, G=1, RB=M // 128, K=Kd, b=xp.data_ptr(), R=R,
+                             rows_dense=T, n_cap=n_cap, epi=0, alpha=1.0, out_f32=out.data_ptr(), ldo=M,
+                             k_splits=1, split_stride=R * M, codec=cdc, codec_raw=int(cdc != 0))
+        K.gemm(C.byref(args), stream())
         torch.cuda.synchronize()
         outs.append(out.cpu())
     assert torch.equal(outs[0], outs[1])
