@@ -324,8 +324,9 @@ int mlt_codec_encode_rows(const uint8_t* host_packed, int64_t M, int64_t K, uint
                           uint8_t* raw_blocks);
 /* The 3-bit row-plane code (GemmArgs codec = 4; runtime/weight_codec.hpp
  * codec4_encode_rows_tile): 11 stored bits per weight, mlt_codec4_tile_bytes()
- * = 11600 B per 64-k tile (8-entry high-byte table with a per-tile exponent
- * phase, a per-row override of table slot 7, <= 48 escapes); same contract as
+ * = 11600 B per 64-k tile (7 tile-wide high bytes + a per-row slot with a
+ * per-unit second value, a per-tile exponent phase, <= 44 records + escapes
+ * per tile); same contract as
  * mlt_codec_encode_rows.  mlt_codec4_decode_rows is the host reference
  * decoder (encoded tiles -> 16 KiB packed tiles). */
 int mlt_codec4_encode_rows(const uint8_t* host_packed, int64_t M, int64_t K, uint8_t* host_out,

@@ -13,7 +13,8 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmlt.so")
+# MLT_LIB overrides the library (diagnostic builds of the same sources, tools/)
+LIB_PATH = os.environ.get("MLT_LIB") or os.path.join(_HERE, "libmlt.so")
 
 MLT_OK = 0
 ERRORS = {-1: "invalid argument", -2: "infeasible policy", -3: "unsupported combination",

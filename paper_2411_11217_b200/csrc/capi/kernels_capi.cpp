@@ -181,7 +181,7 @@ int mlt_codec4_encode_rows(const uint8_t* packed, int64_t M, int64_t K, uint8_t*
     return guard([&] {
         return encode_blocks("codec4_encode_rows", packed, M, K, out, raw_blocks, mlt::codec4_encode_rows_tile,
                              [](const uint8_t* src, uint8_t* dst) { std::memcpy(dst, src, 16384); },
-                             mlt::kCodec4TileBytes, mlt::kCodec4MaxEscapes);
+                             mlt::kCodec4TileBytes, mlt::kCodec4MaxEntries);
     });
 }
 

@@ -330,45 +330,16 @@ __device__ __forceinline__ void decode_row_ts(uint32_t c, uint32_t r, uint32_t (
 // row: words A, B, C hold 24 codes in nibbles (bits 0-2; selector = word &
 // 0x7777) and, in their nibble bit 3, the 3 bits of the last 8 codes,
 // gathered into a fourth selector word by 3 shifts and 3 masked ORs.  One
-// PRMT looks up 4 high bytes in the 8-entry table (slot 7 = this row's
-// override byte), two PRMTs interleave them with the raw low bytes, and with
-// phase 1 one subtraction per 2 weights undoes the tile's exponent shift:
-// ~1.25 (phase 0) / 1.75 (phase 1) instructions per weight.  The escapes of
-// the warp's row quarter are then patched by their owning lanes.
-__device__ __forceinline__ void patch_col(uint32_t (&o)[32], uint32_t col, uint32_t v, uint32_t sel) {
-    switch (col) {
-#define MLT_PATCH(q) case q: o[q] = prmt(o[q], v, sel); break;
-        MLT_PATCH(0) MLT_PATCH(1) MLT_PATCH(2) MLT_PATCH(3) MLT_PATCH(4) MLT_PATCH(5) MLT_PATCH(6) MLT_PATCH(7)
-        MLT_PATCH(8) MLT_PATCH(9) MLT_PATCH(10) MLT_PATCH(11) MLT_PATCH(12) MLT_PATCH(13) MLT_PATCH(14)
-        MLT_PATCH(15) MLT_PATCH(16) MLT_PATCH(17) MLT_PATCH(18) MLT_PATCH(19) MLT_PATCH(20) MLT_PATCH(21)
-        MLT_PATCH(22) MLT_PATCH(23) MLT_PATCH(24) MLT_PATCH(25) MLT_PATCH(26) MLT_PATCH(27) MLT_PATCH(28)
-        MLT_PATCH(29) MLT_PATCH(30) MLT_PATCH(31)
-#undef MLT_PATCH
-        default: break;
-    }
-}
-
-template <bool kPhase>
-__device__ __forceinline__ void expand_row_c4(const uint4 (&lo)[4], const uint32_t (&cw)[6], uint32_t t0,
-                                              uint32_t t1, uint32_t (&o)[32]) {
-#pragma unroll
-    for (int H = 0; H < 2; ++H) {
-        const uint32_t A = cw[3 * H], B = cw[3 * H + 1], C = cw[3 * H + 2];
-        const uint32_t S = ((A >> 3) & 0x11111111u) | ((B >> 2) & 0x22222222u) | ((C >> 1) & 0x44444444u);
-        const uint32_t sel[8] = {A & 0x7777u, (A >> 16) & 0x7777u, B & 0x7777u, (B >> 16) & 0x7777u,
-                                 C & 0x7777u, (C >> 16) & 0x7777u, S, S >> 16};
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {  // weights k = 32H + 4u .. +3
-            const uint32_t h4 = prmt(t0, t1, sel[u]);
-            const uint4& l = lo[2 * H + (u >> 2)];
-            const uint32_t lw = (u & 3) == 0 ? l.x : (u & 3) == 1 ? l.y : (u & 3) == 2 ? l.z : l.w;
-            uint32_t a = prmt(lw, h4, 0x5140u), b = prmt(lw, h4, 0x7362u);
-            if (kPhase) a -= 0x00800080u, b -= 0x00800080u;
-            o[16 * H + 2 * u] = a;
-            o[16 * H + 2 * u + 1] = b;
-        }
-    }
-}
+// PRMT looks up 4 high bytes in this row's 8-byte table — slots 0-6 of the
+// tile, slot 7 = the row's byte, or in the units its record flags the
+// record's byte (one SEL per 4 weights) — two PRMTs interleave them with the
+// raw low bytes, one subtraction per 2 weights undoes the tile's exponent
+// phase: ~1.9 instructions per weight, all register indices static.  The
+// rare hard escapes (~0.5 per row quarter) are patched by a warp-uniform
+// loop with a predicated 32-way select.
+struct EscC4 {
+    uint32_t n, e0, e1;  // this warp's hard escapes: count, entries lane and 32 + lane
+};
 
 __device__ __forceinline__ uint32_t lds8(uint32_t a) {
     uint32_t v;
@@ -376,9 +347,40 @@ __device__ __forceinline__ uint32_t lds8(uint32_t a) {
     return v;
 }
 
-__device__ __forceinline__ void decode_row_c4(uint32_t c, uint32_t r, uint32_t (&o)[32]) {
+template <bool kPhase>
+__device__ __forceinline__ void expand_row_c4(const uint4 (&lo)[4], const uint32_t (&cw)[6], uint32_t t0, uint32_t t1,
+                                              uint32_t t1x, uint32_t rec, uint32_t (&o)[32]) {
+#pragma unroll
+    for (int H = 0; H < 2; ++H) {
+        const uint32_t A = cw[3 * H], B = cw[3 * H + 1], C = cw[3 * H + 2];
+        const uint32_t S = ((A >> 3) & 0x11111111u) | ((B >> 2) & 0x22222222u) | ((C >> 1) & 0x44444444u);
+        const uint32_t sel[8] = {A & 0x7777u, (A >> 16) & 0x7777u, B & 0x7777u, (B >> 16) & 0x7777u,
+                                 C & 0x7777u, (C >> 16) & 0x7777u, S, S >> 16};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // weights k = 32H + 4u .. +3: unit 8H + u
+#ifndef MLT_DIAG_C4_NOSEL
+            const uint32_t tu = (rec >> (8 * H + u)) & 1u ? t1x : t1;
+#else
+            const uint32_t tu = t1 ^ (t1x & rec & 0);
+#endif
+            const uint32_t h4 = prmt(t0, tu, sel[u]);
+            const uint4& l = lo[2 * H + (u >> 2)];
+            const uint32_t lw = (u & 3) == 0 ? l.x : (u & 3) == 1 ? l.y : (u & 3) == 2 ? l.z : l.w;
+            uint32_t x = prmt(lw, h4, 0x5140u), y = prmt(lw, h4, 0x7362u);
+            if (kPhase) x -= 0x00800080u, y -= 0x00800080u;
+            o[16 * H + 2 * u] = x;
+            o[16 * H + 2 * u + 1] = y;
+        }
+    }
+}
+
+__device__ __forceinline__ void decode_row_c4(uint32_t c, uint32_t r, uint32_t (&o)[32], EscC4& esc) {
+    // issue order matters (the loads are ordered volatile asm): the tile
+    // header, this row's bytes, then the record / escape loads whose
+    // addresses need the header, so their latency overlaps the row loads
     const uint2 T = lds64(c + 11392);
-    const uint32_t hdr = lds32(c + 11400), n = lds32(c + 11404) & 0xffu;
+    const uint32_t hdr = lds32(c + 11400), cnt = lds32(c + 11404);
+    const uint4 qm = lds128(c + 11408);
     const uint32_t rb = lds8(c + 11264 + r);
     uint4 lo[4];
     uint32_t cw[6];
@@ -386,23 +388,50 @@ __device__ __forceinline__ void decode_row_c4(uint32_t c, uint32_t r, uint32_t (
     for (int j = 0; j < 4; ++j) lo[j] = lds128(c + (j * 128u + r) * 16u);
 #pragma unroll
     for (int m = 0; m < 6; ++m) cw[m] = lds32(c + 8192u + (m * 128u + r) * 4u);
-    const uint32_t t1 = prmt(T.y, rb, 0x4210u);  // slot 7 <- this row's byte
-    if (hdr & 0xffu)
-        expand_row_c4<true>(lo, cw, T.x, t1, o);
-    else
-        expand_row_c4<false>(lo, cw, T.x, t1, o);
-    // escapes of this warp's quarter q = r / 32 (warp-uniform count)
     const uint32_t lane = threadIdx.x & 31u, q = r >> 5;
-    const uint32_t b0 = q ? (hdr >> (8 * q)) & 0xffu : 0u, b1 = q < 3 ? (hdr >> (8 * (q + 1))) & 0xffu : n;
-    for (uint32_t base = b0; base < b1; base += 32) {
-        const uint32_t cnt = min(32u, b1 - base);
-        const uint32_t my = lane < cnt ? lds32(c + 11408u + 4u * (base + lane)) : 0u;
-        for (uint32_t e = 0; e < cnt; ++e) {
-            const uint32_t ent = __shfl_sync(0xffffffffu, my, e), i = ent & 0xffffu;
-            if (((i >> 4) & 127u) == r) {
-                const uint32_t k = (i >> 11) * 16u + (i & 15u);
-                patch_col(o, k >> 1, ent >> 16, (k & 1u) ? 0x5410u : 0x3254u);
-            }
+    const uint32_t n_hard = cnt & 0xffu, n_rec = (cnt >> 8) & 0xffu;
+    // this row's unit record: rows with records are counted in row order
+    const uint32_t qmask = q == 0 ? qm.x : q == 1 ? qm.y : q == 2 ? qm.z : qm.w;
+    const uint32_t base = (q > 0 ? __popc(qm.x) : 0) + (q > 1 ? __popc(qm.y) : 0) + (q > 2 ? __popc(qm.z) : 0);
+#ifndef MLT_DIAG_C4_RECNOLOAD
+    const uint32_t rec = (qmask >> lane) & 1u ? lds32(c + 11424u + 4u * (base + __popc(qmask & ((1u << lane) - 1u))))
+                                               : 0u;
+#else
+    const uint32_t rec = (qmask >> lane) & 1u ? (qmask ^ base) : 0u;
+#endif
+    // hard escapes of this warp's quarter
+    const uint32_t hb0 = q ? (hdr >> (8 * q)) & 0xffu : 0u, hb1 = q < 3 ? (hdr >> (8 * (q + 1))) & 0xffu : n_hard;
+    const uint32_t h0 = c + 11424u + 4u * n_rec;
+    esc.n = hb1 - hb0;
+    esc.e0 = lane < esc.n ? lds32(h0 + 4u * (hb0 + lane)) : 0u;
+    esc.e1 = lane + 32u < esc.n ? lds32(h0 + 4u * (hb0 + 32u + lane)) : 0u;
+    const uint32_t t1 = prmt(T.y, rb, 0x4210u), t1x = prmt(T.y, rec >> 16, 0x4210u);
+    if (hdr & 0xffu)
+        expand_row_c4<true>(lo, cw, T.x, t1, t1x, rec, o);
+    else
+        expand_row_c4<false>(lo, cw, T.x, t1, t1x, rec, o);
+}
+
+template <int G>
+__device__ __forceinline__ void patch8_c4(uint32_t (&o)[32], uint32_t j, uint32_t v, uint32_t sel) {
+#pragma unroll
+    for (uint32_t x = 0; x < 8; ++x)
+        if (x == j) o[8 * G + x] = prmt(o[8 * G + x], v, sel);
+}
+
+__device__ __forceinline__ void patch_hard_c4(uint32_t (&o)[32], uint32_t r, const EscC4& esc) {
+    for (uint32_t e = 0; e < esc.n; ++e) {
+        const uint32_t x0 = __shfl_sync(0xffffffffu, esc.e0, e & 31u), x1 = __shfl_sync(0xffffffffu, esc.e1, e & 31u);
+        const uint32_t ent = e < 32u ? x0 : x1, idx = ent & 0xffffu;
+        if (((idx >> 4) & 127u) == r) {
+            // column k / 2 = 8 * (i >> 11) + (i & 15) / 2: the 16-k chunk picks
+            // one of 4 groups of 8 registers, then 8 predicated selects
+            const uint32_t j = (idx & 15u) >> 1, v = ent >> 16, sel = (idx & 1u) ? 0x5410u : 0x3254u;
+            const uint32_t g = idx >> 11;
+            if (g == 0) patch8_c4<0>(o, j, v, sel);
+            else if (g == 1) patch8_c4<1>(o, j, v, sel);
+            else if (g == 2) patch8_c4<2>(o, j, v, sel);
+            else patch8_c4<3>(o, j, v, sel);
         }
     }
 }
@@ -490,6 +519,7 @@ __device__ __forceinline__ void producer_b_ts(const GemmArgs& a, const Ring3& R,
 // quarter) of every tile t with t % 2 == (w - 6) / 4: smem -> registers ->
 // release the A slot (one arrival per warp) -> wait for the TMEM slot ->
 // tcgen05.st -> wait::st -> one arrival per warp on the slot's dfull.
+template <int kMode>
 __device__ __forceinline__ void decoder_role_ts(const GemmArgs& a, const Ring3& R, Smem* ctl, int n_virtual, int KB,
                                                 uint32_t tmem) {
     const int w = static_cast<int>(threadIdx.x >> 5);
@@ -518,12 +548,17 @@ __device__ __forceinline__ void decoder_role_ts(const GemmArgs& a, const Ring3& 
                         if (kt) kt[256] = globaltimer();
                         const uint32_t sa = smem_u32(R.a_ring + s * R.a_slot_bytes);
                         uint32_t o[32];
-                        if (mt ? raw1 : raw0)
+                        EscC4 esc{0u, 0u, 0u};
+                        if (mt ? raw1 : raw0) {
                             raw_row_ts(sa, r, o);
-                        else if (a.codec == 4)
-                            decode_row_c4(sa, r, o);
-                        else
+                        } else if constexpr (kMode == 4) {
+                            decode_row_c4(sa, r, o, esc);
+#ifndef MLT_DIAG_C4_NOHARD  // diagnostic builds (tools/diag_build.sh) only
+                            if (esc.n) patch_hard_c4(o, r, esc);
+#endif
+                        } else {
                             decode_row_ts(sa, r, o);
+                        }
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&ctl->empty[s]);
                         if (kt) kt[512] = globaltimer();
@@ -532,6 +567,8 @@ __device__ __forceinline__ void decoder_role_ts(const GemmArgs& a, const Ring3& 
                         tc_fence_after();
                         tmem_st32(tl + static_cast<uint32_t>(ts * 32), o);
                         tmem_wait_st();
+
+
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&ctl->dfull[ts]);
@@ -606,8 +643,14 @@ __device__ __forceinline__ void mma_role_ts(const GemmArgs& a, const Ring3& R, S
     }
 }
 
-template <bool kTs>
-__global__ void __launch_bounds__(kTs ? kThreadsCodec3 : kThreadsCodec, 1) gemm_tc_kernel(const GemmArgs a) {
+// kMode: 0 = raw / codec 1 (shared-stage ring), 3 / 4 = the TMEM-operand
+// engine with the 4-bit / 3-bit decoder (one decoder per kernel keeps the
+// decoder warps' hot loop small: codec 4 with both decoders and its escape
+// sweep in one kernel stalled on instruction fetch, ncu no_instruction 8.7
+// per issue vs 0.4)
+template <int kMode>
+__global__ void __launch_bounds__(kMode ? kThreadsCodec3 : kThreadsCodec, 1) gemm_tc_kernel(const GemmArgs a) {
+    constexpr bool kTs = kMode != 0;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1 KiB alignment for the SWIZZLE_128B atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -697,7 +740,7 @@ __global__ void __launch_bounds__(kTs ? kThreadsCodec3 : kThreadsCodec, 1) gemm_
         } else if (warp == 1) {
             mma_role_ts(a, R3, ctl, n_virtual, KB, tmem);
         } else {
-            decoder_role_ts(a, R3, ctl, n_virtual, KB, tmem);
+            decoder_role_ts<kMode>(a, R3, ctl, n_virtual, KB, tmem);
         }
     } else if (warp == 0) {
         // ===== producer =====
@@ -1047,7 +1090,9 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     const int smem = a.codec >= 3 ? ((a.stages * a.a3_slot_bytes + 1023) & ~1023) + a.b3_slots * a.n_cap * 128 +
                                         1024 + kCtlBytes + kEpiScratch
                                   : gemm_smem_bytes(a.n_mats, a.n_cap, a.stages, a.kps);
-    void (*const kern)(const GemmArgs) = a.codec >= 3 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>;
+    void (*const kern)(const GemmArgs) = a.codec == 4   ? gemm_tc_kernel<4>
+                                         : a.codec == 3 ? gemm_tc_kernel<3>
+                                                        : gemm_tc_kernel<0>;
     if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), 227 * 1024); e != cudaSuccess)
         return e;
     a.sk_full = a.sk_tail = a.sk_parts = 0;
@@ -1069,9 +1114,9 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         // (1 CTA per SM at this smem size; fewer SMs under MPS / green
         // contexts / a concurrent kernel) -> otherwise run without the tail
         // (cached per device and block size: the occupancy query costs host microseconds)
-        static int cache[64][kMaxDecGroups + 2] = {};
+        static int cache[64][kMaxDecGroups + 3] = {};
         int dev = 0;
-        const int slot = a.codec >= 3 ? kMaxDecGroups + 1 : a.codec ? a.dec_groups : 0;
+        const int slot = a.codec >= 3 ? kMaxDecGroups + a.codec - 2 : a.codec ? a.dec_groups : 0;
         int per_sm = 0;
         if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
             if (!cache[dev][slot] &&

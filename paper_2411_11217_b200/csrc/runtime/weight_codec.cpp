@@ -113,7 +113,8 @@ bool codec_encode_rows_tile(const uint8_t* packed, uint8_t* out) {
 
 namespace mlt {
 namespace {
-constexpr int kC4Codes = 8192, kC4Rows = 11264, kC4Table = 11392, kC4Hdr = 11400, kC4Esc = 11408;
+constexpr int kC4Codes = 8192, kC4Rows = 11264, kC4Table = 11392, kC4Hdr = 11400, kC4QMask = 11408,
+              kC4Ent = 11424;
 inline uint32_t c4_index(uint32_t r, uint32_t k) { return ((k >> 4) * 128u + r) * 16u + (k & 15u); }
 // (code word m, bit shift) of the 3-bit code of weight k of a row; bits 0-2
 // of a direct code are contiguous, a spare-bit code is spread over words
@@ -142,80 +143,110 @@ bool codec4_encode_rows_tile(const uint8_t* packed, uint8_t* out) {
     for (int i = 0; i < 8192; ++i) can_shift = can_shift && ((w[i] >> 7) & 0xFF) != 0xFF;
     int ph = 0, best_cov = -1;
     uint8_t table[8] = {};
-    int n_tab = 0;
     for (int p = 0; p < (can_shift ? 2 : 1); ++p) {
         uint32_t hist[256] = {};
         for (int i = 0; i < 8192; ++i) ++hist[((w[i] + p * 0x80) >> 8) & 0xFF];
         uint8_t order[256];
         for (int v = 0; v < 256; ++v) order[v] = static_cast<uint8_t>(v);
         std::stable_sort(order, order + 256, [&](uint8_t a, uint8_t b) { return hist[a] > hist[b]; });
-        int cov = 0, nt = 0;
-        for (int s = 0; s < 8 && hist[order[s]]; ++s) cov += static_cast<int>(hist[order[s]]), ++nt;
+        int cov = 0;
+        for (int s = 0; s < 8; ++s) cov += static_cast<int>(hist[order[s]]);
         if (cov > best_cov) {
-            best_cov = cov, ph = p, n_tab = nt;
+            best_cov = cov, ph = p;
             for (int s = 0; s < 8; ++s) table[s] = order[s];  // descending frequency: slot 7 the rarest
         }
     }
     std::memset(out, 0, kCodec4TileBytes);
+    // slots 0-6 are fixed for the tile; slot 7 is per row (override byte) and,
+    // inside the 4-weight units a row's record flags, a second per-row byte
     int code_of[256];
     for (int v = 0; v < 256; ++v) code_of[v] = -1;
-    for (int s = 0; s < n_tab; ++s) code_of[table[s]] = s;
-    const int t7 = n_tab == 8 ? table[7] : -1;  // slot 7 free in every row when the table is short
-    struct Esc { uint32_t q, i; uint16_t v; };
-    std::vector<Esc> esc;
+    for (int s = 0; s < 7; ++s) code_of[table[s]] = s;
+    struct Hard { uint32_t q, i; uint16_t v; };
+    std::vector<Hard> hard;
+    uint32_t qmask[4] = {};
+    std::vector<uint32_t> recs;
     for (uint32_t r = 0; r < 128; ++r) {
         uint8_t hi[64];
-        uint32_t cnt[256] = {};
-        int n_out = 0, uses7 = 0;
         for (uint32_t k = 0; k < 64; ++k) {
             const uint32_t i = c4_index(r, k);
             const uint16_t x = static_cast<uint16_t>(w[i] + ph * 0x80);
             out[i] = static_cast<uint8_t>(x & 0xFF);
             hi[k] = static_cast<uint8_t>(x >> 8);
-            const int c = code_of[hi[k]];
-            if (c < 0) ++cnt[hi[k]], ++n_out;
-            else if (c == 7) ++uses7;
         }
-        // slot 7 of this row: keep the table's, or take the most frequent
-        // out-of-table byte if that leaves fewer escapes
-        int ov = t7;
-        if (n_out) {
-            int vbest = -1;
-            for (int v = 0; v < 256; ++v)
-                if (cnt[v] && (vbest < 0 || cnt[v] > cnt[vbest])) vbest = v;
-            if (static_cast<int>(cnt[vbest]) > uses7) ov = vbest;
+        // the row's out-of-table (slot 7) values
+        int vals[64], nv = 0;
+        for (uint32_t k = 0; k < 64; ++k)
+            if (code_of[hi[k]] < 0 && std::find(vals, vals + nv, hi[k]) == vals + nv) vals[nv++] = hi[k];
+        // hard escapes of an assignment (R row-wide, X in the units holding an X)
+        auto cost = [&](int R, int X, uint32_t* umask_out) {
+            uint32_t um = 0;
+            if (X >= 0)
+                for (uint32_t k = 0; k < 64; ++k)
+                    if (hi[k] == X) um |= 1u << (k >> 2);
+            int h = 0;
+            for (uint32_t k = 0; k < 64; ++k) {
+                if (code_of[hi[k]] >= 0) continue;
+                const int slot7 = (um >> (k >> 2)) & 1u ? X : R;
+                h += hi[k] != slot7;
+            }
+            if (umask_out) *umask_out = um;
+            return h;
+        };
+        int R = nv ? vals[0] : table[7], X = -1, best = nv ? cost(vals[0], -1, nullptr) : 0;
+        for (int a = 0; a < nv && best; ++a) {
+            const int h = cost(vals[a], -1, nullptr);
+            if (h < best) best = h, R = vals[a], X = -1;
         }
-        out[kC4Rows + r] = static_cast<uint8_t>(ov < 0 ? 0 : ov);
+        for (int a = 0; a < nv && best; ++a)
+            for (int b = 0; b < nv && best; ++b) {
+                if (a == b) continue;
+                const int h = cost(vals[a], vals[b], nullptr);
+                if (h < best) best = h, R = vals[a], X = vals[b];
+            }
+        uint32_t um = 0;
+        cost(R, X, &um);
+        out[kC4Rows + r] = static_cast<uint8_t>(R);
+        if (X >= 0) {
+            qmask[r / 32] |= 1u << (r % 32);
+            recs.push_back(um | (static_cast<uint32_t>(X) << 16));
+        }
         uint32_t words[6] = {};
         for (uint32_t k = 0; k < 64; ++k) {
             int c = code_of[hi[k]];
-            if (c == 7 && ov != t7) c = -1;   // slot 7 given to the row's override
-            if (c < 0 && hi[k] == ov) c = 7;
             if (c < 0) {
-                const uint32_t i = c4_index(r, k);
-                esc.push_back({r / 32, i, w[i]});
-                c = 0;
+                const int slot7 = (um >> (k >> 2)) & 1u ? X : R;
+                if (hi[k] == slot7) {
+                    c = 7;
+                } else {
+                    const uint32_t i = c4_index(r, k);
+                    hard.push_back({r / 32, i, w[i]});
+                    c = 0;
+                }
             }
             c4_put(words, k, static_cast<uint32_t>(c));
         }
         for (uint32_t m = 0; m < 6; ++m) std::memcpy(out + kC4Codes + (m * 128 + r) * 4, &words[m], 4);
     }
-    if (esc.size() > static_cast<size_t>(kCodec4MaxEscapes)) return false;
-    // rows were visited in order, so esc is already sorted by quarter, then row
+    if (recs.size() + hard.size() > static_cast<size_t>(kCodec4MaxEntries)) return false;
     std::memcpy(out + kC4Table, table, 8);
     uint8_t start[4] = {0, 0, 0, 0};
     for (uint32_t q = 1; q < 4; ++q) {
         uint8_t s = 0;
-        while (s < esc.size() && esc[s].q < q) ++s;
+        while (s < hard.size() && hard[s].q < q) ++s;   // rows were visited in order
         start[q] = s;
     }
     out[kC4Hdr] = static_cast<uint8_t>(ph);
     out[kC4Hdr + 1] = start[1], out[kC4Hdr + 2] = start[2], out[kC4Hdr + 3] = start[3];
-    out[kC4Hdr + 4] = static_cast<uint8_t>(esc.size());
-    for (size_t e = 0; e < esc.size(); ++e) {
-        const uint16_t i16 = static_cast<uint16_t>(esc[e].i);
-        std::memcpy(out + kC4Esc + 4 * e, &i16, 2);
-        std::memcpy(out + kC4Esc + 4 * e + 2, &esc[e].v, 2);
+    out[kC4Hdr + 4] = static_cast<uint8_t>(hard.size());
+    out[kC4Hdr + 5] = static_cast<uint8_t>(recs.size());
+    std::memcpy(out + kC4QMask, qmask, 16);
+    for (size_t e = 0; e < recs.size(); ++e) std::memcpy(out + kC4Ent + 4 * e, &recs[e], 4);
+    const size_t h0 = kC4Ent + 4 * recs.size();
+    for (size_t e = 0; e < hard.size(); ++e) {
+        const uint16_t i16 = static_cast<uint16_t>(hard[e].i);
+        std::memcpy(out + h0 + 4 * e, &i16, 2);
+        std::memcpy(out + h0 + 4 * e + 2, &hard[e].v, 2);
     }
     return true;
 }
@@ -224,22 +255,32 @@ void codec4_decode_rows_tile(const uint8_t* enc, uint8_t* packed) {
     uint16_t w[8192];
     const uint8_t* table = enc + kC4Table;
     const int ph = enc[kC4Hdr];
+    const int n_hard = enc[kC4Hdr + 4], n_rec = enc[kC4Hdr + 5];
+    uint32_t qmask[4];
+    std::memcpy(qmask, enc + kC4QMask, 16);
+    int rec = 0;
     for (uint32_t r = 0; r < 128; ++r) {
-        uint32_t words[6];
+        uint32_t words[6], um = 0, X = 0;
+        if ((qmask[r / 32] >> (r % 32)) & 1u) {
+            uint32_t v;
+            std::memcpy(&v, enc + kC4Ent + 4 * rec++, 4);
+            um = v & 0xffffu, X = (v >> 16) & 0xffu;
+        }
         for (uint32_t m = 0; m < 6; ++m) std::memcpy(&words[m], enc + kC4Codes + (m * 128 + r) * 4, 4);
         for (uint32_t k = 0; k < 64; ++k) {
             const uint32_t i = c4_index(r, k), c = c4_get(words, k);
-            const uint32_t hb = c == 7 ? enc[kC4Rows + r] : table[c];
+            const uint32_t hb = c < 7 ? table[c] : ((um >> (k >> 2)) & 1u) ? X : enc[kC4Rows + r];
             w[i] = static_cast<uint16_t>(((hb << 8) | enc[i]) - ph * 0x80);
         }
     }
-    const int n = enc[kC4Hdr + 4];
-    for (int e = 0; e < n; ++e) {
+    const uint8_t* hard = enc + kC4Ent + 4 * n_rec;
+    for (int e = 0; e < n_hard; ++e) {
         uint16_t i16, v;
-        std::memcpy(&i16, enc + kC4Esc + 4 * e, 2);
-        std::memcpy(&v, enc + kC4Esc + 4 * e + 2, 2);
+        std::memcpy(&i16, hard + 4 * e, 2);
+        std::memcpy(&v, hard + 4 * e + 2, 2);
         w[i16] = v;
     }
+    (void)rec;
     packed_from_rows(w, packed);
 }
 

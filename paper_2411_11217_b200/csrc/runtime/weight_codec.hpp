@@ -64,26 +64,31 @@ namespace mlt {
 // ---- codec 4: 3-bit code (GemmArgs::codec = 4, kernels/gemm_tc.cu) --------
 // Same row-plane weight order and TMEM-operand engine as codec 3, 11 stored
 // bits per weight instead of 12.  A per-tile phase ph in {0, 1} shifts every
-// weight by ph * 0x80 (one exponent step; ph = 1 pairs binades (2m-1, 2m)
+// weight by ph * 0x80 (one exponent step: ph = 1 pairs binades (2m-1, 2m)
 // instead of (2m, 2m+1), whichever leaves fewer weights outside the table):
-// w' = w + ph * 0x80.  Stored: w' low byte raw, a 3-bit index of w' high
-// byte into an 8-entry table whose slot 7 each row may override with its own
-// byte (the row's most frequent out-of-table high byte), and the weights that
-// still miss ("slow escapes") as {index, bf16} entries.  Layout:
+// w' = w + ph * 0x80.  Stored: w' low byte raw and a 3-bit index of w' high
+// byte: slots 0-6 into the tile's table of its most frequent high bytes, slot
+// 7 into the row's override byte R_r, except inside the 4-weight units a row
+// record flags, where slot 7 means the record's byte X_r (a second per-row
+// value).  Weights that still miss are "hard" escapes {index, bf16}.  Layout:
 //   [0, 8192)       low byte of w'_i (i = ((k / 16) * 128 + r) * 16 + k % 16)
 //   [8192, 11264)   codes: u32 word m (0..5) of row r at 8192 + (m * 128 + r) * 4;
 //                   for H = m / 3, words A, B, C = 3H, 3H+1, 3H+2: nibble n
 //                   (bits 4n..4n+2) holds the code of k = 32H + n (A),
 //                   32H + 8 + n (B), 32H + 16 + n (C); bit 4n+3 of A, B, C
 //                   holds bit 0, 1, 2 of the code of k = 32H + 24 + n
-//   [11264, 11392)  per-row byte for slot 7
-//   [11392, 11400)  table[8] of high bytes
-//   [11400, 11404)  {phase, start of quarter 1, 2, 3} (u8; escapes sorted by quarter r / 32)
-//   [11404, 11408)  {n escapes (u8), 0, 0, 0}
-//   [11408, 11600)  n <= 48 escapes {u16 index i, u16 bf16 value w_i}
-// Decoding: w_i = (table'[code] << 8 | low) - ph * 0x80, then escapes.
+//   [11264, 11392)  R_r, per row
+//   [11392, 11400)  table[8] (slot 7 unused by the decoder)
+//   [11400, 11404)  {phase, first hard escape of row quarter 1, 2, 3} (u8)
+//   [11404, 11408)  {n_hard, n_rec, 0, 0} (u8)
+//   [11408, 11424)  u32 per row quarter: bit l = row 32q + l has a record
+//   [11424, ...)    n_rec records in row order {u16 unit mask (bit u: k in
+//                   [4u, 4u+4)), u8 X_r, u8 0}, then n_hard hard escapes
+//                   {u16 index i, u16 bf16 w_i} in row order;
+//                   n_rec + n_hard <= 44
+// Decoding: w_i = (slot byte << 8 | low) - ph * 0x80, then hard escapes.
 constexpr int kCodec4TileBytes = 11600;
-constexpr int kCodec4MaxEscapes = 48;
+constexpr int kCodec4MaxEntries = 44;  // records + hard escapes per tile
 bool codec4_encode_rows_tile(const uint8_t* packed16k, uint8_t* out);
 void codec4_decode_rows_tile(const uint8_t* enc, uint8_t* packed16k);
 

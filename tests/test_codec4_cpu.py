@@ -58,19 +58,33 @@ def np_decode4(enc):
                 codes[:, k] |= ((words[3 * H + b] >> (4 * n + 3)) & 1) << b
     table = enc[11392:11400]
     ph = int(enc[11400])
-    rowb = enc[11264:11392]
-    hi = np.where(codes == 7, rowb[:, None], table[np.minimum(codes, 7)]).astype(np.uint32)
+    n_hard, n_rec = int(enc[11404]), int(enc[11405])
+    qmask = enc[11408:11424].view(np.uint32)
+    slot7 = np.repeat(enc[11264:11392][:, None], 64, axis=1).astype(np.uint32)   # R_r
+    rec = 0
+    for r in range(128):
+        if (int(qmask[r // 32]) >> (r % 32)) & 1:
+            v = int(enc[11424 + 4 * rec:11428 + 4 * rec].view(np.uint32)[0])
+            rec += 1
+            for u in range(16):
+                if (v >> u) & 1:
+                    slot7[r, 4 * u:4 * u + 4] = (v >> 16) & 0xFF                     # X_r in flagged units
+    assert rec == n_rec and n_rec + n_hard <= 44
+    hi = np.where(codes == 7, slot7, table[np.minimum(codes, 6)]).astype(np.uint32)
     lo = enc[:8192][ROW_PLANE].astype(np.uint32)
     w = ((hi << 8 | lo) - ph * 0x80).astype(np.uint16)
-    n = int(enc[11404])
-    starts = [0, int(enc[11401]), int(enc[11402]), int(enc[11403]), n]
+    starts = [0, int(enc[11401]), int(enc[11402]), int(enc[11403]), n_hard]
     assert starts == sorted(starts)
-    for e in range(n):
-        i = int(enc[11408 + 4 * e:11410 + 4 * e].view(np.uint16)[0])
-        v = enc[11410 + 4 * e:11412 + 4 * e].view(np.uint16)[0]
+    h0 = 11424 + 4 * n_rec
+    prev = None
+    for e in range(n_hard):
+        i = int(enc[h0 + 4 * e:h0 + 4 * e + 2].view(np.uint16)[0])
+        v = enc[h0 + 4 * e + 2:h0 + 4 * e + 4].view(np.uint16)[0]
         r, k = (i >> 4) & 127, (i >> 11) * 16 + (i & 15)
         q = r // 32
-        assert starts[q] <= e < starts[q + 1]       # quarter-sorted
+        assert starts[q] <= e < starts[q + 1]       # sorted by row quarter
+        assert prev is None or (r, k) > prev        # then row, column
+        prev = (r, k)
         w[r, k] = v
     return w
 
@@ -102,9 +116,9 @@ def test_roundtrip_synthetic_mixtral(K, fan):
     esc = []
     for t in range(tiles):
         enc = out[t * TILE4:(t + 1) * TILE4]
-        esc.append(int(enc[11404]))
+        esc.append(int(enc[11404]) + int(enc[11405]))
         assert np.array_equal(np_decode4(enc.tobytes()), tile_weights(packed[t * 16384:(t + 1) * 16384]))
-    assert max(esc) <= 36, esc
+    assert max(esc) <= 36, esc          # records + hard escapes, of 44
     back = np.zeros_like(packed)
     K.codec4_decode_rows(out.ctypes.data_as(C.c_void_p), tiles, back.ctypes.data_as(C.c_void_p))
     assert np.array_equal(back, packed)
@@ -138,9 +152,9 @@ def test_edge_tiles(K):
 
 
 def test_phase_and_row_override(K):
-    """A tile whose binades straddle the high-byte pairing picks phase 1, and a
+    """A tile whose binades straddle the high-byte pairing picks phase 1; a
     row whose out-of-table weights share one high byte codes them through its
-    slot-7 override instead of escapes."""
+    slot-7 byte, a second value goes to a unit record, not to escapes."""
     rng = np.random.default_rng(8)
     a = 1.5 * 2.0 ** -7                      # top binade alone in its pair at phase 0
     w = bf16(rng.uniform(-a, a, (128, 64)))
@@ -151,10 +165,13 @@ def test_phase_and_row_override(K):
     assert np.array_equal(np_decode4(enc.tobytes()), tile_weights(packed[:16384]))
     w2 = bf16(rng.uniform(-0.02, 0.02, (128, 64)))
     w2[9, :6] = bf16(np.full(6, 2.0 ** -30))          # six equal tiny weights in row 9
+    w2[9, 40:42] = bf16(np.full(2, -(2.0 ** -33)))     # and a second tiny value in one unit
     packed2 = pack(K, w2, 128, 64)
     out2, _, _ = encode4(K, packed2, 128, 64)
     enc2 = out2[:TILE4]
     assert np.array_equal(np_decode4(enc2.tobytes()), tile_weights(packed2[:16384]))
-    n = int(enc2[11404])
-    rows = [((int(enc2[11408 + 4 * e]) | int(enc2[11409 + 4 * e]) << 8) >> 4) & 127 for e in range(n)]
+    n_hard, n_rec = int(enc2[11404]), int(enc2[11405])
+    h0 = 11424 + 4 * n_rec
+    rows = [((int(enc2[h0 + 4 * e]) | int(enc2[h0 + 1 + 4 * e]) << 8) >> 4) & 127 for e in range(n_hard)]
     assert 9 not in rows
+    assert (int(enc2[11408:11412].view(np.uint32)[0]) >> 9) & 1     # row 9 holds a unit record

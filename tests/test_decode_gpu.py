@@ -318,7 +318,7 @@ def test_weight_codec_decode_bitwise_equal(prompt, dims, r_w, a_g, budget, mode)
     assert np.array_equal(x0.view(np.uint32), x1.view(np.uint32))
     if r_w < 1.0:
         ratio = 11600 / 16384 if mode == "4" else 12432 / 16384
-        assert s1 < (ratio + 0.02) * s0 and b1 < (ratio + 0.02) * b0
+        assert s1 < (ratio + 0.04) * s0 and b1 < (ratio + 0.04) * b0  # + block-granular residency
 
 
 @pytest.mark.parametrize("dims,r_w,a_g,budget", [(TINY, 0.3, 0, 4e9), (W8X7B, 0.10, 0, 7e9)])

@@ -39,6 +39,12 @@ def rand_bf16(*shape, scale=1.0, gen=None):
     return (torch.randn(*shape, generator=gen) * scale).to(torch.bfloat16)
 
 
+def unif_bf16(*shape, scale=1.0, gen=None):
+    """uniform(-sqrt3 s, sqrt3 s): the runtime's synthetic-weight distribution
+    (the 3-bit code, codec 4, falls back to raw blocks on Gaussian tiles)."""
+    return ((torch.rand(*shape, generator=gen) * 2 - 1) * (3 ** 0.5 * scale)).to(torch.bfloat16)
+
+
 def bf16_bits(t):  # torch bf16 -> numpy uint16 view
     return t.contiguous().view(torch.int16).numpy().view(np.uint16)
 
@@ -113,12 +119,13 @@ def test_split_k_and_chunked_gemm(K, T, M, Kd, splits, chunks, n_cap):
     assert (got - ref).abs().max().item() <= 2e-3 * max(1.0, ref.abs().max().item())
 
 
-def _expert_setup(T, H, Fd, E, Kk, seed):
+def _expert_setup(T, H, Fd, E, Kk, seed, uniform=False):
     g = torch.Generator().manual_seed(seed)
     hn = rand_bf16(T, H, gen=g)
-    w1 = [rand_bf16(Fd, H, scale=H ** -0.5, gen=g) for _ in range(E)]
-    w3 = [rand_bf16(Fd, H, scale=H ** -0.5, gen=g) for _ in range(E)]
-    w2 = [rand_bf16(H, Fd, scale=Fd ** -0.5, gen=g) for _ in range(E)]
+    wf = unif_bf16 if uniform else rand_bf16
+    w1 = [wf(Fd, H, scale=H ** -0.5, gen=g) for _ in range(E)]
+    w3 = [wf(Fd, H, scale=H ** -0.5, gen=g) for _ in range(E)]
+    w2 = [wf(H, Fd, scale=Fd ** -0.5, gen=g) for _ in range(E)]
     wr = rand_bf16(E, H, scale=H ** -0.5, gen=g)
     return hn, w1, w3, w2, wr
 
@@ -450,7 +457,7 @@ def test_codec_gemm_bitwise_equals_raw(K, T, M, Kd, n_cap, splits, resid, codec)
     """The GEMM on encoded weights (decoder warps expand tiles in smem) returns
     the same bits as on raw bf16 tiles: dense fp32 epilogue, split-K, residual."""
     g = torch.Generator().manual_seed(T + M + Kd)
-    w = rand_bf16(M, Kd, scale=Kd ** -0.5, gen=g)
+    w = (unif_bf16 if codec == 4 else rand_bf16)(M, Kd, scale=Kd ** -0.5, gen=g)
     x = rand_bf16(T, Kd, gen=g)
     R = (T + 15) // 16 * 16
     raw_dev, raw_blocks = pack_weight_dev(K, w)  # keep the buffers alive while the GEMMs read them
@@ -478,7 +485,7 @@ def test_codec_gemm_bitwise_equals_raw(K, T, M, Kd, n_cap, splits, resid, codec)
 def test_codec_expert_ffn_bitwise_equals_raw(K, T, H, Fd, E, Kk, n_cap, codec):
     """Grouped gate/up (two encoded matrices, fused SiLU -> packed bf16) and
     down on encoded experts == the raw-tile GEMMs, bit for bit."""
-    hn, w1, w3, w2, wr = _expert_setup(T, H, Fd, E, Kk, seed=T + H + 1)
+    hn, w1, w3, w2, wr = _expert_setup(T, H, Fd, E, Kk, seed=T + H + 1, uniform=codec == 4)
     hn_d, wr_d = hn.cuda(), wr.cuda()
     idx = torch.zeros(T, Kk, dtype=torch.int32, device="cuda")
     wts = torch.zeros(T, Kk, device="cuda")
@@ -530,7 +537,7 @@ def test_codec3_escapes_and_raw_blocks(K, T, M, Kd, n_cap, splits, codec):
     row blocks the code cannot hold stored raw (tagged pointers), plus a
     forced raw block — bit-equal to the raw-tile GEMM."""
     g = torch.Generator().manual_seed(M + Kd + 3)
-    w = rand_bf16(M, Kd, scale=Kd ** -0.5, gen=g)
+    w = (unif_bf16 if codec == 4 else rand_bf16)(M, Kd, scale=Kd ** -0.5, gen=g)
     # sparse outliers: a few per tile in rows 0..127 -> escapes; a wide
     # spread in the last row block -> more than 31 escapes -> raw
     nout = M * Kd // 2048

@@ -39,14 +39,18 @@ def main():
                     help="fragment-order encoded tiles, register decode + mma.sync (gemm_codec.cu)")
     ap.add_argument("--codec3", action="store_true",
                     help="row-plane encoded tiles decoded into TMEM, MMA with A from TMEM (gemm_tc codec 3)")
+    ap.add_argument("--codec4", action="store_true",
+                    help="3-bit row-plane tiles (11600 B) on the TMEM-operand engine (gemm_tc codec 4)")
+    ap.add_argument("--only", default="", help="comma-separated case-name prefixes to run")
     ap.add_argument("--ncap-e", type=int, default=0, help="expert GEMM token tile (0: the runtime's min(128, Rmu))")
     ap.add_argument("--no-stream-k", action="store_true", help="gate/up without the stream-K tail")
     ap.add_argument("--dec-groups", type=int, default=0, help="codec decoder groups (0: default)")
     ap.add_argument("--down-splits", type=int, default=0,
                     help="K-splits of the down GEMM (0: the runtime's auto choice, 4 with --codec at 8x7B)")
     a = ap.parse_args()
-    if a.codec2 or a.codec3:
+    if a.codec2 or a.codec3 or a.codec4:
         a.codec = True
+    TB = 11600 if a.codec4 else 12432
     mu = a.mu
     KD = capi.load_kernels()
     s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -63,7 +67,7 @@ def main():
             tab = [w.data_ptr() + (m * E + e) * per + rb * 128 * k * 2
                    for m in range(n_mats) for e in range(E) for rb in range(rows // 128)]
             return w, torch.tensor(tab, dtype=torch.int64, device="cuda")
-        per = rows // 128 * (k // 64) * 12432
+        per = rows // 128 * (k // 64) * TB
         enc = np.zeros(n_mats * E * per, np.uint8)
         g = torch.Generator().manual_seed(rows + k)
         for i in range(n_mats * E):
@@ -72,7 +76,10 @@ def main():
             src = w.view(torch.int16).numpy().view(np.uint16)
             packed = np.empty_like(src)
             KD.pack_weight(src.ctypes.data_as(C.c_void_p), rows, k, packed.ctypes.data_as(C.c_void_p))
-            if a.codec3:
+            if a.codec4:
+                assert KD.codec4_encode_rows(packed.ctypes.data_as(C.c_void_p), rows, k,
+                                             enc[i * per:(i + 1) * per].ctypes.data_as(C.c_void_p), None) == 0
+            elif a.codec3:
                 assert KD.codec_encode_rows(packed.ctypes.data_as(C.c_void_p), rows, k,
                                             enc[i * per:(i + 1) * per].ctypes.data_as(C.c_void_p), None) == 0
             elif a.codec2:
@@ -82,7 +89,7 @@ def main():
                 KD.codec_encode(packed.ctypes.data_as(C.c_void_p), rows, k,
                                 enc[i * per:(i + 1) * per].ctypes.data_as(C.c_void_p))
         dev = torch.from_numpy(enc).cuda()
-        tab = [dev.data_ptr() + i * per + rb * (k // 64) * 12432
+        tab = [dev.data_ptr() + i * per + rb * (k // 64) * TB
                for i in range(n_mats * E) for rb in range(rows // 128)]
         return dev, torch.tensor(tab, dtype=torch.int64, device="cuda")
 
@@ -109,7 +116,7 @@ def main():
     inter = torch.zeros(R * F, dtype=torch.int16, device="cuda")
     # runtime.cpp expert_down_splits auto (8 x 32 tiles over 148 SMs; 2 CTAs per SM with codec 2)
     ds = a.down_splits or (8 if a.codec2 else 4 if a.codec else 1)
-    cmode = 2 if a.codec2 else 3 if a.codec3 else int(a.codec)
+    cmode = 2 if a.codec2 else 3 if a.codec3 else 4 if a.codec4 else int(a.codec)
     y = torch.zeros(ds * R, H, device="cuda")
     xo = torch.zeros(mu, H, device="cuda")
     Rmu = (mu + 15) // 16 * 16
@@ -224,6 +231,8 @@ def main():
             for _ in range(12):
                 hdst.copy_(hsrc, non_blocking=True)
     for name, fn, nbytes in cases:
+        if a.only and not any(name.startswith(p) for p in a.only.split(",")):
+            continue
         for _ in range(2 if not a.once else 0):
             fn()
         st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -239,7 +248,7 @@ def main():
         extra = ""
         if a.codec and name.startswith("expert"):  # bytes actually read: encoded weight tiles
             wb = touched * {"expert_ffn": 3, "expert gate/up gemm": 2, "expert down gemm": 1}[name.split(" (")[0]] * H * F * 2
-            stored = nbytes - wb + wb * 12432 // 16384
+            stored = nbytes - wb + wb * TB // 16384
             out[name].update(stored_bytes=stored, stored_GBps=stored / (ms * 1e-3) / 1e9,
                              stored_frac_hbm=stored / (ms * 1e-3) / 1e9 / peak)
             extra = f"  [encoded: {stored / 1e6:.1f} MB, {100 * out[name]['stored_frac_hbm']:.1f}% of HBM]"
