@@ -384,7 +384,9 @@ def hrm_kernels(cfg, hw, rep, prof, steps, tp=1, csv_path=None):
 def load_traffic(codec=False):
     """ncu dram read+write bytes per expert-FFN launch of the same kernels at the
     same shape (an ncu capture cannot run inside the timed bench): (bytes, file)."""
-    name = "expert_ffn_traffic_codec.json" if codec else "expert_ffn_traffic.json"
+    # codec 3 (4-bit code): expert_ffn_traffic_codec.json; codec 4 (3-bit, default): ..._codec4.json
+    name = ("expert_ffn_traffic_codec4.json" if CODEC_DT < 1.45 else "expert_ffn_traffic_codec.json") if codec \
+        else "expert_ffn_traffic.json"
     p = os.path.join(ROOT, "profiles", name)
     if os.path.exists(p):
         with open(p) as f:

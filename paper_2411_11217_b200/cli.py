@@ -50,13 +50,13 @@ HOST_FLOPS = 2.0e12   # host-core estimate (the measured box: 16 SPR cores)
 # stored bytes per weight with the weight codec (the runtime's default 3-bit
 # code, 11600 B per tile; 12432 B when MLT_CODEC_MODE selects engine 1-3)
 CODEC_DT = (12432 if os.environ.get("MLT_CODEC_MODE", "4")[:1] in ("1", "2", "3") else 11600) / 8192
-# The codec GEMM moves its stored bytes at ~75-84 % of the HBM peak (codec 3,
-# decode into TMEM: expert FFN 83.8 % at mu = 64, 74.4 % at mu = 256,
-# profiles/r02s2_codec_engines.txt; the bf16 GEMM: ~97 %), i.e. about the time
-# per weight of bf16 pages or less: the search sees the codec's GPU term at the
-# lower of those rates, or it would trade GPU time it does not have for link
+# The codec GEMM moves its stored bytes at ~62-84 % of the HBM peak (the
+# default 3-bit code, codec 4: expert FFN 62.8 % at mu = 64; the 4-bit code,
+# codec 3: 83.8 % at mu = 64, 74.4 % at mu = 256, profiles/r02s2_codec_engines.txt,
+# r02s3_codec4.txt; the bf16 GEMM: ~97 %): the search sees the codec's GPU term
+# at the engine's rate, or it would trade GPU time it does not have for link
 # bytes it saves.
-CODEC_GEMM_HBM_FRAC = 0.74
+CODEC_GEMM_HBM_FRAC = 0.74 if CODEC_DT > 1.45 else 0.62
 
 
 class CliError(Exception):
