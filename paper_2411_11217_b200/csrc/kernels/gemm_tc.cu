@@ -45,9 +45,15 @@ constexpr int kThreadsCodec = 192 + kDecWarpThreads;
 // codec 3: + warp 14, the token-tile (B) producer
 // codec 3: kTsGroups decoder groups of 4 warps (warps 6 .. 6 + 4 kTsGroups - 1)
 // + the token-tile (B) producer warp after them
-constexpr int kTsGroups = 3;
-constexpr int kTsBWarp = 6 + 4 * kTsGroups;
-constexpr int kThreadsCodec3 = 32 * (kTsBWarp + 1);
+// codec 3 runs 3 decoder groups (4 measured no faster, 80 registers); the
+// codec-4 decoder is more latency bound (dependent record loads) and gains
+// from 4 groups: expert FFN at mu = 64 487 -> 462 us (profiles/r02s3_codec4.txt)
+#ifndef MLT_TS_GROUPS_C4
+#define MLT_TS_GROUPS_C4 4
+#endif
+__host__ __device__ constexpr int ts_groups(int codec) { return codec == 4 ? MLT_TS_GROUPS_C4 : 3; }
+__host__ __device__ constexpr int ts_bwarp(int codec) { return 6 + 4 * ts_groups(codec); }
+__host__ __device__ constexpr int ts_threads(int codec) { return 32 * (ts_bwarp(codec) + 1); }
 constexpr int kCodecTile = 12432;   // encoded tile bytes (runtime/weight_codec.hpp)
 constexpr int kCodec4Tile = 11600;  // codec 4: 3-bit code (kCodec4TileBytes)
 __host__ __device__ constexpr int enc_tile_bytes(int codec) { return codec == 4 ? kCodec4Tile : kCodecTile; }
@@ -524,6 +530,7 @@ __device__ __forceinline__ void decoder_role_ts(const GemmArgs& a, const Ring3& 
                                                 uint32_t tmem) {
     const int w = static_cast<int>(threadIdx.x >> 5);
     const uint32_t lane = threadIdx.x & 31u;
+    constexpr int kTsGroups = ts_groups(kMode);
     const int grp = (w - 6) >> 2;    // tile t is decoded by group t % kTsGroups
     const uint32_t q = static_cast<uint32_t>(w) & 3u;  // TMEM lane quarter
     const uint32_t r = q * 32u + lane;
@@ -649,7 +656,7 @@ __device__ __forceinline__ void mma_role_ts(const GemmArgs& a, const Ring3& R, S
 // sweep in one kernel stalled on instruction fetch, ncu no_instruction 8.7
 // per issue vs 0.4)
 template <int kMode>
-__global__ void __launch_bounds__(kMode ? kThreadsCodec3 : kThreadsCodec, 1) gemm_tc_kernel(const GemmArgs a) {
+__global__ void __launch_bounds__(kMode ? ts_threads(kMode) : kThreadsCodec, 1) gemm_tc_kernel(const GemmArgs a) {
     constexpr bool kTs = kMode != 0;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1 KiB alignment for the SWIZZLE_128B atoms.
@@ -735,7 +742,7 @@ __global__ void __launch_bounds__(kMode ? kThreadsCodec3 : kThreadsCodec, 1) gem
         // ===== codec 3: decoupled rings (the epilogue below is shared) =====
         if (warp == 0) {
             if (lane == 0) producer_a_ts(a, R3, ctl, n_virtual, KB);
-        } else if (warp == kTsBWarp) {
+        } else if (warp == ts_bwarp(kMode)) {
             if (lane == 0) producer_b_ts(a, R3, ctl, n_virtual, KB);
         } else if (warp == 1) {
             mma_role_ts(a, R3, ctl, n_virtual, KB, tmem);
@@ -1078,9 +1085,10 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         // are multiples of the group count: every slot then belongs to one group,
         // which meets it phase after phase (a group skipping a phase of a slot it
         // shares could pass a parity wait one phase early: mbarrier parity aliases)
-        a.stages -= a.stages % kTsGroups;
-        a.t3_slots -= a.t3_slots % kTsGroups;
-        if (a.t3_slots < kTsGroups || a.stages < kTsGroups) return cudaErrorInvalidValue;
+        const int groups = ts_groups(a.codec);
+        a.stages -= a.stages % groups;
+        a.t3_slots -= a.t3_slots % groups;
+        if (a.t3_slots < groups || a.stages < groups) return cudaErrorInvalidValue;
         need += a.t3_slots * 32;
     }
     if (a.stages < 2) return cudaErrorInvalidValue;
@@ -1121,7 +1129,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
             if (!cache[dev][slot] &&
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache[dev][slot], kern,
-                                                              a.codec >= 3 ? kThreadsCodec3
+                                                              a.codec >= 3 ? ts_threads(a.codec)
                                                               : a.codec    ? kThreadsCodec
                                                                            : kThreadsRaw,
                                                               227 * 1024 - 1024) != cudaSuccess)
@@ -1133,7 +1141,7 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
     const int n_virtual = a.sk_parts ? a.sk_full + a.sk_tail * a.sk_parts : a.G * a.RB * a.n_chunks * a.k_splits;
     const int grid = n_virtual < num_sms ? n_virtual : num_sms;
     if (grid <= 0) return cudaSuccess;
-    const dim3 block(a.codec >= 3 ? kThreadsCodec3 : a.codec ? kThreadsCodec : kThreadsRaw);
+    const dim3 block(a.codec >= 3 ? ts_threads(a.codec) : a.codec ? kThreadsCodec : kThreadsRaw);
     if (a.sk_parts) {
         // cooperative: the driver guarantees co-residency of the whole grid or
         // refuses the launch (then: the same GEMM without the stream-K tail)
