@@ -114,7 +114,7 @@ def main():
             "measured_optimum": {k: best_meas[k] for k in ("mu", "A_g", "r_w", "hrm_bound_tok_s", "measured_tok_s")},
             "search_pick_within_pct_of_measured_best": 100 * best_model["measured_tok_s"] / best_meas["measured_tok_s"]}
     out = {"what": "HRM policy sweep, Mixtral-8x7B shape, N=256, prompt 512, 1x B200 (tools/hrm_sweep.py)"
-                   + (", weights encoded (weight codec, 12432 B per 16 KiB tile)" if a.codec else ""),
+                   + (f", weights encoded (weight codec, {bench.CODEC_DT * 8192:.0f} B per 16 KiB tile)" if a.codec else ""),
            "link_gbs": link[0], "host_read_gbs": host, "peaks_source": pk_src, "search_reserve_gb": RESERVE / 1e9,
            "decode_steps": a.steps, "rows": rows, "summary": summary}
     js = json.dumps(out, indent=1)
