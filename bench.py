@@ -151,7 +151,8 @@ def model_spec(cfg, stored=False):
     the reference's cost model must see."""
     from paper_2411_11217_b200 import capi
     l, h1, h2, nq, nkv, ne, k = cfg["model"]
-    return capi.ModelSpec(l, h1, h2, nq, nkv, ne, k, CODEC_DT if stored and cfg.get("codec") else 2.0, 2.0)
+    dt = cfg.get("stored_dt", CODEC_DT)  # after runtime creation: the bytes per weight it actually stores
+    return capi.ModelSpec(l, h1, h2, nq, nkv, ne, k, dt if stored and cfg.get("codec") else 2.0, 2.0)
 
 
 def node_host(host_gbs, tp, per_slice_host):
@@ -309,9 +310,10 @@ def expert_roofline(cfg, rep, pk, traffic_src, tp=1):
     mu = cfg["mu"]
     wbytes = ne * 3 * h1 * (h2 // tp) * 2
     tokens = mu * k * 2 * h1 * 2 + mu * h1 * 2
-    # --codec: the kernel must read the encoded tiles (CODEC_DT bytes/weight),
-    # so those are the bytes that bound it; the bf16 figure is reported beside
-    stored = wbytes * CODEC_DT / 2 if cfg.get("codec") else wbytes
+    # --codec: the kernel must read the encoded tiles (the runtime's stored
+    # bytes/weight, ~CODEC_DT), so those are the bytes that bound it; the bf16
+    # figure is reported beside
+    stored = wbytes * cfg.get("stored_dt", CODEC_DT) / 2 if cfg.get("codec") else wbytes
     bytes_launch = stored + tokens
     # in-kernel %globaltimer span of the gate/up and down GEMMs of each launch
     # (CUDA-event deltas on the mostly idle compute stream would add host-launch gaps)
@@ -507,6 +509,11 @@ def run_mlt(args, cfg):
             json.dump(rt.timeline(), fh)
     value = cfg["N"] * args.steps / dev_s        # device-timed (CUDA events), whole job
     e2e = cfg["N"] * args.steps / wall_s         # wall clock around the C-ABI call
+    if cfg.get("codec"):
+        # the bound of the executed run sees the stored bytes per weight the runtime
+        # reports: raw-fallback blocks, or the 12-bit code when the 11-bit one does
+        # not fit the weights, stream more than the search's CODEC_DT assumed
+        cfg["stored_dt"] = info.bytes_per_weight
     bound = hrm_bound(cfg, link_gbs, host_gbs, pk, tp=tp, per_slice_host=args.tp_shard > 1)
     # the bf16-weight bound at the raw policy: the best the unencoded stream could do
     bound_bf16 = hrm_bound(dict(cfg, codec=False, r_w=raw_rw), link_gbs, host_gbs, pk, tp=tp,
@@ -539,7 +546,9 @@ def run_mlt(args, cfg):
                 "weight_gates": args.gates,
                 "l2": "weights streamed per step (>> 126 MB L2): no flush needed"},
         "hrm": {"bound_tok_s": bound.decode_throughput, "frac": value / bound.decode_throughput,
-                "weight_bytes_per_param": CODEC_DT if cfg.get("codec") else 2.0,
+                "weight_bytes_per_param": cfg.get("stored_dt", CODEC_DT) if cfg.get("codec") else 2.0,
+                "weight_bytes_per_param_searched": CODEC_DT if cfg.get("codec") else 2.0,
+                "raw_fallback_blocks_per_layer": info.raw_blocks,
                 "bound_bf16_weights_tok_s": bound_bf16.decode_throughput,
                 "value_over_bf16_bound": value / bound_bf16.decode_throughput,
                 "binding": binding, "link_gbs_measured": link_gbs, "host_read_gbs_measured": host_gbs,

@@ -333,6 +333,13 @@ int mlt_codec4_encode_rows(const uint8_t* host_packed, int64_t M, int64_t K, uin
                            uint8_t* raw_blocks);
 int mlt_codec4_decode_rows(const uint8_t* host_enc, int64_t tiles, uint8_t* host_packed);
 int mlt_codec4_tile_bytes(void);
+/* Capacity variants: cap records + escapes per tile (<= 200), tiles of
+ * mlt_codec4_tile_bytes_for(cap) = 11424 + 4 cap rounded up to 16 bytes (the
+ * runtime sizes cap per weight kind); decode_rows_cap reads such tiles. */
+int mlt_codec4_encode_rows_cap(const uint8_t* host_packed, int64_t M, int64_t K, int32_t cap, uint8_t* host_out,
+                               uint8_t* raw_blocks);
+int mlt_codec4_decode_rows_cap(const uint8_t* host_enc, int64_t tiles, int32_t cap, uint8_t* host_packed);
+int mlt_codec4_tile_bytes_for(int32_t cap);
 /* 16 KiB packed tiles -> fragment-order bf16 tiles (raw codec-2 blocks). */
 int mlt_frag_pack(const uint8_t* host_packed, int64_t tiles, uint8_t* host_out);
 /* Host-core GQA decode attention (A_g = 0: the CpuAttn task, pipesim.hpp:26,
@@ -400,6 +407,8 @@ typedef struct mlt_gemm_args_t {
     int32_t dec_groups;        /* codec 1: decoder groups of 4 warps (2; 0 -> the default) */
     int32_t codec_raw;         /* codec 2: 1 when a page-table entry may carry tag bit 0 (a raw
                                   fragment-order block, mlt_codec_encode_frag raw_blocks) */
+    int32_t enc_tile;          /* codec 4: bytes per encoded tile (mlt_codec4_tile_bytes_for(cap));
+                                  0 -> 11600 (the default capacity, mlt_codec4_encode_rows) */
 } mlt_gemm_args_t;
 
 /* Grouped swap-AB tcgen05 GEMM (SURVEY.md §2c expert_gateup_silu /

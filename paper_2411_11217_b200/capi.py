@@ -566,7 +566,7 @@ class GemmArgs(C.Structure):
                 ("n_chunks", C.c_int32), ("k_splits", C.c_int32), ("split_stride", C.c_int64),
                 ("trace", C.c_void_p), ("codec", C.c_int32), ("ktrace", C.c_void_p),
                 ("sk_scratch", C.c_void_p), ("sk_count", C.c_void_p), ("sk_rows", C.c_int32),
-                ("dec_groups", C.c_int32), ("codec_raw", C.c_int32)]
+                ("dec_groups", C.c_int32), ("codec_raw", C.c_int32), ("enc_tile", C.c_int32)]
 
 
 V, I, F = C.c_void_p, C.c_int, C.c_float
@@ -579,6 +579,9 @@ _KSIGS = {
     "codec4_encode_rows": [V, C.c_int64, C.c_int64, V, V],
     "codec4_decode_rows": [V, C.c_int64, V],
     "codec4_tile_bytes": [],
+    "codec4_encode_rows_cap": [V, C.c_int64, C.c_int64, I, V, V],
+    "codec4_decode_rows_cap": [V, C.c_int64, I, V],
+    "codec4_tile_bytes_for": [I],
     "frag_pack": [V, C.c_int64, V],
     "host_gqa_decode": [V, V, V, V, I, I, I, I, I, V, I],
     "host_gqa_use_amx": [I],

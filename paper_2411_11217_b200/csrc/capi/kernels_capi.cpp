@@ -18,6 +18,10 @@
 #include "../runtime/host_layout.hpp"
 #include "../runtime/host_gqa.hpp"
 #include "../runtime/weight_codec.hpp"
+
+#include <algorithm>
+#include <functional>
+#include <vector>
 #include "lightplan/pipesim.hpp"
 #include "lightplan/planner.hpp"
 #include "lightplan/batcher.hpp"
@@ -81,6 +85,7 @@ mltk::GemmArgs to_args(const mlt_gemm_args_t* a) {
     g.sk_rows = a->sk_rows;
     if (a->dec_groups > 0) g.dec_groups = a->dec_groups;
     g.codec_raw = a->codec_raw;
+    g.enc_tile = a->enc_tile;
     return g;
 }
 
@@ -126,7 +131,7 @@ int mlt_codec_tile_bytes(void) { return mlt::kCodecTileBytes; }
 // engine's raw layout), its flag set in raw_blocks; without raw_blocks such
 // a block is an error.  Returns the number of raw blocks.
 static int encode_blocks(const char* what, const uint8_t* packed, int64_t M, int64_t K, uint8_t* out,
-                         uint8_t* raw_blocks, bool (*enc)(const uint8_t*, uint8_t*),
+                         uint8_t* raw_blocks, const std::function<bool(const uint8_t*, uint8_t*)>& enc,
                          void (*raw_tile)(const uint8_t*, uint8_t*), int tile_bytes = mlt::kCodecTileBytes,
                          int max_escapes = mlt::kCodecMaxEscapes) {
     if (M % 128 || K % 64 || M <= 0 || K <= 0) throw std::invalid_argument(std::string(what) + ": M%128, K%64");
@@ -136,7 +141,8 @@ static int encode_blocks(const char* what, const uint8_t* packed, int64_t M, int
     int bad = 0;
 #pragma omp parallel for schedule(static) reduction(+ : bad)
     for (int64_t r = 0; r < rbs; ++r) {
-        uint8_t tmp[mlt::kCodecTileBytes > mlt::kCodec4TileBytes ? mlt::kCodecTileBytes : mlt::kCodec4TileBytes];
+        std::vector<uint8_t> tmp_v(std::max(mlt::kCodecTileBytes, mlt::codec4_tile_bytes(mlt::kCodec4CapLimit)));
+        uint8_t* tmp = tmp_v.data();
         for (int64_t t = 0; t < kb; ++t)
             if (!enc(packed + (r * kb + t) * 16384, tmp)) {
                 raw[r] = 1;
@@ -177,23 +183,36 @@ int mlt_codec_encode_rows(const uint8_t* packed, int64_t M, int64_t K, uint8_t* 
     });
 }
 
-int mlt_codec4_encode_rows(const uint8_t* packed, int64_t M, int64_t K, uint8_t* out, uint8_t* raw_blocks) {
+int mlt_codec4_encode_rows_cap(const uint8_t* packed, int64_t M, int64_t K, int32_t cap, uint8_t* out,
+                               uint8_t* raw_blocks) {
     return guard([&] {
-        return encode_blocks("codec4_encode_rows", packed, M, K, out, raw_blocks, mlt::codec4_encode_rows_tile,
+        if (cap < 0 || cap > mlt::kCodec4CapLimit) throw std::invalid_argument("codec4_encode_rows: cap in [0, 200]");
+        return encode_blocks("codec4_encode_rows", packed, M, K, out, raw_blocks,
+                             [cap](const uint8_t* a, uint8_t* b) { return mlt::codec4_encode_rows_tile(a, b, cap); },
                              [](const uint8_t* src, uint8_t* dst) { std::memcpy(dst, src, 16384); },
-                             mlt::kCodec4TileBytes, mlt::kCodec4MaxEntries);
+                             mlt::codec4_tile_bytes(cap), cap);
     });
 }
 
-int mlt_codec4_decode_rows(const uint8_t* enc, int64_t tiles, uint8_t* packed) {
+int mlt_codec4_encode_rows(const uint8_t* packed, int64_t M, int64_t K, uint8_t* out, uint8_t* raw_blocks) {
+    return mlt_codec4_encode_rows_cap(packed, M, K, mlt::kCodec4MaxEntries, out, raw_blocks);
+}
+
+int mlt_codec4_decode_rows_cap(const uint8_t* enc, int64_t tiles, int32_t cap, uint8_t* packed) {
     return guard([&] {
-        for (int64_t t = 0; t < tiles; ++t)
-            mlt::codec4_decode_rows_tile(enc + t * mlt::kCodec4TileBytes, packed + t * 16384);
+        if (cap < 0 || cap > mlt::kCodec4CapLimit) throw std::invalid_argument("codec4_decode_rows: cap in [0, 200]");
+        const int tb = mlt::codec4_tile_bytes(cap);
+        for (int64_t t = 0; t < tiles; ++t) mlt::codec4_decode_rows_tile(enc + t * tb, packed + t * 16384);
         return MLT_OK;
     });
 }
 
+int mlt_codec4_decode_rows(const uint8_t* enc, int64_t tiles, uint8_t* packed) {
+    return mlt_codec4_decode_rows_cap(enc, tiles, mlt::kCodec4MaxEntries, packed);
+}
+
 int mlt_codec4_tile_bytes(void) { return mlt::kCodec4TileBytes; }
+int mlt_codec4_tile_bytes_for(int32_t cap) { return mlt::codec4_tile_bytes(cap); }
 
 int mlt_frag_pack(const uint8_t* packed, int64_t tiles, uint8_t* out) {
     return guard([&] {

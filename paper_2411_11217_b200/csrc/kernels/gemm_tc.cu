@@ -55,8 +55,10 @@ __host__ __device__ constexpr int ts_groups(int codec) { return codec == 4 ? MLT
 __host__ __device__ constexpr int ts_bwarp(int codec) { return 6 + 4 * ts_groups(codec); }
 __host__ __device__ constexpr int ts_threads(int codec) { return 32 * (ts_bwarp(codec) + 1); }
 constexpr int kCodecTile = 12432;   // encoded tile bytes (runtime/weight_codec.hpp)
-constexpr int kCodec4Tile = 11600;  // codec 4: 3-bit code (kCodec4TileBytes)
-__host__ __device__ constexpr int enc_tile_bytes(int codec) { return codec == 4 ? kCodec4Tile : kCodecTile; }
+constexpr int kCodec4Tile = 11600;  // codec 4 at the default capacity (GemmArgs::enc_tile)
+__host__ __device__ inline int enc_tile_bytes(const GemmArgs& a) {
+    return a.codec == 4 ? (a.enc_tile ? a.enc_tile : kCodec4Tile) : kCodecTile;
+}
 // codec: an encoded tile lands at the END of its 16 KiB A slot and is
 // expanded in place (every input is in registers before any output store)
 constexpr int kCodecOff = kATileBytes - kCodecTile;  // 3952, 16-byte aligned
@@ -483,7 +485,7 @@ __device__ __forceinline__ void producer_a_ts(const GemmArgs& a, const Ring3& R,
         for (int mt = 0; mt < a.n_mats; ++mt) {
             bool raw;
             ab[mt] = untag(a.a_table[(static_cast<int64_t>(mt) * a.G + tk.g) * a.RB + tk.rb], raw);
-            tile_b[mt] = raw ? kATileBytes : enc_tile_bytes(a.codec);
+            tile_b[mt] = raw ? kATileBytes : enc_tile_bytes(a);
         }
         for (int n0 = tk.c * a.n_cap; n0 < rows; n0 += a.n_chunks * a.n_cap)
             for (int kb = tk.kb0; kb < tk.kb1; ++kb)
@@ -720,7 +722,7 @@ __global__ void __launch_bounds__(kMode ? ts_threads(kMode) : kThreadsCodec, 1) 
         for (int mt = 0; mt < a.n_mats; ++mt) {
             bool raw;
             const uint8_t* p = untag(a.a_table[(static_cast<int64_t>(mt) * a.G + g) * a.RB + rb], raw);
-            const int tile = (a.codec && !raw) ? enc_tile_bytes(a.codec) : kATileBytes;
+            const int tile = (a.codec && !raw) ? enc_tile_bytes(a) : kATileBytes;
             prefetch_l2(p + static_cast<int64_t>(kb0) * tile, static_cast<uint32_t>(nkb * tile));
         }
     }
@@ -1074,7 +1076,9 @@ cudaError_t launch_gemm(GemmArgs a, int num_sms, cudaStream_t stream) {
         // of smem, TMEM A slots (32 columns per tile) next to the accumulators
         a.kps = 1;
         a.b3_slots = a.n_cap * 128 <= 16384 ? 4 : 3;
-        a.a3_slot_bytes = a.codec_raw ? kATileBytes : enc_tile_bytes(a.codec);
+        if (a.codec == 4 && (a.enc_tile % 16 || a.enc_tile < 0 || a.enc_tile > kATileBytes || (a.enc_tile && a.enc_tile < 11424)))
+            return cudaErrorInvalidValue;
+        a.a3_slot_bytes = a.codec_raw ? kATileBytes : enc_tile_bytes(a);
         a.stages = std::min(kMaxRing, (budget - 1024 - a.b3_slots * a.n_cap * 128) / a.a3_slot_bytes);
         if ((512 - need) / 32 < 4 && a.acc_stages == 2) {
             a.acc_stages = 1;

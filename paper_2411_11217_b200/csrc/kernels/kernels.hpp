@@ -42,6 +42,9 @@ struct GemmArgs {
     // mma.sync): 1 when some page-table entry of this GEMM is a raw fallback
     // block (tag bit 0; 16 KiB ring slots instead of 12432 B)
     int codec_raw = 0;
+    // codec 4: stored bytes of one encoded tile (runtime/weight_codec.hpp
+    // codec4_tile_bytes(capacity), sized per weight kind); 0 -> 11600
+    int enc_tile = 0;
     // optional CTA-0 pipeline trace [4][256] (%globaltimer): producer issue,
     // decoder start, decoder done, MMA start per k-block (diagnostic)
     unsigned long long* ktrace = nullptr;

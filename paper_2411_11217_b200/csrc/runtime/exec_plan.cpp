@@ -82,7 +82,7 @@ ShardMap shard_map(const lightplan::ModelSpec& m, const Shard& s, int kind) {
 }
 
 Catalog build_catalog(const lightplan::ModelSpec& m, const lightplan::Policy& p, const Shard& shard_in,
-                      bool codec, const std::vector<uint8_t>* raw_mask, int codec_tile_bytes) {
+                      bool codec, const std::vector<uint8_t>* raw_mask, const int* kind_tile_bytes) {
     Catalog c;
     const Shard sh = shard_in.q_heads ? shard_in : make_shard(m, 0, 1);
     const int H = static_cast<int>(m.hidden_dim), F = static_cast<int>(sh.ffn);
@@ -92,7 +92,8 @@ Catalog build_catalog(const lightplan::ModelSpec& m, const lightplan::Policy& p,
         for (int rb = 0; rb < rows / 128; ++rb) {
             const size_t i = c.blocks.size();
             const bool raw = codec && raw_mask && i < raw_mask->size() && (*raw_mask)[i];
-            const int64_t bytes = (codec && !raw) ? K / 64 * codec_tile_bytes : 128 * K * 2;
+            const int64_t tile = kind_tile_bytes ? kind_tile_bytes[kind] : kCodecTileBytes;
+            const int64_t bytes = (codec && !raw) ? K / 64 * tile : 128 * K * 2;
             c.blocks.push_back({kind, expert, rb, K, bytes, raw, false, 0});
         }
     };

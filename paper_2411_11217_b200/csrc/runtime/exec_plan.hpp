@@ -63,11 +63,13 @@ ShardMap shard_map(const lightplan::ModelSpec& model, const Shard& shard, int ki
 // codec: blocks are stored encoded (weight_codec.hpp: 12432 B per 64-k tile
 // instead of 16384), so the same r_w share holds more weights and the pages
 // stream fewer bytes.
+// kind_tile_bytes (codec only): stored bytes per encoded 64-k tile, indexed by
+// TensorKind (codec 4 sizes its tiles per kind); nullptr: 12432 for every kind.
 // raw_mask (codec only): raw_mask[i] != 0 stores catalog block i as raw
 // 16 KiB tiles in every layer — the fallback for weights the code cannot hold.
 Catalog build_catalog(const lightplan::ModelSpec& model, const lightplan::Policy& policy,
                       const Shard& shard = Shard{}, bool codec = false,
-                      const std::vector<uint8_t>* raw_mask = nullptr, int codec_tile_bytes = kCodecTileBytes);
+                      const std::vector<uint8_t>* raw_mask = nullptr, const int* kind_tile_bytes = nullptr);
 
 // Byte range [begin, end) of page p (1..M) of a layer blob; p = 0: whole.
 std::pair<int64_t, int64_t> page_range(int64_t blob_bytes, int M, int page);

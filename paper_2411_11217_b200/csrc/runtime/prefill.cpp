@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../kernels/kernels.hpp"
+#include "host_layout.hpp"
 #include "runtime.hpp"
 #include "runtime_util.hpp"
 
@@ -270,7 +271,7 @@ PrefillReport Runtime::prefill(const int32_t* tokens, const int32_t* lens, int32
                 a.n_chunks = nchunks;
                 a.out_f32 = pf_y_;
                 a.ldo = W_;
-                codec_args(a);
+                codec_args(a, kWqkv);
                 pl("qkv_gemm", mltk::launch_gemm(a, num_sms_, s_gpu_));
                 // KV: host cache (staged, one strided DMA per sequence) or the paged
                 // device pool (stored by rope_qkv itself)
@@ -304,7 +305,7 @@ PrefillReport Runtime::prefill(const int32_t* tokens, const int32_t* lens, int32
                 o.ldo = H_;
                 o.residual = coll_ ? nullptr : x;
                 o.ldr = H_;
-                codec_args(o);
+                codec_args(o, kWo);
                 pl("o_gemm", mltk::launch_gemm(o, num_sms_, s_gpu_));
                 if (coll_) {
                     coll_->all_reduce_sum(pf_h_, static_cast<size_t>(Tc) * H_, s_gpu_);
@@ -331,7 +332,7 @@ PrefillReport Runtime::prefill(const int32_t* tokens, const int32_t* lens, int32
                 gu.epi = mltk::kEpiSiluPacked;
                 gu.out_packed = pf_inter_;
                 gu.out_R = pf_Re_;
-                codec_args(gu);
+                codec_args(gu, kW1);
                 pl("expert_gateup_gemm", mltk::launch_gemm(gu, num_sms_, s_gpu_));
                 mltk::GemmArgs dn;
                 dn.a_table = tab + tab_w2_;
@@ -346,7 +347,7 @@ PrefillReport Runtime::prefill(const int32_t* tokens, const int32_t* lens, int32
                 dn.n_chunks = nchunks;
                 dn.out_f32 = pf_y_;
                 dn.ldo = H_;
-                codec_args(dn);
+                codec_args(dn, kW2);
                 pl("expert_down_gemm", mltk::launch_gemm(dn, num_sms_, s_gpu_));
                 if (coll_) {
                     pl("moe_combine", mltk::launch_moe_combine(nullptr, pf_y_, H_, pf_inv_, pf_topw_, Tc, H_, K_, x, s_gpu_));

@@ -227,8 +227,10 @@ void Runtime::build_catalog() {
         if (f && f[0] == '1')
             raw_mask_.assign(mlt::build_catalog(model_, policy_, shard_, true).blocks.size(), 1);
     }
+    int kind_tile[16];
+    for (int k = 0; k < 16; ++k) kind_tile[k] = codec_mode_ == 4 ? c4_tile_[k] : codec_tile_bytes(codec_mode_);
     cat_ = mlt::build_catalog(model_, policy_, shard_, opt_.weight_codec, raw_mask_.empty() ? nullptr : &raw_mask_,
-                              codec_tile_bytes(codec_mode_));
+                              kind_tile);
     any_raw_ = false;
     for (const auto& b : cat_.blocks) any_raw_ = any_raw_ || b.raw;
     layer_res_bytes_ = cat_.resident_bytes;
@@ -380,6 +382,9 @@ void Runtime::plain_tensor(int l, int kind, int64_t n, float scale, bool is_norm
 void Runtime::scan_raw_blocks() {
     const Catalog probe = mlt::build_catalog(model_, policy_, shard_, true);
     raw_mask_.assign(probe.blocks.size(), 0);
+    const bool c4 = codec_mode_ == 4;
+    // codec 4: the largest records + escapes count of any tile per block, over all layers
+    std::vector<int> need(probe.blocks.size(), 0);
     std::vector<uint16_t> tmp;
     for (int l = 0; l < L_; ++l)
         for (size_t i = 0; i < probe.blocks.size(); ++i) {
@@ -388,17 +393,34 @@ void Runtime::scan_raw_blocks() {
             tmp.resize(static_cast<size_t>(128) * b.K);
             packed_block(l, b, tmp.data());
             const int tiles = static_cast<int>(b.K / 64);
-            int bad = 0;
-            const bool c4 = codec_mode_ == 4;
-#pragma omp parallel for schedule(static) reduction(+ : bad)
+            int bad = 0, most = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad) reduction(max : most)
             for (int t = 0; t < tiles; ++t) {
-                uint8_t out[kCodecTileBytes];
+                uint8_t out[codec4_tile_bytes(kCodec4CapLimit) > kCodecTileBytes ? codec4_tile_bytes(kCodec4CapLimit)
+                                                                                 : kCodecTileBytes];
                 const uint8_t* src = reinterpret_cast<const uint8_t*>(tmp.data()) +
                                      static_cast<size_t>(t) * mltk::kATileBytes;
-                bad += (c4 ? codec4_encode_rows_tile(src, out) : codec_encode_tile(src, out)) ? 0 : 1;
+                int n = 0;
+                bad += (c4 ? codec4_encode_rows_tile(src, out, kCodec4CapLimit, &n) : codec_encode_tile(src, out)) ? 0 : 1;
+                most = std::max(most, n);
             }
             if (bad) raw_mask_[i] = 1;
+            need[i] = std::max(need[i], most);
         }
+    if (!c4) return;
+    // per weight kind (W1 and W3 share the gate/up GEMM): the capacity of its
+    // fullest coded tile, rounded up to a multiple of 4 (16-byte tiles)
+    for (int k = 0; k < 16; ++k) c4_cap_[k] = 0;
+    for (size_t i = 0; i < probe.blocks.size(); ++i)
+        if (!raw_mask_[i]) {
+            const int k = probe.blocks[i].kind == kW3 ? kW1 : probe.blocks[i].kind;
+            c4_cap_[k] = std::max(c4_cap_[k], need[i]);
+        }
+    c4_cap_[kW3] = c4_cap_[kW1];
+    for (int k = 0; k < 16; ++k) {
+        c4_cap_[k] = (c4_cap_[k] + 3) & ~3;
+        c4_tile_[k] = codec4_tile_bytes(c4_cap_[k]);
+    }
 }
 
 void Runtime::generate_weights() {
@@ -439,10 +461,11 @@ void Runtime::generate_weights() {
                     {
                     const uint8_t* src = reinterpret_cast<const uint8_t*>(tmp_block.data()) +
                                          static_cast<size_t>(t) * mltk::kATileBytes;
-                    uint8_t* out = dst + static_cast<size_t>(t) * codec_tile_bytes(codec_mode_);
+                    uint8_t* out = dst + static_cast<size_t>(t) * (codec_mode_ == 4 ? c4_tile_[b.kind]
+                                                                                 : codec_tile_bytes(codec_mode_));
                     bad += (codec_mode_ == 2   ? codec_encode_frag_tile(src, out)
                             : codec_mode_ == 3 ? codec_encode_rows_tile(src, out)
-                            : codec_mode_ == 4 ? codec4_encode_rows_tile(src, out)
+                            : codec_mode_ == 4 ? codec4_encode_rows_tile(src, out, c4_cap_[b.kind])
                                                : codec_encode_tile(src, out))
                                ? 0
                                : 1;
@@ -660,8 +683,9 @@ void Runtime::dense_tiling(int row_blocks, int& n_cap, int& n_chunks, int& k_spl
 // codec 1 = tcgen05 with in-smem decode (gemm_tc.cu), codec 2 = register
 // decode + mma.sync (gemm_codec.cu: <= 64 tokens per chunk, <= 32 for gate/up),
 // codec 3 = tcgen05 with A decoded into TMEM (gemm_tc.cu, decoupled rings).
-void Runtime::codec_args(mltk::GemmArgs& a) const {
+void Runtime::codec_args(mltk::GemmArgs& a, int kind) const {
     a.codec = codec_mode_;
+    if (codec_mode_ == 4) a.enc_tile = c4_tile_[kind];
     if (codec_mode_ == 2) a.n_cap = std::min(a.n_cap, a.n_mats == 2 ? 32 : 64);
     if (codec_mode_ >= 2) a.codec_raw = any_raw_ ? 1 : 0;  // raw fallback tiles need 16 KiB ring slots
 }
@@ -701,7 +725,7 @@ void Runtime::act_pre_attn(const Ctx& c, int step, int layer, int mb) {
     a.out_f32 = d_qkv_f32_;
     a.ldo = W_;
     a.timing = ktimer("qkv_gemm");
-    codec_args(a);
+    codec_args(a, kWqkv);
     kl("qkv_gemm", mltk::launch_gemm(a, num_sms_, s_gpu_));
     const int32_t* pos = d_pos_ + static_cast<size_t>(step - 1) * N_ + t0;
     uint16_t* qkv = d_qkv_bf16_ + static_cast<size_t>(mb - 1) * mu_ * W_;
@@ -776,7 +800,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     o.residual = coll_ ? nullptr : x;  // unsplit single GPU: residual in the GEMM epilogue
     o.ldr = H_;
     o.timing = ktimer("o_gemm");
-    codec_args(o);
+    codec_args(o, kWo);
     kl("o_gemm", mltk::launch_gemm(o, num_sms_, s_gpu_));
     if (coll_) {
         // TP all-reduce #1: h = x + sum over ranks of this rank's O partial
@@ -827,7 +851,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     gu.sk_count = d_sk_count_;
     gu.sk_rows = Rmu_;  // a token routes to an expert at most once: rows per group <= mu
     gu.timing = ktimer("expert_gateup_gemm");
-    codec_args(gu);
+    codec_args(gu, kW1);
     kl("expert_gateup_gemm", mltk::launch_gemm(gu, num_sms_, s_gpu_));
     mltk::GemmArgs dn;
     dn.a_table = tab + tab_w2_;
@@ -844,7 +868,7 @@ void Runtime::act_post_attn(const Ctx& c, int step, int layer, int mb) {
     dn.k_splits = down_splits_;
     dn.split_stride = static_cast<int64_t>(Re_) * H_;
     dn.timing = ktimer("expert_down_gemm");
-    codec_args(dn);
+    codec_args(dn, kW2);
     kl("expert_down_gemm", mltk::launch_gemm(dn, num_sms_, s_gpu_));
     if (coll_) {
         // TP all-reduce #2: x = h + sum over ranks of this rank's top-k combine (h2 shard)

@@ -217,12 +217,17 @@ class Runtime {
     const uint16_t* ext_tensor(int l, int kind, int expert) const;
     void scan_raw_blocks();  // codec + caller weights: blocks the code cannot hold -> raw_mask_
     void dense_tiling(int row_blocks, int& n_cap, int& n_chunks, int& k_splits) const;
-    void codec_args(mltk::GemmArgs& a) const;
+    void codec_args(mltk::GemmArgs& a, int kind) const;  // kind: the GEMM's weight kind (kWqkv, kWo, kW1, kW2)
     // resident CTA slots of the weight GEMMs: 2 per SM for the register-decode codec GEMM
     int gemm_slots() const { return codec_mode_ == 2 ? 2 * num_sms_ : num_sms_; }
     int codec_mode_ = 0;   // 0 bf16 tiles, 1 encoded (tcgen05 path), 2 encoded fragment order (mma.sync)
     bool any_raw_ = false; // codec: some block is a raw fallback (tagged page-table entry)
     std::vector<uint8_t> raw_mask_;  // codec: per catalog block, stored raw (fallback)
+    // codec 4: capacity (records + escapes per tile) and tile bytes per TensorKind,
+    // sized by scan_raw_blocks from the weights
+    int c4_cap_[16] = {44, 44, 44, 44, 44, 44, 44, 44, 44, 44, 44, 44, 44, 44, 44, 44};
+    int c4_tile_[16] = {11600, 11600, 11600, 11600, 11600, 11600, 11600, 11600,
+                        11600, 11600, 11600, 11600, 11600, 11600, 11600, 11600};
     static constexpr int kMaxSplits = 8;
     void allocate();
     void generate_weights();

@@ -136,7 +136,7 @@ inline uint32_t c4_get(const uint32_t* words, uint32_t k) {
 }
 }  // namespace
 
-bool codec4_encode_rows_tile(const uint8_t* packed, uint8_t* out) {
+bool codec4_encode_rows_tile(const uint8_t* packed, uint8_t* out, int cap, int* entries) {
     uint16_t w[8192];
     rows_from_packed(packed, w);
     bool can_shift = true;  // w + 0x80 must not carry out of the exponent (e = 255)
@@ -156,7 +156,7 @@ bool codec4_encode_rows_tile(const uint8_t* packed, uint8_t* out) {
             for (int s = 0; s < 8; ++s) table[s] = order[s];  // descending frequency: slot 7 the rarest
         }
     }
-    std::memset(out, 0, kCodec4TileBytes);
+    std::memset(out, 0, codec4_tile_bytes(cap));
     // slots 0-6 are fixed for the tile; slot 7 is per row (override byte) and,
     // inside the 4-weight units a row's record flags, a second per-row byte
     int code_of[256];
@@ -228,7 +228,9 @@ bool codec4_encode_rows_tile(const uint8_t* packed, uint8_t* out) {
         }
         for (uint32_t m = 0; m < 6; ++m) std::memcpy(out + kC4Codes + (m * 128 + r) * 4, &words[m], 4);
     }
-    if (recs.size() + hard.size() > static_cast<size_t>(kCodec4MaxEntries)) return false;
+    const int n_ent = static_cast<int>(recs.size() + hard.size());
+    if (entries) *entries = n_ent;
+    if (n_ent > cap || hard.size() > 255) return false;
     std::memcpy(out + kC4Table, table, 8);
     uint8_t start[4] = {0, 0, 0, 0};
     for (uint32_t q = 1; q < 4; ++q) {

@@ -85,11 +85,22 @@ namespace mlt {
 //   [11424, ...)    n_rec records in row order {u16 unit mask (bit u: k in
 //                   [4u, 4u+4)), u8 X_r, u8 0}, then n_hard hard escapes
 //                   {u16 index i, u16 bf16 w_i} in row order;
-//                   n_rec + n_hard <= 44
+//                   n_rec + n_hard <= the tile's capacity
 // Decoding: w_i = (slot byte << 8 | low) - ph * 0x80, then hard escapes.
-constexpr int kCodec4TileBytes = 11600;
-constexpr int kCodec4MaxEntries = 44;  // records + hard escapes per tile
-bool codec4_encode_rows_tile(const uint8_t* packed16k, uint8_t* out);
+// Capacity: records + hard escapes per tile.  The runtime sizes it per weight
+// kind from the weights (scan_raw_blocks: the kind's largest tile), so the
+// tile is codec4_tile_bytes(cap) = 11424 + 4 cap rounded up to 16 B; 44 is
+// the C-ABI default (mlt_codec4_encode_rows: 11600 B).
+constexpr int kCodec4MaxEntries = 44;   // default capacity
+constexpr int kCodec4CapLimit = 200;    // beyond: the block is stored raw
+constexpr int kCodec4TileBytes = 11600;  // at the default capacity
+constexpr int codec4_tile_bytes(int cap) { return (11424 + 4 * cap + 15) & ~15; }
+static_assert(codec4_tile_bytes(kCodec4MaxEntries) == kCodec4TileBytes, "default tile size");
+// Encode one tile with at most cap entries; false if it needs more.  With
+// entries != nullptr the count is reported (also when it exceeds cap; out
+// must then hold codec4_tile_bytes(kCodec4CapLimit) bytes).
+bool codec4_encode_rows_tile(const uint8_t* packed16k, uint8_t* out, int cap = kCodec4MaxEntries,
+                             int* entries = nullptr);
 void codec4_decode_rows_tile(const uint8_t* enc, uint8_t* packed16k);
 
 // stored bytes of one encoded 64-k tile in GemmArgs::codec mode m (1-4)

@@ -175,3 +175,32 @@ def test_phase_and_row_override(K):
     rows = [((int(enc2[h0 + 4 * e]) | int(enc2[h0 + 1 + 4 * e]) << 8) >> 4) & 127 for e in range(n_hard)]
     assert 9 not in rows
     assert (int(enc2[11408:11412].view(np.uint32)[0]) >> 9) & 1     # row 9 holds a unit record
+
+
+def test_capacity_per_weight_kind(K):
+    """A scale whose top binade is nearly empty (DBRX's down projection,
+    sqrt(3/10752) = 1.07 * 2^-6) needs ~31 records + escapes per tile: at the
+    default capacity (44) some blocks overflow to raw; the runtime sizes the
+    capacity per weight kind instead (mlt_codec4_encode_rows_cap, tiles of
+    11424 + 4 cap bytes), which codes every block and round-trips exactly."""
+    from oracle import bind as orc
+    M, Kd = 1024, 1024
+    w = orc.gen_bf16(1234, orc.tensor_id(0, 10, 1), M * Kd, 10752 ** -0.5).reshape(M, Kd)
+    packed = pack(K, w, M, Kd)
+    _, raw, n_raw = encode4(K, packed, M, Kd)
+    assert n_raw > 0
+    cap = 80
+    tb = K.codec4_tile_bytes_for(cap)
+    assert tb == 11424 + 4 * cap and tb % 16 == 0 and K.codec4_tile_bytes_for(44) == TILE4
+    out = np.zeros(M // 128 * (Kd // 64) * 16384, np.uint8)
+    raw = np.zeros(M // 128, np.uint8)
+    assert K.codec4_encode_rows_cap(packed.ctypes.data_as(C.c_void_p), M, Kd, cap, out.ctypes.data_as(C.c_void_p),
+                                    raw.ctypes.data_as(C.c_void_p)) == 0
+    tiles = M // 128 * Kd // 64
+    ent = [int(out[t * tb + 11404]) + int(out[t * tb + 11405]) for t in range(tiles)]
+    assert 44 < max(ent) <= cap
+    back = np.zeros_like(packed)
+    K.codec4_decode_rows_cap(out.ctypes.data_as(C.c_void_p), tiles, cap, back.ctypes.data_as(C.c_void_p))
+    assert np.array_equal(back, packed)
+    with pytest.raises(capi.MltError):
+        K.codec4_encode_rows_cap(packed.ctypes.data_as(C.c_void_p), M, Kd, 201, out.ctypes.data_as(C.c_void_p), None)

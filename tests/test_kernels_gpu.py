@@ -419,13 +419,17 @@ def encode_weight_dev(K, w_bf16, fmt=1):
     return dev, blocks
 
 
-def encode_rows_dev(K, w_bf16, force_raw=(), fmt=3):
+def encode_rows_dev(K, w_bf16, force_raw=(), fmt=3, cap=44):
     """Codec-3 weight blocks (row-plane encoded tiles, mlt_codec_encode_rows),
     or with fmt 4 the 3-bit code (mlt_codec4_encode_rows, 11600 B tiles):
     a row block the code cannot hold (too many escapes in a tile), or listed in
     force_raw, is stored as raw packed tiles with its pointer tagged (bit 0).
     Returns (device buffer, row-block pointers, raw flags)."""
-    enc_fn, tb = (K.codec4_encode_rows, 11600) if fmt == 4 else (K.codec_encode_rows, 12432)
+    if fmt == 4:
+        tb = K.codec4_tile_bytes_for(cap)
+        enc_fn = lambda src, m, k, dst, rr: K.codec4_encode_rows_cap(src, m, k, cap, dst, rr)  # noqa: E731
+    else:
+        enc_fn, tb = K.codec_encode_rows, 12432
     M, Kd = w_bf16.shape
     src = bf16_bits(w_bf16.cpu())
     packed = np.empty_like(src)
@@ -595,6 +599,36 @@ def test_codec4_phase_override_escapes(K, T, n_cap):
         args = capi.GemmArgs(a_table=tab.data_ptr(), n_mats=1, G=1, RB=M // 128, K=Kd, b=xp.data_ptr(), R=R,
                              rows_dense=T, n_cap=n_cap, epi=0, alpha=1.0, out_f32=out.data_ptr(), ldo=M,
                              k_splits=1, split_stride=R * M, codec=cdc, codec_raw=int(cdc != 0))
+        K.gemm(C.byref(args), stream())
+        torch.cuda.synchronize()
+        outs.append(out.cpu())
+    assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("cap", [0, 80, 200])
+def test_codec4_tile_capacity(K, cap):
+    """Codec 4 tiles of a non-default capacity (GemmArgs enc_tile = 11424 +
+    4 cap bytes, the runtime's per-weight-kind sizing): DBRX-down-scale
+    weights (1.07 * 2^-6, ~31 entries per tile) at cap 80 and 200 code every
+    block; cap 0 (no records or escapes) leaves only blocks without them,
+    the rest raw — all bit-equal to the raw-tile GEMM."""
+    g = torch.Generator().manual_seed(cap + 5)
+    M, Kd, T = 384, 1024, 40
+    w = unif_bf16(M, Kd, scale=10752 ** -0.5, gen=g)
+    x = rand_bf16(T, Kd, gen=g)
+    R = (T + 15) // 16 * 16
+    raw_dev, raw_blocks = pack_weight_dev(K, w)
+    enc_dev, enc_blocks, flags = encode_rows_dev(K, w, fmt=4, cap=cap)
+    assert (not any(flags)) if cap else all(flags)
+    xp = pack_rows_dev(K, x, R)
+    outs = []
+    for cdc, blocks in ((0, raw_blocks), (4, enc_blocks)):
+        tab = table([blocks])
+        out = torch.zeros(1, R, M, device="cuda")
+        args = capi.GemmArgs(a_table=tab.data_ptr(), n_mats=1, G=1, RB=M // 128, K=Kd, b=xp.data_ptr(), R=R,
+                             rows_dense=T, n_cap=48, epi=0, alpha=1.0, out_f32=out.data_ptr(), ldo=M,
+                             k_splits=1, split_stride=R * M, codec=cdc, codec_raw=int(any(flags)),
+                             enc_tile=K.codec4_tile_bytes_for(cap) if cdc else 0)
         K.gemm(C.byref(args), stream())
         torch.cuda.synchronize()
         outs.append(out.cpu())
