@@ -514,7 +514,14 @@ def run_mlt(args, cfg):
         # reports: raw-fallback blocks, or the 12-bit code when the 11-bit one does
         # not fit the weights, stream more than the search's CODEC_DT assumed
         cfg["stored_dt"] = info.bytes_per_weight
-    bound = hrm_bound(cfg, link_gbs, host_gbs, pk, tp=tp, per_slice_host=args.tp_shard > 1)
+    try:
+        bound = hrm_bound(cfg, link_gbs, host_gbs, pk, tp=tp, per_slice_host=args.tp_shard > 1)
+    except capi.InfeasiblePolicyError:
+        # the searched r_w does not fit the budget at the stored size (the runtime
+        # held fewer weights resident): bound of the best policy at that size
+        cfg["r_w_bound"] = search_rw(cfg, link_gbs, host_gbs, pk, tp, per_slice_host=args.tp_shard > 1)
+        bound = hrm_bound(dict(cfg, r_w=cfg["r_w_bound"]), link_gbs, host_gbs, pk, tp=tp,
+                          per_slice_host=args.tp_shard > 1)
     # the bf16-weight bound at the raw policy: the best the unencoded stream could do
     bound_bf16 = hrm_bound(dict(cfg, codec=False, r_w=raw_rw), link_gbs, host_gbs, pk, tp=tp,
                            per_slice_host=args.tp_shard > 1) if cfg.get("codec") else bound
@@ -536,6 +543,7 @@ def run_mlt(args, cfg):
         "host": host_info(),
         "run": {"r_w": cfg["r_w"], "weight_codec": "on" if cfg.get("codec") else "off",
                 "r_w_achieved": info.achieved_weight_ratio,
+                **({"r_w_bound": cfg["r_w_bound"]} if "r_w_bound" in cfg else {}),
                 "parallelism_detail": (f"tp{world} (heads + expert h2 sharded, all-reduce x2/layer)"
                                        if world > 1 else
                                        f"tp{tp} job, its largest shard (rank {shard_rank}) measured alone on 1 GPU "

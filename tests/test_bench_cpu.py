@@ -12,6 +12,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa: E402
+from paper_2411_11217_b200 import capi  # noqa: E402
 
 PK = {"hbm_gbs": 6548.5, "bf16_tflops": 1393.0, "bf16_tflops_sustained": 1393.0}
 
@@ -51,6 +52,26 @@ def test_codec_bound_uses_stored_bytes():
     cfg["r_w"] = bench.search_rw(cfg, 55.6, 125.0, PK)
     assert cfg["r_w"] > 0.10  # the same budget holds more encoded weights
     assert bench.hrm_bound(cfg, 55.6, 125.0, PK).decode_throughput > 1.35 * raw.decode_throughput
+
+
+def test_bound_uses_the_runtimes_stored_bytes():
+    """After runtime creation bench.py sets cfg['stored_dt'] to the runtime's
+    reported bytes per weight (raw-fallback blocks, or the 12-bit code when the
+    11-bit one does not fit, stream more): the executed run's bound and the
+    roofline's algorithmic bytes follow it; a larger stored size lowers the
+    link-bound bound by the byte ratio."""
+    cfg = _cfg("mixtral8x7b-16g", codec=True)
+    cfg["r_w"] = 0.18
+    b0 = bench.hrm_bound(cfg, 55.6, 125.0, PK)
+    cfg2 = dict(cfg, stored_dt=12432 / 8192)
+    assert bench.model_spec(cfg2, stored=True).weight_dtype_bytes == pytest.approx(12432 / 8192)
+    with pytest.raises(capi.InfeasiblePolicyError):   # r_w 0.18 does not fit 16 GB at 12432 B / tile
+        bench.hrm_bound(cfg2, 55.6, 125.0, PK)
+    cfg["r_w"] = cfg2["r_w"] = 0.15
+    b0 = bench.hrm_bound(cfg, 55.6, 125.0, PK)
+    b1 = bench.hrm_bound(cfg2, 55.6, 125.0, PK)
+    assert b1.breakdown.link_upload == pytest.approx(b0.breakdown.link_upload * 12432 / 11600, rel=2e-3)
+    assert b1.decode_throughput < b0.decode_throughput
 
 
 def test_nvlink_roof_only_adds_to_gpu_term():
