@@ -340,7 +340,7 @@ __device__ __forceinline__ void decode_row_ts(uint32_t c, uint32_t r, uint32_t (
 // gathered into a fourth selector word by 3 shifts and 3 masked ORs.  One
 // PRMT looks up 4 high bytes in this row's 8-byte table — slots 0-6 of the
 // tile, slot 7 = the row's byte, or in the units its record flags the
-// record's byte (one SEL per 4 weights) — two PRMTs interleave them with the
+// record's byte for that row half (one SEL per 4 weights) — two PRMTs interleave them with the
 // raw low bytes, one subtraction per 2 weights undoes the tile's exponent
 // phase: ~1.9 instructions per weight, all register indices static.  The
 // rare hard escapes (~0.5 per row quarter) are patched by a warp-uniform
@@ -357,9 +357,10 @@ __device__ __forceinline__ uint32_t lds8(uint32_t a) {
 
 template <bool kPhase>
 __device__ __forceinline__ void expand_row_c4(const uint4 (&lo)[4], const uint32_t (&cw)[6], uint32_t t0, uint32_t t1,
-                                              uint32_t t1x, uint32_t rec, uint32_t (&o)[32]) {
+                                              uint32_t t1x0, uint32_t t1x1, uint32_t rec, uint32_t (&o)[32]) {
 #pragma unroll
     for (int H = 0; H < 2; ++H) {
+        const uint32_t t1x = H ? t1x1 : t1x0;
         const uint32_t A = cw[3 * H], B = cw[3 * H + 1], C = cw[3 * H + 2];
         const uint32_t S = ((A >> 3) & 0x11111111u) | ((B >> 2) & 0x22222222u) | ((C >> 1) & 0x44444444u);
         const uint32_t sel[8] = {A & 0x7777u, (A >> 16) & 0x7777u, B & 0x7777u, (B >> 16) & 0x7777u,
@@ -413,11 +414,13 @@ __device__ __forceinline__ void decode_row_c4(uint32_t c, uint32_t r, uint32_t (
     esc.n = hb1 - hb0;
     esc.e0 = lane < esc.n ? lds32(h0 + 4u * (hb0 + lane)) : 0u;
     esc.e1 = lane + 32u < esc.n ? lds32(h0 + 4u * (hb0 + 32u + lane)) : 0u;
-    const uint32_t t1 = prmt(T.y, rb, 0x4210u), t1x = prmt(T.y, rec >> 16, 0x4210u);
+    // slot 7: the row's byte, or in flagged units of row half h the record's byte X_h
+    const uint32_t t1 = prmt(T.y, rb, 0x4210u), t1x0 = prmt(T.y, rec >> 16, 0x4210u),
+                   t1x1 = prmt(T.y, rec >> 24, 0x4210u);
     if (hdr & 0xffu)
-        expand_row_c4<true>(lo, cw, T.x, t1, t1x, rec, o);
+        expand_row_c4<true>(lo, cw, T.x, t1, t1x0, t1x1, rec, o);
     else
-        expand_row_c4<false>(lo, cw, T.x, t1, t1x, rec, o);
+        expand_row_c4<false>(lo, cw, T.x, t1, t1x0, t1x1, rec, o);
 }
 
 template <int G>

@@ -178,44 +178,54 @@ bool codec4_encode_rows_tile(const uint8_t* packed, uint8_t* out, int cap, int* 
         int vals[64], nv = 0;
         for (uint32_t k = 0; k < 64; ++k)
             if (code_of[hi[k]] < 0 && std::find(vals, vals + nv, hi[k]) == vals + nv) vals[nv++] = hi[k];
-        // hard escapes of an assignment (R row-wide, X in the units holding an X)
-        auto cost = [&](int R, int X, uint32_t* umask_out) {
+        // hard escapes of an assignment: R row-wide, X[h] in the units of row half
+        // h (k / 32) that hold an X[h] (the record's unit mask, bits 8h .. 8h + 7)
+        auto cost = [&](int R, const int* X, uint32_t* umask_out) {
             uint32_t um = 0;
-            if (X >= 0)
-                for (uint32_t k = 0; k < 64; ++k)
-                    if (hi[k] == X) um |= 1u << (k >> 2);
+            for (uint32_t k = 0; k < 64; ++k)
+                if (X[k >> 5] >= 0 && hi[k] == X[k >> 5]) um |= 1u << (k >> 2);
             int h = 0;
             for (uint32_t k = 0; k < 64; ++k) {
                 if (code_of[hi[k]] >= 0) continue;
-                const int slot7 = (um >> (k >> 2)) & 1u ? X : R;
+                const int slot7 = (um >> (k >> 2)) & 1u ? X[k >> 5] : R;
                 h += hi[k] != slot7;
             }
             if (umask_out) *umask_out = um;
             return h;
         };
-        int R = nv ? vals[0] : table[7], X = -1, best = nv ? cost(vals[0], -1, nullptr) : 0;
-        for (int a = 0; a < nv && best; ++a) {
-            const int h = cost(vals[a], -1, nullptr);
-            if (h < best) best = h, R = vals[a], X = -1;
-        }
-        for (int a = 0; a < nv && best; ++a)
-            for (int b = 0; b < nv && best; ++b) {
-                if (a == b) continue;
-                const int h = cost(vals[a], vals[b], nullptr);
-                if (h < best) best = h, R = vals[a], X = vals[b];
+        // candidates: the row's most frequent out-of-table values (at most 6)
+        int cnt_v[64] = {};
+        for (int a = 0; a < nv; ++a)
+            for (uint32_t k = 0; k < 64; ++k) cnt_v[a] += hi[k] == vals[a];
+        for (int a = 1; a < nv; ++a)  // stable sort by count, descending
+            for (int b = a; b > 0 && cnt_v[b] > cnt_v[b - 1]; --b) {
+                std::swap(cnt_v[b], cnt_v[b - 1]);
+                std::swap(vals[b], vals[b - 1]);
             }
+        const int nc = std::min(nv, 6);
+        int R = nv ? vals[0] : table[7], X[2] = {-1, -1};
+        int best = nv ? cost(R, X, nullptr) : 0;
+        for (int a = 0; a < nc && best; ++a)
+            for (int b = -1; b < nc && best; ++b)
+                for (int d = -1; d < nc && best; ++d) {
+                    if (b == a || d == a) continue;
+                    const int Xc[2] = {b < 0 ? -1 : vals[b], d < 0 ? -1 : vals[d]};
+                    const int h = cost(vals[a], Xc, nullptr);
+                    if (h < best) best = h, R = vals[a], X[0] = Xc[0], X[1] = Xc[1];
+                }
         uint32_t um = 0;
         cost(R, X, &um);
         out[kC4Rows + r] = static_cast<uint8_t>(R);
-        if (X >= 0) {
+        if (um) {
             qmask[r / 32] |= 1u << (r % 32);
-            recs.push_back(um | (static_cast<uint32_t>(X) << 16));
+            recs.push_back(um | (static_cast<uint32_t>(X[0] < 0 ? 0 : X[0]) << 16) |
+                           (static_cast<uint32_t>(X[1] < 0 ? 0 : X[1]) << 24));
         }
         uint32_t words[6] = {};
         for (uint32_t k = 0; k < 64; ++k) {
             int c = code_of[hi[k]];
             if (c < 0) {
-                const int slot7 = (um >> (k >> 2)) & 1u ? X : R;
+                const int slot7 = (um >> (k >> 2)) & 1u ? X[k >> 5] : R;
                 if (hi[k] == slot7) {
                     c = 7;
                 } else {
@@ -262,16 +272,16 @@ void codec4_decode_rows_tile(const uint8_t* enc, uint8_t* packed) {
     std::memcpy(qmask, enc + kC4QMask, 16);
     int rec = 0;
     for (uint32_t r = 0; r < 128; ++r) {
-        uint32_t words[6], um = 0, X = 0;
+        uint32_t words[6], um = 0, X[2] = {0, 0};
         if ((qmask[r / 32] >> (r % 32)) & 1u) {
             uint32_t v;
             std::memcpy(&v, enc + kC4Ent + 4 * rec++, 4);
-            um = v & 0xffffu, X = (v >> 16) & 0xffu;
+            um = v & 0xffffu, X[0] = (v >> 16) & 0xffu, X[1] = v >> 24;
         }
         for (uint32_t m = 0; m < 6; ++m) std::memcpy(&words[m], enc + kC4Codes + (m * 128 + r) * 4, 4);
         for (uint32_t k = 0; k < 64; ++k) {
             const uint32_t i = c4_index(r, k), c = c4_get(words, k);
-            const uint32_t hb = c < 7 ? table[c] : ((um >> (k >> 2)) & 1u) ? X : enc[kC4Rows + r];
+            const uint32_t hb = c < 7 ? table[c] : ((um >> (k >> 2)) & 1u) ? X[k >> 5] : enc[kC4Rows + r];
             w[i] = static_cast<uint16_t>(((hb << 8) | enc[i]) - ph * 0x80);
         }
     }

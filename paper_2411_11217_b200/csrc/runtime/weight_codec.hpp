@@ -69,8 +69,9 @@ namespace mlt {
 // w' = w + ph * 0x80.  Stored: w' low byte raw and a 3-bit index of w' high
 // byte: slots 0-6 into the tile's table of its most frequent high bytes, slot
 // 7 into the row's override byte R_r, except inside the 4-weight units a row
-// record flags, where slot 7 means the record's byte X_r (a second per-row
-// value).  Weights that still miss are "hard" escapes {index, bf16}.  Layout:
+// record flags, where slot 7 means the record's byte X_{r,h} for that row half
+// h = k / 32 (up to two more per-row values).  Weights that still miss are
+// "hard" escapes {index, bf16}.  Layout:
 //   [0, 8192)       low byte of w'_i (i = ((k / 16) * 128 + r) * 16 + k % 16)
 //   [8192, 11264)   codes: u32 word m (0..5) of row r at 8192 + (m * 128 + r) * 4;
 //                   for H = m / 3, words A, B, C = 3H, 3H+1, 3H+2: nibble n
@@ -83,7 +84,8 @@ namespace mlt {
 //   [11404, 11408)  {n_hard, n_rec, 0, 0} (u8)
 //   [11408, 11424)  u32 per row quarter: bit l = row 32q + l has a record
 //   [11424, ...)    n_rec records in row order {u16 unit mask (bit u: k in
-//                   [4u, 4u+4)), u8 X_r, u8 0}, then n_hard hard escapes
+//                   [4u, 4u+4)), u8 X_{r,0} (units 0-7), u8 X_{r,1} (units
+//                   8-15)}, then n_hard hard escapes
 //                   {u16 index i, u16 bf16 w_i} in row order;
 //                   n_rec + n_hard <= the tile's capacity
 // Decoding: w_i = (slot byte << 8 | low) - ph * 0x80, then hard escapes.

@@ -68,7 +68,7 @@ def np_decode4(enc):
             rec += 1
             for u in range(16):
                 if (v >> u) & 1:
-                    slot7[r, 4 * u:4 * u + 4] = (v >> 16) & 0xFF                     # X_r in flagged units
+                    slot7[r, 4 * u:4 * u + 4] = (v >> (16 + 8 * (u // 8))) & 0xFF    # X_{r,half} in flagged units
     assert rec == n_rec and n_rec + n_hard <= 44
     hi = np.where(codes == 7, slot7, table[np.minimum(codes, 6)]).astype(np.uint32)
     lo = enc[:8192][ROW_PLANE].astype(np.uint32)
@@ -179,16 +179,18 @@ def test_phase_and_row_override(K):
 
 def test_capacity_per_weight_kind(K):
     """A scale whose top binade is nearly empty (DBRX's down projection,
-    sqrt(3/10752) = 1.07 * 2^-6) needs ~31 records + escapes per tile: at the
-    default capacity (44) some blocks overflow to raw; the runtime sizes the
-    capacity per weight kind instead (mlt_codec4_encode_rows_cap, tiles of
-    11424 + 4 cap bytes), which codes every block and round-trips exactly."""
+    sqrt(3/10752) = 1.07 * 2^-6) needs ~28 records + escapes per tile: with
+    too small a capacity blocks overflow to raw; the runtime sizes the
+    capacity per weight kind (mlt_codec4_encode_rows_cap, tiles of 11424 +
+    4 cap bytes), which codes every block and round-trips exactly."""
     from oracle import bind as orc
     M, Kd = 1024, 1024
     w = orc.gen_bf16(1234, orc.tensor_id(0, 10, 1), M * Kd, 10752 ** -0.5).reshape(M, Kd)
     packed = pack(K, w, M, Kd)
-    _, raw, n_raw = encode4(K, packed, M, Kd)
-    assert n_raw > 0
+    small = np.zeros(M // 128 * (Kd // 64) * 16384, np.uint8)
+    raw = np.zeros(M // 128, np.uint8)
+    assert K.codec4_encode_rows_cap(packed.ctypes.data_as(C.c_void_p), M, Kd, 16, small.ctypes.data_as(C.c_void_p),
+                                    raw.ctypes.data_as(C.c_void_p)) > 0     # too small a capacity: raw blocks
     cap = 80
     tb = K.codec4_tile_bytes_for(cap)
     assert tb == 11424 + 4 * cap and tb % 16 == 0 and K.codec4_tile_bytes_for(44) == TILE4
@@ -198,7 +200,7 @@ def test_capacity_per_weight_kind(K):
                                     raw.ctypes.data_as(C.c_void_p)) == 0
     tiles = M // 128 * Kd // 64
     ent = [int(out[t * tb + 11404]) + int(out[t * tb + 11405]) for t in range(tiles)]
-    assert 44 < max(ent) <= cap
+    assert 16 < max(ent) <= cap
     back = np.zeros_like(packed)
     K.codec4_decode_rows_cap(out.ctypes.data_as(C.c_void_p), tiles, cap, back.ctypes.data_as(C.c_void_p))
     assert np.array_equal(back, packed)
