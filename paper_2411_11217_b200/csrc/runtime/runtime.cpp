@@ -137,10 +137,10 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     // raw bf16 (profiles/r02s2_codec_engines.txt).  MLT_CODEC_MODE=1 selects the
     // in-smem decoder, MLT_CODEC_MODE=2 the register-decode mma.sync GEMM
     // (fragment-order tiles, while a micro-batch fits its 64-token chunks).
-    // Codec 4 (the default) is the same engine on the 3-bit code: 11600 B per
+    // Codec 4 (the default) is the same engine on the 3-bit code: ~11600 B per
     // tile instead of 12432 (weight_codec.hpp); MLT_CODEC_MODE=3 keeps the
-    // 4-bit code.  Weights whose tiles overflow the 3-bit code's escapes in
-    // more than 5 % of the 128-row blocks fall back to codec 3 (scan_raw_blocks).
+    // 4-bit code.  Weights the 3-bit code holds badly (see below) fall back to
+    // codec 3 after the scan (scan_raw_blocks).
     codec_mode_ = 0;
     if (opt.weight_codec) {
         const char* m = std::getenv("MLT_CODEC_MODE");
@@ -176,9 +176,15 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
         const char* f = std::getenv("MLT_CODEC_FORCE_RAW");
         if (!(f && f[0] == '1')) {
             scan_raw_blocks();
-            int raw = 0;
+            int raw = 0, cap = 0;
             for (uint8_t b : raw_mask_) raw += b;
-            if (codec_mode_ == 4 && raw * 20 > static_cast<int>(raw_mask_.size())) {
+            for (int k = 0; k < 16; ++k) cap = std::max(cap, c4_cap_[k]);
+            // the 3-bit code pays while its tile stays clearly smaller than the
+            // 4-bit code's 12432 B and hard escapes stay rare: fall back when
+            // more than 5 % of the blocks would be raw or a kind needs more
+            // than 128 entries per tile (11936 B; heavy-tailed weights: ~110
+            // entries, ~30 of them hard escapes)
+            if (codec_mode_ == 4 && (raw * 20 > static_cast<int>(raw_mask_.size()) || cap > 128)) {
                 codec_mode_ = 3;
                 scan_raw_blocks();
             }

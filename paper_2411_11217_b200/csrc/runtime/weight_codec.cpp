@@ -175,9 +175,18 @@ bool codec4_encode_rows_tile(const uint8_t* packed, uint8_t* out, int cap, int* 
             hi[k] = static_cast<uint8_t>(x >> 8);
         }
         // the row's out-of-table (slot 7) values
-        int vals[64], nv = 0;
-        for (uint32_t k = 0; k < 64; ++k)
-            if (code_of[hi[k]] < 0 && std::find(vals, vals + nv, hi[k]) == vals + nv) vals[nv++] = hi[k];
+        int vals[64], nv = 0, cnt_v[64] = {};
+        uint8_t slot_of[256];  // this row's out-of-table value -> index in vals (first seen)
+        for (uint32_t k = 0; k < 64; ++k) {
+            if (code_of[hi[k]] >= 0) continue;
+            bool seen = false;
+            for (int a = 0; a < nv && !seen; ++a) seen = vals[a] == hi[k];  // nv is small unless heavy-tailed
+            if (!seen) {
+                slot_of[hi[k]] = static_cast<uint8_t>(nv);
+                vals[nv++] = hi[k];
+            }
+            ++cnt_v[slot_of[hi[k]]];
+        }
         // hard escapes of an assignment: R row-wide, X[h] in the units of row half
         // h (k / 32) that hold an X[h] (the record's unit mask, bits 8h .. 8h + 7)
         auto cost = [&](int R, const int* X, uint32_t* umask_out) {
@@ -193,26 +202,40 @@ bool codec4_encode_rows_tile(const uint8_t* packed, uint8_t* out, int cap, int* 
             if (umask_out) *umask_out = um;
             return h;
         };
-        // candidates: the row's most frequent out-of-table values (at most 6)
-        int cnt_v[64] = {};
-        for (int a = 0; a < nv; ++a)
-            for (uint32_t k = 0; k < 64; ++k) cnt_v[a] += hi[k] == vals[a];
+        // candidates: the row's most frequent out-of-table values (at most 6).
+        // For a given R the two halves are independent: per half, the X (or
+        // none) with the fewest hard escapes, from per-unit value counts.
         for (int a = 1; a < nv; ++a)  // stable sort by count, descending
             for (int b = a; b > 0 && cnt_v[b] > cnt_v[b - 1]; --b) {
                 std::swap(cnt_v[b], cnt_v[b - 1]);
                 std::swap(vals[b], vals[b - 1]);
             }
         const int nc = std::min(nv, 6);
-        int R = nv ? vals[0] : table[7], X[2] = {-1, -1};
-        int best = nv ? cost(R, X, nullptr) : 0;
-        for (int a = 0; a < nc && best; ++a)
-            for (int b = -1; b < nc && best; ++b)
-                for (int d = -1; d < nc && best; ++d) {
-                    if (b == a || d == a) continue;
-                    const int Xc[2] = {b < 0 ? -1 : vals[b], d < 0 ? -1 : vals[d]};
-                    const int h = cost(vals[a], Xc, nullptr);
-                    if (h < best) best = h, R = vals[a], X[0] = Xc[0], X[1] = Xc[1];
+        int cu[6][16] = {}, ou[16] = {};  // per unit: count of candidate c, of out-of-table weights
+        for (uint32_t k = 0; k < 64; ++k) {
+            if (code_of[hi[k]] >= 0) continue;
+            ++ou[k >> 2];
+            for (int c = 0; c < nc; ++c) cu[c][k >> 2] += hi[k] == vals[c];
+        }
+        int R = nv ? vals[0] : table[7], X[2] = {-1, -1}, best = 1 << 30;
+        for (int a = 0; a < (nv ? nc : 1) && best; ++a) {
+            int tot = 0, xb[2] = {-1, -1};
+            for (int h = 0; h < 2; ++h) {
+                int hb = 1 << 30;
+                for (int x = -1; x < nc; ++x) {
+                    if (x == a) continue;
+                    int hh = 0;
+                    for (int u = 8 * h; u < 8 * h + 8; ++u)
+                        hh += (x >= 0 && cu[x][u]) ? ou[u] - cu[x][u] : ou[u] - (nv ? cu[a][u] : 0);
+                    if (hh < hb) hb = hh, xb[h] = x;
                 }
+                tot += hb;
+            }
+            if (tot < best) {
+                best = tot, R = nv ? vals[a] : table[7];
+                X[0] = xb[0] < 0 ? -1 : vals[xb[0]], X[1] = xb[1] < 0 ? -1 : vals[xb[1]];
+            }
+        }
         uint32_t um = 0;
         cost(R, X, &um);
         out[kC4Rows + r] = static_cast<uint8_t>(R);
