@@ -87,9 +87,15 @@ def main():
                 d = rt.decode(wu.ids[-1], a.steps)
                 rep = d.report
                 val = N * a.steps / rep.seconds
+                if a.codec:  # the bound at the bytes per weight the runtime stored (bench.py does the same)
+                    try:
+                        bound = bench.hrm_bound(dict(cfg, stored_dt=rt.info.bytes_per_weight), link[0], host, pk)
+                    except capi.InfeasiblePolicyError:
+                        pass
                 row = {"budget_gb": budget_gb, "mu": mu, "A_g": a_g, "r_w": r_w,
                        "r_w_achieved": rt.info.achieved_weight_ratio, "feasible": True,
                        "hrm_bound_tok_s": bound.decode_throughput, "measured_tok_s": val,
+                       "stored_bytes_per_weight": rt.info.bytes_per_weight if a.codec else 2.0,
                        "frac": val / bound.decode_throughput,
                        "search_objective_tok_s": plan.decode_throughput,
                        "modeled_layer_ms": bound.breakdown.layer_total * 1e3,
