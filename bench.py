@@ -557,6 +557,8 @@ def run_mlt(args, cfg):
                 "weight_bytes_per_param": cfg.get("stored_dt", CODEC_DT) if cfg.get("codec") else 2.0,
                 "weight_bytes_per_param_searched": CODEC_DT if cfg.get("codec") else 2.0,
                 "raw_fallback_blocks_per_layer": info.raw_blocks,
+                "weight_code": {0: "bf16 tiles", 1: "12-bit (codec 1)", 2: "12-bit (codec 2)", 3: "12-bit (codec 3)",
+                                4: "11-bit (codec 4)"}.get(int(info.codec_engine), "?"),
                 "bound_bf16_weights_tok_s": bound_bf16.decode_throughput,
                 "value_over_bf16_bound": value / bound_bf16.decode_throughput,
                 "binding": binding, "link_gbs_measured": link_gbs, "host_read_gbs_measured": host_gbs,

@@ -587,8 +587,10 @@ typedef struct mlt_runtime_info_t {
     double streamed_bytes_per_layer;
     double arena_used, arena_capacity;
     double pin_seconds, gen_seconds;
-    double bytes_per_weight;  /* projection + expert weights as stored (2 = bf16; codec ~1.52) */
+    double bytes_per_weight;  /* projection + expert weights as stored (2 = bf16; codec ~1.41 / 1.52) */
     double raw_blocks;        /* codec: 128-row blocks per layer stored raw (per-block fallback) */
+    double codec_engine;      /* 0 bf16 tiles; 4 the 11-bit code (default), 3 the 12-bit code
+                                 (MLT_CODEC_MODE=3 or the fallback), 1 / 2 the other engines */
 } mlt_runtime_info_t;
 
 typedef struct mlt_runtime mlt_runtime;

@@ -153,6 +153,7 @@ mlt_dag* mlt_execution_dag(const mlt_dag* ref, const mlt_model_spec_t* m, const 
             info->achieved_weight_ratio = cat.achieved_rw;
             info->streamed_bytes_per_layer = static_cast<double>(cat.blob_bytes);
             info->arena_used = info->arena_capacity = info->pin_seconds = info->gen_seconds = 0;
+            info->bytes_per_weight = info->raw_blocks = info->codec_engine = 0;
         }
         out = reinterpret_cast<mlt_dag*>(d);
         return MLT_OK;
@@ -171,6 +172,7 @@ int mlt_runtime_info(const mlt_runtime* r, mlt_runtime_info_t* out) {
         out->gen_seconds = rt.gen_seconds();
         out->bytes_per_weight = rt.bytes_per_weight();
         out->raw_blocks = static_cast<double>(rt.raw_blocks());
+        out->codec_engine = static_cast<double>(rt.codec_mode());
         return MLT_OK;
     });
 }

@@ -186,6 +186,7 @@ class Runtime {
         }
         return weights > 0 ? bytes / weights : 0.0;
     }
+    int codec_mode() const { return codec_mode_; }
     int raw_blocks() const {
         int n = 0;
         for (const auto& b : cat_.blocks) n += b.raw ? 1 : 0;

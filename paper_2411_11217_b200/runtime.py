@@ -66,7 +66,8 @@ class PrefillReport(C.Structure):
 class RuntimeInfo(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("achieved_weight_ratio", "streamed_bytes_per_layer",
                                           "arena_used", "arena_capacity", "pin_seconds",
-                                          "gen_seconds", "bytes_per_weight", "raw_blocks")]
+                                          "gen_seconds", "bytes_per_weight", "raw_blocks",
+                                          "codec_engine")]
 
 
 # mlt_weight_fn: const uint16_t* get(void* ctx, int layer, int kind, int expert)

@@ -116,6 +116,7 @@ def test_codec_raw_fallback_on_heavy_tailed_weights(weights):
     assert 0 < info.raw_blocks < total_blocks
     assert info_raw.raw_blocks == total_blocks and info_raw.bytes_per_weight == 2.0
     assert 1.5 < info.bytes_per_weight < 2.0
+    assert info.codec_engine == 3  # heavy tails: the 11-bit code's capacity rule falls back to the 12-bit code
     assert np.array_equal(ids, ids_r) and np.array_equal(xs.view(np.uint32), xs_r.view(np.uint32))
 
     # the oracle on the same caller weights, forced onto the GPU's routes

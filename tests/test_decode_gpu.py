@@ -307,6 +307,7 @@ def test_weight_codec_decode_bitwise_equal(prompt, dims, r_w, a_g, budget, mode)
         finally:
             os.environ.pop("MLT_CODEC_FORCE_RAW", None)
             os.environ.pop("MLT_CODEC_MODE", None)
+        assert rt.info.codec_engine == int(mode)
         first = rt.decode(prompt[0], PROMPT, forced=prompt)
         rest = rt.decode(first.ids[-1], 8)
         out.append((first.ids.copy(), rest.ids.copy(), rt.residual().copy(), rt.info.streamed_bytes_per_layer,
