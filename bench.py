@@ -61,7 +61,8 @@ CONFIGS = {
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 NVLINK_BW = 900e9       # B200 NVLink 5, bytes/s per direction (nominal; 1 GPU in this pool)
-HOST_FLOPS = 2.0e12     # host-core fp32 estimate (16 SPR cores AVX-512); host DRAM bandwidth is measured
+HOST_FLOPS = 2.0e12     # fallback host-core fp32 FLOP/s (16 SPR cores AVX-512); measured live when possible
+_host_flops = None
 # An 8-GPU B200 node's host DRAM feeds every GPU's PCIe stream and the host
 # attention together.  This pool leases one GPU with a 16-core slice of a
 # host (its DRAM read bandwidth is measured live); a tp-way job's node is
@@ -162,7 +163,7 @@ def node_host(host_gbs, tp, per_slice_host):
     bw = host_gbs * slices
     if slices > 1:
         bw = min(bw, NODE_HOST_READ_GBS)
-    return bw * 1e9, HOST_FLOPS * slices
+    return bw * 1e9, host_flops() * slices
 
 
 def b200_hw(cfg, link_gbs, host_gbs, pk, tp=1, per_slice_host=False, budget=None):
@@ -214,6 +215,27 @@ def hrm_bound(cfg, link_gbs, host_gbs, pk, tp=1, per_slice_host=False):
         return api.estimate_throughput_b200(hw, m, w, policy(cfg), tp, NVLINK_BW)
     r = api.estimate_throughput(hw, m, w, policy(cfg))
     return r
+
+
+def host_flops():
+    """Host fp32 FLOP/s of this box, measured once (numpy / OpenBLAS sgemm 4096^3
+    on all cores, best of 2; the HardwareSpec's cpu_flops): the fallback
+    HOST_FLOPS only if the measurement fails."""
+    global _host_flops
+    if _host_flops is None:
+        try:
+            import numpy as np
+            a = np.random.default_rng(0).standard_normal((4096, 4096), dtype=np.float32)
+            a @ a
+            best = 0.0
+            for _ in range(2):
+                t = time.perf_counter()
+                a @ a
+                best = max(best, 2 * 4096 ** 3 / (time.perf_counter() - t))
+            _host_flops = best if best > 1e10 else HOST_FLOPS
+        except Exception:  # noqa: BLE001  (no BLAS: keep the stated estimate)
+            _host_flops = HOST_FLOPS
+    return _host_flops
 
 
 def measure_host(api):
@@ -442,7 +464,7 @@ def run_mlt(args, cfg):
     link_gbs = link[0]
     host_gbs = measure_host(api)
     log(f"[bench] rank {rank}: link H2D {link[0]:.2f} GB/s, D2H {link[1]:.2f}, H2D with D2H "
-        f"{link[2]:.2f}; host DRAM read {host_gbs:.1f} GB/s")
+        f"{link[2]:.2f}; host DRAM read {host_gbs:.1f} GB/s; host fp32 {host_flops() / 1e12:.2f} TFLOP/s")
 
     raw_rw = cfg["r_w"]
     if cfg.get("codec"):  # the stored bytes shrink: re-pick r_w for the budget
@@ -562,6 +584,7 @@ def run_mlt(args, cfg):
                 "bound_bf16_weights_tok_s": bound_bf16.decode_throughput,
                 "value_over_bf16_bound": value / bound_bf16.decode_throughput,
                 "binding": binding, "link_gbs_measured": link_gbs, "host_read_gbs_measured": host_gbs,
+                "host_fp32_tflops_measured": host_flops() / 1e12,
                 "modeled_layer_ms": bound.breakdown.layer_total * 1e3,
                 "measured_steady_layer_ms": rep.steady_layer_time * 1e3,
                 "h2d_weight_gbs_achieved": h2d_gbs,

@@ -55,7 +55,7 @@ def main():
         cfg0 = dict(model=model_t, N=N, prompt=prompt, gen=gen, budget=budget_gb * 1e9, codec=a.codec)
         hw = capi.HardwareSpec(budget_gb * 1e9 - bench.arena_extra(dict(cfg0, vocab=32000)), 196e9, pk["hbm_gbs"] * 1e9, host * 1e9,
                                link[0] * 1e9, pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * 1e12,
-                               bench.HOST_FLOPS)
+                               bench.host_flops())
         w = capi.WorkloadSpec(prompt, gen)
         for mu in [int(x) for x in a.mus.split(",")]:
             for a_g in (0, 1):
