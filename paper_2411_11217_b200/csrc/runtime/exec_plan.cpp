@@ -141,13 +141,18 @@ void apply_exact_gates(ScheduleDag& dag, const Catalog& cat, int M) {
         const Task& t = dag.tasks[i];
         if (t.kind == TaskKind::WeightToGpu) pages[(t.step - 1) * dag.layers + t.layer].push_back({t.page, i});
     }
-    auto needs = [&](bool pre, int page) {
-        const auto [b, e] = page_range(cat.blob_bytes, M, page);
+    // page p carries bytes of a QKV block (PreAttn) / of another block
+    // (PostAttn): the same for every layer, so tabulated once per page
+    std::vector<char> need_pre(M + 1, 0), need_post(M + 1, 0);
+    for (int p = 0; p <= M; ++p) {
+        const auto [b, e] = page_range(cat.blob_bytes, M, p);
         for (const auto& blk : cat.blocks) {
-            if (blk.resident || (blk.kind == kWqkv) != pre) continue;
-            if (blk.offset < e && blk.offset + blk.bytes > b) return true;
+            if (blk.resident || !(blk.offset < e && blk.offset + blk.bytes > b)) continue;
+            (blk.kind == kWqkv ? need_pre : need_post)[p] = 1;
         }
-        return false;
+    }
+    auto needs = [&](bool pre, int page) {
+        return page >= 0 && page <= M && (pre ? need_pre : need_post)[page] != 0;
     };
     for (int i = 0; i < n; ++i) {
         Task& t = dag.tasks[i];

@@ -106,6 +106,21 @@ struct Flags {
 // placeholders: the executor runs in issue order and dependency order only
 // (the weight-upload estimate uses the page bytes at a nominal PCIe rate; it
 // orders nothing).
+void Runtime::ensure_task_events(size_t n) {
+    while (task_ev_.size() < n) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "event");
+        task_ev_.push_back(e);
+    }
+}
+
+void Runtime::prefill_task_events(int steps) {
+    const ScheduleDag dag = schedule(std::max(1, std::min(steps, max_steps_)));
+    size_t dev = 0;
+    for (const Task& t : dag.tasks) dev += on_device(t.resource) ? 1 : 0;
+    ensure_task_events(2 * dev);
+}
+
 ScheduleDag Runtime::schedule(int steps) const {
     const double link = 55e9;  // nominal; measured durations replace every modeled one
     return lightplan::sim::build_schedule(
@@ -186,14 +201,21 @@ DecodeReport Runtime::run(ScheduleDag dag, const int32_t* tokens_in, const int32
     struct PdlOff {
         ~PdlOff() { mltk::set_pdl(false); }
     } pdl_off;
-    // task events are created before the measured region opens (tens of
-    // thousands for a long decode; creating them is host work, not decode)
+    // task events come from the runtime's pool (pre-created for a 32-step
+    // decode at construction, grown on demand, reused across calls): creating
+    // tens of thousands per call was ~0.1 s of host work inside every decode
     std::vector<cudaEvent_t> ev_start(n, nullptr), ev_end(n, nullptr);
-    for (int i = 0; i < n; ++i)
-        if (on_device(dag.tasks[i].resource)) {
-            ck(cudaEventCreate(&ev_start[i]), "event");
-            ck(cudaEventCreate(&ev_end[i]), "event");
-        }
+    {
+        size_t dev = 0;
+        for (int i = 0; i < n; ++i) dev += on_device(dag.tasks[i].resource) ? 1 : 0;
+        ensure_task_events(2 * dev);
+        size_t j = 0;
+        for (int i = 0; i < n; ++i)
+            if (on_device(dag.tasks[i].resource)) {
+                ev_start[i] = task_ev_[j++];
+                ev_end[i] = task_ev_[j++];
+            }
+    }
     cudaEvent_t e0, e_end;
     ck(cudaEventCreate(&e0), "event");
     ck(cudaEventCreate(&e_end), "event");
@@ -386,11 +408,6 @@ DecodeReport Runtime::run(ScheduleDag dag, const int32_t* tokens_in, const int32
             rep.dense_launches += kt.launches;
         }
     }
-    for (int i = 0; i < n; ++i)  // task events (the kernel marks above reference the GPU ones)
-        if (ev_start[i]) {
-            cudaEventDestroy(ev_start[i]);
-            cudaEventDestroy(ev_end[i]);
-        }
     rep.seconds = total_ms * 1e-3;
     rep.tokens_per_second = static_cast<double>(N_) * steps / rep.seconds;
     rep.gpu_launches = launches_;

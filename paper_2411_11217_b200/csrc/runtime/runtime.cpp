@@ -193,11 +193,13 @@ Runtime::Runtime(const lightplan::ModelSpec& model, const ModelExt& ext,
     build_catalog();
     allocate();
     generate_weights();
+    prefill_task_events(32);  // a 32-step decode's task events, outside every decode call
 }
 
 Runtime::~Runtime() {
     cudaDeviceSynchronize();
     for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+    for (cudaEvent_t e : task_ev_) cudaEventDestroy(e);
     host_free(host_blob_, host_blob_pinned_);
     host_free(staging_, true);
     if (h_qkv_) cudaFreeHost(h_qkv_);

@@ -364,6 +364,9 @@ class Runtime {
     float* h_pfx_ = nullptr;             // pinned [tokens][H] residual store
     int64_t h_pfx_tokens_ = 0;
     std::vector<cudaEvent_t> event_pool_;
+    std::vector<cudaEvent_t> task_ev_;  // per-task start / end events of the executor, reused across calls
+    void ensure_task_events(size_t n);
+    void prefill_task_events(int steps);
     size_t event_next_ = 0;
     double pin_seconds_ = 0, gen_seconds_ = 0;
 
