@@ -219,21 +219,22 @@ def hrm_bound(cfg, link_gbs, host_gbs, pk, tp=1, per_slice_host=False):
 
 def host_flops():
     """Host fp32 FLOP/s of this box, measured once (numpy / OpenBLAS sgemm 4096^3
-    on all cores, best of 2; the HardwareSpec's cpu_flops): the fallback
-    HOST_FLOPS only if the measurement fails."""
+    on all cores, best of 2; the HardwareSpec's cpu_flops) in a child process, so
+    no BLAS worker threads outlive the measurement next to the runtime's host
+    attention pool; the fallback HOST_FLOPS only if the measurement fails."""
     global _host_flops
     if _host_flops is None:
+        code = ("import numpy as np, time\n"
+                "a = np.random.default_rng(0).standard_normal((4096, 4096), dtype=np.float32)\n"
+                "a @ a\nbest = 0.0\n"
+                "for _ in range(2):\n"
+                "    t = time.perf_counter(); a @ a; best = max(best, 2 * 4096 ** 3 / (time.perf_counter() - t))\n"
+                "print(best)\n")
         try:
-            import numpy as np
-            a = np.random.default_rng(0).standard_normal((4096, 4096), dtype=np.float32)
-            a @ a
-            best = 0.0
-            for _ in range(2):
-                t = time.perf_counter()
-                a @ a
-                best = max(best, 2 * 4096 ** 3 / (time.perf_counter() - t))
+            r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+            best = float(r.stdout.strip().splitlines()[-1])
             _host_flops = best if best > 1e10 else HOST_FLOPS
-        except Exception:  # noqa: BLE001  (no BLAS: keep the stated estimate)
+        except Exception:  # noqa: BLE001  (no BLAS / no child: keep the stated estimate)
             _host_flops = HOST_FLOPS
     return _host_flops
 
