@@ -26,6 +26,7 @@ struct Handle {
     lightplan::sim::Timeline tl;
     bool has_tl = false;
     std::vector<mlt::DecodeReport::KernelTime> kernels, kernel_exec;
+    bool kernels_fresh = true;  // kernels holds the last decode call's event breakdown
 };
 
 Handle* H(mlt_runtime* r) { return reinterpret_cast<Handle*>(r); }
@@ -208,7 +209,7 @@ int mlt_runtime_decode(mlt_runtime* r, const int32_t* tokens, const int32_t* for
         Handle* h = H(r);
         const mlt::DecodeReport d = h->rt->decode(tokens, forced, steps, out, &h->dag, &h->tl);
         h->has_tl = true;
-        h->kernels = d.kernels;
+        h->kernels_fresh = false;
         h->kernel_exec = d.kernel_exec;
         if (rep) {
             rep->seconds = d.seconds;
@@ -240,7 +241,7 @@ int mlt_runtime_execute(mlt_runtime* r, const mlt_dag* dag, const int32_t* token
         const auto& d0 = *reinterpret_cast<const lightplan::sim::ScheduleDag*>(dag);
         const mlt::DecodeReport d = h->rt->execute(d0, tokens, forced, out, &h->dag, &h->tl);
         h->has_tl = true;
-        h->kernels = d.kernels;
+        h->kernels_fresh = false;
         h->kernel_exec = d.kernel_exec;
         if (rep) {
             rep->seconds = d.seconds;
@@ -268,6 +269,10 @@ int mlt_runtime_kernel_profile(mlt_runtime* r, char* buf, size_t cap) {
         std::string s = "{";
         char line[256];
         const char* keys[2] = {"events", "exec"};
+        if (!H(r)->kernels_fresh) {  // event deltas read on demand (Runtime::kernel_events)
+            H(r)->kernels = H(r)->rt->kernel_events();
+            H(r)->kernels_fresh = true;
+        }
         const std::vector<mlt::DecodeReport::KernelTime>* lists[2] = {&H(r)->kernels, &H(r)->kernel_exec};
         for (int L = 0; L < 2; ++L) {
             s += std::string(L ? "," : "") + "\"" + keys[L] + "\":[";

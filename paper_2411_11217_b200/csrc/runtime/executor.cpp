@@ -25,6 +25,8 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <array>
 #include <atomic>
 #include <chrono>
@@ -106,6 +108,29 @@ struct Flags {
 // placeholders: the executor runs in issue order and dependency order only
 // (the weight-upload estimate uses the page bytes at a nominal PCIe rate; it
 // orders nothing).
+// Per-kernel event deltas of the last decode call on the compute stream
+// (diagnostic breakdown, mlt_runtime_kernel_profile "events"): read on demand
+// after the call instead of inside it (tens of thousands of event queries
+// were ~0.1 s of every decode call); valid until the next decode call.
+std::vector<DecodeReport::KernelTime> Runtime::kernel_events() const {
+    std::vector<DecodeReport::KernelTime> out;
+    for (size_t k = 1; k < marks_.size(); ++k) {
+        const char* name = marks_[k].first;
+        if (!name) continue;  // a task start: the interval before it is not a kernel
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, marks_[k - 1].second, marks_[k].second), "elapsed");
+        auto it = std::find_if(out.begin(), out.end(),
+                               [&](const DecodeReport::KernelTime& kt) { return kt.name == name; });
+        if (it == out.end()) {
+            out.push_back({name, 0.0, 0});
+            it = out.end() - 1;
+        }
+        it->ms += ms;
+        it->launches += 1;
+    }
+    return out;
+}
+
 void Runtime::ensure_task_events(size_t n) {
     while (task_ev_.size() < n) {
         cudaEvent_t e;
@@ -168,6 +193,7 @@ DecodeReport Runtime::execute(const ScheduleDag& dag, const int32_t* tokens_in, 
 
 DecodeReport Runtime::run(ScheduleDag dag, const int32_t* tokens_in, const int32_t* forced, int steps, int32_t* out,
                           ScheduleDag* dag_out, Timeline* tl_out) {
+    const auto call_t0 = std::chrono::steady_clock::now();  // MLT_HOST_TIMING=1: host phases to stderr
     for (int i = 0; i < N_; ++i)
         if (pos_[i] + steps > max_ctx_) throw std::invalid_argument("KV capacity exceeded (max_ctx)");
     // token ids index the [vocab, h1] embedding on the device: reject bad ids here
@@ -222,6 +248,7 @@ DecodeReport Runtime::run(ScheduleDag dag, const int32_t* tokens_in, const int32
     ck(cudaEventRecord(e0, s_gpu_), "event");
     ck(cudaEventSynchronize(e0), "event sync");
     const auto host_t0 = std::chrono::steady_clock::now();
+    const double setup_s = std::chrono::duration<double>(host_t0 - call_t0).count();
     std::memcpy(h_tok_, tokens_in, N_ * 4);
     if (forced) std::memcpy(h_tok_, forced, static_cast<size_t>(steps) * N_ * 4);
     std::memcpy(h_tok_ + static_cast<size_t>(max_steps_) * N_, step_pos_.data(), step_pos_.size() * 4);
@@ -368,21 +395,7 @@ DecodeReport Runtime::run(ScheduleDag dag, const int32_t* tokens_in, const int32
     cudaEventDestroy(e_end);
     cudaEventDestroy(e_inputs);
 
-    DecodeReport rep;
-    for (size_t k = 1; k < marks_.size(); ++k) {
-        const char* name = marks_[k].first;
-        if (!name) continue;  // a task start: the interval before it is not a kernel
-        float ms = 0;
-        ck(cudaEventElapsedTime(&ms, marks_[k - 1].second, marks_[k].second), "elapsed");
-        auto it = std::find_if(rep.kernels.begin(), rep.kernels.end(),
-                               [&](const DecodeReport::KernelTime& kt) { return kt.name == name; });
-        if (it == rep.kernels.end()) {
-            rep.kernels.push_back({name, 0.0, 0});
-            it = rep.kernels.end() - 1;
-        }
-        it->ms += ms;
-        it->launches += 1;
-    }
+    DecodeReport rep;  // (the per-kernel event breakdown is read on demand: kernel_events())
     {  // in-kernel execution times of the GEMMs
         std::vector<unsigned long long> tv(2 * ktime_names_.size());
         if (!tv.empty())
@@ -443,6 +456,11 @@ DecodeReport Runtime::run(ScheduleDag dag, const int32_t* tokens_in, const int32
     for (int r = 0; r < 5; ++r) rep.utilization[r] = m.utilization[r];
     if (dag_out) *dag_out = std::move(measured);
     if (tl_out) *tl_out = std::move(tl);
+    if (const char* ht = std::getenv("MLT_HOST_TIMING"); ht && ht[0] == '1') {
+        const double tot = std::chrono::duration<double>(std::chrono::steady_clock::now() - call_t0).count();
+        std::fprintf(stderr, "[mlt] decode call host phases: setup %.1f ms, device region %.1f ms, report %.1f ms\n",
+                     setup_s * 1e3, host_end * 1e3, (tot - setup_s - host_end) * 1e3);
+    }
     return rep;
 }
 

@@ -102,7 +102,7 @@ struct DecodeReport {
         double ms = 0;
         int launches = 0;
     };
-    std::vector<KernelTime> kernels;  // live per-kernel breakdown (event deltas on the compute stream)
+    std::vector<KernelTime> kernels;  // (empty: the event breakdown is Runtime::kernel_events(), on demand)
     std::vector<KernelTime> kernel_exec;  // in-kernel first-CTA-start to last-CTA-end (GEMMs)
 };
 
@@ -187,6 +187,7 @@ class Runtime {
         return weights > 0 ? bytes / weights : 0.0;
     }
     int codec_mode() const { return codec_mode_; }
+    std::vector<DecodeReport::KernelTime> kernel_events() const;  // last call's per-kernel event deltas
     int raw_blocks() const {
         int n = 0;
         for (const auto& b : cat_.blocks) n += b.raw ? 1 : 0;
